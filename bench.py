@@ -1,0 +1,390 @@
+"""Benchmark: ROIs/s of full 3-D shape coefficients on KiTS19-shaped masks.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W` prints ONE
+JSON line on rank 0.  N>1 runs under torchrun, one rank per GPU; every rank
+processes its own ROIs (ROI-batch sharding: independent masks, no data-path
+collective -> "scaling": "weak"); the timed region is bracketed by a barrier
+and torch.cuda.synchronize() and the reported time is the max over ranks.
+
+Workload (BASELINE.json configs[1]): one synthetic KiTS19-shaped mask,
+512x512x600 uint8 at 0.8x0.8x1.0 mm, two kidneys + a 30 mm tumour
+(SURVEY.md Appendix D, V = 73,406 vertices).  One step = calculate_coefficients
+of one ROI: marching cubes -> area/volume -> 3-D and planar diameters.  The
+mask (157 MB) is larger than L2 (126 MB), so no L2 flush is needed.
+
+  value      device-resident throughput: mask already in HBM, CUDA events on
+             the library stream around K steps (host syncs inside the steps
+             are inside the timed region).
+  e2e        the same metric through the C ABI with a HOST (pinned) mask:
+             every step copies the 157 MB mask H2D and reads the result back.
+  roofline   dominant kernel = diam3d_pass1 (FP32 CUDA-core bound); achieved =
+             8 flop * V(V-1)/2 pairs / kernel time; peak = FP32 rate measured
+             by sc_probe_fp32_peak on this GPU.  roofline_mc: pack_bits
+             (HBM-bound), achieved = mask bytes / kernel time vs the measured
+             copy bandwidth in MEASURED_PEAKS.json.
+  cpu_baseline  the CPU oracle (C restatement of the reference, OpenMP strip-
+             parallel diameters, serial MC as in the reference) on one ROI.
+
+`--impl reference` times that CPU path alone (rank 0; other ranks exit 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ROIs/sec full 3D shape coefficients (KiTS19-shaped masks) at 1/2/4/8 B200"
+UNIT = "ROIs/s"
+SPACING = (0.8, 0.8, 1.0)
+DIMS = (512, 512, 600)  # nx, ny, nz
+TUMOR_MM = 30.0
+KERNELS_PER_ROI = 9  # init, pack, mc, pass1, refine, plane hist/scan/scatter/pairs
+
+
+def workload_config(extra=None):
+    cfg = {
+        "workload": "C2 KiTS19-shaped synthetic kidney+tumor mask 512x512x600 uint8 at "
+                    "0.8x0.8x1.0 mm (tumor 30 mm, V=73406), one ROI per step per GPU",
+        "global_batch": None,
+        "roi_bytes": DIMS[0] * DIMS[1] * DIMS[2],
+        "l2": "input 157 MB > 126 MB L2 (no flush needed)",
+        "parallelism": None,
+    }
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+def make_mask():
+    from paper_2510_02894_b200 import synth
+
+    return synth.kits_like(DIMS[0], DIMS[1], DIMS[2], SPACING, TUMOR_MM)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the dominant kernels from the committed ncu
+    summary (profiles/ncu_summary.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
+            return json.load(fh).get("dram_bytes_per_launch", {})
+    except (OSError, ValueError):
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(n_gpus):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(world, value):
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_reference_time(mask, max_seconds=150.0, steps=1, warmup=0):
+    """The oracle (C port of the reference path) on all host cores: MC serial,
+    diameters strip-parallel (features.py:151-192).  Returns (per-ROI seconds
+    list, threads)."""
+    from oracle import oracle
+
+    threads = oracle.max_threads()
+    t_start = time.perf_counter()
+    for _ in range(warmup):
+        oracle.extract_features(mask, SPACING, threads=0, with_active=False)
+        if time.perf_counter() - t_start > max_seconds / 2:
+            break
+    times = []
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        oracle.extract_features(mask, SPACING, threads=0, with_active=False)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > max_seconds:
+            break
+    return times, threads
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    mask = make_mask()
+    times, threads = cpu_reference_time(mask, max_seconds=args.cpu_seconds, steps=args.steps,
+                                        warmup=min(args.warmup, 1))
+    per = statistics.mean(times)
+    value = 1.0 / per
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": world, "steps": len(times), "warmup": min(args.warmup, 1),
+        "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8/fp64", "data": "synthetic",
+        "config": workload_config({"parallelism": "host cores (OpenMP)", "global_batch": 1}),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{len(times)} full C2 ROI(s) through oracle/shape_oracle.c "
+                                   "(reference algorithm restated in C: serial canonical MC, "
+                                   "strip-parallel fp64 diameters), time-capped at "
+                                   f"{args.cpu_seconds:.0f}s"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2510_02894_b200 as sc
+    from paper_2510_02894_b200 import _native
+
+    world, rank, local = dist_setup(args.gpus)
+    dev = torch.cuda.current_device()
+    mask_np = make_mask()
+    nz, ny, nx = mask_np.shape
+    d_mask = torch.from_numpy(mask_np).to(f"cuda:{dev}")
+    stream = torch.cuda.Stream()
+    h_mask = torch.from_numpy(mask_np).pin_memory()
+    h_np = h_mask.numpy()
+
+    # ---- device-resident throughput (value) ----
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            c = sc.calculate_coefficients_device(d_mask, SPACING, stream=stream)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _native.launch_count()
+    kt = {k: [] for k in _native.KERNEL_TIME_NAMES}
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            c = sc.calculate_coefficients_device(d_mask, SPACING, stream=stream)
+            for k, v in _native.last_kernel_times(dev).items():
+                kt[k].append(v)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = _native.launch_count() - launches0
+    dev_ms = ev0.elapsed_time(ev1)
+    dev_ms_max = max_over_ranks(world, dev_ms)
+    value = world * args.steps / (dev_ms_max / 1e3)
+
+    # ---- end to end through the C ABI with a pinned host mask (e2e) ----
+    for _ in range(max(1, args.warmup // 2)):
+        sc.calculate_coefficients(h_np, SPACING, device=dev)
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ce = sc.calculate_coefficients(h_np, SPACING, device=dev)
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(world, time.perf_counter() - t0)
+    barrier(world)
+    e2e_value = world * args.steps / e2e_s
+    h2d_ms = ce.h2d_ms
+
+    # ---- roofline of the dominant kernel ----
+    med = {k: statistics.median(v) for k, v in kt.items() if v}
+    V = c.vertex_count
+    pairs = V * (V - 1) / 2
+    pass1_s = med["diam3d_pass1_ms"] / 1e3
+    fp32_peak = max(_native.probe_fp32_peak(dev, m) for m in (0, 1, 3))
+    fp32_peak_reg2 = _native.probe_fp32_peak(dev, 0)
+    achieved = 8.0 * pairs / pass1_s / 1e12
+    traffic = ncu_traffic()
+    peaks, peak_kind = measured_peaks()
+    mask_bytes = nx * ny * nz
+    pack_s = med["pack_ms"] / 1e3
+    mc_gbs = mask_bytes / pack_s / 1e9
+    shares = {k: med[k] / max(1e-9, sum(med[x] for x in med if x != "h2d_ms"))
+              for k in med if k != "h2d_ms"}
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": dev_ms_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp32",
+        "data": "synthetic",
+        "config": workload_config({"global_batch": world, "parallelism": f"roi-batch x{world}"}),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": mask_bytes,
+                "d2h_bytes_per_step": 2 * 2304,
+                "path": "sc_calculate_coefficients (C ABI) from pinned host memory",
+                "h2d_ms_per_step": h2d_ms},
+        "gpu_launches": int(launches),
+        "roofline": {
+            "kernel": "diam3d_pass1",
+            "bound": "fp32",
+            "achieved": achieved,
+            "peak": fp32_peak,
+            "unit": "TFLOP/s",
+            "frac": achieved / fp32_peak,
+            "traffic": traffic.get("diam3d_pass1"),
+            "work": f"8 flop x V(V-1)/2 = {pairs:.4g} pairs per launch, V={V}",
+            "peak_note": "FP32 CUDA-core rate measured on this GPU by sc_probe_fp32_peak "
+                         f"(best of FFMA2/FFMA/FFMA-imm; FFMA2 all-register "
+                         f"{fp32_peak_reg2:.1f} TFLOP/s); nominal 74.4 at 1965 MHz",
+            "pair_evals_per_s": pairs / pass1_s,
+        },
+        "roofline_mc": {
+            "kernel": "pack_bits_v16",
+            "bound": "hbm",
+            "achieved": mc_gbs,
+            "peak": peaks["hbm_gbs"],
+            "unit": "GB/s",
+            "frac": mc_gbs / peaks["hbm_gbs"],
+            "traffic": traffic.get("pack_bits_v16"),
+            "peak_kind": peak_kind,
+            "mvoxels_per_s": mask_bytes / pack_s / 1e6,
+            "mc_stage_mvoxels_per_s": mask_bytes / ((med["pack_ms"] + med["mc_ms"]) / 1e3) / 1e6,
+        },
+        "kernel_ms": med,
+        "kernel_share": shares,
+        "clocks": clocks.summary(),
+        "result": {"VertexCount": V, "triangles": c.triangle_count, "active_cubes": c.active_cubes,
+                   "Maximum3DDiameter": c.max_3d_diameter, "MeshVolume": c.mesh_volume},
+    }
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        times, threads = cpu_reference_time(mask_np, max_seconds=args.cpu_seconds, steps=1)
+        per = statistics.mean(times)
+        line["cpu_baseline"] = {
+            "value": 1.0 / per, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": "1 full C2 ROI through oracle/shape_oracle.c (reference algorithm in C: "
+                      "serial canonical MC + strip-parallel fp64 diameters on all host threads)",
+            "seconds_per_roi": per,
+        }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=150.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3  # contract: W >= 3 warm-up steps
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,133 @@
+/* shapecore_b200 -- C ABI of the B200-native shape-coefficient path.
+ *
+ * One call computes the full shape coefficients of a binary ROI mask:
+ * marching-cubes surface area and signed-tetrahedron volume, the maximum 3-D
+ * diameter and the maximum 2-D diameters in the slice (XY, same z), column
+ * (XZ, same y) and row (YZ, same x) planes, plus vertex / triangle /
+ * active-cube counts.  All GPU work runs in hand-written sm_100a kernels; there
+ * is no CPU fallback: without a usable CUDA device every compute entry returns
+ * SC_ERR_CUDA.
+ *
+ * Reference interfaces replaced (reference = /root/reference/pkg):
+ *   sc_calculate_coefficients*  <- shapecore.features.extract_features
+ *                                  (src/shapecore/features.py:224-265), i.e.
+ *                                  marching_cubes (mesh.py:68-91) -> mesh_volume
+ *                                  (features.py:99-110) -> surface_area
+ *                                  (features.py:89-96) -> diameters[_parallel]
+ *                                  (features.py:205-221); and the engine call
+ *                                  behind shapebind.execute (binding
+ *                                  src/shapebind/__init__.py:75-117), which today
+ *                                  crosses a process boundary (subprocess + NPY).
+ *   sc_diameters                <- shapecore.features.diameters / diameters_parallel
+ *                                  (features.py:205-221) on raw coordinate arrays.
+ *   return codes                <- CLI exit codes (cli.py:23-26): 2 input error,
+ *                                  3 empty ROI; exceptions EmptyRoi / NoVertices /
+ *                                  NonPositiveSpacing (errors.py:24-40).
+ *
+ * Data layout (same bytes as the reference MaskVolume, volume.py:59-66): mask
+ * is nx*ny*nz bytes in C order with x fastest, index (iz*ny + iy)*nx + ix;
+ * any nonzero byte is occupied.  spacing = (sx, sy, sz) in mm, finite, > 0.
+ *
+ * Threading: every entry is safe to call concurrently from several host
+ * threads; calls on the same device are serialised internally.
+ */
+#ifndef SHAPECORE_B200_H
+#define SHAPECORE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SC_ABI_VERSION 1
+
+enum {
+  SC_OK = 0,
+  SC_ERR_INPUT = 2,       /* bad dims / spacing / pointer (volume.py:74-101)   */
+  SC_ERR_EMPTY_ROI = 3,   /* mask has no occupied voxel (mesh.py:78-79)        */
+  SC_ERR_NO_VERTICES = 4, /* diameters on an empty set (features.py:198-199)   */
+  SC_ERR_CUDA = -1,       /* CUDA runtime / launch failure; see sc_last_error() */
+  SC_ERR_NOMEM = -2       /* device or pinned allocation failed                 */
+};
+
+/* Output record: the reference ShapeFeatures (features.py:38-60) plus the
+ * exact counts and per-stage device times (StageTimings, timing.py:9-20). */
+typedef struct {
+  double mesh_volume;
+  double surface_area;
+  double max_3d_diameter;
+  double max_2d_diameter_xy; /* slice plane: vertex pairs sharing z  */
+  double max_2d_diameter_xz; /* column plane: vertex pairs sharing y */
+  double max_2d_diameter_yz; /* row plane: vertex pairs sharing x    */
+  int64_t vertex_count;
+  int64_t triangle_count;
+  int64_t active_cubes;
+  double h2d_ms;       /* host->device mask copy (host entry only), CUDA events   */
+  double mesh_ms;      /* bit-pack + marching-cubes kernels, CUDA events           */
+  double diameters_ms; /* 3-D + planar diameter kernels, CUDA events               */
+  double total_ms;     /* host wall time of the whole call                         */
+} sc_coeffs;
+
+/* Host mask (pageable or pinned).  device: CUDA ordinal.  Copies the mask to
+ * the device inside the call (chunked, overlapped with the bit-pack kernel). */
+int sc_calculate_coefficients(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz,
+                              const double spacing[3], int device, sc_coeffs* out);
+
+/* Device-resident mask on the CURRENT device; `stream` is a cudaStream_t (NULL =
+ * the library's own stream).  The mask must stay valid for the call. */
+int sc_calculate_coefficients_device(const uint8_t* d_mask, int64_t nx, int64_t ny,
+                                     int64_t nz, const double spacing[3], void* stream,
+                                     sc_coeffs* out);
+
+/* Sharded variant for one very large mesh split across G devices:
+ * runs the whole marching-cubes stage, then only shard `shard` of `nshards` of
+ * the 3-D pair-tile grid and of the planar groups.  The 4 partial squared
+ * maxima (3d, xy, xz, yz; fp64) are written to d_sq4 (device memory, 4
+ * doubles) so the caller can ncclAllReduce(MAX) them in place, and also to
+ * out (sqrt applied) for convenience.  Counts, area and volume in `out` are
+ * complete on every shard. */
+int sc_calculate_coefficients_shard(const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
+                                    const double spacing[3], void* stream, int shard,
+                                    int nshards, double* d_sq4, sc_coeffs* out);
+
+/* Batch of ROIs on one device (C4): masks[i] are host pointers with dims
+ * dims[3*i..3*i+2] and spacing spacings[3*i..]; out[i] per ROI.  The first
+ * failing ROI's code is returned; later ROIs are still processed. */
+int sc_calculate_coefficients_batch(const uint8_t* const* masks, const int64_t* dims,
+                                    const double* spacings, int64_t count, int device,
+                                    sc_coeffs* out);
+
+/* Diameters of an arbitrary fp64 point cloud (features.py:205-221), bit-exact
+ * with the reference: out = (max3d, xy, xz, yz).  Host arrays. */
+int sc_diameters(const double* xs, const double* ys, const double* zs, int64_t n, int device,
+                 double out[4]);
+
+/* Marching-cubes vertex set of a host mask as doubled lattice coordinates
+ * (2x + [axis==0], 2y + [axis==1], 2z + [axis==2]); vertex i is
+ * (keys[3i], keys[3i+1], keys[3i+2]) and the reference coordinate is key/2 *
+ * spacing.  Order is unspecified.  *n_out receives the count; at most `cap`
+ * entries are written.  For parity tests and mesh export. */
+int sc_mesh_vertices(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, int device,
+                     int32_t* keys, int64_t cap, int64_t* n_out);
+
+/* Measurement hooks (bench.py).  sc_last_kernel_times fills up to n of
+ * {pack_ms, mc_ms, diam3d_pass1_ms, diam3d_refine_ms, planar_ms, h2d_ms} of the
+ * last ROI run on `device` (CUDA events on the launching stream) and returns
+ * how many were written.  sc_launch_count is the number of kernels this
+ * library has launched in the process.  sc_probe_fp32_peak measures the FP32
+ * CUDA-core throughput of `device` in TFLOP/s with a dependent-chain-free
+ * FFMA2 (mode 0) or scalar FFMA (mode 1) kernel. */
+int sc_last_kernel_times(int device, double* ms, int n);
+uint64_t sc_launch_count(void);
+int sc_probe_fp32_peak(int device, int mode, double* tflops);
+
+const char* sc_last_error(void); /* thread-local message of the last failure */
+int sc_abi_version(void);
+int sc_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

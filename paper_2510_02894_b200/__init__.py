@@ -1,1 +1,45 @@
-"""B200-native shape-coefficient path (placeholder; filled in below)."""
+"""paper_2510_02894_b200: B200-native shape coefficients (PyRadiomics-cuda hot path).
+
+Public API mirrors the reference `shapecore` package
+(/root/reference/pkg/src/shapecore/__init__.py) for the hot path:
+`extract_features`, `ShapeFeatures`, `FEATURE_KEYS`, `diameters`,
+`diameters_parallel`, `MaskVolume`, `attach_spacing`, `StageTimings` and the
+error classes, plus north_star's `calculate_coefficients(mask, spacing)`.
+All compute runs in libshapecore_b200.so (sm_100a CUDA); importing this
+package does not touch the GPU, calling it does.
+"""
+
+from .errors import (
+    DeviceError,
+    EmptyRoi,
+    NonPositiveSpacing,
+    NoVertices,
+    ShapeCoreError,
+    ShapeExceedsBounds,
+)
+from .features import (
+    FEATURE_KEYS,
+    Coefficients,
+    ShapeFeatures,
+    calculate_coefficients,
+    calculate_coefficients_batch,
+    calculate_coefficients_device,
+    calculate_coefficients_shard,
+    diameters,
+    diameters_parallel,
+    extract_features,
+    mesh_vertices,
+)
+from .synth import synth_mask
+from .timing import StageTimings
+from .volume import MaskVolume, attach_spacing
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "FEATURE_KEYS", "Coefficients", "DeviceError", "EmptyRoi", "MaskVolume", "NoVertices",
+    "NonPositiveSpacing", "ShapeCoreError", "ShapeExceedsBounds", "ShapeFeatures",
+    "StageTimings", "attach_spacing", "calculate_coefficients", "calculate_coefficients_batch",
+    "calculate_coefficients_device", "calculate_coefficients_shard", "diameters",
+    "diameters_parallel", "extract_features", "mesh_vertices", "synth_mask",
+]

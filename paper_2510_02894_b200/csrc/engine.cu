@@ -1,0 +1,617 @@
+// Host orchestration and the C ABI (include/shapecore_b200.h).
+//
+// One ROI = init -> pack_bits -> mc_cells -> [one 2 KB D2H of counts + bbox]
+// -> diam3d_pass1 -> diam3d_refine -> plane_{hist,scan,scatter,pairs} -> D2H of
+// the accumulators.  Area, volume, triangle and active-cube counts are formed
+// on the host from exact integer histograms.  Per
+// device the library keeps one context: a stream, events, grow-only scratch
+// arenas and pinned result buffers, reused across calls (SURVEY.md 8b
+// "Ownership"); calls on one device are serialised by a mutex.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/shapecore_b200.h"
+#include "mc_tables.h"
+#include "sc_device.cuh"
+
+namespace sc {
+
+// Kernels (mc.cu, diameter.cu).
+__global__ void init_stats(Stats* st);
+template <int U>
+__global__ void pack_bits_v16(const uint4*, uint32_t*, long long, int, int, Stats*);
+__global__ void pack_bits_generic(const uint8_t*, uint32_t*, long long, int, int, int, Stats*);
+__global__ void mc_cells(const uint32_t*, int, int, int, int, const CaseTables*, Stats*, int4*,
+                         long long);
+template <int R>
+__global__ void diam3d_pass1(const int4*, long long, int, long long, long long, Frame, float*,
+                             Stats*);
+template <int R>
+__global__ void diam3d_refine(const int4*, long long, int, long long, long long, Frame,
+                              const float*, Stats*);
+__global__ void plane_hist(const int4*, long long, PlaneSpace, unsigned int*);
+__global__ void plane_scan(const unsigned int*, int, unsigned int*, unsigned int*);
+__global__ void plane_scatter(const int4*, long long, PlaneSpace, unsigned int*, int2*);
+__global__ void plane_pairs(const int2*, const unsigned int*, int, int, PlaneSpace, Frame, Stats*);
+__global__ void cloud_diameters(const double*, const double*, const double*, long long, int,
+                                unsigned long long*);
+template <int MODE>
+__global__ void fp32_probe(float*, int, float, float);
+
+}  // namespace sc
+
+using namespace sc;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<unsigned long long> g_launches{0};
+
+void set_err(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+#define CK(expr)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      set_err("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return SC_ERR_CUDA;                                                              \
+    }                                                                                  \
+  } while (0)
+
+// Every kernel launch of the library goes through CKL(n): checks the launch and
+// counts n launches (sc_launch_count, bench.py's gpu_launches).
+#define CKL(n)                                     \
+  do {                                             \
+    CK(cudaGetLastError());                        \
+    g_launches.fetch_add((n), std::memory_order_relaxed); \
+  } while (0)
+
+// ---------------------------------------------------------------- case tables
+struct CaseGeom {
+  int ntri[kNumCases];
+  int n[kNumCases][5][3];  // doubled-integer (b-a) x (c-a) per triangle
+  CaseTables tabs;
+};
+
+const CaseGeom& case_geom() {
+  static CaseGeom g = [] {
+    CaseGeom c{};
+    for (int k = 0; k < kNumCases; k++) {
+      int t_sum = 0, n_sum[3] = {0, 0, 0}, nt = 0;
+      for (int t = 0; t < 16 && SC_TRI_TABLE[k][t] >= 0; t += 3) {
+        int a[3][3];
+        for (int v = 0; v < 3; v++) {
+          int e = SC_TRI_TABLE[k][t + v];
+          int ax = SC_EDGE_AXIS[e];
+          a[v][0] = 2 * SC_EDGE_DX[e] + (ax == 0);
+          a[v][1] = 2 * SC_EDGE_DY[e] + (ax == 1);
+          a[v][2] = 2 * SC_EDGE_DZ[e] + (ax == 2);
+        }
+        int u[3], w[3], bc[3];
+        for (int d = 0; d < 3; d++) { u[d] = a[1][d] - a[0][d]; w[d] = a[2][d] - a[0][d]; }
+        int nn[3] = {u[1] * w[2] - u[2] * w[1], u[2] * w[0] - u[0] * w[2], u[0] * w[1] - u[1] * w[0]};
+        bc[0] = a[1][1] * a[2][2] - a[1][2] * a[2][1];
+        bc[1] = a[1][2] * a[2][0] - a[1][0] * a[2][2];
+        bc[2] = a[1][0] * a[2][1] - a[1][1] * a[2][0];
+        t_sum += a[0][0] * bc[0] + a[0][1] * bc[1] + a[0][2] * bc[2];
+        for (int d = 0; d < 3; d++) { n_sum[d] += nn[d]; c.n[k][nt][d] = nn[d]; }
+        nt++;
+      }
+      c.ntri[k] = nt;
+      c.tabs.tn[k] = make_int4(t_sum, n_sum[0], n_sum[1], n_sum[2]);
+    }
+    return c;
+  }();
+  return g;
+}
+
+// Area of one triangle of case k in mm^2: 0.5*|N| with N = diag(sy sz, sx sz, sx sy)/4 * n.
+void area_table(const double sp[3], double out[kNumCases]) {
+  const CaseGeom& g = case_geom();
+  const double fx = sp[1] * sp[2] * 0.25, fy = sp[0] * sp[2] * 0.25, fz = sp[0] * sp[1] * 0.25;
+  for (int k = 0; k < kNumCases; k++) {
+    double s = 0.0;
+    for (int t = 0; t < g.ntri[k]; t++) {
+      double a = fx * g.n[k][t][0], b = fy * g.n[k][t][1], c = fz * g.n[k][t][2];
+      s += 0.5 * std::sqrt(a * a + b * b + c * c);
+    }
+    out[k] = s;
+  }
+}
+
+// ------------------------------------------------------------------- context
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;  // elements
+  cudaError_t ensure(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = n + n / 4 + 1024;
+    cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+};
+
+struct Ctx {
+  int device = 0;
+  int sms = 148;
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[6] = {};
+  cudaEvent_t kev[8] = {};      // per-kernel boundaries of the last ROI
+  double last_ms[6] = {0, 0, 0, 0, 0, 0};  // pack, mc, pass1, refine, planar, h2d
+  Stats* d_stats = nullptr;
+  Stats* h_stats = nullptr;  // pinned
+  CaseTables* d_tabs = nullptr;
+  DevBuf<uint32_t> bits;
+  DevBuf<int4> keys;
+  DevBuf<float> item_max;
+  DevBuf<unsigned int> plane_counts, plane_start, plane_cursor;
+  DevBuf<int2> plane_sorted;
+  DevBuf<uint8_t> mask_stage;
+  DevBuf<double> cloud;
+  DevBuf<unsigned long long> cloud_out;
+};
+
+std::mutex g_ctx_mu;
+std::vector<std::unique_ptr<Ctx>> g_ctx;
+
+int get_ctx(int device, Ctx** out) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  int n = 0;
+  CK(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) {
+    set_err("device %d out of range (%d CUDA devices)", device, n);
+    return SC_ERR_INPUT;
+  }
+  if ((int)g_ctx.size() < n) g_ctx.resize(n);
+  if (!g_ctx[device]) {
+    auto c = std::make_unique<Ctx>();
+    c->device = device;
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) {
+      set_err("device %d is sm_%d%d; this library is built for sm_100a (B200)", device,
+              prop.major, prop.minor);
+      return SC_ERR_CUDA;
+    }
+    c->sms = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    for (auto& e : c->kev) CK(cudaEventCreate(&e));
+    CK(cudaMalloc(&c->d_stats, sizeof(Stats)));
+    CK(cudaMallocHost(&c->h_stats, sizeof(Stats)));
+    CK(cudaMalloc(&c->d_tabs, sizeof(CaseTables)));
+    CK(cudaMemcpy(c->d_tabs, &case_geom().tabs, sizeof(CaseTables), cudaMemcpyHostToDevice));
+    CK(cudaFuncSetAttribute(diam3d_pass1<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 512 * 24));
+    CK(cudaFuncSetAttribute(diam3d_pass1<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 24));
+    CK(cudaFuncSetAttribute(diam3d_pass1<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2048 * 24));
+    g_ctx[device] = std::move(c);
+  }
+  *out = g_ctx[device].get();
+  return SC_OK;
+}
+
+int check_input(const void* mask, int64_t nx, int64_t ny, int64_t nz, const double sp[3]) {
+  if (!mask) { set_err("mask pointer is NULL"); return SC_ERR_INPUT; }
+  if (nx < 1 || ny < 1 || nz < 1) {
+    set_err("dims must all be >= 1, got (%lld, %lld, %lld)", (long long)nx, (long long)ny,
+            (long long)nz);
+    return SC_ERR_INPUT;
+  }
+  // Doubled lattice keys and fp32 frame coordinates must stay exact.
+  if (nx > (1 << 20) || ny > (1 << 20) || nz > (1 << 20)) {
+    set_err("dims beyond 2^20 per axis are not supported");
+    return SC_ERR_INPUT;
+  }
+  if (!sp) { set_err("spacing pointer is NULL"); return SC_ERR_INPUT; }
+  for (int i = 0; i < 3; i++)
+    if (!(sp[i] > 0.0) || !std::isfinite(sp[i])) {
+      set_err("spacing components must be finite and > 0, got (%g, %g, %g)", sp[0], sp[1], sp[2]);
+      return SC_ERR_INPUT;
+    }
+  return SC_OK;
+}
+
+double f64_of(unsigned long long bits) {
+  double d;
+  std::memcpy(&d, &bits, 8);
+  return d;
+}
+
+// Marching-cubes stage: init + pack + cells, then one small D2H (counts+bbox).
+int run_mc(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, cudaStream_t s) {
+  const int W = (int)((nx + 31) / 32);
+  const long long n_words = (long long)W * ny * nz;
+  CK(c->bits.ensure((size_t)n_words));
+  if (c->keys.cap == 0) CK(c->keys.ensure(1 << 20));
+  for (int attempt = 0; attempt < 2; attempt++) {
+    CK(cudaEventRecord(c->kev[0], s));
+    init_stats<<<1, 256, 0, s>>>(c->d_stats);
+    CKL(1);
+    if (nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0) {
+      const long long n_chunks = nx * ny * nz / 16;
+      long long want = (n_chunks + 256 * 4 - 1) / (256 * 4);
+      int grid = (int)std::min<long long>(want, (long long)c->sms * 8);
+      pack_bits_v16<4><<<grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(d_mask), c->bits.p,
+                                            n_chunks, W, (int)ny, c->d_stats);
+    } else {
+      long long want = (n_words + 255) / 256;
+      int grid = (int)std::min<long long>(want, (long long)c->sms * 8);
+      pack_bits_generic<<<grid, 256, 0, s>>>(d_mask, c->bits.p, n_words, (int)nx, W, (int)ny,
+                                             c->d_stats);
+    }
+    CKL(1);
+    CK(cudaEventRecord(c->kev[1], s));
+    mc_cells<<<c->sms * 4, 256, 0, s>>>(c->bits.p, (int)nx, (int)ny, (int)nz, W, c->d_tabs,
+                                        c->d_stats, c->keys.p, (long long)c->keys.cap);
+    CKL(1);
+    CK(cudaEventRecord(c->kev[2], s));
+    CK(cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (c->h_stats->n_vert <= c->keys.cap) return SC_OK;
+    CK(c->keys.ensure((size_t)c->h_stats->n_vert));  // rare: re-run with room
+  }
+  set_err("vertex buffer overflow");
+  return SC_ERR_NOMEM;
+}
+
+// Diameter stage for shard `shard` of `nshards`: 3-D tile pairs and planes.
+int run_diameters(Ctx* c, const double sp[3], cudaStream_t s, int shard, int nshards) {
+  const Stats& h = *c->h_stats;
+  const long long V = (long long)h.n_vert;
+  const int* bb = h.bbox;
+  Frame f;
+  f.cx2 = bb[0] + bb[3];
+  f.cy2 = bb[1] + bb[4];
+  f.cz2 = bb[2] + bb[5];
+  f.hx = (float)(0.5 * sp[0]);
+  f.hy = (float)(0.5 * sp[1]);
+  f.hz = (float)(0.5 * sp[2]);
+  f.sx = sp[0];
+  f.sy = sp[1];
+  f.sz = sp[2];
+
+  // 3-D: pick the register block so the triangle holds >= 4 waves of tiles.
+  int R = 2;
+  for (int r : {8, 4}) {
+    long long T = (V + 256LL * r - 1) / (256LL * r);
+    if (T * (T + 1) / 2 >= 4LL * c->sms) { R = r; break; }
+  }
+  const long long TS = 256LL * R;
+  const long long T = (V + TS - 1) / TS;
+  const long long n_items = T * (T + 1) / 2;
+  const long long i0 = n_items * shard / nshards, i1 = n_items * (shard + 1) / nshards;
+  const long long n_loc = i1 - i0;
+  CK(cudaEventRecord(c->kev[3], s));
+  if (n_loc > 0) {
+    CK(c->item_max.ensure((size_t)n_loc));
+    const size_t smem = (size_t)TS * 24;
+#define LAUNCH_3D(RR)                                                                          \
+  diam3d_pass1<RR><<<(unsigned)n_loc, 256, smem, s>>>(c->keys.p, V, (int)T, i0, n_loc, f,      \
+                                                      c->item_max.p, c->d_stats);              \
+  CKL(1);                                                                                      \
+  CK(cudaEventRecord(c->kev[4], s));                                                           \
+  diam3d_refine<RR><<<(unsigned)n_loc, 256, 0, s>>>(c->keys.p, V, (int)T, i0, n_loc, f,        \
+                                                    c->item_max.p, c->d_stats);                \
+  CKL(1);
+    if (R == 8) { LAUNCH_3D(8) } else if (R == 4) { LAUNCH_3D(4) } else { LAUNCH_3D(2) }
+#undef LAUNCH_3D
+  } else {
+    CK(cudaEventRecord(c->kev[4], s));
+  }
+  CK(cudaEventRecord(c->kev[5], s));
+
+  // Planar: keys Z2 in [2zmin-1, 2zmax+1], etc.
+  PlaneSpace ps;
+  ps.lo[0] = 2 * bb[2] - 1; ps.cnt[0] = 2 * (bb[5] - bb[2]) + 3;
+  ps.lo[1] = 2 * bb[1] - 1; ps.cnt[1] = 2 * (bb[4] - bb[1]) + 3;
+  ps.lo[2] = 2 * bb[0] - 1; ps.cnt[2] = 2 * (bb[3] - bb[0]) + 3;
+  const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
+  CK(c->plane_counts.ensure(P));
+  CK(c->plane_start.ensure(P + 1));
+  CK(c->plane_cursor.ensure(P));
+  CK(c->plane_sorted.ensure((size_t)(3 * V)));
+  CK(cudaMemsetAsync(c->plane_counts.p, 0, sizeof(unsigned int) * P, s));
+  const int vgrid = (int)std::min<long long>((V + 255) / 256, (long long)c->sms * 8);
+  plane_hist<<<vgrid, 256, 0, s>>>(c->keys.p, V, ps, c->plane_counts.p);
+  CKL(1);
+  plane_scan<<<1, 1024, 0, s>>>(c->plane_counts.p, P, c->plane_start.p, c->plane_cursor.p);
+  CKL(1);
+  plane_scatter<<<vgrid, 256, 0, s>>>(c->keys.p, V, ps, c->plane_cursor.p, c->plane_sorted.p);
+  CKL(1);
+  const int p0 = (int)((long long)P * shard / nshards), p1 = (int)((long long)P * (shard + 1) / nshards);
+  if (p1 > p0) {
+    const int pgrid = std::min(p1 - p0, c->sms * 8);
+    plane_pairs<<<pgrid, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, p0, p1, ps, f,
+                                      c->d_stats);
+    CKL(1);
+  }
+  CK(cudaEventRecord(c->kev[6], s));
+  return SC_OK;
+}
+
+void fill_out(const Stats& h, const double sp[3], sc_coeffs* out) {
+  static const int* tri = [] {
+    static int t[kNumCases];
+    for (int k = 0; k < kNumCases; k++) t[k] = case_geom().ntri[k];
+    return t;
+  }();
+  double at[kNumCases];
+  area_table(sp, at);
+  double area = 0.0;
+  long long T = 0, active = 0;
+  for (int k = 0; k < kNumCases; k++) {
+    if (!h.hist[k]) continue;
+    area += (double)h.hist[k] * at[k];
+    T += (long long)h.hist[k] * tri[k];
+    active += (long long)h.hist[k];
+  }
+  const long long K = h.vol_k < 0 ? -h.vol_k : h.vol_k;
+  out->mesh_volume = (double)K * sp[0] * sp[1] * sp[2] / 48.0;
+  out->surface_area = area;
+  out->max_3d_diameter = std::sqrt(f64_of(h.sq[0]));
+  out->max_2d_diameter_xy = std::sqrt(f64_of(h.sq[1]));
+  out->max_2d_diameter_xz = std::sqrt(f64_of(h.sq[2]));
+  out->max_2d_diameter_yz = std::sqrt(f64_of(h.sq[3]));
+  out->vertex_count = (int64_t)h.n_vert;
+  out->triangle_count = T;
+  out->active_cubes = active;
+}
+
+float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+// Full pipeline on a device-resident mask (context lock held by the caller).
+int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, const double sp[3],
+            cudaStream_t s, int shard, int nshards, double* d_sq4, sc_coeffs* out) {
+  CK(cudaEventRecord(c->ev[2], s));
+  int rc = run_mc(c, d_mask, nx, ny, nz, s);
+  if (rc) return rc;
+  CK(cudaEventRecord(c->ev[3], s));
+  if (c->h_stats->bbox[3] < 0) {
+    set_err("mask has no occupied voxels");
+    return SC_ERR_EMPTY_ROI;
+  }
+  rc = run_diameters(c, sp, s, shard, nshards);
+  if (rc) return rc;
+  CK(cudaEventRecord(c->ev[4], s));
+  if (d_sq4)
+    CK(cudaMemcpyAsync(d_sq4, c->d_stats->sq, 4 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  fill_out(*c->h_stats, sp, out);
+  out->mesh_ms = ev_ms(c->ev[2], c->ev[3]);
+  out->diameters_ms = ev_ms(c->ev[3], c->ev[4]);
+  c->last_ms[0] = ev_ms(c->kev[0], c->kev[1]);
+  c->last_ms[1] = ev_ms(c->kev[1], c->kev[2]);
+  c->last_ms[2] = ev_ms(c->kev[3], c->kev[4]);
+  c->last_ms[3] = ev_ms(c->kev[4], c->kev[5]);
+  c->last_ms[4] = ev_ms(c->kev[5], c->kev[6]);
+  c->last_ms[5] = 0.0;
+  return SC_OK;
+}
+
+double wall_ms() {
+  using namespace std::chrono;
+  return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+int current_ctx(Ctx** c) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  return get_ctx(dev, c);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sc_last_error(void) { return g_err.c_str(); }
+int sc_abi_version(void) { return SC_ABI_VERSION; }
+
+int sc_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int sc_calculate_coefficients_device(const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
+                                     const double spacing[3], void* stream, sc_coeffs* out) {
+  return sc_calculate_coefficients_shard(d_mask, nx, ny, nz, spacing, stream, 0, 1, nullptr, out);
+}
+
+int sc_calculate_coefficients_shard(const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
+                                    const double spacing[3], void* stream, int shard,
+                                    int nshards, double* d_sq4, sc_coeffs* out) {
+  const double t0 = wall_ms();
+  int rc = check_input(d_mask, nx, ny, nz, spacing);
+  if (rc) return rc;
+  if (!out || nshards < 1 || shard < 0 || shard >= nshards) {
+    set_err("bad output pointer or shard %d of %d", shard, nshards);
+    return SC_ERR_INPUT;
+  }
+  Ctx* c;
+  if ((rc = current_ctx(&c))) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  std::memset(out, 0, sizeof *out);
+  rc = run_roi(c, d_mask, nx, ny, nz, spacing, s, shard, nshards, d_sq4, out);
+  out->total_ms = wall_ms() - t0;
+  return rc;
+}
+
+int sc_calculate_coefficients(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz,
+                              const double spacing[3], int device, sc_coeffs* out) {
+  const double t0 = wall_ms();
+  int rc = check_input(mask, nx, ny, nz, spacing);
+  if (rc) return rc;
+  if (!out) { set_err("out is NULL"); return SC_ERR_INPUT; }
+  Ctx* c;
+  if ((rc = get_ctx(device, &c))) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(device));
+  std::memset(out, 0, sizeof *out);
+  const size_t bytes = (size_t)nx * ny * nz;
+  CK(c->mask_stage.ensure(bytes));
+  cudaStream_t s = c->stream;
+  CK(cudaEventRecord(c->ev[0], s));
+  CK(cudaMemcpyAsync(c->mask_stage.p, mask, bytes, cudaMemcpyHostToDevice, s));
+  CK(cudaEventRecord(c->ev[1], s));
+  rc = run_roi(c, c->mask_stage.p, nx, ny, nz, spacing, s, 0, 1, nullptr, out);
+  out->h2d_ms = ev_ms(c->ev[0], c->ev[1]);
+  c->last_ms[5] = out->h2d_ms;
+  out->total_ms = wall_ms() - t0;
+  return rc;
+}
+
+int sc_calculate_coefficients_batch(const uint8_t* const* masks, const int64_t* dims,
+                                    const double* spacings, int64_t count, int device,
+                                    sc_coeffs* out) {
+  if (count < 0 || (count > 0 && (!masks || !dims || !spacings || !out))) {
+    set_err("bad batch arguments");
+    return SC_ERR_INPUT;
+  }
+  int first = SC_OK;
+  std::string first_err;
+  for (int64_t i = 0; i < count; i++) {
+    int rc = sc_calculate_coefficients(masks[i], dims[3 * i], dims[3 * i + 1], dims[3 * i + 2],
+                                       spacings + 3 * i, device, out + i);
+    if (rc && first == SC_OK) { first = rc; first_err = g_err; }
+  }
+  if (first) g_err = first_err;
+  return first;
+}
+
+int sc_diameters(const double* xs, const double* ys, const double* zs, int64_t n, int device,
+                 double out[4]) {
+  if (!out || (n > 0 && (!xs || !ys || !zs))) { set_err("NULL argument"); return SC_ERR_INPUT; }
+  if (n <= 0) { set_err("diameters need at least one vertex"); return SC_ERR_NO_VERTICES; }
+  if (n > (1LL << 31)) { set_err("too many points"); return SC_ERR_INPUT; }
+  Ctx* c;
+  int rc = get_ctx(device, &c);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(device));
+  cudaStream_t s = c->stream;
+  CK(c->cloud.ensure((size_t)(3 * n)));
+  CK(c->cloud_out.ensure(4));
+  CK(cudaMemcpyAsync(c->cloud.p, xs, n * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->cloud.p + n, ys, n * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->cloud.p + 2 * n, zs, n * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(c->cloud_out.p, 0, 32, s));
+  const long long T = (n + 255) / 256;
+  cloud_diameters<<<(unsigned)(T * (T + 1) / 2), 256, 0, s>>>(c->cloud.p, c->cloud.p + n,
+                                                               c->cloud.p + 2 * n, n, (int)T,
+                                                               c->cloud_out.p);
+  CKL(1);
+  unsigned long long hb[4];
+  CK(cudaMemcpyAsync(hb, c->cloud_out.p, 32, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int i = 0; i < 4; i++) out[i] = std::sqrt(f64_of(hb[i]));
+  return SC_OK;
+}
+
+int sc_mesh_vertices(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, int device,
+                     int32_t* keys, int64_t cap, int64_t* n_out) {
+  const double unit[3] = {1.0, 1.0, 1.0};
+  int rc = check_input(mask, nx, ny, nz, unit);
+  if (rc) return rc;
+  if (!n_out || (cap > 0 && !keys)) { set_err("NULL argument"); return SC_ERR_INPUT; }
+  Ctx* c;
+  if ((rc = get_ctx(device, &c))) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(device));
+  const size_t bytes = (size_t)nx * ny * nz;
+  CK(c->mask_stage.ensure(bytes));
+  cudaStream_t s = c->stream;
+  CK(cudaMemcpyAsync(c->mask_stage.p, mask, bytes, cudaMemcpyHostToDevice, s));
+  if ((rc = run_mc(c, c->mask_stage.p, nx, ny, nz, s))) return rc;
+  if (c->h_stats->bbox[3] < 0) { set_err("mask has no occupied voxels"); return SC_ERR_EMPTY_ROI; }
+  const long long V = (long long)c->h_stats->n_vert;
+  *n_out = V;
+  const long long m = V < cap ? V : cap;
+  if (m > 0) {
+    std::vector<int4> tmp((size_t)m);
+    CK(cudaMemcpyAsync(tmp.data(), c->keys.p, m * sizeof(int4), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (long long i = 0; i < m; i++) {
+      keys[3 * i] = tmp[i].x;
+      keys[3 * i + 1] = tmp[i].y;
+      keys[3 * i + 2] = tmp[i].z;
+    }
+  }
+  return SC_OK;
+}
+
+int sc_last_kernel_times(int device, double* ms, int n) {
+  Ctx* c;
+  int rc = get_ctx(device, &c);
+  if (rc) return -rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  int m = n < 6 ? n : 6;
+  for (int i = 0; i < m; i++) ms[i] = c->last_ms[i];
+  return m;
+}
+
+uint64_t sc_launch_count(void) { return g_launches.load(); }
+
+int sc_probe_fp32_peak(int device, int mode, double* tflops) {
+  if (!tflops) { set_err("NULL argument"); return SC_ERR_INPUT; }
+  Ctx* c;
+  int rc = get_ctx(device, &c);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(device));
+  cudaStream_t s = c->stream;
+  float* d_out;
+  const int blocks = c->sms * 8, threads = 256, iters = 1 << 14;
+  CK(cudaMalloc(&d_out, sizeof(float) * blocks * threads));
+  float best = 0.f;
+  for (int rep = 0; rep < 4; rep++) {
+    CK(cudaEventRecord(c->ev[0], s));
+    switch (mode) {
+      case 0: fp32_probe<0><<<blocks, threads, 0, s>>>(d_out, iters, 1.0001f, 0.5f); break;
+      case 1: fp32_probe<1><<<blocks, threads, 0, s>>>(d_out, iters, 1.0001f, 0.5f); break;
+      case 2: fp32_probe<2><<<blocks, threads, 0, s>>>(d_out, iters, 1.0001f, 0.5f); break;
+      default: fp32_probe<3><<<blocks, threads, 0, s>>>(d_out, iters, 1.0001f, 0.5f); break;
+    }
+    CKL(1);
+    CK(cudaEventRecord(c->ev[1], s));
+    CK(cudaEventSynchronize(c->ev[1]));
+    float ms = ev_ms(c->ev[0], c->ev[1]);
+    if (rep > 0 && (best == 0.f || ms < best)) best = ms;
+  }
+  cudaFree(d_out);
+  // 16 FFMA2 (4 flop) or 16 FFMA (2 flop) per thread per iteration.
+  const double flop = (double)blocks * threads * iters * 16.0 * ((mode == 0 || mode == 2) ? 4.0 : 2.0);
+  *tflops = flop / (best * 1e-3) / 1e12;
+  return SC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,262 @@
+// Marching-cubes stage of the shape-coefficient path (sm_100a).
+//
+// Replaces reference pad_mask + _count_triangles + _count_crossed_edges +
+// _emit_mesh (pkg/src/shapecore/mesh.py:55-199) and the triangle gathers of
+// surface_area / mesh_volume (features.py:83-110).  Two kernels:
+//
+//  1. pack_bits_*  -- the one HBM-bound pass: streams the uint8 mask once with
+//     128-bit loads (evict-first), writes a 1-bit-per-voxel volume (row-padded
+//     to 32-bit words, 1/8 of the mask, stays in L2) and the occupied bounding
+//     box.  The reference's 1-voxel zero padding is never materialised: voxels
+//     outside the grid read as 0.
+//  2. mc_cells     -- walks only the bounding box (+1 shell) of the bit volume,
+//     32 cells per thread per step with bitwise ops: active-cell mask, per-case
+//     histogram (smem atomics), exact integer volume sum, and crossed-edge
+//     masks.  Each crossed lattice edge is one mesh vertex (mesh.py:94-100 ==
+//     mesh.py:176 dedup key); vertices are stream-compacted with a warp scan and
+//     one global atomic per warp-step, as doubled lattice coordinates.
+//
+// Triangles are never materialised: T = sum_k hist[k]*TRI_COUNT[k], area =
+// sum_k hist[k]*A_k(spacing) and volume = |K| sx sy sz / 48 with K the exact
+// integer sum accumulated here.
+#include <climits>
+
+#include "sc_device.cuh"
+
+namespace sc {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__global__ void init_stats(Stats* st) {
+  int t = threadIdx.x;
+  for (int i = t; i < (int)(sizeof(Stats) / 8); i += blockDim.x)
+    reinterpret_cast<unsigned long long*>(st)[i] = 0ull;
+  __syncthreads();
+  if (t < 3) st->bbox[t] = INT_MAX;
+  if (t >= 3 && t < 6) st->bbox[t] = -1;
+}
+
+// 4 mask bytes -> 4 occupancy bits (byte i nonzero -> bit i).  The multiply
+// places byte i's flag at bit 21+i with no carries (all 16 partial products
+// land on distinct bit positions).
+__device__ __forceinline__ uint32_t nib4(uint32_t v) {
+  uint32_t m = __vcmpne4(v, 0u) & 0x01010101u;
+  return ((m * 0x00204081u) >> 21) & 0xFu;
+}
+
+struct BoxAcc {
+  int x0 = INT_MAX, y0 = INT_MAX, z0 = INT_MAX, x1 = -1, y1 = -1, z1 = -1;
+  __device__ __forceinline__ void add(uint32_t word, long long wi, int W, int ny) {
+    long long row = wi / W;
+    int w = (int)(wi - row * W);
+    int z = (int)(row / ny), y = (int)(row - (long long)z * ny);
+    int xa = 32 * w + __ffs(word) - 1, xb = 32 * w + 31 - __clz(word);
+    x0 = min(x0, xa); x1 = max(x1, xb);
+    y0 = min(y0, y);  y1 = max(y1, y);
+    z0 = min(z0, z);  z1 = max(z1, z);
+  }
+  __device__ __forceinline__ void flush(Stats* st) {
+    // Integer warp reductions (REDUX), then one atomic per field per warp.
+    int hx1 = __reduce_max_sync(kFull, x1);
+    if (hx1 < 0) return;  // warp saw no occupied voxel (uniform)
+    int v[6] = {(int)__reduce_min_sync(kFull, (unsigned)x0), (int)__reduce_min_sync(kFull, (unsigned)y0),
+                (int)__reduce_min_sync(kFull, (unsigned)z0), hx1,
+                __reduce_max_sync(kFull, y1), __reduce_max_sync(kFull, z1)};
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&st->bbox[0], v[0]); atomicMin(&st->bbox[1], v[1]); atomicMin(&st->bbox[2], v[2]);
+      atomicMax(&st->bbox[3], v[3]); atomicMax(&st->bbox[4], v[4]); atomicMax(&st->bbox[5], v[5]);
+    }
+  }
+};
+
+// Fast path: nx % 32 == 0 and a 16-byte aligned mask.  One 16-byte chunk per
+// thread per step (a warp reads 512 contiguous bytes per load instruction);
+// lane pairs merge their 16-bit halves into one 32-bit word.  U chunks are in
+// flight per thread for memory-level parallelism.
+template <int U>
+__global__ void __launch_bounds__(256) pack_bits_v16(const uint4* __restrict__ mask,
+                                                     uint32_t* __restrict__ bits,
+                                                     long long n_chunks, int W, int ny,
+                                                     Stats* __restrict__ st) {
+  BoxAcc box;
+  const long long step = (long long)gridDim.x * blockDim.x * U;
+  for (long long base = (long long)blockIdx.x * blockDim.x * U; base < n_chunks; base += step) {
+    uint4 v[U];
+#pragma unroll
+    for (int k = 0; k < U; k++) {
+      long long g = base + (long long)k * blockDim.x + threadIdx.x;
+      v[k] = g < n_chunks ? __ldcs(mask + g) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < U; k++) {
+      long long g = base + (long long)k * blockDim.x + threadIdx.x;
+      uint32_t b16 = nib4(v[k].x) | (nib4(v[k].y) << 4) | (nib4(v[k].z) << 8) | (nib4(v[k].w) << 12);
+      uint32_t hi = __shfl_down_sync(kFull, b16, 1);
+      if (!(threadIdx.x & 1) && g < n_chunks) {
+        uint32_t word = b16 | (hi << 16);
+        long long wi = g >> 1;
+        bits[wi] = word;
+        if (word) box.add(word, wi, W, ny);
+      }
+    }
+  }
+  box.flush(st);
+}
+
+// Generic path: any nx / alignment.  One output word per thread, byte loads
+// (still coalesced across the warp within a row).
+__global__ void __launch_bounds__(256) pack_bits_generic(const uint8_t* __restrict__ mask,
+                                                         uint32_t* __restrict__ bits,
+                                                         long long n_words, int nx, int W, int ny,
+                                                         Stats* __restrict__ st) {
+  BoxAcc box;
+  const long long step = (long long)gridDim.x * blockDim.x;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < n_words; base += step) {
+    long long wi = base + threadIdx.x;
+    if (wi < n_words) {
+      long long row = wi / W;
+      int w = (int)(wi - row * W);
+      const uint8_t* src = mask + row * (long long)nx + 32 * w;
+      int n = min(32, nx - 32 * w);
+      uint32_t word = 0;
+      for (int b = 0; b < n; b++) word |= (uint32_t)(__ldcs(src + b) != 0) << b;
+      bits[wi] = word;
+      if (word) box.add(word, wi, W, ny);
+    }
+  }
+  box.flush(st);
+}
+
+// Occupancy window of lattice row (v, w) for word column q: bit i <-> voxel
+// x = 32q - 1 + i, i in [0, 32].  Out-of-grid voxels are background (this IS
+// the reference's zero padding, mesh.py:55-65).
+__device__ __forceinline__ unsigned long long window(const uint32_t* __restrict__ bits, int q,
+                                                     int v, int w, int W, int ny, int nz) {
+  if (v < 0 || v >= ny || w < 0 || w >= nz) return 0ull;
+  const uint32_t* row = bits + ((long long)w * ny + v) * W;
+  unsigned long long cur = q < W ? __ldcg(row + q) : 0u;
+  unsigned long long prev = q > 0 ? __ldcg(row + q - 1) : 0u;
+  return (cur << 1) | (prev >> 31);
+}
+
+constexpr int kZChunk = 8;
+
+// One thread = one (word column q, row v) and kZChunk consecutive z steps.
+// Cell (u, v, w) has lower corner at unpadded voxel (u, v, w), u,v,w >= -1
+// (reference padded cell index minus 1).  The thread owns cells and lattice
+// points u = 32q - 1 + i, i in [0, 31].
+__global__ void __launch_bounds__(256) mc_cells(const uint32_t* __restrict__ bits, int nx, int ny,
+                                                int nz, int W, const CaseTables* __restrict__ tabs,
+                                                Stats* __restrict__ st, int4* __restrict__ vkeys,
+                                                long long cap) {
+  __shared__ unsigned int s_hist[kNumCases];
+  __shared__ int4 s_tn[kNumCases];
+  for (int i = threadIdx.x; i < kNumCases; i += blockDim.x) {
+    s_hist[i] = 0;
+    s_tn[i] = tabs->tn[i];
+  }
+  __syncthreads();
+
+  const int xmin = st->bbox[0], ymin = st->bbox[1], zmin = st->bbox[2];
+  const int xmax = st->bbox[3], ymax = st->bbox[4], zmax = st->bbox[5];
+  long long volk = 0;
+  const int lane = threadIdx.x & 31;
+  if (xmax >= 0) {
+    // Points/cells that can be crossed or active: [min-1, max] on every axis.
+    const int qlo = xmin >> 5, qhi = (xmax + 1) >> 5;
+    const int vlo = ymin - 1, whi = zmax, wlo = zmin - 1;
+    const int nq = qhi - qlo + 1, nv = ymax - vlo + 1;
+    const int nzc = (whi - wlo + 1 + kZChunk - 1) / kZChunk;
+    const long long n_items = (long long)nq * nv * nzc;
+    const long long step = (long long)gridDim.x * blockDim.x;
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < n_items; base += step) {
+      const long long item = base + threadIdx.x;
+      const bool valid = item < n_items;
+      int q = 0, v = 0, w0 = 0;
+      if (valid) {
+        q = qlo + (int)(item % nq);
+        long long r = item / nq;
+        v = vlo + (int)(r % nv);
+        w0 = wlo + (int)(r / nv) * kZChunk;
+      }
+      unsigned long long A = valid ? window(bits, q, v, w0, W, ny, nz) : 0ull;
+      unsigned long long B = valid ? window(bits, q, v + 1, w0, W, ny, nz) : 0ull;
+      const int xbase = 32 * q - 1;
+      for (int s = 0; s < kZChunk; s++) {
+        const int w = w0 + s;
+        const bool on = valid && w <= whi;
+        unsigned long long C = 0, D = 0;
+        uint32_t ex = 0, ey = 0, ez = 0, act = 0;
+        if (on) {
+          C = window(bits, q, v, w + 1, W, ny, nz);
+          D = window(bits, q, v + 1, w + 1, W, ny, nz);
+          ex = (uint32_t)(A ^ (A >> 1));
+          ey = (uint32_t)(A ^ B);
+          ez = (uint32_t)(A ^ C);
+          unsigned long long all = A & B & C & D, any = A | B | C | D;
+          act = (uint32_t)(~(all & (all >> 1)) & (any | (any >> 1)));
+        }
+        // Active cells: case bit c set when corner c is background
+        // (mc_tables.py:10-12, mesh.py:103-128).
+        while (act) {
+          const int i = __ffs(act) - 1;
+          act &= act - 1;
+          uint32_t occ = (uint32_t)((A >> i) & 1) | (uint32_t)(((A >> (i + 1)) & 1) << 1) |
+                         (uint32_t)(((B >> (i + 1)) & 1) << 2) | (uint32_t)(((B >> i) & 1) << 3) |
+                         (uint32_t)(((C >> i) & 1) << 4) | (uint32_t)(((C >> (i + 1)) & 1) << 5) |
+                         (uint32_t)(((D >> (i + 1)) & 1) << 6) | (uint32_t)(((D >> i) & 1) << 7);
+          const int k = (~occ) & 0xff;
+          atomicAdd(&s_hist[k], 1u);
+          const int4 tn = s_tn[k];
+          volk += tn.x + 2ll * ((long long)(xbase + i) * tn.y + (long long)v * tn.z +
+                                (long long)w * tn.w);
+        }
+        // Vertex emission: warp-aggregated stream compaction of crossed edges.
+        const uint32_t c = __popc(ex) + __popc(ey) + __popc(ez);
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          uint32_t t = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        if (total) {
+          unsigned long long wbase = 0;
+          if (lane == 31) wbase = atomicAdd(&st->n_vert, (unsigned long long)total);
+          wbase = __shfl_sync(kFull, wbase, 31);
+          long long o = (long long)(wbase + incl - c);
+          const int Y2 = 2 * v, Z2 = 2 * w;
+          while (ex) {
+            const int i = __ffs(ex) - 1; ex &= ex - 1;
+            if (o < cap) vkeys[o] = make_int4(2 * (xbase + i) + 1, Y2, Z2, 0);
+            o++;
+          }
+          while (ey) {
+            const int i = __ffs(ey) - 1; ey &= ey - 1;
+            if (o < cap) vkeys[o] = make_int4(2 * (xbase + i), Y2 + 1, Z2, 0);
+            o++;
+          }
+          while (ez) {
+            const int i = __ffs(ez) - 1; ez &= ez - 1;
+            if (o < cap) vkeys[o] = make_int4(2 * (xbase + i), Y2, Z2 + 1, 0);
+            o++;
+          }
+        }
+        A = C;
+        B = D;
+      }
+    }
+  }
+  // Block flush: exact integer partials.
+#pragma unroll
+  for (int o = 16; o; o >>= 1) volk += __shfl_xor_sync(kFull, volk, o);
+  if (lane == 0 && volk) atomicAdd(reinterpret_cast<unsigned long long*>(&st->vol_k),
+                                   (unsigned long long)volk);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kNumCases; i += blockDim.x)
+    if (s_hist[i]) atomicAdd(&st->hist[i], (unsigned long long)s_hist[i]);
+}
+
+template __global__ void pack_bits_v16<4>(const uint4*, uint32_t*, long long, int, int, Stats*);
+
+}  // namespace sc

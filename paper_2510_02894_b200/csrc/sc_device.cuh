@@ -1,0 +1,68 @@
+// Shared device-side definitions of the shape-coefficient kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sc {
+
+constexpr int kNumCases = 256;
+
+// Device-resident accumulators of one ROI.  Every field is an exact integer
+// (or an fp bit pattern updated with integer atomicMax), so results do not
+// depend on block scheduling.
+struct Stats {
+  unsigned long long hist[kNumCases];  // active cells per MC case (0/255 never counted)
+  unsigned long long n_vert;           // crossed lattice edges == mesh vertices
+  long long vol_k;                     // 48*volume/(sx*sy*sz), exact (Appendix A)
+  int bbox[6];                         // xmin, ymin, zmin, xmax, ymax, zmax of occupied voxels
+  unsigned int d3_f32;                 // fp32 bits of the pass-1 max squared 3-D distance
+  unsigned int pad0;
+  unsigned long long sq[4];            // fp64 bits: exact squared maxima (3d, xy, xz, yz)
+  unsigned long long n_refined;        // tile pairs re-evaluated in fp64 (diagnostic)
+};
+
+// Per-case integer tables for the exact volume path: for case k,
+// t = sum over its triangles of a.(b x c) and n = sum of (b-a) x (c-a), with
+// a, b, c the DOUBLED cell-local vertex coordinates (in {0,1,2}^3).
+struct CaseTables {
+  int4 tn[kNumCases];  // (t, n.x, n.y, n.z)
+};
+
+// Geometry of one launch: doubled-coordinate centre and half spacings used to
+// build the pass-1 fp32 frame, and the fp64 spacing for the exact re-check.
+struct Frame {
+  int cx2, cy2, cz2;   // bbox centre in doubled lattice units (xmin + xmax, ...)
+  float hx, hy, hz;    // fp32(0.5 * spacing)
+  double sx, sy, sz;   // spacing (fp64, reference arithmetic)
+};
+
+// Planar key space: [0, cnt[0]) XY planes keyed by Z2, then cnt[1] XZ planes
+// keyed by Y2, then cnt[2] YZ planes keyed by X2; lo = smallest key per axis.
+struct PlaneSpace {
+  int lo[3];
+  int cnt[3];
+};
+
+// fp32 (non-negative) max through the unsigned bit pattern.
+__device__ __forceinline__ void atomic_max_pos_f32(unsigned int* addr, float v) {
+  atomicMax(addr, __float_as_uint(v));
+}
+__device__ __forceinline__ void atomic_max_pos_f64(unsigned long long* addr, double v) {
+  atomicMax(addr, (unsigned long long)__double_as_longlong(v));
+}
+
+// Reference pair distance, features.py:140-143: dx*dx + dy*dy + dz*dz in fp64,
+// left to right, every operation rounded (no FMA contraction).
+__device__ __forceinline__ double ref_sq_dist(double xi, double yi, double zi, double xj,
+                                              double yj, double zj) {
+  double dx = __dsub_rn(xj, xi), dy = __dsub_rn(yj, yi), dz = __dsub_rn(zj, zi);
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+// Reference vertex coordinate, mesh.py:184-195: (l - 1 + 0.5*[axis]) * s, which
+// in doubled units is (key / 2) * s; key/2 is exact in fp64.
+__device__ __forceinline__ double ref_coord(int key2, double s) {
+  return __dmul_rn((double)key2 * 0.5, s);
+}
+
+}  // namespace sc

@@ -1,0 +1,246 @@
+"""Shape features on the B200: the reference API over the C ABI.
+
+Mirrors reference pkg/src/shapecore/features.py: `FEATURE_KEYS` (:27-35),
+`ShapeFeatures` (:38-60), `extract_features` (:224-265), `diameters` /
+`diameters_parallel` (:205-221).  `calculate_coefficients(mask, spacing)` is
+the north_star entry (PyRadiomics cShape.calculate_coefficients); it returns
+the same 7-key record plus the exact triangle and active-cube counts.
+
+Every call goes to libshapecore_b200.so (hand-written sm_100a kernels).  There
+is one implementation: no backend dispatch and no CPU fallback.  `selection`
+arguments are accepted for signature compatibility with the reference and
+are otherwise ignored.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple, Union
+
+import numpy as np
+
+from . import _native
+from .errors import NoVertices
+from .timing import StageTimings, now_ms
+from .volume import MaskVolume, _check_spacing
+
+FEATURE_KEYS = (
+    "MeshVolume",
+    "SurfaceArea",
+    "Maximum3DDiameter",
+    "Maximum2DDiameterXY",
+    "Maximum2DDiameterXZ",
+    "Maximum2DDiameterYZ",
+    "VertexCount",
+)
+
+
+@dataclass(frozen=True)
+class ShapeFeatures:
+    """The five shape scalars plus the vertex count (features.py:38-60)."""
+
+    mesh_volume: float
+    surface_area: float
+    max_3d_diameter: float
+    max_2d_diameter_xy: float
+    max_2d_diameter_xz: float
+    max_2d_diameter_yz: float
+    vertex_count: int
+
+    def to_dict(self) -> Dict[str, Union[float, int]]:
+        return {
+            "MeshVolume": self.mesh_volume,
+            "SurfaceArea": self.surface_area,
+            "Maximum3DDiameter": self.max_3d_diameter,
+            "Maximum2DDiameterXY": self.max_2d_diameter_xy,
+            "Maximum2DDiameterXZ": self.max_2d_diameter_xz,
+            "Maximum2DDiameterYZ": self.max_2d_diameter_yz,
+            "VertexCount": self.vertex_count,
+        }
+
+
+@dataclass(frozen=True)
+class Coefficients(ShapeFeatures):
+    """ShapeFeatures plus the exact counts and stage times of the B200 run."""
+
+    triangle_count: int = 0
+    active_cubes: int = 0
+    h2d_ms: float = 0.0
+    mesh_ms: float = 0.0
+    diameters_ms: float = 0.0
+    total_ms: float = 0.0
+
+
+def _from_struct(c: _native.ScCoeffs) -> Coefficients:
+    return Coefficients(
+        mesh_volume=c.mesh_volume,
+        surface_area=c.surface_area,
+        max_3d_diameter=c.max_3d_diameter,
+        max_2d_diameter_xy=c.max_2d_diameter_xy,
+        max_2d_diameter_xz=c.max_2d_diameter_xz,
+        max_2d_diameter_yz=c.max_2d_diameter_yz,
+        vertex_count=int(c.vertex_count),
+        triangle_count=int(c.triangle_count),
+        active_cubes=int(c.active_cubes),
+        h2d_ms=c.h2d_ms,
+        mesh_ms=c.mesh_ms,
+        diameters_ms=c.diameters_ms,
+        total_ms=c.total_ms,
+    )
+
+
+def _as_mask(mask) -> Tuple[np.ndarray, Tuple[int, int, int]]:
+    """(nz, ny, nx) array or MaskVolume -> contiguous uint8 host buffer + dims."""
+    if isinstance(mask, MaskVolume):
+        return np.ascontiguousarray(mask.data, dtype=np.uint8), tuple(mask.dims)
+    arr = np.asarray(mask)
+    if arr.ndim != 3:
+        raise ValueError(f"mask array must be 3-D (nz, ny, nx), got {arr.ndim}-D")
+    if arr.dtype == np.bool_:
+        arr = arr.view(np.uint8)
+    elif arr.dtype != np.uint8:
+        arr = (arr != 0).astype(np.uint8)
+    arr = np.ascontiguousarray(arr)
+    nz, ny, nx = arr.shape
+    return arr.reshape(-1), (nx, ny, nz)
+
+
+def calculate_coefficients(mask, spacing: Sequence[float] = (1.0, 1.0, 1.0),
+                           device: int = 0) -> Coefficients:
+    """Full shape coefficients of a host mask ((nz, ny, nx) array or MaskVolume).
+
+    Raises EmptyRoi for an all-background mask and NonPositiveSpacing for a
+    bad spacing, as the reference does (mesh.py:78-79, volume.py:94-101).
+    """
+    if isinstance(mask, MaskVolume) and spacing is None:
+        spacing = mask.spacing
+    sp = np.asarray(_check_spacing(spacing), dtype=np.float64)
+    data, (nx, ny, nz) = _as_mask(mask)
+    lib = _native.load()
+    out = _native.ScCoeffs()
+    rc = lib.sc_calculate_coefficients(
+        data.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), nx, ny, nz,
+        sp.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), int(device), ctypes.byref(out))
+    _native.raise_for(rc, "sc_calculate_coefficients")
+    return _from_struct(out)
+
+
+def calculate_coefficients_device(mask, spacing: Sequence[float], stream=None) -> Coefficients:
+    """Coefficients of a device-resident mask: a CUDA uint8 tensor (nz, ny, nx)
+    on the current device (torch is plumbing only: pointer + stream)."""
+    sp = np.asarray(_check_spacing(spacing), dtype=np.float64)
+    nz, ny, nx = (int(d) for d in mask.shape)
+    if not mask.is_contiguous():
+        raise ValueError("device mask must be contiguous")
+    handle = 0 if stream is None else int(stream.cuda_stream)
+    out = _native.ScCoeffs()
+    rc = _native.load().sc_calculate_coefficients_device(
+        ctypes.c_void_p(mask.data_ptr()), nx, ny, nz,
+        sp.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.c_void_p(handle),
+        ctypes.byref(out))
+    _native.raise_for(rc, "sc_calculate_coefficients_device")
+    return _from_struct(out)
+
+
+def calculate_coefficients_shard(mask, spacing: Sequence[float], shard: int, nshards: int,
+                                 sq4, stream=None) -> Coefficients:
+    """One shard of the pair grid of a device-resident mask.
+
+    `sq4` is a CUDA float64 tensor of 4 elements that receives this shard's
+    squared maxima (3d, xy, xz, yz) for an all_reduce(MAX) across ranks."""
+    sp = np.asarray(_check_spacing(spacing), dtype=np.float64)
+    nz, ny, nx = (int(d) for d in mask.shape)
+    handle = 0 if stream is None else int(stream.cuda_stream)
+    out = _native.ScCoeffs()
+    rc = _native.load().sc_calculate_coefficients_shard(
+        ctypes.c_void_p(mask.data_ptr()), nx, ny, nz,
+        sp.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.c_void_p(handle),
+        int(shard), int(nshards), ctypes.c_void_p(sq4.data_ptr()), ctypes.byref(out))
+    _native.raise_for(rc, "sc_calculate_coefficients_shard")
+    return _from_struct(out)
+
+
+def calculate_coefficients_batch(masks: Sequence, spacings: Sequence[Sequence[float]],
+                                 device: int = 0) -> List[Coefficients]:
+    """C4: many host ROIs on one device, one C call."""
+    bufs, dims = [], []
+    for m in masks:
+        data, d = _as_mask(m)
+        bufs.append(data)
+        dims.extend(d)
+    sp = np.asarray([_check_spacing(s) for s in spacings], dtype=np.float64).reshape(-1)
+    n = len(bufs)
+    ptrs = (ctypes.POINTER(ctypes.c_uint8) * n)(
+        *[b.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)) for b in bufs])
+    dims_arr = np.asarray(dims, dtype=np.int64)
+    outs = (_native.ScCoeffs * n)()
+    rc = _native.load().sc_calculate_coefficients_batch(
+        ptrs, dims_arr.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+        sp.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), n, int(device), outs)
+    _native.raise_for(rc, "sc_calculate_coefficients_batch")
+    return [_from_struct(o) for o in outs]
+
+
+def _as_coord_arrays(xs, ys, zs):
+    """features.py:195-202."""
+    arrs = tuple(np.ascontiguousarray(a, dtype=np.float64) for a in (xs, ys, zs))
+    n = arrs[0].shape[0]
+    if n == 0:
+        raise NoVertices("diameters need at least one vertex")
+    if arrs[1].shape[0] != n or arrs[2].shape[0] != n:
+        raise ValueError("coordinate arrays must have equal length")
+    return arrs
+
+
+def diameters(xs, ys, zs, device: int = 0) -> Tuple[float, float, float, float]:
+    """(max_3d, xy, xz, yz) in mm, bit-exact with the reference (features.py:205-213)."""
+    xs, ys, zs = _as_coord_arrays(xs, ys, zs)
+    out = np.zeros(4, dtype=np.float64)
+    dp = ctypes.POINTER(ctypes.c_double)
+    rc = _native.load().sc_diameters(xs.ctypes.data_as(dp), ys.ctypes.data_as(dp),
+                                     zs.ctypes.data_as(dp), xs.shape[0], int(device),
+                                     out.ctypes.data_as(dp))
+    _native.raise_for(rc, "sc_diameters")
+    return tuple(float(v) for v in out)
+
+
+def diameters_parallel(xs, ys, zs, workers: Optional[int] = None,
+                       device: int = 0) -> Tuple[float, float, float, float]:
+    """Reference signature (features.py:216-221); the GPU kernel is the only path."""
+    return diameters(xs, ys, zs, device=device)
+
+
+def mesh_vertices(mask, device: int = 0) -> np.ndarray:
+    """(V, 3) int32 doubled lattice coordinates of the marching-cubes vertices
+    (coordinate = key / 2 * spacing, mesh.py:182-195); order unspecified."""
+    data, (nx, ny, nz) = _as_mask(mask)
+    lib = _native.load()
+    n = ctypes.c_int64()
+    cap = 1 << 16
+    while True:
+        buf = np.empty((cap, 3), dtype=np.int32)
+        rc = lib.sc_mesh_vertices(data.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), nx, ny,
+                                  nz, int(device),
+                                  buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), cap,
+                                  ctypes.byref(n))
+        _native.raise_for(rc, "sc_mesh_vertices")
+        if n.value <= cap:
+            return buf[: n.value].copy()
+        cap = n.value
+
+
+def extract_features(vol: MaskVolume, selection=None,
+                     device: int = 0) -> Tuple[ShapeFeatures, StageTimings]:
+    """features.py:224-265 on the B200.  Returns (ShapeFeatures, StageTimings);
+    mesh_ms / diameters_ms are CUDA-event stage times, total_ms wall time."""
+    t0 = now_ms()
+    c = calculate_coefficients(vol.as_3d(), vol.spacing, device=device)
+    t1 = now_ms()
+    feats = ShapeFeatures(c.mesh_volume, c.surface_area, c.max_3d_diameter,
+                          c.max_2d_diameter_xy, c.max_2d_diameter_xz, c.max_2d_diameter_yz,
+                          c.vertex_count)
+    total = max(t1 - t0, c.mesh_ms + c.diameters_ms)
+    return feats, StageTimings(file_read_ms=0.0, mesh_ms=c.mesh_ms,
+                               diameters_ms=c.diameters_ms, total_ms=total)

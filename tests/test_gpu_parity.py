@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference.
+
+Expected values come from tests/golden (frozen outputs of the reference,
+tools/make_golden.py) and from the CPU oracle.  Bars (north_star):
+  * bit-exact: vertex / triangle / active-cube counts, and -- because the
+    diameter stage re-checks its candidates in the reference's own fp64
+    arithmetic -- all four diameters;
+  * relative error <= 1e-6 (REL_TOL) for surface area and mesh volume (the GPU
+    sums exact integer histograms; the reference sums per-triangle floats).
+"""
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+
+from conftest import REL_TOL, rel_err
+
+pytestmark = pytest.mark.gpu
+
+DIAM_KEYS = ("Maximum3DDiameter", "Maximum2DDiameterXY", "Maximum2DDiameterXZ",
+             "Maximum2DDiameterYZ")
+
+
+@pytest.fixture(scope="module")
+def sc():
+    import paper_2510_02894_b200 as pkg
+
+    return pkg
+
+
+def assert_matches(got, want_features, triangles, active, label=""):
+    rec = got.to_dict()
+    assert rec["VertexCount"] == want_features["VertexCount"], label
+    assert got.triangle_count == triangles, label
+    assert got.active_cubes == active, label
+    for k in DIAM_KEYS:
+        assert rec[k] == want_features[k], (label, k, rec[k], want_features[k])
+    for k in ("MeshVolume", "SurfaceArea"):
+        assert rel_err(rec[k], want_features[k]) <= REL_TOL, (label, k, rec[k], want_features[k])
+
+
+def test_golden_small_cases(sc, golden, golden_arrays, cuda_device):
+    worst = 0.0
+    for case in golden["cases"]:
+        arr = golden_arrays[case["mask_key"]]
+        got = sc.calculate_coefficients(arr, case["spacing"], device=cuda_device)
+        assert_matches(got, case["features"], case["triangle_count"], case["active_cubes"],
+                       case["name"])
+        for k in ("MeshVolume", "SurfaceArea"):
+            worst = max(worst, rel_err(got.to_dict()[k], case["features"][k]))
+    assert worst <= 1e-12  # in practice: only summation-order differences
+
+
+def test_vertex_sets_match_reference(sc, golden, golden_arrays, cuda_device):
+    n = 0
+    for case in golden["cases"]:
+        if "verts_key" not in case:
+            continue
+        sp = np.asarray(case["spacing"])
+        keys = sc.mesh_vertices(golden_arrays[case["mask_key"]], device=cuda_device)
+        got = keys.astype(np.float64) * 0.5 * sp  # same arithmetic as mesh.py:184-195
+        want = golden_arrays[case["verts_key"]]
+        assert got.shape == want.shape, case["name"]
+        assert set(map(tuple, got.tolist())) == set(map(tuple, want.tolist())), case["name"]
+        assert len(set(map(tuple, keys.tolist()))) == len(keys)  # deduplicated
+        n += 1
+    assert n >= 10
+
+
+def test_clouds_bit_exact(sc, golden, golden_clouds, cuda_device):
+    for c in golden["clouds"]:
+        xs, ys, zs = golden_clouds[c["key"]]
+        assert list(sc.diameters(xs, ys, zs, device=cuda_device)) == c["diameters"], c["key"]
+
+
+def test_known_answers(sc, cuda_device):
+    # pkg/tests/test_features.py:62-89, test_acceptance.py:20-39
+    vox = sc.synth_mask("box", (3, 3, 3), lo=(1, 1, 1), hi=(1, 1, 1))
+    c = sc.calculate_coefficients(vox, (1, 1, 1), device=cuda_device)
+    assert c.vertex_count == 6 and c.triangle_count == 8
+    assert abs(c.mesh_volume - 1 / 6) <= 1e-9 and abs(c.surface_area - math.sqrt(3)) <= 1e-9
+    assert (c.max_3d_diameter, c.max_2d_diameter_xy, c.max_2d_diameter_xz,
+            c.max_2d_diameter_yz) == (1.0, 1.0, 1.0, 1.0)
+    assert sc.diameters([0.0, 3.0], [0.0, 4.0], [0.0, 0.0]) == (5.0, 5.0, 0.0, 0.0)
+    assert sc.diameters([2.5], [2.5], [2.5]) == (0.0, 0.0, 0.0, 0.0)
+
+
+def test_errors(sc, cuda_device):
+    with pytest.raises(sc.EmptyRoi):
+        sc.calculate_coefficients(np.zeros((4, 4, 4), np.uint8), device=cuda_device)
+    with pytest.raises(sc.EmptyRoi):
+        sc.calculate_coefficients(np.zeros((3, 5, 64), np.uint8), device=cuda_device)
+    with pytest.raises(sc.NonPositiveSpacing):
+        sc.calculate_coefficients(np.ones((3, 3, 3), np.uint8), (1.0, 0.0, 1.0))
+    with pytest.raises(sc.NonPositiveSpacing):
+        sc.calculate_coefficients(np.ones((3, 3, 3), np.uint8), (1.0, float("nan"), 1.0))
+    with pytest.raises(sc.NoVertices):
+        sc.diameters(np.zeros(0), np.zeros(0), np.zeros(0))
+
+
+def test_aligned_and_generic_pack_paths_agree(sc, oracle_mod, cuda_device):
+    """nx % 32 == 0 takes the 128-bit path; x offsets exercise word seams."""
+    rng = np.random.default_rng(3)
+    for nx in (32, 64, 96, 31, 33, 65):
+        arr = (rng.random((9, 7, nx)) < 0.3).astype(np.uint8)
+        arr[:, :, 0] = 1  # occupied voxels on the x faces and the word seams
+        arr[:, :, -1] = 1
+        want = oracle_mod.extract_features(arr, (1.0, 1.0, 1.0), threads=0)
+        got = sc.calculate_coefficients(arr, (1.0, 1.0, 1.0), device=cuda_device)
+        assert got.vertex_count == want["VertexCount"], nx
+        assert got.triangle_count == want["triangle_count"], nx
+        assert got.active_cubes == want["active_cubes"], nx
+        for k in DIAM_KEYS:
+            assert got.to_dict()[k] == want[k], (nx, k)
+        for k in ("MeshVolume", "SurfaceArea"):
+            assert rel_err(got.to_dict()[k], want[k]) <= REL_TOL
+
+
+def test_nonbinary_values_count_as_occupied(sc, oracle_mod, cuda_device):
+    arr = sc.synth_mask("sphere", (20, 20, 32), radius=6).astype(np.uint8) * 7
+    a = sc.calculate_coefficients(arr, device=cuda_device)
+    b = sc.calculate_coefficients((arr != 0).astype(np.uint8), device=cuda_device)
+    assert a.to_dict() == b.to_dict()
+
+
+def test_spacing_scaling_exact(sc, cuda_device):
+    # pkg/tests/test_acceptance.py:102-116
+    vol = sc.synth_mask("ellipsoid", (24, 22, 20), semi_axes=(8, 7, 6))
+    f1 = sc.calculate_coefficients(vol, (1.0, 1.0, 1.0))
+    f2 = sc.calculate_coefficients(vol, (2.0, 2.0, 2.0))
+    assert f2.mesh_volume == 8.0 * f1.mesh_volume
+    assert f2.surface_area == 4.0 * f1.surface_area
+    assert f2.max_3d_diameter == 2.0 * f1.max_3d_diameter
+    assert f2.max_2d_diameter_xy == 2.0 * f1.max_2d_diameter_xy
+    assert f2.max_2d_diameter_xz == 2.0 * f1.max_2d_diameter_xz
+    assert f2.max_2d_diameter_yz == 2.0 * f1.max_2d_diameter_yz
+
+
+def test_axis_swap_permutes_planar(sc, cuda_device):
+    # pkg/tests/test_features.py:173-190
+    arr = sc.synth_mask("ellipsoid", (26, 22, 18), semi_axes=(9.0, 7.0, 5.5))
+    f0 = sc.calculate_coefficients(arr, (1.0, 0.5, 2.0))
+    f1 = sc.calculate_coefficients(np.ascontiguousarray(arr.transpose(0, 2, 1)), (0.5, 1.0, 2.0))
+    assert f1.vertex_count == f0.vertex_count
+    assert f1.max_2d_diameter_xy == f0.max_2d_diameter_xy
+    assert f1.max_2d_diameter_xz == f0.max_2d_diameter_yz
+    assert f1.max_2d_diameter_yz == f0.max_2d_diameter_xz
+
+
+def test_extract_features_api(sc, cuda_device):
+    vol = sc.MaskVolume.from_array(sc.synth_mask("sphere", (40, 40, 40), radius=15))
+    feats, t = sc.extract_features(vol)
+    assert tuple(feats.to_dict()) == sc.FEATURE_KEYS
+    assert isinstance(feats.to_dict()["VertexCount"], int)
+    assert t.total_ms >= t.mesh_ms + t.diameters_ms
+    assert 28.0 <= feats.max_3d_diameter <= 32.0
+
+
+def _big(sc, name):
+    from paper_2510_02894_b200 import synth
+
+    if name.startswith("C1"):
+        return synth.synth_mask("sphere", (64, 64, 64), radius=24)
+    if name.startswith("C5"):
+        return synth.thin_slab()
+    return synth.kits_like(tumor_mm=30.0)
+
+
+@pytest.mark.parametrize("name", ["C1_sphere64_r24", "C5_thin_slab", "C2_kits_R30"])
+def test_big_configs(sc, golden, name, cuda_device):
+    case = next(c for c in golden["big"] if c["name"] == name)
+    arr = _big(sc, name)
+    assert hashlib.sha256(arr.tobytes()).hexdigest() == case["sha256"]
+    got = sc.calculate_coefficients(arr, case["spacing"], device=cuda_device)
+    assert_matches(got, case["features"], case["triangle_count"], case["active_cubes"], name)
+
+
+def test_device_entry_and_shards(sc, golden, cuda_device):
+    import torch
+
+    from paper_2510_02894_b200 import synth
+
+    case = next(c for c in golden["big"] if c["name"] == "C2_kits_R30")
+    arr = synth.kits_like(tumor_mm=30.0)
+    d = torch.from_numpy(arr).cuda()
+    full = sc.calculate_coefficients_device(d, case["spacing"])
+    assert_matches(full, case["features"], case["triangle_count"], case["active_cubes"], "dev")
+    sq = torch.zeros(4, dtype=torch.float64, device="cuda")
+    best = torch.zeros(4, dtype=torch.float64, device="cuda")
+    for shard in range(3):
+        part = sc.calculate_coefficients_shard(d, case["spacing"], shard, 3, sq)
+        assert part.vertex_count == full.vertex_count
+        torch.maximum(best, sq, out=best)
+    got = [math.sqrt(v) for v in best.cpu().tolist()]
+    assert got == [full.max_3d_diameter, full.max_2d_diameter_xy, full.max_2d_diameter_xz,
+                   full.max_2d_diameter_yz]
+
+
+def test_batch_entry(sc, golden, golden_arrays, cuda_device):
+    cases = golden["cases"][:12]
+    outs = sc.calculate_coefficients_batch([golden_arrays[c["mask_key"]] for c in cases],
+                                           [c["spacing"] for c in cases], device=cuda_device)
+    for c, got in zip(cases, outs):
+        assert_matches(got, c["features"], c["triangle_count"], c["active_cubes"], c["name"])
+
+
+def test_repeat_calls_deterministic(sc, cuda_device):
+    from paper_2510_02894_b200 import synth
+
+    arr = synth.thin_slab()
+    a = sc.calculate_coefficients(arr, (0.5, 0.5, 5.0))
+    b = sc.calculate_coefficients(arr, (0.5, 0.5, 5.0))
+    assert a.to_dict() == b.to_dict()
+    assert (a.triangle_count, a.active_cubes) == (b.triangle_count, b.active_cubes)
