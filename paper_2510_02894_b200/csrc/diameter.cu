@@ -6,17 +6,17 @@
 // and x (YZ) bit for bit (features.py:145-147).
 //
 //  * diam3d_pass1<R>  -- the O(V^2) hot loop.  Triangular grid of square tile
-//    pairs (I <= J); the J tile is staged in shared memory as duplicated
-//    (x,x,y,y),(z,z) so every pair-of-pairs is three FADD2 + FMUL2 + two FFMA2
-//    on the packed fp32 pipe plus one 3-input FMNMX3.  Coordinates are fp32 in
-//    a bbox-centred frame.  Each tile pair's maximum is kept (item_max) and the
-//    global maximum is an integer atomicMax on the fp32 bit pattern.
-//  * diam3d_refine    -- exactness: every tile pair whose pass-1 maximum lies
-//    within kRefineRel of the global pass-1 maximum is re-evaluated in fp64
-//    with the reference's own arithmetic on the reference's own coordinates,
-//    so the final 3-D diameter is the reference's value bit for bit.  Tile
-//    pairs below the threshold provably cannot hold the maximum (the pass-1
-//    error is < 17 * 2^-24 relative).
+//    pairs (I <= J); the J tile is staged in shared memory as (x, y, z, |p|^2)
+//    and each thread register-blocks R i vertices, so a pair costs three FFMA
+//    (dot form) plus half an FMNMX3 on fp32 CUDA cores.  Coordinates are fp32
+//    in a bbox-centred frame.  One maximum per (tile pair, warp) is kept and
+//    the global maximum is an integer atomicMax on the fp32 bit pattern.
+//  * diam3d_select / diam3d_refine -- exactness: every (tile pair, warp)
+//    whose pass-1 maximum lies within kRefineRel of the global pass-1 maximum
+//    is re-evaluated in fp64 with the reference's own arithmetic on the
+//    reference's own coordinates, so the final 3-D diameter is the
+//    reference's value bit for bit.  Units below the threshold provably cannot
+//    hold the maximum (pass-1 error < ~1e-6 of D^2).
 //  * plane_*          -- keyed planar pass: counting-sort vertices by the
 //    doubled lattice key of z / y / x (bit-equal fp64 coordinate <=> equal
 //    key), then an fp64 reference-arithmetic pair max inside every plane.
@@ -53,117 +53,136 @@ __device__ __forceinline__ float3 frame_coord(int4 k, const Frame& f) {
                      (float)(k.z - f.cz2) * f.hz);
 }
 
+constexpr int kWarps = kDiamThreads / 32;
+
+// Pass 1: max over the tile pair of the squared distance in "dot" form,
+// |pj|^2 - 2 pi.pj (+ |pi|^2 once per i), i.e. three FFMA per pair plus half a
+// 3-input FMNMX3 -- issue-bound at ~3.5 instructions per pair.  The form
+// cancels for near pairs but not at the maximum: in the bbox-centred frame
+// |p| <= D/2*sqrt(3) so the absolute error is < ~12 * 2^-24 * D^2,
+// far inside the kRefineRel margin that decides which warps are re-checked
+// exactly.  One maximum per (tile pair, warp) is kept for that selection.
 template <int R>
 __global__ void __launch_bounds__(kDiamThreads) diam3d_pass1(const int4* __restrict__ keys,
                                                              long long n, int T, long long item0,
                                                              long long n_items, Frame f,
-                                                             float* __restrict__ item_max,
+                                                             float* __restrict__ warp_max,
                                                              Stats* __restrict__ st) {
   constexpr int TS = kDiamThreads * R;
-  extern __shared__ float4 smem4[];
-  float4* sA = smem4;                                    // (x, x, y, y)
-  float2* sB = reinterpret_cast<float2*>(smem4 + TS);    // (z, z)
+  extern __shared__ float4 sj[];  // (x, y, z, |p|^2) of the J tile
   const long long item = item0 + blockIdx.x;
   if (item >= item0 + n_items) return;
   int I, J;
   tile_pair(item, T, I, J);
-
-  // Stage the J tile (indices past n repeat the last vertex: harmless for a max).
   for (int t = threadIdx.x; t < TS; t += kDiamThreads) {
     long long j = (long long)J * TS + t;
-    if (j >= n) j = n - 1;
+    if (j >= n) j = n - 1;  // repeats of a real vertex are harmless for a max
     float3 c = frame_coord(keys[j], f);
-    sA[t] = make_float4(c.x, c.x, c.y, c.y);
-    sB[t] = make_float2(c.z, c.z);
+    sj[t] = make_float4(c.x, c.y, c.z, fmaf(c.x, c.x, fmaf(c.y, c.y, c.z * c.z)));
   }
-  // Register-block R i vertices as R/2 packed pairs, negated for FADD2.
-  float2 nx2[R / 2], ny2[R / 2], nz2[R / 2];
+  float a[R], b[R], c[R], m[R], ni[R];
 #pragma unroll
-  for (int p = 0; p < R / 2; p++) {
-    long long i0 = (long long)I * TS + (2 * p) * kDiamThreads + threadIdx.x;
-    long long i1 = i0 + kDiamThreads;
-    float3 a = frame_coord(keys[i0 < n ? i0 : n - 1], f);
-    float3 b = frame_coord(keys[i1 < n ? i1 : n - 1], f);
-    nx2[p] = make_float2(-a.x, -b.x);
-    ny2[p] = make_float2(-a.y, -b.y);
-    nz2[p] = make_float2(-a.z, -b.z);
+  for (int r = 0; r < R; r++) {
+    long long i = (long long)I * TS + r * kDiamThreads + threadIdx.x;
+    float3 p = frame_coord(keys[i < n ? i : n - 1], f);
+    a[r] = -2.f * p.x;
+    b[r] = -2.f * p.y;
+    c[r] = -2.f * p.z;
+    ni[r] = fmaf(p.x, p.x, fmaf(p.y, p.y, p.z * p.z));
+    m[r] = -3.0e38f;
   }
   __syncthreads();
-
-  float m0 = 0.f, m1 = 0.f;
 #pragma unroll 2
-  for (int j = 0; j < TS; j++) {
-    const float4 a = sA[j];
-    const float2 zz = sB[j];
-    const float2 xx = make_float2(a.x, a.y), yy = make_float2(a.z, a.w);
+  for (int j = 0; j < TS; j += 2) {
+    const float4 q0 = sj[j], q1 = sj[j + 1];
 #pragma unroll
-    for (int p = 0; p < R / 2; p++) {
-      float2 dx = __fadd2_rn(xx, nx2[p]);
-      float2 dy = __fadd2_rn(yy, ny2[p]);
-      float2 dz = __fadd2_rn(zz, nz2[p]);
-      float2 d = __fmul2_rn(dx, dx);
-      d = __ffma2_rn(dy, dy, d);
-      d = __ffma2_rn(dz, dz, d);
-      if (p & 1) m1 = fmax3f(m1, d.x, d.y);
-      else m0 = fmax3f(m0, d.x, d.y);
+    for (int r = 0; r < R; r++) {
+      float t0 = fmaf(q0.x, a[r], q0.w);
+      float t1 = fmaf(q1.x, a[r], q1.w);
+      t0 = fmaf(q0.y, b[r], t0);
+      t1 = fmaf(q1.y, b[r], t1);
+      t0 = fmaf(q0.z, c[r], t0);
+      t1 = fmaf(q1.z, c[r], t1);
+      m[r] = fmax3f(m[r], t0, t1);
     }
   }
-  float m = fmaxf(m0, m1);
+  float best = 0.f;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  __shared__ float s_red[kDiamThreads / 32];
-  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < kDiamThreads / 32; w++) m = fmaxf(m, s_red[w]);
-    item_max[blockIdx.x] = m;
-    atomic_max_pos_f32(&st->d3_f32, m);
+  for (int r = 0; r < R; r++) best = fmaxf(best, m[r] + ni[r]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) {
+    warp_max[blockIdx.x * (long long)kWarps + (threadIdx.x >> 5)] = best;
+    atomic_max_pos_f32(&st->d3_f32, best);
   }
 }
 
-// Relative margin of the pass-1 re-check threshold.  The fp32 frame error is
-// bounded by 17*2^-24 ~ 1.0e-6 of D^2; tile pairs whose pass-1
-// maximum is below M*(1 - kRefineRel) cannot contain the exact maximum.
+// Relative margin of the re-check threshold.  Pass-1 error is below ~1e-6 of
+// D^2; a (tile pair, warp) whose pass-1 maximum is below
+// M*(1 - kRefineRel) provably cannot hold the exact maximum pair.
 constexpr float kRefineRel = 8e-6f;
 
+// Compact the (tile pair, warp) units that may hold the maximum.
+__global__ void diam3d_select(const float* __restrict__ warp_max, long long n_units,
+                              Stats* __restrict__ st, unsigned int* __restrict__ cand) {
+  const float tau = __uint_as_float(st->d3_f32) * (1.f - kRefineRel);
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < n_units;
+       base += (long long)gridDim.x * blockDim.x) {
+    const long long u = base + threadIdx.x;
+    const bool hit = u < n_units && warp_max[u] >= tau;
+    const unsigned int mask = __ballot_sync(0xffffffffu, hit);
+    if (!mask) continue;
+    unsigned long long pos = 0;
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) pos = atomicAdd(&st->n_cand, (unsigned long long)__popc(mask));
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (hit) cand[pos + __popc(mask & ((1u << lane) - 1))] = (unsigned int)u;
+  }
+}
+
+// Exact re-check: every selected warp's 32*R i-rows against its J tile, in
+// fp64 with the reference arithmetic on the reference coordinates.  Work unit
+// = (candidate, 256-wide j chunk); a persistent grid walks the units.
 template <int R>
 __global__ void __launch_bounds__(kDiamThreads) diam3d_refine(const int4* __restrict__ keys,
                                                               long long n, int T,
-                                                              long long item0, long long n_items,
-                                                              Frame f,
-                                                              const float* __restrict__ item_max,
+                                                              long long item0, Frame f,
+                                                              const unsigned int* __restrict__ cand,
                                                               Stats* __restrict__ st) {
   constexpr int TS = kDiamThreads * R;
-  const long long item = item0 + blockIdx.x;
-  if (item >= item0 + n_items) return;
-  const float tau = __uint_as_float(st->d3_f32) * (1.f - kRefineRel);
-  if (item_max[blockIdx.x] < tau) return;
-  int I, J;
-  tile_pair(item, T, I, J);
+  constexpr int CHUNKS = TS / kDiamThreads;
   __shared__ double sx[kDiamThreads], sy[kDiamThreads], sz[kDiamThreads];
+  const long long units = (long long)st->n_cand * CHUNKS;
   double best = 0.0;
-  for (int r = 0; r < R; r++) {
-    long long i = (long long)I * TS + r * kDiamThreads + threadIdx.x;
-    const bool iv = i < n;
-    int4 ki = keys[iv ? i : n - 1];
-    double xi = ref_coord(ki.x, f.sx), yi = ref_coord(ki.y, f.sy), zi = ref_coord(ki.z, f.sz);
-    for (int c = 0; c < TS; c += kDiamThreads) {
-      __syncthreads();
-      long long j = (long long)J * TS + c + threadIdx.x;
+  for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+    const unsigned int cu = cand[u / CHUNKS];
+    const int q = (int)(u % CHUNKS);
+    const long long item = item0 + cu / kWarps;
+    const int warp = cu % kWarps;
+    int I, J;
+    tile_pair(item, T, I, J);
+    __syncthreads();
+    {
+      long long j = (long long)J * TS + q * kDiamThreads + threadIdx.x;
       int4 kj = keys[j < n ? j : n - 1];
       sx[threadIdx.x] = ref_coord(kj.x, f.sx);
       sy[threadIdx.x] = ref_coord(kj.y, f.sy);
       sz[threadIdx.x] = ref_coord(kj.z, f.sz);
-      __syncthreads();
-      if (iv)
-        for (int t = 0; t < kDiamThreads; t++)
-          best = fmax(best, ref_sq_dist(xi, yi, zi, sx[t], sy[t], sz[t]));
+    }
+    __syncthreads();
+    const int r = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long i = (long long)I * TS + r * kDiamThreads + warp * 32 + lane;
+    if (r < R && i < n) {
+      int4 ki = keys[i];
+      const double xi = ref_coord(ki.x, f.sx), yi = ref_coord(ki.y, f.sy), zi = ref_coord(ki.z, f.sz);
+#pragma unroll 4
+      for (int t = 0; t < kDiamThreads; t++)
+        best = fmax(best, ref_sq_dist(xi, yi, zi, sx[t], sy[t], sz[t]));
     }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
-  if ((threadIdx.x & 31) == 0) atomic_max_pos_f64(&st->sq[0], best);
-  if (threadIdx.x == 0) atomicAdd(&st->n_refined, 1ull);
+  if ((threadIdx.x & 31) == 0 && best > 0.0) atomic_max_pos_f64(&st->sq[0], best);
 }
 
 // ---- planar pass -----------------------------------------------------------
@@ -175,15 +194,29 @@ __device__ __forceinline__ void plane_ids(int4 k, const PlaneSpace& ps, int out[
   out[2] = ps.cnt[0] + ps.cnt[1] + (k.x - ps.lo[2]);
 }
 
+// Warp-aggregated increment: lanes with equal `id` (vertices of one plane are
+// emitted together by the MC warps) share one global atomic.  Returns the
+// slot of this lane within its group's reservation.
+__device__ __forceinline__ unsigned int group_add(unsigned int* base, int id, bool ok) {
+  const int lane = threadIdx.x & 31;
+  const unsigned int peers = __match_any_sync(0xffffffffu, ok ? id : -1 - lane);
+  const int leader = __ffs(peers) - 1;
+  unsigned int pos = 0;
+  if (ok && lane == leader) pos = atomicAdd(base + id, (unsigned int)__popc(peers));
+  pos = __shfl_sync(0xffffffffu, pos, leader);
+  return pos + __popc(peers & ((1u << lane) - 1));
+}
+
 __global__ void plane_hist(const int4* __restrict__ keys, long long n, PlaneSpace ps,
                            unsigned int* __restrict__ counts) {
-  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += (long long)gridDim.x * blockDim.x) {
-    int id[3];
-    plane_ids(keys[v], ps, id);
-    atomicAdd(&counts[id[0]], 1u);
-    atomicAdd(&counts[id[1]], 1u);
-    atomicAdd(&counts[id[2]], 1u);
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < n;
+       base += (long long)gridDim.x * blockDim.x) {
+    const long long v = base + threadIdx.x;
+    const bool ok = v < n;
+    int id[3] = {0, 0, 0};
+    if (ok) plane_ids(keys[v], ps, id);
+#pragma unroll
+    for (int a = 0; a < 3; a++) group_add(counts, id[a], ok);
   }
 }
 
@@ -217,14 +250,24 @@ __global__ void __launch_bounds__(1024) plane_scan(const unsigned int* __restric
 
 __global__ void plane_scatter(const int4* __restrict__ keys, long long n, PlaneSpace ps,
                               unsigned int* __restrict__ cursor, int2* __restrict__ sorted) {
-  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += (long long)gridDim.x * blockDim.x) {
-    int4 k = keys[v];
-    int id[3];
-    plane_ids(k, ps, id);
-    sorted[atomicAdd(&cursor[id[0]], 1u)] = make_int2(k.x, k.y);  // XY: (X, Y)
-    sorted[atomicAdd(&cursor[id[1]], 1u)] = make_int2(k.x, k.z);  // XZ: (X, Z)
-    sorted[atomicAdd(&cursor[id[2]], 1u)] = make_int2(k.y, k.z);  // YZ: (Y, Z)
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < n;
+       base += (long long)gridDim.x * blockDim.x) {
+    const long long v = base + threadIdx.x;
+    const bool ok = v < n;
+    int4 k = make_int4(0, 0, 0, 0);
+    int id[3] = {0, 0, 0};
+    if (ok) {
+      k = keys[v];
+      plane_ids(k, ps, id);
+    }
+    const unsigned int p0 = group_add(cursor, id[0], ok);  // XY: (X, Y)
+    const unsigned int p1 = group_add(cursor, id[1], ok);  // XZ: (X, Z)
+    const unsigned int p2 = group_add(cursor, id[2], ok);  // YZ: (Y, Z)
+    if (ok) {
+      sorted[p0] = make_int2(k.x, k.y);
+      sorted[p1] = make_int2(k.x, k.z);
+      sorted[p2] = make_int2(k.y, k.z);
+    }
   }
 }
 
@@ -359,17 +402,14 @@ template __global__ void fp32_probe<2>(float*, int, float, float);
 template __global__ void fp32_probe<3>(float*, int, float, float);
 
 // Explicit instantiations used by the engine.
-template __global__ void diam3d_pass1<2>(const int4*, long long, int, long long, long long, Frame,
-                                         float*, Stats*);
-template __global__ void diam3d_pass1<4>(const int4*, long long, int, long long, long long, Frame,
-                                         float*, Stats*);
-template __global__ void diam3d_pass1<8>(const int4*, long long, int, long long, long long, Frame,
-                                         float*, Stats*);
-template __global__ void diam3d_refine<2>(const int4*, long long, int, long long, long long, Frame,
-                                          const float*, Stats*);
-template __global__ void diam3d_refine<4>(const int4*, long long, int, long long, long long, Frame,
-                                          const float*, Stats*);
-template __global__ void diam3d_refine<8>(const int4*, long long, int, long long, long long, Frame,
-                                          const float*, Stats*);
+#define SC_INST(RR)                                                                            \
+  template __global__ void diam3d_pass1<RR>(const int4*, long long, int, long long, long long,   \
+                                            Frame, float*, Stats*);                              \
+  template __global__ void diam3d_refine<RR>(const int4*, long long, int, long long, Frame,      \
+                                             const unsigned int*, Stats*);
+SC_INST(2)
+SC_INST(4)
+SC_INST(8)
+#undef SC_INST
 
 }  // namespace sc

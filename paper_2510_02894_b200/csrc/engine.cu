@@ -36,9 +36,10 @@ __global__ void mc_cells(const uint32_t*, int, int, int, int, const CaseTables*,
 template <int R>
 __global__ void diam3d_pass1(const int4*, long long, int, long long, long long, Frame, float*,
                              Stats*);
+__global__ void diam3d_select(const float*, long long, Stats*, unsigned int*);
 template <int R>
-__global__ void diam3d_refine(const int4*, long long, int, long long, long long, Frame,
-                              const float*, Stats*);
+__global__ void diam3d_refine(const int4*, long long, int, long long, Frame, const unsigned int*,
+                              Stats*);
 __global__ void plane_hist(const int4*, long long, PlaneSpace, unsigned int*);
 __global__ void plane_scan(const unsigned int*, int, unsigned int*, unsigned int*);
 __global__ void plane_scatter(const int4*, long long, PlaneSpace, unsigned int*, int2*);
@@ -166,7 +167,8 @@ struct Ctx {
   CaseTables* d_tabs = nullptr;
   DevBuf<uint32_t> bits;
   DevBuf<int4> keys;
-  DevBuf<float> item_max;
+  DevBuf<float> warp_max;
+  DevBuf<unsigned int> cand;
   DevBuf<unsigned int> plane_counts, plane_start, plane_cursor;
   DevBuf<int2> plane_sorted;
   DevBuf<uint8_t> mask_stage;
@@ -205,9 +207,9 @@ int get_ctx(int device, Ctx** out) {
     CK(cudaMallocHost(&c->h_stats, sizeof(Stats)));
     CK(cudaMalloc(&c->d_tabs, sizeof(CaseTables)));
     CK(cudaMemcpy(c->d_tabs, &case_geom().tabs, sizeof(CaseTables), cudaMemcpyHostToDevice));
-    CK(cudaFuncSetAttribute(diam3d_pass1<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 512 * 24));
-    CK(cudaFuncSetAttribute(diam3d_pass1<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 24));
-    CK(cudaFuncSetAttribute(diam3d_pass1<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2048 * 24));
+    CK(cudaFuncSetAttribute(diam3d_pass1<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 512 * 16));
+    CK(cudaFuncSetAttribute(diam3d_pass1<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
+    CK(cudaFuncSetAttribute(diam3d_pass1<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2048 * 16));
     g_ctx[device] = std::move(c);
   }
   *out = g_ctx[device].get();
@@ -253,10 +255,16 @@ int run_mc(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, cu
     CKL(1);
     if (nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0) {
       const long long n_chunks = nx * ny * nz / 16;
+      const int C16 = (int)(nx / 16);
+      // grid * 1024 must be a multiple of C16 (whole rows per grid stride).
+      int unit = C16;
+      for (int g = 1024; g % 2 == 0 && unit % 2 == 0;) { g /= 2; unit /= 2; }
       long long want = (n_chunks + 256 * 4 - 1) / (256 * 4);
-      int grid = (int)std::min<long long>(want, (long long)c->sms * 8);
-      pack_bits_v16<4><<<grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(d_mask), c->bits.p,
-                                            n_chunks, W, (int)ny, c->d_stats);
+      long long grid = std::min<long long>(want, (long long)c->sms * 8);
+      grid = std::max<long long>(unit, (grid + unit - 1) / unit * unit);
+      pack_bits_v16<4><<<(unsigned)grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(d_mask),
+                                                      c->bits.p, n_chunks, C16, (int)ny,
+                                                      c->d_stats);
     } else {
       long long want = (n_words + 255) / 256;
       int grid = (int)std::min<long long>(want, (long long)c->sms * 8);
@@ -307,15 +315,20 @@ int run_diameters(Ctx* c, const double sp[3], cudaStream_t s, int shard, int nsh
   const long long n_loc = i1 - i0;
   CK(cudaEventRecord(c->kev[3], s));
   if (n_loc > 0) {
-    CK(c->item_max.ensure((size_t)n_loc));
-    const size_t smem = (size_t)TS * 24;
+    const long long n_units = n_loc * 8;  // (tile pair, warp)
+    CK(c->warp_max.ensure((size_t)n_units));
+    CK(c->cand.ensure((size_t)n_units));
+    const size_t smem = (size_t)TS * 16;
+    const int sgrid = (int)std::min<long long>((n_units + 255) / 256, (long long)c->sms * 8);
 #define LAUNCH_3D(RR)                                                                          \
   diam3d_pass1<RR><<<(unsigned)n_loc, 256, smem, s>>>(c->keys.p, V, (int)T, i0, n_loc, f,      \
-                                                      c->item_max.p, c->d_stats);              \
+                                                      c->warp_max.p, c->d_stats);              \
   CKL(1);                                                                                      \
   CK(cudaEventRecord(c->kev[4], s));                                                           \
-  diam3d_refine<RR><<<(unsigned)n_loc, 256, 0, s>>>(c->keys.p, V, (int)T, i0, n_loc, f,        \
-                                                    c->item_max.p, c->d_stats);                \
+  diam3d_select<<<sgrid, 256, 0, s>>>(c->warp_max.p, n_units, c->d_stats, c->cand.p);          \
+  CKL(1);                                                                                      \
+  diam3d_refine<RR><<<c->sms * 2, 256, 0, s>>>(c->keys.p, V, (int)T, i0, f, c->cand.p,         \
+                                               c->d_stats);                                    \
   CKL(1);
     if (R == 8) { LAUNCH_3D(8) } else if (R == 4) { LAUNCH_3D(4) } else { LAUNCH_3D(2) }
 #undef LAUNCH_3D

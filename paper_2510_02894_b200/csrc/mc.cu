@@ -36,12 +36,13 @@ __global__ void init_stats(Stats* st) {
   if (t >= 3 && t < 6) st->bbox[t] = -1;
 }
 
-// 4 mask bytes -> 4 occupancy bits (byte i nonzero -> bit i).  The multiply
-// places byte i's flag at bit 21+i with no carries (all 16 partial products
-// land on distinct bit positions).
+// 4 mask bytes -> 4 occupancy bits (byte i nonzero -> bit i).  Bit 7 of each
+// byte of t is "byte nonzero" (the classic SWAR zero-byte test); the multiply
+// then moves the flag of byte i (bit 7+8i) to bit 28+i with no carries (all 16
+// partial products land on distinct bit positions).  3 ALU ops + 1 IMAD.
 __device__ __forceinline__ uint32_t nib4(uint32_t v) {
-  uint32_t m = __vcmpne4(v, 0u) & 0x01010101u;
-  return ((m * 0x00204081u) >> 21) & 0xFu;
+  const uint32_t t = (((v & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | v) & 0x80808080u;
+  return (t * 0x00204081u) >> 28;
 }
 
 struct BoxAcc {
@@ -72,32 +73,54 @@ struct BoxAcc {
 // Fast path: nx % 32 == 0 and a 16-byte aligned mask.  One 16-byte chunk per
 // thread per step (a warp reads 512 contiguous bytes per load instruction);
 // lane pairs merge their 16-bit halves into one 32-bit word.  U chunks are in
-// flight per thread for memory-level parallelism.
+// flight per thread for memory-level parallelism.  The host sizes the grid so
+// the grid stride is a whole number of rows: each thread then keeps a fixed
+// x column per k and advances (y, z) incrementally -- no divisions in the loop.
 template <int U>
 __global__ void __launch_bounds__(256) pack_bits_v16(const uint4* __restrict__ mask,
                                                      uint32_t* __restrict__ bits,
-                                                     long long n_chunks, int W, int ny,
+                                                     long long n_chunks, int C16, int ny,
                                                      Stats* __restrict__ st) {
   BoxAcc box;
   const long long step = (long long)gridDim.x * blockDim.x * U;
+  const long long rowstep = step / C16;
+  const int dy = (int)(rowstep % ny), dz = (int)(rowstep / ny);
+  int col[U], y[U], z[U];
+#pragma unroll
+  for (int k = 0; k < U; k++) {
+    const long long g0 = (long long)blockIdx.x * blockDim.x * U + (long long)k * blockDim.x + threadIdx.x;
+    const long long row0 = g0 / C16;
+    col[k] = (int)(g0 - row0 * C16);
+    y[k] = (int)(row0 % ny);
+    z[k] = (int)(row0 / ny);
+  }
   for (long long base = (long long)blockIdx.x * blockDim.x * U; base < n_chunks; base += step) {
     uint4 v[U];
 #pragma unroll
     for (int k = 0; k < U; k++) {
-      long long g = base + (long long)k * blockDim.x + threadIdx.x;
+      const long long g = base + (long long)k * blockDim.x + threadIdx.x;
       v[k] = g < n_chunks ? __ldcs(mask + g) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int k = 0; k < U; k++) {
-      long long g = base + (long long)k * blockDim.x + threadIdx.x;
-      uint32_t b16 = nib4(v[k].x) | (nib4(v[k].y) << 4) | (nib4(v[k].z) << 8) | (nib4(v[k].w) << 12);
-      uint32_t hi = __shfl_down_sync(kFull, b16, 1);
+      const long long g = base + (long long)k * blockDim.x + threadIdx.x;
+      const uint32_t b16 = nib4(v[k].x) | (nib4(v[k].y) << 4) | (nib4(v[k].z) << 8) |
+                           (nib4(v[k].w) << 12);
+      const uint32_t hi = __shfl_down_sync(kFull, b16, 1);
       if (!(threadIdx.x & 1) && g < n_chunks) {
-        uint32_t word = b16 | (hi << 16);
-        long long wi = g >> 1;
-        bits[wi] = word;
-        if (word) box.add(word, wi, W, ny);
+        const uint32_t word = b16 | (hi << 16);
+        bits[g >> 1] = word;
+        if (word) {
+          const int xb = 16 * col[k];
+          box.x0 = min(box.x0, xb + __ffs(word) - 1);
+          box.x1 = max(box.x1, xb + 31 - __clz(word));
+          box.y0 = min(box.y0, y[k]); box.y1 = max(box.y1, y[k]);
+          box.z0 = min(box.z0, z[k]); box.z1 = max(box.z1, z[k]);
+        }
       }
+      y[k] += dy;
+      z[k] += dz;
+      if (y[k] >= ny) { y[k] -= ny; z[k]++; }
     }
   }
   box.flush(st);
@@ -139,12 +162,24 @@ __device__ __forceinline__ unsigned long long window(const uint32_t* __restrict_
   return (cur << 1) | (prev >> 31);
 }
 
-constexpr int kZChunk = 8;
+constexpr int kZChunk = 4;
+
+__device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits, int q, int v, int w,
+                                          int W, int ny, int nz, bool on, uint32_t& cur,
+                                          uint32_t& prev) {
+  cur = prev = 0u;
+  if (on && v >= 0 && v < ny && w >= 0 && w < nz) {
+    const uint32_t* row = bits + ((long long)w * ny + v) * W;
+    if (q < W) cur = row[q];
+    if (q > 0) prev = row[q - 1];
+  }
+}
 
 // One thread = one (word column q, row v) and kZChunk consecutive z steps.
 // Cell (u, v, w) has lower corner at unpadded voxel (u, v, w), u,v,w >= -1
 // (reference padded cell index minus 1).  The thread owns cells and lattice
-// points u = 32q - 1 + i, i in [0, 31].
+// points u = 32q - 1 + i, i in [0, 31].  All 2*(kZChunk+1) row words are
+// loaded up front (L2-resident bit volume; latency, not bandwidth, bound).
 __global__ void __launch_bounds__(256) mc_cells(const uint32_t* __restrict__ bits, int nx, int ny,
                                                 int nz, int W, const CaseTables* __restrict__ tabs,
                                                 Stats* __restrict__ st, int4* __restrict__ vkeys,
@@ -179,21 +214,28 @@ __global__ void __launch_bounds__(256) mc_cells(const uint32_t* __restrict__ bit
         v = vlo + (int)(r % nv);
         w0 = wlo + (int)(r / nv) * kZChunk;
       }
-      unsigned long long A = valid ? window(bits, q, v, w0, W, ny, nz) : 0ull;
-      unsigned long long B = valid ? window(bits, q, v + 1, w0, W, ny, nz) : 0ull;
+      uint32_t c0[kZChunk + 1], p0[kZChunk + 1], c1[kZChunk + 1], p1[kZChunk + 1];
+#pragma unroll
+      for (int s = 0; s <= kZChunk; s++) {
+        const bool on = valid && w0 + s <= whi + 1;
+        row_words(bits, q, v, w0 + s, W, ny, nz, on, c0[s], p0[s]);
+        row_words(bits, q, v + 1, w0 + s, W, ny, nz, on, c1[s], p1[s]);
+      }
       const int xbase = 32 * q - 1;
+#pragma unroll
       for (int s = 0; s < kZChunk; s++) {
         const int w = w0 + s;
         const bool on = valid && w <= whi;
-        unsigned long long C = 0, D = 0;
+        const unsigned long long A = ((unsigned long long)c0[s] << 1) | (p0[s] >> 31);
+        const unsigned long long B = ((unsigned long long)c1[s] << 1) | (p1[s] >> 31);
+        const unsigned long long C = ((unsigned long long)c0[s + 1] << 1) | (p0[s + 1] >> 31);
+        const unsigned long long D = ((unsigned long long)c1[s + 1] << 1) | (p1[s + 1] >> 31);
         uint32_t ex = 0, ey = 0, ez = 0, act = 0;
         if (on) {
-          C = window(bits, q, v, w + 1, W, ny, nz);
-          D = window(bits, q, v + 1, w + 1, W, ny, nz);
           ex = (uint32_t)(A ^ (A >> 1));
           ey = (uint32_t)(A ^ B);
           ez = (uint32_t)(A ^ C);
-          unsigned long long all = A & B & C & D, any = A | B | C | D;
+          const unsigned long long all = A & B & C & D, any = A | B | C | D;
           act = (uint32_t)(~(all & (all >> 1)) & (any | (any >> 1)));
         }
         // Active cells: case bit c set when corner c is background
@@ -242,8 +284,6 @@ __global__ void __launch_bounds__(256) mc_cells(const uint32_t* __restrict__ bit
             o++;
           }
         }
-        A = C;
-        B = D;
       }
     }
   }

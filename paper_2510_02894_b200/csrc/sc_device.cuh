@@ -18,7 +18,7 @@ struct Stats {
   unsigned int d3_f32;                 // fp32 bits of the pass-1 max squared 3-D distance
   unsigned int pad0;
   unsigned long long sq[4];            // fp64 bits: exact squared maxima (3d, xy, xz, yz)
-  unsigned long long n_refined;        // tile pairs re-evaluated in fp64 (diagnostic)
+  unsigned long long n_cand;           // (tile pair, warp) units re-checked in fp64
 };
 
 // Per-case integer tables for the exact volume path: for case k,

@@ -1,0 +1,115 @@
+"""Multi-GPU partitioning of the shape-coefficient path.
+
+Two shapes of work shard naturally; nothing else is split:
+
+* ROI batches (C4): independent masks.  `assign_rois` places them on ranks by
+  longest-processing-time on an estimated cost; each rank runs its ROIs with
+  no data-path collective; the 9-scalar records are gathered once at the end.
+* One very large mesh (C3): every rank runs the (cheap, ~50 us) marching-cubes
+  stage on the full mask, then only its slice of the triangular pair-tile grid
+  and of the planar groups (`sc_calculate_coefficients_shard`).  The four
+  partial squared maxima are combined with one all_reduce(MAX) over NCCL /
+  NVLink -- the only exchange the path has.
+
+One process per GPU; torch.distributed is plumbing (process group, NCCL
+all-reduce), the compute is the C ABI.  The combine logic takes an injectable
+`compute` callable so it is tested on CPU with the gloo backend.
+"""
+
+from __future__ import annotations
+
+import heapq
+import math
+from typing import Callable, List, Optional, Sequence, Tuple
+
+
+def shard_range(n_items: int, shard: int, nshards: int) -> Tuple[int, int]:
+    """[begin, end) of shard `shard` -- the exact integer split the C engine
+    uses for tile pairs and planes (engine.cu run_diameters)."""
+    return n_items * shard // nshards, n_items * (shard + 1) // nshards
+
+
+def roi_cost(occupied_voxels: int, voxels: int) -> float:
+    """Cost model for LPT: a streaming term for the mask plus the O(V^2)
+    diameter term with V ~ surface ~ occupied^(2/3)."""
+    v = max(1.0, float(occupied_voxels)) ** (2.0 / 3.0) * 6.0
+    return voxels / 6.45e12 * 2 + v * v / 2 / 3e12
+
+
+def assign_rois(costs: Sequence[float], nranks: int) -> List[List[int]]:
+    """Longest-processing-time-first assignment; returns ROI indices per rank
+    (each list in ascending index order)."""
+    heap = [(0.0, r) for r in range(nranks)]
+    heapq.heapify(heap)
+    out: List[List[int]] = [[] for _ in range(nranks)]
+    for i in sorted(range(len(costs)), key=lambda i: (-costs[i], i)):
+        load, r = heapq.heappop(heap)
+        out[r].append(i)
+        heapq.heappush(heap, (load + costs[i], r))
+    return [sorted(x) for x in out]
+
+
+def batch_coefficients(masks: Sequence, spacings: Sequence[Sequence[float]],
+                       costs: Optional[Sequence[float]] = None, group=None,
+                       compute: Optional[Callable] = None):
+    """C4 on the calling rank's GPU: compute the ROIs LPT-assigned to this rank
+    and all-gather the records (a list in input order, on every rank)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if costs is None:
+        costs = [float(getattr(m, "size", 1)) for m in masks]
+    mine = assign_rois(costs, world)[rank]
+    if compute is None:
+        from .features import calculate_coefficients_batch
+
+        def compute(ms, sps):
+            return [c.to_dict() | {"triangle_count": c.triangle_count,
+                                   "active_cubes": c.active_cubes}
+                    for c in calculate_coefficients_batch(ms, sps)]
+    local = compute([masks[i] for i in mine], [spacings[i] for i in mine]) if mine else []
+    pairs = list(zip(mine, local))
+    if world == 1:
+        gathered = [pairs]
+    else:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, pairs, group=group)
+    out = [None] * len(masks)
+    for part in gathered:
+        for i, rec in part:
+            out[i] = rec
+    return out
+
+
+def sharded_coefficients(mask, spacing: Sequence[float], group=None,
+                         compute: Optional[Callable] = None):
+    """One large ROI split across the ranks of `group`: each rank evaluates its
+    shard of the pair grid, then one all_reduce(MAX) of the 4 squared maxima.
+
+    compute(shard, nshards, sq4) -> record dict; must write the shard's squared
+    maxima into the 4-element float64 tensor sq4 (default: the C ABI)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if compute is None:
+        from .features import calculate_coefficients_shard
+
+        def compute(shard, nshards, sq4):
+            c = calculate_coefficients_shard(mask, spacing, shard, nshards, sq4)
+            return c.to_dict() | {"triangle_count": c.triangle_count,
+                                  "active_cubes": c.active_cubes}
+        device = mask.device
+    else:
+        device = torch.device("cpu")
+    sq4 = torch.zeros(4, dtype=torch.float64, device=device)
+    rec = compute(rank, world, sq4)
+    if world > 1:
+        dist.all_reduce(sq4, op=dist.ReduceOp.MAX, group=group)
+    d = [math.sqrt(v) for v in sq4.cpu().tolist()]
+    rec = dict(rec)
+    rec.update({"Maximum3DDiameter": d[0], "Maximum2DDiameterXY": d[1],
+                "Maximum2DDiameterXZ": d[2], "Maximum2DDiameterYZ": d[3]})
+    return rec
