@@ -5,28 +5,43 @@
 // of the squared distance, and the maxima over pairs sharing z (XY), y (XZ)
 // and x (YZ) bit for bit (features.py:145-147).
 //
-//  * diam3d_pass1<R>  -- the O(V^2) hot loop.  Triangular grid of square tile
-//    pairs (I <= J); the J tile is staged in shared memory as (x, y, z, |p|^2)
-//    and each thread register-blocks R i vertices, so a pair costs three FFMA
-//    (dot form) plus half an FMNMX3 on fp32 CUDA cores.  Coordinates are fp32
-//    in a bbox-centred frame.  One maximum per (tile pair, warp) is kept and
-//    the global maximum is an integer atomicMax on the fp32 bit pattern.
-//  * diam3d_select / diam3d_refine -- exactness: every (tile pair, warp)
-//    whose pass-1 maximum lies within kRefineRel of the global pass-1 maximum
-//    is re-evaluated in fp64 with the reference's own arithmetic on the
-//    reference's own coordinates, so the final 3-D diameter is the
-//    reference's value bit for bit.  Units below the threshold provably cannot
-//    hold the maximum (pass-1 error < ~1e-6 of D^2).
-//  * plane_*          -- keyed planar pass: counting-sort vertices by the
+// Every kernel here is device-driven: the vertex count, bounding box and plane
+// layout are read from the Stats the marching-cubes stage wrote, so a whole
+// ROI is enqueued without a host round trip (and can be graph-captured).
+//
+//  * diam3d_pass1   -- the O(V^2) hot loop.  Triangular grid of 2048x2048 tile
+//    pairs, each split into 8 work units of 2048 i x 256 j; a persistent grid
+//    walks the units.  The j chunk is staged in shared memory as
+//    (x, y, z, |p|^2); each thread register-blocks 8 i vertices, so a pair
+//    costs three FFMA (dot form |pj|^2 - 2 pi.pj) plus half an FMNMX3 on the
+//    fp32 CUDA cores.  fp32 coordinates live in a bbox-centred frame.  One
+//    maximum per (tile pair, warp) is kept for the exact re-check.
+//  * diam3d_select / diam3d_refine -- exactness: every (tile pair, warp) whose
+//    pass-1 maximum lies within kRefineRel of the pass-1 maximum is
+//    re-evaluated in fp64 with the reference's own arithmetic on the
+//    reference's own coordinates, so the 3-D diameter is the reference's value
+//    bit for bit.  Units below the threshold provably cannot hold the maximum
+//    (pass-1 error < ~1e-6 of D^2).
+//  * plane_*        -- keyed planar pass: counting sort of the vertices by the
 //    doubled lattice key of z / y / x (bit-equal fp64 coordinate <=> equal
-//    key), then an fp64 reference-arithmetic pair max inside every plane.
-//  * cloud_diameters  -- the generic diameters(xs, ys, zs) API on arbitrary
+//    key), then the same fp32-dot pass + fp64 re-check inside every plane.
+//  * cloud_diameters -- the generic diameters(xs, ys, zs) API on arbitrary
 //    fp64 points with the reference's in-loop bit-equality tests.
 #include "sc_device.cuh"
 
 namespace sc {
 
 constexpr int kDiamThreads = 256;
+constexpr int kWarps = kDiamThreads / 32;
+constexpr int kR = 8;                          // i vertices per thread
+constexpr int kTile = kDiamThreads * kR;       // 2048: tile edge
+constexpr int kChunk = kDiamThreads;           // 256: j chunk per work unit
+constexpr int kChunks = kTile / kChunk;        // 8 units per tile pair
+
+// Relative margin of the re-check threshold.  Pass-1 error is below ~1e-6 of
+// D^2; a unit whose pass-1 maximum is below M*(1 - kRefineRel)
+// provably cannot hold the exact maximum pair.
+constexpr float kRefineRel = 8e-6f;
 
 __device__ __forceinline__ float fmax3f(float a, float b, float c) {
   float r;
@@ -35,17 +50,28 @@ __device__ __forceinline__ float fmax3f(float a, float b, float c) {
 }
 
 // Upper-triangle tile-pair index -> (I, J), I <= J, row-major over I.
-__device__ __forceinline__ void tile_pair(long long t, int T, int& I, int& J) {
-  // off(I) = I*T - I*(I-1)/2 ; solve off(I) <= t < off(I+1)
+__device__ __forceinline__ void tile_pair(long long t, long long T, int& I, int& J) {
   double b = 2.0 * T + 1.0;
-  int i = (int)((b - sqrt(b * b - 8.0 * (double)t)) * 0.5);
+  long long i = (long long)((b - sqrt(b * b - 8.0 * (double)t)) * 0.5);
   if (i < 0) i = 0;
   if (i > T - 1) i = T - 1;
   auto off = [T](long long r) { return r * T - r * (r - 1) / 2; };
   while (i > 0 && off(i) > t) i--;
   while (i < T - 1 && off(i + 1) <= t) i++;
-  I = i;
+  I = (int)i;
   J = (int)(i + (t - off(i)));
+}
+
+__device__ __forceinline__ long long n_vertices(const Stats* st, long long cap) {
+  long long n = (long long)st->n_vert;
+  return n < cap ? n : cap;
+}
+
+// Bbox-centred fp32 frame: centre (doubled units) from the MC bbox.
+__device__ __forceinline__ void frame_centre(const Stats* st, Frame& f) {
+  f.cx2 = st->bbox[0] + st->bbox[3];
+  f.cy2 = st->bbox[1] + st->bbox[4];
+  f.cz2 = st->bbox[2] + st->bbox[5];
 }
 
 __device__ __forceinline__ float3 frame_coord(int4 k, const Frame& f) {
@@ -53,131 +79,144 @@ __device__ __forceinline__ float3 frame_coord(int4 k, const Frame& f) {
                      (float)(k.z - f.cz2) * f.hz);
 }
 
-constexpr int kWarps = kDiamThreads / 32;
-
-// Pass 1: max over the tile pair of the squared distance in "dot" form,
-// |pj|^2 - 2 pi.pj (+ |pi|^2 once per i), i.e. three FFMA per pair plus half a
-// 3-input FMNMX3 -- issue-bound at ~3.5 instructions per pair.  The form
-// cancels for near pairs but not at the maximum: in the bbox-centred frame
-// |p| <= D/2*sqrt(3) so the absolute error is < ~12 * 2^-24 * D^2,
-// far inside the kRefineRel margin that decides which warps are re-checked
-// exactly.  One maximum per (tile pair, warp) is kept for that selection.
-template <int R>
-__global__ void __launch_bounds__(kDiamThreads) diam3d_pass1(const int4* __restrict__ keys,
-                                                             long long n, int T, long long item0,
-                                                             long long n_items, Frame f,
-                                                             float* __restrict__ warp_max,
-                                                             Stats* __restrict__ st) {
-  constexpr int TS = kDiamThreads * R;
-  extern __shared__ float4 sj[];  // (x, y, z, |p|^2) of the J tile
-  const long long item = item0 + blockIdx.x;
-  if (item >= item0 + n_items) return;
-  int I, J;
-  tile_pair(item, T, I, J);
-  for (int t = threadIdx.x; t < TS; t += kDiamThreads) {
-    long long j = (long long)J * TS + t;
-    if (j >= n) j = n - 1;  // repeats of a real vertex are harmless for a max
-    float3 c = frame_coord(keys[j], f);
-    sj[t] = make_float4(c.x, c.y, c.z, fmaf(c.x, c.x, fmaf(c.y, c.y, c.z * c.z)));
-  }
-  float a[R], b[R], c[R], m[R], ni[R];
-#pragma unroll
-  for (int r = 0; r < R; r++) {
-    long long i = (long long)I * TS + r * kDiamThreads + threadIdx.x;
-    float3 p = frame_coord(keys[i < n ? i : n - 1], f);
-    a[r] = -2.f * p.x;
-    b[r] = -2.f * p.y;
-    c[r] = -2.f * p.z;
-    ni[r] = fmaf(p.x, p.x, fmaf(p.y, p.y, p.z * p.z));
-    m[r] = -3.0e38f;
-  }
-  __syncthreads();
-#pragma unroll 2
-  for (int j = 0; j < TS; j += 2) {
-    const float4 q0 = sj[j], q1 = sj[j + 1];
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-      float t0 = fmaf(q0.x, a[r], q0.w);
-      float t1 = fmaf(q1.x, a[r], q1.w);
-      t0 = fmaf(q0.y, b[r], t0);
-      t1 = fmaf(q1.y, b[r], t1);
-      t0 = fmaf(q0.z, c[r], t0);
-      t1 = fmaf(q1.z, c[r], t1);
-      m[r] = fmax3f(m[r], t0, t1);
-    }
-  }
-  float best = 0.f;
-#pragma unroll
-  for (int r = 0; r < R; r++) best = fmaxf(best, m[r] + ni[r]);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
-  if ((threadIdx.x & 31) == 0) {
-    warp_max[blockIdx.x * (long long)kWarps + (threadIdx.x >> 5)] = best;
-    atomic_max_pos_f32(&st->d3_f32, best);
-  }
+__device__ __forceinline__ void shard_span(long long n, int shard, int nshards, long long& a,
+                                           long long& b) {
+  a = n * shard / nshards;
+  b = n * (shard + 1) / nshards;
 }
 
-// Relative margin of the re-check threshold.  Pass-1 error is below ~1e-6 of
-// D^2; a (tile pair, warp) whose pass-1 maximum is below
-// M*(1 - kRefineRel) provably cannot hold the exact maximum pair.
-constexpr float kRefineRel = 8e-6f;
+__device__ __forceinline__ long long tri(long long T) { return T * (T + 1) / 2; }
+
+// Zero the per-(tile pair, warp) maxima of this ROI (size known on device only).
+__global__ void diam3d_prep(long long cap, const Stats* __restrict__ st,
+                            float* __restrict__ warp_max) {
+  const long long n = n_vertices(st, cap);
+  const long long units = tri((n + kTile - 1) / kTile) * kWarps;
+  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < units;
+       u += (long long)gridDim.x * blockDim.x)
+    warp_max[u] = 0.f;
+}
+
+// Pass 1 (see header).  Error of the dot form: in the bbox-centred frame
+// |p| <= D*sqrt(3)/2, so the absolute error is < ~12 * 2^-24 * D^2.
+__global__ void __launch_bounds__(kDiamThreads, 4) diam3d_pass1(const int4* __restrict__ keys,
+                                                             long long cap, Frame f, int shard,
+                                                             int nshards,
+                                                             float* __restrict__ warp_max,
+                                                             Stats* __restrict__ st) {
+  __shared__ float4 sj[kChunk];  // (x, y, z, |p|^2)
+  const long long n = n_vertices(st, cap);
+  if (n == 0) return;
+  frame_centre(st, f);
+  const long long T = (n + kTile - 1) / kTile;
+  long long u0, u1;
+  shard_span(tri(T) * kChunks, shard, nshards, u0, u1);
+  const int warp = threadIdx.x >> 5;
+  float run = 0.f;
+  for (long long u = u0 + blockIdx.x; u < u1; u += gridDim.x) {
+    const long long item = u / kChunks;
+    const int q = (int)(u - item * kChunks);
+    int I, J;
+    tile_pair(item, T, I, J);
+    float a[kR], b[kR], c[kR], m[kR], ni[kR];
+#pragma unroll
+    for (int r = 0; r < kR; r++) {
+      const long long i = (long long)I * kTile + r * kDiamThreads + threadIdx.x;
+      const float3 p = frame_coord(keys[i < n ? i : n - 1], f);
+      a[r] = -2.f * p.x;
+      b[r] = -2.f * p.y;
+      c[r] = -2.f * p.z;
+      ni[r] = fmaf(p.x, p.x, fmaf(p.y, p.y, p.z * p.z));
+      m[r] = -3.0e38f;
+    }
+    __syncthreads();  // the previous unit is done with sj
+    {
+      long long j = (long long)J * kTile + q * kChunk + threadIdx.x;
+      if (j >= n) j = n - 1;  // repeats of a real vertex are harmless for a max
+      const float3 p = frame_coord(keys[j], f);
+      sj[threadIdx.x] = make_float4(p.x, p.y, p.z, fmaf(p.x, p.x, fmaf(p.y, p.y, p.z * p.z)));
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int j = 0; j < kChunk; j += 2) {
+      const float4 q0 = sj[j], q1 = sj[j + 1];
+#pragma unroll
+      for (int r = 0; r < kR; r++) {
+        float t0 = fmaf(q0.x, a[r], q0.w);
+        float t1 = fmaf(q1.x, a[r], q1.w);
+        t0 = fmaf(q0.y, b[r], t0);
+        t1 = fmaf(q1.y, b[r], t1);
+        t0 = fmaf(q0.z, c[r], t0);
+        t1 = fmaf(q1.z, c[r], t1);
+        m[r] = fmax3f(m[r], t0, t1);
+      }
+    }
+    float best = 0.f;
+#pragma unroll
+    for (int r = 0; r < kR; r++) best = fmaxf(best, m[r] + ni[r]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if ((threadIdx.x & 31) == 0) atomic_max_pos_f32(
+        reinterpret_cast<unsigned int*>(warp_max) + item * kWarps + warp, best);
+    run = fmaxf(run, best);
+  }
+  if ((threadIdx.x & 31) == 0) atomic_max_pos_f32(&st->d3_f32, run);
+}
 
 // Compact the (tile pair, warp) units that may hold the maximum.
-__global__ void diam3d_select(const float* __restrict__ warp_max, long long n_units,
+__global__ void diam3d_select(const float* __restrict__ warp_max, long long cap,
                               Stats* __restrict__ st, unsigned int* __restrict__ cand) {
+  const long long n = n_vertices(st, cap);
+  const long long units = tri((n + kTile - 1) / kTile) * kWarps;
   const float tau = __uint_as_float(st->d3_f32) * (1.f - kRefineRel);
-  for (long long base = (long long)blockIdx.x * blockDim.x; base < n_units;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < units;
        base += (long long)gridDim.x * blockDim.x) {
     const long long u = base + threadIdx.x;
-    const bool hit = u < n_units && warp_max[u] >= tau;
+    const bool hit = u < units && warp_max[u] >= tau;
     const unsigned int mask = __ballot_sync(0xffffffffu, hit);
     if (!mask) continue;
-    unsigned long long pos = 0;
     const int lane = threadIdx.x & 31;
+    unsigned long long pos = 0;
     if (lane == 0) pos = atomicAdd(&st->n_cand, (unsigned long long)__popc(mask));
     pos = __shfl_sync(0xffffffffu, pos, 0);
     if (hit) cand[pos + __popc(mask & ((1u << lane) - 1))] = (unsigned int)u;
   }
 }
 
-// Exact re-check: every selected warp's 32*R i-rows against its J tile, in
-// fp64 with the reference arithmetic on the reference coordinates.  Work unit
-// = (candidate, 256-wide j chunk); a persistent grid walks the units.
-template <int R>
+// Exact re-check: a selected warp's 32*kR i rows against its J tile in fp64
+// with the reference arithmetic on the reference coordinates.  Work unit =
+// (candidate, 256-wide j chunk); a persistent grid walks the units.
 __global__ void __launch_bounds__(kDiamThreads) diam3d_refine(const int4* __restrict__ keys,
-                                                              long long n, int T,
-                                                              long long item0, Frame f,
+                                                              long long cap, Frame f,
                                                               const unsigned int* __restrict__ cand,
                                                               Stats* __restrict__ st) {
-  constexpr int TS = kDiamThreads * R;
-  constexpr int CHUNKS = TS / kDiamThreads;
-  __shared__ double sx[kDiamThreads], sy[kDiamThreads], sz[kDiamThreads];
-  const long long units = (long long)st->n_cand * CHUNKS;
+  __shared__ double sx[kChunk], sy[kChunk], sz[kChunk];
+  const long long n = n_vertices(st, cap);
+  const long long T = (n + kTile - 1) / kTile;
+  const long long units = (long long)st->n_cand * kChunks;
   double best = 0.0;
   for (long long u = blockIdx.x; u < units; u += gridDim.x) {
-    const unsigned int cu = cand[u / CHUNKS];
-    const int q = (int)(u % CHUNKS);
-    const long long item = item0 + cu / kWarps;
+    const unsigned int cu = cand[u / kChunks];
+    const int q = (int)(u % kChunks);
     const int warp = cu % kWarps;
     int I, J;
-    tile_pair(item, T, I, J);
+    tile_pair(cu / kWarps, T, I, J);
     __syncthreads();
     {
-      long long j = (long long)J * TS + q * kDiamThreads + threadIdx.x;
-      int4 kj = keys[j < n ? j : n - 1];
+      const long long j = (long long)J * kTile + q * kChunk + threadIdx.x;
+      const int4 kj = keys[j < n ? j : n - 1];
       sx[threadIdx.x] = ref_coord(kj.x, f.sx);
       sy[threadIdx.x] = ref_coord(kj.y, f.sy);
       sz[threadIdx.x] = ref_coord(kj.z, f.sz);
     }
     __syncthreads();
     const int r = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long i = (long long)I * TS + r * kDiamThreads + warp * 32 + lane;
-    if (r < R && i < n) {
-      int4 ki = keys[i];
+    const long long i = (long long)I * kTile + r * kDiamThreads + warp * 32 + lane;
+    if (i < n) {
+      const int4 ki = keys[i];
       const double xi = ref_coord(ki.x, f.sx), yi = ref_coord(ki.y, f.sy), zi = ref_coord(ki.z, f.sz);
 #pragma unroll 4
-      for (int t = 0; t < kDiamThreads; t++)
-        best = fmax(best, ref_sq_dist(xi, yi, zi, sx[t], sy[t], sz[t]));
+      for (int t = 0; t < kChunk; t++) best = fmax(best, ref_sq_dist(xi, yi, zi, sx[t], sy[t], sz[t]));
     }
   }
 #pragma unroll
@@ -186,8 +225,19 @@ __global__ void __launch_bounds__(kDiamThreads) diam3d_refine(const int4* __rest
 }
 
 // ---- planar pass -----------------------------------------------------------
-// Plane index space: [0, nZ) XY planes keyed by Z2, [nZ, nZ+nY) XZ by Y2,
-// [nZ+nY, P) YZ by X2, where key ranges come from the occupied bbox.
+// Plane index space (PlaneSpace): [0, cnt0) XY planes keyed by Z2, then XZ by
+// Y2, then YZ by X2; keys Z2 in [2 zmin - 1, 2 zmax + 1] etc.
+constexpr int kPT = 256;  // planar tile edge (threads per block)
+
+__device__ __forceinline__ PlaneSpace plane_space(const Stats* st) {
+  PlaneSpace ps;
+  const int* bb = st->bbox;
+  ps.lo[0] = 2 * bb[2] - 1; ps.cnt[0] = 2 * (bb[5] - bb[2]) + 3;
+  ps.lo[1] = 2 * bb[1] - 1; ps.cnt[1] = 2 * (bb[4] - bb[1]) + 3;
+  ps.lo[2] = 2 * bb[0] - 1; ps.cnt[2] = 2 * (bb[3] - bb[0]) + 3;
+  return ps;
+}
+
 __device__ __forceinline__ void plane_ids(int4 k, const PlaneSpace& ps, int out[3]) {
   out[0] = k.z - ps.lo[0];
   out[1] = ps.cnt[0] + (k.y - ps.lo[1]);
@@ -195,8 +245,8 @@ __device__ __forceinline__ void plane_ids(int4 k, const PlaneSpace& ps, int out[
 }
 
 // Warp-aggregated increment: lanes with equal `id` (vertices of one plane are
-// emitted together by the MC warps) share one global atomic.  Returns the
-// slot of this lane within its group's reservation.
+// emitted together by the MC warps) share one global atomic.  Returns this
+// lane's slot within its group's reservation.
 __device__ __forceinline__ unsigned int group_add(unsigned int* base, int id, bool ok) {
   const int lane = threadIdx.x & 31;
   const unsigned int peers = __match_any_sync(0xffffffffu, ok ? id : -1 - lane);
@@ -207,8 +257,10 @@ __device__ __forceinline__ unsigned int group_add(unsigned int* base, int id, bo
   return pos + __popc(peers & ((1u << lane) - 1));
 }
 
-__global__ void plane_hist(const int4* __restrict__ keys, long long n, PlaneSpace ps,
-                           unsigned int* __restrict__ counts) {
+__global__ void plane_hist(const int4* __restrict__ keys, long long cap,
+                           const Stats* __restrict__ st, unsigned int* __restrict__ counts) {
+  const long long n = n_vertices(st, cap);
+  const PlaneSpace ps = plane_space(st);
   for (long long base = (long long)blockIdx.x * blockDim.x; base < n;
        base += (long long)gridDim.x * blockDim.x) {
     const long long v = base + threadIdx.x;
@@ -220,36 +272,61 @@ __global__ void plane_hist(const int4* __restrict__ keys, long long n, PlaneSpac
   }
 }
 
-// Exclusive scan of P counts (P <= a few 10^4) in one block of 1024 threads.
-__global__ void __launch_bounds__(1024) plane_scan(const unsigned int* __restrict__ counts, int P,
-                                                   unsigned int* __restrict__ start,
-                                                   unsigned int* __restrict__ cursor) {
-  __shared__ unsigned int s[1024];
-  __shared__ unsigned int carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < P; base += 1024) {
-    int i = base + threadIdx.x;
-    unsigned int v = i < P ? counts[i] : 0u;
-    s[threadIdx.x] = v;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-      unsigned int t = threadIdx.x >= o ? s[threadIdx.x - o] : 0u;
-      __syncthreads();
-      s[threadIdx.x] += t;
-      __syncthreads();
-    }
-    unsigned int excl = carry + s[threadIdx.x] - v;
-    if (i < P) { start[i] = excl; cursor[i] = excl; }
-    __syncthreads();
-    if (threadIdx.x == 1023) carry += s[1023];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) start[P] = carry;
+__device__ __forceinline__ unsigned int plane_tiles(unsigned int np) {
+  if (np < 2) return 0u;
+  const unsigned int t = (np + kPT - 1) / kPT;
+  return t * (t + 1) / 2;
 }
 
-__global__ void plane_scatter(const int4* __restrict__ keys, long long n, PlaneSpace ps,
-                              unsigned int* __restrict__ cursor, int2* __restrict__ sorted) {
+// One block of 1024 threads: exclusive scans of the plane populations (start,
+// cursor) and of their tile-pair counts (tstart), P from the bbox.
+__global__ void __launch_bounds__(1024) plane_scan(const unsigned int* __restrict__ counts,
+                                                   Stats* __restrict__ st,
+                                                   unsigned int* __restrict__ start,
+                                                   unsigned int* __restrict__ cursor,
+                                                   unsigned int* __restrict__ tstart) {
+  __shared__ unsigned int s[1024], s2[1024];
+  __shared__ unsigned int carry, carry2;
+  if (st->bbox[3] < 0) return;
+  const PlaneSpace ps = plane_space(st);
+  const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
+  if (threadIdx.x == 0) carry = carry2 = 0;
+  __syncthreads();
+  for (int base = 0; base < P; base += 1024) {
+    const int i = base + threadIdx.x;
+    const unsigned int v = i < P ? counts[i] : 0u;
+    const unsigned int w = plane_tiles(v);
+    s[threadIdx.x] = v;
+    s2[threadIdx.x] = w;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+      const unsigned int t = threadIdx.x >= o ? s[threadIdx.x - o] : 0u;
+      const unsigned int t2 = threadIdx.x >= o ? s2[threadIdx.x - o] : 0u;
+      __syncthreads();
+      s[threadIdx.x] += t;
+      s2[threadIdx.x] += t2;
+      __syncthreads();
+    }
+    if (i < P) {
+      start[i] = cursor[i] = carry + s[threadIdx.x] - v;
+      tstart[i] = carry2 + s2[threadIdx.x] - w;
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) { carry += s[1023]; carry2 += s2[1023]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    start[P] = carry;
+    tstart[P] = carry2;
+    st->plane_units = carry2;
+  }
+}
+
+__global__ void plane_scatter(const int4* __restrict__ keys, long long cap,
+                              const Stats* __restrict__ st, unsigned int* __restrict__ cursor,
+                              int2* __restrict__ sorted) {
+  const long long n = n_vertices(st, cap);
+  const PlaneSpace ps = plane_space(st);
   for (long long base = (long long)blockIdx.x * blockDim.x; base < n;
        base += (long long)gridDim.x * blockDim.x) {
     const long long v = base + threadIdx.x;
@@ -271,41 +348,164 @@ __global__ void plane_scatter(const int4* __restrict__ keys, long long n, PlaneS
   }
 }
 
-constexpr int kPlaneChunk = 2048;
+// Planar work unit u (global tile-pair index over all planes) -> plane p and
+// its in-plane tile pair (I, J); binary search over tstart.
+__device__ __forceinline__ int plane_of_unit(const unsigned int* __restrict__ tstart, int P,
+                                             unsigned int u) {
+  int lo = 0, hi = P;  // tstart[lo] <= u < tstart[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (tstart[mid] <= u) lo = mid; else hi = mid;
+  }
+  return lo;
+}
 
-// One block per plane (grid-strided over planes [p0, p1)): exact fp64 max over
-// the plane's vertex pairs with the reference formula (the out-of-plane delta
-// is exactly 0, so dx*dx + dy*dy + 0 == the reference's 3-term sum).
-__global__ void __launch_bounds__(256) plane_pairs(const int2* __restrict__ sorted,
+struct PlaneAxes {  // in-plane (a, b) coordinate frame of one plane family
+  int ca, cb;       // centre, doubled units
+  float ha, hb;     // fp32 half spacings
+  double sa, sb;    // fp64 spacings
+};
+
+__device__ __forceinline__ PlaneAxes plane_axes(int axis, const Stats* st, const Frame& f) {
+  const int* bb = st->bbox;
+  PlaneAxes x;
+  if (axis == 0) {         // XY plane: (X, Y)
+    x.ca = bb[0] + bb[3]; x.cb = bb[1] + bb[4]; x.ha = f.hx; x.hb = f.hy; x.sa = f.sx; x.sb = f.sy;
+  } else if (axis == 1) {  // XZ plane: (X, Z)
+    x.ca = bb[0] + bb[3]; x.cb = bb[2] + bb[5]; x.ha = f.hx; x.hb = f.hz; x.sa = f.sx; x.sb = f.sz;
+  } else {                 // YZ plane: (Y, Z)
+    x.ca = bb[1] + bb[4]; x.cb = bb[2] + bb[5]; x.ha = f.hy; x.hb = f.hz; x.sa = f.sy; x.sb = f.sz;
+  }
+  return x;
+}
+
+// Planar pass 1: fp32 dot form over every in-plane tile pair (256 x 256), one
+// maximum per unit; per-axis maxima in st->pl_f32[axis].
+__global__ void __launch_bounds__(kPT) plane_pass1(const int2* __restrict__ sorted,
                                                    const unsigned int* __restrict__ start,
-                                                   int p0, int p1, PlaneSpace ps, Frame f,
+                                                   const unsigned int* __restrict__ tstart,
+                                                   Frame f, int shard, int nshards,
+                                                   long long ucap, float* __restrict__ umax,
                                                    Stats* __restrict__ st) {
-  __shared__ double sa[kPlaneChunk], sb[kPlaneChunk];
-  __shared__ double s_red[8];
-  for (int p = p0 + blockIdx.x; p < p1; p += gridDim.x) {
+  __shared__ float4 sj[kPT];  // (a, b, |p|^2, -)
+  __shared__ float s_red[kPT / 32];
+  if (st->bbox[3] < 0 || (long long)st->plane_units > ucap) return;  // host re-runs bigger
+  const PlaneSpace ps = plane_space(st);
+  const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
+  long long u0, u1;
+  shard_span(tstart[P], shard, nshards, u0, u1);
+  for (long long u = u0 + blockIdx.x; u < u1; u += gridDim.x) {
+    const int p = plane_of_unit(tstart, P, (unsigned int)u);
     const int axis = p < ps.cnt[0] ? 0 : (p < ps.cnt[0] + ps.cnt[1] ? 1 : 2);
-    const unsigned int b = start[p], e = start[p + 1];
-    const int np = (int)(e - b);
-    if (np < 2) continue;  // block-uniform
-    const double s_a = axis == 2 ? f.sy : f.sx;
-    const double s_b = axis == 0 ? f.sy : f.sz;
-    double best = 0.0;
-    for (int c0 = 0; c0 < np; c0 += kPlaneChunk) {
-      const int c1 = min(np, c0 + kPlaneChunk);
-      __syncthreads();
-      for (int t = c0 + threadIdx.x; t < c1; t += blockDim.x) {
-        int2 k = sorted[b + t];
-        sa[t - c0] = ref_coord(k.x, s_a);
-        sb[t - c0] = ref_coord(k.y, s_b);
+    const PlaneAxes ax = plane_axes(axis, st, f);
+    const unsigned int b0 = start[p], np = start[p + 1] - b0;
+    int I, J;
+    tile_pair(u - tstart[p], (np + kPT - 1) / kPT, I, J);
+    const unsigned int i = I * kPT + threadIdx.x, j = J * kPT + threadIdx.x;
+    const unsigned int jn = min((unsigned int)kPT, np - J * kPT);
+    __syncthreads();
+    if (j < np) {
+      const int2 k = sorted[b0 + j];
+      const float pa = (float)(k.x - ax.ca) * ax.ha, pb = (float)(k.y - ax.cb) * ax.hb;
+      sj[threadIdx.x] = make_float4(pa, pb, fmaf(pa, pa, pb * pb), 0.f);
+    }
+    __syncthreads();
+    float best = 0.f;
+    if (i < np) {
+      const int2 k = sorted[b0 + i];
+      const float pa = (float)(k.x - ax.ca) * ax.ha, pb = (float)(k.y - ax.cb) * ax.hb;
+      const float a2 = -2.f * pa, b2 = -2.f * pb;
+      float m = -3.0e38f;
+      unsigned int t = 0;
+      for (; t + 1 < jn; t += 2) {
+        const float4 q0 = sj[t], q1 = sj[t + 1];
+        m = fmax3f(m, fmaf(q0.y, b2, fmaf(q0.x, a2, q0.z)), fmaf(q1.y, b2, fmaf(q1.x, a2, q1.z)));
       }
-      __syncthreads();
-      for (int i = threadIdx.x; i < c1 - 1; i += blockDim.x) {
-        int2 k = sorted[b + i];
-        const double ai = ref_coord(k.x, s_a), bi = ref_coord(k.y, s_b);
-        for (int j = max(i + 1, c0); j < c1; j++) {
-          double da = __dsub_rn(sa[j - c0], ai), db = __dsub_rn(sb[j - c0], bi);
-          best = fmax(best, __dadd_rn(__dmul_rn(da, da), __dmul_rn(db, db)));
-        }
+      if (t < jn) m = fmaxf(m, fmaf(sj[t].y, b2, fmaf(sj[t].x, a2, sj[t].z)));
+      best = fmaxf(0.f, m + fmaf(pa, pa, pb * pb));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < kPT / 32; w++) best = fmaxf(best, s_red[w]);
+      umax[u] = best;
+      atomic_max_pos_f32(&st->pl_f32[axis], best);
+    }
+  }
+}
+
+__global__ void plane_select(const unsigned int* __restrict__ start,
+                             const unsigned int* __restrict__ tstart,
+                             const float* __restrict__ umax, int shard, int nshards,
+                             long long ucap, Stats* __restrict__ st,
+                             unsigned int* __restrict__ cand) {
+  if (st->bbox[3] < 0 || (long long)st->plane_units > ucap) return;
+  const PlaneSpace ps = plane_space(st);
+  const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
+  const float tau[3] = {__uint_as_float(st->pl_f32[0]) * (1.f - kRefineRel),
+                        __uint_as_float(st->pl_f32[1]) * (1.f - kRefineRel),
+                        __uint_as_float(st->pl_f32[2]) * (1.f - kRefineRel)};
+  long long u0, u1;
+  shard_span(tstart[P], shard, nshards, u0, u1);
+  for (long long base = u0 + (long long)blockIdx.x * blockDim.x; base < u1;
+       base += (long long)gridDim.x * blockDim.x) {
+    const long long u = base + threadIdx.x;
+    bool hit = false;
+    if (u < u1) {
+      const int p = plane_of_unit(tstart, P, (unsigned int)u);
+      const int axis = p < ps.cnt[0] ? 0 : (p < ps.cnt[0] + ps.cnt[1] ? 1 : 2);
+      hit = umax[u] >= tau[axis];
+    }
+    const unsigned int mask = __ballot_sync(0xffffffffu, hit);
+    if (!mask) continue;
+    const int lane = threadIdx.x & 31;
+    unsigned long long pos = 0;
+    if (lane == 0) pos = atomicAdd(&st->n_pcand, (unsigned long long)__popc(mask));
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (hit) cand[pos + __popc(mask & ((1u << lane) - 1))] = (unsigned int)u;
+  }
+}
+
+// Exact planar re-check of the selected in-plane tile pairs (fp64, reference
+// arithmetic: the out-of-plane delta is exactly 0, so da*da + db*db is the
+// reference's 3-term sum bit for bit).
+__global__ void __launch_bounds__(kPT) plane_refine(const int2* __restrict__ sorted,
+                                                    const unsigned int* __restrict__ start,
+                                                    const unsigned int* __restrict__ tstart,
+                                                    Frame f, const unsigned int* __restrict__ cand,
+                                                    Stats* __restrict__ st) {
+  __shared__ double sa[kPT], sb[kPT];
+  __shared__ double s_red[kPT / 32];
+  if (st->bbox[3] < 0) return;
+  const PlaneSpace ps = plane_space(st);
+  const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
+  const long long nc = (long long)st->n_pcand;
+  for (long long c = blockIdx.x; c < nc; c += gridDim.x) {
+    const unsigned int u = cand[c];
+    const int p = plane_of_unit(tstart, P, u);
+    const int axis = p < ps.cnt[0] ? 0 : (p < ps.cnt[0] + ps.cnt[1] ? 1 : 2);
+    const PlaneAxes ax = plane_axes(axis, st, f);
+    const unsigned int b0 = start[p], np = start[p + 1] - b0;
+    int I, J;
+    tile_pair(u - tstart[p], (np + kPT - 1) / kPT, I, J);
+    const unsigned int i = I * kPT + threadIdx.x, j = J * kPT + threadIdx.x;
+    const unsigned int jn = min((unsigned int)kPT, np - J * kPT);
+    __syncthreads();
+    if (j < np) {
+      const int2 k = sorted[b0 + j];
+      sa[threadIdx.x] = ref_coord(k.x, ax.sa);
+      sb[threadIdx.x] = ref_coord(k.y, ax.sb);
+    }
+    __syncthreads();
+    double best = 0.0;
+    if (i < np) {
+      const int2 k = sorted[b0 + i];
+      const double ai = ref_coord(k.x, ax.sa), bi = ref_coord(k.y, ax.sb);
+      for (unsigned int t = 0; t < jn; t++) {
+        const double da = __dsub_rn(sa[t], ai), db = __dsub_rn(sb[t], bi);
+        best = fmax(best, __dadd_rn(__dmul_rn(da, da), __dmul_rn(db, db)));
       }
     }
 #pragma unroll
@@ -313,10 +513,9 @@ __global__ void __launch_bounds__(256) plane_pairs(const int2* __restrict__ sort
     if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = best;
     __syncthreads();
     if (threadIdx.x == 0) {
-      for (int w = 1; w < (int)(blockDim.x >> 5); w++) best = fmax(best, s_red[w]);
-      atomic_max_pos_f64(&st->sq[1 + axis], best);
+      for (int w = 1; w < kPT / 32; w++) best = fmax(best, s_red[w]);
+      if (best > 0.0) atomic_max_pos_f64(&st->sq[1 + axis], best);
     }
-    __syncthreads();
   }
 }
 
@@ -400,16 +599,5 @@ template __global__ void fp32_probe<0>(float*, int, float, float);
 template __global__ void fp32_probe<1>(float*, int, float, float);
 template __global__ void fp32_probe<2>(float*, int, float, float);
 template __global__ void fp32_probe<3>(float*, int, float, float);
-
-// Explicit instantiations used by the engine.
-#define SC_INST(RR)                                                                            \
-  template __global__ void diam3d_pass1<RR>(const int4*, long long, int, long long, long long,   \
-                                            Frame, float*, Stats*);                              \
-  template __global__ void diam3d_refine<RR>(const int4*, long long, int, long long, Frame,      \
-                                             const unsigned int*, Stats*);
-SC_INST(2)
-SC_INST(4)
-SC_INST(8)
-#undef SC_INST
 
 }  // namespace sc

@@ -33,17 +33,20 @@ __global__ void pack_bits_v16(const uint4*, uint32_t*, long long, int, int, Stat
 __global__ void pack_bits_generic(const uint8_t*, uint32_t*, long long, int, int, int, Stats*);
 __global__ void mc_cells(const uint32_t*, int, int, int, int, const CaseTables*, Stats*, int4*,
                          long long);
-template <int R>
-__global__ void diam3d_pass1(const int4*, long long, int, long long, long long, Frame, float*,
-                             Stats*);
+__global__ void diam3d_prep(long long, const Stats*, float*);
+__global__ void diam3d_pass1(const int4*, long long, Frame, int, int, float*, Stats*);
 __global__ void diam3d_select(const float*, long long, Stats*, unsigned int*);
-template <int R>
-__global__ void diam3d_refine(const int4*, long long, int, long long, Frame, const unsigned int*,
-                              Stats*);
-__global__ void plane_hist(const int4*, long long, PlaneSpace, unsigned int*);
-__global__ void plane_scan(const unsigned int*, int, unsigned int*, unsigned int*);
-__global__ void plane_scatter(const int4*, long long, PlaneSpace, unsigned int*, int2*);
-__global__ void plane_pairs(const int2*, const unsigned int*, int, int, PlaneSpace, Frame, Stats*);
+__global__ void diam3d_refine(const int4*, long long, Frame, const unsigned int*, Stats*);
+__global__ void plane_hist(const int4*, long long, const Stats*, unsigned int*);
+__global__ void plane_scan(const unsigned int*, Stats*, unsigned int*, unsigned int*,
+                           unsigned int*);
+__global__ void plane_scatter(const int4*, long long, const Stats*, unsigned int*, int2*);
+__global__ void plane_pass1(const int2*, const unsigned int*, const unsigned int*, Frame, int, int,
+                            long long, float*, Stats*);
+__global__ void plane_select(const unsigned int*, const unsigned int*, const float*, int, int,
+                             long long, Stats*, unsigned int*);
+__global__ void plane_refine(const int2*, const unsigned int*, const unsigned int*, Frame,
+                             const unsigned int*, Stats*);
 __global__ void cloud_diameters(const double*, const double*, const double*, long long, int,
                                 unsigned long long*);
 template <int MODE>
@@ -162,14 +165,16 @@ struct Ctx {
   cudaEvent_t ev[6] = {};
   cudaEvent_t kev[8] = {};      // per-kernel boundaries of the last ROI
   double last_ms[6] = {0, 0, 0, 0, 0, 0};  // pack, mc, pass1, refine, planar, h2d
+  long long dcap = 0;  // vertices the diameter-side buffers are sized for
+  int occ_pass1 = 1, occ_plane = 1;  // resident blocks/SM of the persistent kernels
   Stats* d_stats = nullptr;
   Stats* h_stats = nullptr;  // pinned
   CaseTables* d_tabs = nullptr;
   DevBuf<uint32_t> bits;
   DevBuf<int4> keys;
-  DevBuf<float> warp_max;
-  DevBuf<unsigned int> cand;
-  DevBuf<unsigned int> plane_counts, plane_start, plane_cursor;
+  DevBuf<float> warp_max, plane_umax;
+  DevBuf<unsigned int> cand, plane_cand;
+  DevBuf<unsigned int> plane_counts, plane_start, plane_cursor, plane_tstart;
   DevBuf<int2> plane_sorted;
   DevBuf<uint8_t> mask_stage;
   DevBuf<double> cloud;
@@ -207,9 +212,8 @@ int get_ctx(int device, Ctx** out) {
     CK(cudaMallocHost(&c->h_stats, sizeof(Stats)));
     CK(cudaMalloc(&c->d_tabs, sizeof(CaseTables)));
     CK(cudaMemcpy(c->d_tabs, &case_geom().tabs, sizeof(CaseTables), cudaMemcpyHostToDevice));
-    CK(cudaFuncSetAttribute(diam3d_pass1<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 512 * 16));
-    CK(cudaFuncSetAttribute(diam3d_pass1<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
-    CK(cudaFuncSetAttribute(diam3d_pass1<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2048 * 16));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pass1, diam3d_pass1, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_plane, plane_pass1, 256, 0));
     g_ctx[device] = std::move(c);
   }
   *out = g_ctx[device].get();
@@ -243,125 +247,124 @@ double f64_of(unsigned long long bits) {
   return d;
 }
 
-// Marching-cubes stage: init + pack + cells, then one small D2H (counts+bbox).
-int run_mc(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, cudaStream_t s) {
-  const int W = (int)((nx + 31) / 32);
-  const long long n_words = (long long)W * ny * nz;
-  CK(c->bits.ensure((size_t)n_words));
-  if (c->keys.cap == 0) CK(c->keys.ensure(1 << 20));
-  for (int attempt = 0; attempt < 2; attempt++) {
-    CK(cudaEventRecord(c->kev[0], s));
-    init_stats<<<1, 256, 0, s>>>(c->d_stats);
-    CKL(1);
-    if (nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0) {
-      const long long n_chunks = nx * ny * nz / 16;
-      const int C16 = (int)(nx / 16);
-      // grid * 1024 must be a multiple of C16 (whole rows per grid stride).
-      int unit = C16;
-      for (int g = 1024; g % 2 == 0 && unit % 2 == 0;) { g /= 2; unit /= 2; }
-      long long want = (n_chunks + 256 * 4 - 1) / (256 * 4);
-      long long grid = std::min<long long>(want, (long long)c->sms * 8);
-      grid = std::max<long long>(unit, (grid + unit - 1) / unit * unit);
-      pack_bits_v16<4><<<(unsigned)grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(d_mask),
-                                                      c->bits.p, n_chunks, C16, (int)ny,
-                                                      c->d_stats);
-    } else {
-      long long want = (n_words + 255) / 256;
-      int grid = (int)std::min<long long>(want, (long long)c->sms * 8);
-      pack_bits_generic<<<grid, 256, 0, s>>>(d_mask, c->bits.p, n_words, (int)nx, W, (int)ny,
-                                             c->d_stats);
-    }
-    CKL(1);
-    CK(cudaEventRecord(c->kev[1], s));
-    mc_cells<<<c->sms * 4, 256, 0, s>>>(c->bits.p, (int)nx, (int)ny, (int)nz, W, c->d_tabs,
-                                        c->d_stats, c->keys.p, (long long)c->keys.cap);
-    CKL(1);
-    CK(cudaEventRecord(c->kev[2], s));
-    CK(cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (c->h_stats->n_vert <= c->keys.cap) return SC_OK;
-    CK(c->keys.ensure((size_t)c->h_stats->n_vert));  // rare: re-run with room
-  }
-  set_err("vertex buffer overflow");
-  return SC_ERR_NOMEM;
+constexpr long long kTile = 2048;  // diameter.cu kTile
+
+// Capacity of the per-ROI vertex arrays.  V is only known on the device, so
+// the arrays are sized up front (grow-only) and an overflow, detected after
+// the single end-of-ROI sync, re-runs the ROI with exact capacity.
+long long vertex_capacity(int64_t nx, int64_t ny, int64_t nz, long long hint) {
+  const long long vox = nx * ny * nz;
+  long long cap = std::max<long long>(1 << 20, vox / 16);
+  return std::max(cap, hint);
 }
 
-// Diameter stage for shard `shard` of `nshards`: 3-D tile pairs and planes.
-int run_diameters(Ctx* c, const double sp[3], cudaStream_t s, int shard, int nshards) {
-  const Stats& h = *c->h_stats;
-  const long long V = (long long)h.n_vert;
-  const int* bb = h.bbox;
+// keys (MC output) hold up to `cap` vertices; the diameter-side arrays (whose
+// tile-pair bookkeeping grows as V^2) hold up to `dcap` <= cap.
+int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, long long dcap,
+                   long long punits) {
+  const int W = (int)((nx + 31) / 32);
+  CK(c->bits.ensure((size_t)((long long)W * ny * nz)));
+  CK(c->keys.ensure((size_t)cap));
+  const long long T = (dcap + kTile - 1) / kTile;
+  CK(c->warp_max.ensure((size_t)(T * (T + 1) / 2 * 8)));
+  CK(c->cand.ensure((size_t)(T * (T + 1) / 2 * 8)));
+  const long long P = 2 * (nx + ny + nz) + 9;
+  CK(c->plane_counts.ensure((size_t)P));
+  CK(c->plane_start.ensure((size_t)P + 1));
+  CK(c->plane_cursor.ensure((size_t)P));
+  CK(c->plane_tstart.ensure((size_t)P + 1));
+  CK(c->plane_sorted.ensure((size_t)(3 * dcap)));
+  // planar tile pairs: sum over planes of t(t+1)/2, t = ceil(n_p/256); bounded
+  // by (3 dcap / 256)^2 / 2 + P, far below in practice: size for the bound
+  // with a 64-plane spread.
+  const long long t = (3 * dcap) / 256 + 1;
+  const long long pu = std::max(std::min(t * (t + 1) / 2, t * 64) + P + 1, punits);
+  CK(c->plane_umax.ensure((size_t)pu));
+  CK(c->plane_cand.ensure((size_t)pu));
+  return SC_OK;
+}
+
+// Enqueue one whole ROI on stream s; no host synchronisation.  Kernel order:
+// init, pack, mc | prep, pass1, select, refine | plane hist, scan, scatter,
+// pass1, select, refine.  kev[] brackets the stages for sc_last_kernel_times.
+int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
+                const double sp[3], cudaStream_t s, int shard, int nshards, long long cap,
+                long long dcap) {
+  const int W = (int)((nx + 31) / 32);
+  const long long n_words = (long long)W * ny * nz;
+  CK(cudaEventRecord(c->kev[0], s));
+  init_stats<<<1, 256, 0, s>>>(c->d_stats);
+  CKL(1);
+  if (nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0) {
+    const long long n_chunks = nx * ny * nz / 16;
+    const int C16 = (int)(nx / 16);
+    // grid * 1024 must be a multiple of C16 (whole rows per grid stride).
+    int unit = C16;
+    for (int g = 1024; g % 2 == 0 && unit % 2 == 0;) { g /= 2; unit /= 2; }
+    long long want = (n_chunks + 256 * 4 - 1) / (256 * 4);
+    long long grid = std::min<long long>(want, (long long)c->sms * 8);
+    grid = std::max<long long>(unit, (grid + unit - 1) / unit * unit);
+    pack_bits_v16<4><<<(unsigned)grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(d_mask),
+                                                    c->bits.p, n_chunks, C16, (int)ny, c->d_stats);
+  } else {
+    long long want = (n_words + 255) / 256;
+    int grid = (int)std::min<long long>(want, (long long)c->sms * 8);
+    pack_bits_generic<<<grid, 256, 0, s>>>(d_mask, c->bits.p, n_words, (int)nx, W, (int)ny,
+                                           c->d_stats);
+  }
+  CKL(1);
+  CK(cudaEventRecord(c->kev[1], s));
+  mc_cells<<<c->sms * 4, 256, 0, s>>>(c->bits.p, (int)nx, (int)ny, (int)nz, W, c->d_tabs,
+                                      c->d_stats, c->keys.p, cap);
+  CKL(1);
+  CK(cudaEventRecord(c->kev[2], s));
+
   Frame f;
-  f.cx2 = bb[0] + bb[3];
-  f.cy2 = bb[1] + bb[4];
-  f.cz2 = bb[2] + bb[5];
+  f.cx2 = f.cy2 = f.cz2 = 0;  // set on the device from the bbox
   f.hx = (float)(0.5 * sp[0]);
   f.hy = (float)(0.5 * sp[1]);
   f.hz = (float)(0.5 * sp[2]);
   f.sx = sp[0];
   f.sy = sp[1];
   f.sz = sp[2];
-
-  // 3-D: pick the register block so the triangle holds >= 4 waves of tiles.
-  int R = 2;
-  for (int r : {8, 4}) {
-    long long T = (V + 256LL * r - 1) / (256LL * r);
-    if (T * (T + 1) / 2 >= 4LL * c->sms) { R = r; break; }
-  }
-  const long long TS = 256LL * R;
-  const long long T = (V + TS - 1) / TS;
-  const long long n_items = T * (T + 1) / 2;
-  const long long i0 = n_items * shard / nshards, i1 = n_items * (shard + 1) / nshards;
-  const long long n_loc = i1 - i0;
-  CK(cudaEventRecord(c->kev[3], s));
-  if (n_loc > 0) {
-    const long long n_units = n_loc * 8;  // (tile pair, warp)
-    CK(c->warp_max.ensure((size_t)n_units));
-    CK(c->cand.ensure((size_t)n_units));
-    const size_t smem = (size_t)TS * 16;
-    const int sgrid = (int)std::min<long long>((n_units + 255) / 256, (long long)c->sms * 8);
-#define LAUNCH_3D(RR)                                                                          \
-  diam3d_pass1<RR><<<(unsigned)n_loc, 256, smem, s>>>(c->keys.p, V, (int)T, i0, n_loc, f,      \
-                                                      c->warp_max.p, c->d_stats);              \
-  CKL(1);                                                                                      \
-  CK(cudaEventRecord(c->kev[4], s));                                                           \
-  diam3d_select<<<sgrid, 256, 0, s>>>(c->warp_max.p, n_units, c->d_stats, c->cand.p);          \
-  CKL(1);                                                                                      \
-  diam3d_refine<RR><<<c->sms * 2, 256, 0, s>>>(c->keys.p, V, (int)T, i0, f, c->cand.p,         \
-                                               c->d_stats);                                    \
+  // Persistent grids: exactly the resident blocks, so the static round-robin
+  // split of work units is also the load balance.
+  const int pgrid = c->sms * std::max(1, c->occ_pass1);
+  const int plgrid = c->sms * std::max(1, c->occ_plane);
+  diam3d_prep<<<c->sms * 2, 256, 0, s>>>(dcap, c->d_stats, c->warp_max.p);
   CKL(1);
-    if (R == 8) { LAUNCH_3D(8) } else if (R == 4) { LAUNCH_3D(4) } else { LAUNCH_3D(2) }
-#undef LAUNCH_3D
-  } else {
-    CK(cudaEventRecord(c->kev[4], s));
-  }
+  CK(cudaEventRecord(c->kev[3], s));
+  diam3d_pass1<<<pgrid, 256, 0, s>>>(c->keys.p, dcap, f, shard, nshards, c->warp_max.p,
+                                     c->d_stats);
+  CKL(1);
+  CK(cudaEventRecord(c->kev[4], s));
+  diam3d_select<<<c->sms * 2, 256, 0, s>>>(c->warp_max.p, dcap, c->d_stats, c->cand.p);
+  CKL(1);
+  diam3d_refine<<<c->sms * 2, 256, 0, s>>>(c->keys.p, dcap, f, c->cand.p, c->d_stats);
+  CKL(1);
   CK(cudaEventRecord(c->kev[5], s));
 
-  // Planar: keys Z2 in [2zmin-1, 2zmax+1], etc.
-  PlaneSpace ps;
-  ps.lo[0] = 2 * bb[2] - 1; ps.cnt[0] = 2 * (bb[5] - bb[2]) + 3;
-  ps.lo[1] = 2 * bb[1] - 1; ps.cnt[1] = 2 * (bb[4] - bb[1]) + 3;
-  ps.lo[2] = 2 * bb[0] - 1; ps.cnt[2] = 2 * (bb[3] - bb[0]) + 3;
-  const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
-  CK(c->plane_counts.ensure(P));
-  CK(c->plane_start.ensure(P + 1));
-  CK(c->plane_cursor.ensure(P));
-  CK(c->plane_sorted.ensure((size_t)(3 * V)));
+  const long long P = 2 * (nx + ny + nz) + 9;
   CK(cudaMemsetAsync(c->plane_counts.p, 0, sizeof(unsigned int) * P, s));
-  const int vgrid = (int)std::min<long long>((V + 255) / 256, (long long)c->sms * 8);
-  plane_hist<<<vgrid, 256, 0, s>>>(c->keys.p, V, ps, c->plane_counts.p);
+  plane_hist<<<c->sms * 4, 256, 0, s>>>(c->keys.p, dcap, c->d_stats, c->plane_counts.p);
   CKL(1);
-  plane_scan<<<1, 1024, 0, s>>>(c->plane_counts.p, P, c->plane_start.p, c->plane_cursor.p);
+  plane_scan<<<1, 1024, 0, s>>>(c->plane_counts.p, c->d_stats, c->plane_start.p,
+                                c->plane_cursor.p, c->plane_tstart.p);
   CKL(1);
-  plane_scatter<<<vgrid, 256, 0, s>>>(c->keys.p, V, ps, c->plane_cursor.p, c->plane_sorted.p);
+  plane_scatter<<<c->sms * 4, 256, 0, s>>>(c->keys.p, dcap, c->d_stats, c->plane_cursor.p,
+                                           c->plane_sorted.p);
   CKL(1);
-  const int p0 = (int)((long long)P * shard / nshards), p1 = (int)((long long)P * (shard + 1) / nshards);
-  if (p1 > p0) {
-    const int pgrid = std::min(p1 - p0, c->sms * 8);
-    plane_pairs<<<pgrid, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, p0, p1, ps, f,
-                                      c->d_stats);
-    CKL(1);
-  }
+  plane_pass1<<<plgrid, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_tstart.p, f,
+                                    shard, nshards, (long long)c->plane_umax.cap, c->plane_umax.p,
+                                    c->d_stats);
+  CKL(1);
+  plane_select<<<c->sms * 2, 256, 0, s>>>(c->plane_start.p, c->plane_tstart.p, c->plane_umax.p,
+                                          shard, nshards, (long long)c->plane_umax.cap, c->d_stats,
+                                          c->plane_cand.p);
+  CKL(1);
+  plane_refine<<<c->sms * 2, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p,
+                                          c->plane_tstart.p, f, c->plane_cand.p, c->d_stats);
+  CKL(1);
   CK(cudaEventRecord(c->kev[6], s));
   return SC_OK;
 }
@@ -400,33 +403,47 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
-// Full pipeline on a device-resident mask (context lock held by the caller).
+// Full pipeline on a device-resident mask (context lock held by the caller):
+// enqueue everything, one D2H of the accumulators, one sync.
 int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, const double sp[3],
             cudaStream_t s, int shard, int nshards, double* d_sq4, sc_coeffs* out) {
-  CK(cudaEventRecord(c->ev[2], s));
-  int rc = run_mc(c, d_mask, nx, ny, nz, s);
-  if (rc) return rc;
-  CK(cudaEventRecord(c->ev[3], s));
+  long long cap = vertex_capacity(nx, ny, nz, (long long)c->keys.cap);
+  long long dcap = std::min<long long>(cap, std::max<long long>(4LL << 20, c->dcap));
+  long long punits = 0;
+  for (int attempt = 0; attempt < 2; attempt++) {
+    int rc = ensure_buffers(c, nx, ny, nz, cap, dcap, punits);
+    if (rc) return rc;
+    cap = (long long)c->keys.cap;
+    c->dcap = std::max(c->dcap, dcap);
+    rc = enqueue_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, cap, dcap);
+    if (rc) return rc;
+    if (d_sq4)
+      CK(cudaMemcpyAsync(d_sq4, c->d_stats->sq, 4 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const long long V = (long long)c->h_stats->n_vert;
+    const long long PU = (long long)c->h_stats->plane_units;
+    if (V <= dcap && PU <= (long long)c->plane_umax.cap) break;
+    if (attempt == 1) { set_err("vertex buffer overflow"); return SC_ERR_NOMEM; }
+    // rare: more vertices / planar tiles than reserved -> exact re-run
+    cap = std::max(cap, V);
+    dcap = std::max(dcap, V);
+    punits = PU;
+  }
   if (c->h_stats->bbox[3] < 0) {
     set_err("mask has no occupied voxels");
     return SC_ERR_EMPTY_ROI;
   }
-  rc = run_diameters(c, sp, s, shard, nshards);
-  if (rc) return rc;
-  CK(cudaEventRecord(c->ev[4], s));
-  if (d_sq4)
-    CK(cudaMemcpyAsync(d_sq4, c->d_stats->sq, 4 * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  CK(cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
   fill_out(*c->h_stats, sp, out);
-  out->mesh_ms = ev_ms(c->ev[2], c->ev[3]);
-  out->diameters_ms = ev_ms(c->ev[3], c->ev[4]);
+  for (int i = 0; i < 5; i++) c->last_ms[i] = 0.0;
   c->last_ms[0] = ev_ms(c->kev[0], c->kev[1]);
   c->last_ms[1] = ev_ms(c->kev[1], c->kev[2]);
   c->last_ms[2] = ev_ms(c->kev[3], c->kev[4]);
   c->last_ms[3] = ev_ms(c->kev[4], c->kev[5]);
   c->last_ms[4] = ev_ms(c->kev[5], c->kev[6]);
   c->last_ms[5] = 0.0;
+  out->mesh_ms = ev_ms(c->kev[0], c->kev[2]);
+  out->diameters_ms = ev_ms(c->kev[2], c->kev[6]);
   return SC_OK;
 }
 
@@ -564,8 +581,11 @@ int sc_mesh_vertices(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, in
   CK(c->mask_stage.ensure(bytes));
   cudaStream_t s = c->stream;
   CK(cudaMemcpyAsync(c->mask_stage.p, mask, bytes, cudaMemcpyHostToDevice, s));
-  if ((rc = run_mc(c, c->mask_stage.p, nx, ny, nz, s))) return rc;
-  if (c->h_stats->bbox[3] < 0) { set_err("mask has no occupied voxels"); return SC_ERR_EMPTY_ROI; }
+  {
+    const double unit[3] = {1.0, 1.0, 1.0};
+    sc_coeffs tmp;
+    if ((rc = run_roi(c, c->mask_stage.p, nx, ny, nz, unit, s, 0, 1, nullptr, &tmp))) return rc;
+  }
   const long long V = (long long)c->h_stats->n_vert;
   *n_out = V;
   const long long m = V < cap ? V : cap;

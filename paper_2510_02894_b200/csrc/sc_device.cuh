@@ -18,7 +18,10 @@ struct Stats {
   unsigned int d3_f32;                 // fp32 bits of the pass-1 max squared 3-D distance
   unsigned int pad0;
   unsigned long long sq[4];            // fp64 bits: exact squared maxima (3d, xy, xz, yz)
-  unsigned long long n_cand;           // (tile pair, warp) units re-checked in fp64
+  unsigned long long n_cand;           // 3-D (tile pair, warp) units re-checked in fp64
+  unsigned long long n_pcand;          // planar tile pairs re-checked in fp64
+  unsigned int pl_f32[4];              // fp32 bits of pass-1 planar maxima (xy, xz, yz, -)
+  unsigned long long plane_units;      // in-plane tile pairs of the planar pass
 };
 
 // Per-case integer tables for the exact volume path: for case k,
