@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -34,6 +35,7 @@ __global__ void pack_bits_generic(const uint8_t*, uint32_t*, long long, int, int
 __global__ void mc_cells(const uint32_t*, int, int, int, int, const CaseTables*, Stats*, int4*,
                          long long);
 __global__ void diam3d_prep(long long, const Stats*, float*);
+template <bool PACKED>
 __global__ void diam3d_pass1(const int4*, long long, Frame, int, int, float*, Stats*);
 __global__ void diam3d_select(const float*, long long, Stats*, unsigned int*);
 __global__ void diam3d_refine(const int4*, long long, Frame, const unsigned int*, Stats*);
@@ -166,7 +168,8 @@ struct Ctx {
   cudaEvent_t kev[8] = {};      // per-kernel boundaries of the last ROI
   double last_ms[6] = {0, 0, 0, 0, 0, 0};  // pack, mc, pass1, refine, planar, h2d
   long long dcap = 0;  // vertices the diameter-side buffers are sized for
-  int occ_pass1 = 1, occ_plane = 1;  // resident blocks/SM of the persistent kernels
+  int occ_pass1 = 1, occ_pass1s = 1, occ_plane = 1;  // resident blocks/SM (persistent kernels)
+  bool pass1_packed = true;  // FFMA2 variant of diam3d_pass1 (SC_PASS1=scalar selects FFMA)
   Stats* d_stats = nullptr;
   Stats* h_stats = nullptr;  // pinned
   CaseTables* d_tabs = nullptr;
@@ -212,7 +215,9 @@ int get_ctx(int device, Ctx** out) {
     CK(cudaMallocHost(&c->h_stats, sizeof(Stats)));
     CK(cudaMalloc(&c->d_tabs, sizeof(CaseTables)));
     CK(cudaMemcpy(c->d_tabs, &case_geom().tabs, sizeof(CaseTables), cudaMemcpyHostToDevice));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pass1, diam3d_pass1, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pass1, diam3d_pass1<true>, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pass1s, diam3d_pass1<false>, 256, 0));
+    if (const char* v = getenv("SC_PASS1")) c->pass1_packed = std::strcmp(v, "scalar") != 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_plane, plane_pass1, 256, 0));
     g_ctx[device] = std::move(c);
   }
@@ -334,8 +339,12 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
   diam3d_prep<<<c->sms * 2, 256, 0, s>>>(dcap, c->d_stats, c->warp_max.p);
   CKL(1);
   CK(cudaEventRecord(c->kev[3], s));
-  diam3d_pass1<<<pgrid, 256, 0, s>>>(c->keys.p, dcap, f, shard, nshards, c->warp_max.p,
-                                     c->d_stats);
+  if (c->pass1_packed)
+    diam3d_pass1<true><<<pgrid, 256, 0, s>>>(c->keys.p, dcap, f, shard, nshards, c->warp_max.p,
+                                             c->d_stats);
+  else
+    diam3d_pass1<false><<<c->sms * std::max(1, c->occ_pass1s), 256, 0, s>>>(
+        c->keys.p, dcap, f, shard, nshards, c->warp_max.p, c->d_stats);
   CKL(1);
   CK(cudaEventRecord(c->kev[4], s));
   diam3d_select<<<c->sms * 2, 256, 0, s>>>(c->warp_max.p, dcap, c->d_stats, c->cand.p);
