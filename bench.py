@@ -17,11 +17,13 @@ mask (157 MB) is larger than L2 (126 MB), so no L2 flush is needed.
              are inside the timed region).
   e2e        the same metric through the C ABI with a HOST (pinned) mask:
              every step copies the 157 MB mask H2D and reads the result back.
-  roofline   dominant kernel = diam3d_pass1 (FP32 CUDA-core bound); achieved =
-             8 flop * V(V-1)/2 pairs / kernel time; peak = FP32 rate measured
-             by sc_probe_fp32_peak on this GPU.  roofline_mc: pack_bits
-             (HBM-bound), achieved = mask bytes / kernel time vs the measured
-             copy bandwidth in MEASURED_PEAKS.json.
+  roofline   the dominant kernel of the step.  diam3d_pass1 is FP32
+             CUDA-core bound: achieved = 8 flop x evaluated pairs / kernel time,
+             peak = FP32 rate measured by sc_probe_fp32_peak on this GPU.
+             pack_bits_v16 is HBM-bound: achieved = mask bytes / kernel time vs
+             the measured copy bandwidth in MEASURED_PEAKS.json.
+  allpairs   the same exact results with work pruning disabled (every pair
+             through pass 1): the brute-force pass-1 roofline.
   cpu_baseline  the CPU oracle (C restatement of the reference, OpenMP strip-
              parallel diameters, serial MC as in the reference) on one ROI.
 
@@ -237,6 +239,38 @@ def run_reference(args):
     return 0
 
 
+def measure_device(sc, _native, d_mask, stream, steps, warmup, dev, world, clocks=None):
+    """K device-resident steps on `stream`, CUDA events around the whole loop;
+    returns (elapsed ms max over ranks, per-kernel median ms, diag, launches, c)."""
+    import torch
+
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            c = sc.calculate_coefficients_device(d_mask, SPACING, stream=stream)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kt = {k: [] for k in _native.KERNEL_TIME_NAMES}
+    launches0 = _native.launch_count()
+    barrier(world)
+    torch.cuda.synchronize()
+    if clocks is not None:
+        clocks.__enter__()
+    ev0.record(stream)
+    for _ in range(steps):
+        c = sc.calculate_coefficients_device(d_mask, SPACING, stream=stream)
+        for k, v in _native.last_kernel_times(dev).items():
+            kt[k].append(v)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if clocks is not None:
+        clocks.__exit__(None, None, None)
+    barrier(world)
+    launches = _native.launch_count() - launches0
+    ms = max_over_ranks(world, ev0.elapsed_time(ev1))
+    med = {k: statistics.median(v) for k, v in kt.items() if v}
+    return ms, med, _native.last_diagnostics(dev), launches, c
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -253,29 +287,18 @@ def run_ours(args):
     h_mask = torch.from_numpy(mask_np).pin_memory()
     h_np = h_mask.numpy()
 
-    # ---- device-resident throughput (value) ----
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            c = sc.calculate_coefficients_device(d_mask, SPACING, stream=stream)
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = _native.launch_count()
-    kt = {k: [] for k in _native.KERNEL_TIME_NAMES}
-    barrier(world)
-    torch.cuda.synchronize()
-    with ClockSampler(dev) as clocks:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            c = sc.calculate_coefficients_device(d_mask, SPACING, stream=stream)
-            for k, v in _native.last_kernel_times(dev).items():
-                kt[k].append(v)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    barrier(world)
-    launches = _native.launch_count() - launches0
-    dev_ms = ev0.elapsed_time(ev1)
-    dev_ms_max = max_over_ranks(world, dev_ms)
-    value = world * args.steps / (dev_ms_max / 1e3)
+    # ---- device-resident throughput (value): exact pruned path (default) ----
+    clocks = ClockSampler(dev)
+    dev_ms, med, diag, launches, c = measure_device(sc, _native, d_mask, stream, args.steps,
+                                                    args.warmup, dev, world, clocks)
+    value = world * args.steps / (dev_ms / 1e3)
+
+    # ---- same, all pairs evaluated (no pruning): the pass-1 roofline case ----
+    _native.set_option("prune", 0)
+    bf_ms, bf_med, bf_diag, _, c_bf = measure_device(sc, _native, d_mask, stream,
+                                                     max(3, args.steps // 2), 3, dev, world)
+    _native.set_option("prune", 1)
+    assert c_bf.to_dict() == c.to_dict(), "pruned and all-pairs results differ"
 
     # ---- end to end through the C ABI with a pinned host mask (e2e) ----
     for _ in range(max(1, args.warmup // 2)):
@@ -289,23 +312,44 @@ def run_ours(args):
     e2e_s = max_over_ranks(world, time.perf_counter() - t0)
     barrier(world)
     e2e_value = world * args.steps / e2e_s
-    h2d_ms = ce.h2d_ms
 
-    # ---- roofline of the dominant kernel ----
-    med = {k: statistics.median(v) for k, v in kt.items() if v}
+    # ---- rooflines ----
     V = c.vertex_count
-    pairs = V * (V - 1) / 2
-    pass1_s = med["diam3d_pass1_ms"] / 1e3
+    pairs_alg = V * (V - 1) / 2
     fp32_peak = max(_native.probe_fp32_peak(dev, m) for m in (0, 1, 3))
-    fp32_peak_reg2 = _native.probe_fp32_peak(dev, 0)
-    achieved = 8.0 * pairs / pass1_s / 1e12
+    fp32_ffma2 = _native.probe_fp32_peak(dev, 0)
     traffic = ncu_traffic()
     peaks, peak_kind = measured_peaks()
     mask_bytes = nx * ny * nz
+
+    def pass1_roof(m, d, label):
+        evaluated = d["work_units"] * _native.PAIRS_PER_UNIT
+        t = m["diam3d_pass1_ms"] / 1e3
+        ach = 8.0 * evaluated / t / 1e12
+        return {"kernel": "diam3d_pass1", "bound": "fp32", "achieved": ach, "peak": fp32_peak,
+                "unit": "TFLOP/s", "frac": ach / fp32_peak,
+                "traffic": traffic.get("diam3d_pass1"),
+                "work": f"{label}: 8 flop x {evaluated:.4g} evaluated pairs "
+                        f"({d['work_units']} of {d['total_units']} units of 2048x256)",
+                "pair_evals_per_s": evaluated / t,
+                "peak_note": "FP32 CUDA-core rate measured on this GPU by sc_probe_fp32_peak "
+                             f"(best of FFMA/FFMA-imm/FFMA2; FFMA2 alone {fp32_ffma2:.1f} "
+                             "TFLOP/s); nominal 74.4 at 1965 MHz"}
+
     pack_s = med["pack_ms"] / 1e3
     mc_gbs = mask_bytes / pack_s / 1e9
-    shares = {k: med[k] / max(1e-9, sum(med[x] for x in med if x != "h2d_ms"))
-              for k in med if k != "h2d_ms"}
+    roof_mc = {"kernel": "pack_bits_v16", "bound": "hbm", "achieved": mc_gbs,
+               "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": mc_gbs / peaks["hbm_gbs"],
+               "traffic": traffic.get("pack_bits_v16"), "peak_kind": peak_kind,
+               "work": f"{mask_bytes} mask bytes read once per launch",
+               "mvoxels_per_s": mask_bytes / pack_s / 1e6,
+               "mc_stage_mvoxels_per_s": mask_bytes / ((med["pack_ms"] + med["mc_ms"]) / 1e3) / 1e6}
+    roof_p1 = pass1_roof(med, diag, "pruned")
+    roof_p1_bf = pass1_roof(bf_med, bf_diag, "all pairs")
+    stage = {k: v for k, v in med.items() if k != "h2d_ms"}
+    dominant = max(stage, key=stage.get)
+    roofline = roof_p1 if dominant == "diam3d_pass1_ms" else roof_mc
+    total_k = sum(stage.values())
 
     line = {
         "metric": METRIC,
@@ -314,7 +358,7 @@ def run_ours(args):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": dev_ms_max / args.steps,
+        "ms_per_step": dev_ms / args.steps,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -324,39 +368,22 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": mask_bytes,
                 "d2h_bytes_per_step": 2 * 2304,
                 "path": "sc_calculate_coefficients (C ABI) from pinned host memory",
-                "h2d_ms_per_step": h2d_ms},
+                "h2d_ms_per_step": ce.h2d_ms},
         "gpu_launches": int(launches),
-        "roofline": {
-            "kernel": "diam3d_pass1",
-            "bound": "fp32",
-            "achieved": achieved,
-            "peak": fp32_peak,
-            "unit": "TFLOP/s",
-            "frac": achieved / fp32_peak,
-            "traffic": traffic.get("diam3d_pass1"),
-            "work": f"8 flop x V(V-1)/2 = {pairs:.4g} pairs per launch, V={V}",
-            "peak_note": "FP32 CUDA-core rate measured on this GPU by sc_probe_fp32_peak "
-                         f"(best of FFMA2/FFMA/FFMA-imm; FFMA2 all-register "
-                         f"{fp32_peak_reg2:.1f} TFLOP/s); nominal 74.4 at 1965 MHz",
-            "pair_evals_per_s": pairs / pass1_s,
-        },
-        "roofline_mc": {
-            "kernel": "pack_bits_v16",
-            "bound": "hbm",
-            "achieved": mc_gbs,
-            "peak": peaks["hbm_gbs"],
-            "unit": "GB/s",
-            "frac": mc_gbs / peaks["hbm_gbs"],
-            "traffic": traffic.get("pack_bits_v16"),
-            "peak_kind": peak_kind,
-            "mvoxels_per_s": mask_bytes / pack_s / 1e6,
-            "mc_stage_mvoxels_per_s": mask_bytes / ((med["pack_ms"] + med["mc_ms"]) / 1e3) / 1e6,
-        },
+        "roofline": roofline,
+        "roofline_mc": roof_mc,
+        "roofline_pass1": roof_p1,
+        "allpairs": {"value": world * max(3, args.steps // 2) / (bf_ms / 1e3), "unit": UNIT,
+                     "note": "same exact results with pruning disabled (every pair evaluated)",
+                     "kernel_ms": bf_med, "roofline_pass1": roof_p1_bf},
         "kernel_ms": med,
-        "kernel_share": shares,
+        "kernel_share": {k: v / total_k for k, v in stage.items()},
+        "dominant_stage": dominant,
+        "diagnostics": diag,
         "clocks": clocks.summary(),
         "result": {"VertexCount": V, "triangles": c.triangle_count, "active_cubes": c.active_cubes,
-                   "Maximum3DDiameter": c.max_3d_diameter, "MeshVolume": c.mesh_volume},
+                   "Maximum3DDiameter": c.max_3d_diameter, "MeshVolume": c.mesh_volume,
+                   "pairs": pairs_alg},
     }
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -113,13 +113,21 @@ int sc_mesh_vertices(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, in
                      int32_t* keys, int64_t cap, int64_t* n_out);
 
 /* Measurement hooks (bench.py).  sc_last_kernel_times fills up to n of
- * {pack_ms, mc_ms, diam3d_pass1_ms, diam3d_refine_ms, planar_ms, h2d_ms} of the
+ * {pack_ms, mc_ms, prune_ms, diam3d_pass1_ms, diam3d_refine_ms, planar_ms, h2d_ms} of the
  * last ROI run on `device` (CUDA events on the launching stream) and returns
  * how many were written.  sc_launch_count is the number of kernels this
  * library has launched in the process.  sc_probe_fp32_peak measures the FP32
  * CUDA-core throughput of `device` in TFLOP/s with a dependent-chain-free
  * FFMA2 (mode 0) or scalar FFMA (mode 1) kernel. */
 int sc_last_kernel_times(int device, double* ms, int n);
+/* Work counters of the last ROI on `device`: {3-D work units evaluated, 3-D
+ * work units total, fp64 re-check candidates, planar tile pairs, planar
+ * re-check candidates}; a unit is 2048 x 256 vertex pairs.  Returns count. */
+int sc_last_diagnostics(int device, int64_t* out, int n);
+/* Process-wide switches (all default 1): "prune" = exact bbox pruning of
+ * 3-D work units; "pass1_packed" = FFMA2 variant of the 3-D pass.  Results
+ * are identical either way; 0 on success, SC_ERR_INPUT for an unknown name. */
+int sc_set_option(const char* name, int value);
 uint64_t sc_launch_count(void);
 int sc_probe_fp32_peak(int device, int mode, double* tflops);
 

@@ -30,6 +30,8 @@ EXPORTED = (
     "sc_diameters",
     "sc_mesh_vertices",
     "sc_last_kernel_times",
+    "sc_last_diagnostics",
+    "sc_set_option",
     "sc_launch_count",
     "sc_probe_fp32_peak",
     "sc_last_error",
@@ -93,6 +95,8 @@ def load():
                                        ctypes.POINTER(i64)]
         L.sc_last_kernel_times.argtypes = [ctypes.c_int, dp, ctypes.c_int]
         L.sc_launch_count.restype = ctypes.c_uint64
+        L.sc_last_diagnostics.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
+        L.sc_set_option.argtypes = [ctypes.c_char_p, ctypes.c_int]
         L.sc_probe_fp32_peak.argtypes = [ctypes.c_int, ctypes.c_int, dp]
         L.sc_last_error.restype = ctypes.c_char_p
         L.sc_abi_version.restype = ctypes.c_int
@@ -127,14 +131,14 @@ def raise_for(rc: int, what: str = "") -> None:
     raise errors.DeviceError(f"{what}: {msg} (code {rc})")
 
 
-KERNEL_TIME_NAMES = ("pack_ms", "mc_ms", "diam3d_pass1_ms", "diam3d_refine_ms", "planar_ms",
-                     "h2d_ms")
+KERNEL_TIME_NAMES = ("pack_ms", "mc_ms", "prune_ms", "diam3d_pass1_ms", "diam3d_refine_ms",
+                     "planar_ms", "h2d_ms")
 
 
 def last_kernel_times(device: int = 0) -> dict:
     """Per-kernel CUDA-event times (ms) of the last ROI on `device`."""
-    buf = (ctypes.c_double * 6)()
-    n = load().sc_last_kernel_times(int(device), buf, 6)
+    buf = (ctypes.c_double * 7)()
+    n = load().sc_last_kernel_times(int(device), buf, 7)
     if n < 0:
         raise_for(-n, "sc_last_kernel_times")
     return {k: buf[i] for i, k in enumerate(KERNEL_TIME_NAMES[:n])}
@@ -150,3 +154,20 @@ def probe_fp32_peak(device: int = 0, mode: int = 0) -> float:
     raise_for(load().sc_probe_fp32_peak(int(device), int(mode), ctypes.byref(out)),
               "sc_probe_fp32_peak")
     return out.value
+
+
+DIAG_NAMES = ("work_units", "total_units", "refine_candidates", "planar_units",
+              "planar_candidates")
+PAIRS_PER_UNIT = 2048 * 256
+
+
+def last_diagnostics(device: int = 0) -> dict:
+    buf = (ctypes.c_int64 * 5)()
+    n = load().sc_last_diagnostics(int(device), buf, 5)
+    if n < 0:
+        raise_for(-n, "sc_last_diagnostics")
+    return {k: int(buf[i]) for i, k in enumerate(DIAG_NAMES[:n])}
+
+
+def set_option(name: str, value: int) -> None:
+    raise_for(load().sc_set_option(name.encode(), int(value)), "sc_set_option")

@@ -107,6 +107,7 @@ template <bool PACKED>
 __global__ void __launch_bounds__(kDiamThreads, 4) diam3d_pass1(const int4* __restrict__ keys,
                                                                 long long cap, Frame f, int shard,
                                                                 int nshards,
+                                                                const unsigned int* __restrict__ work,
                                                                 float* __restrict__ warp_max,
                                                                 Stats* __restrict__ st) {
   __shared__ float4 sj[kChunk];  // (x, y, z, |p|^2)
@@ -114,11 +115,12 @@ __global__ void __launch_bounds__(kDiamThreads, 4) diam3d_pass1(const int4* __re
   if (n == 0) return;
   frame_centre(st, f);
   const long long T = (n + kTile - 1) / kTile;
-  long long u0, u1;
-  shard_span(tri(T) * kChunks, shard, nshards, u0, u1);
+  long long w0, w1;
+  shard_span((long long)st->n_work, shard, nshards, w0, w1);  // surviving units (prune.cu)
   const int warp = threadIdx.x >> 5;
   float run = 0.f;
-  for (long long u = u0 + blockIdx.x; u < u1; u += gridDim.x) {
+  for (long long w = w0 + blockIdx.x; w < w1; w += gridDim.x) {
+    const long long u = work[w];
     const long long item = u / kChunks;
     const int q = (int)(u - item * kChunks);
     int I, J;
@@ -192,8 +194,10 @@ __global__ void __launch_bounds__(kDiamThreads, 4) diam3d_pass1(const int4* __re
   }
   if ((threadIdx.x & 31) == 0) atomic_max_pos_f32(&st->d3_f32, run);
 }
-template __global__ void diam3d_pass1<true>(const int4*, long long, Frame, int, int, float*, Stats*);
-template __global__ void diam3d_pass1<false>(const int4*, long long, Frame, int, int, float*, Stats*);
+template __global__ void diam3d_pass1<true>(const int4*, long long, Frame, int, int,
+                                            const unsigned int*, float*, Stats*);
+template __global__ void diam3d_pass1<false>(const int4*, long long, Frame, int, int,
+                                             const unsigned int*, float*, Stats*);
 
 // Compact the (tile pair, warp) units that may hold the maximum.
 __global__ void diam3d_select(const float* __restrict__ warp_max, long long cap,

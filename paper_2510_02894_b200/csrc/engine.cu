@@ -36,7 +36,15 @@ __global__ void mc_cells(const uint32_t*, int, int, int, int, const CaseTables*,
                          long long);
 __global__ void diam3d_prep(long long, const Stats*, float*);
 template <bool PACKED>
-__global__ void diam3d_pass1(const int4*, long long, Frame, int, int, float*, Stats*);
+__global__ void diam3d_pass1(const int4*, long long, Frame, int, int, const unsigned int*, float*,
+                             Stats*);
+__global__ void sort_hist(const int4*, long long, const Stats*, unsigned int*);
+__global__ void sort_scan(unsigned int*, unsigned int*);
+__global__ void sort_scatter(const int4*, long long, const Stats*, unsigned int*, int4*);
+__global__ void chunk_boxes(const int4*, long long, const Stats*, int4*);
+__global__ void extremes(const int4*, long long, Frame, Stats*);
+__global__ void lower_bound(const int4*, Frame, Stats*);
+__global__ void unit_filter(const int4*, long long, Frame, int, Stats*, unsigned int*);
 __global__ void diam3d_select(const float*, long long, Stats*, unsigned int*);
 __global__ void diam3d_refine(const int4*, long long, Frame, const unsigned int*, Stats*);
 __global__ void plane_hist(const int4*, long long, const Stats*, unsigned int*);
@@ -61,6 +69,7 @@ using namespace sc;
 namespace {
 
 thread_local std::string g_err;
+std::atomic<bool> g_opt_prune{true}, g_opt_packed{true};
 std::atomic<unsigned long long> g_launches{0};
 
 void set_err(const char* fmt, ...) {
@@ -166,15 +175,16 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[6] = {};
   cudaEvent_t kev[8] = {};      // per-kernel boundaries of the last ROI
-  double last_ms[6] = {0, 0, 0, 0, 0, 0};  // pack, mc, pass1, refine, planar, h2d
+  double last_ms[7] = {0, 0, 0, 0, 0, 0, 0};  // pack, mc, prune, pass1, refine, planar, h2d
   long long dcap = 0;  // vertices the diameter-side buffers are sized for
+  long long last_diag[5] = {0, 0, 0, 0, 0};
   int occ_pass1 = 1, occ_pass1s = 1, occ_plane = 1;  // resident blocks/SM (persistent kernels)
-  bool pass1_packed = true;  // FFMA2 variant of diam3d_pass1 (SC_PASS1=scalar selects FFMA)
   Stats* d_stats = nullptr;
   Stats* h_stats = nullptr;  // pinned
   CaseTables* d_tabs = nullptr;
   DevBuf<uint32_t> bits;
-  DevBuf<int4> keys;
+  DevBuf<int4> keys, keys_sorted, boxes;
+  DevBuf<unsigned int> sort_counts, sort_cursor, work;
   DevBuf<float> warp_max, plane_umax;
   DevBuf<unsigned int> cand, plane_cand;
   DevBuf<unsigned int> plane_counts, plane_start, plane_cursor, plane_tstart;
@@ -217,7 +227,8 @@ int get_ctx(int device, Ctx** out) {
     CK(cudaMemcpy(c->d_tabs, &case_geom().tabs, sizeof(CaseTables), cudaMemcpyHostToDevice));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pass1, diam3d_pass1<true>, 256, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pass1s, diam3d_pass1<false>, 256, 0));
-    if (const char* v = getenv("SC_PASS1")) c->pass1_packed = std::strcmp(v, "scalar") != 0;
+    if (const char* v = getenv("SC_PASS1")) g_opt_packed = std::strcmp(v, "scalar") != 0;
+    if (const char* v = getenv("SC_PRUNE")) g_opt_prune = std::strcmp(v, "0") != 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_plane, plane_pass1, 256, 0));
     g_ctx[device] = std::move(c);
   }
@@ -273,6 +284,14 @@ int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, lo
   const long long T = (dcap + kTile - 1) / kTile;
   CK(c->warp_max.ensure((size_t)(T * (T + 1) / 2 * 8)));
   CK(c->cand.ensure((size_t)(T * (T + 1) / 2 * 8)));
+  CK(c->work.ensure((size_t)(T * (T + 1) / 2 * 8)));
+  CK(c->keys_sorted.ensure((size_t)dcap));
+  CK(c->boxes.ensure((size_t)(2 * ((dcap + 255) / 256))));
+  if (c->sort_counts.cap == 0) {
+    CK(c->sort_counts.ensure(1 << 15));
+    CK(cudaMemset(c->sort_counts.p, 0, sizeof(unsigned int) * c->sort_counts.cap));
+    CK(c->sort_cursor.ensure(1 << 15));
+  }
   const long long P = 2 * (nx + ny + nz) + 9;
   CK(c->plane_counts.ensure((size_t)P));
   CK(c->plane_start.ensure((size_t)P + 1));
@@ -336,31 +355,49 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
   // split of work units is also the load balance.
   const int pgrid = c->sms * std::max(1, c->occ_pass1);
   const int plgrid = c->sms * std::max(1, c->occ_plane);
+  // Spatial (Morton brick) order, chunk boxes, exact lower bound, pruning.
+  const int vgrid = c->sms * 4;
+  sort_hist<<<vgrid, 256, 0, s>>>(c->keys.p, dcap, c->d_stats, c->sort_counts.p);
+  CKL(1);
+  sort_scan<<<1, 1024, 0, s>>>(c->sort_counts.p, c->sort_cursor.p);
+  CKL(1);
+  sort_scatter<<<vgrid, 256, 0, s>>>(c->keys.p, dcap, c->d_stats, c->sort_cursor.p,
+                                     c->keys_sorted.p);
+  CKL(1);
+  chunk_boxes<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, c->d_stats, c->boxes.p);
+  CKL(1);
+  extremes<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, f, c->d_stats);
+  CKL(1);
+  lower_bound<<<1, 256, 0, s>>>(c->keys_sorted.p, f, c->d_stats);
+  CKL(1);
   diam3d_prep<<<c->sms * 2, 256, 0, s>>>(dcap, c->d_stats, c->warp_max.p);
   CKL(1);
+  unit_filter<<<c->sms * 4, 256, 0, s>>>(c->boxes.p, dcap, f, g_opt_prune.load() ? 1 : 0, c->d_stats,
+                                         c->work.p);
+  CKL(1);
   CK(cudaEventRecord(c->kev[3], s));
-  if (c->pass1_packed)
-    diam3d_pass1<true><<<pgrid, 256, 0, s>>>(c->keys.p, dcap, f, shard, nshards, c->warp_max.p,
-                                             c->d_stats);
+  if (g_opt_packed.load())
+    diam3d_pass1<true><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, f, shard, nshards,
+                                             c->work.p, c->warp_max.p, c->d_stats);
   else
     diam3d_pass1<false><<<c->sms * std::max(1, c->occ_pass1s), 256, 0, s>>>(
-        c->keys.p, dcap, f, shard, nshards, c->warp_max.p, c->d_stats);
+        c->keys_sorted.p, dcap, f, shard, nshards, c->work.p, c->warp_max.p, c->d_stats);
   CKL(1);
   CK(cudaEventRecord(c->kev[4], s));
   diam3d_select<<<c->sms * 2, 256, 0, s>>>(c->warp_max.p, dcap, c->d_stats, c->cand.p);
   CKL(1);
-  diam3d_refine<<<c->sms * 2, 256, 0, s>>>(c->keys.p, dcap, f, c->cand.p, c->d_stats);
+  diam3d_refine<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, f, c->cand.p, c->d_stats);
   CKL(1);
   CK(cudaEventRecord(c->kev[5], s));
 
   const long long P = 2 * (nx + ny + nz) + 9;
   CK(cudaMemsetAsync(c->plane_counts.p, 0, sizeof(unsigned int) * P, s));
-  plane_hist<<<c->sms * 4, 256, 0, s>>>(c->keys.p, dcap, c->d_stats, c->plane_counts.p);
+  plane_hist<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, dcap, c->d_stats, c->plane_counts.p);
   CKL(1);
   plane_scan<<<1, 1024, 0, s>>>(c->plane_counts.p, c->d_stats, c->plane_start.p,
                                 c->plane_cursor.p, c->plane_tstart.p);
   CKL(1);
-  plane_scatter<<<c->sms * 4, 256, 0, s>>>(c->keys.p, dcap, c->d_stats, c->plane_cursor.p,
+  plane_scatter<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, dcap, c->d_stats, c->plane_cursor.p,
                                            c->plane_sorted.p);
   CKL(1);
   plane_pass1<<<plgrid, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_tstart.p, f,
@@ -444,13 +481,22 @@ int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, c
     return SC_ERR_EMPTY_ROI;
   }
   fill_out(*c->h_stats, sp, out);
-  for (int i = 0; i < 5; i++) c->last_ms[i] = 0.0;
   c->last_ms[0] = ev_ms(c->kev[0], c->kev[1]);
   c->last_ms[1] = ev_ms(c->kev[1], c->kev[2]);
-  c->last_ms[2] = ev_ms(c->kev[3], c->kev[4]);
-  c->last_ms[3] = ev_ms(c->kev[4], c->kev[5]);
-  c->last_ms[4] = ev_ms(c->kev[5], c->kev[6]);
-  c->last_ms[5] = 0.0;
+  c->last_ms[2] = ev_ms(c->kev[2], c->kev[3]);
+  c->last_ms[3] = ev_ms(c->kev[3], c->kev[4]);
+  c->last_ms[4] = ev_ms(c->kev[4], c->kev[5]);
+  c->last_ms[5] = ev_ms(c->kev[5], c->kev[6]);
+  c->last_ms[6] = 0.0;
+  {
+    const Stats& h = *c->h_stats;
+    const long long V = (long long)h.n_vert, T = (V + kTile - 1) / kTile;
+    c->last_diag[0] = (long long)h.n_work;
+    c->last_diag[1] = T * (T + 1) / 2 * 8;
+    c->last_diag[2] = (long long)h.n_cand;
+    c->last_diag[3] = (long long)h.plane_units;
+    c->last_diag[4] = (long long)h.n_pcand;
+  }
   out->mesh_ms = ev_ms(c->kev[0], c->kev[2]);
   out->diameters_ms = ev_ms(c->kev[2], c->kev[6]);
   return SC_OK;
@@ -524,7 +570,7 @@ int sc_calculate_coefficients(const uint8_t* mask, int64_t nx, int64_t ny, int64
   CK(cudaEventRecord(c->ev[1], s));
   rc = run_roi(c, c->mask_stage.p, nx, ny, nz, spacing, s, 0, 1, nullptr, out);
   out->h2d_ms = ev_ms(c->ev[0], c->ev[1]);
-  c->last_ms[5] = out->h2d_ms;
+  c->last_ms[6] = out->h2d_ms;
   out->total_ms = wall_ms() - t0;
   return rc;
 }
@@ -616,12 +662,30 @@ int sc_last_kernel_times(int device, double* ms, int n) {
   int rc = get_ctx(device, &c);
   if (rc) return -rc;
   std::lock_guard<std::mutex> lk(c->mu);
-  int m = n < 6 ? n : 6;
+  int m = n < 7 ? n : 7;
   for (int i = 0; i < m; i++) ms[i] = c->last_ms[i];
   return m;
 }
 
 uint64_t sc_launch_count(void) { return g_launches.load(); }
+
+int sc_last_diagnostics(int device, int64_t* out, int n) {
+  Ctx* c;
+  int rc = get_ctx(device, &c);
+  if (rc) return -rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  int m = n < 5 ? n : 5;
+  for (int i = 0; i < m; i++) out[i] = c->last_diag[i];
+  return m;
+}
+
+int sc_set_option(const char* name, int value) {
+  if (!name) { set_err("NULL option name"); return SC_ERR_INPUT; }
+  if (std::strcmp(name, "prune") == 0) g_opt_prune = value != 0;
+  else if (std::strcmp(name, "pass1_packed") == 0) g_opt_packed = value != 0;
+  else { set_err("unknown option %s", name); return SC_ERR_INPUT; }
+  return SC_OK;
+}
 
 int sc_probe_fp32_peak(int device, int mode, double* tflops) {
   if (!tflops) { set_err("NULL argument"); return SC_ERR_INPUT; }

@@ -22,6 +22,9 @@ struct Stats {
   unsigned long long n_pcand;          // planar tile pairs re-checked in fp64
   unsigned int pl_f32[4];              // fp32 bits of pass-1 planar maxima (xy, xz, yz, -)
   unsigned long long plane_units;      // in-plane tile pairs of the planar pass
+  unsigned long long ext[26];          // packed (projection, index) of 13-direction extremes
+  unsigned long long lb;               // fp64 bits: exact squared distance lower bound
+  unsigned long long n_work;           // surviving 3-D work units after pruning
 };
 
 // Per-case integer tables for the exact volume path: for case k,
