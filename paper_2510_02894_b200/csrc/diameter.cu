@@ -315,46 +315,38 @@ __device__ __forceinline__ unsigned int plane_tiles(unsigned int np) {
 }
 
 // One block of 1024 threads: exclusive scans of the plane populations (start,
-// cursor) and of their tile-pair counts (tstart), P from the bbox.
+// cursor) and of their tile-pair counts (tstart); P from the bbox.  Each
+// thread owns ceil(P/1024) consecutive planes.
 __global__ void __launch_bounds__(1024) plane_scan(const unsigned int* __restrict__ counts,
                                                    Stats* __restrict__ st,
                                                    unsigned int* __restrict__ start,
                                                    unsigned int* __restrict__ cursor,
                                                    unsigned int* __restrict__ tstart) {
-  __shared__ unsigned int s[1024], s2[1024];
-  __shared__ unsigned int carry, carry2;
   if (st->bbox[3] < 0) return;
   const PlaneSpace ps = plane_space(st);
   const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
-  if (threadIdx.x == 0) carry = carry2 = 0;
-  __syncthreads();
-  for (int base = 0; base < P; base += 1024) {
-    const int i = base + threadIdx.x;
-    const unsigned int v = i < P ? counts[i] : 0u;
-    const unsigned int w = plane_tiles(v);
-    s[threadIdx.x] = v;
-    s2[threadIdx.x] = w;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-      const unsigned int t = threadIdx.x >= o ? s[threadIdx.x - o] : 0u;
-      const unsigned int t2 = threadIdx.x >= o ? s2[threadIdx.x - o] : 0u;
-      __syncthreads();
-      s[threadIdx.x] += t;
-      s2[threadIdx.x] += t2;
-      __syncthreads();
-    }
-    if (i < P) {
-      start[i] = cursor[i] = carry + s[threadIdx.x] - v;
-      tstart[i] = carry2 + s2[threadIdx.x] - w;
-    }
-    __syncthreads();
-    if (threadIdx.x == 1023) { carry += s[1023]; carry2 += s2[1023]; }
-    __syncthreads();
+  const int per = (P + 1023) / 1024;
+  const int b = threadIdx.x * per, e = min(P, b + per);
+  unsigned int s1 = 0, s2 = 0;
+  for (int i = b; i < e; i++) {
+    const unsigned int v = counts[i];
+    s1 += v;
+    s2 += plane_tiles(v);
+  }
+  unsigned int t1, t2;
+  unsigned int r1 = block_exscan_1024(s1, &t1);
+  unsigned int r2 = block_exscan_1024(s2, &t2);
+  for (int i = b; i < e; i++) {
+    const unsigned int v = counts[i];
+    start[i] = cursor[i] = r1;
+    tstart[i] = r2;
+    r1 += v;
+    r2 += plane_tiles(v);
   }
   if (threadIdx.x == 0) {
-    start[P] = carry;
-    tstart[P] = carry2;
-    st->plane_units = carry2;
+    start[P] = t1;
+    tstart[P] = t2;
+    st->plane_units = t2;
   }
 }
 

@@ -77,27 +77,29 @@ __global__ void sort_hist(const int4* __restrict__ keys, long long cap,
   }
 }
 
+// 32768 bins, 1024 threads x 32 consecutive bins each: one pass.
 __global__ void __launch_bounds__(1024) sort_scan(unsigned int* __restrict__ counts,
                                                   unsigned int* __restrict__ cursor) {
-  __shared__ unsigned int sm[1024];
-  __shared__ unsigned int carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < kSortBins; base += 1024) {
-    const unsigned int v = counts[base + threadIdx.x];
-    sm[threadIdx.x] = v;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-      const unsigned int t = threadIdx.x >= o ? sm[threadIdx.x - o] : 0u;
-      __syncthreads();
-      sm[threadIdx.x] += t;
-      __syncthreads();
-    }
-    cursor[base + threadIdx.x] = carry + sm[threadIdx.x] - v;
-    counts[base + threadIdx.x] = 0u;  // leave the histogram zeroed for the next ROI
-    __syncthreads();
-    if (threadIdx.x == 1023) carry += sm[1023];
-    __syncthreads();
+  uint4* c4 = reinterpret_cast<uint4*>(counts) + threadIdx.x * 8;
+  uint4* o4 = reinterpret_cast<uint4*>(cursor) + threadIdx.x * 8;
+  uint4 v[8];
+  unsigned int sum = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    v[k] = c4[k];
+    sum += v[k].x + v[k].y + v[k].z + v[k].w;
+  }
+  unsigned int total;
+  unsigned int run = block_exscan_1024(sum, &total);
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    uint4 o;
+    o.x = run; run += v[k].x;
+    o.y = run; run += v[k].y;
+    o.z = run; run += v[k].z;
+    o.w = run; run += v[k].w;
+    o4[k] = o;
+    c4[k] = make_uint4(0, 0, 0, 0);  // leave the histogram zeroed for the next ROI
   }
 }
 

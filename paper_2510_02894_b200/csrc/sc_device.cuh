@@ -49,6 +49,36 @@ struct PlaneSpace {
   int cnt[3];
 };
 
+// Exclusive scan of one value per thread across a 1024-thread block (warp
+// shuffles, two levels, 2 barriers).  Returns the exclusive prefix; *total
+// receives the block sum.  Must be called by all 1024 threads.
+__device__ __forceinline__ unsigned int block_exscan_1024(unsigned int v, unsigned int* total) {
+  __shared__ unsigned int wsum[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned int t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned int y = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned int t = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += t;
+    }
+    wsum[lane] = y;
+  }
+  __syncthreads();
+  const unsigned int excl = x - v + (wid ? wsum[wid - 1] : 0u);
+  *total = wsum[31];
+  __syncthreads();  // wsum reusable after return
+  return excl;
+}
+
 // fp32 (non-negative) max through the unsigned bit pattern.
 __device__ __forceinline__ void atomic_max_pos_f32(unsigned int* addr, float v) {
   atomicMax(addr, __float_as_uint(v));

@@ -214,3 +214,26 @@ def test_repeat_calls_deterministic(sc, cuda_device):
     b = sc.calculate_coefficients(arr, (0.5, 0.5, 5.0))
     assert a.to_dict() == b.to_dict()
     assert (a.triangle_count, a.active_cubes) == (b.triangle_count, b.active_cubes)
+
+
+def test_pruning_and_pass1_variants_identical(sc, golden, golden_arrays, cuda_device):
+    """Work pruning and the FFMA/FFMA2 pass-1 variants never change a result."""
+    from paper_2510_02894_b200 import _native, synth
+
+    cases = [(golden_arrays[c["mask_key"]], c["spacing"]) for c in golden["cases"]]
+    cases.append((synth.thin_slab(), (0.5, 0.5, 5.0)))
+    cases.append((synth.kits_like(tumor_mm=60.0), (0.8, 0.8, 1.0)))
+    base = [sc.calculate_coefficients(a, sp).to_dict() for a, sp in cases]
+    try:
+        for opt, val in (("prune", 0), ("pass1_packed", 0)):
+            _native.set_option(opt, val)
+            for (a, sp), want in zip(cases, base):
+                assert sc.calculate_coefficients(a, sp).to_dict() == want, opt
+            _native.set_option(opt, 1)
+    finally:
+        _native.set_option("prune", 1)
+        _native.set_option("pass1_packed", 1)
+    _native.set_option("prune", 1)
+    sc.calculate_coefficients(cases[-1][0], cases[-1][1])
+    d = _native.last_diagnostics(cuda_device)
+    assert 0 < d["work_units"] < d["total_units"]  # the KiTS-like ROI actually prunes
