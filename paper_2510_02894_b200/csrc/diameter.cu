@@ -87,14 +87,22 @@ __device__ __forceinline__ void shard_span(long long n, int shard, int nshards, 
 
 __device__ __forceinline__ long long tri(long long T) { return T * (T + 1) / 2; }
 
-// Zero the per-(tile pair, warp) maxima of this ROI (size known on device only).
-__global__ void diam3d_prep(long long cap, const Stats* __restrict__ st,
-                            float* __restrict__ warp_max) {
-  const long long n = n_vertices(st, cap);
-  const long long units = tri((n + kTile - 1) / kTile) * kWarps;
-  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < units;
-       u += (long long)gridDim.x * blockDim.x)
-    warp_max[u] = 0.f;
+// Compact the units whose pass-1 maximum can hold the exact maximum
+// (one block; called by the last block of the pass-1 grid).
+__device__ __forceinline__ void select_units(const float* __restrict__ umax, long long units,
+                                             Stats* __restrict__ st, unsigned int* __restrict__ cand) {
+  const float tau = __uint_as_float(__ldcg(&st->d3_f32)) * (1.f - kRefineRel);
+  const int lane = threadIdx.x & 31;
+  for (long long base = 0; base < units; base += blockDim.x) {
+    const long long u = base + threadIdx.x;
+    const bool hit = u < units && __ldcg(umax + u) >= tau;
+    const unsigned int mask = __ballot_sync(0xffffffffu, hit);
+    if (!mask) continue;
+    unsigned long long pos = 0;
+    if (lane == 0) pos = atomicAdd(&st->n_cand, (unsigned long long)__popc(mask));
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (hit) cand[pos + __popc(mask & ((1u << lane) - 1))] = (unsigned int)u;
+  }
 }
 
 // Pass 1 (see header).  Error of the dot form: in the bbox-centred frame
@@ -109,6 +117,7 @@ __global__ void __launch_bounds__(kDiamThreads, 4) diam3d_pass1(const int4* __re
                                                                 int nshards,
                                                                 const unsigned int* __restrict__ work,
                                                                 float* __restrict__ warp_max,
+                                                                unsigned int* __restrict__ cand,
                                                                 Stats* __restrict__ st) {
   __shared__ float4 sj[kChunk];  // (x, y, z, |p|^2)
   const long long n = n_vertices(st, cap);
@@ -193,31 +202,14 @@ __global__ void __launch_bounds__(kDiamThreads, 4) diam3d_pass1(const int4* __re
     run = fmaxf(run, best);
   }
   if ((threadIdx.x & 31) == 0) atomic_max_pos_f32(&st->d3_f32, run);
+  // The last block to finish compacts the (tile pair, warp) units within
+  // kRefineRel of the global pass-1 maximum for the exact re-check.
+  if (last_block(&st->done1)) select_units(warp_max, tri(T) * kWarps, st, cand);
 }
 template __global__ void diam3d_pass1<true>(const int4*, long long, Frame, int, int,
-                                            const unsigned int*, float*, Stats*);
+                                            const unsigned int*, float*, unsigned int*, Stats*);
 template __global__ void diam3d_pass1<false>(const int4*, long long, Frame, int, int,
-                                             const unsigned int*, float*, Stats*);
-
-// Compact the (tile pair, warp) units that may hold the maximum.
-__global__ void diam3d_select(const float* __restrict__ warp_max, long long cap,
-                              Stats* __restrict__ st, unsigned int* __restrict__ cand) {
-  const long long n = n_vertices(st, cap);
-  const long long units = tri((n + kTile - 1) / kTile) * kWarps;
-  const float tau = __uint_as_float(st->d3_f32) * (1.f - kRefineRel);
-  for (long long base = (long long)blockIdx.x * blockDim.x; base < units;
-       base += (long long)gridDim.x * blockDim.x) {
-    const long long u = base + threadIdx.x;
-    const bool hit = u < units && warp_max[u] >= tau;
-    const unsigned int mask = __ballot_sync(0xffffffffu, hit);
-    if (!mask) continue;
-    const int lane = threadIdx.x & 31;
-    unsigned long long pos = 0;
-    if (lane == 0) pos = atomicAdd(&st->n_cand, (unsigned long long)__popc(mask));
-    pos = __shfl_sync(0xffffffffu, pos, 0);
-    if (hit) cand[pos + __popc(mask & ((1u << lane) - 1))] = (unsigned int)u;
-  }
-}
+                                             const unsigned int*, float*, unsigned int*, Stats*);
 
 // Exact re-check: a selected warp's 32*kR i rows against its J tile in fp64
 // with the reference arithmetic on the reference coordinates.  Work unit =
@@ -266,126 +258,10 @@ __global__ void __launch_bounds__(kDiamThreads) diam3d_refine(const int4* __rest
 constexpr int kPT = 256;  // planar tile edge (threads per block)
 
 __device__ __forceinline__ PlaneSpace plane_space(const Stats* st) {
-  PlaneSpace ps;
-  const int* bb = st->bbox;
-  ps.lo[0] = 2 * bb[2] - 1; ps.cnt[0] = 2 * (bb[5] - bb[2]) + 3;
-  ps.lo[1] = 2 * bb[1] - 1; ps.cnt[1] = 2 * (bb[4] - bb[1]) + 3;
-  ps.lo[2] = 2 * bb[0] - 1; ps.cnt[2] = 2 * (bb[3] - bb[0]) + 3;
-  return ps;
-}
-
-__device__ __forceinline__ void plane_ids(int4 k, const PlaneSpace& ps, int out[3]) {
-  out[0] = k.z - ps.lo[0];
-  out[1] = ps.cnt[0] + (k.y - ps.lo[1]);
-  out[2] = ps.cnt[0] + ps.cnt[1] + (k.x - ps.lo[2]);
-}
-
-// Warp-aggregated increment: lanes with equal `id` (vertices of one plane are
-// emitted together by the MC warps) share one global atomic.  Returns this
-// lane's slot within its group's reservation.
-__device__ __forceinline__ unsigned int group_add(unsigned int* base, int id, bool ok) {
-  const int lane = threadIdx.x & 31;
-  const unsigned int peers = __match_any_sync(0xffffffffu, ok ? id : -1 - lane);
-  const int leader = __ffs(peers) - 1;
-  unsigned int pos = 0;
-  if (ok && lane == leader) pos = atomicAdd(base + id, (unsigned int)__popc(peers));
-  pos = __shfl_sync(0xffffffffu, pos, leader);
-  return pos + __popc(peers & ((1u << lane) - 1));
-}
-
-__global__ void plane_hist(const int4* __restrict__ keys, long long cap,
-                           const Stats* __restrict__ st, unsigned int* __restrict__ counts) {
-  const long long n = n_vertices(st, cap);
-  const PlaneSpace ps = plane_space(st);
-  for (long long base = (long long)blockIdx.x * blockDim.x; base < n;
-       base += (long long)gridDim.x * blockDim.x) {
-    const long long v = base + threadIdx.x;
-    const bool ok = v < n;
-    int id[3] = {0, 0, 0};
-    if (ok) plane_ids(keys[v], ps, id);
+  int bb[6];
 #pragma unroll
-    for (int a = 0; a < 3; a++) group_add(counts, id[a], ok);
-  }
-}
-
-__device__ __forceinline__ unsigned int plane_tiles(unsigned int np) {
-  if (np < 2) return 0u;
-  const unsigned int t = (np + kPT - 1) / kPT;
-  return t * (t + 1) / 2;
-}
-
-// One block of 1024 threads: exclusive scans of the plane populations (start,
-// cursor) and of their tile-pair counts (tstart); P from the bbox.  Each
-// thread owns ceil(P/1024) consecutive planes.
-__global__ void __launch_bounds__(1024) plane_scan(const unsigned int* __restrict__ counts,
-                                                   Stats* __restrict__ st,
-                                                   unsigned int* __restrict__ start,
-                                                   unsigned int* __restrict__ cursor,
-                                                   unsigned int* __restrict__ tstart) {
-  if (st->bbox[3] < 0) return;
-  const PlaneSpace ps = plane_space(st);
-  const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
-  const int per = (P + 1023) / 1024;
-  const int b = threadIdx.x * per, e = min(P, b + per);
-  unsigned int s1 = 0, s2 = 0;
-  for (int i = b; i < e; i++) {
-    const unsigned int v = counts[i];
-    s1 += v;
-    s2 += plane_tiles(v);
-  }
-  unsigned int t1, t2;
-  unsigned int r1 = block_exscan_1024(s1, &t1);
-  unsigned int r2 = block_exscan_1024(s2, &t2);
-  for (int i = b; i < e; i++) {
-    const unsigned int v = counts[i];
-    start[i] = cursor[i] = r1;
-    tstart[i] = r2;
-    r1 += v;
-    r2 += plane_tiles(v);
-  }
-  if (threadIdx.x == 0) {
-    start[P] = t1;
-    tstart[P] = t2;
-    st->plane_units = t2;
-  }
-}
-
-__global__ void plane_scatter(const int4* __restrict__ keys, long long cap,
-                              const Stats* __restrict__ st, unsigned int* __restrict__ cursor,
-                              int2* __restrict__ sorted) {
-  const long long n = n_vertices(st, cap);
-  const PlaneSpace ps = plane_space(st);
-  for (long long base = (long long)blockIdx.x * blockDim.x; base < n;
-       base += (long long)gridDim.x * blockDim.x) {
-    const long long v = base + threadIdx.x;
-    const bool ok = v < n;
-    int4 k = make_int4(0, 0, 0, 0);
-    int id[3] = {0, 0, 0};
-    if (ok) {
-      k = keys[v];
-      plane_ids(k, ps, id);
-    }
-    const unsigned int p0 = group_add(cursor, id[0], ok);  // XY: (X, Y)
-    const unsigned int p1 = group_add(cursor, id[1], ok);  // XZ: (X, Z)
-    const unsigned int p2 = group_add(cursor, id[2], ok);  // YZ: (Y, Z)
-    if (ok) {
-      sorted[p0] = make_int2(k.x, k.y);
-      sorted[p1] = make_int2(k.x, k.z);
-      sorted[p2] = make_int2(k.y, k.z);
-    }
-  }
-}
-
-// Planar work unit u (global tile-pair index over all planes) -> plane p and
-// its in-plane tile pair (I, J); binary search over tstart.
-__device__ __forceinline__ int plane_of_unit(const unsigned int* __restrict__ tstart, int P,
-                                             unsigned int u) {
-  int lo = 0, hi = P;  // tstart[lo] <= u < tstart[hi]
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (tstart[mid] <= u) lo = mid; else hi = mid;
-  }
-  return lo;
+  for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
+  return plane_space(bb);
 }
 
 struct PlaneAxes {  // in-plane (a, b) coordinate frame of one plane family
@@ -407,24 +283,32 @@ __device__ __forceinline__ PlaneAxes plane_axes(int axis, const Stats* st, const
   return x;
 }
 
-// Planar pass 1: fp32 dot form over every in-plane tile pair (256 x 256), one
-// maximum per unit; per-axis maxima in st->pl_f32[axis].
+__device__ __forceinline__ int plane_axis(int p, const PlaneSpace& ps) {
+  return p < ps.cnt[0] ? 0 : (p < ps.cnt[0] + ps.cnt[1] ? 1 : 2);
+}
+
+// Planar pass 1: fp32 dot form over every in-plane tile pair (kPT x kPT), one
+// maximum per unit; per-axis maxima in st->pl_f32[axis].  umap[u] is the plane
+// of unit u (scan_all).  The last block compacts the re-check candidates.
 __global__ void __launch_bounds__(kPT) plane_pass1(const int2* __restrict__ sorted,
                                                    const unsigned int* __restrict__ start,
                                                    const unsigned int* __restrict__ tstart,
+                                                   const unsigned int* __restrict__ umap,
                                                    Frame f, int shard, int nshards,
                                                    long long ucap, float* __restrict__ umax,
+                                                   unsigned int* __restrict__ cand,
                                                    Stats* __restrict__ st) {
   __shared__ float4 sj[kPT];  // (a, b, |p|^2, -)
   __shared__ float s_red[kPT / 32];
-  if (st->bbox[3] < 0 || (long long)st->plane_units > ucap) return;  // host re-runs bigger
+  const long long units = (long long)st->plane_units;
+  if (st->bbox[3] < 0 || units > ucap) return;  // host re-runs with room
   const PlaneSpace ps = plane_space(st);
-  const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
   long long u0, u1;
-  shard_span(tstart[P], shard, nshards, u0, u1);
+  shard_span(units, shard, nshards, u0, u1);
+  float run0 = 0.f, run1 = 0.f, run2 = 0.f;  // per-axis maxima (registers, not an array)
   for (long long u = u0 + blockIdx.x; u < u1; u += gridDim.x) {
-    const int p = plane_of_unit(tstart, P, (unsigned int)u);
-    const int axis = p < ps.cnt[0] ? 0 : (p < ps.cnt[0] + ps.cnt[1] ? 1 : 2);
+    const int p = (int)umap[u];
+    const int axis = plane_axis(p, ps);
     const PlaneAxes ax = plane_axes(axis, st, f);
     const unsigned int b0 = start[p], np = start[p + 1] - b0;
     int I, J;
@@ -459,36 +343,31 @@ __global__ void __launch_bounds__(kPT) plane_pass1(const int2* __restrict__ sort
     if (threadIdx.x == 0) {
       for (int w = 1; w < kPT / 32; w++) best = fmaxf(best, s_red[w]);
       umax[u] = best;
-      atomic_max_pos_f32(&st->pl_f32[axis], best);
+      if (axis == 0) run0 = fmaxf(run0, best);
+      else if (axis == 1) run1 = fmaxf(run1, best);
+      else run2 = fmaxf(run2, best);
     }
   }
-}
-
-__global__ void plane_select(const unsigned int* __restrict__ start,
-                             const unsigned int* __restrict__ tstart,
-                             const float* __restrict__ umax, int shard, int nshards,
-                             long long ucap, Stats* __restrict__ st,
-                             unsigned int* __restrict__ cand) {
-  if (st->bbox[3] < 0 || (long long)st->plane_units > ucap) return;
-  const PlaneSpace ps = plane_space(st);
-  const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
-  const float tau[3] = {__uint_as_float(st->pl_f32[0]) * (1.f - kRefineRel),
-                        __uint_as_float(st->pl_f32[1]) * (1.f - kRefineRel),
-                        __uint_as_float(st->pl_f32[2]) * (1.f - kRefineRel)};
-  long long u0, u1;
-  shard_span(tstart[P], shard, nshards, u0, u1);
-  for (long long base = u0 + (long long)blockIdx.x * blockDim.x; base < u1;
-       base += (long long)gridDim.x * blockDim.x) {
+  if (threadIdx.x == 0) {
+    if (run0 > 0.f) atomic_max_pos_f32(&st->pl_f32[0], run0);
+    if (run1 > 0.f) atomic_max_pos_f32(&st->pl_f32[1], run1);
+    if (run2 > 0.f) atomic_max_pos_f32(&st->pl_f32[2], run2);
+  }
+  if (!last_block(&st->done2)) return;
+  // Last block: candidates within kRefineRel of their axis maximum.
+  const float tau0 = __uint_as_float(__ldcg(&st->pl_f32[0])) * (1.f - kRefineRel);
+  const float tau1 = __uint_as_float(__ldcg(&st->pl_f32[1])) * (1.f - kRefineRel);
+  const float tau2 = __uint_as_float(__ldcg(&st->pl_f32[2])) * (1.f - kRefineRel);
+  const int lane = threadIdx.x & 31;
+  for (long long base = u0; base < u1; base += blockDim.x) {
     const long long u = base + threadIdx.x;
     bool hit = false;
     if (u < u1) {
-      const int p = plane_of_unit(tstart, P, (unsigned int)u);
-      const int axis = p < ps.cnt[0] ? 0 : (p < ps.cnt[0] + ps.cnt[1] ? 1 : 2);
-      hit = umax[u] >= tau[axis];
+      const int a = plane_axis((int)umap[u], ps);
+      hit = __ldcg(umax + u) >= (a == 0 ? tau0 : (a == 1 ? tau1 : tau2));
     }
     const unsigned int mask = __ballot_sync(0xffffffffu, hit);
     if (!mask) continue;
-    const int lane = threadIdx.x & 31;
     unsigned long long pos = 0;
     if (lane == 0) pos = atomicAdd(&st->n_pcand, (unsigned long long)__popc(mask));
     pos = __shfl_sync(0xffffffffu, pos, 0);
@@ -502,18 +381,18 @@ __global__ void plane_select(const unsigned int* __restrict__ start,
 __global__ void __launch_bounds__(kPT) plane_refine(const int2* __restrict__ sorted,
                                                     const unsigned int* __restrict__ start,
                                                     const unsigned int* __restrict__ tstart,
+                                                    const unsigned int* __restrict__ umap,
                                                     Frame f, const unsigned int* __restrict__ cand,
                                                     Stats* __restrict__ st) {
   __shared__ double sa[kPT], sb[kPT];
   __shared__ double s_red[kPT / 32];
   if (st->bbox[3] < 0) return;
   const PlaneSpace ps = plane_space(st);
-  const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
   const long long nc = (long long)st->n_pcand;
   for (long long c = blockIdx.x; c < nc; c += gridDim.x) {
     const unsigned int u = cand[c];
-    const int p = plane_of_unit(tstart, P, u);
-    const int axis = p < ps.cnt[0] ? 0 : (p < ps.cnt[0] + ps.cnt[1] ? 1 : 2);
+    const int p = (int)umap[u];
+    const int axis = plane_axis(p, ps);
     const PlaneAxes ax = plane_axes(axis, st, f);
     const unsigned int b0 = start[p], np = start[p + 1] - b0;
     int I, J;

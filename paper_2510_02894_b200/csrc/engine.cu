@@ -33,30 +33,23 @@ template <int U>
 __global__ void pack_bits_v16(const uint4*, uint32_t*, long long, int, int, Stats*);
 __global__ void pack_bits_generic(const uint8_t*, uint32_t*, long long, int, int, int, Stats*);
 __global__ void mc_cells(const uint32_t*, int, int, int, int, const CaseTables*, Stats*, int4*,
-                         long long);
-__global__ void diam3d_prep(long long, const Stats*, float*);
+                         long long, unsigned int*, unsigned int*);
+__global__ void scan_all(unsigned int*, unsigned int*, unsigned int*, unsigned int*, unsigned int*,
+                         unsigned int*, unsigned int*, long long, int, Stats*);
+__global__ void scatter_all(const int4*, long long, const Stats*, unsigned int*, int4*,
+                            unsigned int*, int2*);
+__global__ void boxes_extremes(const int4*, long long, Frame, Stats*, int4*);
+__global__ void unit_filter(const int4*, const int4*, long long, Frame, int, Stats*, float*,
+                            unsigned int*);
 template <bool PACKED>
 __global__ void diam3d_pass1(const int4*, long long, Frame, int, int, const unsigned int*, float*,
-                             Stats*);
-__global__ void sort_hist(const int4*, long long, const Stats*, unsigned int*);
-__global__ void sort_scan(unsigned int*, unsigned int*);
-__global__ void sort_scatter(const int4*, long long, const Stats*, unsigned int*, int4*);
-__global__ void chunk_boxes(const int4*, long long, const Stats*, int4*);
-__global__ void extremes(const int4*, long long, Frame, Stats*);
-__global__ void lower_bound(const int4*, Frame, Stats*);
-__global__ void unit_filter(const int4*, long long, Frame, int, Stats*, unsigned int*);
-__global__ void diam3d_select(const float*, long long, Stats*, unsigned int*);
+                             unsigned int*, Stats*);
 __global__ void diam3d_refine(const int4*, long long, Frame, const unsigned int*, Stats*);
-__global__ void plane_hist(const int4*, long long, const Stats*, unsigned int*);
-__global__ void plane_scan(const unsigned int*, Stats*, unsigned int*, unsigned int*,
-                           unsigned int*);
-__global__ void plane_scatter(const int4*, long long, const Stats*, unsigned int*, int2*);
-__global__ void plane_pass1(const int2*, const unsigned int*, const unsigned int*, Frame, int, int,
-                            long long, float*, Stats*);
-__global__ void plane_select(const unsigned int*, const unsigned int*, const float*, int, int,
-                             long long, Stats*, unsigned int*);
-__global__ void plane_refine(const int2*, const unsigned int*, const unsigned int*, Frame,
-                             const unsigned int*, Stats*);
+__global__ void plane_pass1(const int2*, const unsigned int*, const unsigned int*,
+                            const unsigned int*, Frame, int, int, long long, float*, unsigned int*,
+                            Stats*);
+__global__ void plane_refine(const int2*, const unsigned int*, const unsigned int*,
+                             const unsigned int*, Frame, const unsigned int*, Stats*);
 __global__ void cloud_diameters(const double*, const double*, const double*, long long, int,
                                 unsigned long long*);
 template <int MODE>
@@ -68,6 +61,7 @@ using namespace sc;
 
 namespace {
 
+constexpr int kMcPlaneSmem = 160 * 1024;  // mc_cells plane histogram (dynamic smem) limit
 thread_local std::string g_err;
 std::atomic<bool> g_opt_prune{true}, g_opt_packed{true};
 std::atomic<unsigned long long> g_launches{0};
@@ -186,7 +180,7 @@ struct Ctx {
   DevBuf<int4> keys, keys_sorted, boxes;
   DevBuf<unsigned int> sort_counts, sort_cursor, work;
   DevBuf<float> warp_max, plane_umax;
-  DevBuf<unsigned int> cand, plane_cand;
+  DevBuf<unsigned int> cand, plane_cand, plane_umap;
   DevBuf<unsigned int> plane_counts, plane_start, plane_cursor, plane_tstart;
   DevBuf<int2> plane_sorted;
   DevBuf<uint8_t> mask_stage;
@@ -230,6 +224,7 @@ int get_ctx(int device, Ctx** out) {
     if (const char* v = getenv("SC_PASS1")) g_opt_packed = std::strcmp(v, "scalar") != 0;
     if (const char* v = getenv("SC_PRUNE")) g_opt_prune = std::strcmp(v, "0") != 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_plane, plane_pass1, 256, 0));
+    CK(cudaFuncSetAttribute(mc_cells, cudaFuncAttributeMaxDynamicSharedMemorySize, kMcPlaneSmem));
     g_ctx[device] = std::move(c);
   }
   *out = g_ctx[device].get();
@@ -241,6 +236,12 @@ int check_input(const void* mask, int64_t nx, int64_t ny, int64_t nz, const doub
   if (nx < 1 || ny < 1 || nz < 1) {
     set_err("dims must all be >= 1, got (%lld, %lld, %lld)", (long long)nx, (long long)ny,
             (long long)nz);
+    return SC_ERR_INPUT;
+  }
+  // mc_cells keeps one plane counter per doubled key in shared memory.
+  if ((2 * (nx + ny + nz) + 9) * 4 > 160 * 1024) {
+    set_err("dims (%lld, %lld, %lld): nx+ny+nz too large for the planar histogram",
+            (long long)nx, (long long)ny, (long long)nz);
     return SC_ERR_INPUT;
   }
   // Doubled lattice keys and fp32 frame coordinates must stay exact.
@@ -287,13 +288,20 @@ int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, lo
   CK(c->work.ensure((size_t)(T * (T + 1) / 2 * 8)));
   CK(c->keys_sorted.ensure((size_t)dcap));
   CK(c->boxes.ensure((size_t)(2 * ((dcap + 255) / 256))));
-  if (c->sort_counts.cap == 0) {
-    CK(c->sort_counts.ensure(1 << 15));
-    CK(cudaMemset(c->sort_counts.p, 0, sizeof(unsigned int) * c->sort_counts.cap));
-    CK(c->sort_cursor.ensure(1 << 15));
+  {
+    unsigned int* before = c->sort_counts.p;
+    CK(c->sort_counts.ensure(kSortBins));
+    CK(c->sort_cursor.ensure(kSortBins));
+    if (c->sort_counts.p != before)  // histograms are self-cleaning after the first zeroing
+      CK(cudaMemset(c->sort_counts.p, 0, sizeof(unsigned int) * c->sort_counts.cap));
   }
   const long long P = 2 * (nx + ny + nz) + 9;
-  CK(c->plane_counts.ensure((size_t)P));
+  {
+    unsigned int* before = c->plane_counts.p;
+    CK(c->plane_counts.ensure((size_t)P));
+    if (c->plane_counts.p != before)
+      CK(cudaMemset(c->plane_counts.p, 0, sizeof(unsigned int) * c->plane_counts.cap));
+  }
   CK(c->plane_start.ensure((size_t)P + 1));
   CK(c->plane_cursor.ensure((size_t)P));
   CK(c->plane_tstart.ensure((size_t)P + 1));
@@ -305,6 +313,7 @@ int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, lo
   const long long pu = std::max(std::min(t * (t + 1) / 2, t * 64) + P + 1, punits);
   CK(c->plane_umax.ensure((size_t)pu));
   CK(c->plane_cand.ensure((size_t)pu));
+  CK(c->plane_umap.ensure((size_t)pu));
   return SC_OK;
 }
 
@@ -338,8 +347,13 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
   }
   CKL(1);
   CK(cudaEventRecord(c->kev[1], s));
-  mc_cells<<<c->sms * 4, 256, 0, s>>>(c->bits.p, (int)nx, (int)ny, (int)nz, W, c->d_tabs,
-                                      c->d_stats, c->keys.p, cap);
+  const long long Pmax = 2 * (nx + ny + nz) + 9;
+  int mc_occ = 1;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mc_occ, mc_cells, 256,
+                                                   Pmax * sizeof(unsigned int)));
+  mc_cells<<<c->sms * std::max(1, mc_occ), 256, Pmax * sizeof(unsigned int), s>>>(
+      c->bits.p, (int)nx, (int)ny, (int)nz, W, c->d_tabs, c->d_stats, c->keys.p, cap,
+      c->sort_counts.p, c->plane_counts.p);
   CKL(1);
   CK(cudaEventRecord(c->kev[2], s));
 
@@ -353,63 +367,43 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
   f.sz = sp[2];
   // Persistent grids: exactly the resident blocks, so the static round-robin
   // split of work units is also the load balance.
-  const int pgrid = c->sms * std::max(1, c->occ_pass1);
+  const int pgrid = c->sms * std::max(1, g_opt_packed.load() ? c->occ_pass1 : c->occ_pass1s);
   const int plgrid = c->sms * std::max(1, c->occ_plane);
-  // Spatial (Morton brick) order, chunk boxes, exact lower bound, pruning.
-  const int vgrid = c->sms * 4;
-  sort_hist<<<vgrid, 256, 0, s>>>(c->keys.p, dcap, c->d_stats, c->sort_counts.p);
+  const long long pucap = (long long)c->plane_umax.cap;
+
+  // Orders (Morton bricks, planes), chunk boxes + extremes, exact LB + pruning.
+  scan_all<<<2, 1024, 0, s>>>(c->sort_counts.p, c->sort_cursor.p, c->plane_counts.p,
+                              c->plane_start.p, c->plane_cursor.p, c->plane_tstart.p,
+                              c->plane_umap.p, pucap, 256, c->d_stats);
   CKL(1);
-  sort_scan<<<1, 1024, 0, s>>>(c->sort_counts.p, c->sort_cursor.p);
+  scatter_all<<<c->sms * 4, 256, 0, s>>>(c->keys.p, dcap, c->d_stats, c->sort_cursor.p,
+                                         c->keys_sorted.p, c->plane_cursor.p, c->plane_sorted.p);
   CKL(1);
-  sort_scatter<<<vgrid, 256, 0, s>>>(c->keys.p, dcap, c->d_stats, c->sort_cursor.p,
-                                     c->keys_sorted.p);
+  boxes_extremes<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, f, c->d_stats, c->boxes.p);
   CKL(1);
-  chunk_boxes<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, c->d_stats, c->boxes.p);
-  CKL(1);
-  extremes<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, f, c->d_stats);
-  CKL(1);
-  lower_bound<<<1, 256, 0, s>>>(c->keys_sorted.p, f, c->d_stats);
-  CKL(1);
-  diam3d_prep<<<c->sms * 2, 256, 0, s>>>(dcap, c->d_stats, c->warp_max.p);
-  CKL(1);
-  unit_filter<<<c->sms * 4, 256, 0, s>>>(c->boxes.p, dcap, f, g_opt_prune.load() ? 1 : 0, c->d_stats,
+  unit_filter<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, c->boxes.p, dcap, f,
+                                         g_opt_prune.load() ? 1 : 0, c->d_stats, c->warp_max.p,
                                          c->work.p);
   CKL(1);
   CK(cudaEventRecord(c->kev[3], s));
   if (g_opt_packed.load())
     diam3d_pass1<true><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, f, shard, nshards,
-                                             c->work.p, c->warp_max.p, c->d_stats);
+                                             c->work.p, c->warp_max.p, c->cand.p, c->d_stats);
   else
-    diam3d_pass1<false><<<c->sms * std::max(1, c->occ_pass1s), 256, 0, s>>>(
-        c->keys_sorted.p, dcap, f, shard, nshards, c->work.p, c->warp_max.p, c->d_stats);
+    diam3d_pass1<false><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, f, shard, nshards,
+                                              c->work.p, c->warp_max.p, c->cand.p, c->d_stats);
   CKL(1);
   CK(cudaEventRecord(c->kev[4], s));
-  diam3d_select<<<c->sms * 2, 256, 0, s>>>(c->warp_max.p, dcap, c->d_stats, c->cand.p);
-  CKL(1);
   diam3d_refine<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, f, c->cand.p, c->d_stats);
   CKL(1);
   CK(cudaEventRecord(c->kev[5], s));
-
-  const long long P = 2 * (nx + ny + nz) + 9;
-  CK(cudaMemsetAsync(c->plane_counts.p, 0, sizeof(unsigned int) * P, s));
-  plane_hist<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, dcap, c->d_stats, c->plane_counts.p);
-  CKL(1);
-  plane_scan<<<1, 1024, 0, s>>>(c->plane_counts.p, c->d_stats, c->plane_start.p,
-                                c->plane_cursor.p, c->plane_tstart.p);
-  CKL(1);
-  plane_scatter<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, dcap, c->d_stats, c->plane_cursor.p,
-                                           c->plane_sorted.p);
-  CKL(1);
-  plane_pass1<<<plgrid, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_tstart.p, f,
-                                    shard, nshards, (long long)c->plane_umax.cap, c->plane_umax.p,
-                                    c->d_stats);
-  CKL(1);
-  plane_select<<<c->sms * 2, 256, 0, s>>>(c->plane_start.p, c->plane_tstart.p, c->plane_umax.p,
-                                          shard, nshards, (long long)c->plane_umax.cap, c->d_stats,
-                                          c->plane_cand.p);
+  plane_pass1<<<plgrid, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_tstart.p,
+                                     c->plane_umap.p, f, shard, nshards, pucap, c->plane_umax.p,
+                                     c->plane_cand.p, c->d_stats);
   CKL(1);
   plane_refine<<<c->sms * 2, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p,
-                                          c->plane_tstart.p, f, c->plane_cand.p, c->d_stats);
+                                          c->plane_tstart.p, c->plane_umap.p, f,
+                                          c->plane_cand.p, c->d_stats);
   CKL(1);
   CK(cudaEventRecord(c->kev[6], s));
   return SC_OK;

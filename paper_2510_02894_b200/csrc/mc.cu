@@ -180,20 +180,35 @@ __device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits, int
 // (reference padded cell index minus 1).  The thread owns cells and lattice
 // points u = 32q - 1 + i, i in [0, 31].  All 2*(kZChunk+1) row words are
 // loaded up front (L2-resident bit volume; latency, not bandwidth, bound).
+//
+// Every emitted vertex is also counted into two block-private histograms that
+// the diameter stage needs: its Morton brick (spatial sort) and its three
+// planes (planar pass).  They are flushed once per block (nonzero bins only).
 __global__ void __launch_bounds__(256) mc_cells(const uint32_t* __restrict__ bits, int nx, int ny,
                                                 int nz, int W, const CaseTables* __restrict__ tabs,
                                                 Stats* __restrict__ st, int4* __restrict__ vkeys,
-                                                long long cap) {
+                                                long long cap, unsigned int* __restrict__ sort_counts,
+                                                unsigned int* __restrict__ plane_counts) {
   __shared__ unsigned int s_hist[kNumCases];
   __shared__ int4 s_tn[kNumCases];
+  __shared__ unsigned int s_bin[kSortBins];
+  extern __shared__ unsigned int s_plane[];  // P = cnt0 + cnt1 + cnt2 bins
+  int bb[6];
+#pragma unroll
+  for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
+  const PlaneSpace ps = plane_space(bb);
+  const int P = bb[3] >= 0 ? ps.cnt[0] + ps.cnt[1] + ps.cnt[2] : 0;
+  const int bshift = brick_shift(bb);
   for (int i = threadIdx.x; i < kNumCases; i += blockDim.x) {
     s_hist[i] = 0;
     s_tn[i] = tabs->tn[i];
   }
+  for (int i = threadIdx.x; i < kSortBins; i += blockDim.x) s_bin[i] = 0;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) s_plane[i] = 0;
   __syncthreads();
 
-  const int xmin = st->bbox[0], ymin = st->bbox[1], zmin = st->bbox[2];
-  const int xmax = st->bbox[3], ymax = st->bbox[4], zmax = st->bbox[5];
+  const int xmin = bb[0], ymin = bb[1], zmin = bb[2];
+  const int xmax = bb[3], ymax = bb[4], zmax = bb[5];
   long long volk = 0;
   const int lane = threadIdx.x & 31;
   if (xmax >= 0) {
@@ -268,20 +283,27 @@ __global__ void __launch_bounds__(256) mc_cells(const uint32_t* __restrict__ bit
           wbase = __shfl_sync(kFull, wbase, 31);
           long long o = (long long)(wbase + incl - c);
           const int Y2 = 2 * v, Z2 = 2 * w;
+          auto emit = [&](int X, int Y, int Z) {
+            if (o < cap) vkeys[o] = make_int4(X, Y, Z, 0);
+            o++;
+            atomicAdd(&s_bin[brick_bin(X, Y, Z, bb, bshift)], 1u);
+            int id[3];
+            plane_ids(X, Y, Z, ps, id);
+            atomicAdd(&s_plane[id[0]], 1u);
+            atomicAdd(&s_plane[id[1]], 1u);
+            atomicAdd(&s_plane[id[2]], 1u);
+          };
           while (ex) {
             const int i = __ffs(ex) - 1; ex &= ex - 1;
-            if (o < cap) vkeys[o] = make_int4(2 * (xbase + i) + 1, Y2, Z2, 0);
-            o++;
+            emit(2 * (xbase + i) + 1, Y2, Z2);
           }
           while (ey) {
             const int i = __ffs(ey) - 1; ey &= ey - 1;
-            if (o < cap) vkeys[o] = make_int4(2 * (xbase + i), Y2 + 1, Z2, 0);
-            o++;
+            emit(2 * (xbase + i), Y2 + 1, Z2);
           }
           while (ez) {
             const int i = __ffs(ez) - 1; ez &= ez - 1;
-            if (o < cap) vkeys[o] = make_int4(2 * (xbase + i), Y2, Z2 + 1, 0);
-            o++;
+            emit(2 * (xbase + i), Y2, Z2 + 1);
           }
         }
       }
@@ -295,6 +317,10 @@ __global__ void __launch_bounds__(256) mc_cells(const uint32_t* __restrict__ bit
   __syncthreads();
   for (int i = threadIdx.x; i < kNumCases; i += blockDim.x)
     if (s_hist[i]) atomicAdd(&st->hist[i], (unsigned long long)s_hist[i]);
+  for (int i = threadIdx.x; i < kSortBins; i += blockDim.x)
+    if (s_bin[i]) atomicAdd(&sort_counts[i], s_bin[i]);
+  for (int i = threadIdx.x; i < P; i += blockDim.x)
+    if (s_plane[i]) atomicAdd(&plane_counts[i], s_plane[i]);
 }
 
 template __global__ void pack_bits_v16<4>(const uint4*, uint32_t*, long long, int, int, Stats*);

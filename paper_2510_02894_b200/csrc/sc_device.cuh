@@ -25,6 +25,7 @@ struct Stats {
   unsigned long long ext[26];          // packed (projection, index) of 13-direction extremes
   unsigned long long lb;               // fp64 bits: exact squared distance lower bound
   unsigned long long n_work;           // surviving 3-D work units after pruning
+  unsigned int done1, done2;           // block tickets (last-block selection); self-resetting
 };
 
 // Per-case integer tables for the exact volume path: for case k,
@@ -48,6 +49,79 @@ struct PlaneSpace {
   int lo[3];
   int cnt[3];
 };
+
+// ---- vertex binning shared by the MC emission, the sort and the planar pass ----
+
+// Morton brick order: 4 bits per axis (4096 bins) over the occupied bbox.
+constexpr int kSortBits = 12;
+constexpr int kSortBins = 1 << kSortBits;
+
+__device__ __forceinline__ unsigned int spread4(unsigned int v) {  // 4 bits -> every 3rd bit
+  v &= 15u;
+  v = (v | (v << 4)) & 0x0C3u;
+  v = (v | (v << 2)) & 0x249u;
+  return v;
+}
+
+// Brick shift (doubled units) so the bbox spans <= 16 bricks per axis.
+__device__ __forceinline__ int brick_shift(const int* bb) {
+  const int ext = max(bb[3] - bb[0], max(bb[4] - bb[1], bb[5] - bb[2])) * 2 + 3;
+  int s = 4;
+  while ((ext >> s) >= 16) s++;
+  return s;
+}
+
+__device__ __forceinline__ unsigned int brick_bin(int X, int Y, int Z, const int* bb, int s) {
+  const unsigned int bx = (unsigned int)(X - (2 * bb[0] - 1)) >> s;
+  const unsigned int by = (unsigned int)(Y - (2 * bb[1] - 1)) >> s;
+  const unsigned int bz = (unsigned int)(Z - (2 * bb[2] - 1)) >> s;
+  return spread4(bx) | (spread4(by) << 1) | (spread4(bz) << 2);
+}
+
+__device__ __forceinline__ PlaneSpace plane_space(const int* bb) {
+  PlaneSpace ps;
+  ps.lo[0] = 2 * bb[2] - 1; ps.cnt[0] = 2 * (bb[5] - bb[2]) + 3;
+  ps.lo[1] = 2 * bb[1] - 1; ps.cnt[1] = 2 * (bb[4] - bb[1]) + 3;
+  ps.lo[2] = 2 * bb[0] - 1; ps.cnt[2] = 2 * (bb[3] - bb[0]) + 3;
+  return ps;
+}
+
+// XY plane keyed by Z2, XZ by Y2, YZ by X2 (bit-equal fp64 coordinate <=>
+// equal doubled lattice key, since (key/2)*s is strictly monotone in key).
+__device__ __forceinline__ void plane_ids(int X, int Y, int Z, const PlaneSpace& ps, int out[3]) {
+  out[0] = Z - ps.lo[0];
+  out[1] = ps.cnt[0] + (Y - ps.lo[1]);
+  out[2] = ps.cnt[0] + ps.cnt[1] + (X - ps.lo[2]);
+}
+
+// Warp-aggregated increment: lanes with equal `id` share one global atomic.
+// Returns this lane's slot within its group's reservation.  All lanes call.
+__device__ __forceinline__ unsigned int group_add(unsigned int* base, unsigned int id, bool ok) {
+  const int lane = threadIdx.x & 31;
+  const unsigned int peers = __match_any_sync(0xffffffffu, ok ? id : 0x80000000u + lane);
+  const int leader = __ffs(peers) - 1;
+  unsigned int pos = 0;
+  if (ok && lane == leader) pos = atomicAdd(base + id, (unsigned int)__popc(peers));
+  pos = __shfl_sync(0xffffffffu, pos, leader);
+  return pos + __popc(peers & ((1u << lane) - 1));
+}
+
+// Last-block ticket: returns true in exactly one block, after every block of
+// the grid has passed this point (its prior global writes made visible).
+__device__ __forceinline__ bool last_block(unsigned int* ticket) {
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    if (threadIdx.x == 0) *ticket = 0u;  // ready for the next ROI
+  }
+  return s_last;
+}
 
 // Exclusive scan of one value per thread across a 1024-thread block (warp
 // shuffles, two levels, 2 barriers).  Returns the exclusive prefix; *total
