@@ -158,7 +158,7 @@ def probe_fp32_peak(device: int = 0, mode: int = 0) -> float:
 
 DIAG_NAMES = ("work_units", "total_units", "refine_candidates", "planar_units",
               "planar_candidates")
-PAIRS_PER_UNIT = 2048 * 256
+PAIRS_PER_UNIT = 256 * 256
 
 
 def last_diagnostics(device: int = 0) -> dict:

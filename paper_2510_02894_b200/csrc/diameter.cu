@@ -33,10 +33,8 @@ namespace sc {
 
 constexpr int kDiamThreads = 256;
 constexpr int kWarps = kDiamThreads / 32;
-constexpr int kR = 8;                          // i vertices per thread
-constexpr int kTile = kDiamThreads * kR;       // 2048: tile edge
-constexpr int kChunk = kDiamThreads;           // 256: j chunk per work unit
-constexpr int kChunks = kTile / kChunk;        // 8 units per tile pair
+constexpr int kChunk = 256;                    // vertices per chunk (pair unit = chunk x chunk)
+constexpr int kR = kChunk / 32;                // 8 i vertices per lane
 
 // Relative margin of the re-check threshold.  Pass-1 error is below ~1e-6 of
 // D^2; a unit whose pass-1 maximum is below M*(1 - kRefineRel)
@@ -49,7 +47,7 @@ __device__ __forceinline__ float fmax3f(float a, float b, float c) {
   return r;
 }
 
-// Upper-triangle tile-pair index -> (I, J), I <= J, row-major over I.
+// Upper-triangle pair index -> (I, J), I <= J, row-major over I.
 __device__ __forceinline__ void tile_pair(long long t, long long T, int& I, int& J) {
   double b = 2.0 * T + 1.0;
   long long i = (long long)((b - sqrt(b * b - 8.0 * (double)t)) * 0.5);
@@ -105,8 +103,12 @@ __device__ __forceinline__ void select_units(const float* __restrict__ umax, lon
   }
 }
 
-// Pass 1 (see header).  Error of the dot form: in the bbox-centred frame
-// |p| <= D*sqrt(3)/2, so the absolute error is < ~12 * 2^-24 * D^2.
+// Pass 1 (see header).  Work unit = one surviving chunk pair (I <= J, 256 x
+// 256 vertex pairs, listed by unit_filter); every WARP is an independent
+// worker with its own shared-memory copy of the J chunk, so load balance is
+// per unit and no block barrier is involved.  Error of the dot form: in the
+// bbox-centred frame |p| <= D*sqrt(3)/2, so the absolute error is
+// < ~12 * 2^-24 * D^2.
 //
 // PACKED: two i vertices share one FFMA2 (the j coordinate is the broadcast
 // scalar operand), so 4 pairs cost 6 FFMA2 + 2 FMNMX3 = 2 issue slots per
@@ -116,43 +118,41 @@ __global__ void __launch_bounds__(kDiamThreads, 4) diam3d_pass1(const int4* __re
                                                                 long long cap, Frame f, int shard,
                                                                 int nshards,
                                                                 const unsigned int* __restrict__ work,
-                                                                float* __restrict__ warp_max,
+                                                                float* __restrict__ umax,
                                                                 unsigned int* __restrict__ cand,
                                                                 Stats* __restrict__ st) {
-  __shared__ float4 sj[kChunk];  // (x, y, z, |p|^2)
+  __shared__ float4 sj_all[kWarps][kChunk];  // (x, y, z, |p|^2) per warp
   const long long n = n_vertices(st, cap);
   if (n == 0) return;
   frame_centre(st, f);
-  const long long T = (n + kTile - 1) / kTile;
+  const long long C = (n + kChunk - 1) / kChunk;
+  const long long n_work = (long long)st->n_work;
   long long w0, w1;
-  shard_span((long long)st->n_work, shard, nshards, w0, w1);  // surviving units (prune.cu)
-  const int warp = threadIdx.x >> 5;
+  shard_span(n_work, shard, nshards, w0, w1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float4* sj = sj_all[warp];
+  const long long gwarps = (long long)gridDim.x * kWarps;
   float run = 0.f;
-  for (long long w = w0 + blockIdx.x; w < w1; w += gridDim.x) {
-    const long long u = work[w];
-    const long long item = u / kChunks;
-    const int q = (int)(u - item * kChunks);
+  for (long long w = w0 + (long long)blockIdx.x * kWarps + warp; w < w1; w += gwarps) {
     int I, J;
-    tile_pair(item, T, I, J);
+    tile_pair(work[w], C, I, J);
     float a[kR], b[kR], c[kR], m[kR], ni[kR];
+    __syncwarp();  // previous unit is done with sj
 #pragma unroll
     for (int r = 0; r < kR; r++) {
-      const long long i = (long long)I * kTile + r * kDiamThreads + threadIdx.x;
+      long long i = (long long)I * kChunk + r * 32 + lane;
       const float3 p = frame_coord(keys[i < n ? i : n - 1], f);
       a[r] = -2.f * p.x;
       b[r] = -2.f * p.y;
       c[r] = -2.f * p.z;
       ni[r] = fmaf(p.x, p.x, fmaf(p.y, p.y, p.z * p.z));
       m[r] = -3.0e38f;
-    }
-    __syncthreads();  // the previous unit is done with sj
-    {
-      long long j = (long long)J * kTile + q * kChunk + threadIdx.x;
+      long long j = (long long)J * kChunk + r * 32 + lane;
       if (j >= n) j = n - 1;  // repeats of a real vertex are harmless for a max
-      const float3 p = frame_coord(keys[j], f);
-      sj[threadIdx.x] = make_float4(p.x, p.y, p.z, fmaf(p.x, p.x, fmaf(p.y, p.y, p.z * p.z)));
+      const float3 q = frame_coord(keys[j], f);
+      sj[r * 32 + lane] = make_float4(q.x, q.y, q.z, fmaf(q.x, q.x, fmaf(q.y, q.y, q.z * q.z)));
     }
-    __syncthreads();
+    __syncwarp();
     if (PACKED) {
       float2 a2[kR / 2], b2[kR / 2], c2[kR / 2];
 #pragma unroll
@@ -197,49 +197,45 @@ __global__ void __launch_bounds__(kDiamThreads, 4) diam3d_pass1(const int4* __re
     for (int r = 0; r < kR; r++) best = fmaxf(best, m[r] + ni[r]);
 #pragma unroll
     for (int o = 16; o; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
-    if ((threadIdx.x & 31) == 0) atomic_max_pos_f32(
-        reinterpret_cast<unsigned int*>(warp_max) + item * kWarps + warp, best);
+    if (lane == 0) umax[w] = best;
     run = fmaxf(run, best);
   }
-  if ((threadIdx.x & 31) == 0) atomic_max_pos_f32(&st->d3_f32, run);
-  // The last block to finish compacts the (tile pair, warp) units within
-  // kRefineRel of the global pass-1 maximum for the exact re-check.
-  if (last_block(&st->done1)) select_units(warp_max, tri(T) * kWarps, st, cand);
+  if (lane == 0) atomic_max_pos_f32(&st->d3_f32, run);
+  // The last block to finish compacts the units within kRefineRel of the
+  // global pass-1 maximum for the exact re-check.
+  if (last_block(&st->done1)) select_units(umax, n_work, st, cand);
 }
 template __global__ void diam3d_pass1<true>(const int4*, long long, Frame, int, int,
                                             const unsigned int*, float*, unsigned int*, Stats*);
 template __global__ void diam3d_pass1<false>(const int4*, long long, Frame, int, int,
                                              const unsigned int*, float*, unsigned int*, Stats*);
 
-// Exact re-check: a selected warp's 32*kR i rows against its J tile in fp64
-// with the reference arithmetic on the reference coordinates.  Work unit =
-// (candidate, 256-wide j chunk); a persistent grid walks the units.
+// Exact re-check: each selected chunk pair, 256 x 256 in fp64 with the
+// reference arithmetic on the reference coordinates; one block per candidate
+// (thread = one i vertex), persistent grid.
 __global__ void __launch_bounds__(kDiamThreads) diam3d_refine(const int4* __restrict__ keys,
                                                               long long cap, Frame f,
+                                                              const unsigned int* __restrict__ work,
                                                               const unsigned int* __restrict__ cand,
                                                               Stats* __restrict__ st) {
   __shared__ double sx[kChunk], sy[kChunk], sz[kChunk];
   const long long n = n_vertices(st, cap);
-  const long long T = (n + kTile - 1) / kTile;
-  const long long units = (long long)st->n_cand * kChunks;
+  const long long C = (n + kChunk - 1) / kChunk;
+  const long long nc = (long long)st->n_cand;
   double best = 0.0;
-  for (long long u = blockIdx.x; u < units; u += gridDim.x) {
-    const unsigned int cu = cand[u / kChunks];
-    const int q = (int)(u % kChunks);
-    const int warp = cu % kWarps;
+  for (long long u = blockIdx.x; u < nc; u += gridDim.x) {
     int I, J;
-    tile_pair(cu / kWarps, T, I, J);
+    tile_pair(work[cand[u]], C, I, J);
     __syncthreads();
     {
-      const long long j = (long long)J * kTile + q * kChunk + threadIdx.x;
+      const long long j = (long long)J * kChunk + threadIdx.x;
       const int4 kj = keys[j < n ? j : n - 1];
       sx[threadIdx.x] = ref_coord(kj.x, f.sx);
       sy[threadIdx.x] = ref_coord(kj.y, f.sy);
       sz[threadIdx.x] = ref_coord(kj.z, f.sz);
     }
     __syncthreads();
-    const int r = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long i = (long long)I * kTile + r * kDiamThreads + warp * 32 + lane;
+    const long long i = (long long)I * kChunk + threadIdx.x;
     if (i < n) {
       const int4 ki = keys[i];
       const double xi = ref_coord(ki.x, f.sx), yi = ref_coord(ki.y, f.sy), zi = ref_coord(ki.z, f.sz);

@@ -39,12 +39,13 @@ __global__ void scan_all(unsigned int*, unsigned int*, unsigned int*, unsigned i
 __global__ void scatter_all(const int4*, long long, const Stats*, unsigned int*, int4*,
                             unsigned int*, int2*);
 __global__ void boxes_extremes(const int4*, long long, Frame, Stats*, int4*);
-__global__ void unit_filter(const int4*, const int4*, long long, Frame, int, Stats*, float*,
+__global__ void unit_filter(const int4*, const int4*, long long, Frame, int, Stats*,
                             unsigned int*);
 template <bool PACKED>
 __global__ void diam3d_pass1(const int4*, long long, Frame, int, int, const unsigned int*, float*,
                              unsigned int*, Stats*);
-__global__ void diam3d_refine(const int4*, long long, Frame, const unsigned int*, Stats*);
+__global__ void diam3d_refine(const int4*, long long, Frame, const unsigned int*,
+                              const unsigned int*, Stats*);
 __global__ void plane_pass1(const int2*, const unsigned int*, const unsigned int*,
                             const unsigned int*, Frame, int, int, long long, float*, unsigned int*,
                             Stats*);
@@ -264,7 +265,7 @@ double f64_of(unsigned long long bits) {
   return d;
 }
 
-constexpr long long kTile = 2048;  // diameter.cu kTile
+constexpr long long kChunk = 256;  // diameter.cu kChunk: pair unit = chunk x chunk
 
 // Capacity of the per-ROI vertex arrays.  V is only known on the device, so
 // the arrays are sized up front (grow-only) and an overflow, detected after
@@ -282,10 +283,10 @@ int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, lo
   const int W = (int)((nx + 31) / 32);
   CK(c->bits.ensure((size_t)((long long)W * ny * nz)));
   CK(c->keys.ensure((size_t)cap));
-  const long long T = (dcap + kTile - 1) / kTile;
-  CK(c->warp_max.ensure((size_t)(T * (T + 1) / 2 * 8)));
-  CK(c->cand.ensure((size_t)(T * (T + 1) / 2 * 8)));
-  CK(c->work.ensure((size_t)(T * (T + 1) / 2 * 8)));
+  const long long C = (dcap + kChunk - 1) / kChunk;  // chunk pairs: C(C+1)/2
+  CK(c->warp_max.ensure((size_t)(C * (C + 1) / 2)));
+  CK(c->cand.ensure((size_t)(C * (C + 1) / 2)));
+  CK(c->work.ensure((size_t)(C * (C + 1) / 2)));
   CK(c->keys_sorted.ensure((size_t)dcap));
   CK(c->boxes.ensure((size_t)(2 * ((dcap + 255) / 256))));
   {
@@ -382,8 +383,7 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
   boxes_extremes<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, f, c->d_stats, c->boxes.p);
   CKL(1);
   unit_filter<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, c->boxes.p, dcap, f,
-                                         g_opt_prune.load() ? 1 : 0, c->d_stats, c->warp_max.p,
-                                         c->work.p);
+                                         g_opt_prune.load() ? 1 : 0, c->d_stats, c->work.p);
   CKL(1);
   CK(cudaEventRecord(c->kev[3], s));
   if (g_opt_packed.load())
@@ -394,7 +394,8 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
                                               c->work.p, c->warp_max.p, c->cand.p, c->d_stats);
   CKL(1);
   CK(cudaEventRecord(c->kev[4], s));
-  diam3d_refine<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, f, c->cand.p, c->d_stats);
+  diam3d_refine<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, f, c->work.p, c->cand.p,
+                                           c->d_stats);
   CKL(1);
   CK(cudaEventRecord(c->kev[5], s));
   plane_pass1<<<plgrid, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_tstart.p,
@@ -448,7 +449,7 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, const double sp[3],
             cudaStream_t s, int shard, int nshards, double* d_sq4, sc_coeffs* out) {
   long long cap = vertex_capacity(nx, ny, nz, (long long)c->keys.cap);
-  long long dcap = std::min<long long>(cap, std::max<long long>(4LL << 20, c->dcap));
+  long long dcap = std::min<long long>(cap, std::max<long long>(2LL << 20, c->dcap));
   long long punits = 0;
   for (int attempt = 0; attempt < 2; attempt++) {
     int rc = ensure_buffers(c, nx, ny, nz, cap, dcap, punits);
@@ -484,9 +485,9 @@ int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, c
   c->last_ms[6] = 0.0;
   {
     const Stats& h = *c->h_stats;
-    const long long V = (long long)h.n_vert, T = (V + kTile - 1) / kTile;
+    const long long V = (long long)h.n_vert, C = (V + kChunk - 1) / kChunk;
     c->last_diag[0] = (long long)h.n_work;
-    c->last_diag[1] = T * (T + 1) / 2 * 8;
+    c->last_diag[1] = C * (C + 1) / 2;
     c->last_diag[2] = (long long)h.n_cand;
     c->last_diag[3] = (long long)h.plane_units;
     c->last_diag[4] = (long long)h.n_pcand;

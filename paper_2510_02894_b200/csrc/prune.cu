@@ -2,10 +2,9 @@
 //
 // The maximum pair distance D^2 is at least LB = the largest exact pair value
 // among a few extreme vertices (13 directions, both ends).  After a Morton
-// brick ordering of the vertices, every 2048-vertex tile and every 256-vertex
-// chunk is spatially compact, so most (tile, chunk) work units have an upper
-// bound UB^2 = max distance^2 between their boxes below LB: they cannot hold
-// the maximum pair and are not evaluated.  Surviving units run through
+// brick ordering of the vertices, every 256-vertex chunk is spatially compact,
+// so most chunk pairs have an upper bound UB^2 = max distance^2 between their
+// boxes below LB: they cannot hold the maximum pair and are not evaluated.  Surviving units run through
 // diam3d_pass1 and the fp64 re-check keeps the result bit-identical to the
 // reference's all-pairs loop (features.py:121-192).
 //
@@ -14,7 +13,7 @@
 //   scatter_all     -- counting-sort scatter: keys by brick, plane coordinates
 //                      by plane (histograms were built by mc_cells)
 //   boxes_extremes  -- integer box of every 256-chunk + 13-direction extremes
-//   unit_filter     -- exact LB, zero the per-warp maxima, compact survivors
+//   unit_filter     -- exact LB, compact the surviving chunk pairs
 #include <climits>
 
 #include "sc_device.cuh"
@@ -22,7 +21,6 @@
 namespace sc {
 
 constexpr int kChunkV = 256;  // == diameter.cu kChunk
-constexpr int kTileV = 2048;  // == diameter.cu kTile
 constexpr int kNDir = 13;
 
 __device__ __forceinline__ long long n_verts(const Stats* st, long long cap) {
@@ -217,7 +215,7 @@ __global__ void __launch_bounds__(256) boxes_extremes(const int4* __restrict__ k
     atomicMax(&st->ext[threadIdx.x], s_ext[threadIdx.x]);
 }
 
-// Upper-triangle tile-pair index -> (I, J), I <= J (as diameter.cu).
+// Upper-triangle pair index -> (I, J), I <= J (as diameter.cu).
 __device__ __forceinline__ void tile_pair_p(long long t, long long T, int& I, int& J) {
   double b = 2.0 * T + 1.0;
   long long i = (long long)((b - sqrt(b * b - 8.0 * (double)t)) * 0.5);
@@ -237,14 +235,12 @@ __device__ __forceinline__ double axis_reach(int loA, int hiA, int loB, int hiB,
 
 // Every block: LB = max exact (reference fp64 arithmetic) squared distance
 // among the 26 extreme vertices (a real pair, so LB <= D^2; block 0 also seeds
-// the exact 3-D maximum with it).  Then, per work unit (tile pair item, j chunk
-// q): zero warp_max[u] (the per-(item, warp) maxima of pass 1 have the same
-// count) and keep the unit iff the max distance between the I tile box and the
-// chunk box can reach LB.
+// the exact 3-D maximum with it).  Then every chunk pair (I <= J) is kept iff
+// the max distance between the two chunk boxes can reach LB; survivors are
+// compacted into `work` (pair index t over the C x C upper triangle).
 __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys,
                                                    const int4* __restrict__ boxes, long long cap,
                                                    Frame f, int prune, Stats* __restrict__ st,
-                                                   float* __restrict__ warp_max,
                                                    unsigned int* __restrict__ work) {
   __shared__ double px[2 * kNDir], py[2 * kNDir], pz[2 * kNDir];
   __shared__ double s_lb[8];
@@ -274,9 +270,8 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
     atomic_max_pos_f64(&st->sq[0], lb);
   }
   const double thr = lb * (1.0 - 1e-9);  // UB and LB are exact up to fp64 rounding
-  const long long T = (n + kTileV - 1) / kTileV;
-  const long long chunks = (n + kChunkV - 1) / kChunkV;
-  const long long units = T * (T + 1) / 2 * (kTileV / kChunkV);
+  const long long C = (n + kChunkV - 1) / kChunkV;
+  const long long units = C * (C + 1) / 2;
   const double hx = 0.5 * f.sx, hy = 0.5 * f.sy, hz = 0.5 * f.sz;
   const int lane = threadIdx.x & 31;
   for (long long base = (long long)blockIdx.x * blockDim.x; base < units;
@@ -284,27 +279,17 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
     const long long u = base + threadIdx.x;
     bool keep = false;
     if (u < units) {
-      warp_max[u] = 0.f;
-      const long long item = u / (kTileV / kChunkV);
-      const int q = (int)(u - item * (kTileV / kChunkV));
-      int I, J;
-      tile_pair_p(item, T, I, J);
-      const long long cj = (long long)J * (kTileV / kChunkV) + q;
-      if (cj < chunks) {
-        int4 ilo = make_int4(INT_MAX, INT_MAX, INT_MAX, 0);
-        int4 ihi = make_int4(INT_MIN, INT_MIN, INT_MIN, 0);
-        for (int r = 0; r < kTileV / kChunkV; r++) {
-          const long long ci = (long long)I * (kTileV / kChunkV) + r;
-          if (ci >= chunks) break;
-          const int4 a = boxes[2 * ci], b = boxes[2 * ci + 1];
-          ilo.x = min(ilo.x, a.x); ilo.y = min(ilo.y, a.y); ilo.z = min(ilo.z, a.z);
-          ihi.x = max(ihi.x, b.x); ihi.y = max(ihi.y, b.y); ihi.z = max(ihi.z, b.z);
-        }
-        const int4 jlo = boxes[2 * cj], jhi = boxes[2 * cj + 1];
+      if (!prune) {
+        keep = true;
+      } else {
+        int I, J;
+        tile_pair_p(u, C, I, J);
+        const int4 ilo = boxes[2 * I], ihi = boxes[2 * I + 1];
+        const int4 jlo = boxes[2 * J], jhi = boxes[2 * J + 1];
         const double ub = axis_reach(ilo.x, ihi.x, jlo.x, jhi.x, hx) +
                           axis_reach(ilo.y, ihi.y, jlo.y, jhi.y, hy) +
                           axis_reach(ilo.z, ihi.z, jlo.z, jhi.z, hz);
-        keep = !prune || ub >= thr;
+        keep = ub >= thr;
       }
     }
     const unsigned int mask = __ballot_sync(0xffffffffu, keep);
