@@ -114,7 +114,7 @@ __device__ __forceinline__ void select_units(const float* __restrict__ umax, lon
 // scalar operand), so 4 pairs cost 6 FFMA2 + 2 FMNMX3 = 2 issue slots per
 // pair instead of 3.5 for scalar FFMA.
 template <bool PACKED>
-__global__ void __launch_bounds__(kDiamThreads, 4) diam3d_pass1(const int4* __restrict__ keys,
+__global__ void __launch_bounds__(kDiamThreads, 3) diam3d_pass1(const int4* __restrict__ keys,
                                                                 long long cap, Frame f, int shard,
                                                                 int nshards,
                                                                 const unsigned int* __restrict__ work,
@@ -131,27 +131,37 @@ __global__ void __launch_bounds__(kDiamThreads, 4) diam3d_pass1(const int4* __re
   shard_span(n_work, shard, nshards, w0, w1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float4* sj = sj_all[warp];
+  // Each warp takes a contiguous run of units, so consecutive units usually
+  // share the I chunk (always, without pruning) and its registers are reused.
   const long long gwarps = (long long)gridDim.x * kWarps;
+  const long long gw = (long long)blockIdx.x * kWarps + warp;
+  const long long per = (w1 - w0 + gwarps - 1) / gwarps;
+  const long long wb = w0 + gw * per, we = min(w1, wb + per);
   float run = 0.f;
-  for (long long w = w0 + (long long)blockIdx.x * kWarps + warp; w < w1; w += gwarps) {
+  int prevI = -1;
+  float a[kR], b[kR], c[kR], ni[kR];
+  for (long long w = wb; w < we; w++) {
     int I, J;
     tile_pair(work[w], C, I, J);
-    float a[kR], b[kR], c[kR], m[kR], ni[kR];
+    float m[kR];
     __syncwarp();  // previous unit is done with sj
 #pragma unroll
     for (int r = 0; r < kR; r++) {
-      long long i = (long long)I * kChunk + r * 32 + lane;
-      const float3 p = frame_coord(keys[i < n ? i : n - 1], f);
-      a[r] = -2.f * p.x;
-      b[r] = -2.f * p.y;
-      c[r] = -2.f * p.z;
-      ni[r] = fmaf(p.x, p.x, fmaf(p.y, p.y, p.z * p.z));
+      if (I != prevI) {
+        const long long i = (long long)I * kChunk + r * 32 + lane;
+        const float3 p = frame_coord(keys[i < n ? i : n - 1], f);
+        a[r] = -2.f * p.x;
+        b[r] = -2.f * p.y;
+        c[r] = -2.f * p.z;
+        ni[r] = fmaf(p.x, p.x, fmaf(p.y, p.y, p.z * p.z));
+      }
       m[r] = -3.0e38f;
       long long j = (long long)J * kChunk + r * 32 + lane;
       if (j >= n) j = n - 1;  // repeats of a real vertex are harmless for a max
       const float3 q = frame_coord(keys[j], f);
       sj[r * 32 + lane] = make_float4(q.x, q.y, q.z, fmaf(q.x, q.x, fmaf(q.y, q.y, q.z * q.z)));
     }
+    prevI = I;
     __syncwarp();
     if (PACKED) {
       float2 a2[kR / 2], b2[kR / 2], c2[kR / 2];
