@@ -125,8 +125,9 @@ int sc_last_kernel_times(int device, double* ms, int n);
  * re-check candidates}; a unit is 2048 x 256 vertex pairs.  Returns count. */
 int sc_last_diagnostics(int device, int64_t* out, int n);
 /* Process-wide switches (all default 1): "prune" = exact bbox pruning of
- * 3-D work units; "pass1_packed" = FFMA2 variant of the 3-D pass.  Results
- * are identical either way; 0 on success, SC_ERR_INPUT for an unknown name. */
+ * 3-D work units; "pass1_packed" = FFMA2 variant of the 3-D pass; "graphs" =
+ * replay each ROI pipeline as a cached CUDA graph.  Results are identical
+ * either way; 0 on success, SC_ERR_INPUT for an unknown name. */
 int sc_set_option(const char* name, int value);
 uint64_t sc_launch_count(void);
 int sc_probe_fp32_peak(int device, int mode, double* tflops);

@@ -64,7 +64,7 @@ namespace {
 
 constexpr int kMcPlaneSmem = 160 * 1024;  // mc_cells plane histogram (dynamic smem) limit
 thread_local std::string g_err;
-std::atomic<bool> g_opt_prune{true}, g_opt_packed{true};
+std::atomic<bool> g_opt_prune{true}, g_opt_packed{true}, g_opt_graphs{true};
 std::atomic<unsigned long long> g_launches{0};
 
 void set_err(const char* fmt, ...) {
@@ -173,7 +173,7 @@ struct Ctx {
   double last_ms[7] = {0, 0, 0, 0, 0, 0, 0};  // pack, mc, prune, pass1, refine, planar, h2d
   long long dcap = 0;  // vertices the diameter-side buffers are sized for
   long long last_diag[5] = {0, 0, 0, 0, 0};
-  int occ_pass1 = 1, occ_pass1s = 1, occ_plane = 1;  // resident blocks/SM (persistent kernels)
+  int occ_pass1 = 1, occ_pass1s = 1, occ_plane = 1, occ_pack = 1;  // resident blocks/SM
   Stats* d_stats = nullptr;
   Stats* h_stats = nullptr;  // pinned
   CaseTables* d_tabs = nullptr;
@@ -187,6 +187,36 @@ struct Ctx {
   DevBuf<uint8_t> mask_stage;
   DevBuf<double> cloud;
   DevBuf<unsigned long long> cloud_out;
+  // CUDA graphs of whole ROIs, keyed by everything baked into the nodes.
+  struct GraphEntry {
+    const void* mask;
+    int64_t nx, ny, nz;
+    double sp[3];
+    cudaStream_t s;
+    int shard, nshards;
+    void* d_sq4;
+    long long cap, dcap;
+    bool prune, packed;
+    unsigned long long gen;
+    cudaGraphExec_t exec;
+    unsigned long long launches;
+  };
+  std::vector<GraphEntry> graphs;
+  unsigned long long gen = 0;  // bumped whenever a scratch buffer moves
+
+  unsigned long long fingerprint() const {
+    unsigned long long h = 1469598103934665603ull;
+    const void* ps[] = {bits.p, keys.p, keys_sorted.p, boxes.p, sort_counts.p, sort_cursor.p,
+                        work.p, warp_max.p, plane_umax.p, cand.p, plane_cand.p, plane_umap.p,
+                        plane_counts.p, plane_start.p, plane_cursor.p, plane_tstart.p,
+                        plane_sorted.p};
+    for (const void* p : ps) h = (h ^ (unsigned long long)(uintptr_t)p) * 1099511628211ull;
+    return h;
+  }
+  void drop_graphs() {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    graphs.clear();
+  }
 };
 
 std::mutex g_ctx_mu;
@@ -225,6 +255,7 @@ int get_ctx(int device, Ctx** out) {
     if (const char* v = getenv("SC_PASS1")) g_opt_packed = std::strcmp(v, "scalar") != 0;
     if (const char* v = getenv("SC_PRUNE")) g_opt_prune = std::strcmp(v, "0") != 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_plane, plane_pass1, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pack, pack_bits_v16<4>, 256, 0));
     CK(cudaFuncSetAttribute(mc_cells, cudaFuncAttributeMaxDynamicSharedMemorySize, kMcPlaneSmem));
     g_ctx[device] = std::move(c);
   }
@@ -336,8 +367,8 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
     int unit = C16;
     for (int g = 1024; g % 2 == 0 && unit % 2 == 0;) { g /= 2; unit /= 2; }
     long long want = (n_chunks + 256 * 4 - 1) / (256 * 4);
-    long long grid = std::min<long long>(want, (long long)c->sms * 8);
-    grid = std::max<long long>(unit, (grid + unit - 1) / unit * unit);
+    long long grid = std::min<long long>(want, (long long)c->sms * std::max(1, c->occ_pack));
+    grid = std::max<long long>(unit, grid / unit * unit);
     pack_bits_v16<4><<<(unsigned)grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(d_mask),
                                                     c->bits.p, n_chunks, C16, (int)ny, c->d_stats);
   } else {
@@ -444,6 +475,61 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
+// Enqueue one ROI plus its result copies, replaying a cached CUDA graph when
+// the same (mask, dims, spacing, stream, shard, buffers, options) was seen
+// before; the first occurrence is captured.  Graph replay removes the per-
+// kernel launch cost of the ~11-kernel pipeline (SC option "graphs").
+int enqueue_with_copies(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
+                        const double sp[3], cudaStream_t s, int shard, int nshards,
+                        double* d_sq4, long long cap, long long dcap) {
+  int rc = enqueue_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, cap, dcap);
+  if (rc) return rc;
+  if (d_sq4)
+    CK(cudaMemcpyAsync(d_sq4, c->d_stats->sq, 4 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
+  return SC_OK;
+}
+
+int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
+               const double sp[3], cudaStream_t s, int shard, int nshards, double* d_sq4,
+               long long cap, long long dcap) {
+  if (!g_opt_graphs.load() || s == nullptr)
+    return enqueue_with_copies(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, cap, dcap);
+  const bool prune = g_opt_prune.load(), packed = g_opt_packed.load();
+  for (auto& g : c->graphs)
+    if (g.mask == d_mask && g.nx == nx && g.ny == ny && g.nz == nz && g.sp[0] == sp[0] &&
+        g.sp[1] == sp[1] && g.sp[2] == sp[2] && g.s == s && g.shard == shard &&
+        g.nshards == nshards && g.d_sq4 == d_sq4 && g.cap == cap && g.dcap == dcap &&
+        g.prune == prune && g.packed == packed && g.gen == c->gen) {
+      CK(cudaGraphLaunch(g.exec, s));
+      g_launches.fetch_add(g.launches, std::memory_order_relaxed);
+      return SC_OK;
+    }
+  const unsigned long long before = g_launches.load();
+  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  int rc = enqueue_with_copies(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, cap, dcap);
+  cudaGraph_t graph = nullptr;
+  cudaError_t ec = cudaStreamEndCapture(s, &graph);
+  const unsigned long long launches = g_launches.load() - before;
+  g_launches.fetch_sub(launches, std::memory_order_relaxed);  // captured, not launched
+  if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
+  CK(ec);
+  cudaGraphExec_t exec = nullptr;
+  ec = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  CK(ec);
+  if (c->graphs.size() >= 8) {
+    cudaGraphExecDestroy(c->graphs.front().exec);
+    c->graphs.erase(c->graphs.begin());
+  }
+  Ctx::GraphEntry g{d_mask, nx, ny, nz, {sp[0], sp[1], sp[2]}, s, shard, nshards, d_sq4,
+                    cap, dcap, prune, packed, c->gen, exec, launches};
+  c->graphs.push_back(g);
+  CK(cudaGraphLaunch(exec, s));
+  g_launches.fetch_add(launches, std::memory_order_relaxed);
+  return SC_OK;
+}
+
 // Full pipeline on a device-resident mask (context lock held by the caller):
 // enqueue everything, one D2H of the accumulators, one sync.
 int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, const double sp[3],
@@ -452,15 +538,17 @@ int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, c
   long long dcap = std::min<long long>(cap, std::max<long long>(2LL << 20, c->dcap));
   long long punits = 0;
   for (int attempt = 0; attempt < 2; attempt++) {
+    const unsigned long long fp0 = c->fingerprint();
     int rc = ensure_buffers(c, nx, ny, nz, cap, dcap, punits);
     if (rc) return rc;
+    if (c->fingerprint() != fp0) {
+      c->gen++;
+      c->drop_graphs();
+    }
     cap = (long long)c->keys.cap;
     c->dcap = std::max(c->dcap, dcap);
-    rc = enqueue_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, cap, dcap);
+    rc = launch_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, cap, dcap);
     if (rc) return rc;
-    if (d_sq4)
-      CK(cudaMemcpyAsync(d_sq4, c->d_stats->sq, 4 * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     const long long V = (long long)c->h_stats->n_vert;
     const long long PU = (long long)c->h_stats->plane_units;
@@ -678,6 +766,7 @@ int sc_set_option(const char* name, int value) {
   if (!name) { set_err("NULL option name"); return SC_ERR_INPUT; }
   if (std::strcmp(name, "prune") == 0) g_opt_prune = value != 0;
   else if (std::strcmp(name, "pass1_packed") == 0) g_opt_packed = value != 0;
+  else if (std::strcmp(name, "graphs") == 0) g_opt_graphs = value != 0;
   else { set_err("unknown option %s", name); return SC_ERR_INPUT; }
   return SC_OK;
 }

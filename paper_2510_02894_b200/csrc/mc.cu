@@ -94,12 +94,21 @@ __global__ void __launch_bounds__(256) pack_bits_v16(const uint4* __restrict__ m
     y[k] = (int)(row0 % ny);
     z[k] = (int)(row0 / ny);
   }
-  for (long long base = (long long)blockIdx.x * blockDim.x * U; base < n_chunks; base += step) {
-    uint4 v[U];
+  // Software pipeline: the next step's U loads are in flight while this
+  // step's chunks are converted.
+  uint4 v[U];
+  long long base = (long long)blockIdx.x * blockDim.x * U;
+#pragma unroll
+  for (int k = 0; k < U; k++) {
+    const long long g = base + (long long)k * blockDim.x + threadIdx.x;
+    v[k] = g < n_chunks ? __ldcs(mask + g) : make_uint4(0, 0, 0, 0);
+  }
+  for (; base < n_chunks; base += step) {
+    uint4 nv[U];
 #pragma unroll
     for (int k = 0; k < U; k++) {
-      const long long g = base + (long long)k * blockDim.x + threadIdx.x;
-      v[k] = g < n_chunks ? __ldcs(mask + g) : make_uint4(0, 0, 0, 0);
+      const long long g = base + step + (long long)k * blockDim.x + threadIdx.x;
+      nv[k] = g < n_chunks ? __ldcs(mask + g) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int k = 0; k < U; k++) {
@@ -121,6 +130,7 @@ __global__ void __launch_bounds__(256) pack_bits_v16(const uint4* __restrict__ m
       y[k] += dy;
       z[k] += dz;
       if (y[k] >= ny) { y[k] -= ny; z[k]++; }
+      v[k] = nv[k];
     }
   }
   box.flush(st);

@@ -225,7 +225,7 @@ def test_pruning_and_pass1_variants_identical(sc, golden, golden_arrays, cuda_de
     cases.append((synth.kits_like(tumor_mm=60.0), (0.8, 0.8, 1.0)))
     base = [sc.calculate_coefficients(a, sp).to_dict() for a, sp in cases]
     try:
-        for opt, val in (("prune", 0), ("pass1_packed", 0)):
+        for opt, val in (("prune", 0), ("pass1_packed", 0), ("graphs", 0)):
             _native.set_option(opt, val)
             for (a, sp), want in zip(cases, base):
                 assert sc.calculate_coefficients(a, sp).to_dict() == want, opt
@@ -233,7 +233,27 @@ def test_pruning_and_pass1_variants_identical(sc, golden, golden_arrays, cuda_de
     finally:
         _native.set_option("prune", 1)
         _native.set_option("pass1_packed", 1)
+        _native.set_option("graphs", 1)
     _native.set_option("prune", 1)
     sc.calculate_coefficients(cases[-1][0], cases[-1][1])
     d = _native.last_diagnostics(cuda_device)
     assert 0 < d["work_units"] < d["total_units"]  # the KiTS-like ROI actually prunes
+
+
+def test_graph_replay_sees_new_mask_contents(sc, cuda_device):
+    """A cached CUDA graph keyed on the same device pointer must read the new
+    contents of that buffer (device entry reuse, as in a serving loop)."""
+    import torch
+
+    from paper_2510_02894_b200 import synth
+
+    a = synth.synth_mask("sphere", (64, 64, 64), radius=20)
+    b = synth.synth_mask("ellipsoid", (64, 64, 64), semi_axes=(25, 15, 10))
+    d = torch.from_numpy(a).cuda()
+    ra = sc.calculate_coefficients_device(d, (1.0, 1.0, 1.0))
+    ra2 = sc.calculate_coefficients_device(d, (1.0, 1.0, 1.0))  # graph replay
+    d.copy_(torch.from_numpy(b))
+    rb = sc.calculate_coefficients_device(d, (1.0, 1.0, 1.0))
+    assert ra.to_dict() == ra2.to_dict()
+    assert rb.to_dict() == sc.calculate_coefficients(b, (1.0, 1.0, 1.0)).to_dict()
+    assert rb.to_dict() != ra.to_dict()
