@@ -257,6 +257,19 @@ int get_ctx(int device, Ctx** out) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_plane, plane_pass1, 256, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pack, pack_bits_v16<4>, 256, 0));
     CK(cudaFuncSetAttribute(mc_cells, cudaFuncAttributeMaxDynamicSharedMemorySize, kMcPlaneSmem));
+    {
+      // Lazy module loading must not happen inside a stream capture: touch
+      // every kernel once here.
+      cudaFuncAttributes fa;
+      const void* kernels[] = {(const void*)init_stats, (const void*)pack_bits_v16<4>,
+                               (const void*)pack_bits_generic, (const void*)mc_cells,
+                               (const void*)scan_all, (const void*)scatter_all,
+                               (const void*)boxes_extremes, (const void*)unit_filter,
+                               (const void*)diam3d_pass1<true>, (const void*)diam3d_pass1<false>,
+                               (const void*)diam3d_refine, (const void*)plane_pass1,
+                               (const void*)plane_refine, (const void*)cloud_diameters};
+      for (const void* k : kernels) CK(cudaFuncGetAttributes(&fa, k));
+    }
     g_ctx[device] = std::move(c);
   }
   *out = g_ctx[device].get();
@@ -357,7 +370,7 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
                 long long dcap) {
   const int W = (int)((nx + 31) / 32);
   const long long n_words = (long long)W * ny * nz;
-  CK(cudaEventRecord(c->kev[0], s));
+  CK(cudaEventRecordWithFlags(c->kev[0], s, cudaEventRecordExternal));
   init_stats<<<1, 256, 0, s>>>(c->d_stats);
   CKL(1);
   if (nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0) {
@@ -378,7 +391,7 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
                                            c->d_stats);
   }
   CKL(1);
-  CK(cudaEventRecord(c->kev[1], s));
+  CK(cudaEventRecordWithFlags(c->kev[1], s, cudaEventRecordExternal));
   const long long Pmax = 2 * (nx + ny + nz) + 9;
   int mc_occ = 1;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mc_occ, mc_cells, 256,
@@ -387,7 +400,7 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
       c->bits.p, (int)nx, (int)ny, (int)nz, W, c->d_tabs, c->d_stats, c->keys.p, cap,
       c->sort_counts.p, c->plane_counts.p);
   CKL(1);
-  CK(cudaEventRecord(c->kev[2], s));
+  CK(cudaEventRecordWithFlags(c->kev[2], s, cudaEventRecordExternal));
 
   Frame f;
   f.cx2 = f.cy2 = f.cz2 = 0;  // set on the device from the bbox
@@ -416,7 +429,7 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
   unit_filter<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, c->boxes.p, dcap, f,
                                          g_opt_prune.load() ? 1 : 0, c->d_stats, c->work.p);
   CKL(1);
-  CK(cudaEventRecord(c->kev[3], s));
+  CK(cudaEventRecordWithFlags(c->kev[3], s, cudaEventRecordExternal));
   if (g_opt_packed.load())
     diam3d_pass1<true><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, f, shard, nshards,
                                              c->work.p, c->warp_max.p, c->cand.p, c->d_stats);
@@ -424,11 +437,11 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
     diam3d_pass1<false><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, f, shard, nshards,
                                               c->work.p, c->warp_max.p, c->cand.p, c->d_stats);
   CKL(1);
-  CK(cudaEventRecord(c->kev[4], s));
+  CK(cudaEventRecordWithFlags(c->kev[4], s, cudaEventRecordExternal));
   diam3d_refine<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, f, c->work.p, c->cand.p,
                                            c->d_stats);
   CKL(1);
-  CK(cudaEventRecord(c->kev[5], s));
+  CK(cudaEventRecordWithFlags(c->kev[5], s, cudaEventRecordExternal));
   plane_pass1<<<plgrid, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_tstart.p,
                                      c->plane_umap.p, f, shard, nshards, pucap, c->plane_umax.p,
                                      c->plane_cand.p, c->d_stats);
@@ -437,7 +450,7 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
                                           c->plane_tstart.p, c->plane_umap.p, f,
                                           c->plane_cand.p, c->d_stats);
   CKL(1);
-  CK(cudaEventRecord(c->kev[6], s));
+  CK(cudaEventRecordWithFlags(c->kev[6], s, cudaEventRecordExternal));
   return SC_OK;
 }
 
