@@ -203,6 +203,7 @@ struct Ctx {
   };
   std::vector<GraphEntry> graphs;
   unsigned long long gen = 0;  // bumped whenever a scratch buffer moves
+  bool capturing = false;      // inside a stream capture of launch_roi
 
   unsigned long long fingerprint() const {
     unsigned long long h = 1469598103934665603ull;
@@ -311,6 +312,13 @@ double f64_of(unsigned long long bits) {
 
 constexpr long long kChunk = 256;  // diameter.cu kChunk: pair unit = chunk x chunk
 
+// Stage events: inside a capture they must be external event nodes so that
+// graph replays record them (plain records only order the capture).
+cudaError_t record(Ctx* c, cudaEvent_t ev, cudaStream_t s) {
+  return c->capturing ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal)
+                      : cudaEventRecord(ev, s);
+}
+
 // Capacity of the per-ROI vertex arrays.  V is only known on the device, so
 // the arrays are sized up front (grow-only) and an overflow, detected after
 // the single end-of-ROI sync, re-runs the ROI with exact capacity.
@@ -370,7 +378,7 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
                 long long dcap) {
   const int W = (int)((nx + 31) / 32);
   const long long n_words = (long long)W * ny * nz;
-  CK(cudaEventRecordWithFlags(c->kev[0], s, cudaEventRecordExternal));
+  CK(record(c, c->kev[0], s));
   init_stats<<<1, 256, 0, s>>>(c->d_stats);
   CKL(1);
   if (nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0) {
@@ -391,7 +399,7 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
                                            c->d_stats);
   }
   CKL(1);
-  CK(cudaEventRecordWithFlags(c->kev[1], s, cudaEventRecordExternal));
+  CK(record(c, c->kev[1], s));
   const long long Pmax = 2 * (nx + ny + nz) + 9;
   int mc_occ = 1;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mc_occ, mc_cells, 256,
@@ -400,7 +408,7 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
       c->bits.p, (int)nx, (int)ny, (int)nz, W, c->d_tabs, c->d_stats, c->keys.p, cap,
       c->sort_counts.p, c->plane_counts.p);
   CKL(1);
-  CK(cudaEventRecordWithFlags(c->kev[2], s, cudaEventRecordExternal));
+  CK(record(c, c->kev[2], s));
 
   Frame f;
   f.cx2 = f.cy2 = f.cz2 = 0;  // set on the device from the bbox
@@ -429,7 +437,7 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
   unit_filter<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, c->boxes.p, dcap, f,
                                          g_opt_prune.load() ? 1 : 0, c->d_stats, c->work.p);
   CKL(1);
-  CK(cudaEventRecordWithFlags(c->kev[3], s, cudaEventRecordExternal));
+  CK(record(c, c->kev[3], s));
   if (g_opt_packed.load())
     diam3d_pass1<true><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, f, shard, nshards,
                                              c->work.p, c->warp_max.p, c->cand.p, c->d_stats);
@@ -437,11 +445,11 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
     diam3d_pass1<false><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, f, shard, nshards,
                                               c->work.p, c->warp_max.p, c->cand.p, c->d_stats);
   CKL(1);
-  CK(cudaEventRecordWithFlags(c->kev[4], s, cudaEventRecordExternal));
+  CK(record(c, c->kev[4], s));
   diam3d_refine<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, f, c->work.p, c->cand.p,
                                            c->d_stats);
   CKL(1);
-  CK(cudaEventRecordWithFlags(c->kev[5], s, cudaEventRecordExternal));
+  CK(record(c, c->kev[5], s));
   plane_pass1<<<plgrid, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_tstart.p,
                                      c->plane_umap.p, f, shard, nshards, pucap, c->plane_umax.p,
                                      c->plane_cand.p, c->d_stats);
@@ -450,7 +458,7 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
                                           c->plane_tstart.p, c->plane_umap.p, f,
                                           c->plane_cand.p, c->d_stats);
   CKL(1);
-  CK(cudaEventRecordWithFlags(c->kev[6], s, cudaEventRecordExternal));
+  CK(record(c, c->kev[6], s));
   return SC_OK;
 }
 
@@ -520,7 +528,9 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
     }
   const unsigned long long before = g_launches.load();
   CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  c->capturing = true;
   int rc = enqueue_with_copies(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, cap, dcap);
+  c->capturing = false;
   cudaGraph_t graph = nullptr;
   cudaError_t ec = cudaStreamEndCapture(s, &graph);
   const unsigned long long launches = g_launches.load() - before;
