@@ -12,11 +12,14 @@ Workload (BASELINE.json configs[1]): one synthetic KiTS19-shaped mask,
 of one ROI: marching cubes -> area/volume -> 3-D and planar diameters.  The
 mask (157 MB) is larger than L2 (126 MB), so no L2 flush is needed.
 
-  value      device-resident throughput: mask already in HBM, CUDA events on
-             the library stream around K steps (host syncs inside the steps
-             are inside the timed region).
-  e2e        the same metric through the C ABI with a HOST (pinned) mask:
-             every step copies the 157 MB mask H2D and reads the result back.
+  value      device-resident throughput: mask already in HBM, K ROIs through the
+             pipelined device batch entry, CUDA events on the caller's stream
+             (the batch is ordered against it), host round trips included.
+  e2e        the same metric through the C ABI with a HOST (pinned) mask: the
+             pipelined host batch entry copies the 157 MB mask H2D for every
+             ROI and reads every result back.
+  single_roi one synchronous call per ROI (no cross-ROI overlap); its
+             per-kernel CUDA-event times feed kernel_ms and the rooflines.
   roofline   the dominant kernel of the step.  diam3d_pass1 is FP32
              CUDA-core bound: achieved = 8 flop x evaluated pairs / kernel time,
              peak = FP32 rate measured by sc_probe_fp32_peak on this GPU.
@@ -287,11 +290,35 @@ def run_ours(args):
     h_mask = torch.from_numpy(mask_np).pin_memory()
     h_np = h_mask.numpy()
 
-    # ---- device-resident throughput (value): exact pruned path (default) ----
+    # ---- device-resident throughput (value): K ROIs through the pipelined
+    # device batch entry (two slots: ROI i+1 is enqueued before ROI i is
+    # collected), CUDA events on `stream`, which the batch is ordered against.
     clocks = ClockSampler(dev)
-    dev_ms, med, diag, launches, c = measure_device(sc, _native, d_mask, stream, args.steps,
-                                                    args.warmup, dev, world, clocks)
+    sc.calculate_coefficients_device_batch([d_mask] * args.warmup, [SPACING] * args.warmup,
+                                           stream=stream)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _native.launch_count()
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.__enter__()
+    ev0.record(stream)
+    outs = sc.calculate_coefficients_device_batch([d_mask] * args.steps, [SPACING] * args.steps,
+                                                  stream=stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clocks.__exit__(None, None, None)
+    barrier(world)
+    launches = _native.launch_count() - launches0
+    dev_ms = max_over_ranks(world, ev0.elapsed_time(ev1))
     value = world * args.steps / (dev_ms / 1e3)
+    c = outs[-1]
+    assert all(o.to_dict() == c.to_dict() for o in outs)
+
+    # ---- one ROI per call (no cross-ROI overlap): per-kernel times ----
+    one_ms, med, diag, _, c1 = measure_device(sc, _native, d_mask, stream, args.steps,
+                                              args.warmup, dev, world)
+    assert c1.to_dict() == c.to_dict()
 
     # ---- same, all pairs evaluated (no pruning): the pass-1 roofline case ----
     _native.set_option("prune", 0)
@@ -300,18 +327,21 @@ def run_ours(args):
     _native.set_option("prune", 1)
     assert c_bf.to_dict() == c.to_dict(), "pruned and all-pairs results differ"
 
-    # ---- end to end through the C ABI with a pinned host mask (e2e) ----
-    for _ in range(max(1, args.warmup // 2)):
-        sc.calculate_coefficients(h_np, SPACING, device=dev)
+    # ---- end to end through the C ABI from pinned host memory (e2e): the
+    # pipelined host batch entry, 157 MB H2D per ROI inside the timed region.
+    sc.calculate_coefficients_batch([h_np] * max(2, args.warmup // 2),
+                                    [SPACING] * max(2, args.warmup // 2), device=dev)
     barrier(world)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        ce = sc.calculate_coefficients(h_np, SPACING, device=dev)
+    e_outs = sc.calculate_coefficients_batch([h_np] * args.steps, [SPACING] * args.steps,
+                                             device=dev)
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(world, time.perf_counter() - t0)
     barrier(world)
     e2e_value = world * args.steps / e2e_s
+    ce = e_outs[-1]
+    assert ce.to_dict() == c.to_dict()
 
     # ---- rooflines ----
     V = c.vertex_count
@@ -367,9 +397,12 @@ def run_ours(args):
         "config": workload_config({"global_batch": world, "parallelism": f"roi-batch x{world}"}),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": mask_bytes,
                 "d2h_bytes_per_step": 2 * 2304,
-                "path": "sc_calculate_coefficients (C ABI) from pinned host memory",
-                "h2d_ms_per_step": ce.h2d_ms},
+                "path": "sc_calculate_coefficients_batch (C ABI, pipelined) from pinned host memory",
+                "h2d_ms_per_roi": ce.h2d_ms},
+        "single_roi": {"value": world * args.steps / (one_ms / 1e3), "unit": UNIT,
+                       "path": "sc_calculate_coefficients_device, one synchronous call per ROI"},
         "gpu_launches": int(launches),
+        "path": "sc_calculate_coefficients_device_batch (C ABI), device-resident masks",
         "roofline": roofline,
         "roofline_mc": roof_mc,
         "roofline_pass1": roof_p1,

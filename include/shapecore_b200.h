@@ -93,11 +93,19 @@ int sc_calculate_coefficients_shard(const uint8_t* d_mask, int64_t nx, int64_t n
                                     int nshards, double* d_sq4, sc_coeffs* out);
 
 /* Batch of ROIs on one device (C4): masks[i] are host pointers with dims
- * dims[3*i..3*i+2] and spacing spacings[3*i..]; out[i] per ROI.  The first
- * failing ROI's code is returned; later ROIs are still processed. */
+ * dims[3*i..3*i+2] and spacing spacings[3*i..]; out[i] per ROI.  Two pipeline
+ * slots alternate, so the H2D copy of ROI i+1 overlaps the kernels of ROI i.
+ * The first failing ROI's code is returned; later ROIs are still processed. */
 int sc_calculate_coefficients_batch(const uint8_t* const* masks, const int64_t* dims,
                                     const double* spacings, int64_t count, int device,
                                     sc_coeffs* out);
+
+/* Same for device-resident masks on the CURRENT device (pipelined likewise).
+ * If `stream` (cudaStream_t) is non-NULL the batch is ordered after prior work
+ * on it, and work enqueued on it later is ordered after the batch. */
+int sc_calculate_coefficients_device_batch(const uint8_t* const* d_masks, const int64_t* dims,
+                                           const double* spacings, int64_t count, void* stream,
+                                           sc_coeffs* out);
 
 /* Diameters of an arbitrary fp64 point cloud (features.py:205-221), bit-exact
  * with the reference: out = (max3d, xy, xz, yz).  Host arrays. */

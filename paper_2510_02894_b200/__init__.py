@@ -24,6 +24,7 @@ from .features import (
     calculate_coefficients,
     calculate_coefficients_batch,
     calculate_coefficients_device,
+    calculate_coefficients_device_batch,
     calculate_coefficients_shard,
     diameters,
     diameters_parallel,
@@ -40,6 +41,7 @@ __all__ = [
     "FEATURE_KEYS", "Coefficients", "DeviceError", "EmptyRoi", "MaskVolume", "NoVertices",
     "NonPositiveSpacing", "ShapeCoreError", "ShapeExceedsBounds", "ShapeFeatures",
     "StageTimings", "attach_spacing", "calculate_coefficients", "calculate_coefficients_batch",
-    "calculate_coefficients_device", "calculate_coefficients_shard", "diameters",
+    "calculate_coefficients_device", "calculate_coefficients_device_batch",
+    "calculate_coefficients_shard", "diameters",
     "diameters_parallel", "extract_features", "mesh_vertices", "synth_mask",
 ]

@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <array>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -220,10 +221,14 @@ struct Ctx {
   }
 };
 
+// Two independent pipeline slots per device (stream, events, scratch, graphs):
+// single-ROI calls use slot 0; batch calls alternate slots so the H2D copy and
+// kernels of ROI i+1 overlap the tail and the host round trip of ROI i.
+constexpr int kSlots = 2;
 std::mutex g_ctx_mu;
-std::vector<std::unique_ptr<Ctx>> g_ctx;
+std::vector<std::array<std::unique_ptr<Ctx>, kSlots>> g_ctx;
 
-int get_ctx(int device, Ctx** out) {
+int get_ctx(int device, Ctx** out, int slot = 0) {
   std::lock_guard<std::mutex> lk(g_ctx_mu);
   int n = 0;
   CK(cudaGetDeviceCount(&n));
@@ -232,7 +237,7 @@ int get_ctx(int device, Ctx** out) {
     return SC_ERR_INPUT;
   }
   if ((int)g_ctx.size() < n) g_ctx.resize(n);
-  if (!g_ctx[device]) {
+  if (!g_ctx[device][slot]) {
     auto c = std::make_unique<Ctx>();
     c->device = device;
     CK(cudaSetDevice(device));
@@ -271,9 +276,9 @@ int get_ctx(int device, Ctx** out) {
                                (const void*)plane_refine, (const void*)cloud_diameters};
       for (const void* k : kernels) CK(cudaFuncGetAttributes(&fa, k));
     }
-    g_ctx[device] = std::move(c);
+    g_ctx[device][slot] = std::move(c);
   }
-  *out = g_ctx[device].get();
+  *out = g_ctx[device][slot].get();
   return SC_OK;
 }
 
@@ -553,40 +558,66 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   return SC_OK;
 }
 
-// Full pipeline on a device-resident mask (context lock held by the caller):
-// enqueue everything, one D2H of the accumulators, one sync.
-int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, const double sp[3],
-            cudaStream_t s, int shard, int nshards, double* d_sq4, sc_coeffs* out) {
+// Start one ROI on slot c: make room, enqueue (graph replay when cached).
+// No synchronisation; finish_roi collects it.
+struct Pending {
+  const uint8_t* d_mask;
+  int64_t nx, ny, nz;
+  double sp[3];
+  cudaStream_t s;
+  int shard, nshards;
+  double* d_sq4;
+  long long cap, dcap;
+};
+
+int start_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
+              const double sp[3], cudaStream_t s, int shard, int nshards, double* d_sq4,
+              long long punits, Pending* p) {
   long long cap = vertex_capacity(nx, ny, nz, (long long)c->keys.cap);
   long long dcap = std::min<long long>(cap, std::max<long long>(2LL << 20, c->dcap));
-  long long punits = 0;
-  for (int attempt = 0; attempt < 2; attempt++) {
-    const unsigned long long fp0 = c->fingerprint();
-    int rc = ensure_buffers(c, nx, ny, nz, cap, dcap, punits);
-    if (rc) return rc;
-    if (c->fingerprint() != fp0) {
-      c->gen++;
-      c->drop_graphs();
-    }
-    cap = (long long)c->keys.cap;
-    c->dcap = std::max(c->dcap, dcap);
-    rc = launch_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, cap, dcap);
-    if (rc) return rc;
-    CK(cudaStreamSynchronize(s));
-    const long long V = (long long)c->h_stats->n_vert;
-    const long long PU = (long long)c->h_stats->plane_units;
-    if (V <= dcap && PU <= (long long)c->plane_umax.cap) break;
-    if (attempt == 1) { set_err("vertex buffer overflow"); return SC_ERR_NOMEM; }
+  if (p->cap > 0) {  // re-run after an overflow: exact sizes
+    cap = std::max(cap, p->cap);
+    dcap = std::max(dcap, p->dcap);
+  }
+  const unsigned long long fp0 = c->fingerprint();
+  int rc = ensure_buffers(c, nx, ny, nz, cap, dcap, punits);
+  if (rc) return rc;
+  if (c->fingerprint() != fp0) {
+    c->gen++;
+    c->drop_graphs();
+  }
+  cap = (long long)c->keys.cap;
+  c->dcap = std::max(c->dcap, dcap);
+  *p = Pending{d_mask, nx, ny, nz, {sp[0], sp[1], sp[2]}, s, shard, nshards, d_sq4, cap, dcap};
+  return launch_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, cap, dcap);
+}
+
+// Wait for the ROI started on slot c, re-run it once with exact buffer sizes
+// if the device reported an overflow, and fill `out`.
+int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
+  CK(cudaStreamSynchronize(p->s));
+  const long long V = (long long)c->h_stats->n_vert;
+  const long long PU = (long long)c->h_stats->plane_units;
+  if (V > p->dcap || PU > (long long)c->plane_umax.cap) {
     // rare: more vertices / planar tiles than reserved -> exact re-run
-    cap = std::max(cap, V);
-    dcap = std::max(dcap, V);
-    punits = PU;
+    Pending q = *p;
+    q.cap = std::max(p->cap, V);
+    q.dcap = std::max(p->dcap, V);
+    int rc = start_roi(c, q.d_mask, q.nx, q.ny, q.nz, q.sp, q.s, q.shard, q.nshards, q.d_sq4, PU,
+                       &q);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(q.s));
+    if ((long long)c->h_stats->n_vert > q.dcap ||
+        (long long)c->h_stats->plane_units > (long long)c->plane_umax.cap) {
+      set_err("vertex buffer overflow");
+      return SC_ERR_NOMEM;
+    }
   }
   if (c->h_stats->bbox[3] < 0) {
     set_err("mask has no occupied voxels");
     return SC_ERR_EMPTY_ROI;
   }
-  fill_out(*c->h_stats, sp, out);
+  fill_out(*c->h_stats, p->sp, out);
   c->last_ms[0] = ev_ms(c->kev[0], c->kev[1]);
   c->last_ms[1] = ev_ms(c->kev[1], c->kev[2]);
   c->last_ms[2] = ev_ms(c->kev[2], c->kev[3]);
@@ -596,7 +627,7 @@ int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, c
   c->last_ms[6] = 0.0;
   {
     const Stats& h = *c->h_stats;
-    const long long V = (long long)h.n_vert, C = (V + kChunk - 1) / kChunk;
+    const long long Vv = (long long)h.n_vert, C = (Vv + kChunk - 1) / kChunk;
     c->last_diag[0] = (long long)h.n_work;
     c->last_diag[1] = C * (C + 1) / 2;
     c->last_diag[2] = (long long)h.n_cand;
@@ -608,9 +639,98 @@ int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, c
   return SC_OK;
 }
 
+// Full pipeline on a device-resident mask (context lock held by the caller).
+int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, const double sp[3],
+            cudaStream_t s, int shard, int nshards, double* d_sq4, sc_coeffs* out) {
+  Pending p{};
+  int rc = start_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, 0, &p);
+  if (rc) return rc;
+  return finish_roi(c, &p, out);
+}
+
 double wall_ms() {
   using namespace std::chrono;
   return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+// Pipelined batch on the two slots of `device`: ROI i+1 is enqueued (H2D copy
+// included for host masks) before ROI i is collected, so copies, kernels and
+// the host round trip of neighbouring ROIs overlap.  The first failing ROI's
+// code is returned; every other ROI is still processed.
+int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
+              const double* spacings, int64_t count, bool host, sc_coeffs* out,
+              cudaStream_t user) {
+  if (count < 0 || (count > 0 && (!masks || !dims || !spacings || !out))) {
+    set_err("bad batch arguments");
+    return SC_ERR_INPUT;
+  }
+  if (count == 0) return SC_OK;
+  Ctx* cs[kSlots];
+  for (int k = 0; k < kSlots; k++) {
+    int rc = get_ctx(device, &cs[k], k);
+    if (rc) return rc;
+  }
+  std::lock_guard<std::mutex> l0(cs[0]->mu);
+  std::lock_guard<std::mutex> l1(cs[1]->mu);
+  CK(cudaSetDevice(device));
+  if (user) {  // order the batch after prior work on the caller's stream
+    CK(cudaEventRecord(cs[0]->ev[4], user));
+    for (int k = 0; k < kSlots; k++) CK(cudaStreamWaitEvent(cs[k]->stream, cs[0]->ev[4], 0));
+  }
+  Pending pend[kSlots] = {};
+  int64_t idx[kSlots] = {-1, -1};
+  double t_start[kSlots] = {0, 0};
+  int first = SC_OK;
+  std::string first_err;
+  auto note = [&](int rc) {
+    if (rc && first == SC_OK) { first = rc; first_err = g_err; }
+  };
+  auto collect = [&](int k) {
+    if (idx[k] < 0) return;
+    Ctx* c = cs[k];
+    sc_coeffs* o = &out[idx[k]];
+    note(finish_roi(c, &pend[k], o));
+    if (host) {
+      o->h2d_ms = ev_ms(c->ev[0], c->ev[1]);
+      c->last_ms[6] = o->h2d_ms;
+    }
+    o->total_ms = wall_ms() - t_start[k];
+    idx[k] = -1;
+  };
+  for (int64_t i = 0; i < count; i++) {
+    const int k = (int)(i % kSlots);
+    collect(k);
+    std::memset(&out[i], 0, sizeof out[i]);
+    const int64_t nx = dims[3 * i], ny = dims[3 * i + 1], nz = dims[3 * i + 2];
+    const double* sp = spacings + 3 * i;
+    int rc = check_input(masks[i], nx, ny, nz, sp);
+    if (rc) { note(rc); continue; }
+    Ctx* c = cs[k];
+    cudaStream_t s = c->stream;
+    t_start[k] = wall_ms();
+    const uint8_t* dm = masks[i];
+    if (host) {
+      const size_t bytes = (size_t)nx * ny * nz;
+      CK(c->mask_stage.ensure(bytes));
+      CK(cudaEventRecord(c->ev[0], s));
+      CK(cudaMemcpyAsync(c->mask_stage.p, masks[i], bytes, cudaMemcpyHostToDevice, s));
+      CK(cudaEventRecord(c->ev[1], s));
+      dm = c->mask_stage.p;
+    }
+    pend[k] = Pending{};
+    rc = start_roi(c, dm, nx, ny, nz, sp, s, 0, 1, nullptr, 0, &pend[k]);
+    if (rc) { note(rc); continue; }
+    idx[k] = i;
+  }
+  for (int64_t i = 0; i < kSlots; i++) collect((int)((count + i) % kSlots));
+  if (user) {  // ... and later work on it after the batch
+    for (int k = 0; k < kSlots; k++) {
+      CK(cudaEventRecord(cs[k]->ev[5], cs[k]->stream));
+      CK(cudaStreamWaitEvent(user, cs[k]->ev[5], 0));
+    }
+  }
+  if (first) g_err = first_err;
+  return first;
 }
 
 int current_ctx(Ctx** c) {
@@ -684,19 +804,15 @@ int sc_calculate_coefficients(const uint8_t* mask, int64_t nx, int64_t ny, int64
 int sc_calculate_coefficients_batch(const uint8_t* const* masks, const int64_t* dims,
                                     const double* spacings, int64_t count, int device,
                                     sc_coeffs* out) {
-  if (count < 0 || (count > 0 && (!masks || !dims || !spacings || !out))) {
-    set_err("bad batch arguments");
-    return SC_ERR_INPUT;
-  }
-  int first = SC_OK;
-  std::string first_err;
-  for (int64_t i = 0; i < count; i++) {
-    int rc = sc_calculate_coefficients(masks[i], dims[3 * i], dims[3 * i + 1], dims[3 * i + 2],
-                                       spacings + 3 * i, device, out + i);
-    if (rc && first == SC_OK) { first = rc; first_err = g_err; }
-  }
-  if (first) g_err = first_err;
-  return first;
+  return run_batch(device, masks, dims, spacings, count, true, out, nullptr);
+}
+
+int sc_calculate_coefficients_device_batch(const uint8_t* const* d_masks, const int64_t* dims,
+                                           const double* spacings, int64_t count, void* stream,
+                                           sc_coeffs* out) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  return run_batch(dev, d_masks, dims, spacings, count, false, out, (cudaStream_t)stream);
 }
 
 int sc_diameters(const double* xs, const double* ys, const double* zs, int64_t n, int device,

@@ -183,6 +183,28 @@ def calculate_coefficients_batch(masks: Sequence, spacings: Sequence[Sequence[fl
     return [_from_struct(o) for o in outs]
 
 
+def calculate_coefficients_device_batch(masks: Sequence, spacings: Sequence[Sequence[float]],
+                                        stream=None) -> List[Coefficients]:
+    """Many device-resident masks (CUDA uint8 tensors (nz, ny, nx) on the
+    current device) in one pipelined C call, ordered after prior work on
+    `stream` (a torch.cuda.Stream) and before later work on it."""
+    n = len(masks)
+    ptrs = (ctypes.c_void_p * n)(*[m.data_ptr() for m in masks])
+    dims = np.asarray([(int(m.shape[2]), int(m.shape[1]), int(m.shape[0])) for m in masks],
+                      dtype=np.int64).reshape(-1)
+    sp = np.asarray([_check_spacing(s) for s in spacings], dtype=np.float64).reshape(-1)
+    for m in masks:
+        if not m.is_contiguous():
+            raise ValueError("device masks must be contiguous")
+    outs = (_native.ScCoeffs * n)()
+    handle = 0 if stream is None else int(stream.cuda_stream)
+    rc = _native.load().sc_calculate_coefficients_device_batch(
+        ptrs, dims.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+        sp.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), n, ctypes.c_void_p(handle), outs)
+    _native.raise_for(rc, "sc_calculate_coefficients_device_batch")
+    return [_from_struct(o) for o in outs]
+
+
 def _as_coord_arrays(xs, ys, zs):
     """features.py:195-202."""
     arrs = tuple(np.ascontiguousarray(a, dtype=np.float64) for a in (xs, ys, zs))

@@ -206,6 +206,23 @@ def test_batch_entry(sc, golden, golden_arrays, cuda_device):
         assert_matches(got, c["features"], c["triangle_count"], c["active_cubes"], c["name"])
 
 
+def test_device_batch_pipeline(sc, golden, golden_arrays, cuda_device):
+    import torch
+
+    cases = golden["cases"][:10]
+    ds = [torch.from_numpy(np.ascontiguousarray(golden_arrays[c["mask_key"]])).cuda()
+          for c in cases]
+    outs = sc.calculate_coefficients_device_batch(ds, [c["spacing"] for c in cases],
+                                                  stream=torch.cuda.current_stream())
+    for c, got in zip(cases, outs):
+        assert_matches(got, c["features"], c["triangle_count"], c["active_cubes"], c["name"])
+    # an empty ROI inside a batch fails alone
+    ds2 = [ds[0], torch.zeros((4, 4, 4), dtype=torch.uint8, device="cuda"), ds[1]]
+    with pytest.raises(sc.EmptyRoi):
+        sc.calculate_coefficients_device_batch(ds2, [cases[0]["spacing"], (1, 1, 1),
+                                                     cases[1]["spacing"]])
+
+
 def test_repeat_calls_deterministic(sc, cuda_device):
     from paper_2510_02894_b200 import synth
 
