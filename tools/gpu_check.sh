@@ -12,7 +12,7 @@ if [ "${1:-}" != "quick" ]; then
   timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_bench.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on \
-      -k regex:"diam3d_pass1|pack_bits_v16|mc_cells|plane_pass1|extremes|sort_|unit_filter|chunk_boxes|plane_hist|plane_scatter" -s 12 -c 12 \
+      -k regex:"diam3d_pass1|pack_bits_v16|mc_cells|plane_pass1|boxes_extremes|scan_all|scatter_all|unit_filter|refine" -s 9 -c 9 \
       -o $OUT/prof -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_full.log 2>&1
 fi
 echo done
