@@ -48,30 +48,51 @@ sys.path.insert(0, ROOT)
 
 METRIC = "ROIs/sec full 3D shape coefficients (KiTS19-shaped masks) at 1/2/4/8 B200"
 UNIT = "ROIs/s"
-SPACING = (0.8, 0.8, 1.0)
-DIMS = (512, 512, 600)  # nx, ny, nz
-TUMOR_MM = 30.0
-KERNELS_PER_ROI = 9  # init, pack, mc, pass1, refine, plane hist/scan/scatter/pairs
+
+# SURVEY.md 8(d) configurations.  The default (headline, BASELINE.json
+# configs[1]) is c2; the others are selectable with --workload.
+WORKLOADS = {
+    "c2": "C2 KiTS19-shaped synthetic kidney+tumor mask 512x512x600 uint8 at 0.8x0.8x1.0 mm "
+          "(tumor 30 mm, V=73406), one ROI per step per GPU",
+    "c3": "C3 noisy-boundary ellipsoid 512^3 at 1 mm (sigma 0.02, seed 1234, V=1963474, "
+          "1.93e12 pairs), one ROI per step per GPU",
+    "c4": "C4 batch of 300 varied KiTS19-shaped masks (512x512x[200..700], seed 2025), "
+          "LPT-sharded across GPUs, one ROI per step, cycling the rank's share",
+    "c5": "C5 thin slab 512x512x24 at 0.5x0.5x5 mm, 400 blobs (seed 7, V=127664), "
+          "one ROI per step per GPU",
+}
 
 
-def workload_config(extra=None):
+def load_workload(name, rank=0, world=1):
+    """[(mask (nz,ny,nx) uint8, spacing)] for this rank, plus a config dict."""
+    from paper_2510_02894_b200 import sharding, synth
+
+    if name == "c2":
+        rois = [(synth.kits_like(512, 512, 600, (0.8, 0.8, 1.0), 30.0), (0.8, 0.8, 1.0))]
+    elif name == "c3":
+        rois = [(synth.noisy_ellipsoid(512, 0.02, 1234), (1.0, 1.0, 1.0))]
+    elif name == "c5":
+        rois = [(synth.thin_slab(), (0.5, 0.5, 5.0))]
+    elif name == "c4":
+        params = synth.kits_batch_params(300, 2025)
+        # cost: streamed voxels + (surface ~ tumour/kidney size)^2 pairs
+        costs = [sharding.roi_cost(int((p["tumor_mm"] / p["sp"][0]) ** 3 * 4.2 + 2.6e5),
+                                   p["nx"] * p["ny"] * p["nz"]) for p in params]
+        mine = sharding.assign_rois(costs, world)[rank]
+        rois = [(synth.kits_from_params(params[i]), tuple(params[i]["sp"])) for i in mine]
+    else:
+        raise SystemExit(f"unknown workload {name}")
     cfg = {
-        "workload": "C2 KiTS19-shaped synthetic kidney+tumor mask 512x512x600 uint8 at "
-                    "0.8x0.8x1.0 mm (tumor 30 mm, V=73406), one ROI per step per GPU",
+        "workload": WORKLOADS[name],
+        "name": name,
         "global_batch": None,
-        "roi_bytes": DIMS[0] * DIMS[1] * DIMS[2],
-        "l2": "input 157 MB > 126 MB L2 (no flush needed)",
+        "roi_bytes_mean": sum(m.size for m, _ in rois) / max(1, len(rois)),
+        "rois_per_rank": len(rois),
+        "l2": "every mask > 126 MB L2 (no flush needed)" if min(m.size for m, _ in rois) > 126e6
+              else "mask < L2: steps cycle distinct ROIs / the mask is re-read from L2",
         "parallelism": None,
     }
-    if extra:
-        cfg.update(extra)
-    return cfg
-
-
-def make_mask():
-    from paper_2510_02894_b200 import synth
-
-    return synth.kits_like(DIMS[0], DIMS[1], DIMS[2], SPACING, TUMOR_MM)
+    return rois, cfg
 
 
 def measured_peaks():
@@ -193,26 +214,49 @@ def max_over_ranks(world, value):
     return float(t.item())
 
 
-def cpu_reference_time(mask, max_seconds=150.0, steps=1, warmup=0):
-    """The oracle (C port of the reference path) on all host cores: MC serial,
-    diameters strip-parallel (features.py:151-192).  Returns (per-ROI seconds
-    list, threads)."""
+def cpu_reference_time(mask, spacing, max_seconds=150.0, steps=1, warmup=0):
+    """The oracle (C port of the reference path) on all host cores: MC serial
+    (mesh.py:68-199), diameters strip-parallel (features.py:151-192).
+    Returns (per-ROI seconds list, threads, sample description).  When the
+    full pair loop would exceed the budget (C3), the diameters are timed on a
+    random vertex subset and extrapolated by pair count (labelled as such)."""
+    import numpy as np
+
     from oracle import oracle
 
     threads = oracle.max_threads()
-    t_start = time.perf_counter()
-    for _ in range(warmup):
-        oracle.extract_features(mask, SPACING, threads=0, with_active=False)
-        if time.perf_counter() - t_start > max_seconds / 2:
-            break
-    times = []
-    for _ in range(max(1, steps)):
-        t0 = time.perf_counter()
-        oracle.extract_features(mask, SPACING, threads=0, with_active=False)
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_start > max_seconds:
-            break
-    return times, threads
+    t0 = time.perf_counter()
+    mesh = oracle.marching_cubes(mask, spacing)
+    t_mc = time.perf_counter() - t0
+    V = mesh.vertex_count
+    pairs = V * (V - 1) / 2
+    if pairs <= 4e10:
+        t_start = time.perf_counter()
+        for _ in range(warmup):
+            oracle.extract_features(mask, spacing, threads=0, with_active=False)
+            if time.perf_counter() - t_start > max_seconds / 2:
+                break
+        times = []
+        for _ in range(max(1, steps)):
+            t1 = time.perf_counter()
+            oracle.extract_features(mask, spacing, threads=0, with_active=False)
+            times.append(time.perf_counter() - t1)
+            if time.perf_counter() - t_start > max_seconds:
+                break
+        return times, threads, f"{len(times)} full ROI(s)"
+    m = int((2 * 2e10) ** 0.5)
+    idx = np.sort(np.random.default_rng(0).choice(V, size=m, replace=False))
+    t1 = time.perf_counter()
+    oracle.diameters(mesh.xs[idx], mesh.ys[idx], mesh.zs[idx], threads=0)
+    t_d = (time.perf_counter() - t1) * pairs / (m * (m - 1) / 2)
+    t_area = 0.0
+    t2 = time.perf_counter()
+    oracle.surface_area(mesh)
+    oracle.mesh_volume(mesh)
+    t_area = time.perf_counter() - t2
+    return [t_mc + t_area + t_d], threads, (
+        f"full MC ({t_mc:.1f}s) + area/volume + diameters timed on a {m}-vertex random subset "
+        f"and extrapolated by pair count ({pairs:.3g} pairs -> {t_d:.0f}s)")
 
 
 def run_reference(args):
@@ -220,20 +264,22 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    mask = make_mask()
-    times, threads = cpu_reference_time(mask, max_seconds=args.cpu_seconds, steps=args.steps,
-                                        warmup=min(args.warmup, 1))
+    rois, cfg = load_workload(args.workload, 0, 1)
+    mask, sp = rois[len(rois) // 2]
+    times, threads, sample = cpu_reference_time(mask, sp, max_seconds=args.cpu_seconds,
+                                                steps=args.steps, warmup=min(args.warmup, 1))
     per = statistics.mean(times)
     value = 1.0 / per
+    cfg.update({"parallelism": "host cores (OpenMP)", "global_batch": 1})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": world, "steps": len(times), "warmup": min(args.warmup, 1),
         "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8/fp64", "data": "synthetic",
-        "config": workload_config({"parallelism": "host cores (OpenMP)", "global_batch": 1}),
+        "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{len(times)} full C2 ROI(s) through oracle/shape_oracle.c "
-                                   "(reference algorithm restated in C: serial canonical MC, "
+                         "sample": f"{sample} through oracle/shape_oracle.c (reference "
+                                   "algorithm restated in C: serial canonical MC, "
                                    "strip-parallel fp64 diameters), time-capped at "
                                    f"{args.cpu_seconds:.0f}s"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -242,31 +288,28 @@ def run_reference(args):
     return 0
 
 
-def measure_device(sc, _native, d_mask, stream, steps, warmup, dev, world, clocks=None):
-    """K device-resident steps on `stream`, CUDA events around the whole loop;
-    returns (elapsed ms max over ranks, per-kernel median ms, diag, launches, c)."""
+def measure_device(sc, _native, d_mask, sp, stream, steps, warmup, dev, world):
+    """One synchronous call per ROI (no cross-ROI overlap): K steps on `stream`,
+    CUDA events around the loop; returns (ms max over ranks, per-kernel median
+    ms, diagnostics, launches, last result)."""
     import torch
 
     with torch.cuda.stream(stream):
         for _ in range(warmup):
-            c = sc.calculate_coefficients_device(d_mask, SPACING, stream=stream)
+            c = sc.calculate_coefficients_device(d_mask, sp, stream=stream)
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kt = {k: [] for k in _native.KERNEL_TIME_NAMES}
     launches0 = _native.launch_count()
     barrier(world)
     torch.cuda.synchronize()
-    if clocks is not None:
-        clocks.__enter__()
     ev0.record(stream)
     for _ in range(steps):
-        c = sc.calculate_coefficients_device(d_mask, SPACING, stream=stream)
+        c = sc.calculate_coefficients_device(d_mask, sp, stream=stream)
         for k, v in _native.last_kernel_times(dev).items():
             kt[k].append(v)
     ev1.record(stream)
     torch.cuda.synchronize()
-    if clocks is not None:
-        clocks.__exit__(None, None, None)
     barrier(world)
     launches = _native.launch_count() - launches0
     ms = max_over_ranks(world, ev0.elapsed_time(ev1))
@@ -283,19 +326,23 @@ def run_ours(args):
 
     world, rank, local = dist_setup(args.gpus)
     dev = torch.cuda.current_device()
-    mask_np = make_mask()
-    nz, ny, nx = mask_np.shape
-    d_mask = torch.from_numpy(mask_np).to(f"cuda:{dev}")
+    rois, cfg = load_workload(args.workload, rank, world)
+    d_masks = [torch.from_numpy(m).to(f"cuda:{dev}") for m, _ in rois]
+    sps = [sp for _, sp in rois]
     stream = torch.cuda.Stream()
-    h_mask = torch.from_numpy(mask_np).pin_memory()
-    h_np = h_mask.numpy()
+    n_host = min(len(rois), 8)
+    h_masks = [torch.from_numpy(m).pin_memory().numpy() for m, _ in rois[:n_host]]
+    K = args.steps
+    step_masks = [d_masks[i % len(d_masks)] for i in range(K)]
+    step_sps = [sps[i % len(sps)] for i in range(K)]
 
     # ---- device-resident throughput (value): K ROIs through the pipelined
     # device batch entry (two slots: ROI i+1 is enqueued before ROI i is
     # collected), CUDA events on `stream`, which the batch is ordered against.
     clocks = ClockSampler(dev)
-    sc.calculate_coefficients_device_batch([d_mask] * args.warmup, [SPACING] * args.warmup,
-                                           stream=stream)
+    W = args.warmup
+    sc.calculate_coefficients_device_batch([d_masks[i % len(d_masks)] for i in range(W)],
+                                           [sps[i % len(sps)] for i in range(W)], stream=stream)
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = _native.launch_count()
@@ -303,45 +350,46 @@ def run_ours(args):
     torch.cuda.synchronize()
     clocks.__enter__()
     ev0.record(stream)
-    outs = sc.calculate_coefficients_device_batch([d_mask] * args.steps, [SPACING] * args.steps,
-                                                  stream=stream)
+    outs = sc.calculate_coefficients_device_batch(step_masks, step_sps, stream=stream)
     ev1.record(stream)
     torch.cuda.synchronize()
     clocks.__exit__(None, None, None)
     barrier(world)
     launches = _native.launch_count() - launches0
     dev_ms = max_over_ranks(world, ev0.elapsed_time(ev1))
-    value = world * args.steps / (dev_ms / 1e3)
-    c = outs[-1]
-    assert all(o.to_dict() == c.to_dict() for o in outs)
+    value = world * K / (dev_ms / 1e3)
+    for i, o in enumerate(outs[len(d_masks):]):
+        assert o.to_dict() == outs[i % len(d_masks)].to_dict()
 
-    # ---- one ROI per call (no cross-ROI overlap): per-kernel times ----
-    one_ms, med, diag, _, c1 = measure_device(sc, _native, d_mask, stream, args.steps,
-                                              args.warmup, dev, world)
-    assert c1.to_dict() == c.to_dict()
+    # ---- one ROI per call on the first ROI: per-kernel times ----
+    d0, sp0 = d_masks[0], sps[0]
+    one_steps = max(3, min(K, 30))
+    one_ms, med, diag, _, c = measure_device(sc, _native, d0, sp0, stream, one_steps, 3, dev, world)
+    assert c.to_dict() == outs[0].to_dict()
 
     # ---- same, all pairs evaluated (no pruning): the pass-1 roofline case ----
     _native.set_option("prune", 0)
-    bf_ms, bf_med, bf_diag, _, c_bf = measure_device(sc, _native, d_mask, stream,
-                                                     max(3, args.steps // 2), 3, dev, world)
+    bf_steps = 3 if args.workload == "c3" else max(3, one_steps // 2)
+    bf_ms, bf_med, bf_diag, _, c_bf = measure_device(sc, _native, d0, sp0, stream, bf_steps, 1,
+                                                     dev, world)
     _native.set_option("prune", 1)
     assert c_bf.to_dict() == c.to_dict(), "pruned and all-pairs results differ"
 
     # ---- end to end through the C ABI from pinned host memory (e2e): the
-    # pipelined host batch entry, 157 MB H2D per ROI inside the timed region.
-    sc.calculate_coefficients_batch([h_np] * max(2, args.warmup // 2),
-                                    [SPACING] * max(2, args.warmup // 2), device=dev)
+    # pipelined host batch entry; every step copies its mask H2D.
+    sc.calculate_coefficients_batch([h_masks[i % n_host] for i in range(2)],
+                                    [sps[i % n_host] for i in range(2)], device=dev)
     barrier(world)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    e_outs = sc.calculate_coefficients_batch([h_np] * args.steps, [SPACING] * args.steps,
-                                             device=dev)
+    e_outs = sc.calculate_coefficients_batch([h_masks[i % n_host] for i in range(K)],
+                                             [sps[i % n_host] for i in range(K)], device=dev)
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(world, time.perf_counter() - t0)
     barrier(world)
-    e2e_value = world * args.steps / e2e_s
-    ce = e_outs[-1]
-    assert ce.to_dict() == c.to_dict()
+    e2e_value = world * K / e2e_s
+    h2d_bytes = sum(h_masks[i % n_host].size for i in range(K)) / K
+    assert e_outs[0].to_dict() == outs[0].to_dict()
 
     # ---- rooflines ----
     V = c.vertex_count
@@ -350,7 +398,7 @@ def run_ours(args):
     fp32_ffma2 = _native.probe_fp32_peak(dev, 0)
     traffic = ncu_traffic()
     peaks, peak_kind = measured_peaks()
-    mask_bytes = nx * ny * nz
+    mask_bytes = d0.numel()
 
     def pass1_roof(m, d, label):
         evaluated = d["work_units"] * _native.PAIRS_PER_UNIT
@@ -380,33 +428,34 @@ def run_ours(args):
     dominant = max(stage, key=stage.get)
     roofline = roof_p1 if dominant == "diam3d_pass1_ms" else roof_mc
     total_k = sum(stage.values())
+    cfg.update({"global_batch": world, "parallelism": f"roi-batch x{world}"})
 
     line = {
         "metric": METRIC,
         "value": value,
         "unit": UNIT,
         "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": dev_ms / args.steps,
+        "steps": K,
+        "warmup": W,
+        "ms_per_step": dev_ms / K,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "fp32",
         "data": "synthetic",
-        "config": workload_config({"global_batch": world, "parallelism": f"roi-batch x{world}"}),
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": mask_bytes,
-                "d2h_bytes_per_step": 2 * 2304,
+        "config": cfg,
+        "path": "sc_calculate_coefficients_device_batch (C ABI), device-resident masks",
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d_bytes),
+                "d2h_bytes_per_step": 2400,  # one Stats record (sc_device.cuh)
                 "path": "sc_calculate_coefficients_batch (C ABI, pipelined) from pinned host memory",
-                "h2d_ms_per_roi": ce.h2d_ms},
-        "single_roi": {"value": world * args.steps / (one_ms / 1e3), "unit": UNIT,
+                "h2d_ms_per_roi": e_outs[-1].h2d_ms},
+        "single_roi": {"value": world * one_steps / (one_ms / 1e3), "unit": UNIT,
                        "path": "sc_calculate_coefficients_device, one synchronous call per ROI"},
         "gpu_launches": int(launches),
-        "path": "sc_calculate_coefficients_device_batch (C ABI), device-resident masks",
         "roofline": roofline,
         "roofline_mc": roof_mc,
         "roofline_pass1": roof_p1,
-        "allpairs": {"value": world * max(3, args.steps // 2) / (bf_ms / 1e3), "unit": UNIT,
+        "allpairs": {"value": world * bf_steps / (bf_ms / 1e3), "unit": UNIT,
                      "note": "same exact results with pruning disabled (every pair evaluated)",
                      "kernel_ms": bf_med, "roofline_pass1": roof_p1_bf},
         "kernel_ms": med,
@@ -420,11 +469,12 @@ def run_ours(args):
     }
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        times, threads = cpu_reference_time(mask_np, max_seconds=args.cpu_seconds, steps=1)
+        m, sp = rois[0]
+        times, threads, sample = cpu_reference_time(m, sp, max_seconds=args.cpu_seconds, steps=1)
         per = statistics.mean(times)
         line["cpu_baseline"] = {
             "value": 1.0 / per, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": "1 full C2 ROI through oracle/shape_oracle.c (reference algorithm in C: "
+            "sample": f"{sample} through oracle/shape_oracle.c (reference algorithm in C: "
                       "serial canonical MC + strip-parallel fp64 diameters on all host threads)",
             "seconds_per_roi": per,
         }
@@ -445,6 +495,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=150.0)
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # contract: W >= 3 warm-up steps

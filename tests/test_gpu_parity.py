@@ -274,3 +274,50 @@ def test_graph_replay_sees_new_mask_contents(sc, cuda_device):
     assert ra.to_dict() == ra2.to_dict()
     assert rb.to_dict() == sc.calculate_coefficients(b, (1.0, 1.0, 1.0)).to_dict()
     assert rb.to_dict() != ra.to_dict()
+
+
+def _hull_max_sq(pts, oracle_mod):
+    """Reference-arithmetic max squared distance over the convex-hull vertices
+    of pts (n, d); the maximum pair of a point set always lies on its hull."""
+    from scipy.spatial import ConvexHull, QhullError
+
+    if len(pts) < 2:
+        return 0.0
+    try:
+        idx = ConvexHull(pts).vertices if len(pts) > pts.shape[1] + 1 else np.arange(len(pts))
+    except QhullError:  # degenerate (collinear / coplanar): use every point
+        idx = np.arange(len(pts))
+    sub = pts[np.sort(idx)]
+    cols = [sub[:, k] for k in range(sub.shape[1])] + [np.zeros(len(sub))] * (3 - sub.shape[1])
+    return oracle_mod.diameters(*cols, threads=0)[0] ** 2
+
+
+@pytest.mark.timeout(900)
+def test_c3_noisy_ellipsoid(sc, oracle_mod, cuda_device):
+    """C3 (512^3, ~2M vertices, 1.93e12 pairs): counts, area and volume against
+    the oracle's full marching cubes; diameters against the reference
+    arithmetic on convex-hull subsets ("hull-subset parity")."""
+    from paper_2510_02894_b200 import synth
+
+    arr = synth.noisy_ellipsoid(512)
+    assert int(arr.sum()) == 30765643  # SURVEY.md Appendix D
+    got = sc.calculate_coefficients(arr, (1.0, 1.0, 1.0), device=cuda_device)
+    assert got.vertex_count == 1963474 and got.triangle_count == 3870288
+    mesh = oracle_mod.marching_cubes(arr)
+    assert mesh.vertex_count == got.vertex_count and mesh.triangle_count == got.triangle_count
+    assert got.active_cubes == oracle_mod.active_cubes(arr)
+    assert rel_err(got.surface_area, oracle_mod.surface_area(mesh)) <= REL_TOL
+    assert rel_err(got.mesh_volume, oracle_mod.mesh_volume(mesh)) <= REL_TOL
+    pts = np.column_stack((mesh.xs, mesh.ys, mesh.zs))
+    d3 = math.sqrt(_hull_max_sq(pts, oracle_mod))
+    assert rel_err(got.max_3d_diameter, d3) <= 1e-12
+    for col, key, inplane in ((2, "max_2d_diameter_xy", (0, 1)), (1, "max_2d_diameter_xz", (0, 2)),
+                              (0, "max_2d_diameter_yz", (1, 2))):
+        order = np.argsort(pts[:, col], kind="stable")
+        vals = pts[order, col]
+        cuts = np.flatnonzero(np.diff(vals)) + 1
+        best = 0.0
+        for grp in np.split(order, cuts):
+            if len(grp) >= 2:
+                best = max(best, _hull_max_sq(pts[grp][:, inplane], oracle_mod))
+        assert rel_err(getattr(got, key), math.sqrt(best)) <= 1e-12, key
