@@ -172,7 +172,7 @@ struct Ctx {
   cudaEvent_t ev[6] = {};
   cudaEvent_t kev[8] = {};      // per-kernel boundaries of the last ROI
   double last_ms[7] = {0, 0, 0, 0, 0, 0, 0};  // pack, mc, prune, pass1, refine, planar, h2d
-  long long dcap = 0;  // vertices the diameter-side buffers are sized for
+  long long cap_floor = 0, dcap_floor = 0;  // raised by overflow re-runs only
   long long last_diag[5] = {0, 0, 0, 0, 0};
   int occ_pass1 = 1, occ_pass1s = 1, occ_plane = 1, occ_pack = 1;  // resident blocks/SM
   Stats* d_stats = nullptr;
@@ -573,12 +573,14 @@ struct Pending {
 int start_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
               const double sp[3], cudaStream_t s, int shard, int nshards, double* d_sq4,
               long long punits, Pending* p) {
-  long long cap = vertex_capacity(nx, ny, nz, (long long)c->keys.cap);
-  long long dcap = std::min<long long>(cap, std::max<long long>(2LL << 20, c->dcap));
-  if (p->cap > 0) {  // re-run after an overflow: exact sizes
-    cap = std::max(cap, p->cap);
-    dcap = std::max(dcap, p->dcap);
+  // Requested sizes depend only on the dims and on floors raised by overflow
+  // re-runs (never on the allocated capacities, so graphs stay valid).
+  if (p->cap > 0) {  // re-run after an overflow: exact sizes from now on
+    c->cap_floor = std::max(c->cap_floor, p->cap);
+    c->dcap_floor = std::max(c->dcap_floor, p->dcap);
   }
+  long long cap = vertex_capacity(nx, ny, nz, c->cap_floor);
+  long long dcap = std::min<long long>(cap, std::max<long long>(2LL << 20, c->dcap_floor));
   const unsigned long long fp0 = c->fingerprint();
   int rc = ensure_buffers(c, nx, ny, nz, cap, dcap, punits);
   if (rc) return rc;
@@ -586,8 +588,6 @@ int start_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
     c->gen++;
     c->drop_graphs();
   }
-  cap = (long long)c->keys.cap;
-  c->dcap = std::max(c->dcap, dcap);
   *p = Pending{d_mask, nx, ny, nz, {sp[0], sp[1], sp[2]}, s, shard, nshards, d_sq4, cap, dcap};
   return launch_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, cap, dcap);
 }
