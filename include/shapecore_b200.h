@@ -129,8 +129,9 @@ int sc_mesh_vertices(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, in
  * FFMA2 (mode 0) or scalar FFMA (mode 1) kernel. */
 int sc_last_kernel_times(int device, double* ms, int n);
 /* Work counters of the last ROI on `device`: {3-D work units evaluated, 3-D
- * work units total, fp64 re-check candidates, planar tile pairs, planar
- * re-check candidates}; a unit is 2048 x 256 vertex pairs.  Returns count. */
+ * work units total, 3-D fp64 re-check candidates, planar tile pairs total,
+ * planar re-check candidates, planar tile pairs evaluated}; a unit is 256 x
+ * 256 vertex pairs.  Returns how many were written. */
 int sc_last_diagnostics(int device, int64_t* out, int n);
 /* Process-wide switches (all default 1): "prune" = exact bbox pruning of
  * 3-D work units; "pass1_packed" = FFMA2 variant of the 3-D pass; "graphs" =

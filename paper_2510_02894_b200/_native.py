@@ -161,13 +161,13 @@ def probe_fp32_peak(device: int = 0, mode: int = 0) -> float:
 
 
 DIAG_NAMES = ("work_units", "total_units", "refine_candidates", "planar_units",
-              "planar_candidates")
+              "planar_candidates", "planar_work_units")
 PAIRS_PER_UNIT = 256 * 256
 
 
 def last_diagnostics(device: int = 0) -> dict:
-    buf = (ctypes.c_int64 * 5)()
-    n = load().sc_last_diagnostics(int(device), buf, 5)
+    buf = (ctypes.c_int64 * 6)()
+    n = load().sc_last_diagnostics(int(device), buf, 6)
     if n < 0:
         raise_for(-n, "sc_last_diagnostics")
     return {k: int(buf[i]) for i, k in enumerate(DIAG_NAMES[:n])}

@@ -36,55 +36,6 @@ constexpr int kWarps = kDiamThreads / 32;
 constexpr int kChunk = 256;                    // vertices per chunk (pair unit = chunk x chunk)
 constexpr int kR = kChunk / 32;                // 8 i vertices per lane
 
-// Relative margin of the re-check threshold.  Pass-1 error is below ~1e-6 of
-// D^2; a unit whose pass-1 maximum is below M*(1 - kRefineRel)
-// provably cannot hold the exact maximum pair.
-constexpr float kRefineRel = 8e-6f;
-
-__device__ __forceinline__ float fmax3f(float a, float b, float c) {
-  float r;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
-}
-
-// Upper-triangle pair index -> (I, J), I <= J, row-major over I.
-__device__ __forceinline__ void tile_pair(long long t, long long T, int& I, int& J) {
-  double b = 2.0 * T + 1.0;
-  long long i = (long long)((b - sqrt(b * b - 8.0 * (double)t)) * 0.5);
-  if (i < 0) i = 0;
-  if (i > T - 1) i = T - 1;
-  auto off = [T](long long r) { return r * T - r * (r - 1) / 2; };
-  while (i > 0 && off(i) > t) i--;
-  while (i < T - 1 && off(i + 1) <= t) i++;
-  I = (int)i;
-  J = (int)(i + (t - off(i)));
-}
-
-__device__ __forceinline__ long long n_vertices(const Stats* st, long long cap) {
-  long long n = (long long)st->n_vert;
-  return n < cap ? n : cap;
-}
-
-// Bbox-centred fp32 frame: centre (doubled units) from the MC bbox.
-__device__ __forceinline__ void frame_centre(const Stats* st, Frame& f) {
-  f.cx2 = st->bbox[0] + st->bbox[3];
-  f.cy2 = st->bbox[1] + st->bbox[4];
-  f.cz2 = st->bbox[2] + st->bbox[5];
-}
-
-__device__ __forceinline__ float3 frame_coord(int4 k, const Frame& f) {
-  return make_float3((float)(k.x - f.cx2) * f.hx, (float)(k.y - f.cy2) * f.hy,
-                     (float)(k.z - f.cz2) * f.hz);
-}
-
-__device__ __forceinline__ void shard_span(long long n, int shard, int nshards, long long& a,
-                                           long long& b) {
-  a = n * shard / nshards;
-  b = n * (shard + 1) / nshards;
-}
-
-__device__ __forceinline__ long long tri(long long T) { return T * (T + 1) / 2; }
-
 // Compact the units whose pass-1 maximum can hold the exact maximum
 // (one block; called by the last block of the pass-1 grid).
 __device__ __forceinline__ void select_units(const float* __restrict__ umax, long long units,
@@ -256,180 +207,6 @@ __global__ void __launch_bounds__(kDiamThreads) diam3d_refine(const int4* __rest
 #pragma unroll
   for (int o = 16; o; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
   if ((threadIdx.x & 31) == 0 && best > 0.0) atomic_max_pos_f64(&st->sq[0], best);
-}
-
-// ---- planar pass -----------------------------------------------------------
-// Plane index space (PlaneSpace): [0, cnt0) XY planes keyed by Z2, then XZ by
-// Y2, then YZ by X2; keys Z2 in [2 zmin - 1, 2 zmax + 1] etc.
-constexpr int kPT = 256;  // planar tile edge (threads per block)
-
-__device__ __forceinline__ PlaneSpace plane_space(const Stats* st) {
-  int bb[6];
-#pragma unroll
-  for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
-  return plane_space(bb);
-}
-
-struct PlaneAxes {  // in-plane (a, b) coordinate frame of one plane family
-  int ca, cb;       // centre, doubled units
-  float ha, hb;     // fp32 half spacings
-  double sa, sb;    // fp64 spacings
-};
-
-__device__ __forceinline__ PlaneAxes plane_axes(int axis, const Stats* st, const Frame& f) {
-  const int* bb = st->bbox;
-  PlaneAxes x;
-  if (axis == 0) {         // XY plane: (X, Y)
-    x.ca = bb[0] + bb[3]; x.cb = bb[1] + bb[4]; x.ha = f.hx; x.hb = f.hy; x.sa = f.sx; x.sb = f.sy;
-  } else if (axis == 1) {  // XZ plane: (X, Z)
-    x.ca = bb[0] + bb[3]; x.cb = bb[2] + bb[5]; x.ha = f.hx; x.hb = f.hz; x.sa = f.sx; x.sb = f.sz;
-  } else {                 // YZ plane: (Y, Z)
-    x.ca = bb[1] + bb[4]; x.cb = bb[2] + bb[5]; x.ha = f.hy; x.hb = f.hz; x.sa = f.sy; x.sb = f.sz;
-  }
-  return x;
-}
-
-__device__ __forceinline__ int plane_axis(int p, const PlaneSpace& ps) {
-  return p < ps.cnt[0] ? 0 : (p < ps.cnt[0] + ps.cnt[1] ? 1 : 2);
-}
-
-// Planar pass 1: fp32 dot form over every in-plane tile pair (kPT x kPT), one
-// maximum per unit; per-axis maxima in st->pl_f32[axis].  umap[u] is the plane
-// of unit u (scan_all).  The last block compacts the re-check candidates.
-__global__ void __launch_bounds__(kPT) plane_pass1(const int2* __restrict__ sorted,
-                                                   const unsigned int* __restrict__ start,
-                                                   const unsigned int* __restrict__ tstart,
-                                                   const unsigned int* __restrict__ umap,
-                                                   Frame f, int shard, int nshards,
-                                                   long long ucap, float* __restrict__ umax,
-                                                   unsigned int* __restrict__ cand,
-                                                   Stats* __restrict__ st) {
-  __shared__ float4 sj[kPT];  // (a, b, |p|^2, -)
-  __shared__ float s_red[kPT / 32];
-  const long long units = (long long)st->plane_units;
-  if (st->bbox[3] < 0 || units > ucap) return;  // host re-runs with room
-  const PlaneSpace ps = plane_space(st);
-  long long u0, u1;
-  shard_span(units, shard, nshards, u0, u1);
-  float run0 = 0.f, run1 = 0.f, run2 = 0.f;  // per-axis maxima (registers, not an array)
-  for (long long u = u0 + blockIdx.x; u < u1; u += gridDim.x) {
-    const int p = (int)umap[u];
-    const int axis = plane_axis(p, ps);
-    const PlaneAxes ax = plane_axes(axis, st, f);
-    const unsigned int b0 = start[p], np = start[p + 1] - b0;
-    int I, J;
-    tile_pair(u - tstart[p], (np + kPT - 1) / kPT, I, J);
-    const unsigned int i = I * kPT + threadIdx.x, j = J * kPT + threadIdx.x;
-    const unsigned int jn = min((unsigned int)kPT, np - J * kPT);
-    __syncthreads();
-    if (j < np) {
-      const int2 k = sorted[b0 + j];
-      const float pa = (float)(k.x - ax.ca) * ax.ha, pb = (float)(k.y - ax.cb) * ax.hb;
-      sj[threadIdx.x] = make_float4(pa, pb, fmaf(pa, pa, pb * pb), 0.f);
-    }
-    __syncthreads();
-    float best = 0.f;
-    if (i < np) {
-      const int2 k = sorted[b0 + i];
-      const float pa = (float)(k.x - ax.ca) * ax.ha, pb = (float)(k.y - ax.cb) * ax.hb;
-      const float a2 = -2.f * pa, b2 = -2.f * pb;
-      float m = -3.0e38f;
-      unsigned int t = 0;
-      for (; t + 1 < jn; t += 2) {
-        const float4 q0 = sj[t], q1 = sj[t + 1];
-        m = fmax3f(m, fmaf(q0.y, b2, fmaf(q0.x, a2, q0.z)), fmaf(q1.y, b2, fmaf(q1.x, a2, q1.z)));
-      }
-      if (t < jn) m = fmaxf(m, fmaf(sj[t].y, b2, fmaf(sj[t].x, a2, sj[t].z)));
-      best = fmaxf(0.f, m + fmaf(pa, pa, pb * pb));
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
-    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = best;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int w = 1; w < kPT / 32; w++) best = fmaxf(best, s_red[w]);
-      umax[u] = best;
-      if (axis == 0) run0 = fmaxf(run0, best);
-      else if (axis == 1) run1 = fmaxf(run1, best);
-      else run2 = fmaxf(run2, best);
-    }
-  }
-  if (threadIdx.x == 0) {
-    if (run0 > 0.f) atomic_max_pos_f32(&st->pl_f32[0], run0);
-    if (run1 > 0.f) atomic_max_pos_f32(&st->pl_f32[1], run1);
-    if (run2 > 0.f) atomic_max_pos_f32(&st->pl_f32[2], run2);
-  }
-  if (!last_block(&st->done2)) return;
-  // Last block: candidates within kRefineRel of their axis maximum.
-  const float tau0 = __uint_as_float(__ldcg(&st->pl_f32[0])) * (1.f - kRefineRel);
-  const float tau1 = __uint_as_float(__ldcg(&st->pl_f32[1])) * (1.f - kRefineRel);
-  const float tau2 = __uint_as_float(__ldcg(&st->pl_f32[2])) * (1.f - kRefineRel);
-  const int lane = threadIdx.x & 31;
-  for (long long base = u0; base < u1; base += blockDim.x) {
-    const long long u = base + threadIdx.x;
-    bool hit = false;
-    if (u < u1) {
-      const int a = plane_axis((int)umap[u], ps);
-      hit = __ldcg(umax + u) >= (a == 0 ? tau0 : (a == 1 ? tau1 : tau2));
-    }
-    const unsigned int mask = __ballot_sync(0xffffffffu, hit);
-    if (!mask) continue;
-    unsigned long long pos = 0;
-    if (lane == 0) pos = atomicAdd(&st->n_pcand, (unsigned long long)__popc(mask));
-    pos = __shfl_sync(0xffffffffu, pos, 0);
-    if (hit) cand[pos + __popc(mask & ((1u << lane) - 1))] = (unsigned int)u;
-  }
-}
-
-// Exact planar re-check of the selected in-plane tile pairs (fp64, reference
-// arithmetic: the out-of-plane delta is exactly 0, so da*da + db*db is the
-// reference's 3-term sum bit for bit).
-__global__ void __launch_bounds__(kPT) plane_refine(const int2* __restrict__ sorted,
-                                                    const unsigned int* __restrict__ start,
-                                                    const unsigned int* __restrict__ tstart,
-                                                    const unsigned int* __restrict__ umap,
-                                                    Frame f, const unsigned int* __restrict__ cand,
-                                                    Stats* __restrict__ st) {
-  __shared__ double sa[kPT], sb[kPT];
-  __shared__ double s_red[kPT / 32];
-  if (st->bbox[3] < 0) return;
-  const PlaneSpace ps = plane_space(st);
-  const long long nc = (long long)st->n_pcand;
-  for (long long c = blockIdx.x; c < nc; c += gridDim.x) {
-    const unsigned int u = cand[c];
-    const int p = (int)umap[u];
-    const int axis = plane_axis(p, ps);
-    const PlaneAxes ax = plane_axes(axis, st, f);
-    const unsigned int b0 = start[p], np = start[p + 1] - b0;
-    int I, J;
-    tile_pair(u - tstart[p], (np + kPT - 1) / kPT, I, J);
-    const unsigned int i = I * kPT + threadIdx.x, j = J * kPT + threadIdx.x;
-    const unsigned int jn = min((unsigned int)kPT, np - J * kPT);
-    __syncthreads();
-    if (j < np) {
-      const int2 k = sorted[b0 + j];
-      sa[threadIdx.x] = ref_coord(k.x, ax.sa);
-      sb[threadIdx.x] = ref_coord(k.y, ax.sb);
-    }
-    __syncthreads();
-    double best = 0.0;
-    if (i < np) {
-      const int2 k = sorted[b0 + i];
-      const double ai = ref_coord(k.x, ax.sa), bi = ref_coord(k.y, ax.sb);
-      for (unsigned int t = 0; t < jn; t++) {
-        const double da = __dsub_rn(sa[t], ai), db = __dsub_rn(sb[t], bi);
-        best = fmax(best, __dadd_rn(__dmul_rn(da, da), __dmul_rn(db, db)));
-      }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
-    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = best;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int w = 1; w < kPT / 32; w++) best = fmax(best, s_red[w]);
-      if (best > 0.0) atomic_max_pos_f64(&st->sq[1 + axis], best);
-    }
-  }
 }
 
 // ---- generic fp64 cloud (diameters API) ------------------------------------

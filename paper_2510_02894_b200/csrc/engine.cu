@@ -35,10 +35,13 @@ __global__ void pack_bits_v16(const uint4*, uint32_t*, long long, int, int, Stat
 __global__ void pack_bits_generic(const uint8_t*, uint32_t*, long long, int, int, int, Stats*);
 __global__ void mc_cells(const uint32_t*, int, int, int, int, const CaseTables*, Stats*, int4*,
                          long long, unsigned int*, unsigned int*);
-__global__ void scan_all(unsigned int*, unsigned int*, unsigned int*, unsigned int*, unsigned int*,
-                         unsigned int*, unsigned int*, long long, int, Stats*);
+__global__ void plane_bins_scan(unsigned int*, unsigned int*, unsigned int*, unsigned long long*,
+                                const Stats*);
+__global__ void scan_all(unsigned int*, unsigned int*, const unsigned int*, unsigned int*,
+                         unsigned int*, unsigned int*, unsigned int*, unsigned int*, long long,
+                         long long, int, Stats*);
 __global__ void scatter_all(const int4*, long long, const Stats*, unsigned int*, int4*,
-                            unsigned int*, int2*);
+                            const unsigned int*, unsigned int*, int2*);
 __global__ void boxes_extremes(const int4*, long long, Frame, Stats*, int4*);
 __global__ void unit_filter(const int4*, const int4*, long long, Frame, int, Stats*,
                             unsigned int*);
@@ -47,11 +50,19 @@ __global__ void diam3d_pass1(const int4*, long long, Frame, int, int, const unsi
                              unsigned int*, Stats*);
 __global__ void diam3d_refine(const int4*, long long, Frame, const unsigned int*,
                               const unsigned int*, Stats*);
+__global__ void plane_boxes(const int2*, const unsigned int*, const unsigned int*,
+                            const unsigned int*, Frame, const Stats*, int4*, unsigned long long*);
+__global__ void plane_lb(const int2*, const unsigned int*, const unsigned long long*, Frame,
+                         Stats*);
+__global__ void plane_filter(const unsigned int*, const unsigned int*, const unsigned int*,
+                             const unsigned int*, const int4*, Frame, int, long long, Stats*,
+                             unsigned int*);
 __global__ void plane_pass1(const int2*, const unsigned int*, const unsigned int*,
-                            const unsigned int*, Frame, int, int, long long, float*, unsigned int*,
-                            Stats*);
+                            const unsigned int*, const unsigned int*, Frame, int, int, long long,
+                            float*, unsigned int*, Stats*);
 __global__ void plane_refine(const int2*, const unsigned int*, const unsigned int*,
-                             const unsigned int*, Frame, const unsigned int*, Stats*);
+                             const unsigned int*, const unsigned int*, Frame,
+                             const unsigned int*, Stats*);
 __global__ void cloud_diameters(const double*, const double*, const double*, long long, int,
                                 unsigned long long*);
 template <int MODE>
@@ -63,7 +74,6 @@ using namespace sc;
 
 namespace {
 
-constexpr int kMcPlaneSmem = 160 * 1024;  // mc_cells plane histogram (dynamic smem) limit
 thread_local std::string g_err;
 std::atomic<bool> g_opt_prune{true}, g_opt_packed{true}, g_opt_graphs{true};
 std::atomic<unsigned long long> g_launches{0};
@@ -173,7 +183,7 @@ struct Ctx {
   cudaEvent_t kev[8] = {};      // per-kernel boundaries of the last ROI
   double last_ms[7] = {0, 0, 0, 0, 0, 0, 0};  // pack, mc, prune, pass1, refine, planar, h2d
   long long cap_floor = 0, dcap_floor = 0;  // raised by overflow re-runs only
-  long long last_diag[5] = {0, 0, 0, 0, 0};
+  long long last_diag[6] = {0, 0, 0, 0, 0, 0};
   int occ_pass1 = 1, occ_pass1s = 1, occ_plane = 1, occ_pack = 1;  // resident blocks/SM
   Stats* d_stats = nullptr;
   Stats* h_stats = nullptr;  // pinned
@@ -182,8 +192,11 @@ struct Ctx {
   DevBuf<int4> keys, keys_sorted, boxes;
   DevBuf<unsigned int> sort_counts, sort_cursor, work;
   DevBuf<float> warp_max, plane_umax;
-  DevBuf<unsigned int> cand, plane_cand, plane_umap;
-  DevBuf<unsigned int> plane_counts, plane_start, plane_cursor, plane_tstart;
+  DevBuf<unsigned int> cand, plane_cand, plane_umap, plane_cmap, plane_work;
+  DevBuf<unsigned int> plane_counts, plane_start, plane_tstart, plane_cstart;
+  DevBuf<unsigned int> pbin_counts, pbin_cursor;
+  DevBuf<unsigned long long> plane_ext;
+  DevBuf<int4> plane_boxes_buf;
   DevBuf<int2> plane_sorted;
   DevBuf<uint8_t> mask_stage;
   DevBuf<double> cloud;
@@ -210,8 +223,9 @@ struct Ctx {
     unsigned long long h = 1469598103934665603ull;
     const void* ps[] = {bits.p, keys.p, keys_sorted.p, boxes.p, sort_counts.p, sort_cursor.p,
                         work.p, warp_max.p, plane_umax.p, cand.p, plane_cand.p, plane_umap.p,
-                        plane_counts.p, plane_start.p, plane_cursor.p, plane_tstart.p,
-                        plane_sorted.p};
+                        plane_counts.p, plane_start.p, plane_tstart.p, plane_sorted.p,
+                        plane_cmap.p, plane_work.p, plane_cstart.p, pbin_counts.p, pbin_cursor.p,
+                        plane_ext.p, plane_boxes_buf.p};
     for (const void* p : ps) h = (h ^ (unsigned long long)(uintptr_t)p) * 1099511628211ull;
     return h;
   }
@@ -262,7 +276,6 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     if (const char* v = getenv("SC_PRUNE")) g_opt_prune = std::strcmp(v, "0") != 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_plane, plane_pass1, 256, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pack, pack_bits_v16<4>, 256, 0));
-    CK(cudaFuncSetAttribute(mc_cells, cudaFuncAttributeMaxDynamicSharedMemorySize, kMcPlaneSmem));
     {
       // Lazy module loading must not happen inside a stream capture: touch
       // every kernel once here.
@@ -273,7 +286,9 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
                                (const void*)boxes_extremes, (const void*)unit_filter,
                                (const void*)diam3d_pass1<true>, (const void*)diam3d_pass1<false>,
                                (const void*)diam3d_refine, (const void*)plane_pass1,
-                               (const void*)plane_refine, (const void*)cloud_diameters};
+                               (const void*)plane_refine, (const void*)cloud_diameters,
+                               (const void*)plane_bins_scan, (const void*)plane_boxes,
+                               (const void*)plane_lb, (const void*)plane_filter};
       for (const void* k : kernels) CK(cudaFuncGetAttributes(&fa, k));
     }
     g_ctx[device][slot] = std::move(c);
@@ -287,12 +302,6 @@ int check_input(const void* mask, int64_t nx, int64_t ny, int64_t nz, const doub
   if (nx < 1 || ny < 1 || nz < 1) {
     set_err("dims must all be >= 1, got (%lld, %lld, %lld)", (long long)nx, (long long)ny,
             (long long)nz);
-    return SC_ERR_INPUT;
-  }
-  // mc_cells keeps one plane counter per doubled key in shared memory.
-  if ((2 * (nx + ny + nz) + 9) * 4 > 160 * 1024) {
-    set_err("dims (%lld, %lld, %lld): nx+ny+nz too large for the planar histogram",
-            (long long)nx, (long long)ny, (long long)nz);
     return SC_ERR_INPUT;
   }
   // Doubled lattice keys and fp32 frame coordinates must stay exact.
@@ -316,6 +325,7 @@ double f64_of(unsigned long long bits) {
 }
 
 constexpr long long kChunk = 256;  // diameter.cu kChunk: pair unit = chunk x chunk
+constexpr long long kPlaneBinsHost = 256;  // sc_device.cuh kPlaneBins
 
 // Stage events: inside a capture they must be external event nodes so that
 // graph replays record them (plain records only order the capture).
@@ -354,24 +364,29 @@ int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, lo
       CK(cudaMemset(c->sort_counts.p, 0, sizeof(unsigned int) * c->sort_counts.cap));
   }
   const long long P = 2 * (nx + ny + nz) + 9;
-  {
-    unsigned int* before = c->plane_counts.p;
-    CK(c->plane_counts.ensure((size_t)P));
-    if (c->plane_counts.p != before)
-      CK(cudaMemset(c->plane_counts.p, 0, sizeof(unsigned int) * c->plane_counts.cap));
-  }
+  CK(c->plane_counts.ensure((size_t)P));
   CK(c->plane_start.ensure((size_t)P + 1));
-  CK(c->plane_cursor.ensure((size_t)P));
   CK(c->plane_tstart.ensure((size_t)P + 1));
+  CK(c->plane_cstart.ensure((size_t)P + 1));
+  CK(c->plane_ext.ensure((size_t)P * 8));
+  {
+    unsigned int* before = c->pbin_counts.p;  // self-cleaning after the first zeroing
+    CK(c->pbin_counts.ensure((size_t)P * kPlaneBinsHost));
+    if (c->pbin_counts.p != before)
+      CK(cudaMemset(c->pbin_counts.p, 0, sizeof(unsigned int) * c->pbin_counts.cap));
+    CK(c->pbin_cursor.ensure((size_t)P * kPlaneBinsHost));
+  }
   CK(c->plane_sorted.ensure((size_t)(3 * dcap)));
-  // planar tile pairs: sum over planes of t(t+1)/2, t = ceil(n_p/256); bounded
-  // by (3 dcap / 256)^2 / 2 + P, far below in practice: size for the bound
-  // with a 64-plane spread.
+  // planar tile pairs: sum over planes of t(t+1)/2, t = ceil(n_p/256); sized
+  // for a 64-tile spread (overflow is detected on the device and re-run).
   const long long t = (3 * dcap) / 256 + 1;
   const long long pu = std::max(std::min(t * (t + 1) / 2, t * 64) + P + 1, punits);
   CK(c->plane_umax.ensure((size_t)pu));
   CK(c->plane_cand.ensure((size_t)pu));
   CK(c->plane_umap.ensure((size_t)pu));
+  CK(c->plane_work.ensure((size_t)pu));
+  CK(c->plane_cmap.ensure((size_t)(t + P + 1)));
+  CK(c->plane_boxes_buf.ensure((size_t)(t + P + 1)));
   return SC_OK;
 }
 
@@ -405,13 +420,11 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
   }
   CKL(1);
   CK(record(c, c->kev[1], s));
-  const long long Pmax = 2 * (nx + ny + nz) + 9;
   int mc_occ = 1;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mc_occ, mc_cells, 256,
-                                                   Pmax * sizeof(unsigned int)));
-  mc_cells<<<c->sms * std::max(1, mc_occ), 256, Pmax * sizeof(unsigned int), s>>>(
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mc_occ, mc_cells, 256, 0));
+  mc_cells<<<c->sms * std::max(1, mc_occ), 256, 0, s>>>(
       c->bits.p, (int)nx, (int)ny, (int)nz, W, c->d_tabs, c->d_stats, c->keys.p, cap,
-      c->sort_counts.p, c->plane_counts.p);
+      c->sort_counts.p, c->pbin_counts.p);
   CKL(1);
   CK(record(c, c->kev[2], s));
 
@@ -428,19 +441,26 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
   const int pgrid = c->sms * std::max(1, g_opt_packed.load() ? c->occ_pass1 : c->occ_pass1s);
   const int plgrid = c->sms * std::max(1, c->occ_plane);
   const long long pucap = (long long)c->plane_umax.cap;
+  const long long pccap = (long long)c->plane_cmap.cap;
+  const int prune = g_opt_prune.load() ? 1 : 0;
 
-  // Orders (Morton bricks, planes), chunk boxes + extremes, exact LB + pruning.
+  // Orders (Morton bricks; planes by in-plane brick), chunk boxes + extremes,
+  // exact lower bound, pruned 3-D work list.
+  plane_bins_scan<<<c->sms * 2, 256, 0, s>>>(c->pbin_counts.p, c->pbin_cursor.p,
+                                             c->plane_counts.p, c->plane_ext.p, c->d_stats);
+  CKL(1);
   scan_all<<<2, 1024, 0, s>>>(c->sort_counts.p, c->sort_cursor.p, c->plane_counts.p,
-                              c->plane_start.p, c->plane_cursor.p, c->plane_tstart.p,
-                              c->plane_umap.p, pucap, 256, c->d_stats);
+                              c->plane_start.p, c->plane_tstart.p, c->plane_cstart.p,
+                              c->plane_umap.p, c->plane_cmap.p, pucap, pccap, 256, c->d_stats);
   CKL(1);
   scatter_all<<<c->sms * 4, 256, 0, s>>>(c->keys.p, dcap, c->d_stats, c->sort_cursor.p,
-                                         c->keys_sorted.p, c->plane_cursor.p, c->plane_sorted.p);
+                                         c->keys_sorted.p, c->plane_start.p, c->pbin_cursor.p,
+                                         c->plane_sorted.p);
   CKL(1);
   boxes_extremes<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, f, c->d_stats, c->boxes.p);
   CKL(1);
-  unit_filter<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, c->boxes.p, dcap, f,
-                                         g_opt_prune.load() ? 1 : 0, c->d_stats, c->work.p);
+  unit_filter<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, c->boxes.p, dcap, f, prune,
+                                         c->d_stats, c->work.p);
   CKL(1);
   CK(record(c, c->kev[3], s));
   if (g_opt_packed.load())
@@ -455,12 +475,23 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
                                            c->d_stats);
   CKL(1);
   CK(record(c, c->kev[5], s));
+  plane_boxes<<<c->sms * 2, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_cstart.p,
+                                         c->plane_cmap.p, f, c->d_stats, c->plane_boxes_buf.p,
+                                         c->plane_ext.p);
+  CKL(1);
+  plane_lb<<<c->sms, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_ext.p, f,
+                                  c->d_stats);
+  CKL(1);
+  plane_filter<<<c->sms * 4, 256, 0, s>>>(c->plane_start.p, c->plane_tstart.p, c->plane_cstart.p,
+                                          c->plane_umap.p, c->plane_boxes_buf.p, f, prune, pucap,
+                                          c->d_stats, c->plane_work.p);
+  CKL(1);
   plane_pass1<<<plgrid, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_tstart.p,
-                                     c->plane_umap.p, f, shard, nshards, pucap, c->plane_umax.p,
-                                     c->plane_cand.p, c->d_stats);
+                                     c->plane_umap.p, c->plane_work.p, f, shard, nshards, pucap,
+                                     c->plane_umax.p, c->plane_cand.p, c->d_stats);
   CKL(1);
   plane_refine<<<c->sms * 2, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p,
-                                          c->plane_tstart.p, c->plane_umap.p, f,
+                                          c->plane_tstart.p, c->plane_umap.p, c->plane_work.p, f,
                                           c->plane_cand.p, c->d_stats);
   CKL(1);
   CK(record(c, c->kev[6], s));
@@ -633,6 +664,7 @@ int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
     c->last_diag[2] = (long long)h.n_cand;
     c->last_diag[3] = (long long)h.plane_units;
     c->last_diag[4] = (long long)h.n_pcand;
+    c->last_diag[5] = (long long)h.n_pwork;
   }
   out->mesh_ms = ev_ms(c->kev[0], c->kev[2]);
   out->diameters_ms = ev_ms(c->kev[2], c->kev[6]);
@@ -896,7 +928,7 @@ int sc_last_diagnostics(int device, int64_t* out, int n) {
   int rc = get_ctx(device, &c);
   if (rc) return -rc;
   std::lock_guard<std::mutex> lk(c->mu);
-  int m = n < 5 ? n : 5;
+  int m = n < 6 ? n : 6;
   for (int i = 0; i < m; i++) out[i] = c->last_diag[i];
   return m;
 }

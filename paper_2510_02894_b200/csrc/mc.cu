@@ -191,30 +191,28 @@ __device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits, int
 // points u = 32q - 1 + i, i in [0, 31].  All 2*(kZChunk+1) row words are
 // loaded up front (L2-resident bit volume; latency, not bandwidth, bound).
 //
-// Every emitted vertex is also counted into two block-private histograms that
-// the diameter stage needs: its Morton brick (spatial sort) and its three
-// planes (planar pass).  They are flushed once per block (nonzero bins only).
+// Every emitted vertex is also counted into the histograms the diameter stage
+// sorts by: its 3-D Morton brick (block-private, flushed once per block) and
+// its (plane, in-plane brick) bin in each of its three planes (global).
 __global__ void __launch_bounds__(256) mc_cells(const uint32_t* __restrict__ bits, int nx, int ny,
                                                 int nz, int W, const CaseTables* __restrict__ tabs,
                                                 Stats* __restrict__ st, int4* __restrict__ vkeys,
                                                 long long cap, unsigned int* __restrict__ sort_counts,
-                                                unsigned int* __restrict__ plane_counts) {
+                                                unsigned int* __restrict__ pbin_counts) {
   __shared__ unsigned int s_hist[kNumCases];
   __shared__ int4 s_tn[kNumCases];
   __shared__ unsigned int s_bin[kSortBins];
-  extern __shared__ unsigned int s_plane[];  // P = cnt0 + cnt1 + cnt2 bins
   int bb[6];
 #pragma unroll
   for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
   const PlaneSpace ps = plane_space(bb);
-  const int P = bb[3] >= 0 ? ps.cnt[0] + ps.cnt[1] + ps.cnt[2] : 0;
+  const PlaneBricks pbk = plane_bricks(bb);
   const int bshift = brick_shift(bb);
   for (int i = threadIdx.x; i < kNumCases; i += blockDim.x) {
     s_hist[i] = 0;
     s_tn[i] = tabs->tn[i];
   }
   for (int i = threadIdx.x; i < kSortBins; i += blockDim.x) s_bin[i] = 0;
-  for (int i = threadIdx.x; i < P; i += blockDim.x) s_plane[i] = 0;
   __syncthreads();
 
   const int xmin = bb[0], ymin = bb[1], zmin = bb[2];
@@ -298,10 +296,12 @@ __global__ void __launch_bounds__(256) mc_cells(const uint32_t* __restrict__ bit
             o++;
             atomicAdd(&s_bin[brick_bin(X, Y, Z, bb, bshift)], 1u);
             int id[3];
+            unsigned int pbin[3];
             plane_ids(X, Y, Z, ps, id);
-            atomicAdd(&s_plane[id[0]], 1u);
-            atomicAdd(&s_plane[id[1]], 1u);
-            atomicAdd(&s_plane[id[2]], 1u);
+            plane_bins(X, Y, Z, pbk, pbin);
+#pragma unroll
+            for (int a = 0; a < 3; a++)
+              atomicAdd(&pbin_counts[(long long)id[a] * kPlaneBins + pbin[a]], 1u);
           };
           while (ex) {
             const int i = __ffs(ex) - 1; ex &= ex - 1;
@@ -329,8 +329,6 @@ __global__ void __launch_bounds__(256) mc_cells(const uint32_t* __restrict__ bit
     if (s_hist[i]) atomicAdd(&st->hist[i], (unsigned long long)s_hist[i]);
   for (int i = threadIdx.x; i < kSortBins; i += blockDim.x)
     if (s_bin[i]) atomicAdd(&sort_counts[i], s_bin[i]);
-  for (int i = threadIdx.x; i < P; i += blockDim.x)
-    if (s_plane[i]) atomicAdd(&plane_counts[i], s_plane[i]);
 }
 
 template __global__ void pack_bits_v16<4>(const uint4*, uint32_t*, long long, int, int, Stats*);

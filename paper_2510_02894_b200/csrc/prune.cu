@@ -35,17 +35,20 @@ __device__ __forceinline__ unsigned int plane_tiles(unsigned int np, int pt) {
 }
 
 // Two blocks of 1024 threads.  Block 0: exclusive scan of the 4096 brick
-// counts -> sort cursor.  Block 1: plane populations -> start / cursor, their
-// tile-pair counts -> tstart and the unit -> plane map.  Both zero their
-// histograms for the next ROI (mc_cells accumulates into them).
+// counts -> sort cursor (and zero the counts for the next ROI).  Block 1:
+// plane populations (plane_bins_scan) -> start; in-plane tile pairs -> tstart
+// and the unit -> plane map; in-plane 256-entry chunks -> cstart and the
+// chunk -> plane map.
 __global__ void __launch_bounds__(1024) scan_all(unsigned int* __restrict__ sort_counts,
                                                  unsigned int* __restrict__ sort_cursor,
-                                                 unsigned int* __restrict__ plane_counts,
+                                                 const unsigned int* __restrict__ plane_counts,
                                                  unsigned int* __restrict__ start,
-                                                 unsigned int* __restrict__ cursor,
                                                  unsigned int* __restrict__ tstart,
-                                                 unsigned int* __restrict__ umap, long long ucap,
-                                                 int plane_tile, Stats* __restrict__ st) {
+                                                 unsigned int* __restrict__ cstart,
+                                                 unsigned int* __restrict__ umap,
+                                                 unsigned int* __restrict__ cmap, long long ucap,
+                                                 long long ccap, int plane_tile,
+                                                 Stats* __restrict__ st) {
   int bb[6];
 #pragma unroll
   for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
@@ -72,39 +75,49 @@ __global__ void __launch_bounds__(1024) scan_all(unsigned int* __restrict__ sort
   const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
   const int per = (P + 1023) / 1024;
   const int b = threadIdx.x * per, e = min(P, b + per);
-  unsigned int s1 = 0, s2 = 0;
+  unsigned int s1 = 0, s2 = 0, s3 = 0;
   for (int i = b; i < e; i++) {
     const unsigned int v = plane_counts[i];
     s1 += v;
     s2 += plane_tiles(v, plane_tile);
+    s3 += v >= 2 ? (v + plane_tile - 1) / plane_tile : 0u;
   }
-  unsigned int t1, t2;
+  unsigned int t1, t2, t3;
   unsigned int r1 = block_exscan_1024(s1, &t1);
   unsigned int r2 = block_exscan_1024(s2, &t2);
+  unsigned int r3 = block_exscan_1024(s3, &t3);
   for (int i = b; i < e; i++) {
     const unsigned int v = plane_counts[i];
     const unsigned int nt = plane_tiles(v, plane_tile);
-    start[i] = cursor[i] = r1;
+    const unsigned int nc = v >= 2 ? (v + plane_tile - 1) / plane_tile : 0u;
+    start[i] = r1;
     tstart[i] = r2;
+    cstart[i] = r3;
     if ((long long)t2 <= ucap)
       for (unsigned int u = 0; u < nt; u++) umap[r2 + u] = (unsigned int)i;
-    plane_counts[i] = 0u;
+    if ((long long)t3 <= ccap)
+      for (unsigned int u = 0; u < nc; u++) cmap[r3 + u] = (unsigned int)i;
     r1 += v;
     r2 += nt;
+    r3 += nc;
   }
   if (threadIdx.x == 0) {
     start[P] = t1;
     tstart[P] = t2;
+    cstart[P] = t3;
     st->plane_units = t2;
+    st->plane_chunks = t3;
   }
 }
 
 // Counting-sort scatter: keys into Morton-brick order (keys_sorted), and the
-// in-plane coordinates of every vertex into its three plane lists:
-// XY -> (X, Y), XZ -> (X, Z), YZ -> (Y, Z).
+// in-plane coordinates of every vertex into its three plane lists, each in
+// in-plane brick order: XY -> (X, Y), XZ -> (X, Z), YZ -> (Y, Z).
 __global__ void scatter_all(const int4* __restrict__ keys, long long cap,
                             const Stats* __restrict__ st, unsigned int* __restrict__ sort_cursor,
-                            int4* __restrict__ keys_sorted, unsigned int* __restrict__ plane_cursor,
+                            int4* __restrict__ keys_sorted,
+                            const unsigned int* __restrict__ plane_start,
+                            unsigned int* __restrict__ pbin_cursor,
                             int2* __restrict__ plane_sorted) {
   const long long n = n_verts(st, cap);
   int bb[6];
@@ -112,27 +125,32 @@ __global__ void scatter_all(const int4* __restrict__ keys, long long cap,
   for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
   const int s = brick_shift(bb);
   const PlaneSpace ps = plane_space(bb);
+  const PlaneBricks pbk = plane_bricks(bb);
   for (long long base = (long long)blockIdx.x * blockDim.x; base < n;
        base += (long long)gridDim.x * blockDim.x) {
     const long long v = base + threadIdx.x;
     const bool ok = v < n;
     int4 k = make_int4(0, 0, 0, 0);
     int id[3] = {0, 0, 0};
+    unsigned int pb[3] = {0u, 0u, 0u};
     unsigned int bin = 0;
     if (ok) {
       k = keys[v];
       bin = brick_bin(k.x, k.y, k.z, bb, s);
       plane_ids(k.x, k.y, k.z, ps, id);
+      plane_bins(k.x, k.y, k.z, pbk, pb);
     }
     const unsigned int pk = group_add(sort_cursor, bin, ok);
-    const unsigned int p0 = group_add(plane_cursor, (unsigned int)id[0], ok);
-    const unsigned int p1 = group_add(plane_cursor, (unsigned int)id[1], ok);
-    const unsigned int p2 = group_add(plane_cursor, (unsigned int)id[2], ok);
+    unsigned int pos[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+      pos[a] = group_add(pbin_cursor, (unsigned int)id[a] * kPlaneBins + pb[a], ok) +
+               (ok ? plane_start[id[a]] : 0u);
     if (ok) {
       keys_sorted[pk] = k;
-      plane_sorted[p0] = make_int2(k.x, k.y);
-      plane_sorted[p1] = make_int2(k.x, k.z);
-      plane_sorted[p2] = make_int2(k.y, k.z);
+      plane_sorted[pos[0]] = make_int2(k.x, k.y);
+      plane_sorted[pos[1]] = make_int2(k.x, k.z);
+      plane_sorted[pos[2]] = make_int2(k.y, k.z);
     }
   }
 }
@@ -215,19 +233,6 @@ __global__ void __launch_bounds__(256) boxes_extremes(const int4* __restrict__ k
     atomicMax(&st->ext[threadIdx.x], s_ext[threadIdx.x]);
 }
 
-// Upper-triangle pair index -> (I, J), I <= J (as diameter.cu).
-__device__ __forceinline__ void tile_pair_p(long long t, long long T, int& I, int& J) {
-  double b = 2.0 * T + 1.0;
-  long long i = (long long)((b - sqrt(b * b - 8.0 * (double)t)) * 0.5);
-  if (i < 0) i = 0;
-  if (i > T - 1) i = T - 1;
-  auto off = [T](long long r) { return r * T - r * (r - 1) / 2; };
-  while (i > 0 && off(i) > t) i--;
-  while (i < T - 1 && off(i + 1) <= t) i++;
-  I = (int)i;
-  J = (int)(i + (t - off(i)));
-}
-
 __device__ __forceinline__ double axis_reach(int loA, int hiA, int loB, int hiB, double h) {
   const double d = (double)max(hiA - loB, hiB - loA) * h;
   return d * d;
@@ -283,7 +288,7 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
         keep = true;
       } else {
         int I, J;
-        tile_pair_p(u, C, I, J);
+        tile_pair(u, C, I, J);
         const int4 ilo = boxes[2 * I], ihi = boxes[2 * I + 1];
         const int4 jlo = boxes[2 * J], jhi = boxes[2 * J + 1];
         const double ub = axis_reach(ilo.x, ihi.x, jlo.x, jhi.x, hx) +

@@ -26,6 +26,9 @@ struct Stats {
   unsigned long long lb;               // fp64 bits: exact squared distance lower bound
   unsigned long long n_work;           // surviving 3-D work units after pruning
   unsigned int done1, done2;           // block tickets (last-block selection); self-resetting
+  unsigned long long plb[3];           // fp64 bits: exact planar lower bounds per family
+  unsigned long long n_pwork;          // surviving planar units after pruning
+  unsigned long long plane_chunks;     // 256-entry chunks over all planes
 };
 
 // Per-case integer tables for the exact volume path: for case k,
@@ -94,6 +97,50 @@ __device__ __forceinline__ void plane_ids(int X, int Y, int Z, const PlaneSpace&
   out[2] = ps.cnt[0] + ps.cnt[1] + (X - ps.lo[2]);
 }
 
+// In-plane bricks: each plane family is bucketed by a 16 x 16 Morton brick of
+// its two in-plane doubled coordinates (256 bins per plane), so every plane's
+// vertex list comes out spatially compact (enables exact planar pruning).
+constexpr int kPlaneBins = 256;
+
+__device__ __forceinline__ int axis_shift(int lo, int hi) {  // voxel bbox [lo, hi]
+  const int ext = 2 * (hi - lo) + 3;
+  int s = 0;
+  while ((ext >> s) >= 16) s++;
+  return s;
+}
+
+__device__ __forceinline__ unsigned int spread2x4(unsigned int v) {  // 4 bits -> even bits
+  v &= 15u;
+  v = (v | (v << 2)) & 0x33u;
+  v = (v | (v << 1)) & 0x55u;
+  return v;
+}
+
+struct PlaneBricks {
+  int lo[3];     // smallest doubled key per axis (x, y, z)
+  int shift[3];  // brick shift per axis (<= 16 bricks)
+};
+
+__device__ __forceinline__ PlaneBricks plane_bricks(const int* bb) {
+  PlaneBricks pb;
+  for (int a = 0; a < 3; a++) {
+    pb.lo[a] = 2 * bb[a] - 1;
+    pb.shift[a] = axis_shift(bb[a], bb[a + 3]);
+  }
+  return pb;
+}
+
+// Bin of a vertex inside each of its three planes (XY: (X,Y), XZ: (X,Z), YZ: (Y,Z)).
+__device__ __forceinline__ void plane_bins(int X, int Y, int Z, const PlaneBricks& pb,
+                                           unsigned int out[3]) {
+  const unsigned int bx = (unsigned int)(X - pb.lo[0]) >> pb.shift[0];
+  const unsigned int by = (unsigned int)(Y - pb.lo[1]) >> pb.shift[1];
+  const unsigned int bz = (unsigned int)(Z - pb.lo[2]) >> pb.shift[2];
+  out[0] = spread2x4(bx) | (spread2x4(by) << 1);
+  out[1] = spread2x4(bx) | (spread2x4(bz) << 1);
+  out[2] = spread2x4(by) | (spread2x4(bz) << 1);
+}
+
 // Warp-aggregated increment: lanes with equal `id` share one global atomic.
 // Returns this lane's slot within its group's reservation.  All lanes call.
 __device__ __forceinline__ unsigned int group_add(unsigned int* base, unsigned int id, bool ok) {
@@ -122,6 +169,88 @@ __device__ __forceinline__ bool last_block(unsigned int* ticket) {
   }
   return s_last;
 }
+
+// ---- helpers shared by the diameter, pruning and planar kernels ----
+// Relative margin of the re-check threshold.  Pass-1 error is below ~1e-6 of
+// D^2; a unit whose pass-1 maximum is below M*(1 - kRefineRel)
+// provably cannot hold the exact maximum pair.
+constexpr float kRefineRel = 8e-6f;
+
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// Upper-triangle pair index -> (I, J), I <= J, row-major over I.
+__device__ __forceinline__ void tile_pair(long long t, long long T, int& I, int& J) {
+  double b = 2.0 * T + 1.0;
+  long long i = (long long)((b - sqrt(b * b - 8.0 * (double)t)) * 0.5);
+  if (i < 0) i = 0;
+  if (i > T - 1) i = T - 1;
+  auto off = [T](long long r) { return r * T - r * (r - 1) / 2; };
+  while (i > 0 && off(i) > t) i--;
+  while (i < T - 1 && off(i + 1) <= t) i++;
+  I = (int)i;
+  J = (int)(i + (t - off(i)));
+}
+
+__device__ __forceinline__ long long n_vertices(const Stats* st, long long cap) {
+  long long n = (long long)st->n_vert;
+  return n < cap ? n : cap;
+}
+
+// Bbox-centred fp32 frame: centre (doubled units) from the MC bbox.
+__device__ __forceinline__ void frame_centre(const Stats* st, Frame& f) {
+  f.cx2 = st->bbox[0] + st->bbox[3];
+  f.cy2 = st->bbox[1] + st->bbox[4];
+  f.cz2 = st->bbox[2] + st->bbox[5];
+}
+
+__device__ __forceinline__ float3 frame_coord(int4 k, const Frame& f) {
+  return make_float3((float)(k.x - f.cx2) * f.hx, (float)(k.y - f.cy2) * f.hy,
+                     (float)(k.z - f.cz2) * f.hz);
+}
+
+__device__ __forceinline__ void shard_span(long long n, int shard, int nshards, long long& a,
+                                           long long& b) {
+  a = n * shard / nshards;
+  b = n * (shard + 1) / nshards;
+}
+
+__device__ __forceinline__ long long tri(long long T) { return T * (T + 1) / 2; }
+
+
+__device__ __forceinline__ PlaneSpace plane_space(const Stats* st) {
+  int bb[6];
+#pragma unroll
+  for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
+  return plane_space(bb);
+}
+
+struct PlaneAxes {  // in-plane (a, b) coordinate frame of one plane family
+  int ca, cb;       // centre, doubled units
+  float ha, hb;     // fp32 half spacings
+  double sa, sb;    // fp64 spacings
+};
+
+__device__ __forceinline__ PlaneAxes plane_axes(int axis, const Stats* st, const Frame& f) {
+  const int* bb = st->bbox;
+  PlaneAxes x;
+  if (axis == 0) {         // XY plane: (X, Y)
+    x.ca = bb[0] + bb[3]; x.cb = bb[1] + bb[4]; x.ha = f.hx; x.hb = f.hy; x.sa = f.sx; x.sb = f.sy;
+  } else if (axis == 1) {  // XZ plane: (X, Z)
+    x.ca = bb[0] + bb[3]; x.cb = bb[2] + bb[5]; x.ha = f.hx; x.hb = f.hz; x.sa = f.sx; x.sb = f.sz;
+  } else {                 // YZ plane: (Y, Z)
+    x.ca = bb[1] + bb[4]; x.cb = bb[2] + bb[5]; x.ha = f.hy; x.hb = f.hz; x.sa = f.sy; x.sb = f.sz;
+  }
+  return x;
+}
+
+__device__ __forceinline__ int plane_axis(int p, const PlaneSpace& ps) {
+  return p < ps.cnt[0] ? 0 : (p < ps.cnt[0] + ps.cnt[1] ? 1 : 2);
+}
+
 
 // Exclusive scan of one value per thread across a 1024-thread block (warp
 // shuffles, two levels, 2 barriers).  Returns the exclusive prefix; *total
