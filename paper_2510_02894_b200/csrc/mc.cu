@@ -70,67 +70,48 @@ struct BoxAcc {
   }
 };
 
-// Fast path: nx % 32 == 0 and a 16-byte aligned mask.  One 16-byte chunk per
-// thread per step (a warp reads 512 contiguous bytes per load instruction);
-// lane pairs merge their 16-bit halves into one 32-bit word.  U chunks are in
-// flight per thread for memory-level parallelism.  The host sizes the grid so
-// the grid stride is a whole number of rows: each thread then keeps a fixed
-// x column per k and advances (y, z) incrementally -- no divisions in the loop.
-template <int U>
-__global__ void __launch_bounds__(256) pack_bits_v16(const uint4* __restrict__ mask,
-                                                     uint32_t* __restrict__ bits,
-                                                     long long n_chunks, int C16, int ny,
-                                                     Stats* __restrict__ st) {
+// Fast path: nx % 32 == 0 and a 16-byte aligned mask.  A warp owns whole rows
+// (y, z): lane l loads 16-byte chunk l of the row (a warp reads 512
+// contiguous bytes per load instruction), lane pairs merge their 16-bit
+// halves into one 32-bit word.  RPI rows are in flight per warp; the row's
+// (y, z) and the bbox update are per row (warp-uniform), not per chunk.
+template <int RPI>
+__global__ void __launch_bounds__(256, 3) pack_bits_v16(const uint4* __restrict__ mask,
+                                                     uint32_t* __restrict__ bits, int n_rows,
+                                                     int C16, int ny, Stats* __restrict__ st) {
   BoxAcc box;
-  const long long step = (long long)gridDim.x * blockDim.x * U;
-  const long long rowstep = step / C16;
-  const int dy = (int)(rowstep % ny), dz = (int)(rowstep / ny);
-  int col[U], y[U], z[U];
+  const int lane = threadIdx.x & 31;
+  const int W = C16 >> 1;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  for (int r0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RPI; r0 < n_rows;
+       r0 += nwarps * RPI) {
+    for (int cb = 0; cb < C16; cb += 32) {
+      const int c = cb + lane;
+      uint4 v[RPI];
 #pragma unroll
-  for (int k = 0; k < U; k++) {
-    const long long g0 = (long long)blockIdx.x * blockDim.x * U + (long long)k * blockDim.x + threadIdx.x;
-    const long long row0 = g0 / C16;
-    col[k] = (int)(g0 - row0 * C16);
-    y[k] = (int)(row0 % ny);
-    z[k] = (int)(row0 / ny);
-  }
-  // Software pipeline: the next step's U loads are in flight while this
-  // step's chunks are converted.
-  uint4 v[U];
-  long long base = (long long)blockIdx.x * blockDim.x * U;
+      for (int k = 0; k < RPI; k++) {
+        const int r = r0 + k;
+        v[k] = (r < n_rows && c < C16) ? __ldcs(mask + (size_t)r * C16 + c) : make_uint4(0, 0, 0, 0);
+      }
 #pragma unroll
-  for (int k = 0; k < U; k++) {
-    const long long g = base + (long long)k * blockDim.x + threadIdx.x;
-    v[k] = g < n_chunks ? __ldcs(mask + g) : make_uint4(0, 0, 0, 0);
-  }
-  for (; base < n_chunks; base += step) {
-    uint4 nv[U];
-#pragma unroll
-    for (int k = 0; k < U; k++) {
-      const long long g = base + step + (long long)k * blockDim.x + threadIdx.x;
-      nv[k] = g < n_chunks ? __ldcs(mask + g) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int k = 0; k < U; k++) {
-      const long long g = base + (long long)k * blockDim.x + threadIdx.x;
-      const uint32_t b16 = nib4(v[k].x) | (nib4(v[k].y) << 4) | (nib4(v[k].z) << 8) |
-                           (nib4(v[k].w) << 12);
-      const uint32_t hi = __shfl_down_sync(kFull, b16, 1);
-      if (!(threadIdx.x & 1) && g < n_chunks) {
-        const uint32_t word = b16 | (hi << 16);
-        bits[g >> 1] = word;
-        if (word) {
-          const int xb = 16 * col[k];
-          box.x0 = min(box.x0, xb + __ffs(word) - 1);
-          box.x1 = max(box.x1, xb + 31 - __clz(word));
-          box.y0 = min(box.y0, y[k]); box.y1 = max(box.y1, y[k]);
-          box.z0 = min(box.z0, z[k]); box.z1 = max(box.z1, z[k]);
+      for (int k = 0; k < RPI; k++) {
+        const int r = r0 + k;
+        const uint32_t b16 = nib4(v[k].x) | (nib4(v[k].y) << 4) | (nib4(v[k].z) << 8) |
+                             (nib4(v[k].w) << 12);
+        const uint32_t word = b16 | (__shfl_down_sync(kFull, b16, 1) << 16);
+        const bool mine = !(lane & 1) && r < n_rows && c < C16;
+        if (mine) bits[(size_t)r * W + (c >> 1)] = word;
+        const bool occ = mine && word != 0u;
+        if (__any_sync(kFull, occ)) {  // rare: rows crossing the ROI
+          if (occ) {
+            box.x0 = min(box.x0, 16 * c + __ffs(word) - 1);
+            box.x1 = max(box.x1, 16 * c + 31 - __clz(word));
+          }
+          const int z = r / ny, y = r - z * ny;
+          box.y0 = min(box.y0, y); box.y1 = max(box.y1, y);
+          box.z0 = min(box.z0, z); box.z1 = max(box.z1, z);
         }
       }
-      y[k] += dy;
-      z[k] += dz;
-      if (y[k] >= ny) { y[k] -= ny; z[k]++; }
-      v[k] = nv[k];
     }
   }
   box.flush(st);
@@ -331,6 +312,6 @@ __global__ void __launch_bounds__(256) mc_cells(const uint32_t* __restrict__ bit
     if (s_bin[i]) atomicAdd(&sort_counts[i], s_bin[i]);
 }
 
-template __global__ void pack_bits_v16<4>(const uint4*, uint32_t*, long long, int, int, Stats*);
+template __global__ void pack_bits_v16<8>(const uint4*, uint32_t*, int, int, int, Stats*);
 
 }  // namespace sc
