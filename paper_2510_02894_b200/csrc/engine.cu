@@ -30,8 +30,9 @@ namespace sc {
 
 // Kernels (mc.cu, diameter.cu).
 __global__ void init_stats(Stats* st);
-template <int RPI>
-__global__ void pack_bits_v16(const uint4*, uint32_t*, int, int, int, Stats*);
+template <int U>
+__global__ void pack_bits_v16(const uint4*, uint32_t*, long long);
+__global__ void bits_bbox(const uint4*, long long, int, int, Stats*);
 __global__ void pack_bits_generic(const uint8_t*, uint32_t*, long long, int, int, int, Stats*);
 __global__ void mc_cells(const uint32_t*, int, int, int, int, const CaseTables*, Stats*, int4*,
                          long long, unsigned int*, unsigned int*);
@@ -275,12 +276,13 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     if (const char* v = getenv("SC_PASS1")) g_opt_packed = std::strcmp(v, "scalar") != 0;
     if (const char* v = getenv("SC_PRUNE")) g_opt_prune = std::strcmp(v, "0") != 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_plane, plane_pass1, 256, 0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pack, pack_bits_v16<8>, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pack, pack_bits_v16<4>, 256, 0));
     {
       // Lazy module loading must not happen inside a stream capture: touch
       // every kernel once here.
       cudaFuncAttributes fa;
-      const void* kernels[] = {(const void*)init_stats, (const void*)pack_bits_v16<8>,
+      const void* kernels[] = {(const void*)init_stats, (const void*)pack_bits_v16<4>,
+                               (const void*)bits_bbox,
                                (const void*)pack_bits_generic, (const void*)mc_cells,
                                (const void*)scan_all, (const void*)scatter_all,
                                (const void*)boxes_extremes, (const void*)unit_filter,
@@ -401,14 +403,17 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
   CK(record(c, c->kev[0], s));
   init_stats<<<1, 256, 0, s>>>(c->d_stats);
   CKL(1);
-  if (nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0 && ny * nz < (1LL << 31)) {
-    const int n_rows = (int)(ny * nz);
-    const long long want = ((long long)n_rows + 8 * 8 - 1) / (8 * 8);  // 8 warps x 8 rows
+  if (nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0) {
+    const long long n_chunks = nx * ny * nz / 16;
+    const long long want = (n_chunks + 256 * 4 - 1) / (256 * 4);
     const long long grid = std::max<long long>(
         1, std::min<long long>(want, (long long)c->sms * std::max(1, c->occ_pack)));
-    pack_bits_v16<8><<<(unsigned)grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(d_mask),
-                                                    c->bits.p, n_rows, (int)(nx / 16), (int)ny,
-                                                    c->d_stats);
+    pack_bits_v16<4><<<(unsigned)grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(d_mask),
+                                                    c->bits.p, n_chunks);
+    CKL(1);
+    const long long wgrid = std::min<long long>((n_words / 4 + 255) / 256, (long long)c->sms * 8);
+    bits_bbox<<<(unsigned)std::max<long long>(1, wgrid), 256, 0, s>>>(
+        reinterpret_cast<const uint4*>(c->bits.p), n_words, W, (int)ny, c->d_stats);
   } else {
     long long want = (n_words + 255) / 256;
     int grid = (int)std::min<long long>(want, (long long)c->sms * 8);
