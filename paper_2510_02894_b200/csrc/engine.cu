@@ -400,9 +400,9 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
                 long long dcap) {
   const int W = (int)((nx + 31) / 32);
   const long long n_words = (long long)W * ny * nz;
-  CK(record(c, c->kev[0], s));
   init_stats<<<1, 256, 0, s>>>(c->d_stats);
   CKL(1);
+  CK(record(c, c->kev[0], s));  // kev0..kev1 = the HBM pass alone
   if (nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0) {
     const long long n_chunks = nx * ny * nz / 16;
     const long long want = (n_chunks + 256 * 4 - 1) / (256 * 4);
@@ -411,17 +411,19 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
     pack_bits_v16<4><<<(unsigned)grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(d_mask),
                                                     c->bits.p, n_chunks);
     CKL(1);
+    CK(record(c, c->kev[1], s));
     const long long wgrid = std::min<long long>((n_words / 4 + 255) / 256, (long long)c->sms * 8);
     bits_bbox<<<(unsigned)std::max<long long>(1, wgrid), 256, 0, s>>>(
         reinterpret_cast<const uint4*>(c->bits.p), n_words, W, (int)ny, c->d_stats);
+    CKL(1);
   } else {
     long long want = (n_words + 255) / 256;
     int grid = (int)std::min<long long>(want, (long long)c->sms * 8);
     pack_bits_generic<<<grid, 256, 0, s>>>(d_mask, c->bits.p, n_words, (int)nx, W, (int)ny,
                                            c->d_stats);
+    CKL(1);
+    CK(record(c, c->kev[1], s));
   }
-  CKL(1);
-  CK(record(c, c->kev[1], s));
   int mc_occ = 1;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mc_occ, mc_cells, 256, 0));
   mc_cells<<<c->sms * std::max(1, mc_occ), 256, 0, s>>>(
