@@ -77,6 +77,7 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<bool> g_opt_prune{true}, g_opt_packed{true}, g_opt_graphs{true};
+std::atomic<int> g_opt_slots{2};  // pipeline slots used by the batch entries
 std::atomic<unsigned long long> g_launches{0};
 
 void set_err(const char* fmt, ...) {
@@ -239,7 +240,7 @@ struct Ctx {
 // Two independent pipeline slots per device (stream, events, scratch, graphs):
 // single-ROI calls use slot 0; batch calls alternate slots so the H2D copy and
 // kernels of ROI i+1 overlap the tail and the host round trip of ROI i.
-constexpr int kSlots = 2;
+constexpr int kSlots = 4;
 std::mutex g_ctx_mu;
 std::vector<std::array<std::unique_ptr<Ctx>, kSlots>> g_ctx;
 
@@ -701,21 +702,23 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
     return SC_ERR_INPUT;
   }
   if (count == 0) return SC_OK;
-  Ctx* cs[kSlots];
-  for (int k = 0; k < kSlots; k++) {
+  const int nslots = std::max(1, std::min<int>(kSlots, g_opt_slots.load()));
+  Ctx* cs[kSlots] = {};
+  for (int k = 0; k < nslots; k++) {
     int rc = get_ctx(device, &cs[k], k);
     if (rc) return rc;
   }
-  std::lock_guard<std::mutex> l0(cs[0]->mu);
-  std::lock_guard<std::mutex> l1(cs[1]->mu);
+  std::unique_lock<std::mutex> locks[kSlots];
+  for (int k = 0; k < nslots; k++) locks[k] = std::unique_lock<std::mutex>(cs[k]->mu);
   CK(cudaSetDevice(device));
   if (user) {  // order the batch after prior work on the caller's stream
     CK(cudaEventRecord(cs[0]->ev[4], user));
-    for (int k = 0; k < kSlots; k++) CK(cudaStreamWaitEvent(cs[k]->stream, cs[0]->ev[4], 0));
+    for (int k = 0; k < nslots; k++) CK(cudaStreamWaitEvent(cs[k]->stream, cs[0]->ev[4], 0));
   }
   Pending pend[kSlots] = {};
-  int64_t idx[kSlots] = {-1, -1};
-  double t_start[kSlots] = {0, 0};
+  int64_t idx[kSlots];
+  double t_start[kSlots];
+  for (int k = 0; k < kSlots; k++) { idx[k] = -1; t_start[k] = 0.0; }
   int first = SC_OK;
   std::string first_err;
   auto note = [&](int rc) {
@@ -734,7 +737,7 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
     idx[k] = -1;
   };
   for (int64_t i = 0; i < count; i++) {
-    const int k = (int)(i % kSlots);
+    const int k = (int)(i % nslots);
     collect(k);
     std::memset(&out[i], 0, sizeof out[i]);
     const int64_t nx = dims[3 * i], ny = dims[3 * i + 1], nz = dims[3 * i + 2];
@@ -758,9 +761,9 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
     if (rc) { note(rc); continue; }
     idx[k] = i;
   }
-  for (int64_t i = 0; i < kSlots; i++) collect((int)((count + i) % kSlots));
+  for (int64_t i = 0; i < nslots; i++) collect((int)((count + i) % nslots));
   if (user) {  // ... and later work on it after the batch
-    for (int k = 0; k < kSlots; k++) {
+    for (int k = 0; k < nslots; k++) {
       CK(cudaEventRecord(cs[k]->ev[5], cs[k]->stream));
       CK(cudaStreamWaitEvent(user, cs[k]->ev[5], 0));
     }
@@ -942,6 +945,7 @@ int sc_set_option(const char* name, int value) {
   if (std::strcmp(name, "prune") == 0) g_opt_prune = value != 0;
   else if (std::strcmp(name, "pass1_packed") == 0) g_opt_packed = value != 0;
   else if (std::strcmp(name, "graphs") == 0) g_opt_graphs = value != 0;
+  else if (std::strcmp(name, "slots") == 0) g_opt_slots = value;
   else { set_err("unknown option %s", name); return SC_ERR_INPUT; }
   return SC_OK;
 }
