@@ -77,7 +77,7 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<bool> g_opt_prune{true}, g_opt_packed{true}, g_opt_graphs{true};
-std::atomic<int> g_opt_slots{2};  // pipeline slots used by the batch entries
+std::atomic<int> g_opt_slots{8};  // pipeline slots used by the batch entries
 std::atomic<unsigned long long> g_launches{0};
 
 void set_err(const char* fmt, ...) {
@@ -240,7 +240,7 @@ struct Ctx {
 // Two independent pipeline slots per device (stream, events, scratch, graphs):
 // single-ROI calls use slot 0; batch calls alternate slots so the H2D copy and
 // kernels of ROI i+1 overlap the tail and the host round trip of ROI i.
-constexpr int kSlots = 4;
+constexpr int kSlots = 8;
 std::mutex g_ctx_mu;
 std::vector<std::array<std::unique_ptr<Ctx>, kSlots>> g_ctx;
 
