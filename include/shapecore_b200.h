@@ -93,8 +93,9 @@ int sc_calculate_coefficients_shard(const uint8_t* d_mask, int64_t nx, int64_t n
                                     int nshards, double* d_sq4, sc_coeffs* out);
 
 /* Batch of ROIs on one device (C4): masks[i] are host pointers with dims
- * dims[3*i..3*i+2] and spacing spacings[3*i..]; out[i] per ROI.  Two pipeline
- * slots alternate, so the H2D copy of ROI i+1 overlaps the kernels of ROI i.
+ * dims[3*i..3*i+2] and spacing spacings[3*i..]; out[i] per ROI.  Up to 8
+ * pipeline slots (option "slots") round-robin, so the H2D copy and kernels of
+ * the next ROIs overlap the current one's.
  * The first failing ROI's code is returned; later ROIs are still processed. */
 int sc_calculate_coefficients_batch(const uint8_t* const* masks, const int64_t* dims,
                                     const double* spacings, int64_t count, int device,
@@ -133,10 +134,11 @@ int sc_last_kernel_times(int device, double* ms, int n);
  * planar re-check candidates, planar tile pairs evaluated}; a unit is 256 x
  * 256 vertex pairs.  Returns how many were written. */
 int sc_last_diagnostics(int device, int64_t* out, int n);
-/* Process-wide switches (all default 1): "prune" = exact bbox pruning of
- * 3-D work units; "pass1_packed" = FFMA2 variant of the 3-D pass; "graphs" =
- * replay each ROI pipeline as a cached CUDA graph.  Results are identical
- * either way; 0 on success, SC_ERR_INPUT for an unknown name. */
+/* Process-wide switches: "prune" (default 1) = exact bbox pruning of 3-D and
+ * planar work units; "pass1_packed" (1) = FFMA2 variant of the 3-D pass;
+ * "graphs" (1) = replay each ROI pipeline as a cached CUDA graph; "slots" (8)
+ * = pipeline slots (stream + scratch) the batch entries keep in flight.
+ * Results are identical either way; 0 on success, SC_ERR_INPUT otherwise. */
 int sc_set_option(const char* name, int value);
 uint64_t sc_launch_count(void);
 int sc_probe_fp32_peak(int device, int mode, double* tflops);
