@@ -66,12 +66,13 @@ __device__ __forceinline__ void select_units(const float* __restrict__ umax, lon
 // pair instead of 3.5 for scalar FFMA.
 template <bool PACKED>
 __global__ void __launch_bounds__(kDiamThreads, 3) diam3d_pass1(const int4* __restrict__ keys,
-                                                                long long cap, Frame f, int shard,
+                                                                long long cap, const RoiParams* __restrict__ rp, int shard,
                                                                 int nshards,
                                                                 const unsigned int* __restrict__ work,
                                                                 float* __restrict__ umax,
                                                                 unsigned int* __restrict__ cand,
                                                                 Stats* __restrict__ st) {
+  Frame f = rp->f;
   __shared__ float4 sj_all[kWarps][kChunk];  // (x, y, z, |p|^2) per warp
   const long long n = n_vertices(st, cap);
   if (n == 0) return;
@@ -166,19 +167,20 @@ __global__ void __launch_bounds__(kDiamThreads, 3) diam3d_pass1(const int4* __re
   // global pass-1 maximum for the exact re-check.
   if (last_block(&st->done1)) select_units(umax, n_work, st, cand);
 }
-template __global__ void diam3d_pass1<true>(const int4*, long long, Frame, int, int,
+template __global__ void diam3d_pass1<true>(const int4*, long long, const RoiParams*, int, int,
                                             const unsigned int*, float*, unsigned int*, Stats*);
-template __global__ void diam3d_pass1<false>(const int4*, long long, Frame, int, int,
+template __global__ void diam3d_pass1<false>(const int4*, long long, const RoiParams*, int, int,
                                              const unsigned int*, float*, unsigned int*, Stats*);
 
 // Exact re-check: each selected chunk pair, 256 x 256 in fp64 with the
 // reference arithmetic on the reference coordinates; one block per candidate
 // (thread = one i vertex), persistent grid.
 __global__ void __launch_bounds__(kDiamThreads) diam3d_refine(const int4* __restrict__ keys,
-                                                              long long cap, Frame f,
+                                                              long long cap, const RoiParams* __restrict__ rp,
                                                               const unsigned int* __restrict__ work,
                                                               const unsigned int* __restrict__ cand,
                                                               Stats* __restrict__ st) {
+  Frame f = rp->f;
   __shared__ double sx[kChunk], sy[kChunk], sz[kChunk];
   const long long n = n_vertices(st, cap);
   const long long C = (n + kChunk - 1) / kChunk;

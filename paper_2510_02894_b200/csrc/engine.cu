@@ -28,13 +28,13 @@
 
 namespace sc {
 
-// Kernels (mc.cu, diameter.cu).
+// Kernels (mc.cu, diameter.cu, prune.cu, planar.cu).
 __global__ void init_stats(Stats* st);
 template <int U>
-__global__ void pack_bits_v16(const uint4*, uint32_t*, long long);
-__global__ void bits_bbox(const uint4*, long long, int, int, Stats*);
-__global__ void pack_bits_generic(const uint8_t*, uint32_t*, long long, int, int, int, Stats*);
-__global__ void mc_cells(const uint32_t*, int, int, int, int, const CaseTables*, Stats*, int4*,
+__global__ void pack_bits_v16(const RoiParams*, uint32_t*);
+__global__ void bits_bbox(const RoiParams*, const uint4*, Stats*);
+__global__ void pack_bits_generic(const RoiParams*, uint32_t*, Stats*);
+__global__ void mc_cells(const RoiParams*, const uint32_t*, const CaseTables*, Stats*, int4*,
                          long long, unsigned int*, unsigned int*);
 __global__ void plane_bins_scan(unsigned int*, unsigned int*, unsigned int*, unsigned long long*,
                                 const Stats*);
@@ -43,26 +43,27 @@ __global__ void scan_all(unsigned int*, unsigned int*, const unsigned int*, unsi
                          long long, int, Stats*);
 __global__ void scatter_all(const int4*, long long, const Stats*, unsigned int*, int4*,
                             const unsigned int*, unsigned int*, int2*);
-__global__ void boxes_extremes(const int4*, long long, Frame, Stats*, int4*);
-__global__ void unit_filter(const int4*, const int4*, long long, Frame, int, Stats*,
+__global__ void boxes_extremes(const int4*, long long, const RoiParams*, Stats*, int4*);
+__global__ void unit_filter(const int4*, const int4*, long long, const RoiParams*, int, Stats*,
                             unsigned int*);
 template <bool PACKED>
-__global__ void diam3d_pass1(const int4*, long long, Frame, int, int, const unsigned int*, float*,
-                             unsigned int*, Stats*);
-__global__ void diam3d_refine(const int4*, long long, Frame, const unsigned int*,
+__global__ void diam3d_pass1(const int4*, long long, const RoiParams*, int, int,
+                             const unsigned int*, float*, unsigned int*, Stats*);
+__global__ void diam3d_refine(const int4*, long long, const RoiParams*, const unsigned int*,
                               const unsigned int*, Stats*);
 __global__ void plane_boxes(const int2*, const unsigned int*, const unsigned int*,
-                            const unsigned int*, Frame, const Stats*, int4*, unsigned long long*);
-__global__ void plane_lb(const int2*, const unsigned int*, const unsigned long long*, Frame,
-                         Stats*);
+                            const unsigned int*, const RoiParams*, const Stats*, int4*,
+                            unsigned long long*);
+__global__ void plane_lb(const int2*, const unsigned int*, const unsigned long long*,
+                         const RoiParams*, Stats*);
 __global__ void plane_filter(const unsigned int*, const unsigned int*, const unsigned int*,
-                             const unsigned int*, const int4*, Frame, int, long long, Stats*,
-                             unsigned int*);
+                             const unsigned int*, const int4*, const RoiParams*, int, long long,
+                             Stats*, unsigned int*);
 __global__ void plane_pass1(const int2*, const unsigned int*, const unsigned int*,
-                            const unsigned int*, const unsigned int*, Frame, int, int, long long,
-                            float*, unsigned int*, Stats*);
+                            const unsigned int*, const unsigned int*, const RoiParams*, int, int,
+                            long long, float*, unsigned int*, Stats*);
 __global__ void plane_refine(const int2*, const unsigned int*, const unsigned int*,
-                             const unsigned int*, const unsigned int*, Frame,
+                             const unsigned int*, const unsigned int*, const RoiParams*,
                              const unsigned int*, Stats*);
 __global__ void cloud_diameters(const double*, const double*, const double*, long long, int,
                                 unsigned long long*);
@@ -186,9 +187,12 @@ struct Ctx {
   double last_ms[7] = {0, 0, 0, 0, 0, 0, 0};  // pack, mc, prune, pass1, refine, planar, h2d
   long long cap_floor = 0, dcap_floor = 0;  // raised by overflow re-runs only
   long long last_diag[6] = {0, 0, 0, 0, 0, 0};
-  int occ_pass1 = 1, occ_pass1s = 1, occ_plane = 1, occ_pack = 1;  // resident blocks/SM
+  int occ_pass1 = 1, occ_pass1s = 1, occ_plane = 1, occ_pack = 1, occ_mc = 1;  // blocks/SM
   Stats* d_stats = nullptr;
   Stats* h_stats = nullptr;  // pinned
+  RoiParams* d_rp = nullptr;  // per-ROI launch parameters (device)
+  RoiParams* h_rp = nullptr;  // staging copy (pinned)
+  long long dcap_sz = 0;      // vertices the diameter-side buffers are sized for (monotonic)
   CaseTables* d_tabs = nullptr;
   DevBuf<uint32_t> bits;
   DevBuf<int4> keys, keys_sorted, boxes;
@@ -204,10 +208,8 @@ struct Ctx {
   DevBuf<double> cloud;
   DevBuf<unsigned long long> cloud_out;
   // CUDA graphs of whole ROIs, keyed by everything baked into the nodes.
-  struct GraphEntry {
-    const void* mask;
-    int64_t nx, ny, nz;
-    double sp[3];
+  struct GraphEntry {  // everything a captured ROI graph depends on
+    bool fast;          // 128-bit pack path (nx % 32 == 0, 16-byte aligned mask)
     cudaStream_t s;
     int shard, nshards;
     void* d_sq4;
@@ -270,6 +272,8 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     for (auto& e : c->kev) CK(cudaEventCreate(&e));
     CK(cudaMalloc(&c->d_stats, sizeof(Stats)));
     CK(cudaMallocHost(&c->h_stats, sizeof(Stats)));
+    CK(cudaMalloc(&c->d_rp, sizeof(RoiParams)));
+    CK(cudaMallocHost(&c->h_rp, sizeof(RoiParams)));
     CK(cudaMalloc(&c->d_tabs, sizeof(CaseTables)));
     CK(cudaMemcpy(c->d_tabs, &case_geom().tabs, sizeof(CaseTables), cudaMemcpyHostToDevice));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pass1, diam3d_pass1<true>, 256, 0));
@@ -278,6 +282,7 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     if (const char* v = getenv("SC_PRUNE")) g_opt_prune = std::strcmp(v, "0") != 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_plane, plane_pass1, 256, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pack, pack_bits_v16<4>, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_mc, mc_cells, 256, 0));
     {
       // Lazy module loading must not happen inside a stream capture: touch
       // every kernel once here.
@@ -350,6 +355,7 @@ long long vertex_capacity(int64_t nx, int64_t ny, int64_t nz, long long hint) {
 // tile-pair bookkeeping grows as V^2) hold up to `dcap` <= cap.
 int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, long long dcap,
                    long long punits) {
+  dcap = c->dcap_sz = std::max(c->dcap_sz, dcap);
   const int W = (int)((nx + 31) / 32);
   CK(c->bits.ensure((size_t)((long long)W * ny * nz)));
   CK(c->keys.ensure((size_t)cap));
@@ -393,54 +399,35 @@ int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, lo
   return SC_OK;
 }
 
-// Enqueue one whole ROI on stream s; no host synchronisation.  Kernel order:
-// init, pack, mc | prep, pass1, select, refine | plane hist, scan, scatter,
-// pass1, select, refine.  kev[] brackets the stages for sc_last_kernel_times.
-int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
-                const double sp[3], cudaStream_t s, int shard, int nshards, long long cap,
-                long long dcap) {
-  const int W = (int)((nx + 31) / 32);
-  const long long n_words = (long long)W * ny * nz;
+// Enqueue one whole ROI on stream s; no host synchronisation.  Everything
+// ROI-specific (mask pointer, dims, spacing) is read by the kernels from the
+// slot's RoiParams record, so the enqueued sequence -- and a graph captured
+// from it -- depends only on the pack path, the shard and the slot buffers.
+// kev[] brackets the stages for sc_last_kernel_times.
+int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
+  const RoiParams* rp = c->d_rp;
+  const long long cap = (long long)c->keys.cap, dcap = c->dcap_sz;
   init_stats<<<1, 256, 0, s>>>(c->d_stats);
   CKL(1);
   CK(record(c, c->kev[0], s));  // kev0..kev1 = the HBM pass alone
-  if (nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0) {
-    const long long n_chunks = nx * ny * nz / 16;
-    const long long want = (n_chunks + 256 * 4 - 1) / (256 * 4);
-    const long long grid = std::max<long long>(
-        1, std::min<long long>(want, (long long)c->sms * std::max(1, c->occ_pack)));
-    pack_bits_v16<4><<<(unsigned)grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(d_mask),
-                                                    c->bits.p, n_chunks);
+  if (fast) {
+    pack_bits_v16<4><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(rp, c->bits.p);
     CKL(1);
     CK(record(c, c->kev[1], s));
-    const long long wgrid = std::min<long long>((n_words / 4 + 255) / 256, (long long)c->sms * 8);
-    bits_bbox<<<(unsigned)std::max<long long>(1, wgrid), 256, 0, s>>>(
-        reinterpret_cast<const uint4*>(c->bits.p), n_words, W, (int)ny, c->d_stats);
+    bits_bbox<<<c->sms * 8, 256, 0, s>>>(rp, reinterpret_cast<const uint4*>(c->bits.p),
+                                         c->d_stats);
     CKL(1);
   } else {
-    long long want = (n_words + 255) / 256;
-    int grid = (int)std::min<long long>(want, (long long)c->sms * 8);
-    pack_bits_generic<<<grid, 256, 0, s>>>(d_mask, c->bits.p, n_words, (int)nx, W, (int)ny,
-                                           c->d_stats);
+    pack_bits_generic<<<c->sms * 8, 256, 0, s>>>(rp, c->bits.p, c->d_stats);
     CKL(1);
     CK(record(c, c->kev[1], s));
   }
-  int mc_occ = 1;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mc_occ, mc_cells, 256, 0));
-  mc_cells<<<c->sms * std::max(1, mc_occ), 256, 0, s>>>(
-      c->bits.p, (int)nx, (int)ny, (int)nz, W, c->d_tabs, c->d_stats, c->keys.p, cap,
-      c->sort_counts.p, c->pbin_counts.p);
+  mc_cells<<<c->sms * std::max(1, c->occ_mc), 256, 0, s>>>(rp, c->bits.p, c->d_tabs, c->d_stats,
+                                                          c->keys.p, cap, c->sort_counts.p,
+                                                          c->pbin_counts.p);
   CKL(1);
   CK(record(c, c->kev[2], s));
 
-  Frame f;
-  f.cx2 = f.cy2 = f.cz2 = 0;  // set on the device from the bbox
-  f.hx = (float)(0.5 * sp[0]);
-  f.hy = (float)(0.5 * sp[1]);
-  f.hz = (float)(0.5 * sp[2]);
-  f.sx = sp[0];
-  f.sy = sp[1];
-  f.sz = sp[2];
   // Persistent grids: exactly the resident blocks, so the static round-robin
   // split of work units is also the load balance.
   const int pgrid = c->sms * std::max(1, g_opt_packed.load() ? c->occ_pass1 : c->occ_pass1s);
@@ -462,41 +449,41 @@ int enqueue_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t n
                                          c->keys_sorted.p, c->plane_start.p, c->pbin_cursor.p,
                                          c->plane_sorted.p);
   CKL(1);
-  boxes_extremes<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, f, c->d_stats, c->boxes.p);
+  boxes_extremes<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->d_stats, c->boxes.p);
   CKL(1);
-  unit_filter<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, c->boxes.p, dcap, f, prune,
+  unit_filter<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, c->boxes.p, dcap, rp, prune,
                                          c->d_stats, c->work.p);
   CKL(1);
   CK(record(c, c->kev[3], s));
   if (g_opt_packed.load())
-    diam3d_pass1<true><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, f, shard, nshards,
+    diam3d_pass1<true><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, shard, nshards,
                                              c->work.p, c->warp_max.p, c->cand.p, c->d_stats);
   else
-    diam3d_pass1<false><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, f, shard, nshards,
+    diam3d_pass1<false><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, shard, nshards,
                                               c->work.p, c->warp_max.p, c->cand.p, c->d_stats);
   CKL(1);
   CK(record(c, c->kev[4], s));
-  diam3d_refine<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, f, c->work.p, c->cand.p,
+  diam3d_refine<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->work.p, c->cand.p,
                                            c->d_stats);
   CKL(1);
   CK(record(c, c->kev[5], s));
   plane_boxes<<<c->sms * 2, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_cstart.p,
-                                         c->plane_cmap.p, f, c->d_stats, c->plane_boxes_buf.p,
+                                         c->plane_cmap.p, rp, c->d_stats, c->plane_boxes_buf.p,
                                          c->plane_ext.p);
   CKL(1);
-  plane_lb<<<c->sms, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_ext.p, f,
+  plane_lb<<<c->sms, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_ext.p, rp,
                                   c->d_stats);
   CKL(1);
   plane_filter<<<c->sms * 4, 256, 0, s>>>(c->plane_start.p, c->plane_tstart.p, c->plane_cstart.p,
-                                          c->plane_umap.p, c->plane_boxes_buf.p, f, prune, pucap,
+                                          c->plane_umap.p, c->plane_boxes_buf.p, rp, prune, pucap,
                                           c->d_stats, c->plane_work.p);
   CKL(1);
   plane_pass1<<<plgrid, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_tstart.p,
-                                     c->plane_umap.p, c->plane_work.p, f, shard, nshards, pucap,
+                                     c->plane_umap.p, c->plane_work.p, rp, shard, nshards, pucap,
                                      c->plane_umax.p, c->plane_cand.p, c->d_stats);
   CKL(1);
   plane_refine<<<c->sms * 2, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p,
-                                          c->plane_tstart.p, c->plane_umap.p, c->plane_work.p, f,
+                                          c->plane_tstart.p, c->plane_umap.p, c->plane_work.p, rp,
                                           c->plane_cand.p, c->d_stats);
   CKL(1);
   CK(record(c, c->kev[6], s));
@@ -537,14 +524,14 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
-// Enqueue one ROI plus its result copies, replaying a cached CUDA graph when
-// the same (mask, dims, spacing, stream, shard, buffers, options) was seen
-// before; the first occurrence is captured.  Graph replay removes the per-
-// kernel launch cost of the ~11-kernel pipeline (SC option "graphs").
-int enqueue_with_copies(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
-                        const double sp[3], cudaStream_t s, int shard, int nshards,
-                        double* d_sq4, long long cap, long long dcap) {
-  int rc = enqueue_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, cap, dcap);
+// Enqueue one ROI plus its result copies, replaying the slot's cached CUDA
+// graph for this (pack path, stream, shard, buffers, options) when there is
+// one; otherwise capture it first.  Graph replay removes the per-kernel launch
+// cost of the ~16-kernel pipeline (SC option "graphs").  The ROI's parameters
+// travel in a 96-byte H2D copy ahead of the graph.
+int enqueue_with_copies(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards,
+                        double* d_sq4) {
+  int rc = enqueue_roi(c, fast, s, shard, nshards);
   if (rc) return rc;
   if (d_sq4)
     CK(cudaMemcpyAsync(d_sq4, c->d_stats->sq, 4 * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -553,16 +540,33 @@ int enqueue_with_copies(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, i
 }
 
 int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
-               const double sp[3], cudaStream_t s, int shard, int nshards, double* d_sq4,
-               long long cap, long long dcap) {
+               const double sp[3], cudaStream_t s, int shard, int nshards, double* d_sq4) {
+  RoiParams& h = *c->h_rp;  // the slot's previous ROI has been collected: safe to rewrite
+  h.mask = d_mask;
+  h.nx = nx;
+  h.ny = ny;
+  h.nz = nz;
+  h.W = (int)((nx + 31) / 32);
+  h.n_words = (long long)h.W * ny * nz;
+  h.n_chunks = nx * ny * nz / 16;
+  h.pad = 0;
+  h.f.cx2 = h.f.cy2 = h.f.cz2 = 0;  // set on the device from the bbox
+  h.f.hx = (float)(0.5 * sp[0]);
+  h.f.hy = (float)(0.5 * sp[1]);
+  h.f.hz = (float)(0.5 * sp[2]);
+  h.f.sx = sp[0];
+  h.f.sy = sp[1];
+  h.f.sz = sp[2];
+  CK(cudaMemcpyAsync(c->d_rp, c->h_rp, sizeof(RoiParams), cudaMemcpyHostToDevice, s));
+  const bool fast = nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0;
   if (!g_opt_graphs.load() || s == nullptr)
-    return enqueue_with_copies(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, cap, dcap);
+    return enqueue_with_copies(c, fast, s, shard, nshards, d_sq4);
+  const long long cap = (long long)c->keys.cap, dcap = c->dcap_sz;
   const bool prune = g_opt_prune.load(), packed = g_opt_packed.load();
   for (auto& g : c->graphs)
-    if (g.mask == d_mask && g.nx == nx && g.ny == ny && g.nz == nz && g.sp[0] == sp[0] &&
-        g.sp[1] == sp[1] && g.sp[2] == sp[2] && g.s == s && g.shard == shard &&
-        g.nshards == nshards && g.d_sq4 == d_sq4 && g.cap == cap && g.dcap == dcap &&
-        g.prune == prune && g.packed == packed && g.gen == c->gen) {
+    if (g.fast == fast && g.s == s && g.shard == shard && g.nshards == nshards &&
+        g.d_sq4 == d_sq4 && g.cap == cap && g.dcap == dcap && g.prune == prune &&
+        g.packed == packed && g.gen == c->gen) {
       CK(cudaGraphLaunch(g.exec, s));
       g_launches.fetch_add(g.launches, std::memory_order_relaxed);
       return SC_OK;
@@ -570,7 +574,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   const unsigned long long before = g_launches.load();
   CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   c->capturing = true;
-  int rc = enqueue_with_copies(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, cap, dcap);
+  int rc = enqueue_with_copies(c, fast, s, shard, nshards, d_sq4);
   c->capturing = false;
   cudaGraph_t graph = nullptr;
   cudaError_t ec = cudaStreamEndCapture(s, &graph);
@@ -586,8 +590,8 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
     cudaGraphExecDestroy(c->graphs.front().exec);
     c->graphs.erase(c->graphs.begin());
   }
-  Ctx::GraphEntry g{d_mask, nx, ny, nz, {sp[0], sp[1], sp[2]}, s, shard, nshards, d_sq4,
-                    cap, dcap, prune, packed, c->gen, exec, launches};
+  Ctx::GraphEntry g{fast, s, shard, nshards, d_sq4, cap, dcap, prune, packed, c->gen, exec,
+                    launches};
   c->graphs.push_back(g);
   CK(cudaGraphLaunch(exec, s));
   g_launches.fetch_add(launches, std::memory_order_relaxed);
@@ -624,8 +628,9 @@ int start_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
     c->gen++;
     c->drop_graphs();
   }
-  *p = Pending{d_mask, nx, ny, nz, {sp[0], sp[1], sp[2]}, s, shard, nshards, d_sq4, cap, dcap};
-  return launch_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, cap, dcap);
+  *p = Pending{d_mask, nx, ny, nz, {sp[0], sp[1], sp[2]}, s, shard, nshards, d_sq4,
+               (long long)c->keys.cap, c->dcap_sz};
+  return launch_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4);
 }
 
 // Wait for the ROI started on slot c, re-run it once with exact buffer sizes

@@ -78,9 +78,10 @@ struct BoxAcc {
 // Grid = resident blocks.  tools/microbench/pack_bench.cu: 5.1 TB/s on a 157 MB
 // mask = 88% of the 1 GiB streaming-read rate of the same GPU.
 template <int U>
-__global__ void __launch_bounds__(256) pack_bits_v16(const uint4* __restrict__ mask,
-                                                     uint32_t* __restrict__ bits,
-                                                     long long n_chunks) {
+__global__ void __launch_bounds__(256) pack_bits_v16(const RoiParams* __restrict__ rp,
+                                                     uint32_t* __restrict__ bits) {
+  const uint4* __restrict__ mask = reinterpret_cast<const uint4*>(rp->mask);
+  const long long n_chunks = rp->n_chunks;
   const long long step = (long long)gridDim.x * blockDim.x * U;
   for (long long base = (long long)blockIdx.x * blockDim.x * U; base < n_chunks; base += step) {
     uint4 v[U];
@@ -102,9 +103,11 @@ __global__ void __launch_bounds__(256) pack_bits_v16(const uint4* __restrict__ m
 
 // Occupied bbox from the bit volume (L2-resident right after the pack): only
 // nonzero words locate themselves.  4 words per thread-load.
-__global__ void __launch_bounds__(256) bits_bbox(const uint4* __restrict__ bits4,
-                                                 long long n_words, int W, int ny,
+__global__ void __launch_bounds__(256) bits_bbox(const RoiParams* __restrict__ rp,
+                                                 const uint4* __restrict__ bits4,
                                                  Stats* __restrict__ st) {
+  const long long n_words = rp->n_words;
+  const int W = rp->W, ny = (int)rp->ny;
   BoxAcc box;
   const long long n4 = n_words / 4;
   const long long step = (long long)gridDim.x * blockDim.x;
@@ -130,10 +133,12 @@ __global__ void __launch_bounds__(256) bits_bbox(const uint4* __restrict__ bits4
 
 // Generic path: any nx / alignment.  One output word per thread, byte loads
 // (still coalesced across the warp within a row).
-__global__ void __launch_bounds__(256) pack_bits_generic(const uint8_t* __restrict__ mask,
+__global__ void __launch_bounds__(256) pack_bits_generic(const RoiParams* __restrict__ rp,
                                                          uint32_t* __restrict__ bits,
-                                                         long long n_words, int nx, int W, int ny,
                                                          Stats* __restrict__ st) {
+  const uint8_t* __restrict__ mask = rp->mask;
+  const long long n_words = rp->n_words;
+  const int nx = (int)rp->nx, W = rp->W, ny = (int)rp->ny;
   BoxAcc box;
   const long long step = (long long)gridDim.x * blockDim.x;
   for (long long base = (long long)blockIdx.x * blockDim.x; base < n_words; base += step) {
@@ -186,14 +191,16 @@ __device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits, int
 // Every emitted vertex is also counted into the histograms the diameter stage
 // sorts by: its 3-D Morton brick (block-private, flushed once per block) and
 // its (plane, in-plane brick) bin in each of its three planes (global).
-__global__ void __launch_bounds__(256) mc_cells(const uint32_t* __restrict__ bits, int nx, int ny,
-                                                int nz, int W, const CaseTables* __restrict__ tabs,
+__global__ void __launch_bounds__(256) mc_cells(const RoiParams* __restrict__ rp,
+                                                const uint32_t* __restrict__ bits,
+                                                const CaseTables* __restrict__ tabs,
                                                 Stats* __restrict__ st, int4* __restrict__ vkeys,
                                                 long long cap, unsigned int* __restrict__ sort_counts,
                                                 unsigned int* __restrict__ pbin_counts) {
   __shared__ unsigned int s_hist[kNumCases];
   __shared__ int4 s_tn[kNumCases];
   __shared__ unsigned int s_bin[kSortBins];
+  const int ny = (int)rp->ny, nz = (int)rp->nz, W = rp->W;
   int bb[6];
 #pragma unroll
   for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
@@ -323,6 +330,6 @@ __global__ void __launch_bounds__(256) mc_cells(const uint32_t* __restrict__ bit
     if (s_bin[i]) atomicAdd(&sort_counts[i], s_bin[i]);
 }
 
-template __global__ void pack_bits_v16<4>(const uint4*, uint32_t*, long long);
+template __global__ void pack_bits_v16<4>(const RoiParams*, uint32_t*);
 
 }  // namespace sc

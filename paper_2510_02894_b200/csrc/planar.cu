@@ -74,9 +74,10 @@ __device__ __forceinline__ unsigned long long pack_pext(float v, unsigned int id
 __global__ void plane_boxes(const int2* __restrict__ sorted,
                             const unsigned int* __restrict__ start,
                             const unsigned int* __restrict__ cstart,
-                            const unsigned int* __restrict__ cmap, Frame f,
+                            const unsigned int* __restrict__ cmap, const RoiParams* __restrict__ rp,
                             const Stats* __restrict__ st, int4* __restrict__ pboxes,
                             unsigned long long* __restrict__ pext) {
+  Frame f = rp->f;
   if (st->bbox[3] < 0) return;
   const PlaneSpace ps = plane_space(st);
   const long long chunks = (long long)st->plane_chunks;
@@ -125,8 +126,9 @@ __global__ void plane_boxes(const int2* __restrict__ sorted,
 // of its 8 extreme entries -- a real pair, so it bounds that family's maximum
 // from below and seeds it.
 __global__ void plane_lb(const int2* __restrict__ sorted, const unsigned int* __restrict__ start,
-                         const unsigned long long* __restrict__ pext, Frame f,
+                         const unsigned long long* __restrict__ pext, const RoiParams* __restrict__ rp,
                          Stats* __restrict__ st) {
+  Frame f = rp->f;
   if (st->bbox[3] < 0) return;
   const PlaneSpace ps = plane_space(st);
   const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
@@ -168,8 +170,9 @@ __global__ void plane_filter(const unsigned int* __restrict__ start,
                              const unsigned int* __restrict__ tstart,
                              const unsigned int* __restrict__ cstart,
                              const unsigned int* __restrict__ umap,
-                             const int4* __restrict__ pboxes, Frame f, int prune, long long ucap,
+                             const int4* __restrict__ pboxes, const RoiParams* __restrict__ rp, int prune, long long ucap,
                              Stats* __restrict__ st, unsigned int* __restrict__ pwork) {
+  Frame f = rp->f;
   const long long units = (long long)st->plane_units;
   if (st->bbox[3] < 0 || units > ucap) return;  // host re-runs with room
   const PlaneSpace ps = plane_space(st);
@@ -215,10 +218,11 @@ __global__ void __launch_bounds__(kPT) plane_pass1(const int2* __restrict__ sort
                                                    const unsigned int* __restrict__ tstart,
                                                    const unsigned int* __restrict__ umap,
                                                    const unsigned int* __restrict__ pwork,
-                                                   Frame f, int shard, int nshards,
+                                                   const RoiParams* __restrict__ rp, int shard, int nshards,
                                                    long long ucap, float* __restrict__ umax,
                                                    unsigned int* __restrict__ cand,
                                                    Stats* __restrict__ st) {
+  Frame f = rp->f;
   __shared__ float4 sj[kPT];  // (a, b, |p|^2, -)
   __shared__ float s_red[kPT / 32];
   if (st->bbox[3] < 0 || (long long)st->plane_units > ucap) return;
@@ -304,8 +308,9 @@ __global__ void __launch_bounds__(kPT) plane_refine(const int2* __restrict__ sor
                                                     const unsigned int* __restrict__ tstart,
                                                     const unsigned int* __restrict__ umap,
                                                     const unsigned int* __restrict__ pwork,
-                                                    Frame f, const unsigned int* __restrict__ cand,
+                                                    const RoiParams* __restrict__ rp, const unsigned int* __restrict__ cand,
                                                     Stats* __restrict__ st) {
+  Frame f = rp->f;
   __shared__ double sa[kPT], sb[kPT];
   __shared__ double s_red[kPT / 32];
   if (st->bbox[3] < 0) return;

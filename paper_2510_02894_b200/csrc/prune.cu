@@ -179,9 +179,10 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long b)
 // One warp per 256-chunk of the sorted keys: its integer box (boxes[2c] = lo,
 // boxes[2c+1] = hi) and its contribution to the 26 arg-extremes.
 __global__ void __launch_bounds__(256) boxes_extremes(const int4* __restrict__ keys,
-                                                      long long cap, Frame f,
+                                                      long long cap, const RoiParams* __restrict__ rp,
                                                       Stats* __restrict__ st,
                                                       int4* __restrict__ boxes) {
+  Frame f = rp->f;
   __shared__ unsigned long long s_ext[2 * kNDir];
   if (threadIdx.x < 2 * kNDir) s_ext[threadIdx.x] = 0ull;
   __syncthreads();
@@ -245,8 +246,9 @@ __device__ __forceinline__ double axis_reach(int loA, int hiA, int loB, int hiB,
 // compacted into `work` (pair index t over the C x C upper triangle).
 __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys,
                                                    const int4* __restrict__ boxes, long long cap,
-                                                   Frame f, int prune, Stats* __restrict__ st,
+                                                   const RoiParams* __restrict__ rp, int prune, Stats* __restrict__ st,
                                                    unsigned int* __restrict__ work) {
+  Frame f = rp->f;
   __shared__ double px[2 * kNDir], py[2 * kNDir], pz[2 * kNDir];
   __shared__ double s_lb[8];
   const long long n = n_verts(st, cap);

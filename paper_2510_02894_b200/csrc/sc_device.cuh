@@ -46,6 +46,20 @@ struct Frame {
   double sx, sy, sz;   // spacing (fp64, reference arithmetic)
 };
 
+// Per-ROI launch parameters, read by the kernels from device memory (one
+// record per pipeline slot, written by a 96-byte H2D copy before each launch),
+// so a slot's captured CUDA graph is independent of the mask pointer, the
+// dims and the spacing and is replayed for every ROI.
+struct RoiParams {
+  const uint8_t* mask;
+  long long nx, ny, nz;
+  long long n_chunks;  // nx*ny*nz/16 (fast pack path)
+  long long n_words;   // W*ny*nz
+  int W;               // 32-bit words per bit-volume row
+  int pad;
+  Frame f;             // cx2..cz2 are filled on the device from the bbox
+};
+
 // Planar key space: [0, cnt[0]) XY planes keyed by Z2, then cnt[1] XZ planes
 // keyed by Y2, then cnt[2] YZ planes keyed by X2; lo = smallest key per axis.
 struct PlaneSpace {
