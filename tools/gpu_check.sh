@@ -10,9 +10,9 @@ timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 
 timeout 600 python bench.py --steps 20 --warmup 5 > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
 if [ "${1:-}" != "quick" ]; then
   timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-      --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_bench.log 2>&1
+      --log-file $OUT/launches.csv python tools/one_roi.py > $OUT/ncu_bench.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on \
-      -k regex:"diam3d_pass1|pack_bits_v16|mc_cells|plane_pass1|boxes_extremes|scan_all|scatter_all|unit_filter|refine" -s 9 -c 9 \
-      -o $OUT/prof -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_full.log 2>&1
+      -k regex:"pack_bits_v16|bits_bbox|mc_cells|plane_bins_scan|scan_all|scatter_all|boxes_extremes|unit_filter|diam3d_pass1|diam3d_refine|plane_boxes|plane_lb|plane_filter|plane_pass1|plane_refine" -s 15 -c 15 \
+      -o $OUT/prof -f python tools/one_roi.py > $OUT/ncu_full.log 2>&1
 fi
 echo done
