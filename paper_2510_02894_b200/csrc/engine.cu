@@ -79,6 +79,7 @@ namespace {
 thread_local std::string g_err;
 std::atomic<bool> g_opt_prune{true}, g_opt_packed{true}, g_opt_graphs{true};
 std::atomic<int> g_opt_slots{8};  // pipeline slots used by the batch entries
+std::atomic<long long> g_opt_dcap{2LL << 20};  // default diameter-side vertex capacity
 std::atomic<unsigned long long> g_launches{0};
 
 void set_err(const char* fmt, ...) {
@@ -620,7 +621,7 @@ int start_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
     c->dcap_floor = std::max(c->dcap_floor, p->dcap);
   }
   long long cap = vertex_capacity(nx, ny, nz, c->cap_floor);
-  long long dcap = std::min<long long>(cap, std::max<long long>(2LL << 20, c->dcap_floor));
+  long long dcap = std::min<long long>(cap, std::max<long long>(g_opt_dcap.load(), c->dcap_floor));
   const unsigned long long fp0 = c->fingerprint();
   int rc = ensure_buffers(c, nx, ny, nz, cap, dcap, punits);
   if (rc) return rc;
@@ -951,6 +952,7 @@ int sc_set_option(const char* name, int value) {
   else if (std::strcmp(name, "pass1_packed") == 0) g_opt_packed = value != 0;
   else if (std::strcmp(name, "graphs") == 0) g_opt_graphs = value != 0;
   else if (std::strcmp(name, "slots") == 0) g_opt_slots = value;
+  else if (std::strcmp(name, "dcap") == 0) g_opt_dcap = std::max(256, value);
   else { set_err("unknown option %s", name); return SC_ERR_INPUT; }
   return SC_OK;
 }
