@@ -321,3 +321,37 @@ def test_c3_noisy_ellipsoid(sc, oracle_mod, cuda_device):
             if len(grp) >= 2:
                 best = max(best, _hull_max_sq(pts[grp][:, inplane], oracle_mod))
         assert rel_err(getattr(got, key), math.sqrt(best)) <= 1e-12, key
+
+
+_OVERFLOW_SCRIPT = r"""
+import json, sys
+sys.path.insert(0, sys.argv[1])
+from paper_2510_02894_b200 import _native, synth
+import paper_2510_02894_b200 as sc
+_native.set_option("dcap", 1000)   # before any slot exists: buffers start far too small
+arr = synth.thin_slab()
+outs = sc.calculate_coefficients_batch([arr] * 3, [(0.5, 0.5, 5.0)] * 3)
+one = sc.calculate_coefficients(arr, (0.5, 0.5, 5.0))
+print(json.dumps([o.to_dict() | {"T": o.triangle_count, "A": o.active_cubes} for o in outs + [one]]))
+"""
+
+
+def test_capacity_overflow_rerun(golden, cuda_device):
+    """More vertices than the diameter-side buffers hold: the device reports the
+    overflow, the host re-runs with exact sizes, results are unchanged (fresh
+    process so the slots start small)."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    case = next(c for c in golden["big"] if c["name"] == "C5_thin_slab")
+    out = subprocess.run([sys.executable, "-c", _OVERFLOW_SCRIPT, ROOT], capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    for rec in json.loads(out.stdout.strip().splitlines()[-1]):
+        assert rec["VertexCount"] == case["features"]["VertexCount"]
+        assert rec["T"] == case["triangle_count"] and rec["A"] == case["active_cubes"]
+        for k in DIAM_KEYS:
+            assert rec[k] == case["features"][k], k
