@@ -75,6 +75,19 @@ typedef struct {
 int sc_calculate_coefficients(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz,
                               const double spacing[3], int device, sc_coeffs* out);
 
+/* Typed mask payload straight from an NPY file: `data` is the
+ * host payload of an array of NPY shape (s0, s1, s2) = (nz, ny, nx), C order
+ * or Fortran order; dtype code 0 |b1, 1 |u1, 2 <i2, 3 <i4, 4 <i8, 5 <f4, 6 <f8
+ * (reference volume.py:34-42).  Binarization runs on the device: with
+ * has_label, voxels equal to the label (label_int for integer/bool codes,
+ * label_float for float codes, already converted to the payload dtype) are
+ * foreground, otherwise any nonzero voxel (volume.py:173-177).  h2d_ms covers
+ * the copy and the binarization. */
+int sc_calculate_coefficients_raw(const void* data, int dtype, const int64_t shape[3],
+                                  int fortran_order, int has_label, int64_t label_int,
+                                  double label_float, const double spacing[3], int device,
+                                  sc_coeffs* out);
+
 /* Device-resident mask on the CURRENT device; `stream` is a cudaStream_t (NULL =
  * the library's own stream).  The mask must stay valid for the call. */
 int sc_calculate_coefficients_device(const uint8_t* d_mask, int64_t nx, int64_t ny,

@@ -31,6 +31,8 @@ from .features import (
     extract_features,
     mesh_vertices,
 )
+from .npy import coefficients_from_npy, load_npy, parse_npy_header
+from .pipeline import BenchRecord, bench_run, emit_tsv, parse_tsv, render_tsv, run_pipeline
 from .synth import synth_mask
 from .timing import StageTimings
 from .volume import MaskVolume, attach_spacing
@@ -44,4 +46,6 @@ __all__ = [
     "calculate_coefficients_device", "calculate_coefficients_device_batch",
     "calculate_coefficients_shard", "diameters",
     "diameters_parallel", "extract_features", "mesh_vertices", "synth_mask",
+    "coefficients_from_npy", "load_npy", "parse_npy_header", "BenchRecord", "bench_run",
+    "emit_tsv", "parse_tsv", "render_tsv", "run_pipeline",
 ]

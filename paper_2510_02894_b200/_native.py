@@ -26,6 +26,7 @@ EXPORTED = (
     "sc_calculate_coefficients",
     "sc_calculate_coefficients_device",
     "sc_calculate_coefficients_shard",
+    "sc_calculate_coefficients_raw",
     "sc_calculate_coefficients_batch",
     "sc_calculate_coefficients_device_batch",
     "sc_diameters",
@@ -93,6 +94,10 @@ def load():
         L.sc_calculate_coefficients_device_batch.argtypes = [ctypes.POINTER(ctypes.c_void_p),
                                                              ctypes.POINTER(i64), dp, i64,
                                                              ctypes.c_void_p, cp]
+        L.sc_calculate_coefficients_raw.argtypes = [ctypes.c_void_p, ctypes.c_int,
+                                                    ctypes.POINTER(i64), ctypes.c_int,
+                                                    ctypes.c_int, i64, ctypes.c_double, dp,
+                                                    ctypes.c_int, cp]
         L.sc_diameters.argtypes = [dp, dp, dp, i64, ctypes.c_int, dp]
         L.sc_mesh_vertices.argtypes = [u8p, i64, i64, i64, ctypes.c_int,
                                        ctypes.POINTER(ctypes.c_int32), i64,

@@ -67,6 +67,8 @@ __global__ void plane_refine(const int2*, const unsigned int*, const unsigned in
                              const unsigned int*, Stats*);
 __global__ void cloud_diameters(const double*, const double*, const double*, long long, int,
                                 unsigned long long*);
+int launch_binarize(const void*, int, const long long[3], int, int, long long, double, uint8_t*,
+                    int, cudaStream_t);
 template <int MODE>
 __global__ void fp32_probe(float*, int, float, float);
 
@@ -205,7 +207,7 @@ struct Ctx {
   DevBuf<unsigned long long> plane_ext;
   DevBuf<int4> plane_boxes_buf;
   DevBuf<int2> plane_sorted;
-  DevBuf<uint8_t> mask_stage;
+  DevBuf<uint8_t> mask_stage, raw_stage;
   DevBuf<double> cloud;
   DevBuf<unsigned long long> cloud_out;
   // CUDA graphs of whole ROIs, keyed by everything baked into the nodes.
@@ -838,6 +840,46 @@ int sc_calculate_coefficients(const uint8_t* mask, int64_t nx, int64_t ny, int64
   cudaStream_t s = c->stream;
   CK(cudaEventRecord(c->ev[0], s));
   CK(cudaMemcpyAsync(c->mask_stage.p, mask, bytes, cudaMemcpyHostToDevice, s));
+  CK(cudaEventRecord(c->ev[1], s));
+  rc = run_roi(c, c->mask_stage.p, nx, ny, nz, spacing, s, 0, 1, nullptr, out);
+  out->h2d_ms = ev_ms(c->ev[0], c->ev[1]);
+  c->last_ms[6] = out->h2d_ms;
+  out->total_ms = wall_ms() - t0;
+  return rc;
+}
+
+int sc_calculate_coefficients_raw(const void* data, int dtype, const int64_t shape[3],
+                                  int fortran_order, int has_label, int64_t label_int,
+                                  double label_float, const double spacing[3], int device,
+                                  sc_coeffs* out) {
+  const double t0 = wall_ms();
+  static const int itemsize[7] = {1, 1, 2, 4, 8, 4, 8};
+  if (!shape || dtype < 0 || dtype > 6) {
+    set_err("unsupported element type code %d", dtype);
+    return SC_ERR_INPUT;
+  }
+  const int64_t nx = shape[2], ny = shape[1], nz = shape[0];
+  int rc = check_input(data, nx, ny, nz, spacing);
+  if (rc) return rc;
+  if (!out) { set_err("out is NULL"); return SC_ERR_INPUT; }
+  Ctx* c;
+  if ((rc = get_ctx(device, &c))) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(device));
+  std::memset(out, 0, sizeof *out);
+  const size_t n = (size_t)nx * ny * nz, raw_bytes = n * itemsize[dtype];
+  CK(c->raw_stage.ensure(raw_bytes));
+  CK(c->mask_stage.ensure(n));
+  cudaStream_t s = c->stream;
+  CK(cudaEventRecord(c->ev[0], s));
+  CK(cudaMemcpyAsync(c->raw_stage.p, data, raw_bytes, cudaMemcpyHostToDevice, s));
+  const long long shp[3] = {(long long)shape[0], (long long)shape[1], (long long)shape[2]};
+  if (launch_binarize(c->raw_stage.p, dtype, shp, fortran_order ? 1 : 0, has_label ? 1 : 0,
+                      (long long)label_int, label_float, c->mask_stage.p, c->sms * 8, s)) {
+    set_err("unsupported element type code %d", dtype);
+    return SC_ERR_INPUT;
+  }
+  CKL(1);
   CK(cudaEventRecord(c->ev[1], s));
   rc = run_roi(c, c->mask_stage.p, nx, ny, nz, spacing, s, 0, 1, nullptr, out);
   out->h2d_ms = ev_ms(c->ev[0], c->ev[1]);
