@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(kDiamThreads, 3) diam3d_pass1(const int4* __re
                                                                 float* __restrict__ umax,
                                                                 unsigned int* __restrict__ cand,
                                                                 Stats* __restrict__ st) {
+  if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   __shared__ float4 sj_all[kWarps][kChunk];  // (x, y, z, |p|^2) per warp
   const long long n = n_vertices(st, cap);
@@ -180,6 +181,7 @@ __global__ void __launch_bounds__(kDiamThreads) diam3d_refine(const int4* __rest
                                                               const unsigned int* __restrict__ work,
                                                               const unsigned int* __restrict__ cand,
                                                               Stats* __restrict__ st) {
+  if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   __shared__ double sx[kChunk], sy[kChunk], sz[kChunk];
   const long long n = n_vertices(st, cap);

@@ -40,7 +40,7 @@ __global__ void plane_bins_scan(unsigned int*, unsigned int*, unsigned int*, uns
                                 const Stats*);
 __global__ void scan_all(unsigned int*, unsigned int*, const unsigned int*, unsigned int*,
                          unsigned int*, unsigned int*, unsigned int*, unsigned int*, long long,
-                         long long, int, Stats*);
+                         long long, int, long long, Stats*);
 __global__ void scatter_all(const int4*, long long, const Stats*, unsigned int*, int4*,
                             const unsigned int*, unsigned int*, int2*);
 __global__ void boxes_extremes(const int4*, long long, const RoiParams*, Stats*, int4*);
@@ -446,7 +446,8 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   CKL(1);
   scan_all<<<2, 1024, 0, s>>>(c->sort_counts.p, c->sort_cursor.p, c->plane_counts.p,
                               c->plane_start.p, c->plane_tstart.p, c->plane_cstart.p,
-                              c->plane_umap.p, c->plane_cmap.p, pucap, pccap, 256, c->d_stats);
+                              c->plane_umap.p, c->plane_cmap.p, pucap, pccap, 256, dcap,
+                              c->d_stats);
   CKL(1);
   scatter_all<<<c->sms * 4, 256, 0, s>>>(c->keys.p, dcap, c->d_stats, c->sort_cursor.p,
                                          c->keys_sorted.p, c->plane_start.p, c->pbin_cursor.p,

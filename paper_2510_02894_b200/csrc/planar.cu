@@ -77,6 +77,7 @@ __global__ void plane_boxes(const int2* __restrict__ sorted,
                             const unsigned int* __restrict__ cmap, const RoiParams* __restrict__ rp,
                             const Stats* __restrict__ st, int4* __restrict__ pboxes,
                             unsigned long long* __restrict__ pext) {
+  if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   if (st->bbox[3] < 0) return;
   const PlaneSpace ps = plane_space(st);
@@ -128,6 +129,7 @@ __global__ void plane_boxes(const int2* __restrict__ sorted,
 __global__ void plane_lb(const int2* __restrict__ sorted, const unsigned int* __restrict__ start,
                          const unsigned long long* __restrict__ pext, const RoiParams* __restrict__ rp,
                          Stats* __restrict__ st) {
+  if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   if (st->bbox[3] < 0) return;
   const PlaneSpace ps = plane_space(st);
@@ -172,6 +174,7 @@ __global__ void plane_filter(const unsigned int* __restrict__ start,
                              const unsigned int* __restrict__ umap,
                              const int4* __restrict__ pboxes, const RoiParams* __restrict__ rp, int prune, long long ucap,
                              Stats* __restrict__ st, unsigned int* __restrict__ pwork) {
+  if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   const long long units = (long long)st->plane_units;
   if (st->bbox[3] < 0 || units > ucap) return;  // host re-runs with room
@@ -222,6 +225,7 @@ __global__ void __launch_bounds__(kPT) plane_pass1(const int2* __restrict__ sort
                                                    long long ucap, float* __restrict__ umax,
                                                    unsigned int* __restrict__ cand,
                                                    Stats* __restrict__ st) {
+  if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   __shared__ float4 sj[kPT];  // (a, b, |p|^2, -)
   __shared__ float s_red[kPT / 32];
@@ -310,6 +314,7 @@ __global__ void __launch_bounds__(kPT) plane_refine(const int2* __restrict__ sor
                                                     const unsigned int* __restrict__ pwork,
                                                     const RoiParams* __restrict__ rp, const unsigned int* __restrict__ cand,
                                                     Stats* __restrict__ st) {
+  if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   __shared__ double sa[kPT], sb[kPT];
   __shared__ double s_red[kPT / 32];

@@ -47,12 +47,22 @@ __global__ void __launch_bounds__(1024) scan_all(unsigned int* __restrict__ sort
                                                  unsigned int* __restrict__ cstart,
                                                  unsigned int* __restrict__ umap,
                                                  unsigned int* __restrict__ cmap, long long ucap,
-                                                 long long ccap, int plane_tile,
+                                                 long long ccap, int plane_tile, long long dcap,
                                                  Stats* __restrict__ st) {
   int bb[6];
 #pragma unroll
   for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
   if (bb[3] < 0) return;
+  // More vertices than the diameter-side buffers hold: every later kernel
+  // stands down (positions from the full histograms would overflow) and the
+  // host re-runs the ROI with exact sizes.
+  if ((long long)st->n_vert > dcap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->ovf = 1u;
+    if (blockIdx.x == 0) {  // still leave the brick histogram zeroed for the next ROI
+      for (int i = threadIdx.x; i < kSortBins; i += blockDim.x) sort_counts[i] = 0u;
+    }
+    return;
+  }
   if (blockIdx.x == 0) {
     constexpr int per = kSortBins / 1024;
     unsigned int v[per], sum = 0;
@@ -119,6 +129,7 @@ __global__ void scatter_all(const int4* __restrict__ keys, long long cap,
                             const unsigned int* __restrict__ plane_start,
                             unsigned int* __restrict__ pbin_cursor,
                             int2* __restrict__ plane_sorted) {
+  if (st->ovf) return;  // re-run pending (scan_all)
   const long long n = n_verts(st, cap);
   int bb[6];
 #pragma unroll
@@ -182,6 +193,7 @@ __global__ void __launch_bounds__(256) boxes_extremes(const int4* __restrict__ k
                                                       long long cap, const RoiParams* __restrict__ rp,
                                                       Stats* __restrict__ st,
                                                       int4* __restrict__ boxes) {
+  if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   __shared__ unsigned long long s_ext[2 * kNDir];
   if (threadIdx.x < 2 * kNDir) s_ext[threadIdx.x] = 0ull;
@@ -248,6 +260,7 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
                                                    const int4* __restrict__ boxes, long long cap,
                                                    const RoiParams* __restrict__ rp, int prune, Stats* __restrict__ st,
                                                    unsigned int* __restrict__ work) {
+  if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   __shared__ double px[2 * kNDir], py[2 * kNDir], pz[2 * kNDir];
   __shared__ double s_lb[8];
