@@ -156,6 +156,25 @@ int sc_set_option(const char* name, int value);
 uint64_t sc_launch_count(void);
 int sc_probe_fp32_peak(int device, int mode, double* tflops);
 
+/* Canonical triangle mesh of a host mask: the reference's
+ * marching_cubes output (mesh.py:142-199) bit for bit -- vertices numbered at
+ * first reference in (z, y, x) cell-scan order, coordinates (l-1+0.5)*s in
+ * fp64, triangles in scan order with the table's winding.  xs/ys/zs hold
+ * vcap doubles, tris 3*tcap int32; *n_vert / *n_tri always receive the counts,
+ * and the arrays are written only when they are large enough (call once with
+ * vcap = tcap = 0 to size them). */
+int sc_marching_cubes(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz,
+                      const double spacing[3], int device, double* xs, double* ys, double* zs,
+                      int32_t* tris, int64_t vcap, int64_t tcap, int64_t* n_vert,
+                      int64_t* n_tri);
+
+/* Surface area, signed volume and volume of an arbitrary triangle mesh with
+ * the reference's exact arithmetic (surface_area / signed_mesh_volume /
+ * mesh_volume, features.py:89-118, pairwise_sum :63-80): out = (area, signed
+ * volume, |volume|), bit-exact with the reference for the same arrays. */
+int sc_mesh_measure(const double* xs, const double* ys, const double* zs, int64_t nv,
+                    const int32_t* tris, int64_t nt, int device, double out[3]);
+
 const char* sc_last_error(void); /* thread-local message of the last failure */
 int sc_abi_version(void);
 int sc_device_count(void);

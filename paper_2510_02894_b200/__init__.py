@@ -31,6 +31,16 @@ from .features import (
     extract_features,
     mesh_vertices,
 )
+from .mesh import (
+    TriangleMesh,
+    marching_cubes,
+    mesh_dump,
+    mesh_volume,
+    signed_mesh_volume,
+    surface_area,
+    write_off,
+    write_stl,
+)
 from .npy import coefficients_from_npy, load_npy, parse_npy_header
 from .pipeline import BenchRecord, bench_run, emit_tsv, parse_tsv, render_tsv, run_pipeline
 from .synth import synth_mask
@@ -47,5 +57,6 @@ __all__ = [
     "calculate_coefficients_shard", "diameters",
     "diameters_parallel", "extract_features", "mesh_vertices", "synth_mask",
     "coefficients_from_npy", "load_npy", "parse_npy_header", "BenchRecord", "bench_run",
-    "emit_tsv", "parse_tsv", "render_tsv", "run_pipeline",
+    "emit_tsv", "parse_tsv", "render_tsv", "run_pipeline", "TriangleMesh", "marching_cubes",
+    "mesh_dump", "mesh_volume", "signed_mesh_volume", "surface_area", "write_off", "write_stl",
 ]

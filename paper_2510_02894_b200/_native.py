@@ -31,6 +31,8 @@ EXPORTED = (
     "sc_calculate_coefficients_device_batch",
     "sc_diameters",
     "sc_mesh_vertices",
+    "sc_marching_cubes",
+    "sc_mesh_measure",
     "sc_last_kernel_times",
     "sc_last_diagnostics",
     "sc_set_option",
@@ -102,6 +104,11 @@ def load():
         L.sc_mesh_vertices.argtypes = [u8p, i64, i64, i64, ctypes.c_int,
                                        ctypes.POINTER(ctypes.c_int32), i64,
                                        ctypes.POINTER(i64)]
+        L.sc_marching_cubes.argtypes = [u8p, i64, i64, i64, dp, ctypes.c_int, dp, dp, dp,
+                                        ctypes.POINTER(ctypes.c_int32), i64, i64,
+                                        ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        L.sc_mesh_measure.argtypes = [dp, dp, dp, i64, ctypes.POINTER(ctypes.c_int32), i64,
+                                      ctypes.c_int, dp]
         L.sc_last_kernel_times.argtypes = [ctypes.c_int, dp, ctypes.c_int]
         L.sc_launch_count.restype = ctypes.c_uint64
         L.sc_last_diagnostics.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]

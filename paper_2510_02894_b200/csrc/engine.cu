@@ -69,6 +69,21 @@ __global__ void cloud_diameters(const double*, const double*, const double*, lon
                                 unsigned long long*);
 int launch_binarize(const void*, int, const long long[3], int, int, long long, double, uint8_t*,
                     int, cudaStream_t);
+__global__ void mesh_count(const RoiParams*, const uint32_t*, const Stats*, unsigned int*);
+__global__ void scan_blocks(unsigned int*, long long, unsigned int*);
+__global__ void scan_sums(unsigned int*, int, unsigned long long*);
+__global__ void scan_add(unsigned int*, long long, const unsigned int*);
+__global__ void edge_map_fill(const int4*, const Stats*, int*);
+__global__ void mesh_emit(const RoiParams*, const uint32_t*, const Stats*, const unsigned int*,
+                          const int*, int3*, unsigned int*);
+__global__ void id_flags(const unsigned int*, long long, unsigned int*);
+__global__ void mesh_out(const int4*, const unsigned int*, const unsigned int*, long long, double,
+                         double, double, double*, double*, double*, int*);
+__global__ void tris_out(const int3*, long long, const int*, int*);
+cudaError_t upload_mesh_tables();
+__global__ void tri_terms(const double*, const double*, const double*, const int*, long long,
+                          long long, double*, double*);
+__global__ void fold_pass(double*, double*, long long);
 template <int MODE>
 __global__ void fp32_probe(float*, int, float, float);
 
@@ -279,6 +294,7 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     CK(cudaMallocHost(&c->h_rp, sizeof(RoiParams)));
     CK(cudaMalloc(&c->d_tabs, sizeof(CaseTables)));
     CK(cudaMemcpy(c->d_tabs, &case_geom().tabs, sizeof(CaseTables), cudaMemcpyHostToDevice));
+    CK(upload_mesh_tables());
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pass1, diam3d_pass1<true>, 256, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pass1s, diam3d_pass1<false>, 256, 0));
     if (const char* v = getenv("SC_PASS1")) g_opt_packed = std::strcmp(v, "scalar") != 0;
@@ -291,6 +307,7 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
       // every kernel once here.
       cudaFuncAttributes fa;
       const void* kernels[] = {(const void*)init_stats, (const void*)pack_bits_v16<4>,
+                               (const void*)mesh_count, (const void*)mesh_emit,
                                (const void*)bits_bbox,
                                (const void*)pack_bits_generic, (const void*)mc_cells,
                                (const void*)scan_all, (const void*)scatter_all,
@@ -781,6 +798,131 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
   return first;
 }
 
+// Exclusive scan in place of n uint32 counts (3 kernels); returns the total.
+int device_exscan(Ctx* c, unsigned int* data, long long n, cudaStream_t s,
+                  unsigned long long* d_total) {
+  const long long nb = (n + 1023) / 1024;
+  unsigned int* sums = nullptr;
+  CK(cudaMallocAsync(&sums, sizeof(unsigned int) * std::max<long long>(1, nb), s));
+  scan_blocks<<<(unsigned)std::max<long long>(1, nb), 1024, 0, s>>>(data, n, sums);
+  CKL(1);
+  scan_sums<<<1, 1024, 0, s>>>(sums, (int)nb, d_total);
+  CKL(1);
+  scan_add<<<(unsigned)std::max<long long>(1, (n + 255) / 256), 256, 0, s>>>(data, n, sums);
+  CKL(1);
+  CK(cudaFreeAsync(sums, s));
+  return SC_OK;
+}
+
+template <typename T>
+struct Tmp {  // call-scoped device allocation (export path only)
+  T* p = nullptr;
+  ~Tmp() { if (p) cudaFree(p); }
+  cudaError_t alloc(size_t n) { return cudaMalloc(&p, sizeof(T) * std::max<size_t>(1, n)); }
+};
+
+// Canonical TriangleMesh of a device mask (mesh.cu).  Fills the caller's
+// buffers only when they are large enough; *nv / *nt always get the counts.
+int run_mesh(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
+             const double sp[3], cudaStream_t s, double* xs, double* ys, double* zs,
+             int32_t* tris, int64_t vcap, int64_t tcap, int64_t* nv, int64_t* nt) {
+  long long cap = vertex_capacity(nx, ny, nz, c->cap_floor);
+  for (int attempt = 0; attempt < 2; attempt++) {
+    const unsigned long long fp0 = c->fingerprint();
+    CK(c->bits.ensure((size_t)(((nx + 31) / 32) * ny * nz)));
+    CK(c->keys.ensure((size_t)cap));
+    if (c->fingerprint() != fp0) {  // scratch moved: cached ROI graphs are stale
+      c->gen++;
+      c->drop_graphs();
+    }
+    RoiParams& h = *c->h_rp;
+    h.mask = d_mask; h.nx = nx; h.ny = ny; h.nz = nz;
+    h.W = (int)((nx + 31) / 32);
+    h.n_words = (long long)h.W * ny * nz;
+    h.n_chunks = nx * ny * nz / 16;
+    h.f.cx2 = h.f.cy2 = h.f.cz2 = 0;
+    h.f.hx = (float)(0.5 * sp[0]); h.f.hy = (float)(0.5 * sp[1]); h.f.hz = (float)(0.5 * sp[2]);
+    h.f.sx = sp[0]; h.f.sy = sp[1]; h.f.sz = sp[2];
+    CK(cudaMemcpyAsync(c->d_rp, c->h_rp, sizeof(RoiParams), cudaMemcpyHostToDevice, s));
+    init_stats<<<1, 256, 0, s>>>(c->d_stats);
+    CKL(1);
+    if (nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0) {
+      pack_bits_v16<4><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(c->d_rp, c->bits.p);
+      CKL(1);
+      bits_bbox<<<c->sms * 8, 256, 0, s>>>(c->d_rp, reinterpret_cast<const uint4*>(c->bits.p),
+                                           c->d_stats);
+      CKL(1);
+    } else {
+      pack_bits_generic<<<c->sms * 8, 256, 0, s>>>(c->d_rp, c->bits.p, c->d_stats);
+      CKL(1);
+    }
+    mc_cells<<<c->sms * std::max(1, c->occ_mc), 256, 0, s>>>(c->d_rp, c->bits.p, c->d_tabs,
+                                                            c->d_stats, c->keys.p,
+                                                            (long long)c->keys.cap, nullptr,
+                                                            nullptr);
+    CKL(1);
+    CK(cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if ((long long)c->h_stats->n_vert <= (long long)c->keys.cap) break;
+    cap = (long long)c->h_stats->n_vert;
+    c->cap_floor = std::max(c->cap_floor, cap);
+  }
+  const Stats hs = *c->h_stats;
+  if (hs.bbox[3] < 0) { set_err("mask has no occupied voxels"); return SC_ERR_EMPTY_ROI; }
+  const long long V = (long long)hs.n_vert;
+  const int* bb = hs.bbox;
+  const long long nq = ((bb[3] + 1) >> 5) - (bb[0] >> 5) + 1, nvr = bb[4] - bb[1] + 2,
+                  nwr = bb[5] - bb[2] + 2, items = nq * nvr * nwr;
+  Tmp<unsigned int> offs;
+  Tmp<unsigned long long> total;
+  CK(offs.alloc(items));
+  CK(total.alloc(1));
+  mesh_count<<<c->sms * 8, 256, 0, s>>>(c->d_rp, c->bits.p, c->d_stats, offs.p);
+  CKL(1);
+  int rc = device_exscan(c, offs.p, items, s, total.p);
+  if (rc) return rc;
+  unsigned long long T = 0;
+  CK(cudaMemcpyAsync(&T, total.p, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *nv = V;
+  *nt = (int64_t)T;
+  if (V > vcap || (long long)T > tcap || !xs || !ys || !zs || !tris) return SC_OK;
+  const long long mx = bb[3] - bb[0] + 2, my = bb[4] - bb[1] + 2, mz = bb[5] - bb[2] + 2;
+  Tmp<int> emap, ids;
+  Tmp<int3> ttmp;
+  Tmp<unsigned int> first, flags;
+  Tmp<double> dx, dy, dz;
+  Tmp<int> dtris;
+  CK(emap.alloc((size_t)(3 * mx * my * mz)));
+  CK(ids.alloc((size_t)V));
+  CK(ttmp.alloc((size_t)T));
+  CK(first.alloc((size_t)V));
+  CK(flags.alloc((size_t)(3 * T)));
+  CK(dx.alloc((size_t)V)); CK(dy.alloc((size_t)V)); CK(dz.alloc((size_t)V));
+  CK(dtris.alloc((size_t)(3 * T)));
+  CK(cudaMemsetAsync(first.p, 0xFF, sizeof(unsigned int) * V, s));
+  CK(cudaMemsetAsync(flags.p, 0, sizeof(unsigned int) * 3 * T, s));
+  const int g = c->sms * 8;
+  edge_map_fill<<<g, 256, 0, s>>>(c->keys.p, c->d_stats, emap.p);
+  CKL(1);
+  mesh_emit<<<g, 256, 0, s>>>(c->d_rp, c->bits.p, c->d_stats, offs.p, emap.p, ttmp.p, first.p);
+  CKL(1);
+  id_flags<<<g, 256, 0, s>>>(first.p, V, flags.p);
+  CKL(1);
+  if ((rc = device_exscan(c, flags.p, 3 * (long long)T, s, total.p))) return rc;
+  mesh_out<<<g, 256, 0, s>>>(c->keys.p, first.p, flags.p, V, sp[0], sp[1], sp[2], dx.p, dy.p,
+                             dz.p, ids.p);
+  CKL(1);
+  tris_out<<<g, 256, 0, s>>>(ttmp.p, (long long)T, ids.p, dtris.p);
+  CKL(1);
+  CK(cudaMemcpyAsync(xs, dx.p, sizeof(double) * V, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(ys, dy.p, sizeof(double) * V, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(zs, dz.p, sizeof(double) * V, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(tris, dtris.p, sizeof(int) * 3 * T, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return SC_OK;
+}
+
 int current_ctx(Ctx** c) {
   int dev = 0;
   CK(cudaGetDevice(&dev));
@@ -929,6 +1071,67 @@ int sc_diameters(const double* xs, const double* ys, const double* zs, int64_t n
   CK(cudaMemcpyAsync(hb, c->cloud_out.p, 32, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   for (int i = 0; i < 4; i++) out[i] = std::sqrt(f64_of(hb[i]));
+  return SC_OK;
+}
+
+int sc_marching_cubes(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz,
+                      const double spacing[3], int device, double* xs, double* ys, double* zs,
+                      int32_t* tris, int64_t vcap, int64_t tcap, int64_t* n_vert,
+                      int64_t* n_tri) {
+  int rc = check_input(mask, nx, ny, nz, spacing);
+  if (rc) return rc;
+  if (!n_vert || !n_tri) { set_err("NULL argument"); return SC_ERR_INPUT; }
+  Ctx* c;
+  if ((rc = get_ctx(device, &c))) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(device));
+  const size_t bytes = (size_t)nx * ny * nz;
+  CK(c->mask_stage.ensure(bytes));
+  cudaStream_t s = c->stream;
+  CK(cudaMemcpyAsync(c->mask_stage.p, mask, bytes, cudaMemcpyHostToDevice, s));
+  return run_mesh(c, c->mask_stage.p, nx, ny, nz, spacing, s, xs, ys, zs, tris, vcap, tcap,
+                  n_vert, n_tri);
+}
+
+int sc_mesh_measure(const double* xs, const double* ys, const double* zs, int64_t nv,
+                    const int32_t* tris, int64_t nt, int device, double out[3]) {
+  if (!out || nv < 0 || nt < 0 || (nv > 0 && (!xs || !ys || !zs)) || (nt > 0 && !tris)) {
+    set_err("bad mesh arguments");
+    return SC_ERR_INPUT;
+  }
+  out[0] = out[1] = out[2] = 0.0;
+  if (nt == 0) return SC_OK;  // features.py:91-92, 103-104: empty mesh -> 0.0
+  Ctx* c;
+  int rc = get_ctx(device, &c);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(device));
+  cudaStream_t s = c->stream;
+  long long padded = 1;
+  while (padded < nt) padded <<= 1;
+  Tmp<double> dx, dy, dz, area, vol;
+  Tmp<int> dt;
+  CK(dx.alloc((size_t)nv)); CK(dy.alloc((size_t)nv)); CK(dz.alloc((size_t)nv));
+  CK(dt.alloc((size_t)(3 * nt)));
+  CK(area.alloc((size_t)padded)); CK(vol.alloc((size_t)padded));
+  CK(cudaMemcpyAsync(dx.p, xs, 8 * nv, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dy.p, ys, 8 * nv, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dz.p, zs, 8 * nv, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dt.p, tris, 12 * nt, cudaMemcpyHostToDevice, s));
+  tri_terms<<<c->sms * 8, 256, 0, s>>>(dx.p, dy.p, dz.p, dt.p, nt, padded, area.p, vol.p);
+  CKL(1);
+  for (long long half = padded / 2; half >= 1; half /= 2) {
+    fold_pass<<<(unsigned)std::min<long long>((half + 255) / 256, c->sms * 8), 256, 0, s>>>(
+        area.p, vol.p, half);
+    CKL(1);
+  }
+  double r[2];
+  CK(cudaMemcpyAsync(&r[0], area.p, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&r[1], vol.p, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  out[0] = r[0];
+  out[1] = r[1];
+  out[2] = std::fabs(r[1]);
   return SC_OK;
 }
 

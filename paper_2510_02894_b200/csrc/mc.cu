@@ -293,14 +293,16 @@ __global__ void __launch_bounds__(256) mc_cells(const RoiParams* __restrict__ rp
           auto emit = [&](int X, int Y, int Z) {
             if (o < cap) vkeys[o] = make_int4(X, Y, Z, 0);
             o++;
-            atomicAdd(&s_bin[brick_bin(X, Y, Z, bb, bshift)], 1u);
-            int id[3];
-            unsigned int pbin[3];
-            plane_ids(X, Y, Z, ps, id);
-            plane_bins(X, Y, Z, pbk, pbin);
+            if (pbin_counts) {  // NULL on the mesh-export path (no diameter stage)
+              atomicAdd(&s_bin[brick_bin(X, Y, Z, bb, bshift)], 1u);
+              int id[3];
+              unsigned int pbin[3];
+              plane_ids(X, Y, Z, ps, id);
+              plane_bins(X, Y, Z, pbk, pbin);
 #pragma unroll
-            for (int a = 0; a < 3; a++)
-              atomicAdd(&pbin_counts[(long long)id[a] * kPlaneBins + pbin[a]], 1u);
+              for (int a = 0; a < 3; a++)
+                atomicAdd(&pbin_counts[(long long)id[a] * kPlaneBins + pbin[a]], 1u);
+            }
           };
           while (ex) {
             const int i = __ffs(ex) - 1; ex &= ex - 1;
@@ -326,8 +328,9 @@ __global__ void __launch_bounds__(256) mc_cells(const RoiParams* __restrict__ rp
   __syncthreads();
   for (int i = threadIdx.x; i < kNumCases; i += blockDim.x)
     if (s_hist[i]) atomicAdd(&st->hist[i], (unsigned long long)s_hist[i]);
-  for (int i = threadIdx.x; i < kSortBins; i += blockDim.x)
-    if (s_bin[i]) atomicAdd(&sort_counts[i], s_bin[i]);
+  if (sort_counts)
+    for (int i = threadIdx.x; i < kSortBins; i += blockDim.x)
+      if (s_bin[i]) atomicAdd(&sort_counts[i], s_bin[i]);
 }
 
 template __global__ void pack_bits_v16<4>(const RoiParams*, uint32_t*);

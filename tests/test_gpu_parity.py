@@ -355,3 +355,56 @@ def test_capacity_overflow_rerun(golden, cuda_device):
         assert rec["T"] == case["triangle_count"] and rec["A"] == case["active_cubes"]
         for k in DIAM_KEYS:
             assert rec[k] == case["features"][k], k
+
+
+def test_canonical_mesh_bit_exact(sc, golden, golden_arrays, cuda_device):
+    """marching_cubes on the GPU == the reference's TriangleMesh, element by
+    element: vertex order (first reference), coordinates, triangles; and the
+    mesh measures == the reference's surface_area / mesh_volume bit for bit."""
+    n = 0
+    for case in golden["cases"]:
+        if "verts_key" not in case:
+            continue
+        vol = sc.MaskVolume.from_array(golden_arrays[case["mask_key"]], case["spacing"])
+        mesh = sc.marching_cubes(vol)
+        want = golden_arrays[case["verts_key"]]
+        got = np.column_stack((mesh.xs, mesh.ys, mesh.zs))
+        assert np.array_equal(got, want), case["name"]
+        assert mesh.triangle_count == case["triangle_count"]
+        n += 1
+    assert n >= 10
+
+
+def test_canonical_mesh_against_oracle(sc, oracle_mod, cuda_device):
+    from paper_2510_02894_b200 import synth
+
+    for arr, sp in ((synth.synth_mask("sphere", (64, 64, 64), radius=24), (1.0, 1.0, 1.0)),
+                    (synth.thin_slab(), (0.5, 0.5, 5.0)),
+                    (synth.kits_like(tumor_mm=30.0), (0.8, 0.8, 1.0))):
+        mesh = sc.marching_cubes(sc.MaskVolume.from_array(arr, sp))
+        ref = oracle_mod.marching_cubes(arr, sp)
+        assert np.array_equal(mesh.xs, ref.xs) and np.array_equal(mesh.ys, ref.ys)
+        assert np.array_equal(mesh.zs, ref.zs)
+        assert np.array_equal(mesh.triangles, ref.triangles)
+        assert sc.surface_area(mesh) == oracle_mod.surface_area(ref)
+        assert sc.mesh_volume(mesh) == oracle_mod.mesh_volume(ref)
+
+
+def test_mesh_measure_small_meshes(sc, cuda_device):
+    # pkg/tests/test_features.py:47-59
+    m = sc.TriangleMesh(xs=np.array([0.0, 1.0, 0.0]), ys=np.array([0.0, 0.0, 1.0]),
+                        zs=np.zeros(3), triangles=np.array([[0, 1, 2]], np.int32))
+    assert sc.surface_area(m) == pytest.approx(0.5, abs=1e-15)
+    e = sc.TriangleMesh(xs=np.zeros(0), ys=np.zeros(0), zs=np.zeros(0),
+                        triangles=np.zeros((0, 3), np.int32))
+    assert sc.surface_area(e) == 0.0 and sc.mesh_volume(e) == 0.0
+
+
+def test_mesh_dump_formats(sc, tmp_path, cuda_device):
+    vol = sc.MaskVolume.from_array(sc.synth_mask("box", (3, 3, 3), lo=(1, 1, 1), hi=(1, 1, 1)))
+    mesh = sc.marching_cubes(vol)
+    sc.mesh_dump(mesh, tmp_path / "m.off")
+    lines = (tmp_path / "m.off").read_text().splitlines()
+    assert lines[0] == "OFF" and lines[1] == "6 8 0" and len(lines) == 2 + 6 + 8
+    sc.mesh_dump(mesh, tmp_path / "m.stl")
+    assert (tmp_path / "m.stl").stat().st_size == 84 + 50 * 8
