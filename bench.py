@@ -490,6 +490,56 @@ def run_ours(args):
     return 0
 
 
+def run_split(args):
+    """one very large ROI, its pair grid split across the ranks.
+    Every rank runs marching cubes (cheap) and its 1/N of the surviving 3-D and
+    planar work units; the 4 squared maxima are combined with one NCCL
+    all_reduce(MAX).  Time per step = max over ranks; "scaling": "strong"."""
+    import torch
+
+    import paper_2510_02894_b200 as sc
+    from paper_2510_02894_b200 import sharding
+
+    world, rank, local = dist_setup(args.gpus)
+    dev = torch.cuda.current_device()
+    rois, cfg = load_workload(args.workload, 0, 1)
+    mask, sp = rois[0]
+    d_mask = torch.from_numpy(mask).to(f"cuda:{dev}")
+    for _ in range(max(3, args.warmup)):
+        rec = sharding.sharded_coefficients(d_mask, sp)
+    torch.cuda.synchronize()
+    barrier(world)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(dev)
+    clocks.__enter__()
+    ev0.record()
+    for _ in range(args.steps):
+        rec = sharding.sharded_coefficients(d_mask, sp)
+    ev1.record()
+    torch.cuda.synchronize()
+    clocks.__exit__(None, None, None)
+    ms = max_over_ranks(world, ev0.elapsed_time(ev1))
+    barrier(world)
+    full = sc.calculate_coefficients_device(d_mask, sp)
+    for k in ("Maximum3DDiameter", "Maximum2DDiameterXY", "Maximum2DDiameterXZ",
+              "Maximum2DDiameterYZ", "VertexCount"):
+        assert rec[k] == full.to_dict()[k], k
+    cfg.update({"global_batch": 1, "parallelism": f"pair-grid split x{world} + NCCL all_reduce(MAX)"})
+    line = {"metric": METRIC, "value": args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
+            "data": "synthetic", "config": cfg, "clocks": clocks.summary(),
+            "path": "sharding.sharded_coefficients -> sc_calculate_coefficients_shard",
+            "result": {k: rec[k] for k in ("VertexCount", "Maximum3DDiameter")}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -499,11 +549,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=150.0)
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--split", action="store_true",
+                    help="strong scaling of ONE ROI: every rank evaluates its share of the pair "
+                         "grid (sc_calculate_coefficients_shard) + one NCCL all_reduce(MAX)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # contract: W >= 3 warm-up steps
     if args.impl == "reference":
         return run_reference(args)
+    if args.split:
+        return run_split(args)
     return run_ours(args)
 
 
