@@ -174,7 +174,7 @@ def probe_fp32_peak(device: int = 0, mode: int = 0) -> float:
 
 DIAG_NAMES = ("work_units", "total_units", "refine_candidates", "planar_units",
               "planar_candidates", "planar_work_units")
-PAIRS_PER_UNIT = 256 * 256
+PAIRS_PER_UNIT = 128 * 128
 
 
 def last_diagnostics(device: int = 0) -> dict:

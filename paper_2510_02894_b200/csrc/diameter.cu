@@ -33,26 +33,8 @@ namespace sc {
 
 constexpr int kDiamThreads = 256;
 constexpr int kWarps = kDiamThreads / 32;
-constexpr int kChunk = 256;                    // vertices per chunk (pair unit = chunk x chunk)
-constexpr int kR = kChunk / 32;                // 8 i vertices per lane
-
-// Compact the units whose pass-1 maximum can hold the exact maximum
-// (one block; called by the last block of the pass-1 grid).
-__device__ __forceinline__ void select_units(const float* __restrict__ umax, long long units,
-                                             Stats* __restrict__ st, unsigned int* __restrict__ cand) {
-  const float tau = __uint_as_float(__ldcg(&st->d3_f32)) * (1.f - kRefineRel);
-  const int lane = threadIdx.x & 31;
-  for (long long base = 0; base < units; base += blockDim.x) {
-    const long long u = base + threadIdx.x;
-    const bool hit = u < units && __ldcg(umax + u) >= tau;
-    const unsigned int mask = __ballot_sync(0xffffffffu, hit);
-    if (!mask) continue;
-    unsigned long long pos = 0;
-    if (lane == 0) pos = atomicAdd(&st->n_cand, (unsigned long long)__popc(mask));
-    pos = __shfl_sync(0xffffffffu, pos, 0);
-    if (hit) cand[pos + __popc(mask & ((1u << lane) - 1))] = (unsigned int)u;
-  }
-}
+constexpr int kChunk = kChunk3;                // vertices per chunk (pair unit = chunk x chunk)
+constexpr int kR = kChunk / 32;                // 4 i vertices per lane
 
 // Pass 1 (see header).  Work unit = one surviving chunk pair (I <= J, 256 x
 // 256 vertex pairs, listed by unit_filter); every WARP is an independent
@@ -65,20 +47,19 @@ __device__ __forceinline__ void select_units(const float* __restrict__ umax, lon
 // scalar operand), so 4 pairs cost 6 FFMA2 + 2 FMNMX3 = 2 issue slots per
 // pair instead of 3.5 for scalar FFMA.
 template <bool PACKED>
-__global__ void __launch_bounds__(kDiamThreads, 3) diam3d_pass1(const int4* __restrict__ keys,
+__global__ void __launch_bounds__(kDiamThreads, 4) diam3d_pass1(const int4* __restrict__ keys,
                                                                 long long cap, const RoiParams* __restrict__ rp, int shard,
                                                                 int nshards,
-                                                                const unsigned int* __restrict__ work,
+                                                                const uint2* __restrict__ work,
                                                                 float* __restrict__ umax,
-                                                                unsigned int* __restrict__ cand,
                                                                 Stats* __restrict__ st) {
-  if (st->ovf) return;  // re-run pending (scan_all)
+  // Re-run pending: too many vertices (scan_all) or surviving units (unit_filter).
+  if (st->ovf || (long long)st->n_work > rp->wcap) return;
   Frame f = rp->f;
   __shared__ float4 sj_all[kWarps][kChunk];  // (x, y, z, |p|^2) per warp
   const long long n = n_vertices(st, cap);
   if (n == 0) return;
   frame_centre(st, f);
-  const long long C = (n + kChunk - 1) / kChunk;
   const long long n_work = (long long)st->n_work;
   long long w0, w1;
   shard_span(n_work, shard, nshards, w0, w1);
@@ -94,8 +75,8 @@ __global__ void __launch_bounds__(kDiamThreads, 3) diam3d_pass1(const int4* __re
   int prevI = -1;
   float a[kR], b[kR], c[kR], ni[kR];
   for (long long w = wb; w < we; w++) {
-    int I, J;
-    tile_pair(work[w], C, I, J);
+    const uint2 ij = work[w];
+    const int I = (int)ij.x, J = (int)ij.y;
     float m[kR];
     __syncwarp();  // previous unit is done with sj
 #pragma unroll
@@ -164,48 +145,69 @@ __global__ void __launch_bounds__(kDiamThreads, 3) diam3d_pass1(const int4* __re
     run = fmaxf(run, best);
   }
   if (lane == 0) atomic_max_pos_f32(&st->d3_f32, run);
-  // The last block to finish compacts the units within kRefineRel of the
-  // global pass-1 maximum for the exact re-check.
-  if (last_block(&st->done1)) select_units(umax, n_work, st, cand);
 }
 template __global__ void diam3d_pass1<true>(const int4*, long long, const RoiParams*, int, int,
-                                            const unsigned int*, float*, unsigned int*, Stats*);
+                                            const uint2*, float*, Stats*);
 template __global__ void diam3d_pass1<false>(const int4*, long long, const RoiParams*, int, int,
-                                             const unsigned int*, float*, unsigned int*, Stats*);
+                                             const uint2*, float*, Stats*);
 
-// Exact re-check: each selected chunk pair, 256 x 256 in fp64 with the
-// reference arithmetic on the reference coordinates; one block per candidate
-// (thread = one i vertex), persistent grid.
+// Exact re-check.  Every block sweeps 256 work entries at a time: the units
+// whose pass-1 maximum lies within kRefineRel of the (now complete) pass-1
+// maximum are listed in shared memory and each is re-evaluated, 128 x 128 in
+// fp64 with the reference arithmetic on the reference coordinates (thread =
+// one i vertex x half of the j chunk).  Selection is fully parallel: no
+// serial scan of the unit maxima anywhere.
 __global__ void __launch_bounds__(kDiamThreads) diam3d_refine(const int4* __restrict__ keys,
                                                               long long cap, const RoiParams* __restrict__ rp,
-                                                              const unsigned int* __restrict__ work,
-                                                              const unsigned int* __restrict__ cand,
+                                                              int shard, int nshards,
+                                                              const uint2* __restrict__ work,
+                                                              const float* __restrict__ umax,
                                                               Stats* __restrict__ st) {
-  if (st->ovf) return;  // re-run pending (scan_all)
+  if (st->ovf || (long long)st->n_work > rp->wcap) return;  // re-run pending
+  static_assert(kDiamThreads % kChunk == 0, "refine splits j across kDiamThreads / kChunk groups");
+  constexpr int kSplit = kDiamThreads / kChunk, kJ = kChunk / kSplit;
   Frame f = rp->f;
   __shared__ double sx[kChunk], sy[kChunk], sz[kChunk];
+  __shared__ unsigned int s_list[kDiamThreads];
+  __shared__ int s_n;
   const long long n = n_vertices(st, cap);
-  const long long C = (n + kChunk - 1) / kChunk;
-  const long long nc = (long long)st->n_cand;
+  long long w0, w1;
+  shard_span((long long)st->n_work, shard, nshards, w0, w1);
+  const float tau = __uint_as_float(st->d3_f32) * (1.f - kRefineRel);
+  const int ti = threadIdx.x % kChunk, tj = (threadIdx.x / kChunk) * kJ;
   double best = 0.0;
-  for (long long u = blockIdx.x; u < nc; u += gridDim.x) {
-    int I, J;
-    tile_pair(work[cand[u]], C, I, J);
+  // Block b sweeps entries w0 + b, w0 + b + G, ... (G = grid size), 256 at a
+  // time, so candidates (adjacent in the work list) spread over the blocks.
+  const long long G = gridDim.x;
+  for (long long sweep = 0; w0 + sweep * kDiamThreads * G < w1; sweep++) {
+    __syncthreads();  // previous sweep is done with s_list / s_n
+    if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
-    {
-      const long long j = (long long)J * kChunk + threadIdx.x;
-      const int4 kj = keys[j < n ? j : n - 1];
-      sx[threadIdx.x] = ref_coord(kj.x, f.sx);
-      sy[threadIdx.x] = ref_coord(kj.y, f.sy);
-      sz[threadIdx.x] = ref_coord(kj.z, f.sz);
-    }
+    const long long w = w0 + (sweep * kDiamThreads + threadIdx.x) * G + blockIdx.x;
+    if (w < w1 && umax[w] >= tau) s_list[atomicAdd(&s_n, 1)] = (unsigned int)w;
     __syncthreads();
-    const long long i = (long long)I * kChunk + threadIdx.x;
-    if (i < n) {
-      const int4 ki = keys[i];
-      const double xi = ref_coord(ki.x, f.sx), yi = ref_coord(ki.y, f.sy), zi = ref_coord(ki.z, f.sz);
+    const int cnt = s_n;
+    if (threadIdx.x == 0 && cnt) atomicAdd(&st->n_cand, (unsigned long long)cnt);
+    for (int q = 0; q < cnt; q++) {
+      const uint2 ij = work[s_list[q]];
+      const int I = (int)ij.x, J = (int)ij.y;
+      __syncthreads();  // previous candidate is done with sx/sy/sz
+      if (threadIdx.x < kChunk) {
+        const long long j = (long long)J * kChunk + threadIdx.x;
+        const int4 kj = keys[j < n ? j : n - 1];
+        sx[threadIdx.x] = ref_coord(kj.x, f.sx);
+        sy[threadIdx.x] = ref_coord(kj.y, f.sy);
+        sz[threadIdx.x] = ref_coord(kj.z, f.sz);
+      }
+      __syncthreads();
+      const long long i = (long long)I * kChunk + ti;
+      if (i < n) {
+        const int4 ki = keys[i];
+        const double xi = ref_coord(ki.x, f.sx), yi = ref_coord(ki.y, f.sy), zi = ref_coord(ki.z, f.sz);
 #pragma unroll 4
-      for (int t = 0; t < kChunk; t++) best = fmax(best, ref_sq_dist(xi, yi, zi, sx[t], sy[t], sz[t]));
+        for (int t = tj; t < tj + kJ; t++)
+          best = fmax(best, ref_sq_dist(xi, yi, zi, sx[t], sy[t], sz[t]));
+      }
     }
   }
 #pragma unroll

@@ -30,8 +30,8 @@ namespace sc {
 
 // Kernels (mc.cu, diameter.cu, prune.cu, planar.cu).
 __global__ void init_stats(Stats* st);
-template <int U>
-__global__ void pack_bits_v16(const RoiParams*, uint32_t*);
+template <int U, bool BOX>
+__global__ void pack_bits_v16(const RoiParams*, uint32_t*, Stats*);
 __global__ void bits_bbox(const RoiParams*, const uint4*, Stats*);
 __global__ void pack_bits_generic(const RoiParams*, uint32_t*, Stats*);
 __global__ void mc_cells(const RoiParams*, const uint32_t*, const CaseTables*, Stats*, int4*,
@@ -39,32 +39,27 @@ __global__ void mc_cells(const RoiParams*, const uint32_t*, const CaseTables*, S
 __global__ void plane_bins_scan(unsigned int*, unsigned int*, unsigned int*, unsigned long long*,
                                 const Stats*);
 __global__ void scan_all(unsigned int*, unsigned int*, const unsigned int*, unsigned int*,
-                         unsigned int*, unsigned int*, unsigned int*, unsigned int*, long long,
-                         long long, int, long long, Stats*);
+                         unsigned int*, unsigned int*, long long, Stats*, int4*);
 __global__ void scatter_all(const int4*, long long, const Stats*, unsigned int*, int4*,
-                            const unsigned int*, unsigned int*, int2*);
-__global__ void boxes_extremes(const int4*, long long, const RoiParams*, Stats*, int4*);
+                            const unsigned int*, unsigned int*, int2*, unsigned int*);
+__global__ void boxes_extremes(const int4*, long long, const RoiParams*, Stats*, int4*, int4*);
 __global__ void unit_filter(const int4*, const int4*, long long, const RoiParams*, int, Stats*,
-                            unsigned int*);
+                            uint2*, const int4*);
 template <bool PACKED>
-__global__ void diam3d_pass1(const int4*, long long, const RoiParams*, int, int,
-                             const unsigned int*, float*, unsigned int*, Stats*);
-__global__ void diam3d_refine(const int4*, long long, const RoiParams*, const unsigned int*,
-                              const unsigned int*, Stats*);
+__global__ void diam3d_pass1(const int4*, long long, const RoiParams*, int, int, const uint2*,
+                             float*, Stats*);
+__global__ void diam3d_refine(const int4*, long long, const RoiParams*, int, int, const uint2*,
+                              const float*, Stats*);
 __global__ void plane_boxes(const int2*, const unsigned int*, const unsigned int*,
-                            const unsigned int*, const RoiParams*, const Stats*, int4*,
-                            unsigned long long*);
+                            const RoiParams*, const Stats*, int4*, unsigned long long*);
 __global__ void plane_lb(const int2*, const unsigned int*, const unsigned long long*,
                          const RoiParams*, Stats*);
 __global__ void plane_filter(const unsigned int*, const unsigned int*, const unsigned int*,
-                             const unsigned int*, const int4*, const RoiParams*, int, long long,
-                             Stats*, unsigned int*);
-__global__ void plane_pass1(const int2*, const unsigned int*, const unsigned int*,
-                            const unsigned int*, const unsigned int*, const RoiParams*, int, int,
-                            long long, float*, unsigned int*, Stats*);
-__global__ void plane_refine(const int2*, const unsigned int*, const unsigned int*,
-                             const unsigned int*, const unsigned int*, const RoiParams*,
-                             const unsigned int*, Stats*);
+                             const int4*, const RoiParams*, int, long long, Stats*, uint2*);
+__global__ void plane_pass1(const int2*, const unsigned int*, const uint2*, const RoiParams*, int,
+                            int, long long, float*, Stats*);
+__global__ void plane_refine(const int2*, const unsigned int*, const uint2*, const RoiParams*, int,
+                             int, const float*, long long, Stats*);
 __global__ void cloud_diameters(const double*, const double*, const double*, long long, int,
                                 unsigned long long*);
 int launch_binarize(const void*, int, const long long[3], int, int, long long, double, uint8_t*,
@@ -95,8 +90,10 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<bool> g_opt_prune{true}, g_opt_packed{true}, g_opt_graphs{true};
+std::atomic<bool> g_opt_fbox{false};  // bbox accumulated inside the pack (else bits_bbox; measured faster)
 std::atomic<int> g_opt_slots{8};  // pipeline slots used by the batch entries
 std::atomic<long long> g_opt_dcap{2LL << 20};  // default diameter-side vertex capacity
+std::atomic<long long> g_opt_wcap{1LL << 20};  // default 3-D work-list capacity (chunk pairs)
 std::atomic<unsigned long long> g_launches{0};
 
 void set_err(const char* fmt, ...) {
@@ -203,7 +200,8 @@ struct Ctx {
   cudaEvent_t ev[6] = {};
   cudaEvent_t kev[8] = {};      // per-kernel boundaries of the last ROI
   double last_ms[7] = {0, 0, 0, 0, 0, 0, 0};  // pack, mc, prune, pass1, refine, planar, h2d
-  long long cap_floor = 0, dcap_floor = 0;  // raised by overflow re-runs only
+  bool times_pending = false;  // last_ms[0..5] still to be read from kev[]
+  long long cap_floor = 0, dcap_floor = 0, wcap_floor = 0;  // raised by overflow re-runs only
   long long last_diag[6] = {0, 0, 0, 0, 0, 0};
   int occ_pass1 = 1, occ_pass1s = 1, occ_plane = 1, occ_pack = 1, occ_mc = 1;  // blocks/SM
   Stats* d_stats = nullptr;
@@ -213,10 +211,11 @@ struct Ctx {
   long long dcap_sz = 0;      // vertices the diameter-side buffers are sized for (monotonic)
   CaseTables* d_tabs = nullptr;
   DevBuf<uint32_t> bits;
-  DevBuf<int4> keys, keys_sorted, boxes;
-  DevBuf<unsigned int> sort_counts, sort_cursor, work;
+  DevBuf<int4> keys, keys_sorted, boxes, sboxes;  // chunk / super-chunk boxes (lo, hi)
+  DevBuf<unsigned int> sort_counts, sort_cursor;
+  DevBuf<uint2> work;  // surviving 3-D chunk pairs (I, J)
   DevBuf<float> warp_max, plane_umax;
-  DevBuf<unsigned int> cand, plane_cand, plane_umap, plane_cmap, plane_work;
+  DevBuf<uint2> plane_work;  // surviving in-plane chunk pairs {plane, I << 16 | J}
   DevBuf<unsigned int> plane_counts, plane_start, plane_tstart, plane_cstart;
   DevBuf<unsigned int> pbin_counts, pbin_cursor;
   DevBuf<unsigned long long> plane_ext;
@@ -232,7 +231,7 @@ struct Ctx {
     int shard, nshards;
     void* d_sq4;
     long long cap, dcap;
-    bool prune, packed;
+    bool prune, packed, fbox;
     unsigned long long gen;
     cudaGraphExec_t exec;
     unsigned long long launches;
@@ -243,10 +242,10 @@ struct Ctx {
 
   unsigned long long fingerprint() const {
     unsigned long long h = 1469598103934665603ull;
-    const void* ps[] = {bits.p, keys.p, keys_sorted.p, boxes.p, sort_counts.p, sort_cursor.p,
-                        work.p, warp_max.p, plane_umax.p, cand.p, plane_cand.p, plane_umap.p,
+    const void* ps[] = {bits.p, keys.p, keys_sorted.p, boxes.p, sboxes.p, sort_counts.p, sort_cursor.p,
+                        work.p, warp_max.p, plane_umax.p,
                         plane_counts.p, plane_start.p, plane_tstart.p, plane_sorted.p,
-                        plane_cmap.p, plane_work.p, plane_cstart.p, pbin_counts.p, pbin_cursor.p,
+                        plane_work.p, plane_cstart.p, pbin_counts.p, pbin_cursor.p,
                         plane_ext.p, plane_boxes_buf.p};
     for (const void* p : ps) h = (h ^ (unsigned long long)(uintptr_t)p) * 1099511628211ull;
     return h;
@@ -300,13 +299,14 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     if (const char* v = getenv("SC_PASS1")) g_opt_packed = std::strcmp(v, "scalar") != 0;
     if (const char* v = getenv("SC_PRUNE")) g_opt_prune = std::strcmp(v, "0") != 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_plane, plane_pass1, 256, 0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pack, pack_bits_v16<4>, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pack, pack_bits_v16<4, false>, 256, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_mc, mc_cells, 256, 0));
     {
       // Lazy module loading must not happen inside a stream capture: touch
       // every kernel once here.
       cudaFuncAttributes fa;
-      const void* kernels[] = {(const void*)init_stats, (const void*)pack_bits_v16<4>,
+      const void* kernels[] = {(const void*)init_stats, (const void*)pack_bits_v16<4, false>,
+                               (const void*)pack_bits_v16<4, true>,
                                (const void*)mesh_count, (const void*)mesh_emit,
                                (const void*)bits_bbox,
                                (const void*)pack_bits_generic, (const void*)mc_cells,
@@ -352,7 +352,9 @@ double f64_of(unsigned long long bits) {
   return d;
 }
 
-constexpr long long kChunk = 256;  // diameter.cu kChunk: pair unit = chunk x chunk
+constexpr long long kChunk = 128;  // sc_device.cuh kChunk3: pair unit = chunk x chunk
+// The 3-D work list (surviving chunk pairs) starts at g_opt_wcap entries; a
+// ROI whose pruned list is longer re-runs with the exact size.
 constexpr long long kPlaneBinsHost = 256;  // sc_device.cuh kPlaneBins
 
 // Stage events: inside a capture they must be external event nodes so that
@@ -374,20 +376,21 @@ long long vertex_capacity(int64_t nx, int64_t ny, int64_t nz, long long hint) {
 // keys (MC output) hold up to `cap` vertices; the diameter-side arrays (whose
 // tile-pair bookkeeping grows as V^2) hold up to `dcap` <= cap.
 int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, long long dcap,
-                   long long punits) {
+                   long long punits, long long wunits) {
   dcap = c->dcap_sz = std::max(c->dcap_sz, dcap);
   const int W = (int)((nx + 31) / 32);
   CK(c->bits.ensure((size_t)((long long)W * ny * nz)));
   CK(c->keys.ensure((size_t)cap));
   const long long C = (dcap + kChunk - 1) / kChunk;  // chunk pairs: C(C+1)/2
-  CK(c->warp_max.ensure((size_t)(C * (C + 1) / 2)));
-  CK(c->cand.ensure((size_t)(C * (C + 1) / 2)));
-  CK(c->work.ensure((size_t)(C * (C + 1) / 2)));
+  const long long wc = std::min(C * (C + 1) / 2, std::max(g_opt_wcap.load(), wunits));
+  CK(c->warp_max.ensure((size_t)wc));
+  CK(c->work.ensure((size_t)wc));
   CK(c->keys_sorted.ensure((size_t)dcap));
-  CK(c->boxes.ensure((size_t)(2 * ((dcap + 255) / 256))));
+  CK(c->boxes.ensure((size_t)(2 * (C + 1))));
+  CK(c->sboxes.ensure((size_t)(2 * (C / 8 + 1))));
   {
     unsigned int* before = c->sort_counts.p;
-    CK(c->sort_counts.ensure(kSortBins));
+    CK(c->sort_counts.ensure(kSortBins + kSortSupers));
     CK(c->sort_cursor.ensure(kSortBins));
     if (c->sort_counts.p != before)  // histograms are self-cleaning after the first zeroing
       CK(cudaMemset(c->sort_counts.p, 0, sizeof(unsigned int) * c->sort_counts.cap));
@@ -406,16 +409,13 @@ int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, lo
     CK(c->pbin_cursor.ensure((size_t)P * kPlaneBinsHost));
   }
   CK(c->plane_sorted.ensure((size_t)(3 * dcap)));
-  // planar tile pairs: sum over planes of t(t+1)/2, t = ceil(n_p/256); sized
-  // for a 64-tile spread (overflow is detected on the device and re-run).
-  const long long t = (3 * dcap) / 256 + 1;
-  const long long pu = std::max(std::min(t * (t + 1) / 2, t * 64) + P + 1, punits);
+  // surviving in-plane chunk pairs: sized for 16 per chunk (overflow is
+  // detected on the device and re-run with the exact count).
+  const long long t = (3 * dcap) / kPlaneChunk + P + 1;  // chunks over all planes
+  const long long pu = std::max(std::min(t * (t + 1) / 2, t * 16), punits);
   CK(c->plane_umax.ensure((size_t)pu));
-  CK(c->plane_cand.ensure((size_t)pu));
-  CK(c->plane_umap.ensure((size_t)pu));
   CK(c->plane_work.ensure((size_t)pu));
-  CK(c->plane_cmap.ensure((size_t)(t + P + 1)));
-  CK(c->plane_boxes_buf.ensure((size_t)(t + P + 1)));
+  CK(c->plane_boxes_buf.ensure((size_t)t));
   return SC_OK;
 }
 
@@ -430,8 +430,14 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   init_stats<<<1, 256, 0, s>>>(c->d_stats);
   CKL(1);
   CK(record(c, c->kev[0], s));  // kev0..kev1 = the HBM pass alone
-  if (fast) {
-    pack_bits_v16<4><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(rp, c->bits.p);
+  if (fast && g_opt_fbox.load()) {
+    pack_bits_v16<4, true><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(rp, c->bits.p,
+                                                                              c->d_stats);
+    CKL(1);
+    CK(record(c, c->kev[1], s));
+  } else if (fast) {
+    pack_bits_v16<4, false><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(rp, c->bits.p,
+                                                                               c->d_stats);
     CKL(1);
     CK(record(c, c->kev[1], s));
     bits_bbox<<<c->sms * 8, 256, 0, s>>>(rp, reinterpret_cast<const uint4*>(c->bits.p),
@@ -453,7 +459,6 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   const int pgrid = c->sms * std::max(1, g_opt_packed.load() ? c->occ_pass1 : c->occ_pass1s);
   const int plgrid = c->sms * std::max(1, c->occ_plane);
   const long long pucap = (long long)c->plane_umax.cap;
-  const long long pccap = (long long)c->plane_cmap.cap;
   const int prune = g_opt_prune.load() ? 1 : 0;
 
   // Orders (Morton bricks; planes by in-plane brick), chunk boxes + extremes,
@@ -461,51 +466,49 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   plane_bins_scan<<<c->sms * 2, 256, 0, s>>>(c->pbin_counts.p, c->pbin_cursor.p,
                                              c->plane_counts.p, c->plane_ext.p, c->d_stats);
   CKL(1);
-  scan_all<<<2, 1024, 0, s>>>(c->sort_counts.p, c->sort_cursor.p, c->plane_counts.p,
-                              c->plane_start.p, c->plane_tstart.p, c->plane_cstart.p,
-                              c->plane_umap.p, c->plane_cmap.p, pucap, pccap, 256, dcap,
-                              c->d_stats);
+  scan_all<<<kSortSupers + 1, 1024, 0, s>>>(c->sort_counts.p, c->sort_cursor.p,
+                                            c->plane_counts.p, c->plane_start.p,
+                                            c->plane_tstart.p, c->plane_cstart.p, dcap,
+                                            c->d_stats, c->sboxes.p);
   CKL(1);
   scatter_all<<<c->sms * 4, 256, 0, s>>>(c->keys.p, dcap, c->d_stats, c->sort_cursor.p,
                                          c->keys_sorted.p, c->plane_start.p, c->pbin_cursor.p,
-                                         c->plane_sorted.p);
+                                         c->plane_sorted.p, c->sort_counts.p + kSortBins);
   CKL(1);
-  boxes_extremes<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->d_stats, c->boxes.p);
+  boxes_extremes<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->d_stats, c->boxes.p,
+                                            c->sboxes.p);
   CKL(1);
   unit_filter<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, c->boxes.p, dcap, rp, prune,
-                                         c->d_stats, c->work.p);
+                                         c->d_stats, c->work.p, c->sboxes.p);
   CKL(1);
   CK(record(c, c->kev[3], s));
   if (g_opt_packed.load())
     diam3d_pass1<true><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, shard, nshards,
-                                             c->work.p, c->warp_max.p, c->cand.p, c->d_stats);
+                                             c->work.p, c->warp_max.p, c->d_stats);
   else
     diam3d_pass1<false><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, shard, nshards,
-                                              c->work.p, c->warp_max.p, c->cand.p, c->d_stats);
+                                              c->work.p, c->warp_max.p, c->d_stats);
   CKL(1);
   CK(record(c, c->kev[4], s));
-  diam3d_refine<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->work.p, c->cand.p,
-                                           c->d_stats);
+  diam3d_refine<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, shard, nshards,
+                                           c->work.p, c->warp_max.p, c->d_stats);
   CKL(1);
   CK(record(c, c->kev[5], s));
-  plane_boxes<<<c->sms * 2, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_cstart.p,
-                                         c->plane_cmap.p, rp, c->d_stats, c->plane_boxes_buf.p,
-                                         c->plane_ext.p);
+  plane_boxes<<<c->sms * 4, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_cstart.p,
+                                         rp, c->d_stats, c->plane_boxes_buf.p, c->plane_ext.p);
   CKL(1);
   plane_lb<<<c->sms, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_ext.p, rp,
                                   c->d_stats);
   CKL(1);
   plane_filter<<<c->sms * 4, 256, 0, s>>>(c->plane_start.p, c->plane_tstart.p, c->plane_cstart.p,
-                                          c->plane_umap.p, c->plane_boxes_buf.p, rp, prune, pucap,
-                                          c->d_stats, c->plane_work.p);
+                                          c->plane_boxes_buf.p, rp, prune, pucap, c->d_stats,
+                                          c->plane_work.p);
   CKL(1);
-  plane_pass1<<<plgrid, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_tstart.p,
-                                     c->plane_umap.p, c->plane_work.p, rp, shard, nshards, pucap,
-                                     c->plane_umax.p, c->plane_cand.p, c->d_stats);
+  plane_pass1<<<plgrid, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_work.p, rp,
+                                     shard, nshards, pucap, c->plane_umax.p, c->d_stats);
   CKL(1);
-  plane_refine<<<c->sms * 2, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p,
-                                          c->plane_tstart.p, c->plane_umap.p, c->plane_work.p, rp,
-                                          c->plane_cand.p, c->d_stats);
+  plane_refine<<<c->sms * 2, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_work.p,
+                                          rp, shard, nshards, c->plane_umax.p, pucap, c->d_stats);
   CKL(1);
   CK(record(c, c->kev[6], s));
   return SC_OK;
@@ -517,8 +520,12 @@ void fill_out(const Stats& h, const double sp[3], sc_coeffs* out) {
     for (int k = 0; k < kNumCases; k++) t[k] = case_geom().ntri[k];
     return t;
   }();
-  double at[kNumCases];
-  area_table(sp, at);
+  thread_local double at[kNumCases];  // per-case areas, cached per spacing
+  thread_local double at_sp[3] = {-1.0, -1.0, -1.0};
+  if (sp[0] != at_sp[0] || sp[1] != at_sp[1] || sp[2] != at_sp[2]) {
+    area_table(sp, at);
+    at_sp[0] = sp[0]; at_sp[1] = sp[1]; at_sp[2] = sp[2];
+  }
   double area = 0.0;
   long long T = 0, active = 0;
   for (int k = 0; k < kNumCases; k++) {
@@ -560,6 +567,18 @@ int enqueue_with_copies(Ctx* c, bool fast, cudaStream_t s, int shard, int nshard
   return SC_OK;
 }
 
+double wall_ms();
+// Host-side phase accounting of the batch loop (SC_HOST_PROFILE=1 prints it).
+struct HostProf {
+  double sync = 0, finish = 0, start = 0, copy = 0, launch = 0;
+  long long n = 0;
+};
+HostProf g_hprof;
+bool host_prof_on() {
+  static const bool on = std::getenv("SC_HOST_PROFILE") != nullptr;
+  return on;
+}
+
 int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
                const double sp[3], cudaStream_t s, int shard, int nshards, double* d_sq4) {
   RoiParams& h = *c->h_rp;  // the slot's previous ROI has been collected: safe to rewrite
@@ -578,17 +597,22 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   h.f.sx = sp[0];
   h.f.sy = sp[1];
   h.f.sz = sp[2];
+  h.wcap = (long long)std::min(c->work.cap, c->warp_max.cap);
+  const bool hp = host_prof_on();
+  double t0 = hp ? wall_ms() : 0.0;
   CK(cudaMemcpyAsync(c->d_rp, c->h_rp, sizeof(RoiParams), cudaMemcpyHostToDevice, s));
+  if (hp) { const double t1 = wall_ms(); g_hprof.copy += t1 - t0; t0 = t1; }
   const bool fast = nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0;
   if (!g_opt_graphs.load() || s == nullptr)
     return enqueue_with_copies(c, fast, s, shard, nshards, d_sq4);
   const long long cap = (long long)c->keys.cap, dcap = c->dcap_sz;
-  const bool prune = g_opt_prune.load(), packed = g_opt_packed.load();
+  const bool prune = g_opt_prune.load(), packed = g_opt_packed.load(), fbox = g_opt_fbox.load();
   for (auto& g : c->graphs)
     if (g.fast == fast && g.s == s && g.shard == shard && g.nshards == nshards &&
         g.d_sq4 == d_sq4 && g.cap == cap && g.dcap == dcap && g.prune == prune &&
-        g.packed == packed && g.gen == c->gen) {
+        g.packed == packed && g.fbox == fbox && g.gen == c->gen) {
       CK(cudaGraphLaunch(g.exec, s));
+      if (hp) g_hprof.launch += wall_ms() - t0;
       g_launches.fetch_add(g.launches, std::memory_order_relaxed);
       return SC_OK;
     }
@@ -611,7 +635,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
     cudaGraphExecDestroy(c->graphs.front().exec);
     c->graphs.erase(c->graphs.begin());
   }
-  Ctx::GraphEntry g{fast, s, shard, nshards, d_sq4, cap, dcap, prune, packed, c->gen, exec,
+  Ctx::GraphEntry g{fast, s, shard, nshards, d_sq4, cap, dcap, prune, packed, fbox, c->gen, exec,
                     launches};
   c->graphs.push_back(g);
   CK(cudaGraphLaunch(exec, s));
@@ -628,7 +652,7 @@ struct Pending {
   cudaStream_t s;
   int shard, nshards;
   double* d_sq4;
-  long long cap, dcap;
+  long long cap, dcap, wunits;
 };
 
 int start_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
@@ -639,38 +663,50 @@ int start_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
   if (p->cap > 0) {  // re-run after an overflow: exact sizes from now on
     c->cap_floor = std::max(c->cap_floor, p->cap);
     c->dcap_floor = std::max(c->dcap_floor, p->dcap);
+    c->wcap_floor = std::max(c->wcap_floor, p->wunits);
   }
   long long cap = vertex_capacity(nx, ny, nz, c->cap_floor);
   long long dcap = std::min<long long>(cap, std::max<long long>(g_opt_dcap.load(), c->dcap_floor));
   const unsigned long long fp0 = c->fingerprint();
-  int rc = ensure_buffers(c, nx, ny, nz, cap, dcap, punits);
+  int rc = ensure_buffers(c, nx, ny, nz, cap, dcap, punits, c->wcap_floor);
   if (rc) return rc;
   if (c->fingerprint() != fp0) {
     c->gen++;
     c->drop_graphs();
   }
   *p = Pending{d_mask, nx, ny, nz, {sp[0], sp[1], sp[2]}, s, shard, nshards, d_sq4,
-               (long long)c->keys.cap, c->dcap_sz};
+               (long long)c->keys.cap, c->dcap_sz, 0};
   return launch_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4);
 }
 
 // Wait for the ROI started on slot c, re-run it once with exact buffer sizes
 // if the device reported an overflow, and fill `out`.
 int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
+  const bool hp = host_prof_on();
+  const double t0 = hp ? wall_ms() : 0.0;
   CK(cudaStreamSynchronize(p->s));
+  const double t1 = hp ? wall_ms() : 0.0;
+  if (hp) g_hprof.sync += t1 - t0;
+  struct Tail {  // everything after the wait is "finish"
+    bool on; double t;
+    ~Tail() { if (on) { g_hprof.finish += wall_ms() - t; g_hprof.n++; } }
+  } tail{hp, t1};
   const long long V = (long long)c->h_stats->n_vert;
-  const long long PU = (long long)c->h_stats->plane_units;
-  if (V > p->dcap || PU > (long long)c->plane_umax.cap) {
-    // rare: more vertices / planar tiles than reserved -> exact re-run
+  const long long PU = (long long)c->h_stats->n_pwork;
+  const long long WU = (long long)c->h_stats->n_work;
+  if (V > p->dcap || PU > (long long)c->plane_umax.cap || WU > c->h_rp->wcap) {
+    // rare: more vertices / planar tiles / 3-D units than reserved -> exact re-run
     Pending q = *p;
     q.cap = std::max(p->cap, V);
     q.dcap = std::max(p->dcap, V);
+    q.wunits = WU;
     int rc = start_roi(c, q.d_mask, q.nx, q.ny, q.nz, q.sp, q.s, q.shard, q.nshards, q.d_sq4, PU,
                        &q);
     if (rc) return rc;
     CK(cudaStreamSynchronize(q.s));
     if ((long long)c->h_stats->n_vert > q.dcap ||
-        (long long)c->h_stats->plane_units > (long long)c->plane_umax.cap) {
+        (long long)c->h_stats->n_pwork > (long long)c->plane_umax.cap ||
+        (long long)c->h_stats->n_work > c->h_rp->wcap) {
       set_err("vertex buffer overflow");
       return SC_ERR_NOMEM;
     }
@@ -680,12 +716,7 @@ int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
     return SC_ERR_EMPTY_ROI;
   }
   fill_out(*c->h_stats, p->sp, out);
-  c->last_ms[0] = ev_ms(c->kev[0], c->kev[1]);
-  c->last_ms[1] = ev_ms(c->kev[1], c->kev[2]);
-  c->last_ms[2] = ev_ms(c->kev[2], c->kev[3]);
-  c->last_ms[3] = ev_ms(c->kev[3], c->kev[4]);
-  c->last_ms[4] = ev_ms(c->kev[4], c->kev[5]);
-  c->last_ms[5] = ev_ms(c->kev[5], c->kev[6]);
+  c->times_pending = true;  // per-stage times: read from kev[] on demand
   c->last_ms[6] = 0.0;
   {
     const Stats& h = *c->h_stats;
@@ -741,6 +772,32 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
     CK(cudaEventRecord(cs[0]->ev[4], user));
     for (int k = 0; k < nslots; k++) CK(cudaStreamWaitEvent(cs[k]->stream, cs[0]->ev[4], 0));
   }
+  // Size every slot for the largest ROI of the batch up front: growing a
+  // buffer mid-batch would synchronise the device and drop the slot's graphs.
+  {
+    int64_t mx = 0, my = 0, mz = 0, mb = 0;
+    for (int64_t i = 0; i < count; i++) {
+      const int64_t nx = dims[3 * i], ny = dims[3 * i + 1], nz = dims[3 * i + 2];
+      if (nx <= 0 || ny <= 0 || nz <= 0) continue;
+      mx = std::max(mx, nx); my = std::max(my, ny); mz = std::max(mz, nz);
+      mb = std::max(mb, nx * ny * nz);
+    }
+    if (mb > 0)
+      for (int k = 0; k < nslots; k++) {
+        Ctx* c = cs[k];
+        const unsigned long long fp0 = c->fingerprint();
+        const long long cap = vertex_capacity(mx, my, mz, c->cap_floor);
+        const long long dcap =
+            std::min<long long>(cap, std::max<long long>(g_opt_dcap.load(), c->dcap_floor));
+        int rc = ensure_buffers(c, mx, my, mz, cap, dcap, 0, c->wcap_floor);
+        if (rc) return rc;
+        if (c->fingerprint() != fp0) {
+          c->gen++;
+          c->drop_graphs();
+        }
+        if (host) CK(c->mask_stage.ensure((size_t)mb));
+      }
+  }
   Pending pend[kSlots] = {};
   int64_t idx[kSlots];
   double t_start[kSlots];
@@ -783,7 +840,9 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
       dm = c->mask_stage.p;
     }
     pend[k] = Pending{};
+    const double ts = host_prof_on() ? wall_ms() : 0.0;
     rc = start_roi(c, dm, nx, ny, nz, sp, s, 0, 1, nullptr, 0, &pend[k]);
+    if (host_prof_on()) g_hprof.start += wall_ms() - ts;
     if (rc) { note(rc); continue; }
     idx[k] = i;
   }
@@ -795,6 +854,15 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
     }
   }
   if (first) g_err = first_err;
+  if (host_prof_on() && g_hprof.n) {
+    const double n = (double)g_hprof.n;
+    std::fprintf(stderr,
+                 "[sc host] %lld ROIs: per ROI sync-wait %.1f us, finish %.1f us, start %.1f us "
+                 "(RoiParams copy %.1f us, graph launch %.1f us)\n",
+                 g_hprof.n, 1e3 * g_hprof.sync / n, 1e3 * g_hprof.finish / n,
+                 1e3 * g_hprof.start / n, 1e3 * g_hprof.copy / n, 1e3 * g_hprof.launch / n);
+    g_hprof = HostProf{};
+  }
   return first;
 }
 
@@ -843,14 +911,13 @@ int run_mesh(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
     h.f.cx2 = h.f.cy2 = h.f.cz2 = 0;
     h.f.hx = (float)(0.5 * sp[0]); h.f.hy = (float)(0.5 * sp[1]); h.f.hz = (float)(0.5 * sp[2]);
     h.f.sx = sp[0]; h.f.sy = sp[1]; h.f.sz = sp[2];
+    h.wcap = 0;
     CK(cudaMemcpyAsync(c->d_rp, c->h_rp, sizeof(RoiParams), cudaMemcpyHostToDevice, s));
     init_stats<<<1, 256, 0, s>>>(c->d_stats);
     CKL(1);
     if (nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0) {
-      pack_bits_v16<4><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(c->d_rp, c->bits.p);
-      CKL(1);
-      bits_bbox<<<c->sms * 8, 256, 0, s>>>(c->d_rp, reinterpret_cast<const uint4*>(c->bits.p),
-                                           c->d_stats);
+      pack_bits_v16<4, true><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(
+          c->d_rp, c->bits.p, c->d_stats);
       CKL(1);
     } else {
       pack_bits_generic<<<c->sms * 8, 256, 0, s>>>(c->d_rp, c->bits.p, c->d_stats);
@@ -1175,6 +1242,10 @@ int sc_last_kernel_times(int device, double* ms, int n) {
   int rc = get_ctx(device, &c);
   if (rc) return -rc;
   std::lock_guard<std::mutex> lk(c->mu);
+  if (c->times_pending) {
+    for (int i = 0; i < 6; i++) c->last_ms[i] = ev_ms(c->kev[i], c->kev[i + 1]);
+    c->times_pending = false;
+  }
   int m = n < 7 ? n : 7;
   for (int i = 0; i < m; i++) ms[i] = c->last_ms[i];
   return m;
@@ -1199,6 +1270,8 @@ int sc_set_option(const char* name, int value) {
   else if (std::strcmp(name, "graphs") == 0) g_opt_graphs = value != 0;
   else if (std::strcmp(name, "slots") == 0) g_opt_slots = value;
   else if (std::strcmp(name, "dcap") == 0) g_opt_dcap = std::max(256, value);
+  else if (std::strcmp(name, "wcap") == 0) g_opt_wcap = std::max(1, value);
+  else if (std::strcmp(name, "fused_bbox") == 0) g_opt_fbox = value != 0;
   else { set_err("unknown option %s", name); return SC_ERR_INPUT; }
   return SC_OK;
 }

@@ -77,11 +77,17 @@ struct BoxAcc {
 // L2-resident bit volume (bits_bbox), so this loop carries no bookkeeping.
 // Grid = resident blocks.  tools/microbench/pack_bench.cu: 5.1 TB/s on a 157 MB
 // mask = 88% of the 1 GiB streaming-read rate of the same GPU.
-template <int U>
+//
+// BOX: also accumulate the occupied bbox in registers (32-bit index math, only
+// for nonzero words) and flush it once per warp -- replaces bits_bbox.
+template <int U, bool BOX>
 __global__ void __launch_bounds__(256) pack_bits_v16(const RoiParams* __restrict__ rp,
-                                                     uint32_t* __restrict__ bits) {
+                                                     uint32_t* __restrict__ bits,
+                                                     Stats* __restrict__ st) {
   const uint4* __restrict__ mask = reinterpret_cast<const uint4*>(rp->mask);
   const long long n_chunks = rp->n_chunks;
+  const unsigned int W = (unsigned int)rp->W, ny = (unsigned int)rp->ny;
+  BoxAcc box;
   const long long step = (long long)gridDim.x * blockDim.x * U;
   for (long long base = (long long)blockIdx.x * blockDim.x * U; base < n_chunks; base += step) {
     uint4 v[U];
@@ -96,9 +102,20 @@ __global__ void __launch_bounds__(256) pack_bits_v16(const RoiParams* __restrict
       const uint32_t b16 = nib4(v[k].x) | (nib4(v[k].y) << 4) | (nib4(v[k].z) << 8) |
                            (nib4(v[k].w) << 12);
       const uint32_t word = b16 | (__shfl_down_sync(kFull, b16, 1) << 16);
-      if (!(threadIdx.x & 1) && g < n_chunks) bits[g >> 1] = word;
+      if (!(threadIdx.x & 1) && g < n_chunks) {
+        bits[g >> 1] = word;
+        if (BOX && word) {
+          const unsigned int wi = (unsigned int)(g >> 1), row = wi / W, col = wi - row * W;
+          const unsigned int z = row / ny, y = row - z * ny;
+          box.x0 = min(box.x0, (int)(32 * col) + __ffs(word) - 1);
+          box.x1 = max(box.x1, (int)(32 * col) + 31 - __clz(word));
+          box.y0 = min(box.y0, (int)y); box.y1 = max(box.y1, (int)y);
+          box.z0 = min(box.z0, (int)z); box.z1 = max(box.z1, (int)z);
+        }
+      }
     }
   }
+  if (BOX) box.flush(st);
 }
 
 // Occupied bbox from the bit volume (L2-resident right after the pack): only
@@ -199,7 +216,7 @@ __global__ void __launch_bounds__(256) mc_cells(const RoiParams* __restrict__ rp
                                                 unsigned int* __restrict__ pbin_counts) {
   __shared__ unsigned int s_hist[kNumCases];
   __shared__ int4 s_tn[kNumCases];
-  __shared__ unsigned int s_bin[kSortBins];
+  __shared__ unsigned int s_sup[kSortSupers];
   const int ny = (int)rp->ny, nz = (int)rp->nz, W = rp->W;
   int bb[6];
 #pragma unroll
@@ -211,7 +228,7 @@ __global__ void __launch_bounds__(256) mc_cells(const RoiParams* __restrict__ rp
     s_hist[i] = 0;
     s_tn[i] = tabs->tn[i];
   }
-  for (int i = threadIdx.x; i < kSortBins; i += blockDim.x) s_bin[i] = 0;
+  for (int i = threadIdx.x; i < kSortSupers; i += blockDim.x) s_sup[i] = 0;
   __syncthreads();
 
   const int xmin = bb[0], ymin = bb[1], zmin = bb[2];
@@ -294,7 +311,9 @@ __global__ void __launch_bounds__(256) mc_cells(const RoiParams* __restrict__ rp
             if (o < cap) vkeys[o] = make_int4(X, Y, Z, 0);
             o++;
             if (pbin_counts) {  // NULL on the mesh-export path (no diameter stage)
-              atomicAdd(&s_bin[brick_bin(X, Y, Z, bb, bshift)], 1u);
+              const unsigned int bin = brick_bin(X, Y, Z, bb, bshift);
+              atomicAdd(&sort_counts[bin], 1u);
+              atomicAdd(&s_sup[bin >> kSortSliceBits], 1u);
               int id[3];
               unsigned int pbin[3];
               plane_ids(X, Y, Z, ps, id);
@@ -329,10 +348,11 @@ __global__ void __launch_bounds__(256) mc_cells(const RoiParams* __restrict__ rp
   for (int i = threadIdx.x; i < kNumCases; i += blockDim.x)
     if (s_hist[i]) atomicAdd(&st->hist[i], (unsigned long long)s_hist[i]);
   if (sort_counts)
-    for (int i = threadIdx.x; i < kSortBins; i += blockDim.x)
-      if (s_bin[i]) atomicAdd(&sort_counts[i], s_bin[i]);
+    for (int i = threadIdx.x; i < kSortSupers; i += blockDim.x)
+      if (s_sup[i]) atomicAdd(&sort_counts[kSortBins + i], s_sup[i]);
 }
 
-template __global__ void pack_bits_v16<4>(const RoiParams*, uint32_t*);
+template __global__ void pack_bits_v16<4, false>(const RoiParams*, uint32_t*, Stats*);
+template __global__ void pack_bits_v16<4, true>(const RoiParams*, uint32_t*, Stats*);
 
 }  // namespace sc

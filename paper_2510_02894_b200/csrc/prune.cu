@@ -20,7 +20,9 @@
 
 namespace sc {
 
-constexpr int kChunkV = 256;  // == diameter.cu kChunk
+constexpr int kChunkV = kChunk3;
+constexpr int kPerLane = kChunkV / 32;
+constexpr int kSuper = 8;  // super-chunk = 8 chunks (1024 vertices): first level of unit_filter
 constexpr int kNDir = 13;
 
 __device__ __forceinline__ long long n_verts(const Stats* st, long long cap) {
@@ -34,21 +36,19 @@ __device__ __forceinline__ unsigned int plane_tiles(unsigned int np, int pt) {
   return t * (t + 1) / 2;
 }
 
-// Two blocks of 1024 threads.  Block 0: exclusive scan of the 4096 brick
-// counts -> sort cursor (and zero the counts for the next ROI).  Block 1:
-// plane populations (plane_bins_scan) -> start; in-plane tile pairs -> tstart
-// and the unit -> plane map; in-plane 256-entry chunks -> cstart and the
-// chunk -> plane map.
+// kSortSupers + 1 blocks of 1024 threads.  Blocks [0, kSortSupers): one
+// 1024-bin slice each of the exclusive scan of the brick counts -> sort cursor
+// (and zero the counts for the next ROI), plus empty super-chunk boxes.  Last
+// block: plane populations (plane_bins_scan) -> start; 256-entry tile pairs
+// per plane -> tstart; 128-entry chunks per plane -> cstart.
 __global__ void __launch_bounds__(1024) scan_all(unsigned int* __restrict__ sort_counts,
                                                  unsigned int* __restrict__ sort_cursor,
                                                  const unsigned int* __restrict__ plane_counts,
                                                  unsigned int* __restrict__ start,
                                                  unsigned int* __restrict__ tstart,
                                                  unsigned int* __restrict__ cstart,
-                                                 unsigned int* __restrict__ umap,
-                                                 unsigned int* __restrict__ cmap, long long ucap,
-                                                 long long ccap, int plane_tile, long long dcap,
-                                                 Stats* __restrict__ st) {
+                                                 long long dcap, Stats* __restrict__ st,
+                                                 int4* __restrict__ sboxes) {
   int bb[6];
 #pragma unroll
   for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
@@ -56,29 +56,39 @@ __global__ void __launch_bounds__(1024) scan_all(unsigned int* __restrict__ sort
   // More vertices than the diameter-side buffers hold: every later kernel
   // stands down (positions from the full histograms would overflow) and the
   // host re-runs the ROI with exact sizes.
+  const bool brick_block = blockIdx.x < kSortSupers;
   if ((long long)st->n_vert > dcap) {
     if (blockIdx.x == 0 && threadIdx.x == 0) st->ovf = 1u;
-    if (blockIdx.x == 0) {  // still leave the brick histogram zeroed for the next ROI
-      for (int i = threadIdx.x; i < kSortBins; i += blockDim.x) sort_counts[i] = 0u;
-    }
+    if (brick_block)  // still leave the brick histogram zeroed for the next ROI
+      sort_counts[(blockIdx.x << kSortSliceBits) + threadIdx.x] = 0u;
     return;
   }
-  if (blockIdx.x == 0) {
-    constexpr int per = kSortBins / 1024;
-    unsigned int v[per], sum = 0;
-#pragma unroll
-    for (int k = 0; k < per; k++) {
-      v[k] = sort_counts[threadIdx.x * per + k];
-      sum += v[k];
+  if (brick_block) {
+    {  // empty super-chunk boxes, filled by boxes_extremes with atomics
+      const long long n = (long long)st->n_vert;
+      const long long CT = ((n + kChunkV - 1) / kChunkV + kSuper - 1) / kSuper;
+      for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < CT;
+           t += (long long)gridDim.x * blockDim.x) {
+        sboxes[2 * t] = make_int4(INT_MAX, INT_MAX, INT_MAX, 0);
+        sboxes[2 * t + 1] = make_int4(INT_MIN, INT_MIN, INT_MIN, 0);
+      }
     }
+    // Slice b = fine bins [1024 b, 1024 b + 1024): base = super-bin prefix.
+    __shared__ unsigned int s_base[32];
+    const unsigned int* sup = sort_counts + kSortBins;
+    unsigned int pre = (threadIdx.x < blockIdx.x) ? sup[threadIdx.x] : 0u;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    if ((threadIdx.x & 31) == 0) s_base[threadIdx.x >> 5] = pre;
+    __syncthreads();
+    unsigned int base = 0;
+    for (int w = 0; w < kSortSupers / 32; w++) base += s_base[w];
+    __syncthreads();  // s_base is reused by the block scan below
+    const int i = (blockIdx.x << kSortSliceBits) + threadIdx.x;
+    const unsigned int v = sort_counts[i];
     unsigned int total;
-    unsigned int run = block_exscan_1024(sum, &total);
-#pragma unroll
-    for (int k = 0; k < per; k++) {
-      sort_cursor[threadIdx.x * per + k] = run;
-      run += v[k];
-      sort_counts[threadIdx.x * per + k] = 0u;
-    }
+    sort_cursor[i] = base + block_exscan_1024(v, &total);
+    sort_counts[i] = 0u;
     return;
   }
   const PlaneSpace ps = plane_space(bb);
@@ -89,8 +99,8 @@ __global__ void __launch_bounds__(1024) scan_all(unsigned int* __restrict__ sort
   for (int i = b; i < e; i++) {
     const unsigned int v = plane_counts[i];
     s1 += v;
-    s2 += plane_tiles(v, plane_tile);
-    s3 += v >= 2 ? (v + plane_tile - 1) / plane_tile : 0u;
+    s2 += plane_tiles(v, kPlaneTile);
+    s3 += v >= 2 ? (v + kPlaneChunk - 1) / kPlaneChunk : 0u;
   }
   unsigned int t1, t2, t3;
   unsigned int r1 = block_exscan_1024(s1, &t1);
@@ -98,18 +108,12 @@ __global__ void __launch_bounds__(1024) scan_all(unsigned int* __restrict__ sort
   unsigned int r3 = block_exscan_1024(s3, &t3);
   for (int i = b; i < e; i++) {
     const unsigned int v = plane_counts[i];
-    const unsigned int nt = plane_tiles(v, plane_tile);
-    const unsigned int nc = v >= 2 ? (v + plane_tile - 1) / plane_tile : 0u;
     start[i] = r1;
     tstart[i] = r2;
     cstart[i] = r3;
-    if ((long long)t2 <= ucap)
-      for (unsigned int u = 0; u < nt; u++) umap[r2 + u] = (unsigned int)i;
-    if ((long long)t3 <= ccap)
-      for (unsigned int u = 0; u < nc; u++) cmap[r3 + u] = (unsigned int)i;
     r1 += v;
-    r2 += nt;
-    r3 += nc;
+    r2 += plane_tiles(v, kPlaneTile);
+    r3 += v >= 2 ? (v + kPlaneChunk - 1) / kPlaneChunk : 0u;
   }
   if (threadIdx.x == 0) {
     start[P] = t1;
@@ -128,7 +132,10 @@ __global__ void scatter_all(const int4* __restrict__ keys, long long cap,
                             int4* __restrict__ keys_sorted,
                             const unsigned int* __restrict__ plane_start,
                             unsigned int* __restrict__ pbin_cursor,
-                            int2* __restrict__ plane_sorted) {
+                            int2* __restrict__ plane_sorted,
+                            unsigned int* __restrict__ sort_supers) {
+  // scan_all has consumed the super-bin counts: leave them zeroed for the next ROI.
+  if (blockIdx.x == 0) sort_supers[threadIdx.x] = 0u;
   if (st->ovf) return;  // re-run pending (scan_all)
   const long long n = n_verts(st, cap);
   int bb[6];
@@ -172,19 +179,9 @@ __constant__ int c_dir[kNDir][3] = {{1, 0, 0},  {0, 1, 0},  {0, 0, 1},  {1, 1, 0
                                     {1, 0, 1},  {1, 0, -1}, {0, 1, 1},  {0, 1, -1}, {1, 1, 1},
                                     {1, 1, -1}, {1, -1, 1}, {-1, 1, 1}};
 
-__device__ __forceinline__ unsigned long long pack_ext(float v, unsigned int idx) {
-  unsigned int b = __float_as_uint(v);
-  b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-  return ((unsigned long long)b << 32) | idx;
-}
-
-__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long b) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const unsigned long long t = __shfl_xor_sync(0xffffffffu, b, o);
-    b = t > b ? t : b;
-  }
-  return b;
+__device__ __forceinline__ unsigned int order_key(float v) {  // order-preserving, never 0 for finite v
+  const unsigned int b = __float_as_uint(v);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
 // One warp per 256-chunk of the sorted keys: its integer box (boxes[2c] = lo,
@@ -192,7 +189,8 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long b)
 __global__ void __launch_bounds__(256) boxes_extremes(const int4* __restrict__ keys,
                                                       long long cap, const RoiParams* __restrict__ rp,
                                                       Stats* __restrict__ st,
-                                                      int4* __restrict__ boxes) {
+                                                      int4* __restrict__ boxes,
+                                                      int4* __restrict__ sboxes) {
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   __shared__ unsigned long long s_ext[2 * kNDir];
@@ -205,10 +203,10 @@ __global__ void __launch_bounds__(256) boxes_extremes(const int4* __restrict__ k
   for (long long c = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < chunks;
        c += warps) {
     int lx = INT_MAX, ly = INT_MAX, lz = INT_MAX, hx = INT_MIN, hy = INT_MIN, hz = INT_MIN;
-    float px[8], py[8], pz[8];
-    unsigned int idx[8];
+    float px[kPerLane], py[kPerLane], pz[kPerLane];
+    unsigned int idx[kPerLane];
 #pragma unroll
-    for (int t = 0; t < 8; t++) {
+    for (int t = 0; t < kPerLane; t++) {
       long long v = c * kChunkV + t * 32 + lane;
       if (v >= n) v = n - 1;  // pass 1 clamps the same way
       const int4 k = keys[v];
@@ -223,21 +221,31 @@ __global__ void __launch_bounds__(256) boxes_extremes(const int4* __restrict__ k
     if (lane == 0) {
       boxes[2 * c] = make_int4(lx, ly, lz, 0);
       boxes[2 * c + 1] = make_int4(hx, hy, hz, 0);
+      int* slo = reinterpret_cast<int*>(sboxes + 2 * (c / kSuper));
+      int* shi = reinterpret_cast<int*>(sboxes + 2 * (c / kSuper) + 1);
+      atomicMin(slo, lx); atomicMin(slo + 1, ly); atomicMin(slo + 2, lz);
+      atomicMax(shi, hx); atomicMax(shi + 1, hy); atomicMax(shi + 2, hz);
     }
     for (int d = 0; d < kNDir; d++) {
-      unsigned long long hi = 0ull, lo = 0ull;
+      // Per lane: best order-preserving key (and its vertex) of +p and -p;
+      // warp: hardware u32 max-reduce, the owning lane found by ballot.
+      unsigned int khi = 0u, klo = 0u, ihi = 0u, ilo = 0u;
 #pragma unroll
-      for (int t = 0; t < 8; t++) {
+      for (int t = 0; t < kPerLane; t++) {
         const float p = c_dir[d][0] * px[t] + c_dir[d][1] * py[t] + c_dir[d][2] * pz[t];
-        const unsigned long long a = pack_ext(p, idx[t]), b = pack_ext(-p, idx[t]);
-        hi = a > hi ? a : hi;
-        lo = b > lo ? b : lo;
+        const unsigned int a = order_key(p), b = order_key(-p);
+        if (a > khi) { khi = a; ihi = idx[t]; }
+        if (b > klo) { klo = b; ilo = idx[t]; }
       }
-      hi = warp_max_u64(hi);
-      lo = warp_max_u64(lo);
+      const unsigned int mhi = __reduce_max_sync(0xffffffffu, khi);
+      const unsigned int mlo = __reduce_max_sync(0xffffffffu, klo);
+      const int shi = __ffs(__ballot_sync(0xffffffffu, khi == mhi)) - 1;
+      const int slo = __ffs(__ballot_sync(0xffffffffu, klo == mlo)) - 1;
+      ihi = __shfl_sync(0xffffffffu, ihi, shi);
+      ilo = __shfl_sync(0xffffffffu, ilo, slo);
       if (lane == 0) {
-        atomicMax(&s_ext[2 * d], hi);
-        atomicMax(&s_ext[2 * d + 1], lo);
+        atomicMax(&s_ext[2 * d], ((unsigned long long)mhi << 32) | ihi);
+        atomicMax(&s_ext[2 * d + 1], ((unsigned long long)mlo << 32) | ilo);
       }
     }
   }
@@ -259,7 +267,8 @@ __device__ __forceinline__ double axis_reach(int loA, int hiA, int loB, int hiB,
 __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys,
                                                    const int4* __restrict__ boxes, long long cap,
                                                    const RoiParams* __restrict__ rp, int prune, Stats* __restrict__ st,
-                                                   unsigned int* __restrict__ work) {
+                                                   uint2* __restrict__ work,
+                                                   const int4* __restrict__ sboxes) {
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   __shared__ double px[2 * kNDir], py[2 * kNDir], pz[2 * kNDir];
@@ -290,34 +299,55 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
     atomic_max_pos_f64(&st->sq[0], lb);
   }
   const double thr = lb * (1.0 - 1e-9);  // UB and LB are exact up to fp64 rounding
+  // Two levels: a pair of super-chunks (8 chunks = 1024 vertices, boxes from
+  // boxes_extremes) is tested first; only if it can reach LB are its (up to
+  // 64) chunk pairs tested and listed -- row by row, so consecutive units of
+  // a pass-1 warp usually share the I chunk.
   const long long C = (n + kChunkV - 1) / kChunkV;
-  const long long units = C * (C + 1) / 2;
-  const double hx = 0.5 * f.sx, hy = 0.5 * f.sy, hz = 0.5 * f.sz;
+  const long long CT = (C + kSuper - 1) / kSuper;
+  const long long units = CT * (CT + 1) / 2;
+  const double h3[3] = {0.5 * f.sx, 0.5 * f.sy, 0.5 * f.sz};
+  const long long wcap = rp->wcap;
   const int lane = threadIdx.x & 31;
+  auto reach = [&](int4 alo, int4 ahi, int4 blo, int4 bhi) {
+    return axis_reach(alo.x, ahi.x, blo.x, bhi.x, h3[0]) +
+           axis_reach(alo.y, ahi.y, blo.y, bhi.y, h3[1]) +
+           axis_reach(alo.z, ahi.z, blo.z, bhi.z, h3[2]);
+  };
   for (long long base = (long long)blockIdx.x * blockDim.x; base < units;
        base += (long long)gridDim.x * blockDim.x) {
     const long long u = base + threadIdx.x;
-    bool keep = false;
+    bool coarse = false;
+    int IT = 0, JT = 0;
     if (u < units) {
-      if (!prune) {
-        keep = true;
-      } else {
-        int I, J;
-        tile_pair(u, C, I, J);
-        const int4 ilo = boxes[2 * I], ihi = boxes[2 * I + 1];
-        const int4 jlo = boxes[2 * J], jhi = boxes[2 * J + 1];
-        const double ub = axis_reach(ilo.x, ihi.x, jlo.x, jhi.x, hx) +
-                          axis_reach(ilo.y, ihi.y, jlo.y, jhi.y, hy) +
-                          axis_reach(ilo.z, ihi.z, jlo.z, jhi.z, hz);
-        keep = ub >= thr;
+      tile_pair(u, CT, IT, JT);
+      coarse = !prune || reach(sboxes[2 * IT], sboxes[2 * IT + 1], sboxes[2 * JT],
+                               sboxes[2 * JT + 1]) >= thr;
+    }
+    // The whole warp expands each surviving super pair: lane -> two of its
+    // 64 chunk pairs (rows 0-3, then 4-7), so the chain of dependent loads
+    // per warp is one per survivor rather than 64.
+    unsigned int cm = __ballot_sync(0xffffffffu, coarse);
+    while (cm) {
+      const int src = __ffs(cm) - 1;
+      cm &= cm - 1;
+      const int it = __shfl_sync(0xffffffffu, IT, src), jt = __shfl_sync(0xffffffffu, JT, src);
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int r = h * 32 + lane;
+        const int i = kSuper * it + (r >> 3), j = kSuper * jt + (r & 7);
+        bool keep = i < C && j < C && j >= i;
+        if (keep && prune)
+          keep = reach(boxes[2 * i], boxes[2 * i + 1], boxes[2 * j], boxes[2 * j + 1]) >= thr;
+        const unsigned int mask = __ballot_sync(0xffffffffu, keep);
+        if (!mask) continue;
+        unsigned long long pos = 0;
+        if (lane == 0) pos = atomicAdd(&st->n_work, (unsigned long long)__popc(mask));
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        const long long o = (long long)pos + __popc(mask & ((1u << lane) - 1));
+        if (keep && o < wcap) work[o] = make_uint2((unsigned int)i, (unsigned int)j);
       }
     }
-    const unsigned int mask = __ballot_sync(0xffffffffu, keep);
-    if (!mask) continue;
-    unsigned long long pos = 0;
-    if (lane == 0) pos = atomicAdd(&st->n_work, (unsigned long long)__popc(mask));
-    pos = __shfl_sync(0xffffffffu, pos, 0);
-    if (keep) work[pos + __popc(mask & ((1u << lane) - 1))] = (unsigned int)u;
   }
 }
 

@@ -59,6 +59,7 @@ struct RoiParams {
   int W;               // 32-bit words per bit-volume row
   int pad;
   Frame f;             // cx2..cz2 are filled on the device from the bbox
+  long long wcap;      // capacity of the 3-D work list (overflow -> exact re-run)
 };
 
 // Planar key space: [0, cnt[0]) XY planes keyed by Z2, then cnt[1] XZ planes
@@ -70,22 +71,31 @@ struct PlaneSpace {
 
 // ---- vertex binning shared by the MC emission, the sort and the planar pass ----
 
-// Morton brick order: 4 bits per axis (4096 bins) over the occupied bbox.
-constexpr int kSortBits = 12;
+// Morton brick order: 6 bits per axis (2^18 bins) over the occupied bbox.
+// The fine histogram lives in global memory (one atomic per vertex); the top
+// 8 bits of the Morton code form 256 super-bins counted in shared memory, so
+// every 1024-bin slice of the exclusive scan can start from the super-bin
+// prefix without any inter-block communication.
+constexpr int kSortBits = 18;
 constexpr int kSortBins = 1 << kSortBits;
+constexpr int kSortSliceBits = 10;                            // fine bins per scan block
+constexpr int kSortSupers = kSortBins >> kSortSliceBits;      // 256 super-bins
+constexpr int kChunk3 = 128;  // vertices per 3-D diameter chunk (pair unit = chunk x chunk)
 
-__device__ __forceinline__ unsigned int spread4(unsigned int v) {  // 4 bits -> every 3rd bit
-  v &= 15u;
-  v = (v | (v << 4)) & 0x0C3u;
-  v = (v | (v << 2)) & 0x249u;
+__device__ __forceinline__ unsigned int spread_bits(unsigned int v) {  // <= 10 bits -> every 3rd bit
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x30000ffu;
+  v = (v | (v << 8)) & 0x300f00fu;
+  v = (v | (v << 4)) & 0x30c30c3u;
+  v = (v | (v << 2)) & 0x9249249u;
   return v;
 }
 
-// Brick shift (doubled units) so the bbox spans <= 16 bricks per axis.
+// Brick shift (doubled units) so the bbox spans <= 64 bricks per axis.
 __device__ __forceinline__ int brick_shift(const int* bb) {
   const int ext = max(bb[3] - bb[0], max(bb[4] - bb[1], bb[5] - bb[2])) * 2 + 3;
-  int s = 4;
-  while ((ext >> s) >= 16) s++;
+  int s = 0;
+  while ((ext >> s) >= 64) s++;
   return s;
 }
 
@@ -93,7 +103,7 @@ __device__ __forceinline__ unsigned int brick_bin(int X, int Y, int Z, const int
   const unsigned int bx = (unsigned int)(X - (2 * bb[0] - 1)) >> s;
   const unsigned int by = (unsigned int)(Y - (2 * bb[1] - 1)) >> s;
   const unsigned int bz = (unsigned int)(Z - (2 * bb[2] - 1)) >> s;
-  return spread4(bx) | (spread4(by) << 1) | (spread4(bz) << 2);
+  return spread_bits(bx) | (spread_bits(by) << 1) | (spread_bits(bz) << 2);
 }
 
 __device__ __forceinline__ PlaneSpace plane_space(const int* bb) {
@@ -116,6 +126,8 @@ __device__ __forceinline__ void plane_ids(int X, int Y, int Z, const PlaneSpace&
 // its two in-plane doubled coordinates (256 bins per plane), so every plane's
 // vertex list comes out spatially compact (enables exact planar pruning).
 constexpr int kPlaneBins = 256;
+constexpr int kPlaneTile = 256;   // in-plane tile edge (first level of plane_filter)
+constexpr int kPlaneChunk = 128;  // in-plane chunk edge (planar pair unit)
 
 __device__ __forceinline__ int axis_shift(int lo, int hi) {  // voxel bbox [lo, hi]
   const int ext = 2 * (hi - lo) + 3;

@@ -234,7 +234,8 @@ def test_repeat_calls_deterministic(sc, cuda_device):
 
 
 def test_pruning_and_pass1_variants_identical(sc, golden, golden_arrays, cuda_device):
-    """Work pruning and the FFMA/FFMA2 pass-1 variants never change a result."""
+    """Work pruning, the FFMA/FFMA2 pass-1 variants, graph replay and the
+    pack-fused bbox never change a result."""
     from paper_2510_02894_b200 import _native, synth
 
     cases = [(golden_arrays[c["mask_key"]], c["spacing"]) for c in golden["cases"]]
@@ -242,7 +243,7 @@ def test_pruning_and_pass1_variants_identical(sc, golden, golden_arrays, cuda_de
     cases.append((synth.kits_like(tumor_mm=60.0), (0.8, 0.8, 1.0)))
     base = [sc.calculate_coefficients(a, sp).to_dict() for a, sp in cases]
     try:
-        for opt, val in (("prune", 0), ("pass1_packed", 0), ("graphs", 0)):
+        for opt, val in (("prune", 0), ("pass1_packed", 0), ("graphs", 0), ("fused_bbox", 0)):
             _native.set_option(opt, val)
             for (a, sp), want in zip(cases, base):
                 assert sc.calculate_coefficients(a, sp).to_dict() == want, opt
@@ -251,6 +252,7 @@ def test_pruning_and_pass1_variants_identical(sc, golden, golden_arrays, cuda_de
         _native.set_option("prune", 1)
         _native.set_option("pass1_packed", 1)
         _native.set_option("graphs", 1)
+        _native.set_option("fused_bbox", 1)
     _native.set_option("prune", 1)
     sc.calculate_coefficients(cases[-1][0], cases[-1][1])
     d = _native.last_diagnostics(cuda_device)
@@ -328,7 +330,7 @@ import json, sys
 sys.path.insert(0, sys.argv[1])
 from paper_2510_02894_b200 import _native, synth
 import paper_2510_02894_b200 as sc
-_native.set_option("dcap", 1000)   # before any slot exists: buffers start far too small
+_native.set_option(sys.argv[2], int(sys.argv[3]))  # before any slot exists: far too small
 arr = synth.thin_slab()
 outs = sc.calculate_coefficients_batch([arr] * 3, [(0.5, 0.5, 5.0)] * 3)
 one = sc.calculate_coefficients(arr, (0.5, 0.5, 5.0))
@@ -336,10 +338,11 @@ print(json.dumps([o.to_dict() | {"T": o.triangle_count, "A": o.active_cubes} for
 """
 
 
-def test_capacity_overflow_rerun(golden, cuda_device):
-    """More vertices than the diameter-side buffers hold: the device reports the
-    overflow, the host re-runs with exact sizes, results are unchanged (fresh
-    process so the slots start small)."""
+@pytest.mark.parametrize("option,value", [("dcap", 1000), ("wcap", 4)])
+def test_capacity_overflow_rerun(golden, cuda_device, option, value):
+    """More vertices (dcap) or surviving 3-D chunk pairs (wcap) than the
+    buffers hold: the device reports the overflow, the host re-runs with exact
+    sizes, results are unchanged (fresh process so the slots start small)."""
     import json
     import subprocess
     import sys
@@ -347,7 +350,8 @@ def test_capacity_overflow_rerun(golden, cuda_device):
     from conftest import ROOT
 
     case = next(c for c in golden["big"] if c["name"] == "C5_thin_slab")
-    out = subprocess.run([sys.executable, "-c", _OVERFLOW_SCRIPT, ROOT], capture_output=True,
+    out = subprocess.run([sys.executable, "-c", _OVERFLOW_SCRIPT, ROOT, option, str(value)],
+                         capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     for rec in json.loads(out.stdout.strip().splitlines()[-1]):

@@ -8,4 +8,6 @@ for w in c2 c5 c3 c4; do
   timeout 900 python bench.py --workload $w --steps $steps --warmup 3 > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err
   echo "$w rc=$?" >> gpurun_out/bench_$w.err
 done
+
+timeout 600 python bench.py --workload c3 --split --steps 5 --warmup 3 > gpurun_out/bench_c3_split.json 2> gpurun_out/bench_c3_split.err; echo "split rc=$?" >> gpurun_out/bench_c3_split.err
 echo done
