@@ -48,8 +48,7 @@ constexpr int kR = kChunk / 32;                // 4 i vertices per lane
 // pair instead of 3.5 for scalar FFMA.
 template <bool PACKED>
 __global__ void __launch_bounds__(kDiamThreads, 4) diam3d_pass1(const int4* __restrict__ keys,
-                                                                long long cap, const RoiParams* __restrict__ rp, int shard,
-                                                                int nshards,
+                                                                long long cap, const RoiParams* __restrict__ rp,
                                                                 const uint2* __restrict__ work,
                                                                 float* __restrict__ umax,
                                                                 Stats* __restrict__ st) {
@@ -62,7 +61,8 @@ __global__ void __launch_bounds__(kDiamThreads, 4) diam3d_pass1(const int4* __re
   frame_centre(st, f);
   const long long n_work = (long long)st->n_work;
   long long w0, w1;
-  shard_span(n_work, shard, nshards, w0, w1);
+  w0 = 0;
+  w1 = n_work;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float4* sj = sj_all[warp];
   // Each warp takes a contiguous run of units, so consecutive units usually
@@ -146,9 +146,9 @@ __global__ void __launch_bounds__(kDiamThreads, 4) diam3d_pass1(const int4* __re
   }
   if (lane == 0) atomic_max_pos_f32(&st->d3_f32, run);
 }
-template __global__ void diam3d_pass1<true>(const int4*, long long, const RoiParams*, int, int,
+template __global__ void diam3d_pass1<true>(const int4*, long long, const RoiParams*,
                                             const uint2*, float*, Stats*);
-template __global__ void diam3d_pass1<false>(const int4*, long long, const RoiParams*, int, int,
+template __global__ void diam3d_pass1<false>(const int4*, long long, const RoiParams*,
                                              const uint2*, float*, Stats*);
 
 // Exact re-check.  Every block sweeps 256 work entries at a time: the units
@@ -159,7 +159,6 @@ template __global__ void diam3d_pass1<false>(const int4*, long long, const RoiPa
 // serial scan of the unit maxima anywhere.
 __global__ void __launch_bounds__(kDiamThreads) diam3d_refine(const int4* __restrict__ keys,
                                                               long long cap, const RoiParams* __restrict__ rp,
-                                                              int shard, int nshards,
                                                               const uint2* __restrict__ work,
                                                               const float* __restrict__ umax,
                                                               Stats* __restrict__ st) {
@@ -172,7 +171,8 @@ __global__ void __launch_bounds__(kDiamThreads) diam3d_refine(const int4* __rest
   __shared__ int s_n;
   const long long n = n_vertices(st, cap);
   long long w0, w1;
-  shard_span((long long)st->n_work, shard, nshards, w0, w1);
+  w0 = 0;
+  w1 = (long long)st->n_work;
   const float tau = __uint_as_float(st->d3_f32) * (1.f - kRefineRel);
   const int ti = threadIdx.x % kChunk, tj = (threadIdx.x / kChunk) * kJ;
   double best = 0.0;

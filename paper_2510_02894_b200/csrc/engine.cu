@@ -43,23 +43,24 @@ __global__ void scan_all(unsigned int*, unsigned int*, const unsigned int*, unsi
 __global__ void scatter_all(const int4*, long long, const Stats*, unsigned int*, int4*,
                             const unsigned int*, unsigned int*, int2*, unsigned int*);
 __global__ void boxes_extremes(const int4*, long long, const RoiParams*, Stats*, int4*, int4*);
-__global__ void unit_filter(const int4*, const int4*, long long, const RoiParams*, int, Stats*,
-                            uint2*, const int4*);
+__global__ void unit_filter(const int4*, const int4*, long long, const RoiParams*, int, int, int,
+                            Stats*, uint2*, const int4*);
 template <bool PACKED>
-__global__ void diam3d_pass1(const int4*, long long, const RoiParams*, int, int, const uint2*,
-                             float*, Stats*);
-__global__ void diam3d_refine(const int4*, long long, const RoiParams*, int, int, const uint2*,
-                              const float*, Stats*);
+__global__ void diam3d_pass1(const int4*, long long, const RoiParams*, const uint2*, float*,
+                             Stats*);
+__global__ void diam3d_refine(const int4*, long long, const RoiParams*, const uint2*, const float*,
+                              Stats*);
 __global__ void plane_boxes(const int2*, const unsigned int*, const unsigned int*,
                             const RoiParams*, const Stats*, int4*, unsigned long long*);
 __global__ void plane_lb(const int2*, const unsigned int*, const unsigned long long*,
                          const RoiParams*, Stats*);
 __global__ void plane_filter(const unsigned int*, const unsigned int*, const unsigned int*,
-                             const int4*, const RoiParams*, int, long long, Stats*, uint2*);
-__global__ void plane_pass1(const int2*, const unsigned int*, const uint2*, const RoiParams*, int,
-                            int, long long, float*, Stats*);
-__global__ void plane_refine(const int2*, const unsigned int*, const uint2*, const RoiParams*, int,
-                             int, const float*, long long, Stats*);
+                             const int4*, const RoiParams*, int, int, int, long long, Stats*,
+                             uint2*);
+__global__ void plane_pass1(const int2*, const unsigned int*, const uint2*, const RoiParams*,
+                            long long, float*, Stats*);
+__global__ void plane_refine(const int2*, const unsigned int*, const uint2*, const RoiParams*,
+                             const float*, long long, Stats*);
 __global__ void cloud_diameters(const double*, const double*, const double*, long long, int,
                                 unsigned long long*);
 int launch_binarize(const void*, int, const long long[3], int, int, long long, double, uint8_t*,
@@ -300,6 +301,7 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     if (const char* v = getenv("SC_PRUNE")) g_opt_prune = std::strcmp(v, "0") != 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_plane, plane_pass1, 256, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pack, pack_bits_v16<4, false>, 256, 0));
+    if (const char* v = getenv("SC_PACK_BPS")) c->occ_pack = std::max(1, std::atoi(v));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_mc, mc_cells, 256, 0));
     {
       // Lazy module loading must not happen inside a stream capture: touch
@@ -440,7 +442,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
                                                                                c->d_stats);
     CKL(1);
     CK(record(c, c->kev[1], s));
-    bits_bbox<<<c->sms * 8, 256, 0, s>>>(rp, reinterpret_cast<const uint4*>(c->bits.p),
+    bits_bbox<<<c->sms * 4, 256, 0, s>>>(rp, reinterpret_cast<const uint4*>(c->bits.p),
                                          c->d_stats);
     CKL(1);
   } else {
@@ -478,20 +480,20 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   boxes_extremes<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->d_stats, c->boxes.p,
                                             c->sboxes.p);
   CKL(1);
-  unit_filter<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, c->boxes.p, dcap, rp, prune,
-                                         c->d_stats, c->work.p, c->sboxes.p);
+  unit_filter<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, c->boxes.p, dcap, rp, prune, shard,
+                                         nshards, c->d_stats, c->work.p, c->sboxes.p);
   CKL(1);
   CK(record(c, c->kev[3], s));
   if (g_opt_packed.load())
-    diam3d_pass1<true><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, shard, nshards,
-                                             c->work.p, c->warp_max.p, c->d_stats);
+    diam3d_pass1<true><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->work.p,
+                                             c->warp_max.p, c->d_stats);
   else
-    diam3d_pass1<false><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, shard, nshards,
-                                              c->work.p, c->warp_max.p, c->d_stats);
+    diam3d_pass1<false><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->work.p,
+                                              c->warp_max.p, c->d_stats);
   CKL(1);
   CK(record(c, c->kev[4], s));
-  diam3d_refine<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, shard, nshards,
-                                           c->work.p, c->warp_max.p, c->d_stats);
+  diam3d_refine<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->work.p, c->warp_max.p,
+                                           c->d_stats);
   CKL(1);
   CK(record(c, c->kev[5], s));
   plane_boxes<<<c->sms * 4, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_cstart.p,
@@ -501,14 +503,14 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
                                   c->d_stats);
   CKL(1);
   plane_filter<<<c->sms * 4, 256, 0, s>>>(c->plane_start.p, c->plane_tstart.p, c->plane_cstart.p,
-                                          c->plane_boxes_buf.p, rp, prune, pucap, c->d_stats,
-                                          c->plane_work.p);
+                                          c->plane_boxes_buf.p, rp, prune, shard, nshards, pucap,
+                                          c->d_stats, c->plane_work.p);
   CKL(1);
   plane_pass1<<<plgrid, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_work.p, rp,
-                                     shard, nshards, pucap, c->plane_umax.p, c->d_stats);
+                                     pucap, c->plane_umax.p, c->d_stats);
   CKL(1);
   plane_refine<<<c->sms * 2, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_work.p,
-                                          rp, shard, nshards, c->plane_umax.p, pucap, c->d_stats);
+                                          rp, c->plane_umax.p, pucap, c->d_stats);
   CKL(1);
   CK(record(c, c->kev[6], s));
   return SC_OK;

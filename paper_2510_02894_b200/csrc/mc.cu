@@ -119,24 +119,31 @@ __global__ void __launch_bounds__(256) pack_bits_v16(const RoiParams* __restrict
 }
 
 // Occupied bbox from the bit volume (L2-resident right after the pack): only
-// nonzero words locate themselves.  4 words per thread-load.
+// nonzero words locate themselves.  Four 16-byte loads in flight per thread.
 __global__ void __launch_bounds__(256) bits_bbox(const RoiParams* __restrict__ rp,
                                                  const uint4* __restrict__ bits4,
                                                  Stats* __restrict__ st) {
+  constexpr int kU = 4;
   const long long n_words = rp->n_words;
   const int W = rp->W, ny = (int)rp->ny;
   BoxAcc box;
   const long long n4 = n_words / 4;
-  const long long step = (long long)gridDim.x * blockDim.x;
-  for (long long base = (long long)blockIdx.x * blockDim.x; base < n4; base += step) {
-    const long long i = base + threadIdx.x;
-    if (i < n4) {
-      const uint4 v = __ldcg(bits4 + i);
-      if (v.x | v.y | v.z | v.w) {
-        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+  const long long step = (long long)gridDim.x * blockDim.x * kU;
+  for (long long base = (long long)blockIdx.x * blockDim.x * kU; base < n4; base += step) {
+    uint4 v[kU];
 #pragma unroll
-        for (int k = 0; k < 4; k++)
-          if (w4[k]) box.add(w4[k], 4 * i + k, W, ny);
+    for (int k = 0; k < kU; k++) {
+      const long long i = base + (long long)k * blockDim.x + threadIdx.x;
+      v[k] = i < n4 ? __ldcg(bits4 + i) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < kU; k++) {
+      if (v[k].x | v[k].y | v[k].z | v[k].w) {
+        const long long i = base + (long long)k * blockDim.x + threadIdx.x;
+        const uint32_t w4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+        for (int t = 0; t < 4; t++)
+          if (w4[t]) box.add(w4[t], 4 * i + t, W, ny);
       }
     }
   }

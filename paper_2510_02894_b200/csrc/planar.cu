@@ -221,8 +221,8 @@ __global__ void plane_filter(const unsigned int* __restrict__ start,
                              const unsigned int* __restrict__ tstart,
                              const unsigned int* __restrict__ cstart,
                              const int4* __restrict__ pboxes, const RoiParams* __restrict__ rp,
-                             int prune, long long wcap, Stats* __restrict__ st,
-                             uint2* __restrict__ pwork) {
+                             int prune, int shard, int nshards, long long wcap,
+                             Stats* __restrict__ st, uint2* __restrict__ pwork) {
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   const long long units = (long long)st->plane_units;
@@ -269,8 +269,10 @@ __global__ void plane_filter(const unsigned int* __restrict__ start,
       const int i = 2 * I + h, j0 = 2 * J, j1 = 2 * J + 1;
       bool k0 = false, k1 = false;
       if (coarse && i < nc) {
-        k0 = j0 >= i && j0 < nc;
-        k1 = j1 < nc;  // j1 = 2J + 1 >= i always
+        // Shards own chunk pairs by identity (coarse unit u, sub-pair), so the
+        // split is the same whatever order the lists come out in.
+        k0 = j0 >= i && j0 < nc && (u * 4 + 2 * h) % nshards == shard;
+        k1 = j1 < nc && (u * 4 + 2 * h + 1) % nshards == shard;  // j1 = 2J + 1 >= i always
         if (prune && (k0 || k1)) {
           const int4 bi = pboxes[c0 + i];
           if (k0) {
@@ -313,15 +315,14 @@ __device__ __forceinline__ float2 plane_point(int2 k, const PlaneAxes& ax) {
 // refine kernel selects the re-check candidates from the unit maxima.
 __global__ void __launch_bounds__(kPlaneThreads, 4) plane_pass1(
     const int2* __restrict__ sorted, const unsigned int* __restrict__ start,
-    const uint2* __restrict__ pwork, const RoiParams* __restrict__ rp, int shard, int nshards,
+    const uint2* __restrict__ pwork, const RoiParams* __restrict__ rp,
     long long wcap, float* __restrict__ umax, Stats* __restrict__ st) {
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   __shared__ float4 sj_all[kPlaneWarps][kPC];
   if (st->bbox[3] < 0 || (long long)st->n_pwork > wcap) return;  // host re-runs with room
   const PlaneSpace ps = plane_space(st);
-  long long w0, w1;
-  shard_span((long long)st->n_pwork, shard, nshards, w0, w1);
+  const long long w0 = 0, w1 = (long long)st->n_pwork;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float4* sj = sj_all[warp];
   const long long gwarps = (long long)gridDim.x * kPlaneWarps;
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(kPlaneThreads, 4) plane_pass1(
 // each: 128 i entries x two halves of the j chunk.
 __global__ void __launch_bounds__(kPlaneThreads) plane_refine(
     const int2* __restrict__ sorted, const unsigned int* __restrict__ start,
-    const uint2* __restrict__ pwork, const RoiParams* __restrict__ rp, int shard, int nshards,
+    const uint2* __restrict__ pwork, const RoiParams* __restrict__ rp,
     const float* __restrict__ umax, long long wcap, Stats* __restrict__ st) {
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
@@ -412,8 +413,7 @@ __global__ void __launch_bounds__(kPlaneThreads) plane_refine(
   __shared__ int s_n;
   if (st->bbox[3] < 0 || (long long)st->n_pwork > wcap) return;
   const PlaneSpace ps = plane_space(st);
-  long long w0, w1;
-  shard_span((long long)st->n_pwork, shard, nshards, w0, w1);
+  const long long w0 = 0, w1 = (long long)st->n_pwork;
   float tau[3];
 #pragma unroll
   for (int a = 0; a < 3; a++) tau[a] = __uint_as_float(st->pl_f32[a]) * (1.f - kRefineRel);

@@ -23,6 +23,7 @@ namespace sc {
 constexpr int kChunkV = kChunk3;
 constexpr int kPerLane = kChunkV / 32;
 constexpr int kSuper = 8;  // super-chunk = 8 chunks (1024 vertices): first level of unit_filter
+constexpr long long kSingleLevelMax = 1LL << 22;  // chunk pairs tested directly below this
 constexpr int kNDir = 13;
 
 __device__ __forceinline__ long long n_verts(const Stats* st, long long cap) {
@@ -266,7 +267,8 @@ __device__ __forceinline__ double axis_reach(int loA, int hiA, int loB, int hiB,
 // compacted into `work` (pair index t over the C x C upper triangle).
 __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys,
                                                    const int4* __restrict__ boxes, long long cap,
-                                                   const RoiParams* __restrict__ rp, int prune, Stats* __restrict__ st,
+                                                   const RoiParams* __restrict__ rp, int prune,
+                                                   int shard, int nshards, Stats* __restrict__ st,
                                                    uint2* __restrict__ work,
                                                    const int4* __restrict__ sboxes) {
   if (st->ovf) return;  // re-run pending (scan_all)
@@ -314,6 +316,30 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
            axis_reach(alo.y, ahi.y, blo.y, bhi.y, h3[1]) +
            axis_reach(alo.z, ahi.z, blo.z, bhi.z, h3[2]);
   };
+  const long long fine_units = C * (C + 1) / 2;
+  if (fine_units <= kSingleLevelMax) {
+    // Small ROI: every chunk pair tested directly (one level, no serial
+    // expansion chains), listed in tile_pair order (I-major).
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < fine_units;
+         base += (long long)gridDim.x * blockDim.x) {
+      const long long u = base + threadIdx.x;
+      bool keep = false;
+      int i = 0, j = 0;
+      if (u < fine_units) {
+        tile_pair(u, C, i, j);
+        keep = u % nshards == shard &&
+               (!prune || reach(boxes[2 * i], boxes[2 * i + 1], boxes[2 * j], boxes[2 * j + 1]) >= thr);
+      }
+      const unsigned int mask = __ballot_sync(0xffffffffu, keep);
+      if (!mask) continue;
+      unsigned long long pos = 0;
+      if (lane == 0) pos = atomicAdd(&st->n_work, (unsigned long long)__popc(mask));
+      pos = __shfl_sync(0xffffffffu, pos, 0);
+      const long long o = (long long)pos + __popc(mask & ((1u << lane) - 1));
+      if (keep && o < wcap) work[o] = make_uint2((unsigned int)i, (unsigned int)j);
+    }
+    return;
+  }
   for (long long base = (long long)blockIdx.x * blockDim.x; base < units;
        base += (long long)gridDim.x * blockDim.x) {
     const long long u = base + threadIdx.x;
@@ -336,7 +362,10 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
       for (int h = 0; h < 2; h++) {
         const int r = h * 32 + lane;
         const int i = kSuper * it + (r >> 3), j = kSuper * jt + (r & 7);
-        bool keep = i < C && j < C && j >= i;
+        // Shards own chunk pairs by identity (their tile_pair index), so the
+        // split is the same whatever order the lists come out in.
+        bool keep = i < C && j < C && j >= i &&
+                    ((long long)i * C - (long long)i * (i - 1) / 2 + (j - i)) % nshards == shard;
         if (keep && prune)
           keep = reach(boxes[2 * i], boxes[2 * i + 1], boxes[2 * j], boxes[2 * j + 1]) >= thr;
         const unsigned int mask = __ballot_sync(0xffffffffu, keep);
