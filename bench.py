@@ -411,7 +411,7 @@ def run_ours(args):
                 "unit": "TFLOP/s", "frac": ach / fp32_peak,
                 "traffic": traffic.get("diam3d_pass1"),
                 "work": f"{label}: 8 flop x {evaluated:.4g} evaluated pairs "
-                        f"({d['work_units']} of {d['total_units']} units of 256x256)",
+                        f"({d['work_units']} of {d['total_units']} units of {int(_native.PAIRS_PER_UNIT ** 0.5)}x{int(_native.PAIRS_PER_UNIT ** 0.5)})",
                 "pair_evals_per_s": evaluated / t,
                 "peak_note": "FP32 CUDA-core rate measured on this GPU by sc_probe_fp32_peak "
                              f"(best of FFMA/FFMA-imm/FFMA2; FFMA2 alone {fp32_ffma2:.1f} "

@@ -194,6 +194,7 @@ __device__ __forceinline__ unsigned long long window(const uint32_t* __restrict_
 }
 
 constexpr int kZChunk = 4;
+constexpr int kStage = 256;  // staged vertices per warp and z step (denser steps emit directly)
 
 __device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits, int q, int v, int w,
                                           int W, int ny, int nz, bool on, uint32_t& cur,
@@ -215,7 +216,7 @@ __device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits, int
 // Every emitted vertex is also counted into the histograms the diameter stage
 // sorts by: its 3-D Morton brick (block-private, flushed once per block) and
 // its (plane, in-plane brick) bin in each of its three planes (global).
-__global__ void __launch_bounds__(256) mc_cells(const RoiParams* __restrict__ rp,
+__global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__ rp,
                                                 const uint32_t* __restrict__ bits,
                                                 const CaseTables* __restrict__ tabs,
                                                 Stats* __restrict__ st, int4* __restrict__ vkeys,
@@ -224,10 +225,17 @@ __global__ void __launch_bounds__(256) mc_cells(const RoiParams* __restrict__ rp
   __shared__ unsigned int s_hist[kNumCases];
   __shared__ int4 s_tn[kNumCases];
   __shared__ unsigned int s_sup[kSortSupers];
+  __shared__ int4 s_stage[256 / 32][kStage];  // per-warp vertex stage (blockDim = 256)
   const int ny = (int)rp->ny, nz = (int)rp->nz, W = rp->W;
   int bb[6];
 #pragma unroll
   for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
+  if (bb[3] < 0) return;  // empty ROI (block-uniform)
+  {  // blocks past the bbox's work items have nothing to do: skip the prologue too
+    const long long items = (long long)(((bb[3] + 1) >> 5) - (bb[0] >> 5) + 1) *
+                            (bb[4] - bb[1] + 2) * ((bb[5] - bb[2] + 2 + kZChunk - 1) / kZChunk);
+    if ((long long)blockIdx.x * blockDim.x >= items) return;
+  }
   const PlaneSpace ps = plane_space(bb);
   const PlaneBricks pbk = plane_bricks(bb);
   const int bshift = brick_shift(bb);
@@ -312,35 +320,74 @@ __global__ void __launch_bounds__(256) mc_cells(const RoiParams* __restrict__ rp
           unsigned long long wbase = 0;
           if (lane == 31) wbase = atomicAdd(&st->n_vert, (unsigned long long)total);
           wbase = __shfl_sync(kFull, wbase, 31);
-          long long o = (long long)(wbase + incl - c);
           const int Y2 = 2 * v, Z2 = 2 * w;
-          auto emit = [&](int X, int Y, int Z) {
-            if (o < cap) vkeys[o] = make_int4(X, Y, Z, 0);
-            o++;
-            if (pbin_counts) {  // NULL on the mesh-export path (no diameter stage)
-              const unsigned int bin = brick_bin(X, Y, Z, bb, bshift);
-              atomicAdd(&sort_counts[bin], 1u);
-              atomicAdd(&s_sup[bin >> kSortSliceBits], 1u);
+          if (pbin_counts && total <= kStage) {
+            // Stage the step's vertices in shared memory (cheap per-lane
+            // loop), then bin and store them with all 32 lanes converged:
+            // coalesced key stores, warp-aggregated histogram atomics.
+            int4* stg = s_stage[threadIdx.x >> 5];
+            uint32_t o = incl - c;
+            while (ex) {
+              const int i = __ffs(ex) - 1; ex &= ex - 1;
+              stg[o++] = make_int4(2 * (xbase + i) + 1, Y2, Z2, 0);
+            }
+            while (ey) {
+              const int i = __ffs(ey) - 1; ey &= ey - 1;
+              stg[o++] = make_int4(2 * (xbase + i), Y2 + 1, Z2, 0);
+            }
+            while (ez) {
+              const int i = __ffs(ez) - 1; ez &= ez - 1;
+              stg[o++] = make_int4(2 * (xbase + i), Y2, Z2 + 1, 0);
+            }
+            __syncwarp();
+            for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+              const uint32_t k = k0 + lane;
+              const bool ok = k < total;
+              const int4 key = stg[ok ? k : 0];
+              const long long g = (long long)wbase + k;
+              if (ok && g < cap) vkeys[g] = key;
+              const unsigned int bin = brick_bin(key.x, key.y, key.z, bb, bshift);
+              group_add(sort_counts, bin, ok);
+              if (ok) atomicAdd(&s_sup[bin >> kSortSliceBits], 1u);
               int id[3];
               unsigned int pbin[3];
-              plane_ids(X, Y, Z, ps, id);
-              plane_bins(X, Y, Z, pbk, pbin);
+              plane_ids(key.x, key.y, key.z, ps, id);
+              plane_bins(key.x, key.y, key.z, pbk, pbin);
 #pragma unroll
-              for (int a = 0; a < 3; a++)
-                atomicAdd(&pbin_counts[(long long)id[a] * kPlaneBins + pbin[a]], 1u);
+              for (int a2 = 0; a2 < 3; a2++)
+                group_add(pbin_counts, (unsigned int)id[a2] * kPlaneBins + pbin[a2], ok);
             }
-          };
-          while (ex) {
-            const int i = __ffs(ex) - 1; ex &= ex - 1;
-            emit(2 * (xbase + i) + 1, Y2, Z2);
-          }
-          while (ey) {
-            const int i = __ffs(ey) - 1; ey &= ey - 1;
-            emit(2 * (xbase + i), Y2 + 1, Z2);
-          }
-          while (ez) {
-            const int i = __ffs(ez) - 1; ez &= ez - 1;
-            emit(2 * (xbase + i), Y2, Z2 + 1);
+            __syncwarp();  // the stage is rewritten by the next step
+          } else {
+            long long o = (long long)(wbase + incl - c);
+            auto emit = [&](int X, int Y, int Z) {
+              if (o < cap) vkeys[o] = make_int4(X, Y, Z, 0);
+              o++;
+              if (pbin_counts) {  // NULL on the mesh-export path (no diameter stage)
+                const unsigned int bin = brick_bin(X, Y, Z, bb, bshift);
+                atomicAdd(&sort_counts[bin], 1u);
+                atomicAdd(&s_sup[bin >> kSortSliceBits], 1u);
+                int id[3];
+                unsigned int pbin[3];
+                plane_ids(X, Y, Z, ps, id);
+                plane_bins(X, Y, Z, pbk, pbin);
+#pragma unroll
+                for (int a2 = 0; a2 < 3; a2++)
+                  atomicAdd(&pbin_counts[(long long)id[a2] * kPlaneBins + pbin[a2]], 1u);
+              }
+            };
+            while (ex) {
+              const int i = __ffs(ex) - 1; ex &= ex - 1;
+              emit(2 * (xbase + i) + 1, Y2, Z2);
+            }
+            while (ey) {
+              const int i = __ffs(ey) - 1; ey &= ey - 1;
+              emit(2 * (xbase + i), Y2 + 1, Z2);
+            }
+            while (ez) {
+              const int i = __ffs(ez) - 1; ez &= ez - 1;
+              emit(2 * (xbase + i), Y2, Z2 + 1);
+            }
           }
         }
       }
