@@ -337,7 +337,7 @@ def run_ours(args):
     step_sps = [sps[i % len(sps)] for i in range(K)]
 
     # ---- device-resident throughput (value): K ROIs through the pipelined
-    # device batch entry (two slots: ROI i+1 is enqueued before ROI i is
+    # device batch entry (8 slots: ROI i+1 is enqueued before ROI i is
     # collected), CUDA events on `stream`, which the batch is ordered against.
     clocks = ClockSampler(dev)
     W = args.warmup

@@ -9,22 +9,18 @@
 // layout are read from the Stats the marching-cubes stage wrote, so a whole
 // ROI is enqueued without a host round trip (and can be graph-captured).
 //
-//  * diam3d_pass1   -- the O(V^2) hot loop.  Triangular grid of 2048x2048 tile
-//    pairs, each split into 8 work units of 2048 i x 256 j; a persistent grid
-//    walks the units.  The j chunk is staged in shared memory as
-//    (x, y, z, |p|^2); each thread register-blocks 8 i vertices, so a pair
-//    costs three FFMA (dot form |pj|^2 - 2 pi.pj) plus half an FMNMX3 on the
-//    fp32 CUDA cores.  fp32 coordinates live in a bbox-centred frame.  One
-//    maximum per (tile pair, warp) is kept for the exact re-check.
-//  * diam3d_select / diam3d_refine -- exactness: every (tile pair, warp) whose
-//    pass-1 maximum lies within kRefineRel of the pass-1 maximum is
-//    re-evaluated in fp64 with the reference's own arithmetic on the
-//    reference's own coordinates, so the 3-D diameter is the reference's value
-//    bit for bit.  Units below the threshold provably cannot hold the maximum
-//    (pass-1 error < ~1e-6 of D^2).
-//  * plane_*        -- keyed planar pass: counting sort of the vertices by the
-//    doubled lattice key of z / y / x (bit-equal fp64 coordinate <=> equal
-//    key), then the same fp32-dot pass + fp64 re-check inside every plane.
+//  * diam3d_pass1   -- the O(V^2) hot loop over the surviving chunk pairs
+//    listed by unit_filter (prune.cu).  A warp evaluates one 128 x 128 unit:
+//    the J chunk is staged in the warp's shared memory as (x, y, z, |p|^2),
+//    each lane register-blocks 4 i vertices, so a pair costs 1.5 FFMA2 plus
+//    half an FMNMX3 on the fp32 CUDA cores (dot form |pj|^2 - 2 pi.pj in a
+//    bbox-centred frame).  One maximum per unit is kept.
+//  * diam3d_refine  -- exactness: every unit whose pass-1 maximum lies within
+//    kRefineRel of the pass-1 maximum is re-evaluated in fp64 with the
+//    reference's own arithmetic on the reference's own coordinates, so the 3-D
+//    diameter is the reference's value bit for bit.  Units below the threshold
+//    provably cannot hold the maximum (pass-1 error < ~1e-6 of D^2).
+//    The planar pass (planar.cu) has the same two steps per plane family.
 //  * cloud_diameters -- the generic diameters(xs, ys, zs) API on arbitrary
 //    fp64 points with the reference's in-loop bit-equality tests.
 #include "sc_device.cuh"

@@ -749,7 +749,7 @@ double wall_ms() {
   return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
 }
 
-// Pipelined batch on the two slots of `device`: ROI i+1 is enqueued (H2D copy
+// Pipelined batch over the slots of `device` (option "slots", default 8): ROI i+1 is enqueued (H2D copy
 // included for host masks) before ROI i is collected, so copies, kernels and
 // the host round trip of neighbouring ROIs overlap.  The first failing ROI's
 // code is returned; every other ROI is still processed.

@@ -2,7 +2,7 @@
 //
 // The maximum pair distance D^2 is at least LB = the largest exact pair value
 // among a few extreme vertices (13 directions, both ends).  After a Morton
-// brick ordering of the vertices, every 256-vertex chunk is spatially compact,
+// brick ordering of the vertices, every 128-vertex chunk is spatially compact,
 // so most chunk pairs have an upper bound UB^2 = max distance^2 between their
 // boxes below LB: they cannot hold the maximum pair and are not evaluated.  Surviving units run through
 // diam3d_pass1 and the fp64 re-check keeps the result bit-identical to the
