@@ -147,8 +147,11 @@ def raise_for(rc: int, what: str = "") -> None:
     raise errors.DeviceError(f"{what}: {msg} (code {rc})")
 
 
-KERNEL_TIME_NAMES = ("pack_ms", "mc_ms", "prune_ms", "diam3d_pass1_ms", "diam3d_refine_ms",
-                     "planar_ms", "h2d_ms")
+# Stage times of the last ROI: HBM pack, bbox + marching cubes, 3-D sort/boxes/
+# filter, pass 1 (3-D + planar lists), exact re-check (both), planar prep
+# (plane boxes / lower bounds / filter), host->device copy.
+KERNEL_TIME_NAMES = ("pack_ms", "mc_ms", "prune_ms", "pass1_ms", "refine_ms", "planar_prep_ms",
+                     "h2d_ms")
 
 
 def last_kernel_times(device: int = 0) -> dict:

@@ -1,8 +1,8 @@
 // Host orchestration and the C ABI (include/shapecore_b200.h).
 //
-// One ROI = init -> pack_bits -> mc_cells -> [one 2 KB D2H of counts + bbox]
-// -> diam3d_pass1 -> diam3d_refine -> plane_{hist,scan,scatter,pairs} -> D2H of
-// the accumulators.  Area, volume, triangle and active-cube counts are formed
+// One ROI = init -> pack -> bbox -> mc_cells -> sort / boxes / filters (3-D and
+// planar) -> one fused pass-1 kernel -> one fused exact re-check -> D2H of the
+// accumulators, enqueued without host round trips.  Area, volume, triangle and active-cube counts are formed
 // on the host from exact integer histograms.  Per
 // device the library keeps one context: a stream, events, grow-only scratch
 // arenas and pinned result buffers, reused across calls (SURVEY.md 8b
@@ -46,10 +46,12 @@ __global__ void boxes_extremes(const int4*, long long, const RoiParams*, Stats*,
 __global__ void unit_filter(const int4*, const int4*, long long, const RoiParams*, int, int, int,
                             Stats*, uint2*, const int4*);
 template <bool PACKED>
-__global__ void diam3d_pass1(const int4*, long long, const RoiParams*, const uint2*, float*,
-                             Stats*);
-__global__ void diam3d_refine(const int4*, long long, const RoiParams*, const uint2*, const float*,
-                              Stats*);
+__global__ void diam_pass1(const int4*, long long, const RoiParams*, const uint2*, float*,
+                           const int2*, const unsigned int*, const uint2*, long long, float*,
+                           Stats*);
+__global__ void diam_refine(const int4*, long long, const RoiParams*, const uint2*, const float*,
+                            const int2*, const unsigned int*, const uint2*, long long,
+                            const float*, Stats*);
 __global__ void plane_boxes(const int2*, const unsigned int*, const unsigned int*,
                             const RoiParams*, const Stats*, int4*, unsigned long long*);
 __global__ void plane_lb(const int2*, const unsigned int*, const unsigned long long*,
@@ -57,10 +59,6 @@ __global__ void plane_lb(const int2*, const unsigned int*, const unsigned long l
 __global__ void plane_filter(const unsigned int*, const unsigned int*, const unsigned int*,
                              const int4*, const RoiParams*, int, int, int, long long, Stats*,
                              uint2*);
-__global__ void plane_pass1(const int2*, const unsigned int*, const uint2*, const RoiParams*,
-                            long long, float*, Stats*);
-__global__ void plane_refine(const int2*, const unsigned int*, const uint2*, const RoiParams*,
-                             const float*, long long, Stats*);
 __global__ void cloud_diameters(const double*, const double*, const double*, long long, int,
                                 unsigned long long*);
 int launch_binarize(const void*, int, const long long[3], int, int, long long, double, uint8_t*,
@@ -91,6 +89,7 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<bool> g_opt_prune{true}, g_opt_packed{true}, g_opt_graphs{true};
+std::atomic<int> g_opt_stages{1 << 30};  // debug: kernels enqueued per ROI
 std::atomic<bool> g_opt_fbox{false};  // bbox accumulated inside the pack (else bits_bbox; measured faster)
 std::atomic<int> g_opt_slots{8};  // pipeline slots used by the batch entries
 std::atomic<long long> g_opt_dcap{2LL << 20};  // default diameter-side vertex capacity
@@ -204,7 +203,7 @@ struct Ctx {
   bool times_pending = false;  // last_ms[0..5] still to be read from kev[]
   long long cap_floor = 0, dcap_floor = 0, wcap_floor = 0;  // raised by overflow re-runs only
   long long last_diag[6] = {0, 0, 0, 0, 0, 0};
-  int occ_pass1 = 1, occ_pass1s = 1, occ_plane = 1, occ_pack = 1, occ_mc = 1;  // blocks/SM
+  int occ_pass1 = 1, occ_pass1s = 1, occ_pack = 1, occ_mc = 1;  // blocks/SM
   Stats* d_stats = nullptr;
   Stats* h_stats = nullptr;  // pinned
   RoiParams* d_rp = nullptr;  // per-ROI launch parameters (device)
@@ -233,6 +232,7 @@ struct Ctx {
     void* d_sq4;
     long long cap, dcap;
     bool prune, packed, fbox;
+    int stages;
     unsigned long long gen;
     cudaGraphExec_t exec;
     unsigned long long launches;
@@ -295,11 +295,10 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     CK(cudaMalloc(&c->d_tabs, sizeof(CaseTables)));
     CK(cudaMemcpy(c->d_tabs, &case_geom().tabs, sizeof(CaseTables), cudaMemcpyHostToDevice));
     CK(upload_mesh_tables());
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pass1, diam3d_pass1<true>, 256, 0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pass1s, diam3d_pass1<false>, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pass1, diam_pass1<true>, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pass1s, diam_pass1<false>, 256, 0));
     if (const char* v = getenv("SC_PASS1")) g_opt_packed = std::strcmp(v, "scalar") != 0;
     if (const char* v = getenv("SC_PRUNE")) g_opt_prune = std::strcmp(v, "0") != 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_plane, plane_pass1, 256, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pack, pack_bits_v16<4, false>, 256, 0));
     if (const char* v = getenv("SC_PACK_BPS")) c->occ_pack = std::max(1, std::atoi(v));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_mc, mc_cells, 256, 0));
@@ -314,9 +313,8 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
                                (const void*)pack_bits_generic, (const void*)mc_cells,
                                (const void*)scan_all, (const void*)scatter_all,
                                (const void*)boxes_extremes, (const void*)unit_filter,
-                               (const void*)diam3d_pass1<true>, (const void*)diam3d_pass1<false>,
-                               (const void*)diam3d_refine, (const void*)plane_pass1,
-                               (const void*)plane_refine, (const void*)cloud_diameters,
+                               (const void*)diam_pass1<true>, (const void*)diam_pass1<false>,
+                               (const void*)diam_refine, (const void*)cloud_diameters,
                                (const void*)plane_bins_scan, (const void*)plane_boxes,
                                (const void*)plane_lb, (const void*)plane_filter};
       for (const void* k : kernels) CK(cudaFuncGetAttributes(&fa, k));
@@ -428,38 +426,47 @@ int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, lo
 // kev[] brackets the stages for sc_last_kernel_times.
 int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   const RoiParams* rp = c->d_rp;
+  // Diagnostic option "debug_stages": enqueue only the first N kernels (results
+  // invalid) to measure the marginal batch cost of each stage.
+  const int lim = g_opt_stages.load();
+  int nk = 0;
   const long long cap = (long long)c->keys.cap, dcap = c->dcap_sz;
   init_stats<<<1, 256, 0, s>>>(c->d_stats);
   CKL(1);
+  if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[0], s));  // kev0..kev1 = the HBM pass alone
   if (fast && g_opt_fbox.load()) {
     pack_bits_v16<4, true><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(rp, c->bits.p,
                                                                               c->d_stats);
     CKL(1);
+    if (++nk >= lim) return SC_OK;
     CK(record(c, c->kev[1], s));
   } else if (fast) {
     pack_bits_v16<4, false><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(rp, c->bits.p,
                                                                                c->d_stats);
     CKL(1);
+    if (++nk >= lim) return SC_OK;
     CK(record(c, c->kev[1], s));
     bits_bbox<<<c->sms * 4, 256, 0, s>>>(rp, reinterpret_cast<const uint4*>(c->bits.p),
                                          c->d_stats);
     CKL(1);
+    if (++nk >= lim) return SC_OK;
   } else {
     pack_bits_generic<<<c->sms * 8, 256, 0, s>>>(rp, c->bits.p, c->d_stats);
     CKL(1);
+    if (++nk >= lim) return SC_OK;
     CK(record(c, c->kev[1], s));
   }
   mc_cells<<<c->sms * std::max(1, c->occ_mc), 256, 0, s>>>(rp, c->bits.p, c->d_tabs, c->d_stats,
                                                           c->keys.p, cap, c->sort_counts.p,
                                                           c->pbin_counts.p);
   CKL(1);
+  if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[2], s));
 
   // Persistent grids: exactly the resident blocks, so the static round-robin
   // split of work units is also the load balance.
   const int pgrid = c->sms * std::max(1, g_opt_packed.load() ? c->occ_pass1 : c->occ_pass1s);
-  const int plgrid = c->sms * std::max(1, c->occ_plane);
   const long long pucap = (long long)c->plane_umax.cap;
   const int prune = g_opt_prune.load() ? 1 : 0;
 
@@ -468,50 +475,58 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   plane_bins_scan<<<c->sms * 2, 256, 0, s>>>(c->pbin_counts.p, c->pbin_cursor.p,
                                              c->plane_counts.p, c->plane_ext.p, c->d_stats);
   CKL(1);
+  if (++nk >= lim) return SC_OK;
   scan_all<<<kSortSupers + 1, 1024, 0, s>>>(c->sort_counts.p, c->sort_cursor.p,
                                             c->plane_counts.p, c->plane_start.p,
                                             c->plane_tstart.p, c->plane_cstart.p, dcap,
                                             c->d_stats, c->sboxes.p);
   CKL(1);
+  if (++nk >= lim) return SC_OK;
   scatter_all<<<c->sms * 4, 256, 0, s>>>(c->keys.p, dcap, c->d_stats, c->sort_cursor.p,
                                          c->keys_sorted.p, c->plane_start.p, c->pbin_cursor.p,
                                          c->plane_sorted.p, c->sort_counts.p + kSortBins);
   CKL(1);
+  if (++nk >= lim) return SC_OK;
   boxes_extremes<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->d_stats, c->boxes.p,
                                             c->sboxes.p);
   CKL(1);
+  if (++nk >= lim) return SC_OK;
   unit_filter<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, c->boxes.p, dcap, rp, prune, shard,
                                          nshards, c->d_stats, c->work.p, c->sboxes.p);
   CKL(1);
+  if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[3], s));
-  if (g_opt_packed.load())
-    diam3d_pass1<true><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->work.p,
-                                             c->warp_max.p, c->d_stats);
-  else
-    diam3d_pass1<false><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->work.p,
-                                              c->warp_max.p, c->d_stats);
-  CKL(1);
-  CK(record(c, c->kev[4], s));
-  diam3d_refine<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->work.p, c->warp_max.p,
-                                           c->d_stats);
-  CKL(1);
-  CK(record(c, c->kev[5], s));
   plane_boxes<<<c->sms * 4, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_cstart.p,
                                          rp, c->d_stats, c->plane_boxes_buf.p, c->plane_ext.p);
   CKL(1);
+  if (++nk >= lim) return SC_OK;
   plane_lb<<<c->sms, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_ext.p, rp,
                                   c->d_stats);
   CKL(1);
+  if (++nk >= lim) return SC_OK;
   plane_filter<<<c->sms * 4, 256, 0, s>>>(c->plane_start.p, c->plane_tstart.p, c->plane_cstart.p,
                                           c->plane_boxes_buf.p, rp, prune, shard, nshards, pucap,
                                           c->d_stats, c->plane_work.p);
   CKL(1);
-  plane_pass1<<<plgrid, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_work.p, rp,
-                                     pucap, c->plane_umax.p, c->d_stats);
+  if (++nk >= lim) return SC_OK;
+  CK(record(c, c->kev[4], s));
+  // One pass-1 kernel and one re-check kernel for the 3-D and the planar lists.
+  if (g_opt_packed.load())
+    diam_pass1<true><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->work.p, c->warp_max.p,
+                                           c->plane_sorted.p, c->plane_start.p, c->plane_work.p,
+                                           pucap, c->plane_umax.p, c->d_stats);
+  else
+    diam_pass1<false><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->work.p, c->warp_max.p,
+                                            c->plane_sorted.p, c->plane_start.p, c->plane_work.p,
+                                            pucap, c->plane_umax.p, c->d_stats);
   CKL(1);
-  plane_refine<<<c->sms * 2, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_work.p,
-                                          rp, c->plane_umax.p, pucap, c->d_stats);
+  if (++nk >= lim) return SC_OK;
+  CK(record(c, c->kev[5], s));
+  diam_refine<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->work.p, c->warp_max.p,
+                                         c->plane_sorted.p, c->plane_start.p, c->plane_work.p,
+                                         pucap, c->plane_umax.p, c->d_stats);
   CKL(1);
+  if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[6], s));
   return SC_OK;
 }
@@ -550,7 +565,10 @@ void fill_out(const Stats& h, const double sp[3], sc_coeffs* out) {
 
 float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, a, b);
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+    (void)cudaGetLastError();  // an unrecorded / pending event is not a launch error
+    ms = 0.f;
+  }
   return ms;
 }
 
@@ -612,7 +630,8 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   for (auto& g : c->graphs)
     if (g.fast == fast && g.s == s && g.shard == shard && g.nshards == nshards &&
         g.d_sq4 == d_sq4 && g.cap == cap && g.dcap == dcap && g.prune == prune &&
-        g.packed == packed && g.fbox == fbox && g.gen == c->gen) {
+        g.packed == packed && g.fbox == fbox && g.stages == g_opt_stages.load() &&
+        g.gen == c->gen) {
       CK(cudaGraphLaunch(g.exec, s));
       if (hp) g_hprof.launch += wall_ms() - t0;
       g_launches.fetch_add(g.launches, std::memory_order_relaxed);
@@ -637,8 +656,8 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
     cudaGraphExecDestroy(c->graphs.front().exec);
     c->graphs.erase(c->graphs.begin());
   }
-  Ctx::GraphEntry g{fast, s, shard, nshards, d_sq4, cap, dcap, prune, packed, fbox, c->gen, exec,
-                    launches};
+  Ctx::GraphEntry g{fast, s, shard, nshards, d_sq4, cap, dcap, prune, packed, fbox,
+                    g_opt_stages.load(), c->gen, exec, launches};
   c->graphs.push_back(g);
   CK(cudaGraphLaunch(exec, s));
   g_launches.fetch_add(launches, std::memory_order_relaxed);
@@ -1245,7 +1264,9 @@ int sc_last_kernel_times(int device, double* ms, int n) {
   if (rc) return -rc;
   std::lock_guard<std::mutex> lk(c->mu);
   if (c->times_pending) {
-    for (int i = 0; i < 6; i++) c->last_ms[i] = ev_ms(c->kev[i], c->kev[i + 1]);
+    // pack, mc, prune (3-D), pass 1 (3-D + planar), re-check (both), planar prep
+    static const int from[6] = {0, 1, 2, 4, 5, 3}, to[6] = {1, 2, 3, 5, 6, 4};
+    for (int i = 0; i < 6; i++) c->last_ms[i] = ev_ms(c->kev[from[i]], c->kev[to[i]]);
     c->times_pending = false;
   }
   int m = n < 7 ? n : 7;
@@ -1274,6 +1295,7 @@ int sc_set_option(const char* name, int value) {
   else if (std::strcmp(name, "dcap") == 0) g_opt_dcap = std::max(256, value);
   else if (std::strcmp(name, "wcap") == 0) g_opt_wcap = std::max(1, value);
   else if (std::strcmp(name, "fused_bbox") == 0) g_opt_fbox = value != 0;
+  else if (std::strcmp(name, "debug_stages") == 0) g_opt_stages = value > 0 ? value : (1 << 30);
   else { set_err("unknown option %s", name); return SC_ERR_INPUT; }
   return SC_OK;
 }

@@ -1,0 +1,49 @@
+// The two O(pairs) kernels of the diameter stage (sm_100a): one pass-1 kernel
+// and one exact re-check kernel, each running the 3-D and the planar work
+// lists back to back (pass_bodies.cuh).  Fusing them halves the kernel
+// boundaries of the diameter stage; the two lists are independent, so every
+// warp simply works through its share of the first list, then of the second.
+#include "pass_bodies.cuh"
+
+namespace sc {
+
+template <bool PACKED>
+__global__ void __launch_bounds__(kDiamThreads, 4) diam_pass1(
+    const int4* __restrict__ keys, long long cap, const RoiParams* __restrict__ rp,
+    const uint2* __restrict__ work, float* __restrict__ umax, const int2* __restrict__ sorted,
+    const unsigned int* __restrict__ start, const uint2* __restrict__ pwork, long long pwcap,
+    float* __restrict__ pumax, Stats* __restrict__ st) {
+  if (st->ovf || st->bbox[3] < 0) return;  // re-run pending (scan_all) / empty
+  __shared__ float4 sj_all[kWarps][kChunk];  // per-warp J chunk, (x, y, z | -, |p|^2)
+  float4* sj = sj_all[threadIdx.x >> 5];
+  // A list longer than its buffer means a re-run with exact sizes is pending.
+  if ((long long)st->n_work <= rp->wcap) pass1_3d<PACKED>(keys, cap, rp, work, umax, st, sj);
+  __syncwarp();
+  if ((long long)st->n_pwork <= pwcap) pass1_planar(sorted, start, pwork, rp, pumax, st, sj);
+}
+template __global__ void diam_pass1<true>(const int4*, long long, const RoiParams*, const uint2*,
+                                          float*, const int2*, const unsigned int*, const uint2*,
+                                          long long, float*, Stats*);
+template __global__ void diam_pass1<false>(const int4*, long long, const RoiParams*, const uint2*,
+                                           float*, const int2*, const unsigned int*,
+                                           const uint2*, long long, float*, Stats*);
+
+__global__ void __launch_bounds__(kDiamThreads) diam_refine(
+    const int4* __restrict__ keys, long long cap, const RoiParams* __restrict__ rp,
+    const uint2* __restrict__ work, const float* __restrict__ umax,
+    const int2* __restrict__ sorted, const unsigned int* __restrict__ start,
+    const uint2* __restrict__ pwork, long long pwcap, const float* __restrict__ pumax,
+    Stats* __restrict__ st) {
+  if (st->ovf || st->bbox[3] < 0) return;  // block-uniform
+  __shared__ double s_a[kChunk], s_b[kChunk], s_c[kChunk];
+  __shared__ double s_red[kDiamThreads / 32];
+  __shared__ unsigned int s_list[kDiamThreads];
+  __shared__ int s_n;
+  if ((long long)st->n_work <= rp->wcap)
+    refine_3d(keys, cap, rp, work, umax, st, s_a, s_b, s_c, s_list, s_n);
+  __syncthreads();
+  if ((long long)st->n_pwork <= pwcap)
+    refine_planar(sorted, start, pwork, rp, pumax, st, s_a, s_b, s_red, s_list, s_n);
+}
+
+}  // namespace sc

@@ -14,8 +14,8 @@
 //   plane_lb         -- exact per-family lower bound from the extremes
 //   plane_filter     -- keep in-plane chunk pairs whose box distance reaches it
 //                       (tile pairs first, then their 2 x 2 chunk pairs)
-//   plane_pass1      -- fp32 dot-form max per surviving unit (+ selection)
-//   plane_refine     -- fp64 reference-arithmetic re-check of the candidates
+//   (pass1_planar / refine_planar in pass_bodies.cuh, run inside the fused
+//    pass-1 and re-check kernels of passes.cu)
 //
 // A unit (work entry) is one in-plane chunk pair: uint2 {plane, I << 16 | J}.
 // The owning plane of a tile pair / chunk is found by binary search over the
@@ -28,9 +28,6 @@ namespace sc {
 
 constexpr int kPT = kPlaneTile;      // in-plane tile edge (first filter level)
 constexpr int kPC = kPlaneChunk;     // in-plane chunk edge (pair unit = chunk x chunk)
-constexpr int kPR = kPC / 32;        // 4 i entries per lane in plane_pass1
-constexpr int kPlaneThreads = 256;
-constexpr int kPlaneWarps = kPlaneThreads / 32;
 
 // Largest p in [0, P) with off[p] <= x (off non-decreasing, off[0] = 0): the
 // plane owning global tile pair / chunk x.
@@ -299,174 +296,6 @@ __global__ void plane_filter(const unsigned int* __restrict__ start,
       }
       if (k1 && o < wcap)
         pwork[o] = make_uint2((unsigned int)p, ((unsigned int)i << 16) | (unsigned int)j1);
-    }
-  }
-}
-
-__device__ __forceinline__ float2 plane_point(int2 k, const PlaneAxes& ax) {
-  return make_float2((float)(k.x - ax.ca) * ax.ha, (float)(k.y - ax.cb) * ax.hb);
-}
-
-// Planar pass 1: fp32 dot form over every surviving in-plane chunk pair
-// (128 x 128).  Every warp is an independent worker (own shared-memory copy
-// of the J chunk as (a, b, |p|^2)); each lane register-blocks 4 i entries and
-// evaluates two of them per FFMA2, so a pair costs one FFMA2 + half an FMNMX3.
-// One maximum per work entry; per-family maxima in st->pl_f32[axis].  The
-// refine kernel selects the re-check candidates from the unit maxima.
-__global__ void __launch_bounds__(kPlaneThreads, 4) plane_pass1(
-    const int2* __restrict__ sorted, const unsigned int* __restrict__ start,
-    const uint2* __restrict__ pwork, const RoiParams* __restrict__ rp,
-    long long wcap, float* __restrict__ umax, Stats* __restrict__ st) {
-  if (st->ovf) return;  // re-run pending (scan_all)
-  Frame f = rp->f;
-  __shared__ float4 sj_all[kPlaneWarps][kPC];
-  if (st->bbox[3] < 0 || (long long)st->n_pwork > wcap) return;  // host re-runs with room
-  const PlaneSpace ps = plane_space(st);
-  const long long w0 = 0, w1 = (long long)st->n_pwork;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float4* sj = sj_all[warp];
-  const long long gwarps = (long long)gridDim.x * kPlaneWarps;
-  const long long gw = (long long)blockIdx.x * kPlaneWarps + warp;
-  const long long per = (w1 - w0 + gwarps - 1) / gwarps;
-  const long long wb = w0 + gw * per, we = min(w1, wb + per);
-  float run0 = 0.f, run1 = 0.f, run2 = 0.f;  // per-family maxima
-  unsigned int prev_p = 0xffffffffu, prev_i = 0xffffffffu;
-  float2 a2[kPR / 2], b2[kPR / 2];
-  float ni[kPR];
-  int axis = 0;
-  for (long long w = wb; w < we; w++) {
-    const uint2 u = pwork[w];
-    const unsigned int p = u.x, I = u.y >> 16, J = u.y & 0xffffu;
-    const unsigned int b0 = start[p], np = start[p + 1] - b0;
-    axis = plane_axis((int)p, ps);
-    const PlaneAxes ax = plane_axes(axis, st, f);
-    __syncwarp();  // previous unit is done with sj
-    if (p != prev_p || I != prev_i) {
-#pragma unroll
-      for (int r = 0; r < kPR / 2; r++) {
-        unsigned int i0 = I * kPC + (2 * r) * 32 + lane, i1 = i0 + 32;
-        const float2 q0 = plane_point(sorted[b0 + min(i0, np - 1)], ax);
-        const float2 q1 = plane_point(sorted[b0 + min(i1, np - 1)], ax);
-        a2[r] = make_float2(-2.f * q0.x, -2.f * q1.x);
-        b2[r] = make_float2(-2.f * q0.y, -2.f * q1.y);
-        ni[2 * r] = fmaf(q0.x, q0.x, q0.y * q0.y);
-        ni[2 * r + 1] = fmaf(q1.x, q1.x, q1.y * q1.y);
-      }
-      prev_p = p;
-      prev_i = I;
-    }
-#pragma unroll
-    for (int r = 0; r < kPR; r++) {
-      const unsigned int j = J * kPC + r * 32 + lane;
-      const float2 q = plane_point(sorted[b0 + min(j, np - 1)], ax);  // repeats are harmless
-      sj[r * 32 + lane] = make_float4(q.x, q.y, fmaf(q.x, q.x, q.y * q.y), 0.f);
-    }
-    __syncwarp();
-    float m[kPR];
-#pragma unroll
-    for (int r = 0; r < kPR; r++) m[r] = -3.0e38f;
-#pragma unroll 2
-    for (int j = 0; j < kPC; j += 2) {
-      const float4 q0 = sj[j], q1 = sj[j + 1];
-#pragma unroll
-      for (int r = 0; r < kPR / 2; r++) {
-        float2 t0 = __ffma2_rn(a2[r], make_float2(q0.x, q0.x), make_float2(q0.z, q0.z));
-        float2 t1 = __ffma2_rn(a2[r], make_float2(q1.x, q1.x), make_float2(q1.z, q1.z));
-        t0 = __ffma2_rn(b2[r], make_float2(q0.y, q0.y), t0);
-        t1 = __ffma2_rn(b2[r], make_float2(q1.y, q1.y), t1);
-        m[2 * r] = fmax3f(m[2 * r], t0.x, t1.x);
-        m[2 * r + 1] = fmax3f(m[2 * r + 1], t0.y, t1.y);
-      }
-    }
-    float best = 0.f;
-#pragma unroll
-    for (int r = 0; r < kPR; r++) best = fmaxf(best, m[r] + ni[r]);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
-    if (lane == 0) umax[w] = best;
-    if (axis == 0) run0 = fmaxf(run0, best);
-    else if (axis == 1) run1 = fmaxf(run1, best);
-    else run2 = fmaxf(run2, best);
-  }
-  if (lane == 0) {
-    if (run0 > 0.f) atomic_max_pos_f32(&st->pl_f32[0], run0);
-    if (run1 > 0.f) atomic_max_pos_f32(&st->pl_f32[1], run1);
-    if (run2 > 0.f) atomic_max_pos_f32(&st->pl_f32[2], run2);
-  }
-}
-
-// Exact planar re-check (fp64, reference arithmetic: the out-of-plane delta
-// is exactly 0, so da*da + db*db is the reference's 3-term sum bit for bit).
-// Every block sweeps 256 work entries at a time, lists those within
-// kRefineRel of their family's pass-1 maximum in shared memory and re-checks
-// each: 128 i entries x two halves of the j chunk.
-__global__ void __launch_bounds__(kPlaneThreads) plane_refine(
-    const int2* __restrict__ sorted, const unsigned int* __restrict__ start,
-    const uint2* __restrict__ pwork, const RoiParams* __restrict__ rp,
-    const float* __restrict__ umax, long long wcap, Stats* __restrict__ st) {
-  if (st->ovf) return;  // re-run pending (scan_all)
-  Frame f = rp->f;
-  constexpr int kSplit = kPlaneThreads / kPC, kJ = kPC / kSplit;
-  __shared__ double sa[kPC], sb[kPC];
-  __shared__ double s_red[kPlaneThreads / 32];
-  __shared__ unsigned int s_list[kPlaneThreads];
-  __shared__ int s_n;
-  if (st->bbox[3] < 0 || (long long)st->n_pwork > wcap) return;
-  const PlaneSpace ps = plane_space(st);
-  const long long w0 = 0, w1 = (long long)st->n_pwork;
-  float tau[3];
-#pragma unroll
-  for (int a = 0; a < 3; a++) tau[a] = __uint_as_float(st->pl_f32[a]) * (1.f - kRefineRel);
-  const int ti = threadIdx.x % kPC, tj = (threadIdx.x / kPC) * kJ;
-  // Block b sweeps entries w0 + b, w0 + b + G, ... (G = grid size), 256 at a
-  // time, so candidates (adjacent in the work list) spread over the blocks.
-  const long long G = gridDim.x;
-  for (long long sweep = 0; w0 + sweep * kPlaneThreads * G < w1; sweep++) {
-    __syncthreads();  // previous sweep is done with s_list / s_n
-    if (threadIdx.x == 0) s_n = 0;
-    __syncthreads();
-    const long long w = w0 + (sweep * kPlaneThreads + threadIdx.x) * G + blockIdx.x;
-    if (w < w1) {
-      const int a = plane_axis((int)pwork[w].x, ps);
-      if (umax[w] >= (a == 0 ? tau[0] : (a == 1 ? tau[1] : tau[2])))
-        s_list[atomicAdd(&s_n, 1)] = (unsigned int)w;
-    }
-    __syncthreads();
-    const int cnt = s_n;
-    if (threadIdx.x == 0 && cnt) atomicAdd(&st->n_pcand, (unsigned long long)cnt);
-    for (int q = 0; q < cnt; q++) {
-      const uint2 u = pwork[s_list[q]];
-      const unsigned int p = u.x, I = u.y >> 16, J = u.y & 0xffffu;
-      const int axis = plane_axis((int)p, ps);
-      const PlaneAxes ax = plane_axes(axis, st, f);
-      const unsigned int b0 = start[p], np = start[p + 1] - b0;
-      const unsigned int i = I * kPC + ti;
-      const unsigned int jn = min((unsigned int)kPC, np - J * kPC);
-      __syncthreads();  // previous candidate is done with sa/sb/s_red
-      if (threadIdx.x < kPC && J * kPC + threadIdx.x < np) {
-        const int2 k = sorted[b0 + J * kPC + threadIdx.x];
-        sa[threadIdx.x] = ref_coord(k.x, ax.sa);
-        sb[threadIdx.x] = ref_coord(k.y, ax.sb);
-      }
-      __syncthreads();
-      double best = 0.0;
-      if (i < np) {
-        const int2 k = sorted[b0 + i];
-        const double ai = ref_coord(k.x, ax.sa), bi = ref_coord(k.y, ax.sb);
-        const unsigned int te = min(jn, (unsigned int)(tj + kJ));
-        for (unsigned int t = tj; t < te; t++) {
-          const double da = __dsub_rn(sa[t], ai), db = __dsub_rn(sb[t], bi);
-          best = fmax(best, __dadd_rn(__dmul_rn(da, da), __dmul_rn(db, db)));
-        }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
-      if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = best;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        for (int wi = 1; wi < kPlaneThreads / 32; wi++) best = fmax(best, s_red[wi]);
-        if (best > 0.0) atomic_max_pos_f64(&st->sq[1 + axis], best);
-      }
     }
   }
 }
