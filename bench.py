@@ -391,8 +391,23 @@ def run_ours(args):
     e2e_s = max_over_ranks(world, time.perf_counter() - t0)
     barrier(world)
     e2e_value = world * K / e2e_s
-    h2d_bytes = sum(h_masks[i % n_host].size for i in range(K)) / K
+    h2d_bytes = sum(o.h2d_bytes for o in e_outs) / K
+    scan_ms = statistics.median(o.host_scan_ms for o in e_outs)
     assert e_outs[0].to_dict() == outs[0].to_dict()
+    # same, copying every mask byte (option host_crop off): the PCIe-bound figure
+    _native.set_option("host_crop", 0)
+    sc.calculate_coefficients_batch([h_masks[i % n_host] for i in range(8)],
+                                    [sps[i % n_host] for i in range(8)], device=dev)
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    f_outs = sc.calculate_coefficients_batch([h_masks[i % n_host] for i in range(K)],
+                                             [sps[i % n_host] for i in range(K)], device=dev)
+    torch.cuda.synchronize()
+    full_s = max_over_ranks(world, time.perf_counter() - t0)
+    barrier(world)
+    _native.set_option("host_crop", 1)
+    assert f_outs[0].to_dict() == outs[0].to_dict()
 
     # ---- rooflines ----
     V = c.vertex_count
@@ -455,8 +470,15 @@ def run_ours(args):
         "path": "sc_calculate_coefficients_device_batch (C ABI), device-resident masks",
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d_bytes),
                 "d2h_bytes_per_step": 2400,  # one Stats record (sc_device.cuh)
-                "path": "sc_calculate_coefficients_batch (C ABI, pipelined) from pinned host memory",
-                "h2d_ms_per_roi": e_outs[-1].h2d_ms},
+                "path": "sc_calculate_coefficients_batch (C ABI, pipelined) from pinned host "
+                        "memory: host scan of every mask byte for the occupied z/y slab "
+                        "(host_threads), then only that slab is copied H2D",
+                "mask_bytes_per_step": int(sum(h_masks[i % n_host].size for i in range(K)) / K),
+                "host_scan_ms_per_roi": scan_ms,
+                "h2d_ms_per_roi": e_outs[-1].h2d_ms,
+                "full_copy": {"value": world * K / full_s, "unit": UNIT,
+                              "h2d_bytes_per_step": int(sum(o.h2d_bytes for o in f_outs) / K),
+                              "note": "option host_crop=0: every mask byte crosses PCIe"}},
         "single_roi": {"value": world * one_steps / (one_ms / 1e3), "unit": UNIT,
                        "path": "sc_calculate_coefficients_device, one synchronous call per ROI"},
         "gpu_launches": int(launches),

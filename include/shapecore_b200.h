@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define SC_ABI_VERSION 1
+#define SC_ABI_VERSION 2
 
 enum {
   SC_OK = 0,
@@ -68,10 +68,17 @@ typedef struct {
   double mesh_ms;      /* bit-pack + marching-cubes kernels, CUDA events           */
   double diameters_ms; /* 3-D + planar diameter kernels, CUDA events               */
   double total_ms;     /* host wall time of the whole call                         */
+  /* ABI 2: host-mask entries copy only the occupied z/y slab (option
+   * "host_crop"); h2d_bytes is what crossed PCIe, host_scan_ms the host scan
+   * that found the slab.  Both 0 for device-resident masks. */
+  int64_t h2d_bytes;
+  double host_scan_ms;
 } sc_coeffs;
 
-/* Host mask (pageable or pinned).  device: CUDA ordinal.  Copies the mask to
- * the device inside the call (chunked, overlapped with the bit-pack kernel). */
+/* Host mask (pageable or pinned).  device: CUDA ordinal.  The host finds the
+ * occupied z/y slab (all host threads) and copies only that slab to the device
+ * (option "host_crop", default 1; 0 = copy all nx*ny*nz bytes).  Results are
+ * identical either way: everything outside the slab is background. */
 int sc_calculate_coefficients(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz,
                               const double spacing[3], int device, sc_coeffs* out);
 
@@ -150,7 +157,9 @@ int sc_last_diagnostics(int device, int64_t* out, int n);
 /* Process-wide switches: "prune" (default 1) = exact bbox pruning of 3-D and
  * planar work units; "pass1_packed" (1) = FFMA2 variant of the 3-D pass;
  * "graphs" (1) = replay each ROI pipeline as a cached CUDA graph; "slots" (8)
- * = pipeline slots (stream + scratch) the batch entries keep in flight.
+ * = pipeline slots (stream + scratch) the batch entries keep in flight;
+ * "host_crop" (1) = host-mask entries copy only the occupied z/y slab;
+ * "host_threads" (hardware threads, <= 32) = threads of the host slab scan.
  * Results are identical either way; 0 on success, SC_ERR_INPUT otherwise. */
 int sc_set_option(const char* name, int value);
 uint64_t sc_launch_count(void);
@@ -174,6 +183,13 @@ int sc_marching_cubes(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz,
  * volume, |volume|), bit-exact with the reference for the same arrays. */
 int sc_mesh_measure(const double* xs, const double* ys, const double* zs, int64_t nv,
                     const int32_t* tris, int64_t nt, int device, double out[3]);
+
+/* Host-only helper behind option "host_crop" (no device needed): occupied
+ * extent of a host mask as out = (z0, z1, y0, y1), inclusive; returns
+ * SC_ERR_EMPTY_ROI (out untouched) when every byte is zero.  threads <= 0 =
+ * the "host_threads" option. */
+int sc_occupied_slab(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, int threads,
+                     int64_t out[4]);
 
 const char* sc_last_error(void); /* thread-local message of the last failure */
 int sc_abi_version(void);

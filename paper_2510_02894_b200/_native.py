@@ -38,6 +38,7 @@ EXPORTED = (
     "sc_set_option",
     "sc_launch_count",
     "sc_probe_fp32_peak",
+    "sc_occupied_slab",
     "sc_last_error",
     "sc_abi_version",
     "sc_device_count",
@@ -61,6 +62,8 @@ class ScCoeffs(ctypes.Structure):
         ("mesh_ms", ctypes.c_double),
         ("diameters_ms", ctypes.c_double),
         ("total_ms", ctypes.c_double),
+        ("h2d_bytes", ctypes.c_int64),
+        ("host_scan_ms", ctypes.c_double),
     ]
 
 
@@ -114,6 +117,7 @@ def load():
         L.sc_last_diagnostics.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
         L.sc_set_option.argtypes = [ctypes.c_char_p, ctypes.c_int]
         L.sc_probe_fp32_peak.argtypes = [ctypes.c_int, ctypes.c_int, dp]
+        L.sc_occupied_slab.argtypes = [u8p, i64, i64, i64, ctypes.c_int, ctypes.POINTER(i64)]
         L.sc_last_error.restype = ctypes.c_char_p
         L.sc_abi_version.restype = ctypes.c_int
         L.sc_device_count.restype = ctypes.c_int
@@ -190,3 +194,20 @@ def last_diagnostics(device: int = 0) -> dict:
 
 def set_option(name: str, value: int) -> None:
     raise_for(load().sc_set_option(name.encode(), int(value)), "sc_set_option")
+
+
+def occupied_slab(mask, threads: int = 0):
+    """(z0, z1, y0, y1) occupied extent of a C-contiguous (nz, ny, nx) uint8
+    mask via the library's host scan (no device needed); None if empty."""
+    import numpy as np
+
+    arr = np.ascontiguousarray(mask, dtype=np.uint8)
+    nz, ny, nx = arr.shape
+    out = (ctypes.c_int64 * 4)()
+    rc = load().sc_occupied_slab(arr.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), nx, ny,
+                                 nz, int(threads), out)
+    if rc == 3:
+        return None
+    if rc != 0:
+        raise ValueError(last_error())
+    return tuple(int(v) for v in out)

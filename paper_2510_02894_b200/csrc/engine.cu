@@ -20,9 +20,11 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/shapecore_b200.h"
+#include "host_crop.h"
 #include "mc_tables.h"
 #include "sc_device.cuh"
 
@@ -94,6 +96,8 @@ std::atomic<bool> g_opt_fbox{false};  // bbox accumulated inside the pack (else 
 std::atomic<int> g_opt_slots{8};  // pipeline slots used by the batch entries
 std::atomic<long long> g_opt_dcap{2LL << 20};  // default diameter-side vertex capacity
 std::atomic<long long> g_opt_wcap{1LL << 20};  // default 3-D work-list capacity (chunk pairs)
+std::atomic<bool> g_opt_crop{true};  // host entries: copy only the occupied z/y slab (host_crop.h)
+std::atomic<int> g_opt_host_threads{(int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()))};
 std::atomic<unsigned long long> g_launches{0};
 
 void set_err(const char* fmt, ...) {
@@ -222,6 +226,8 @@ struct Ctx {
   DevBuf<int4> plane_boxes_buf;
   DevBuf<int2> plane_sorted;
   DevBuf<uint8_t> mask_stage, raw_stage;
+  double last_scan_ms = 0.0;      // host slab scan of the last host-mask ROI
+  long long last_h2d_bytes = 0;   // bytes that crossed PCIe for it
   DevBuf<double> cloud;
   DevBuf<unsigned long long> cloud_out;
   // CUDA graphs of whole ROIs, keyed by everything baked into the nodes.
@@ -600,7 +606,8 @@ bool host_prof_on() {
 }
 
 int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
-               const double sp[3], cudaStream_t s, int shard, int nshards, double* d_sq4) {
+               const double sp[3], cudaStream_t s, int shard, int nshards, double* d_sq4,
+               const int org[3]) {
   RoiParams& h = *c->h_rp;  // the slot's previous ROI has been collected: safe to rewrite
   h.mask = d_mask;
   h.nx = nx;
@@ -617,6 +624,9 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   h.f.sx = sp[0];
   h.f.sy = sp[1];
   h.f.sz = sp[2];
+  h.f.ox2 = 2 * org[0];  // slab origin (host crop); graph-invariant like the rest
+  h.f.oy2 = 2 * org[1];
+  h.f.oz2 = 2 * org[2];
   h.wcap = (long long)std::min(c->work.cap, c->warp_max.cap);
   const bool hp = host_prof_on();
   double t0 = hp ? wall_ms() : 0.0;
@@ -674,11 +684,14 @@ struct Pending {
   int shard, nshards;
   double* d_sq4;
   long long cap, dcap, wunits;
+  int org[3];  // origin of the (cropped) volume in the caller's grid, voxels
 };
 
 int start_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
               const double sp[3], cudaStream_t s, int shard, int nshards, double* d_sq4,
-              long long punits, Pending* p) {
+              long long punits, Pending* p, const int org[3] = nullptr) {
+  static const int kZero[3] = {0, 0, 0};
+  if (!org) org = kZero;
   // Requested sizes depend only on the dims and on floors raised by overflow
   // re-runs (never on the allocated capacities, so graphs stay valid).
   if (p->cap > 0) {  // re-run after an overflow: exact sizes from now on
@@ -696,8 +709,8 @@ int start_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
     c->drop_graphs();
   }
   *p = Pending{d_mask, nx, ny, nz, {sp[0], sp[1], sp[2]}, s, shard, nshards, d_sq4,
-               (long long)c->keys.cap, c->dcap_sz, 0};
-  return launch_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4);
+               (long long)c->keys.cap, c->dcap_sz, 0, {org[0], org[1], org[2]}};
+  return launch_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, org);
 }
 
 // Wait for the ROI started on slot c, re-run it once with exact buffer sizes
@@ -721,8 +734,9 @@ int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
     q.cap = std::max(p->cap, V);
     q.dcap = std::max(p->dcap, V);
     q.wunits = WU;
+    const int org[3] = {q.org[0], q.org[1], q.org[2]};
     int rc = start_roi(c, q.d_mask, q.nx, q.ny, q.nz, q.sp, q.s, q.shard, q.nshards, q.d_sq4, PU,
-                       &q);
+                       &q, org);
     if (rc) return rc;
     CK(cudaStreamSynchronize(q.s));
     if ((long long)c->h_stats->n_vert > q.dcap ||
@@ -756,9 +770,10 @@ int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
 
 // Full pipeline on a device-resident mask (context lock held by the caller).
 int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, const double sp[3],
-            cudaStream_t s, int shard, int nshards, double* d_sq4, sc_coeffs* out) {
+            cudaStream_t s, int shard, int nshards, double* d_sq4, sc_coeffs* out,
+            const int org[3] = nullptr) {
   Pending p{};
-  int rc = start_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, 0, &p);
+  int rc = start_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, 0, &p, org);
   if (rc) return rc;
   return finish_roi(c, &p, out);
 }
@@ -766,6 +781,45 @@ int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, c
 double wall_ms() {
   using namespace std::chrono;
   return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+// Copy a host mask into the slot's staging buffer on stream s (events ev[0] /
+// ev[1] bracket the copy).  With option "host_crop" (default on) the host first
+// finds the occupied z/y slab (host_crop.h, all host threads) and only that
+// slab crosses PCIe, as one 2-D copy of whole x rows; *cy / *cz / org then
+// describe the slab (x is never cropped).  An all-background mask is reported
+// here, before any device work, as the reference does (mesh.py:78-79).
+int stage_host_mask(Ctx* c, const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz,
+                    cudaStream_t s, int64_t* cy, int64_t* cz, int org[3]) {
+  org[0] = org[1] = org[2] = 0;
+  c->last_scan_ms = 0.0;
+  *cy = ny;
+  *cz = nz;
+  const uint8_t* src = mask;
+  if (g_opt_crop.load()) {
+    const double t0 = wall_ms();
+    const Slab sl = occupied_slab(mask, nx, ny, nz, g_opt_host_threads.load());
+    c->last_scan_ms = wall_ms() - t0;
+    if (sl.empty) {
+      set_err("mask has no occupied voxels");
+      return SC_ERR_EMPTY_ROI;
+    }
+    *cy = sl.y1 - sl.y0 + 1;
+    *cz = sl.z1 - sl.z0 + 1;
+    org[1] = (int)sl.y0;
+    org[2] = (int)sl.z0;
+    src = mask + (sl.z0 * ny + sl.y0) * nx;
+  }
+  const size_t width = (size_t)nx * *cy;
+  CK(cudaEventRecord(c->ev[0], s));
+  if (*cy == ny)
+    CK(cudaMemcpyAsync(c->mask_stage.p, src, width * *cz, cudaMemcpyHostToDevice, s));
+  else
+    CK(cudaMemcpy2DAsync(c->mask_stage.p, width, src, (size_t)nx * ny, width, (size_t)*cz,
+                         cudaMemcpyHostToDevice, s));
+  CK(cudaEventRecord(c->ev[1], s));
+  c->last_h2d_bytes = (long long)(width * *cz);
+  return SC_OK;
 }
 
 // Pipelined batch over the slots of `device` (option "slots", default 8): ROI i+1 is enqueued (H2D copy
@@ -835,6 +889,8 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
     note(finish_roi(c, &pend[k], o));
     if (host) {
       o->h2d_ms = ev_ms(c->ev[0], c->ev[1]);
+      o->h2d_bytes = c->last_h2d_bytes;
+      o->host_scan_ms = c->last_scan_ms;
       c->last_ms[6] = o->h2d_ms;
     }
     o->total_ms = wall_ms() - t_start[k];
@@ -852,17 +908,17 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
     cudaStream_t s = c->stream;
     t_start[k] = wall_ms();
     const uint8_t* dm = masks[i];
+    int64_t cx = nx, cy = ny, cz = nz;
+    int org[3] = {0, 0, 0};
     if (host) {
-      const size_t bytes = (size_t)nx * ny * nz;
-      CK(c->mask_stage.ensure(bytes));
-      CK(cudaEventRecord(c->ev[0], s));
-      CK(cudaMemcpyAsync(c->mask_stage.p, masks[i], bytes, cudaMemcpyHostToDevice, s));
-      CK(cudaEventRecord(c->ev[1], s));
+      CK(c->mask_stage.ensure((size_t)nx * ny * nz));
+      rc = stage_host_mask(c, masks[i], nx, ny, nz, s, &cy, &cz, org);
+      if (rc) { note(rc); continue; }
       dm = c->mask_stage.p;
     }
     pend[k] = Pending{};
     const double ts = host_prof_on() ? wall_ms() : 0.0;
-    rc = start_roi(c, dm, nx, ny, nz, sp, s, 0, 1, nullptr, 0, &pend[k]);
+    rc = start_roi(c, dm, cx, cy, cz, sp, s, 0, 1, nullptr, 0, &pend[k], org);
     if (host_prof_on()) g_hprof.start += wall_ms() - ts;
     if (rc) { note(rc); continue; }
     idx[k] = i;
@@ -932,6 +988,7 @@ int run_mesh(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
     h.f.cx2 = h.f.cy2 = h.f.cz2 = 0;
     h.f.hx = (float)(0.5 * sp[0]); h.f.hy = (float)(0.5 * sp[1]); h.f.hz = (float)(0.5 * sp[2]);
     h.f.sx = sp[0]; h.f.sy = sp[1]; h.f.sz = sp[2];
+    h.f.ox2 = h.f.oy2 = h.f.oz2 = 0;
     h.wcap = 0;
     CK(cudaMemcpyAsync(c->d_rp, c->h_rp, sizeof(RoiParams), cudaMemcpyHostToDevice, s));
     init_stats<<<1, 256, 0, s>>>(c->d_stats);
@@ -1066,14 +1123,16 @@ int sc_calculate_coefficients(const uint8_t* mask, int64_t nx, int64_t ny, int64
   std::lock_guard<std::mutex> lk(c->mu);
   CK(cudaSetDevice(device));
   std::memset(out, 0, sizeof *out);
-  const size_t bytes = (size_t)nx * ny * nz;
-  CK(c->mask_stage.ensure(bytes));
+  CK(c->mask_stage.ensure((size_t)nx * ny * nz));
   cudaStream_t s = c->stream;
-  CK(cudaEventRecord(c->ev[0], s));
-  CK(cudaMemcpyAsync(c->mask_stage.p, mask, bytes, cudaMemcpyHostToDevice, s));
-  CK(cudaEventRecord(c->ev[1], s));
-  rc = run_roi(c, c->mask_stage.p, nx, ny, nz, spacing, s, 0, 1, nullptr, out);
+  int64_t cy = ny, cz = nz;
+  int org[3] = {0, 0, 0};
+  rc = stage_host_mask(c, mask, nx, ny, nz, s, &cy, &cz, org);
+  if (rc) return rc;
+  rc = run_roi(c, c->mask_stage.p, nx, cy, cz, spacing, s, 0, 1, nullptr, out, org);
   out->h2d_ms = ev_ms(c->ev[0], c->ev[1]);
+  out->h2d_bytes = c->last_h2d_bytes;
+  out->host_scan_ms = c->last_scan_ms;
   c->last_ms[6] = out->h2d_ms;
   out->total_ms = wall_ms() - t0;
   return rc;
@@ -1114,6 +1173,7 @@ int sc_calculate_coefficients_raw(const void* data, int dtype, const int64_t sha
   CK(cudaEventRecord(c->ev[1], s));
   rc = run_roi(c, c->mask_stage.p, nx, ny, nz, spacing, s, 0, 1, nullptr, out);
   out->h2d_ms = ev_ms(c->ev[0], c->ev[1]);
+  out->h2d_bytes = (int64_t)raw_bytes;
   c->last_ms[6] = out->h2d_ms;
   out->total_ms = wall_ms() - t0;
   return rc;
@@ -1276,6 +1336,22 @@ int sc_last_kernel_times(int device, double* ms, int n) {
 
 uint64_t sc_launch_count(void) { return g_launches.load(); }
 
+int sc_occupied_slab(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, int threads,
+                     int64_t out[4]) {
+  if (!mask || !out || nx < 1 || ny < 1 || nz < 1) {
+    set_err("bad mask pointer, output pointer or dims");
+    return SC_ERR_INPUT;
+  }
+  const Slab sl = occupied_slab(mask, nx, ny, nz,
+                                threads > 0 ? threads : g_opt_host_threads.load());
+  if (sl.empty) {
+    set_err("mask has no occupied voxels");
+    return SC_ERR_EMPTY_ROI;
+  }
+  out[0] = sl.z0; out[1] = sl.z1; out[2] = sl.y0; out[3] = sl.y1;
+  return SC_OK;
+}
+
 int sc_last_diagnostics(int device, int64_t* out, int n) {
   Ctx* c;
   int rc = get_ctx(device, &c);
@@ -1295,6 +1371,8 @@ int sc_set_option(const char* name, int value) {
   else if (std::strcmp(name, "dcap") == 0) g_opt_dcap = std::max(256, value);
   else if (std::strcmp(name, "wcap") == 0) g_opt_wcap = std::max(1, value);
   else if (std::strcmp(name, "fused_bbox") == 0) g_opt_fbox = value != 0;
+  else if (std::strcmp(name, "host_crop") == 0) g_opt_crop = value != 0;
+  else if (std::strcmp(name, "host_threads") == 0) g_opt_host_threads = std::max(1, value);
   else if (std::strcmp(name, "debug_stages") == 0) g_opt_stages = value > 0 ? value : (1 << 30);
   else { set_err("unknown option %s", name); return SC_ERR_INPUT; }
   return SC_OK;

@@ -1,0 +1,154 @@
+// Host-side occupied-slab detection (see host_crop.h).  Plain host C++; lives
+// in a .cu file only so the library builds from one nvcc command.
+#include "host_crop.h"
+
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+namespace sc {
+namespace {
+
+// Minimal persistent worker pool: run(n, fn) calls fn(t) for t in [0, n) on the
+// workers and the calling thread, and returns when every call has finished.
+class Pool {
+ public:
+  explicit Pool(int workers) {
+    for (int i = 0; i < workers; i++) th_.emplace_back([this, i] { loop(i); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return (int)th_.size() + 1; }
+
+  void run(int64_t n, int max_threads, const std::function<void(int64_t)>& fn) {
+    std::lock_guard<std::mutex> serial(run_mu_);  // one job at a time
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      n_ = n;
+      next_.store(0);
+      active_ = std::max(0, std::min<int>(max_threads - 1, (int)th_.size()));
+      pending_ = active_;
+      gen_++;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [this] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void work() {
+    for (int64_t t; (t = next_.fetch_add(1)) < n_;) (*fn_)(t);
+  }
+  void loop(int idx) {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        if (idx >= active_) continue;  // not needed for this job
+      }
+      work();
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+
+  std::vector<std::thread> th_;
+  std::mutex mu_, run_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int64_t)>* fn_ = nullptr;
+  std::atomic<int64_t> next_{0};
+  int64_t n_ = 0;
+  int active_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+Pool& pool() {
+  static Pool p(std::max(0, (int)std::thread::hardware_concurrency() - 1));
+  return p;
+}
+
+// Any nonzero byte in p[0, n)?  Word-wide OR over the whole row (vectorisable,
+// no data-dependent exit inside a row: rows are short and mostly background).
+inline bool row_any(const uint8_t* p, int64_t n) {
+  uint64_t acc = 0;
+  int64_t i = 0;
+  for (; i + 32 <= n; i += 32) {
+    uint64_t w[4];
+    std::memcpy(w, p + i, 32);
+    acc |= w[0] | w[1] | w[2] | w[3];
+  }
+  for (; i < n; i++) acc |= p[i];
+  return acc != 0;
+}
+
+}  // namespace
+
+Slab occupied_slab(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, int threads) {
+  struct Part {
+    int64_t z0 = INT64_MAX, z1 = -1, y0 = INT64_MAX, y1 = -1, read = 0;
+  };
+  const int64_t slice = nx * ny;
+  // ~1 MB tasks: enough of them to balance, few enough to keep the counter cold.
+  const int64_t per = std::max<int64_t>(1, (int64_t(1) << 20) / std::max<int64_t>(1, slice));
+  const int64_t ntask = (nz + per - 1) / per;
+  std::vector<Part> parts((size_t)ntask);
+  auto scan = [&](int64_t t) {
+    Part& r = parts[(size_t)t];
+    const int64_t za = t * per, zb = std::min(nz, za + per);
+    for (int64_t z = za; z < zb; z++) {
+      const uint8_t* s = mask + z * slice;
+      int64_t lo = -1;
+      for (int64_t y = 0; y < ny; y++)
+        if (row_any(s + y * nx, nx)) { lo = y; break; }
+      if (lo < 0) { r.read += slice; continue; }
+      int64_t hi = lo;
+      for (int64_t y = ny - 1; y > lo; y--)
+        if (row_any(s + y * nx, nx)) { hi = y; break; }
+      r.read += (lo + 1 + (ny - hi)) * nx;
+      r.z0 = std::min(r.z0, z);
+      r.z1 = std::max(r.z1, z);
+      r.y0 = std::min(r.y0, lo);
+      r.y1 = std::max(r.y1, hi);
+    }
+  };
+  const int nt = std::max(1, threads);
+  if (nt == 1 || ntask == 1) {
+    for (int64_t t = 0; t < ntask; t++) scan(t);
+  } else {
+    pool().run(ntask, nt, scan);
+  }
+  Part all;
+  for (const Part& r : parts) {
+    all.z0 = std::min(all.z0, r.z0); all.z1 = std::max(all.z1, r.z1);
+    all.y0 = std::min(all.y0, r.y0); all.y1 = std::max(all.y1, r.y1);
+    all.read += r.read;
+  }
+  Slab out;
+  out.empty = all.z1 < 0;
+  out.z0 = out.empty ? 0 : all.z0;
+  out.z1 = out.empty ? -1 : all.z1;
+  out.y0 = out.empty ? 0 : all.y0;
+  out.y1 = out.empty ? -1 : all.y1;
+  out.bytes_read = all.read;
+  return out;
+}
+
+}  // namespace sc

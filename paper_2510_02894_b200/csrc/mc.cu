@@ -193,7 +193,6 @@ __device__ __forceinline__ unsigned long long window(const uint32_t* __restrict_
   return (cur << 1) | (prev >> 31);
 }
 
-constexpr int kZChunk = 4;
 constexpr int kStage = 256;  // staged vertices per warp and z step (denser steps emit directly)
 
 __device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits, int q, int v, int w,
@@ -207,44 +206,27 @@ __device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits, int
   }
 }
 
-// One thread = one (word column q, row v) and kZChunk consecutive z steps.
+// One thread = one (word column q, row v) and KZ consecutive z steps.
 // Cell (u, v, w) has lower corner at unpadded voxel (u, v, w), u,v,w >= -1
 // (reference padded cell index minus 1).  The thread owns cells and lattice
-// points u = 32q - 1 + i, i in [0, 31].  All 2*(kZChunk+1) row words are
+// points u = 32q - 1 + i, i in [0, 31].  All 2*(KZ+1) row words are
 // loaded up front (L2-resident bit volume; latency, not bandwidth, bound).
 //
 // Every emitted vertex is also counted into the histograms the diameter stage
 // sorts by: its 3-D Morton brick (block-private, flushed once per block) and
 // its (plane, in-plane brick) bin in each of its three planes (global).
-__global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__ rp,
-                                                const uint32_t* __restrict__ bits,
-                                                const CaseTables* __restrict__ tabs,
-                                                Stats* __restrict__ st, int4* __restrict__ vkeys,
-                                                long long cap, unsigned int* __restrict__ sort_counts,
-                                                unsigned int* __restrict__ pbin_counts) {
-  __shared__ unsigned int s_hist[kNumCases];
-  __shared__ int4 s_tn[kNumCases];
-  __shared__ unsigned int s_sup[kSortSupers];
-  __shared__ int4 s_stage[256 / 32][kStage];  // per-warp vertex stage (blockDim = 256)
+template <int KZ>
+__device__ __forceinline__ long long mc_body(const RoiParams* __restrict__ rp,
+                                        const uint32_t* __restrict__ bits, Stats* __restrict__ st,
+                                        int4* __restrict__ vkeys, long long cap,
+                                        unsigned int* __restrict__ sort_counts,
+                                        unsigned int* __restrict__ pbin_counts, const int* bb,
+                                        unsigned int* s_hist, const int4* s_tn,
+                                        unsigned int* s_sup, int4 (*s_stage)[kStage]) {
   const int ny = (int)rp->ny, nz = (int)rp->nz, W = rp->W;
-  int bb[6];
-#pragma unroll
-  for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
-  if (bb[3] < 0) return;  // empty ROI (block-uniform)
-  {  // blocks past the bbox's work items have nothing to do: skip the prologue too
-    const long long items = (long long)(((bb[3] + 1) >> 5) - (bb[0] >> 5) + 1) *
-                            (bb[4] - bb[1] + 2) * ((bb[5] - bb[2] + 2 + kZChunk - 1) / kZChunk);
-    if ((long long)blockIdx.x * blockDim.x >= items) return;
-  }
   const PlaneSpace ps = plane_space(bb);
   const PlaneBricks pbk = plane_bricks(bb);
   const int bshift = brick_shift(bb);
-  for (int i = threadIdx.x; i < kNumCases; i += blockDim.x) {
-    s_hist[i] = 0;
-    s_tn[i] = tabs->tn[i];
-  }
-  for (int i = threadIdx.x; i < kSortSupers; i += blockDim.x) s_sup[i] = 0;
-  __syncthreads();
 
   const int xmin = bb[0], ymin = bb[1], zmin = bb[2];
   const int xmax = bb[3], ymax = bb[4], zmax = bb[5];
@@ -255,7 +237,7 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
     const int qlo = xmin >> 5, qhi = (xmax + 1) >> 5;
     const int vlo = ymin - 1, whi = zmax, wlo = zmin - 1;
     const int nq = qhi - qlo + 1, nv = ymax - vlo + 1;
-    const int nzc = (whi - wlo + 1 + kZChunk - 1) / kZChunk;
+    const int nzc = (whi - wlo + 1 + KZ - 1) / KZ;
     const long long n_items = (long long)nq * nv * nzc;
     const long long step = (long long)gridDim.x * blockDim.x;
     for (long long base = (long long)blockIdx.x * blockDim.x; base < n_items; base += step) {
@@ -266,18 +248,18 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
         q = qlo + (int)(item % nq);
         long long r = item / nq;
         v = vlo + (int)(r % nv);
-        w0 = wlo + (int)(r / nv) * kZChunk;
+        w0 = wlo + (int)(r / nv) * KZ;
       }
-      uint32_t c0[kZChunk + 1], p0[kZChunk + 1], c1[kZChunk + 1], p1[kZChunk + 1];
+      uint32_t c0[KZ + 1], p0[KZ + 1], c1[KZ + 1], p1[KZ + 1];
 #pragma unroll
-      for (int s = 0; s <= kZChunk; s++) {
+      for (int s = 0; s <= KZ; s++) {
         const bool on = valid && w0 + s <= whi + 1;
         row_words(bits, q, v, w0 + s, W, ny, nz, on, c0[s], p0[s]);
         row_words(bits, q, v + 1, w0 + s, W, ny, nz, on, c1[s], p1[s]);
       }
       const int xbase = 32 * q - 1;
 #pragma unroll
-      for (int s = 0; s < kZChunk; s++) {
+      for (int s = 0; s < KZ; s++) {
         const int w = w0 + s;
         const bool on = valid && w <= whi;
         const unsigned long long A = ((unsigned long long)c0[s] << 1) | (p0[s] >> 31);
@@ -393,6 +375,50 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
       }
     }
   }
+  return volk;
+}
+
+__global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__ rp,
+                                                const uint32_t* __restrict__ bits,
+                                                const CaseTables* __restrict__ tabs,
+                                                Stats* __restrict__ st, int4* __restrict__ vkeys,
+                                                long long cap, unsigned int* __restrict__ sort_counts,
+                                                unsigned int* __restrict__ pbin_counts) {
+  __shared__ unsigned int s_hist[kNumCases];
+  __shared__ int4 s_tn[kNumCases];
+  __shared__ unsigned int s_sup[kSortSupers];
+  __shared__ int4 s_stage[256 / 32][kStage];  // per-warp vertex stage (blockDim = 256)
+  int bb[6];
+#pragma unroll
+  for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
+  if (bb[3] < 0) return;  // empty ROI (block-uniform)
+  // z steps per thread, chosen per ROI from the bbox: 4 when the bbox gives
+  // every resident thread an item (fewer row loads per step), 1 or 2 for small
+  // bboxes, where parallelism -- not loads -- is the limit (C2: ~22 K items at
+  // depth 4 for ~150 K resident threads).
+  const long long cols = (long long)(((bb[3] + 1) >> 5) - (bb[0] >> 5) + 1) * (bb[4] - bb[1] + 2);
+  const int zs = bb[5] - bb[2] + 2;
+  const long long threads = (long long)gridDim.x * blockDim.x;
+  const int kz = cols * ((zs + 3) / 4) >= threads ? 4 : (cols * ((zs + 1) / 2) >= threads ? 2 : 1);
+  // blocks past the bbox's work items have nothing to do: skip the prologue too
+  if ((long long)blockIdx.x * blockDim.x >= cols * ((zs + kz - 1) / kz)) return;
+  for (int i = threadIdx.x; i < kNumCases; i += blockDim.x) {
+    s_hist[i] = 0;
+    s_tn[i] = tabs->tn[i];
+  }
+  for (int i = threadIdx.x; i < kSortSupers; i += blockDim.x) s_sup[i] = 0;
+  __syncthreads();
+  long long volk;
+  if (kz == 4)
+    volk = mc_body<4>(rp, bits, st, vkeys, cap, sort_counts, pbin_counts, bb, s_hist, s_tn, s_sup,
+                      s_stage);
+  else if (kz == 2)
+    volk = mc_body<2>(rp, bits, st, vkeys, cap, sort_counts, pbin_counts, bb, s_hist, s_tn, s_sup,
+                      s_stage);
+  else
+    volk = mc_body<1>(rp, bits, st, vkeys, cap, sort_counts, pbin_counts, bb, s_hist, s_tn, s_sup,
+                      s_stage);
+  const int lane = threadIdx.x & 31;
   // Block flush: exact integer partials.
 #pragma unroll
   for (int o = 16; o; o >>= 1) volk += __shfl_xor_sync(kFull, volk, o);
@@ -405,6 +431,7 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
     for (int i = threadIdx.x; i < kSortSupers; i += blockDim.x)
       if (s_sup[i]) atomicAdd(&sort_counts[kSortBins + i], s_sup[i]);
 }
+
 
 template __global__ void pack_bits_v16<4, false>(const RoiParams*, uint32_t*, Stats*);
 template __global__ void pack_bits_v16<4, true>(const RoiParams*, uint32_t*, Stats*);

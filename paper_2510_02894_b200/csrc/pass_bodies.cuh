@@ -179,15 +179,15 @@ __device__ __forceinline__ void refine_3d(const int4* __restrict__ keys, long lo
       if (threadIdx.x < kChunk) {
         const long long j = (long long)J * kChunk + threadIdx.x;
         const int4 kj = keys[j < n ? j : n - 1];
-        sx[threadIdx.x] = ref_coord(kj.x, f.sx);
-        sy[threadIdx.x] = ref_coord(kj.y, f.sy);
-        sz[threadIdx.x] = ref_coord(kj.z, f.sz);
+        sx[threadIdx.x] = ref_coord(kj.x + f.ox2, f.sx);
+        sy[threadIdx.x] = ref_coord(kj.y + f.oy2, f.sy);
+        sz[threadIdx.x] = ref_coord(kj.z + f.oz2, f.sz);
       }
       __syncthreads();
       const long long i = (long long)I * kChunk + ti;
       if (i < n) {
         const int4 ki = keys[i];
-        const double xi = ref_coord(ki.x, f.sx), yi = ref_coord(ki.y, f.sy), zi = ref_coord(ki.z, f.sz);
+        const double xi = ref_coord(ki.x + f.ox2, f.sx), yi = ref_coord(ki.y + f.oy2, f.sy), zi = ref_coord(ki.z + f.oz2, f.sz);
 #pragma unroll 4
         for (int t = tj; t < tj + kJ; t++)
           best = fmax(best, ref_sq_dist(xi, yi, zi, sx[t], sy[t], sz[t]));
@@ -336,14 +336,14 @@ __device__ __forceinline__ void refine_planar(const int2* __restrict__ sorted,
       __syncthreads();  // previous candidate is done with sa/sb/s_red
       if (threadIdx.x < kPC && J * kPC + threadIdx.x < np) {
         const int2 k = sorted[b0 + J * kPC + threadIdx.x];
-        sa[threadIdx.x] = ref_coord(k.x, ax.sa);
-        sb[threadIdx.x] = ref_coord(k.y, ax.sb);
+        sa[threadIdx.x] = ref_coord(k.x + ax.oa, ax.sa);
+        sb[threadIdx.x] = ref_coord(k.y + ax.ob, ax.sb);
       }
       __syncthreads();
       double best = 0.0;
       if (i < np) {
         const int2 k = sorted[b0 + i];
-        const double ai = ref_coord(k.x, ax.sa), bi = ref_coord(k.y, ax.sb);
+        const double ai = ref_coord(k.x + ax.oa, ax.sa), bi = ref_coord(k.y + ax.ob, ax.sb);
         const unsigned int te = min(jn, (unsigned int)(tj + kJ));
         for (unsigned int t = tj; t < te; t++) {
           const double da = __dsub_rn(sa[t], ai), db = __dsub_rn(sb[t], bi);

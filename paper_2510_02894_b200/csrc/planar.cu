@@ -188,8 +188,8 @@ __global__ void plane_lb(const int2* __restrict__ sorted, const unsigned int* __
       j += i + 1;
       const int2 ki = sorted[b0 + (unsigned int)(pext[(long long)p * 8 + i] & 0xffffffffu)];
       const int2 kj = sorted[b0 + (unsigned int)(pext[(long long)p * 8 + j] & 0xffffffffu)];
-      const double da = __dsub_rn(ref_coord(kj.x, ax.sa), ref_coord(ki.x, ax.sa));
-      const double db = __dsub_rn(ref_coord(kj.y, ax.sb), ref_coord(ki.y, ax.sb));
+      const double da = __dsub_rn(ref_coord(kj.x + ax.oa, ax.sa), ref_coord(ki.x + ax.oa, ax.sa));
+      const double db = __dsub_rn(ref_coord(kj.y + ax.ob, ax.sb), ref_coord(ki.y + ax.ob, ax.sb));
       best = __dadd_rn(__dmul_rn(da, da), __dmul_rn(db, db));
     }
 #pragma unroll

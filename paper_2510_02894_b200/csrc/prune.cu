@@ -280,9 +280,9 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
   if (threadIdx.x < 2 * kNDir) {
     const unsigned int idx = (unsigned int)(st->ext[threadIdx.x] & 0xffffffffu);
     const int4 k = keys[idx < n ? idx : n - 1];
-    px[threadIdx.x] = ref_coord(k.x, f.sx);
-    py[threadIdx.x] = ref_coord(k.y, f.sy);
-    pz[threadIdx.x] = ref_coord(k.z, f.sz);
+    px[threadIdx.x] = ref_coord(k.x + f.ox2, f.sx);
+    py[threadIdx.x] = ref_coord(k.y + f.oy2, f.sy);
+    pz[threadIdx.x] = ref_coord(k.z + f.oz2, f.sz);
   }
   __syncthreads();
   double lb = 0.0;

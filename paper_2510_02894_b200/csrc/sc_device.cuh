@@ -44,6 +44,8 @@ struct CaseTables {
 struct Frame {
   int cx2, cy2, cz2;   // bbox centre in doubled lattice units (xmin + xmax, ...)
   float hx, hy, hz;    // fp32(0.5 * spacing)
+  int ox2, oy2, oz2;   // doubled origin of the (host-cropped) volume in the full grid:
+                       // reference coordinates use key + o*2 (0 when uncropped)
   double sx, sy, sz;   // spacing (fp64, reference arithmetic)
 };
 
@@ -258,6 +260,7 @@ __device__ __forceinline__ PlaneSpace plane_space(const Stats* st) {
 struct PlaneAxes {  // in-plane (a, b) coordinate frame of one plane family
   int ca, cb;       // centre, doubled units
   float ha, hb;     // fp32 half spacings
+  int oa, ob;       // doubled origin offsets (Frame::ox2 ...)
   double sa, sb;    // fp64 spacings
 };
 
@@ -266,10 +269,13 @@ __device__ __forceinline__ PlaneAxes plane_axes(int axis, const Stats* st, const
   PlaneAxes x;
   if (axis == 0) {         // XY plane: (X, Y)
     x.ca = bb[0] + bb[3]; x.cb = bb[1] + bb[4]; x.ha = f.hx; x.hb = f.hy; x.sa = f.sx; x.sb = f.sy;
+    x.oa = f.ox2; x.ob = f.oy2;
   } else if (axis == 1) {  // XZ plane: (X, Z)
     x.ca = bb[0] + bb[3]; x.cb = bb[2] + bb[5]; x.ha = f.hx; x.hb = f.hz; x.sa = f.sx; x.sb = f.sz;
+    x.oa = f.ox2; x.ob = f.oz2;
   } else {                 // YZ plane: (Y, Z)
     x.ca = bb[1] + bb[4]; x.cb = bb[2] + bb[5]; x.ha = f.hy; x.hb = f.hz; x.sa = f.sy; x.sb = f.sz;
+    x.oa = f.oy2; x.ob = f.oz2;
   }
   return x;
 }

@@ -71,6 +71,8 @@ class Coefficients(ShapeFeatures):
     mesh_ms: float = 0.0
     diameters_ms: float = 0.0
     total_ms: float = 0.0
+    h2d_bytes: int = 0  # host entries: bytes of the occupied slab copied H2D
+    host_scan_ms: float = 0.0  # host scan that found the slab
 
 
 def _from_struct(c: _native.ScCoeffs) -> Coefficients:
@@ -88,6 +90,8 @@ def _from_struct(c: _native.ScCoeffs) -> Coefficients:
         mesh_ms=c.mesh_ms,
         diameters_ms=c.diameters_ms,
         total_ms=c.total_ms,
+        h2d_bytes=int(c.h2d_bytes),
+        host_scan_ms=c.host_scan_ms,
     )
 
 

@@ -37,7 +37,7 @@ def test_library_exports_header(native):
     for name in names:
         assert hasattr(lib, name), name
     assert set(names) == set(native.EXPORTED)
-    assert lib.sc_abi_version() == 1
+    assert lib.sc_abi_version() == 2
 
 
 def test_nm_shows_c_symbols(native):
@@ -49,7 +49,7 @@ def test_nm_shows_c_symbols(native):
 
 def test_struct_layout_matches_header(native):
     # 6 doubles, 3 int64, 4 doubles
-    assert ctypes.sizeof(native.ScCoeffs) == 13 * 8
+    assert ctypes.sizeof(native.ScCoeffs) == 15 * 8
     src = open(os.path.join(ROOT, "include", "shapecore_b200.h")).read()
     body = src[src.index("typedef struct {"):src.index("} sc_coeffs;")]
     fields = re.findall(r"(double|int64_t)\s+(\w+);", body)
@@ -124,3 +124,29 @@ def test_tables_header_matches_reference():
     for name in ("EDGE_AXIS", "EDGE_DX", "EDGE_DY", "EDGE_DZ"):
         vals = re.search(rf"SC_{name}\[12\] = \{{([-0-9,]+)\}}", hdr).group(1)
         assert [int(v) for v in vals.split(",")] == getattr(mod, name).tolist()
+
+
+def test_occupied_slab_host_scan(native):
+    """The host scan behind option host_crop (no device needed) finds the exact
+    occupied z/y extent, with any thread count, odd row lengths included."""
+    rng = np.random.default_rng(5)
+    for trial in range(40):
+        nz, ny, nx = (int(v) for v in rng.integers(1, 40, 3))
+        if trial % 5 == 0:
+            nx = int(rng.integers(100, 700))  # rows longer than one 32-byte step
+        arr = np.zeros((nz, ny, nx), dtype=np.uint8)
+        if trial % 7 == 0:
+            for t in (1, 3):
+                assert native.occupied_slab(arr, threads=t) is None
+            continue
+        k = int(rng.integers(1, 6))
+        idx = (rng.integers(0, nz, k), rng.integers(0, ny, k), rng.integers(0, nx, k))
+        arr[idx] = rng.integers(1, 256, k).astype(np.uint8)
+        zs, ys = np.nonzero(arr.any(axis=2))
+        want = (zs.min(), zs.max(), ys.min(), ys.max())
+        for t in (1, 2, 7, 0):
+            assert native.occupied_slab(arr, threads=t) == tuple(int(v) for v in want)
+    big = np.zeros((600, 64, 512), dtype=np.uint8)
+    big[300, 40, 511] = 1
+    big[17, 3, 0] = 9
+    assert native.occupied_slab(big, threads=8) == (17, 300, 3, 40)

@@ -412,3 +412,60 @@ def test_mesh_dump_formats(sc, tmp_path, cuda_device):
     assert lines[0] == "OFF" and lines[1] == "6 8 0" and len(lines) == 2 + 6 + 8
     sc.mesh_dump(mesh, tmp_path / "m.stl")
     assert (tmp_path / "m.stl").stat().st_size == 84 + 50 * 8
+
+
+def _offset_blobs(seed):
+    """Small occupied regions far from the grid origin (large slab offsets) at
+    spacings whose fp64 coordinates round differently at different offsets."""
+    rng = np.random.default_rng(seed)
+    nz, ny, nx = 70, 90, 64 + 8 * seed
+    arr = np.zeros((nz, ny, nx), dtype=np.uint8)
+    for _ in range(3):
+        c = rng.uniform([40, 55, 10], [nz - 6, ny - 6, nx - 10])
+        r = rng.uniform(2, 5, 3)
+        z, y, x = np.ogrid[:nz, :ny, :nx]
+        arr |= (((z - c[0]) / r[0]) ** 2 + ((y - c[1]) / r[1]) ** 2
+                + ((x - c[2]) / r[2]) ** 2 <= 1).astype(np.uint8)
+    arr[nz - 1, ny - 1, nx - 1] = 1  # touches the far grid corner
+    return arr
+
+
+def test_host_crop_is_exact(sc, oracle_mod, cuda_device):
+    """Host entries copy only the occupied z/y slab and add its origin back on
+    the device: results identical to the uncropped copy, to the device-resident
+    entry and to the oracle (diameters bit-exact at odd spacings)."""
+    import torch
+
+    from paper_2510_02894_b200 import _native
+
+    cases = [(_offset_blobs(s), sp) for s, sp in
+             ((0, (0.7, 0.3, 1.3)), (1, (0.1, 0.9, 3.7)), (2, (1.1, 1.1, 0.45)))]
+    cases.append((np.pad(np.ones((1, 1, 1), np.uint8), ((37, 2), (5, 60), (3, 9))),
+                  (0.37, 0.61, 2.9)))
+    try:
+        for arr, sp in cases:
+            cropped = sc.calculate_coefficients(arr, sp, device=cuda_device)
+            z0, z1, y0, y1 = _native.occupied_slab(arr)
+            assert cropped.h2d_bytes == (z1 - z0 + 1) * (y1 - y0 + 1) * arr.shape[2]
+            dev = sc.calculate_coefficients_device(torch.from_numpy(arr).cuda(), sp)
+            _native.set_option("host_crop", 0)
+            full = sc.calculate_coefficients(arr, sp, device=cuda_device)
+            _native.set_option("host_crop", 1)
+            assert full.h2d_bytes == arr.size
+            assert cropped.to_dict() == full.to_dict() == dev.to_dict()
+            assert (cropped.triangle_count, cropped.active_cubes) == \
+                   (full.triangle_count, full.active_cubes)
+            want = oracle_mod.extract_features(arr, sp)
+            rec = cropped.to_dict()
+            for k in DIAM_KEYS:
+                assert rec[k] == want[k], (k, rec[k], want[k])
+            assert cropped.triangle_count == want["triangle_count"]
+            for k in ("MeshVolume", "SurfaceArea"):
+                assert rel_err(rec[k], want[k]) <= 1e-12
+        # the pipelined host batch crops too
+        outs = sc.calculate_coefficients_batch([a for a, _ in cases], [s for _, s in cases],
+                                               device=cuda_device)
+        for (arr, sp), o in zip(cases, outs):
+            assert o.to_dict() == sc.calculate_coefficients(arr, sp).to_dict()
+    finally:
+        _native.set_option("host_crop", 1)
