@@ -159,7 +159,11 @@ int sc_last_diagnostics(int device, int64_t* out, int n);
  * "graphs" (1) = replay each ROI pipeline as a cached CUDA graph; "slots" (8)
  * = pipeline slots (stream + scratch) the batch entries keep in flight;
  * "host_crop" (1) = host-mask entries copy only the occupied z/y slab;
- * "host_threads" (hardware threads, <= 32) = threads of the host slab scan.
+ * "host_threads" (hardware threads, <= 32) = threads of the host slab scan;
+ * "grid_div" (2) = divisor of the per-ROI kernels' grids (SMs x blocks/SM):
+ * fewer resident blocks per ROI let more ROIs share the GPU;
+ * "batch_stage_times" (0) = per-stage CUDA events in batch graphs (mesh_ms /
+ * diameters_ms of batch results are 0 without them).
  * Results are identical either way; 0 on success, SC_ERR_INPUT otherwise. */
 int sc_set_option(const char* name, int value);
 uint64_t sc_launch_count(void);

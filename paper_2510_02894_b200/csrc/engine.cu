@@ -96,6 +96,11 @@ std::atomic<bool> g_opt_fbox{false};  // bbox accumulated inside the pack (else 
 std::atomic<int> g_opt_slots{8};  // pipeline slots used by the batch entries
 std::atomic<long long> g_opt_dcap{2LL << 20};  // default diameter-side vertex capacity
 std::atomic<long long> g_opt_wcap{1LL << 20};  // default 3-D work-list capacity (chunk pairs)
+std::atomic<bool> g_opt_batch_times{false};  // per-stage event nodes in batch graphs
+std::atomic<int> g_opt_grid_div{2};  // divisor of the latency-bound kernel grids (2: best measured batch rate)
+std::atomic<int> g_opt_pack_bps{0};  // pack blocks per SM (0 = occupancy limit)  // divisor of the latency-bound kernels' grids
+std::atomic<int> g_opt_pack_mode{0};  // bit 0: one step per pack block; bit 1: low-priority pack;
+                                      // bit 2 (debug): no pack, reuse the slot's bit volume
 std::atomic<bool> g_opt_crop{true};  // host entries: copy only the occupied z/y slab (host_crop.h)
 std::atomic<int> g_opt_host_threads{(int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()))};
 std::atomic<unsigned long long> g_launches{0};
@@ -208,6 +213,7 @@ struct Ctx {
   long long cap_floor = 0, dcap_floor = 0, wcap_floor = 0;  // raised by overflow re-runs only
   long long last_diag[6] = {0, 0, 0, 0, 0, 0};
   int occ_pass1 = 1, occ_pass1s = 1, occ_pack = 1, occ_mc = 1;  // blocks/SM
+  int prio_lo = 0, prio_hi = 0;  // stream priority range (least, greatest)
   Stats* d_stats = nullptr;
   Stats* h_stats = nullptr;  // pinned
   RoiParams* d_rp = nullptr;  // per-ROI launch parameters (device)
@@ -239,6 +245,9 @@ struct Ctx {
     long long cap, dcap;
     bool prune, packed, fbox;
     int stages;
+    int packmode;       // pack grid shape / priority (option "pack_mode")
+    int grid_div;       // option "grid_div"
+    bool events;        // per-stage event nodes present
     unsigned long long gen;
     cudaGraphExec_t exec;
     unsigned long long launches;
@@ -246,6 +255,7 @@ struct Ctx {
   std::vector<GraphEntry> graphs;
   unsigned long long gen = 0;  // bumped whenever a scratch buffer moves
   bool capturing = false;      // inside a stream capture of launch_roi
+  bool events_on = true;       // record per-stage events (single calls; batches: option)
 
   unsigned long long fingerprint() const {
     unsigned long long h = 1469598103934665603ull;
@@ -266,7 +276,7 @@ struct Ctx {
 // Two independent pipeline slots per device (stream, events, scratch, graphs):
 // single-ROI calls use slot 0; batch calls alternate slots so the H2D copy and
 // kernels of ROI i+1 overlap the tail and the host round trip of ROI i.
-constexpr int kSlots = 8;
+constexpr int kSlots = 16;
 std::mutex g_ctx_mu;
 std::vector<std::array<std::unique_ptr<Ctx>, kSlots>> g_ctx;
 
@@ -291,7 +301,11 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
       return SC_ERR_CUDA;
     }
     c->sms = prop.multiProcessorCount;
-    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaDeviceGetStreamPriorityRange(&c->prio_lo, &c->prio_hi));
+    // Slot streams run at the greatest priority; the HBM pack is launched at
+    // the least (pack_mode bit 1), so other ROIs' short latency-bound kernels
+    // take SM slots ahead of queued pack blocks.
+    CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, c->prio_hi));
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     for (auto& e : c->kev) CK(cudaEventCreate(&e));
     CK(cudaMalloc(&c->d_stats, sizeof(Stats)));
@@ -366,6 +380,7 @@ constexpr long long kPlaneBinsHost = 256;  // sc_device.cuh kPlaneBins
 // Stage events: inside a capture they must be external event nodes so that
 // graph replays record them (plain records only order the capture).
 cudaError_t record(Ctx* c, cudaEvent_t ev, cudaStream_t s) {
+  if (!c->events_on) return cudaSuccess;  // batch graphs: no stage-event nodes
   return c->capturing ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal)
                       : cudaEventRecord(ev, s);
 }
@@ -425,6 +440,13 @@ int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, lo
   return SC_OK;
 }
 
+// Grid of the latency-bound pipeline kernels: k blocks per SM, divided by the
+// option "grid_div" (fewer blocks = less block-scheduling and prologue work
+// per ROI when several ROIs share the GPU; every kernel is grid-stride).
+int lgrid(const Ctx* c, int k) {
+  return std::max(1, c->sms * k / std::max(1, g_opt_grid_div.load()));
+}
+
 // Enqueue one whole ROI on stream s; no host synchronisation.  Everything
 // ROI-specific (mask pointer, dims, spacing) is read by the kernels from the
 // slot's RoiParams record, so the enqueued sequence -- and a graph captured
@@ -448,22 +470,46 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
     if (++nk >= lim) return SC_OK;
     CK(record(c, c->kev[1], s));
   } else if (fast) {
-    pack_bits_v16<4, false><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(rp, c->bits.p,
-                                                                               c->d_stats);
-    CKL(1);
+    // pack_mode bit 0: one 4 KB step per block (grid covers the slot's largest
+    // mask; extra blocks exit) instead of a persistent grid, so blocks retire
+    // continuously and other streams' kernels interleave; bit 1: low priority.
+    const int pm = g_opt_pack_mode.load();
+    cudaLaunchConfig_t cfg = {};
+    const int pbps = g_opt_pack_bps.load() > 0 ? g_opt_pack_bps.load() : std::max(1, c->occ_pack);
+    cfg.gridDim = dim3((unsigned)(c->sms * pbps));
+    if (pm & 1)
+      cfg.gridDim = dim3((unsigned)std::max<long long>(
+          1, (2 * (long long)c->bits.cap + 256 * 4 - 1) / (256 * 4)));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributePriority;
+    at[0].val.priority = c->prio_lo;
+    cfg.attrs = at;
+    cfg.numAttrs = (pm & 2) ? 1 : 0;
+    if (!(pm & 4)) {  // bit 2 (debug, timing only): reuse the slot's previous bit volume
+      const int pu = (pm >> 3) & 3;  // bits 3-4 (experiment): 16-byte loads in flight per thread
+      if (pu == 1)
+        CK(cudaLaunchKernelEx(&cfg, pack_bits_v16<8, false>, rp, c->bits.p, c->d_stats));
+      else if (pu == 2)
+        CK(cudaLaunchKernelEx(&cfg, pack_bits_v16<16, false>, rp, c->bits.p, c->d_stats));
+      else
+        CK(cudaLaunchKernelEx(&cfg, pack_bits_v16<4, false>, rp, c->bits.p, c->d_stats));
+      CKL(1);
+    }
     if (++nk >= lim) return SC_OK;
     CK(record(c, c->kev[1], s));
-    bits_bbox<<<c->sms * 4, 256, 0, s>>>(rp, reinterpret_cast<const uint4*>(c->bits.p),
+    bits_bbox<<<lgrid(c, 4), 256, 0, s>>>(rp, reinterpret_cast<const uint4*>(c->bits.p),
                                          c->d_stats);
     CKL(1);
     if (++nk >= lim) return SC_OK;
   } else {
-    pack_bits_generic<<<c->sms * 8, 256, 0, s>>>(rp, c->bits.p, c->d_stats);
+    pack_bits_generic<<<lgrid(c, 8), 256, 0, s>>>(rp, c->bits.p, c->d_stats);
     CKL(1);
     if (++nk >= lim) return SC_OK;
     CK(record(c, c->kev[1], s));
   }
-  mc_cells<<<c->sms * std::max(1, c->occ_mc), 256, 0, s>>>(rp, c->bits.p, c->d_tabs, c->d_stats,
+  mc_cells<<<lgrid(c, std::max(1, c->occ_mc)), 256, 0, s>>>(rp, c->bits.p, c->d_tabs, c->d_stats,
                                                           c->keys.p, cap, c->sort_counts.p,
                                                           c->pbin_counts.p);
   CKL(1);
@@ -472,13 +518,13 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
 
   // Persistent grids: exactly the resident blocks, so the static round-robin
   // split of work units is also the load balance.
-  const int pgrid = c->sms * std::max(1, g_opt_packed.load() ? c->occ_pass1 : c->occ_pass1s);
+  const int pgrid = lgrid(c, std::max(1, g_opt_packed.load() ? c->occ_pass1 : c->occ_pass1s));
   const long long pucap = (long long)c->plane_umax.cap;
   const int prune = g_opt_prune.load() ? 1 : 0;
 
   // Orders (Morton bricks; planes by in-plane brick), chunk boxes + extremes,
   // exact lower bound, pruned 3-D work list.
-  plane_bins_scan<<<c->sms * 2, 256, 0, s>>>(c->pbin_counts.p, c->pbin_cursor.p,
+  plane_bins_scan<<<lgrid(c, 2), 256, 0, s>>>(c->pbin_counts.p, c->pbin_cursor.p,
                                              c->plane_counts.p, c->plane_ext.p, c->d_stats);
   CKL(1);
   if (++nk >= lim) return SC_OK;
@@ -488,29 +534,29 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
                                             c->d_stats, c->sboxes.p);
   CKL(1);
   if (++nk >= lim) return SC_OK;
-  scatter_all<<<c->sms * 4, 256, 0, s>>>(c->keys.p, dcap, c->d_stats, c->sort_cursor.p,
+  scatter_all<<<lgrid(c, 4), 256, 0, s>>>(c->keys.p, dcap, c->d_stats, c->sort_cursor.p,
                                          c->keys_sorted.p, c->plane_start.p, c->pbin_cursor.p,
                                          c->plane_sorted.p, c->sort_counts.p + kSortBins);
   CKL(1);
   if (++nk >= lim) return SC_OK;
-  boxes_extremes<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->d_stats, c->boxes.p,
+  boxes_extremes<<<lgrid(c, 2), 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->d_stats, c->boxes.p,
                                             c->sboxes.p);
   CKL(1);
   if (++nk >= lim) return SC_OK;
-  unit_filter<<<c->sms * 4, 256, 0, s>>>(c->keys_sorted.p, c->boxes.p, dcap, rp, prune, shard,
+  unit_filter<<<lgrid(c, 4), 256, 0, s>>>(c->keys_sorted.p, c->boxes.p, dcap, rp, prune, shard,
                                          nshards, c->d_stats, c->work.p, c->sboxes.p);
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[3], s));
-  plane_boxes<<<c->sms * 4, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_cstart.p,
+  plane_boxes<<<lgrid(c, 4), 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_cstart.p,
                                          rp, c->d_stats, c->plane_boxes_buf.p, c->plane_ext.p);
   CKL(1);
   if (++nk >= lim) return SC_OK;
-  plane_lb<<<c->sms, 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_ext.p, rp,
+  plane_lb<<<lgrid(c, 1), 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_ext.p, rp,
                                   c->d_stats);
   CKL(1);
   if (++nk >= lim) return SC_OK;
-  plane_filter<<<c->sms * 4, 256, 0, s>>>(c->plane_start.p, c->plane_tstart.p, c->plane_cstart.p,
+  plane_filter<<<lgrid(c, 4), 256, 0, s>>>(c->plane_start.p, c->plane_tstart.p, c->plane_cstart.p,
                                           c->plane_boxes_buf.p, rp, prune, shard, nshards, pucap,
                                           c->d_stats, c->plane_work.p);
   CKL(1);
@@ -528,7 +574,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[5], s));
-  diam_refine<<<c->sms * 2, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->work.p, c->warp_max.p,
+  diam_refine<<<lgrid(c, 2), 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->work.p, c->warp_max.p,
                                          c->plane_sorted.p, c->plane_start.p, c->plane_work.p,
                                          pucap, c->plane_umax.p, c->d_stats);
   CKL(1);
@@ -641,6 +687,9 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
     if (g.fast == fast && g.s == s && g.shard == shard && g.nshards == nshards &&
         g.d_sq4 == d_sq4 && g.cap == cap && g.dcap == dcap && g.prune == prune &&
         g.packed == packed && g.fbox == fbox && g.stages == g_opt_stages.load() &&
+        g.packmode == g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load() &&
+        g.grid_div == g_opt_grid_div.load() &&
+        g.events == c->events_on &&
         g.gen == c->gen) {
       CK(cudaGraphLaunch(g.exec, s));
       if (hp) g_hprof.launch += wall_ms() - t0;
@@ -667,7 +716,9 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
     c->graphs.erase(c->graphs.begin());
   }
   Ctx::GraphEntry g{fast, s, shard, nshards, d_sq4, cap, dcap, prune, packed, fbox,
-                    g_opt_stages.load(), c->gen, exec, launches};
+                    g_opt_stages.load(), g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load(),
+                    g_opt_grid_div.load(),
+                    c->events_on, c->gen, exec, launches};
   c->graphs.push_back(g);
   CK(cudaGraphLaunch(exec, s));
   g_launches.fetch_add(launches, std::memory_order_relaxed);
@@ -751,7 +802,9 @@ int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
     return SC_ERR_EMPTY_ROI;
   }
   fill_out(*c->h_stats, p->sp, out);
-  c->times_pending = true;  // per-stage times: read from kev[] on demand
+  c->times_pending = c->events_on;  // per-stage times: read from kev[] on demand
+  if (!c->events_on)
+    for (int i = 0; i < 6; i++) c->last_ms[i] = 0.0;
   c->last_ms[6] = 0.0;
   {
     const Stats& h = *c->h_stats;
@@ -763,8 +816,8 @@ int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
     c->last_diag[4] = (long long)h.n_pcand;
     c->last_diag[5] = (long long)h.n_pwork;
   }
-  out->mesh_ms = ev_ms(c->kev[0], c->kev[2]);
-  out->diameters_ms = ev_ms(c->kev[2], c->kev[6]);
+  out->mesh_ms = c->events_on ? ev_ms(c->kev[0], c->kev[2]) : 0.0;
+  out->diameters_ms = c->events_on ? ev_ms(c->kev[2], c->kev[6]) : 0.0;
   return SC_OK;
 }
 
@@ -842,6 +895,13 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
   }
   std::unique_lock<std::mutex> locks[kSlots];
   for (int k = 0; k < nslots; k++) locks[k] = std::unique_lock<std::mutex>(cs[k]->mu);
+  // Batch graphs carry no per-stage event nodes unless asked for (fewer graph
+  // nodes = cheaper launches); the slots go back to single-call mode after.
+  struct EventsMode {
+    Ctx** cs; int n;
+    ~EventsMode() { for (int k = 0; k < n; k++) cs[k]->events_on = true; }
+  } events_mode{cs, nslots};
+  for (int k = 0; k < nslots; k++) cs[k]->events_on = g_opt_batch_times.load();
   CK(cudaSetDevice(device));
   if (user) {  // order the batch after prior work on the caller's stream
     CK(cudaEventRecord(cs[0]->ev[4], user));
@@ -1372,6 +1432,10 @@ int sc_set_option(const char* name, int value) {
   else if (std::strcmp(name, "wcap") == 0) g_opt_wcap = std::max(1, value);
   else if (std::strcmp(name, "fused_bbox") == 0) g_opt_fbox = value != 0;
   else if (std::strcmp(name, "host_crop") == 0) g_opt_crop = value != 0;
+  else if (std::strcmp(name, "pack_mode") == 0) g_opt_pack_mode = value & 31;
+  else if (std::strcmp(name, "pack_bps") == 0) g_opt_pack_bps = std::max(0, value);
+  else if (std::strcmp(name, "grid_div") == 0) g_opt_grid_div = std::max(1, value);
+  else if (std::strcmp(name, "batch_stage_times") == 0) g_opt_batch_times = value != 0;
   else if (std::strcmp(name, "host_threads") == 0) g_opt_host_threads = std::max(1, value);
   else if (std::strcmp(name, "debug_stages") == 0) g_opt_stages = value > 0 ? value : (1 << 30);
   else { set_err("unknown option %s", name); return SC_ERR_INPUT; }

@@ -206,7 +206,10 @@ __device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits, int
   }
 }
 
-// One thread = one (word column q, row v) and KZ consecutive z steps.
+// One thread = one (word column q, row v) and kz <= KZ consecutive z steps
+// (kz is chosen per ROI on the device; steps past kz are predicated off, so
+// one straight-line body serves every depth and the warp intrinsics stay
+// converged -- branching between per-depth bodies made ptxas emulate them).
 // Cell (u, v, w) has lower corner at unpadded voxel (u, v, w), u,v,w >= -1
 // (reference padded cell index minus 1).  The thread owns cells and lattice
 // points u = 32q - 1 + i, i in [0, 31].  All 2*(KZ+1) row words are
@@ -216,7 +219,7 @@ __device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits, int
 // sorts by: its 3-D Morton brick (block-private, flushed once per block) and
 // its (plane, in-plane brick) bin in each of its three planes (global).
 template <int KZ>
-__device__ __forceinline__ long long mc_body(const RoiParams* __restrict__ rp,
+__device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict__ rp,
                                         const uint32_t* __restrict__ bits, Stats* __restrict__ st,
                                         int4* __restrict__ vkeys, long long cap,
                                         unsigned int* __restrict__ sort_counts,
@@ -232,12 +235,39 @@ __device__ __forceinline__ long long mc_body(const RoiParams* __restrict__ rp,
   const int xmax = bb[3], ymax = bb[4], zmax = bb[5];
   long long volk = 0;
   const int lane = threadIdx.x & 31;
+  // Warp-private vertex stage (warp-uniform fill level), see the emission.
+  uint32_t staged = 0;
+  auto flush = [&]() {
+    __syncwarp();
+    unsigned long long wbase = 0;
+    if (lane == 0) wbase = atomicAdd(&st->n_vert, (unsigned long long)staged);
+    wbase = __shfl_sync(kFull, wbase, 0);
+    const int4* stg = s_stage[threadIdx.x >> 5];
+    for (uint32_t k0 = 0; k0 < staged; k0 += 32) {
+      const uint32_t k = k0 + lane;
+      const bool ok = k < staged;
+      const int4 key = stg[ok ? k : 0];
+      const long long g = (long long)wbase + k;
+      if (ok && g < cap) vkeys[g] = key;
+      const unsigned int bin = brick_bin(key.x, key.y, key.z, bb, bshift);
+      group_add(sort_counts, bin, ok);
+      if (ok) atomicAdd(&s_sup[bin >> kSortSliceBits], 1u);
+      int id[3];
+      unsigned int pbin[3];
+      plane_ids(key.x, key.y, key.z, ps, id);
+      plane_bins(key.x, key.y, key.z, pbk, pbin);
+#pragma unroll
+      for (int a2 = 0; a2 < 3; a2++)
+        group_add(pbin_counts, (unsigned int)id[a2] * kPlaneBins + pbin[a2], ok);
+    }
+    __syncwarp();  // the stage is refilled next
+  };
   if (xmax >= 0) {
     // Points/cells that can be crossed or active: [min-1, max] on every axis.
     const int qlo = xmin >> 5, qhi = (xmax + 1) >> 5;
     const int vlo = ymin - 1, whi = zmax, wlo = zmin - 1;
     const int nq = qhi - qlo + 1, nv = ymax - vlo + 1;
-    const int nzc = (whi - wlo + 1 + KZ - 1) / KZ;
+    const int nzc = (whi - wlo + 1 + kz - 1) / kz;
     const long long n_items = (long long)nq * nv * nzc;
     const long long step = (long long)gridDim.x * blockDim.x;
     for (long long base = (long long)blockIdx.x * blockDim.x; base < n_items; base += step) {
@@ -248,12 +278,12 @@ __device__ __forceinline__ long long mc_body(const RoiParams* __restrict__ rp,
         q = qlo + (int)(item % nq);
         long long r = item / nq;
         v = vlo + (int)(r % nv);
-        w0 = wlo + (int)(r / nv) * KZ;
+        w0 = wlo + (int)(r / nv) * kz;
       }
       uint32_t c0[KZ + 1], p0[KZ + 1], c1[KZ + 1], p1[KZ + 1];
 #pragma unroll
       for (int s = 0; s <= KZ; s++) {
-        const bool on = valid && w0 + s <= whi + 1;
+        const bool on = valid && s <= kz && w0 + s <= whi + 1;
         row_words(bits, q, v, w0 + s, W, ny, nz, on, c0[s], p0[s]);
         row_words(bits, q, v + 1, w0 + s, W, ny, nz, on, c1[s], p1[s]);
       }
@@ -261,6 +291,7 @@ __device__ __forceinline__ long long mc_body(const RoiParams* __restrict__ rp,
 #pragma unroll
       for (int s = 0; s < KZ; s++) {
         const int w = w0 + s;
+        if (s >= kz) break;  // block-uniform
         const bool on = valid && w <= whi;
         const unsigned long long A = ((unsigned long long)c0[s] << 1) | (p0[s] >> 31);
         const unsigned long long B = ((unsigned long long)c1[s] << 1) | (p1[s] >> 31);
@@ -299,16 +330,18 @@ __device__ __forceinline__ long long mc_body(const RoiParams* __restrict__ rp,
         }
         const uint32_t total = __shfl_sync(kFull, incl, 31);
         if (total) {
-          unsigned long long wbase = 0;
-          if (lane == 31) wbase = atomicAdd(&st->n_vert, (unsigned long long)total);
-          wbase = __shfl_sync(kFull, wbase, 31);
           const int Y2 = 2 * v, Z2 = 2 * w;
           if (pbin_counts && total <= kStage) {
             // Stage the step's vertices in shared memory (cheap per-lane
-            // loop), then bin and store them with all 32 lanes converged:
-            // coalesced key stores, warp-aggregated histogram atomics.
+            // loop); the stage accumulates over steps and is flushed -- one
+            // global reservation, coalesced key stores, converged binning --
+            // only when the next step would not fit (or at the end).
+            if (staged + total > kStage) {
+              flush();
+              staged = 0;
+            }
             int4* stg = s_stage[threadIdx.x >> 5];
-            uint32_t o = incl - c;
+            uint32_t o = staged + incl - c;
             while (ex) {
               const int i = __ffs(ex) - 1; ex &= ex - 1;
               stg[o++] = make_int4(2 * (xbase + i) + 1, Y2, Z2, 0);
@@ -321,26 +354,11 @@ __device__ __forceinline__ long long mc_body(const RoiParams* __restrict__ rp,
               const int i = __ffs(ez) - 1; ez &= ez - 1;
               stg[o++] = make_int4(2 * (xbase + i), Y2, Z2 + 1, 0);
             }
-            __syncwarp();
-            for (uint32_t k0 = 0; k0 < total; k0 += 32) {
-              const uint32_t k = k0 + lane;
-              const bool ok = k < total;
-              const int4 key = stg[ok ? k : 0];
-              const long long g = (long long)wbase + k;
-              if (ok && g < cap) vkeys[g] = key;
-              const unsigned int bin = brick_bin(key.x, key.y, key.z, bb, bshift);
-              group_add(sort_counts, bin, ok);
-              if (ok) atomicAdd(&s_sup[bin >> kSortSliceBits], 1u);
-              int id[3];
-              unsigned int pbin[3];
-              plane_ids(key.x, key.y, key.z, ps, id);
-              plane_bins(key.x, key.y, key.z, pbk, pbin);
-#pragma unroll
-              for (int a2 = 0; a2 < 3; a2++)
-                group_add(pbin_counts, (unsigned int)id[a2] * kPlaneBins + pbin[a2], ok);
-            }
-            __syncwarp();  // the stage is rewritten by the next step
+            staged += total;
           } else {
+            unsigned long long wbase = 0;
+            if (lane == 31) wbase = atomicAdd(&st->n_vert, (unsigned long long)total);
+            wbase = __shfl_sync(kFull, wbase, 31);
             long long o = (long long)(wbase + incl - c);
             auto emit = [&](int X, int Y, int Z) {
               if (o < cap) vkeys[o] = make_int4(X, Y, Z, 0);
@@ -375,6 +393,7 @@ __device__ __forceinline__ long long mc_body(const RoiParams* __restrict__ rp,
       }
     }
   }
+  if (staged) flush();
   return volk;
 }
 
@@ -408,16 +427,8 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
   }
   for (int i = threadIdx.x; i < kSortSupers; i += blockDim.x) s_sup[i] = 0;
   __syncthreads();
-  long long volk;
-  if (kz == 4)
-    volk = mc_body<4>(rp, bits, st, vkeys, cap, sort_counts, pbin_counts, bb, s_hist, s_tn, s_sup,
-                      s_stage);
-  else if (kz == 2)
-    volk = mc_body<2>(rp, bits, st, vkeys, cap, sort_counts, pbin_counts, bb, s_hist, s_tn, s_sup,
-                      s_stage);
-  else
-    volk = mc_body<1>(rp, bits, st, vkeys, cap, sort_counts, pbin_counts, bb, s_hist, s_tn, s_sup,
-                      s_stage);
+  long long volk = mc_body<4>(kz, rp, bits, st, vkeys, cap, sort_counts, pbin_counts, bb, s_hist,
+                              s_tn, s_sup, s_stage);
   const int lane = threadIdx.x & 31;
   // Block flush: exact integer partials.
 #pragma unroll
@@ -434,6 +445,8 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
 
 
 template __global__ void pack_bits_v16<4, false>(const RoiParams*, uint32_t*, Stats*);
+template __global__ void pack_bits_v16<8, false>(const RoiParams*, uint32_t*, Stats*);
+template __global__ void pack_bits_v16<16, false>(const RoiParams*, uint32_t*, Stats*);
 template __global__ void pack_bits_v16<4, true>(const RoiParams*, uint32_t*, Stats*);
 
 }  // namespace sc
