@@ -193,7 +193,16 @@ __device__ __forceinline__ unsigned long long window(const uint32_t* __restrict_
   return (cur << 1) | (prev >> 31);
 }
 
-constexpr int kStage = 256;  // staged vertices per warp and z step (denser steps emit directly)
+constexpr int kStage = 256;
+
+// Raw corner word of a cell (bits: A_i, A_i+1, B_i, B_i+1, C_i, C_i+1, D_i,
+// D_i+1 with A/B = rows (v, w)/(v+1, w), C/D = rows (v, w+1)/(v+1, w+1)) ->
+// reference case: occupancy in corner order 0..7 = (A_i, A_i+1, B_i+1, B_i,
+// C_i, C_i+1, D_i+1, D_i), complemented (bit set = background corner).
+__device__ __forceinline__ int case_of_idx(int idx) {
+  const int occ = (idx & 0x33) | ((idx >> 1) & 0x44) | ((idx << 1) & 0x88);
+  return (~occ) & 0xff;
+}  // staged vertices per warp and z step (denser steps emit directly)
 
 __device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits, int q, int v, int w,
                                           int W, int ny, int nz, bool on, uint32_t& cur,
@@ -305,21 +314,26 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
           const unsigned long long all = A & B & C & D, any = A | B | C | D;
           act = (uint32_t)(~(all & (all >> 1)) & (any | (any >> 1)));
         }
-        // Active cells: case bit c set when corner c is background
-        // (mc_tables.py:10-12, mesh.py:103-128).
+        // Active cells.  The shared histogram and case table are indexed by
+        // the raw corner word idx = A[i..i+1] | B[i..i+1]<<2 | C[..]<<4 |
+        // D[..]<<6 (4 shift-and pairs); case_of_idx() maps it to the
+        // reference case (bit c set when corner c is background,
+        // mc_tables.py:10-12, mesh.py:103-128) at the table load and flush.
+        // The volume terms are summed in 32 bits per step, widened once.
+        int s0 = 0, sx = 0, sy = 0, sz = 0;
         while (act) {
           const int i = __ffs(act) - 1;
           act &= act - 1;
-          uint32_t occ = (uint32_t)((A >> i) & 1) | (uint32_t)(((A >> (i + 1)) & 1) << 1) |
-                         (uint32_t)(((B >> (i + 1)) & 1) << 2) | (uint32_t)(((B >> i) & 1) << 3) |
-                         (uint32_t)(((C >> i) & 1) << 4) | (uint32_t)(((C >> (i + 1)) & 1) << 5) |
-                         (uint32_t)(((D >> (i + 1)) & 1) << 6) | (uint32_t)(((D >> i) & 1) << 7);
-          const int k = (~occ) & 0xff;
-          atomicAdd(&s_hist[k], 1u);
-          const int4 tn = s_tn[k];
-          volk += tn.x + 2ll * ((long long)(xbase + i) * tn.y + (long long)v * tn.z +
-                                (long long)w * tn.w);
+          const uint32_t idx = (uint32_t)((A >> i) & 3) | ((uint32_t)((B >> i) & 3) << 2) |
+                               ((uint32_t)((C >> i) & 3) << 4) | ((uint32_t)((D >> i) & 3) << 6);
+          atomicAdd(&s_hist[idx], 1u);
+          const int4 tn = s_tn[idx];
+          s0 += tn.x;
+          sx += (xbase + i) * tn.y;
+          sy += tn.z;
+          sz += tn.w;
         }
+        volk += s0 + 2ll * ((long long)sx + (long long)v * sy + (long long)w * sz);
         // Vertex emission: warp-aggregated stream compaction of crossed edges.
         const uint32_t c = __popc(ex) + __popc(ey) + __popc(ez);
         uint32_t incl = c;
@@ -423,7 +437,7 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
   if ((long long)blockIdx.x * blockDim.x >= cols * ((zs + kz - 1) / kz)) return;
   for (int i = threadIdx.x; i < kNumCases; i += blockDim.x) {
     s_hist[i] = 0;
-    s_tn[i] = tabs->tn[i];
+    s_tn[i] = tabs->tn[case_of_idx(i)];
   }
   for (int i = threadIdx.x; i < kSortSupers; i += blockDim.x) s_sup[i] = 0;
   __syncthreads();
@@ -437,7 +451,7 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
                                    (unsigned long long)volk);
   __syncthreads();
   for (int i = threadIdx.x; i < kNumCases; i += blockDim.x)
-    if (s_hist[i]) atomicAdd(&st->hist[i], (unsigned long long)s_hist[i]);
+    if (s_hist[i]) atomicAdd(&st->hist[case_of_idx(i)], (unsigned long long)s_hist[i]);
   if (sort_counts)
     for (int i = threadIdx.x; i < kSortSupers; i += blockDim.x)
       if (s_sup[i]) atomicAdd(&sort_counts[kSortBins + i], s_sup[i]);
