@@ -97,6 +97,7 @@ std::atomic<int> g_opt_slots{8};  // pipeline slots used by the batch entries
 std::atomic<long long> g_opt_dcap{2LL << 20};  // default diameter-side vertex capacity
 std::atomic<long long> g_opt_wcap{1LL << 20};  // default 3-D work-list capacity (chunk pairs)
 std::atomic<bool> g_opt_batch_times{false};  // per-stage event nodes in batch graphs
+std::atomic<bool> g_opt_pdl{false};  // programmatic dependent launch in batch graphs
 std::atomic<int> g_opt_grid_div{2};  // divisor of the latency-bound kernel grids (2: best measured batch rate)
 std::atomic<int> g_opt_pack_bps{0};  // pack blocks per SM (0 = occupancy limit)  // divisor of the latency-bound kernels' grids
 std::atomic<int> g_opt_pack_mode{0};  // bit 0: one step per pack block; bit 1: low-priority pack;
@@ -248,6 +249,7 @@ struct Ctx {
     int packmode;       // pack grid shape / priority (option "pack_mode")
     int grid_div;       // option "grid_div"
     bool events;        // per-stage event nodes present
+    bool pdl;           // option "pdl"
     unsigned long long gen;
     cudaGraphExec_t exec;
     unsigned long long launches;
@@ -447,6 +449,25 @@ int lgrid(const Ctx* c, int k) {
   return std::max(1, c->sms * k / std::max(1, g_opt_grid_div.load()));
 }
 
+// Launch of a per-ROI pipeline kernel.  In batch graphs (no stage-event nodes
+// between the kernels) it carries the programmatic-dependent-launch attribute
+// (option "pdl"): the kernel is scheduled while its predecessor drains and
+// waits on griddepcontrol.wait (pdl_enter) for the predecessor's results.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(const Ctx* c, cudaStream_t s, int grid, int block, void (*k)(KArgs...),
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (g_opt_pdl.load() && !c->events_on) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 // Enqueue one whole ROI on stream s; no host synchronisation.  Everything
 // ROI-specific (mask pointer, dims, spacing) is read by the kernels from the
 // slot's RoiParams record, so the enqueued sequence -- and a graph captured
@@ -499,19 +520,19 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
     }
     if (++nk >= lim) return SC_OK;
     CK(record(c, c->kev[1], s));
-    bits_bbox<<<lgrid(c, 4), 256, 0, s>>>(rp, reinterpret_cast<const uint4*>(c->bits.p),
-                                         c->d_stats);
+    CK(launch_k(c, s, lgrid(c, 4), 256, bits_bbox, rp, reinterpret_cast<const uint4*>(c->bits.p),
+                                         c->d_stats));
     CKL(1);
     if (++nk >= lim) return SC_OK;
   } else {
-    pack_bits_generic<<<lgrid(c, 8), 256, 0, s>>>(rp, c->bits.p, c->d_stats);
+    pack_bits_generic<<<lgrid(c, 8), 256, 0, s>>>(rp, c->bits.p, c->d_stats);  // after init_stats: no PDL
     CKL(1);
     if (++nk >= lim) return SC_OK;
     CK(record(c, c->kev[1], s));
   }
-  mc_cells<<<lgrid(c, std::max(1, c->occ_mc)), 256, 0, s>>>(rp, c->bits.p, c->d_tabs, c->d_stats,
+  CK(launch_k(c, s, lgrid(c, std::max(1, c->occ_mc)), 256, mc_cells, rp, c->bits.p, c->d_tabs, c->d_stats,
                                                           c->keys.p, cap, c->sort_counts.p,
-                                                          c->pbin_counts.p);
+                                                          c->pbin_counts.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[2], s));
@@ -524,59 +545,59 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
 
   // Orders (Morton bricks; planes by in-plane brick), chunk boxes + extremes,
   // exact lower bound, pruned 3-D work list.
-  plane_bins_scan<<<lgrid(c, 2), 256, 0, s>>>(c->pbin_counts.p, c->pbin_cursor.p,
-                                             c->plane_counts.p, c->plane_ext.p, c->d_stats);
+  CK(launch_k(c, s, lgrid(c, 2), 256, plane_bins_scan, c->pbin_counts.p, c->pbin_cursor.p,
+                                             c->plane_counts.p, c->plane_ext.p, c->d_stats));
   CKL(1);
   if (++nk >= lim) return SC_OK;
-  scan_all<<<kSortSupers + 1, 1024, 0, s>>>(c->sort_counts.p, c->sort_cursor.p,
+  CK(launch_k(c, s, kSortSupers + 1, 1024, scan_all, c->sort_counts.p, c->sort_cursor.p,
                                             c->plane_counts.p, c->plane_start.p,
                                             c->plane_tstart.p, c->plane_cstart.p, dcap,
-                                            c->d_stats, c->sboxes.p);
+                                            c->d_stats, c->sboxes.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
-  scatter_all<<<lgrid(c, 4), 256, 0, s>>>(c->keys.p, dcap, c->d_stats, c->sort_cursor.p,
+  CK(launch_k(c, s, lgrid(c, 4), 256, scatter_all, c->keys.p, dcap, c->d_stats, c->sort_cursor.p,
                                          c->keys_sorted.p, c->plane_start.p, c->pbin_cursor.p,
-                                         c->plane_sorted.p, c->sort_counts.p + kSortBins);
+                                         c->plane_sorted.p, c->sort_counts.p + kSortBins));
   CKL(1);
   if (++nk >= lim) return SC_OK;
-  boxes_extremes<<<lgrid(c, 2), 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->d_stats, c->boxes.p,
-                                            c->sboxes.p);
+  CK(launch_k(c, s, lgrid(c, 2), 256, boxes_extremes, c->keys_sorted.p, dcap, rp, c->d_stats, c->boxes.p,
+                                            c->sboxes.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
-  unit_filter<<<lgrid(c, 4), 256, 0, s>>>(c->keys_sorted.p, c->boxes.p, dcap, rp, prune, shard,
-                                         nshards, c->d_stats, c->work.p, c->sboxes.p);
+  CK(launch_k(c, s, lgrid(c, 4), 256, unit_filter, c->keys_sorted.p, c->boxes.p, dcap, rp, prune, shard,
+                                         nshards, c->d_stats, c->work.p, c->sboxes.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[3], s));
-  plane_boxes<<<lgrid(c, 4), 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_cstart.p,
-                                         rp, c->d_stats, c->plane_boxes_buf.p, c->plane_ext.p);
+  CK(launch_k(c, s, lgrid(c, 4), 256, plane_boxes, c->plane_sorted.p, c->plane_start.p, c->plane_cstart.p,
+                                         rp, c->d_stats, c->plane_boxes_buf.p, c->plane_ext.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
-  plane_lb<<<lgrid(c, 1), 256, 0, s>>>(c->plane_sorted.p, c->plane_start.p, c->plane_ext.p, rp,
-                                  c->d_stats);
+  CK(launch_k(c, s, lgrid(c, 1), 256, plane_lb, c->plane_sorted.p, c->plane_start.p, c->plane_ext.p, rp,
+                                  c->d_stats));
   CKL(1);
   if (++nk >= lim) return SC_OK;
-  plane_filter<<<lgrid(c, 4), 256, 0, s>>>(c->plane_start.p, c->plane_tstart.p, c->plane_cstart.p,
+  CK(launch_k(c, s, lgrid(c, 4), 256, plane_filter, c->plane_start.p, c->plane_tstart.p, c->plane_cstart.p,
                                           c->plane_boxes_buf.p, rp, prune, shard, nshards, pucap,
-                                          c->d_stats, c->plane_work.p);
+                                          c->d_stats, c->plane_work.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[4], s));
   // One pass-1 kernel and one re-check kernel for the 3-D and the planar lists.
   if (g_opt_packed.load())
-    diam_pass1<true><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->work.p, c->warp_max.p,
-                                           c->plane_sorted.p, c->plane_start.p, c->plane_work.p,
-                                           pucap, c->plane_umax.p, c->d_stats);
+    CK(launch_k(c, s, pgrid, 256, diam_pass1<true>, c->keys_sorted.p, dcap, rp, c->work.p,
+                c->warp_max.p, c->plane_sorted.p, c->plane_start.p, c->plane_work.p, pucap,
+                c->plane_umax.p, c->d_stats));
   else
-    diam_pass1<false><<<pgrid, 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->work.p, c->warp_max.p,
+    CK(launch_k(c, s, pgrid, 256, diam_pass1<false>, c->keys_sorted.p, dcap, rp, c->work.p, c->warp_max.p,
                                             c->plane_sorted.p, c->plane_start.p, c->plane_work.p,
-                                            pucap, c->plane_umax.p, c->d_stats);
+                                            pucap, c->plane_umax.p, c->d_stats));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[5], s));
-  diam_refine<<<lgrid(c, 2), 256, 0, s>>>(c->keys_sorted.p, dcap, rp, c->work.p, c->warp_max.p,
+  CK(launch_k(c, s, lgrid(c, 2), 256, diam_refine, c->keys_sorted.p, dcap, rp, c->work.p, c->warp_max.p,
                                          c->plane_sorted.p, c->plane_start.p, c->plane_work.p,
-                                         pucap, c->plane_umax.p, c->d_stats);
+                                         pucap, c->plane_umax.p, c->d_stats));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[6], s));
@@ -689,7 +710,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
         g.packed == packed && g.fbox == fbox && g.stages == g_opt_stages.load() &&
         g.packmode == g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load() &&
         g.grid_div == g_opt_grid_div.load() &&
-        g.events == c->events_on &&
+        g.events == c->events_on && g.pdl == g_opt_pdl.load() &&
         g.gen == c->gen) {
       CK(cudaGraphLaunch(g.exec, s));
       if (hp) g_hprof.launch += wall_ms() - t0;
@@ -718,7 +739,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   Ctx::GraphEntry g{fast, s, shard, nshards, d_sq4, cap, dcap, prune, packed, fbox,
                     g_opt_stages.load(), g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load(),
                     g_opt_grid_div.load(),
-                    c->events_on, c->gen, exec, launches};
+                    c->events_on, g_opt_pdl.load(), c->gen, exec, launches};
   c->graphs.push_back(g);
   CK(cudaGraphLaunch(exec, s));
   g_launches.fetch_add(launches, std::memory_order_relaxed);
@@ -1435,6 +1456,7 @@ int sc_set_option(const char* name, int value) {
   else if (std::strcmp(name, "pack_mode") == 0) g_opt_pack_mode = value & 31;
   else if (std::strcmp(name, "pack_bps") == 0) g_opt_pack_bps = std::max(0, value);
   else if (std::strcmp(name, "grid_div") == 0) g_opt_grid_div = std::max(1, value);
+  else if (std::strcmp(name, "pdl") == 0) g_opt_pdl = value != 0;
   else if (std::strcmp(name, "batch_stage_times") == 0) g_opt_batch_times = value != 0;
   else if (std::strcmp(name, "host_threads") == 0) g_opt_host_threads = std::max(1, value);
   else if (std::strcmp(name, "debug_stages") == 0) g_opt_stages = value > 0 ? value : (1 << 30);

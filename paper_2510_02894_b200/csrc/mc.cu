@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(256) pack_bits_v16(const RoiParams* __restrict
 __global__ void __launch_bounds__(256) bits_bbox(const RoiParams* __restrict__ rp,
                                                  const uint4* __restrict__ bits4,
                                                  Stats* __restrict__ st) {
+  pdl_enter();
   constexpr int kU = 4;
   const long long n_words = rp->n_words;
   const int W = rp->W, ny = (int)rp->ny;
@@ -417,6 +418,7 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
                                                 Stats* __restrict__ st, int4* __restrict__ vkeys,
                                                 long long cap, unsigned int* __restrict__ sort_counts,
                                                 unsigned int* __restrict__ pbin_counts) {
+  pdl_enter();
   __shared__ unsigned int s_hist[kNumCases];
   __shared__ int4 s_tn[kNumCases];
   __shared__ unsigned int s_sup[kSortSupers];

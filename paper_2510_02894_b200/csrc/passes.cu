@@ -13,6 +13,7 @@ __global__ void __launch_bounds__(kDiamThreads, 4) diam_pass1(
     const uint2* __restrict__ work, float* __restrict__ umax, const int2* __restrict__ sorted,
     const unsigned int* __restrict__ start, const uint2* __restrict__ pwork, long long pwcap,
     float* __restrict__ pumax, Stats* __restrict__ st) {
+  pdl_enter();
   if (st->ovf || st->bbox[3] < 0) return;  // re-run pending (scan_all) / empty
   __shared__ float4 sj_all[kWarps][kChunk];  // per-warp J chunk, (x, y, z | -, |p|^2)
   float4* sj = sj_all[threadIdx.x >> 5];
@@ -34,6 +35,7 @@ __global__ void __launch_bounds__(kDiamThreads) diam_refine(
     const int2* __restrict__ sorted, const unsigned int* __restrict__ start,
     const uint2* __restrict__ pwork, long long pwcap, const float* __restrict__ pumax,
     Stats* __restrict__ st) {
+  pdl_enter();
   if (st->ovf || st->bbox[3] < 0) return;  // block-uniform
   __shared__ double s_a[kChunk], s_b[kChunk], s_c[kChunk];
   __shared__ double s_red[kDiamThreads / 32];

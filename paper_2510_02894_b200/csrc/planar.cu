@@ -66,6 +66,7 @@ __global__ void plane_bins_scan(unsigned int* __restrict__ pbin_counts,
                                 unsigned int* __restrict__ plane_counts,
                                 unsigned long long* __restrict__ pext,
                                 const Stats* __restrict__ st) {
+  pdl_enter();
   if (st->bbox[3] < 0) return;
   const PlaneSpace ps = plane_space(st);
   const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
@@ -113,6 +114,7 @@ __global__ void plane_boxes(const int2* __restrict__ sorted,
                             const RoiParams* __restrict__ rp,
                             const Stats* __restrict__ st, int4* __restrict__ pboxes,
                             unsigned long long* __restrict__ pext) {
+  pdl_enter();
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   if (st->bbox[3] < 0) return;
@@ -169,6 +171,7 @@ __global__ void plane_boxes(const int2* __restrict__ sorted,
 __global__ void plane_lb(const int2* __restrict__ sorted, const unsigned int* __restrict__ start,
                          const unsigned long long* __restrict__ pext, const RoiParams* __restrict__ rp,
                          Stats* __restrict__ st) {
+  pdl_enter();
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   if (st->bbox[3] < 0) return;
@@ -220,6 +223,7 @@ __global__ void plane_filter(const unsigned int* __restrict__ start,
                              const int4* __restrict__ pboxes, const RoiParams* __restrict__ rp,
                              int prune, int shard, int nshards, long long wcap,
                              Stats* __restrict__ st, uint2* __restrict__ pwork) {
+  pdl_enter();
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   const long long units = (long long)st->plane_units;

@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(1024) scan_all(unsigned int* __restrict__ sort
                                                  unsigned int* __restrict__ cstart,
                                                  long long dcap, Stats* __restrict__ st,
                                                  int4* __restrict__ sboxes) {
+  pdl_enter();
   int bb[6];
 #pragma unroll
   for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
@@ -135,6 +136,7 @@ __global__ void scatter_all(const int4* __restrict__ keys, long long cap,
                             unsigned int* __restrict__ pbin_cursor,
                             int2* __restrict__ plane_sorted,
                             unsigned int* __restrict__ sort_supers) {
+  pdl_enter();
   // scan_all has consumed the super-bin counts: leave them zeroed for the next ROI.
   if (blockIdx.x == 0) sort_supers[threadIdx.x] = 0u;
   if (st->ovf) return;  // re-run pending (scan_all)
@@ -192,6 +194,7 @@ __global__ void __launch_bounds__(256) boxes_extremes(const int4* __restrict__ k
                                                       Stats* __restrict__ st,
                                                       int4* __restrict__ boxes,
                                                       int4* __restrict__ sboxes) {
+  pdl_enter();
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   __shared__ unsigned long long s_ext[2 * kNDir];
@@ -271,6 +274,7 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
                                                    int shard, int nshards, Stats* __restrict__ st,
                                                    uint2* __restrict__ work,
                                                    const int4* __restrict__ sboxes) {
+  pdl_enter();
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   __shared__ double px[2 * kNDir], py[2 * kNDir], pz[2 * kNDir];

@@ -331,6 +331,16 @@ __device__ __forceinline__ double ref_sq_dist(double xi, double yi, double zi, d
   return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
 }
 
+// Programmatic dependent launch: a pipeline kernel launched with the PDL
+// attribute may start while its predecessor drains; it waits here until the
+// predecessor has completed and its writes are visible (a no-op for a normal
+// launch), then lets its own successor launch early.  Called first thing by
+// every per-ROI kernel after the pack.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Reference vertex coordinate, mesh.py:184-195: (l - 1 + 0.5*[axis]) * s, which
 // in doubled units is (key / 2) * s; key/2 is exact in fp64.
 __device__ __forceinline__ double ref_coord(int key2, double s) {

@@ -259,6 +259,35 @@ def test_pruning_and_pass1_variants_identical(sc, golden, golden_arrays, cuda_de
     assert 0 < d["work_units"] < d["total_units"]  # the KiTS-like ROI actually prunes
 
 
+def test_batch_launch_options_identical(sc, golden, golden_arrays, cuda_device):
+    """Launch-shape options of the batch pipeline (grid divisor, programmatic
+    dependent launch, stage events, slot count, pack grid) never change a
+    result, on device and host batches."""
+    import torch
+
+    from paper_2510_02894_b200 import _native, synth
+
+    cases = [(golden_arrays[c["mask_key"]], c["spacing"]) for c in golden["cases"][:8]]
+    cases.append((synth.thin_slab(), (0.5, 0.5, 5.0)))
+    cases.append((synth.kits_like(tumor_mm=45.0), (0.8, 0.8, 1.0)))
+    want = [sc.calculate_coefficients(a, sp).to_dict() for a, sp in cases]
+    ds = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a, _ in cases]
+    sps = [sp for _, sp in cases]
+    defaults = {"grid_div": 2, "pdl": 0, "batch_stage_times": 0, "slots": 8, "pack_mode": 0}
+    try:
+        for opt, val in (("grid_div", 1), ("grid_div", 4), ("pdl", 1), ("batch_stage_times", 1),
+                         ("slots", 16), ("slots", 1), ("pack_mode", 3)):
+            _native.set_option(opt, val)
+            got = sc.calculate_coefficients_device_batch(ds * 2, sps * 2)
+            assert [g.to_dict() for g in got] == want * 2, (opt, val)
+            got = sc.calculate_coefficients_batch([a for a, _ in cases], sps)
+            assert [g.to_dict() for g in got] == want, (opt, val)
+            _native.set_option(opt, defaults[opt])
+    finally:
+        for k, v in defaults.items():
+            _native.set_option(k, v)
+
+
 def test_graph_replay_sees_new_mask_contents(sc, cuda_device):
     """A cached CUDA graph keyed on the same device pointer must read the new
     contents of that buffer (device entry reuse, as in a serving loop)."""

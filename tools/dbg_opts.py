@@ -12,8 +12,11 @@ import paper_2510_02894_b200 as sc  # noqa: E402
 from paper_2510_02894_b200 import _native  # noqa: E402
 
 
-def rate(d, sp, n=100):
-    sc.calculate_coefficients_device_batch([d] * 16, [sp] * 16)
+def rate(d, sp, n=100, ref=None):
+    outs = sc.calculate_coefficients_device_batch([d] * 16, [sp] * 16)
+    if ref is not None:
+        assert all(o.to_dict() == ref for o in outs), "batch result differs"
+
     best = 1e9
     for _ in range(3):
         torch.cuda.synchronize()
@@ -41,6 +44,6 @@ for w in sys.argv[3:]:
             sc.calculate_coefficients_device(d, sp)
             one.append(_native.last_kernel_times(0))
         med = {k: sorted(t[k] for t in one)[5] * 1e3 for k in one[0] if k != "h2d_ms"}
-        print(f"{w} {opt}={v}: batch {rate(d, sp):6.1f} us/ROI | single-call stages (us) "
+        print(f"{w} {opt}={v}: batch {rate(d, sp, ref=ref):6.1f} us/ROI | single-call stages (us) "
               + " ".join(f"{k[:-3]} {t:.1f}" for k, t in med.items()), flush=True)
     _native.set_option(opt, vals[0])
