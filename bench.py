@@ -52,6 +52,8 @@ UNIT = "ROIs/s"
 # SURVEY.md 8(d) configurations.  The default (headline, BASELINE.json
 # configs[1]) is c2; the others are selectable with --workload.
 WORKLOADS = {
+    "c1": "C1 synthetic 64^3 sphere mask (r=24, spacing 1 mm, V=10824; the reference's own "
+          "CPU-runnable case), one ROI per step per GPU",
     "c2": "C2 KiTS19-shaped synthetic kidney+tumor mask 512x512x600 uint8 at 0.8x0.8x1.0 mm "
           "(tumor 30 mm, V=73406), one ROI per step per GPU",
     "c3": "C3 noisy-boundary ellipsoid 512^3 at 1 mm (sigma 0.02, seed 1234, V=1963474, "
@@ -67,7 +69,9 @@ def load_workload(name, rank=0, world=1):
     """[(mask (nz,ny,nx) uint8, spacing)] for this rank, plus a config dict."""
     from paper_2510_02894_b200 import sharding, synth
 
-    if name == "c2":
+    if name == "c1":
+        rois = [(synth.synth_mask("sphere", (64, 64, 64), radius=24), (1.0, 1.0, 1.0))]
+    elif name == "c2":
         rois = [(synth.kits_like(512, 512, 600, (0.8, 0.8, 1.0), 30.0), (0.8, 0.8, 1.0))]
     elif name == "c3":
         rois = [(synth.noisy_ellipsoid(512, 0.02, 1234), (1.0, 1.0, 1.0))]
@@ -421,17 +425,20 @@ def run_ours(args):
     def pass1_roof(m, d, label):
         # One fused kernel runs the 3-D list (8 flop per pair: 3 FMA + |p|^2
         # fold + max) and the planar list (6 flop per pair: 2 FMA + fold + max).
-        edge = int(round(_native.PAIRS_PER_UNIT ** 0.5))
-        p3 = d["work_units"] * _native.PAIRS_PER_UNIT
-        p2 = d["planar_work_units"] * _native.PAIRS_PER_UNIT
+        # Pass 1 evaluates the listed 64 x 64 sub-pairs of every kept unit.
+        edge = 64
+        sub = _native.PAIRS_PER_UNIT // 4
+        p3 = d["work_subunits"] * sub
+        p2 = d["planar_work_subunits"] * sub
         t = m["pass1_ms"] / 1e3
         ach = (8.0 * p3 + 6.0 * p2) / t / 1e12
         return {"kernel": "diam_pass1", "bound": "fp32", "achieved": ach, "peak": fp32_peak,
                 "unit": "TFLOP/s", "frac": ach / fp32_peak,
                 "traffic": traffic.get("diam_pass1"),
-                "work": f"{label}: 8 flop x {p3:.4g} 3-D pairs ({d['work_units']} of "
-                        f"{d['total_units']} {edge}x{edge} chunk pairs) + 6 flop x {p2:.4g} "
-                        f"in-plane pairs ({d['planar_work_units']} chunk pairs)",
+                "work": f"{label}: 8 flop x {p3:.4g} 3-D pairs ({d['work_subunits']} {edge}x{edge} "
+                        f"sub-pairs of {d['work_units']} kept / {d['total_units']} 128x128 "
+                        f"chunk pairs) + 6 flop x {p2:.4g} in-plane pairs "
+                        f"({d['planar_work_subunits']} sub-pairs)",
                 "pair_evals_per_s": (p3 + p2) / t,
                 "peak_note": "FP32 CUDA-core rate measured on this GPU by sc_probe_fp32_peak "
                              f"(best of FFMA/FFMA-imm/FFMA2; FFMA2 alone {fp32_ffma2:.1f} "

@@ -149,10 +149,12 @@ int sc_mesh_vertices(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, in
  * CUDA-core throughput of `device` in TFLOP/s with a dependent-chain-free
  * FFMA2 (mode 0) or scalar FFMA (mode 1) kernel. */
 int sc_last_kernel_times(int device, double* ms, int n);
-/* Work counters of the last ROI on `device`: {3-D work units evaluated, 3-D
- * work units total, 3-D fp64 re-check candidates, planar tile pairs total,
- * planar re-check candidates, planar tile pairs evaluated}; a unit is 256 x
- * 256 vertex pairs.  Returns how many were written. */
+/* Work counters of the last ROI on `device`: {3-D work units kept, 3-D work
+ * units total, 3-D fp64 re-check candidates, planar tile pairs total, planar
+ * re-check candidates, planar units kept, 3-D 64 x 64 sub-pairs evaluated,
+ * planar 64 x 64 sub-pairs evaluated}; a unit is a 128 x 128 chunk pair, of
+ * which pass 1 evaluates the listed 64 x 64 sub-pairs.  Returns how many were
+ * written (<= 8). */
 int sc_last_diagnostics(int device, int64_t* out, int n);
 /* Process-wide switches: "prune" (default 1) = exact bbox pruning of 3-D and
  * planar work units; "pass1_packed" (1) = FFMA2 variant of the 3-D pass;

@@ -44,9 +44,10 @@ __global__ void scan_all(unsigned int*, unsigned int*, const unsigned int*, unsi
                          unsigned int*, unsigned int*, long long, Stats*, int4*);
 __global__ void scatter_all(const int4*, long long, const Stats*, unsigned int*, int4*,
                             const unsigned int*, unsigned int*, int2*, unsigned int*);
-__global__ void boxes_extremes(const int4*, long long, const RoiParams*, Stats*, int4*, int4*);
+__global__ void boxes_extremes(const int4*, long long, const RoiParams*, Stats*, int4*, int4*,
+                               int4*);
 __global__ void unit_filter(const int4*, const int4*, long long, const RoiParams*, int, int, int,
-                            Stats*, uint2*, const int4*);
+                            Stats*, uint2*, const int4*, const int4*);
 template <bool PACKED>
 __global__ void diam_pass1(const int4*, long long, const RoiParams*, const uint2*, float*,
                            const int2*, const unsigned int*, const uint2*, long long, float*,
@@ -55,12 +56,12 @@ __global__ void diam_refine(const int4*, long long, const RoiParams*, const uint
                             const int2*, const unsigned int*, const uint2*, long long,
                             const float*, Stats*);
 __global__ void plane_boxes(const int2*, const unsigned int*, const unsigned int*,
-                            const RoiParams*, const Stats*, int4*, unsigned long long*);
+                            const RoiParams*, const Stats*, int4*, unsigned long long*, int4*);
 __global__ void plane_lb(const int2*, const unsigned int*, const unsigned long long*,
                          const RoiParams*, Stats*);
 __global__ void plane_filter(const unsigned int*, const unsigned int*, const unsigned int*,
                              const int4*, const RoiParams*, int, int, int, long long, Stats*,
-                             uint2*);
+                             uint2*, const int4*);
 __global__ void cloud_diameters(const double*, const double*, const double*, long long, int,
                                 unsigned long long*);
 int launch_binarize(const void*, int, const long long[3], int, int, long long, double, uint8_t*,
@@ -212,7 +213,7 @@ struct Ctx {
   double last_ms[7] = {0, 0, 0, 0, 0, 0, 0};  // pack, mc, prune, pass1, refine, planar, h2d
   bool times_pending = false;  // last_ms[0..5] still to be read from kev[]
   long long cap_floor = 0, dcap_floor = 0, wcap_floor = 0;  // raised by overflow re-runs only
-  long long last_diag[6] = {0, 0, 0, 0, 0, 0};
+  long long last_diag[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int occ_pass1 = 1, occ_pass1s = 1, occ_pack = 1, occ_mc = 1;  // blocks/SM
   int prio_lo = 0, prio_hi = 0;  // stream priority range (least, greatest)
   Stats* d_stats = nullptr;
@@ -223,6 +224,7 @@ struct Ctx {
   CaseTables* d_tabs = nullptr;
   DevBuf<uint32_t> bits;
   DevBuf<int4> keys, keys_sorted, boxes, sboxes;  // chunk / super-chunk boxes (lo, hi)
+  DevBuf<int4> hboxes;  // boxes of the two 64-vertex halves of every chunk
   DevBuf<unsigned int> sort_counts, sort_cursor;
   DevBuf<uint2> work;  // surviving 3-D chunk pairs (I, J)
   DevBuf<float> warp_max, plane_umax;
@@ -231,6 +233,7 @@ struct Ctx {
   DevBuf<unsigned int> pbin_counts, pbin_cursor;
   DevBuf<unsigned long long> plane_ext;
   DevBuf<int4> plane_boxes_buf;
+  DevBuf<int4> plane_hboxes;  // boxes of the two 64-entry halves of every in-plane chunk
   DevBuf<int2> plane_sorted;
   DevBuf<uint8_t> mask_stage, raw_stage;
   double last_scan_ms = 0.0;      // host slab scan of the last host-mask ROI
@@ -261,11 +264,12 @@ struct Ctx {
 
   unsigned long long fingerprint() const {
     unsigned long long h = 1469598103934665603ull;
-    const void* ps[] = {bits.p, keys.p, keys_sorted.p, boxes.p, sboxes.p, sort_counts.p, sort_cursor.p,
+    const void* ps[] = {bits.p, keys.p, keys_sorted.p, boxes.p, sboxes.p, hboxes.p,
+                        sort_counts.p, sort_cursor.p,
                         work.p, warp_max.p, plane_umax.p,
                         plane_counts.p, plane_start.p, plane_tstart.p, plane_sorted.p,
                         plane_work.p, plane_cstart.p, pbin_counts.p, pbin_cursor.p,
-                        plane_ext.p, plane_boxes_buf.p};
+                        plane_ext.p, plane_boxes_buf.p, plane_hboxes.p};
     for (const void* p : ps) h = (h ^ (unsigned long long)(uintptr_t)p) * 1099511628211ull;
     return h;
   }
@@ -410,6 +414,7 @@ int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, lo
   CK(c->work.ensure((size_t)wc));
   CK(c->keys_sorted.ensure((size_t)dcap));
   CK(c->boxes.ensure((size_t)(2 * (C + 1))));
+  CK(c->hboxes.ensure((size_t)(4 * (C + 1))));
   CK(c->sboxes.ensure((size_t)(2 * (C / 8 + 1))));
   {
     unsigned int* before = c->sort_counts.p;
@@ -439,6 +444,7 @@ int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, lo
   CK(c->plane_umax.ensure((size_t)pu));
   CK(c->plane_work.ensure((size_t)pu));
   CK(c->plane_boxes_buf.ensure((size_t)t));
+  CK(c->plane_hboxes.ensure((size_t)(2 * t)));
   return SC_OK;
 }
 
@@ -561,16 +567,16 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(launch_k(c, s, lgrid(c, 2), 256, boxes_extremes, c->keys_sorted.p, dcap, rp, c->d_stats, c->boxes.p,
-                                            c->sboxes.p));
+                                            c->sboxes.p, c->hboxes.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(launch_k(c, s, lgrid(c, 4), 256, unit_filter, c->keys_sorted.p, c->boxes.p, dcap, rp, prune, shard,
-                                         nshards, c->d_stats, c->work.p, c->sboxes.p));
+                                         nshards, c->d_stats, c->work.p, c->sboxes.p, c->hboxes.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[3], s));
   CK(launch_k(c, s, lgrid(c, 4), 256, plane_boxes, c->plane_sorted.p, c->plane_start.p, c->plane_cstart.p,
-                                         rp, c->d_stats, c->plane_boxes_buf.p, c->plane_ext.p));
+                                         rp, c->d_stats, c->plane_boxes_buf.p, c->plane_ext.p, c->plane_hboxes.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(launch_k(c, s, lgrid(c, 1), 256, plane_lb, c->plane_sorted.p, c->plane_start.p, c->plane_ext.p, rp,
@@ -579,7 +585,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   if (++nk >= lim) return SC_OK;
   CK(launch_k(c, s, lgrid(c, 4), 256, plane_filter, c->plane_start.p, c->plane_tstart.p, c->plane_cstart.p,
                                           c->plane_boxes_buf.p, rp, prune, shard, nshards, pucap,
-                                          c->d_stats, c->plane_work.p));
+                                          c->d_stats, c->plane_work.p, c->plane_hboxes.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[4], s));
@@ -836,6 +842,8 @@ int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
     c->last_diag[3] = (long long)h.plane_units;
     c->last_diag[4] = (long long)h.n_pcand;
     c->last_diag[5] = (long long)h.n_pwork;
+    c->last_diag[6] = (long long)h.n_sub;
+    c->last_diag[7] = (long long)h.n_psub;
   }
   out->mesh_ms = c->events_on ? ev_ms(c->kev[0], c->kev[2]) : 0.0;
   out->diameters_ms = c->events_on ? ev_ms(c->kev[2], c->kev[6]) : 0.0;
@@ -1438,7 +1446,7 @@ int sc_last_diagnostics(int device, int64_t* out, int n) {
   int rc = get_ctx(device, &c);
   if (rc) return -rc;
   std::lock_guard<std::mutex> lk(c->mu);
-  int m = n < 6 ? n : 6;
+  int m = n < 8 ? n : 8;
   for (int i = 0; i < m; i++) out[i] = c->last_diag[i];
   return m;
 }

@@ -67,7 +67,8 @@ __device__ __forceinline__ void pass1_3d(const int4* __restrict__ keys, long lon
   float a[kR], b[kR], c[kR], ni[kR];
   for (long long w = wb; w < we; w++) {
     const uint2 ij = work[w];
-    const int I = (int)ij.x, J = (int)ij.y;
+    const int I = (int)ij.x, J = (int)(ij.y & kIdxMask);
+    const unsigned int sub = ij.y >> kSubShift;  // 64 x 64 sub-pairs to evaluate
     float m[kR];
     __syncwarp();  // previous unit is done with sj
 #pragma unroll
@@ -96,36 +97,65 @@ __device__ __forceinline__ void pass1_3d(const int4* __restrict__ keys, long lon
         b2[r] = make_float2(b[2 * r], b[2 * r + 1]);
         c2[r] = make_float2(c[2 * r], c[2 * r + 1]);
       }
+      if (sub == 0xFu) {
 #pragma unroll 2
-      for (int j = 0; j < kChunk; j += 2) {
-        const float4 q0 = sj[j], q1 = sj[j + 1];
+        for (int j = 0; j < kChunk; j += 2) {
+          const float4 q0 = sj[j], q1 = sj[j + 1];
 #pragma unroll
-        for (int r = 0; r < kR / 2; r++) {
-          float2 t0 = __ffma2_rn(a2[r], make_float2(q0.x, q0.x), make_float2(q0.w, q0.w));
-          float2 t1 = __ffma2_rn(a2[r], make_float2(q1.x, q1.x), make_float2(q1.w, q1.w));
-          t0 = __ffma2_rn(b2[r], make_float2(q0.y, q0.y), t0);
-          t1 = __ffma2_rn(b2[r], make_float2(q1.y, q1.y), t1);
-          t0 = __ffma2_rn(c2[r], make_float2(q0.z, q0.z), t0);
-          t1 = __ffma2_rn(c2[r], make_float2(q1.z, q1.z), t1);
-          m[2 * r] = fmax3f(m[2 * r], t0.x, t1.x);
-          m[2 * r + 1] = fmax3f(m[2 * r + 1], t0.y, t1.y);
+          for (int r = 0; r < kR / 2; r++) {
+            float2 t0 = __ffma2_rn(a2[r], make_float2(q0.x, q0.x), make_float2(q0.w, q0.w));
+            float2 t1 = __ffma2_rn(a2[r], make_float2(q1.x, q1.x), make_float2(q1.w, q1.w));
+            t0 = __ffma2_rn(b2[r], make_float2(q0.y, q0.y), t0);
+            t1 = __ffma2_rn(b2[r], make_float2(q1.y, q1.y), t1);
+            t0 = __ffma2_rn(c2[r], make_float2(q0.z, q0.z), t0);
+            t1 = __ffma2_rn(c2[r], make_float2(q1.z, q1.z), t1);
+            m[2 * r] = fmax3f(m[2 * r], t0.x, t1.x);
+            m[2 * r + 1] = fmax3f(m[2 * r + 1], t0.y, t1.y);
+          }
         }
+      } else {
+        // Only the listed 64 x 64 sub-pairs: i half a = packed pair a (i = a*64
+        // + {0, 32} + lane), j half b.  a, b are compile-time in each body.
+#pragma unroll
+        for (int a = 0; a < 2; a++)
+#pragma unroll
+          for (int b = 0; b < 2; b++) {
+            if (!(sub & (1u << (2 * a + b)))) continue;
+#pragma unroll 2
+            for (int j = 64 * b; j < 64 * b + 64; j += 2) {
+              const float4 q0 = sj[j], q1 = sj[j + 1];
+              float2 t0 = __ffma2_rn(a2[a], make_float2(q0.x, q0.x), make_float2(q0.w, q0.w));
+              float2 t1 = __ffma2_rn(a2[a], make_float2(q1.x, q1.x), make_float2(q1.w, q1.w));
+              t0 = __ffma2_rn(b2[a], make_float2(q0.y, q0.y), t0);
+              t1 = __ffma2_rn(b2[a], make_float2(q1.y, q1.y), t1);
+              t0 = __ffma2_rn(c2[a], make_float2(q0.z, q0.z), t0);
+              t1 = __ffma2_rn(c2[a], make_float2(q1.z, q1.z), t1);
+              m[2 * a] = fmax3f(m[2 * a], t0.x, t1.x);
+              m[2 * a + 1] = fmax3f(m[2 * a + 1], t0.y, t1.y);
+            }
+          }
       }
     } else {
-#pragma unroll 2
-      for (int j = 0; j < kChunk; j += 2) {
-        const float4 q0 = sj[j], q1 = sj[j + 1];
 #pragma unroll
-        for (int r = 0; r < kR; r++) {
-          float t0 = fmaf(q0.x, a[r], q0.w);
-          float t1 = fmaf(q1.x, a[r], q1.w);
-          t0 = fmaf(q0.y, b[r], t0);
-          t1 = fmaf(q1.y, b[r], t1);
-          t0 = fmaf(q0.z, c[r], t0);
-          t1 = fmaf(q1.z, c[r], t1);
-          m[r] = fmax3f(m[r], t0, t1);
+      for (int ha = 0; ha < 2; ha++)
+#pragma unroll
+        for (int hb = 0; hb < 2; hb++) {
+          if (!(sub & (1u << (2 * ha + hb)))) continue;
+#pragma unroll 2
+          for (int j = 64 * hb; j < 64 * hb + 64; j += 2) {
+            const float4 q0 = sj[j], q1 = sj[j + 1];
+#pragma unroll
+            for (int r = 2 * ha; r < 2 * ha + 2; r++) {
+              float t0 = fmaf(q0.x, a[r], q0.w);
+              float t1 = fmaf(q1.x, a[r], q1.w);
+              t0 = fmaf(q0.y, b[r], t0);
+              t1 = fmaf(q1.y, b[r], t1);
+              t0 = fmaf(q0.z, c[r], t0);
+              t1 = fmaf(q1.z, c[r], t1);
+              m[r] = fmax3f(m[r], t0, t1);
+            }
+          }
         }
-      }
     }
     float best = 0.f;
 #pragma unroll
@@ -174,7 +204,7 @@ __device__ __forceinline__ void refine_3d(const int4* __restrict__ keys, long lo
     if (threadIdx.x == 0 && cnt) atomicAdd(&st->n_cand, (unsigned long long)cnt);
     for (int q = 0; q < cnt; q++) {
       const uint2 ij = work[s_list[q]];
-      const int I = (int)ij.x, J = (int)ij.y;
+      const int I = (int)ij.x, J = (int)(ij.y & kIdxMask);
       __syncthreads();  // previous candidate is done with sx/sy/sz
       if (threadIdx.x < kChunk) {
         const long long j = (long long)J * kChunk + threadIdx.x;
@@ -230,7 +260,8 @@ __device__ __forceinline__ void pass1_planar(const int2* __restrict__ sorted,
   int axis = 0;
   for (long long w = wb; w < we; w++) {
     const uint2 u = pwork[w];
-    const unsigned int p = u.x, I = u.y >> 16, J = u.y & 0xffffu;
+    const unsigned int p = u.x & kIdxMask, I = u.y >> 16, J = u.y & 0xffffu;
+    const unsigned int sub = u.x >> kSubShift;  // 64 x 64 sub-pairs to evaluate
     const unsigned int b0 = start[p], np = start[p + 1] - b0;
     axis = plane_axis((int)p, ps);
     const PlaneAxes ax = plane_axes(axis, st, f);
@@ -259,18 +290,38 @@ __device__ __forceinline__ void pass1_planar(const int2* __restrict__ sorted,
     float m[kPR];
 #pragma unroll
     for (int r = 0; r < kPR; r++) m[r] = -3.0e38f;
+    if (sub == 0xFu) {
 #pragma unroll 2
-    for (int j = 0; j < kPC; j += 2) {
-      const float4 q0 = sj[j], q1 = sj[j + 1];
+      for (int j = 0; j < kPC; j += 2) {
+        const float4 q0 = sj[j], q1 = sj[j + 1];
 #pragma unroll
-      for (int r = 0; r < kPR / 2; r++) {
-        float2 t0 = __ffma2_rn(a2[r], make_float2(q0.x, q0.x), make_float2(q0.z, q0.z));
-        float2 t1 = __ffma2_rn(a2[r], make_float2(q1.x, q1.x), make_float2(q1.z, q1.z));
-        t0 = __ffma2_rn(b2[r], make_float2(q0.y, q0.y), t0);
-        t1 = __ffma2_rn(b2[r], make_float2(q1.y, q1.y), t1);
-        m[2 * r] = fmax3f(m[2 * r], t0.x, t1.x);
-        m[2 * r + 1] = fmax3f(m[2 * r + 1], t0.y, t1.y);
+        for (int r = 0; r < kPR / 2; r++) {
+          float2 t0 = __ffma2_rn(a2[r], make_float2(q0.x, q0.x), make_float2(q0.z, q0.z));
+          float2 t1 = __ffma2_rn(a2[r], make_float2(q1.x, q1.x), make_float2(q1.z, q1.z));
+          t0 = __ffma2_rn(b2[r], make_float2(q0.y, q0.y), t0);
+          t1 = __ffma2_rn(b2[r], make_float2(q1.y, q1.y), t1);
+          m[2 * r] = fmax3f(m[2 * r], t0.x, t1.x);
+          m[2 * r + 1] = fmax3f(m[2 * r + 1], t0.y, t1.y);
+        }
       }
+    } else {
+      // Only the listed 64 x 64 sub-pairs (i half a = packed pair a).
+#pragma unroll
+      for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 2; b++) {
+          if (!(sub & (1u << (2 * a + b)))) continue;
+#pragma unroll 2
+          for (int j = 64 * b; j < 64 * b + 64; j += 2) {
+            const float4 q0 = sj[j], q1 = sj[j + 1];
+            float2 t0 = __ffma2_rn(a2[a], make_float2(q0.x, q0.x), make_float2(q0.z, q0.z));
+            float2 t1 = __ffma2_rn(a2[a], make_float2(q1.x, q1.x), make_float2(q1.z, q1.z));
+            t0 = __ffma2_rn(b2[a], make_float2(q0.y, q0.y), t0);
+            t1 = __ffma2_rn(b2[a], make_float2(q1.y, q1.y), t1);
+            m[2 * a] = fmax3f(m[2 * a], t0.x, t1.x);
+            m[2 * a + 1] = fmax3f(m[2 * a + 1], t0.y, t1.y);
+          }
+        }
     }
     float best = 0.f;
 #pragma unroll
@@ -318,7 +369,7 @@ __device__ __forceinline__ void refine_planar(const int2* __restrict__ sorted,
     __syncthreads();
     const long long w = w0 + (sweep * kPlaneThreads + threadIdx.x) * G + blockIdx.x;
     if (w < w1) {
-      const int a = plane_axis((int)pwork[w].x, ps);
+      const int a = plane_axis((int)(pwork[w].x & kIdxMask), ps);
       if (umax[w] >= (a == 0 ? tau[0] : (a == 1 ? tau[1] : tau[2])))
         s_list[atomicAdd(&s_n, 1)] = (unsigned int)w;
     }
@@ -327,7 +378,7 @@ __device__ __forceinline__ void refine_planar(const int2* __restrict__ sorted,
     if (threadIdx.x == 0 && cnt) atomicAdd(&st->n_pcand, (unsigned long long)cnt);
     for (int q = 0; q < cnt; q++) {
       const uint2 u = pwork[s_list[q]];
-      const unsigned int p = u.x, I = u.y >> 16, J = u.y & 0xffffu;
+      const unsigned int p = u.x & kIdxMask, I = u.y >> 16, J = u.y & 0xffffu;
       const int axis = plane_axis((int)p, ps);
       const PlaneAxes ax = plane_axes(axis, st, f);
       const unsigned int b0 = start[p], np = start[p + 1] - b0;

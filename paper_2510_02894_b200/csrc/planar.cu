@@ -113,7 +113,7 @@ __global__ void plane_boxes(const int2* __restrict__ sorted,
                             const unsigned int* __restrict__ cstart,
                             const RoiParams* __restrict__ rp,
                             const Stats* __restrict__ st, int4* __restrict__ pboxes,
-                            unsigned long long* __restrict__ pext) {
+                            unsigned long long* __restrict__ pext, int4* __restrict__ hpboxes) {
   pdl_enter();
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
@@ -133,13 +133,20 @@ __global__ void plane_boxes(const int2* __restrict__ sorted,
     const unsigned int b0 = start[p], np = start[p + 1] - b0;
     const unsigned int e0 = (unsigned int)(c - coff[p]) * kPC;
     const unsigned int e1 = min(np, e0 + kPC);
-    int la = INT_MAX, lb = INT_MAX, ha = INT_MIN, hb = INT_MIN;
+    // Boxes of the two 64-entry halves (entries past the end clamp to the
+    // last one, as pass 1 does) and their union.
+    int la[2] = {INT_MAX, INT_MAX}, lb[2] = {INT_MAX, INT_MAX};
+    int ha[2] = {INT_MIN, INT_MIN}, hb[2] = {INT_MIN, INT_MIN};
     unsigned long long ext[8];
 #pragma unroll
     for (int d = 0; d < 8; d++) ext[d] = 0ull;
-    for (unsigned int e = e0 + lane; e < e1; e += 32) {
+#pragma unroll
+    for (int t = 0; t < kPC / 32; t++) {
+      const unsigned int e = min(e0 + t * 32 + lane, e1 - 1);
+      const int hh = t / (kPC / 64);
       const int2 k = sorted[b0 + e];
-      la = min(la, k.x); lb = min(lb, k.y); ha = max(ha, k.x); hb = max(hb, k.y);
+      la[hh] = min(la[hh], k.x); lb[hh] = min(lb[hh], k.y);
+      ha[hh] = max(ha[hh], k.x); hb[hh] = max(hb[hh], k.y);
       const float a = (float)k.x * ax.ha, b = (float)k.y * ax.hb;
       const float pr[4] = {a, b, a + b, a - b};
 #pragma unroll
@@ -149,9 +156,17 @@ __global__ void plane_boxes(const int2* __restrict__ sorted,
         ext[2 * d + 1] = lo > ext[2 * d + 1] ? lo : ext[2 * d + 1];
       }
     }
-    la = __reduce_min_sync(0xffffffffu, la); lb = __reduce_min_sync(0xffffffffu, lb);
-    ha = __reduce_max_sync(0xffffffffu, ha); hb = __reduce_max_sync(0xffffffffu, hb);
-    if (lane == 0) pboxes[c] = make_int4(la, lb, ha, hb);
+#pragma unroll
+    for (int hh = 0; hh < 2; hh++) {
+      la[hh] = __reduce_min_sync(0xffffffffu, la[hh]); lb[hh] = __reduce_min_sync(0xffffffffu, lb[hh]);
+      ha[hh] = __reduce_max_sync(0xffffffffu, ha[hh]); hb[hh] = __reduce_max_sync(0xffffffffu, hb[hh]);
+    }
+    if (lane == 0) {
+      pboxes[c] = make_int4(min(la[0], la[1]), min(lb[0], lb[1]), max(ha[0], ha[1]),
+                            max(hb[0], hb[1]));
+      hpboxes[2 * c] = make_int4(la[0], lb[0], ha[0], hb[0]);
+      hpboxes[2 * c + 1] = make_int4(la[1], lb[1], ha[1], hb[1]);
+    }
 #pragma unroll
     for (int d = 0; d < 8; d++) {
       unsigned long long x = ext[d];
@@ -222,7 +237,8 @@ __global__ void plane_filter(const unsigned int* __restrict__ start,
                              const unsigned int* __restrict__ cstart,
                              const int4* __restrict__ pboxes, const RoiParams* __restrict__ rp,
                              int prune, int shard, int nshards, long long wcap,
-                             Stats* __restrict__ st, uint2* __restrict__ pwork) {
+                             Stats* __restrict__ st, uint2* __restrict__ pwork,
+                             const int4* __restrict__ hpboxes) {
   pdl_enter();
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
@@ -286,20 +302,48 @@ __global__ void plane_filter(const unsigned int* __restrict__ start,
           }
         }
       }
+      // 64 x 64 sub-pairs that can reach the bound (bit 2a + b; for i == j
+      // the mirrored (1, 0) repeats (0, 1)); 0xF = whole unit without pruning.
+      unsigned int s0 = 0xFu, s1 = 0xFu;
+      if (prune && (k0 || k1)) {
+        auto subs = [&](int ci, int cj) {
+          unsigned int m = 0u;
+#pragma unroll
+          for (int a = 0; a < 2; a++)
+#pragma unroll
+            for (int b = 0; b < 2; b++) {
+              if (ci == cj && a == 1 && b == 0) continue;
+              const int4 bi = hpboxes[2 * (c0 + ci) + a], bj = hpboxes[2 * (c0 + cj) + b];
+              if (reach2(bi.x, bi.z, bj.x, bj.z, hA) + reach2(bi.y, bi.w, bj.y, bj.w, hB) >= th)
+                m |= 1u << (2 * a + b);
+            }
+          return m;
+        };
+        if (k0) { s0 = subs(i, j0); k0 = s0 != 0u; }
+        if (k1) { s1 = subs(i, j1); k1 = s1 != 0u; }
+      }
       const unsigned int m0 = __ballot_sync(0xffffffffu, k0);
       const unsigned int m1 = __ballot_sync(0xffffffffu, k1);
       if (!(m0 | m1)) continue;
+      const unsigned int nsub =
+          __reduce_add_sync(0xffffffffu, (k0 ? __popc(s0) : 0u) + (k1 ? __popc(s1) : 0u));
       unsigned long long pos = 0;
-      if (lane == 0) pos = atomicAdd(&st->n_pwork, (unsigned long long)(__popc(m0) + __popc(m1)));
+      if (lane == 0) {
+        pos = atomicAdd(&st->n_pwork, (unsigned long long)(__popc(m0) + __popc(m1)));
+        atomicAdd(&st->n_psub, (unsigned long long)nsub);
+      }
       pos = __shfl_sync(0xffffffffu, pos, 0);
       const unsigned int lt = (1u << lane) - 1;
       long long o = (long long)pos + __popc(m0 & lt) + __popc(m1 & lt);
       if (k0) {
-        if (o < wcap) pwork[o] = make_uint2((unsigned int)p, ((unsigned int)i << 16) | (unsigned int)j0);
+        if (o < wcap)
+          pwork[o] = make_uint2((unsigned int)p | (s0 << kSubShift),
+                                ((unsigned int)i << 16) | (unsigned int)j0);
         o++;
       }
       if (k1 && o < wcap)
-        pwork[o] = make_uint2((unsigned int)p, ((unsigned int)i << 16) | (unsigned int)j1);
+        pwork[o] = make_uint2((unsigned int)p | (s1 << kSubShift),
+                              ((unsigned int)i << 16) | (unsigned int)j1);
     }
   }
 }

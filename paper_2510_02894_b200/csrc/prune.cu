@@ -193,7 +193,8 @@ __global__ void __launch_bounds__(256) boxes_extremes(const int4* __restrict__ k
                                                       long long cap, const RoiParams* __restrict__ rp,
                                                       Stats* __restrict__ st,
                                                       int4* __restrict__ boxes,
-                                                      int4* __restrict__ sboxes) {
+                                                      int4* __restrict__ sboxes,
+                                                      int4* __restrict__ hboxes) {
   pdl_enter();
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
@@ -206,25 +207,41 @@ __global__ void __launch_bounds__(256) boxes_extremes(const int4* __restrict__ k
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   for (long long c = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < chunks;
        c += warps) {
-    int lx = INT_MAX, ly = INT_MAX, lz = INT_MAX, hx = INT_MIN, hy = INT_MIN, hz = INT_MIN;
+    // Boxes of the two 64-vertex halves (t = 0,1 and t = 2,3), and their union.
+    int l[2][3], u[2][3];
     float px[kPerLane], py[kPerLane], pz[kPerLane];
     unsigned int idx[kPerLane];
+#pragma unroll
+    for (int hh = 0; hh < 2; hh++)
+#pragma unroll
+      for (int a = 0; a < 3; a++) { l[hh][a] = INT_MAX; u[hh][a] = INT_MIN; }
 #pragma unroll
     for (int t = 0; t < kPerLane; t++) {
       long long v = c * kChunkV + t * 32 + lane;
       if (v >= n) v = n - 1;  // pass 1 clamps the same way
       const int4 k = keys[v];
-      lx = min(lx, k.x); ly = min(ly, k.y); lz = min(lz, k.z);
-      hx = max(hx, k.x); hy = max(hy, k.y); hz = max(hz, k.z);
+      const int hh = t / (kPerLane / 2);
+      l[hh][0] = min(l[hh][0], k.x); l[hh][1] = min(l[hh][1], k.y); l[hh][2] = min(l[hh][2], k.z);
+      u[hh][0] = max(u[hh][0], k.x); u[hh][1] = max(u[hh][1], k.y); u[hh][2] = max(u[hh][2], k.z);
       px[t] = (float)k.x * f.hx; py[t] = (float)k.y * f.hy; pz[t] = (float)k.z * f.hz;
       idx[t] = (unsigned int)v;
     }
-    lx = __reduce_min_sync(0xffffffffu, lx); ly = __reduce_min_sync(0xffffffffu, ly);
-    lz = __reduce_min_sync(0xffffffffu, lz); hx = __reduce_max_sync(0xffffffffu, hx);
-    hy = __reduce_max_sync(0xffffffffu, hy); hz = __reduce_max_sync(0xffffffffu, hz);
+#pragma unroll
+    for (int hh = 0; hh < 2; hh++)
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        l[hh][a] = __reduce_min_sync(0xffffffffu, l[hh][a]);
+        u[hh][a] = __reduce_max_sync(0xffffffffu, u[hh][a]);
+      }
+    const int lx = min(l[0][0], l[1][0]), ly = min(l[0][1], l[1][1]), lz = min(l[0][2], l[1][2]);
+    const int hx = max(u[0][0], u[1][0]), hy = max(u[0][1], u[1][1]), hz = max(u[0][2], u[1][2]);
     if (lane == 0) {
       boxes[2 * c] = make_int4(lx, ly, lz, 0);
       boxes[2 * c + 1] = make_int4(hx, hy, hz, 0);
+      hboxes[4 * c] = make_int4(l[0][0], l[0][1], l[0][2], 0);
+      hboxes[4 * c + 1] = make_int4(u[0][0], u[0][1], u[0][2], 0);
+      hboxes[4 * c + 2] = make_int4(l[1][0], l[1][1], l[1][2], 0);
+      hboxes[4 * c + 3] = make_int4(u[1][0], u[1][1], u[1][2], 0);
       int* slo = reinterpret_cast<int*>(sboxes + 2 * (c / kSuper));
       int* shi = reinterpret_cast<int*>(sboxes + 2 * (c / kSuper) + 1);
       atomicMin(slo, lx); atomicMin(slo + 1, ly); atomicMin(slo + 2, lz);
@@ -273,7 +290,8 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
                                                    const RoiParams* __restrict__ rp, int prune,
                                                    int shard, int nshards, Stats* __restrict__ st,
                                                    uint2* __restrict__ work,
-                                                   const int4* __restrict__ sboxes) {
+                                                   const int4* __restrict__ sboxes,
+                                                   const int4* __restrict__ hboxes) {
   pdl_enter();
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
@@ -320,6 +338,36 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
            axis_reach(alo.y, ahi.y, blo.y, bhi.y, h3[1]) +
            axis_reach(alo.z, ahi.z, blo.z, bhi.z, h3[2]);
   };
+  // Which 64 x 64 sub-pairs of a kept chunk pair (i, j) can reach LB
+  // (bit 2a + b, half a of i, half b of j; for i == j the mirrored (1, 0) is
+  // the same pairs as (0, 1)).
+  auto subs = [&](int i, int j) {
+    unsigned int m = 0u;
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+      for (int b = 0; b < 2; b++)
+        if (!(i == j && a == 1 && b == 0) &&
+            reach(hboxes[4 * i + 2 * a], hboxes[4 * i + 2 * a + 1], hboxes[4 * j + 2 * b],
+                  hboxes[4 * j + 2 * b + 1]) >= thr)
+          m |= 1u << (2 * a + b);
+    return m;
+  };
+  // Append the kept units of this warp step (all lanes call).
+  auto emit = [&](bool keep, int i, int j, unsigned int sub) {
+    const unsigned int mask = __ballot_sync(0xffffffffu, keep);
+    if (!mask) return;
+    const unsigned int nsub = __reduce_add_sync(0xffffffffu, keep ? __popc(sub) : 0u);
+    unsigned long long pos = 0;
+    if (lane == 0) {
+      pos = atomicAdd(&st->n_work, (unsigned long long)__popc(mask));
+      atomicAdd(&st->n_sub, (unsigned long long)nsub);
+    }
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    const long long o = (long long)pos + __popc(mask & ((1u << lane) - 1));
+    if (keep && o < wcap)
+      work[o] = make_uint2((unsigned int)i, (unsigned int)j | (sub << kSubShift));
+  };
   const long long fine_units = C * (C + 1) / 2;
   if (fine_units <= kSingleLevelMax) {
     // Small ROI: every chunk pair tested directly (one level, no serial
@@ -329,18 +377,17 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
       const long long u = base + threadIdx.x;
       bool keep = false;
       int i = 0, j = 0;
+      unsigned int sub = 0xFu;
       if (u < fine_units) {
         tile_pair(u, C, i, j);
         keep = u % nshards == shard &&
                (!prune || reach(boxes[2 * i], boxes[2 * i + 1], boxes[2 * j], boxes[2 * j + 1]) >= thr);
+        if (keep && prune) {
+          sub = subs(i, j);
+          keep = sub != 0u;
+        }
       }
-      const unsigned int mask = __ballot_sync(0xffffffffu, keep);
-      if (!mask) continue;
-      unsigned long long pos = 0;
-      if (lane == 0) pos = atomicAdd(&st->n_work, (unsigned long long)__popc(mask));
-      pos = __shfl_sync(0xffffffffu, pos, 0);
-      const long long o = (long long)pos + __popc(mask & ((1u << lane) - 1));
-      if (keep && o < wcap) work[o] = make_uint2((unsigned int)i, (unsigned int)j);
+      emit(keep, i, j, sub);
     }
     return;
   }
@@ -372,13 +419,12 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
                     ((long long)i * C - (long long)i * (i - 1) / 2 + (j - i)) % nshards == shard;
         if (keep && prune)
           keep = reach(boxes[2 * i], boxes[2 * i + 1], boxes[2 * j], boxes[2 * j + 1]) >= thr;
-        const unsigned int mask = __ballot_sync(0xffffffffu, keep);
-        if (!mask) continue;
-        unsigned long long pos = 0;
-        if (lane == 0) pos = atomicAdd(&st->n_work, (unsigned long long)__popc(mask));
-        pos = __shfl_sync(0xffffffffu, pos, 0);
-        const long long o = (long long)pos + __popc(mask & ((1u << lane) - 1));
-        if (keep && o < wcap) work[o] = make_uint2((unsigned int)i, (unsigned int)j);
+        unsigned int sub = 0xFu;
+        if (keep && prune) {
+          sub = subs(i, j);
+          keep = sub != 0u;
+        }
+        emit(keep, i, j, sub);
       }
     }
   }

@@ -30,7 +30,15 @@ struct Stats {
   unsigned long long plb[3];           // fp64 bits: exact planar lower bounds per family
   unsigned long long n_pwork;          // surviving planar units after pruning
   unsigned long long plane_chunks;     // 256-entry chunks over all planes
+  unsigned long long n_sub;            // 3-D 64 x 64 sub-pairs kept (pass 1 evaluates these)
+  unsigned long long n_psub;           // planar 64 x 64 sub-pairs kept
 };
+
+// Work entries carry, in the top 4 bits of the J field, which 64 x 64 sub-pairs
+// of the 128 x 128 chunk pair can reach the lower bound (bit 2a + b: I half a,
+// J half b); pass 1 evaluates only those.  0xF = the whole unit.
+constexpr unsigned int kSubShift = 28;
+constexpr unsigned int kIdxMask = (1u << kSubShift) - 1u;
 
 // Per-case integer tables for the exact volume path: for case k,
 // t = sum over its triangles of a.(b x c) and n = sum of (b-a) x (c-a), with
