@@ -330,6 +330,11 @@ def run_ours(args):
 
     world, rank, local = dist_setup(args.gpus)
     dev = torch.cuda.current_device()
+    # The host slab scan of the e2e leg uses a share of the host cores per rank
+    # (one process per GPU on one node).
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    host_threads = max(1, (os.cpu_count() or 1) // max(1, local_world))
+    _native.set_option("host_threads", min(32, host_threads))
     rois, cfg = load_workload(args.workload, rank, world)
     d_masks = [torch.from_numpy(m).to(f"cuda:{dev}") for m, _ in rois]
     sps = [sp for _, sp in rois]
@@ -481,6 +486,7 @@ def run_ours(args):
                         "memory: host scan of every mask byte for the occupied z/y slab "
                         "(host_threads), then only that slab is copied H2D",
                 "mask_bytes_per_step": int(sum(h_masks[i % n_host].size for i in range(K)) / K),
+                "host_threads_per_rank": min(32, host_threads),
                 "host_scan_ms_per_roi": scan_ms,
                 "h2d_ms_per_roi": e_outs[-1].h2d_ms,
                 "full_copy": {"value": world * K / full_s, "unit": UNIT,
