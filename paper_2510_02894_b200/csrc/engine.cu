@@ -555,7 +555,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
                                              c->plane_counts.p, c->plane_ext.p, c->d_stats));
   CKL(1);
   if (++nk >= lim) return SC_OK;
-  CK(launch_k(c, s, kSortSupers + 1, 1024, scan_all, c->sort_counts.p, c->sort_cursor.p,
+  CK(launch_k(c, s, kScanBlocks + 1, kScanThreads, scan_all, c->sort_counts.p, c->sort_cursor.p,
                                             c->plane_counts.p, c->plane_start.p,
                                             c->plane_tstart.p, c->plane_cstart.p, dcap,
                                             c->d_stats, c->sboxes.p));

@@ -37,32 +37,38 @@ __device__ __forceinline__ unsigned int plane_tiles(unsigned int np, int pt) {
   return t * (t + 1) / 2;
 }
 
-// kSortSupers + 1 blocks of 1024 threads.  Blocks [0, kSortSupers): one
-// 1024-bin slice each of the exclusive scan of the brick counts -> sort cursor
-// (and zero the counts for the next ROI), plus empty super-chunk boxes.  Last
-// block: plane populations (plane_bins_scan) -> start; 256-entry tile pairs
-// per plane -> tstart; 128-entry chunks per plane -> cstart.
-__global__ void __launch_bounds__(1024) scan_all(unsigned int* __restrict__ sort_counts,
-                                                 unsigned int* __restrict__ sort_cursor,
-                                                 const unsigned int* __restrict__ plane_counts,
-                                                 unsigned int* __restrict__ start,
-                                                 unsigned int* __restrict__ tstart,
-                                                 unsigned int* __restrict__ cstart,
-                                                 long long dcap, Stats* __restrict__ st,
-                                                 int4* __restrict__ sboxes) {
+// kScanBlocks + 1 blocks of kScanThreads threads.  Blocks [0, kScanBlocks):
+// kScanSlices 1024-bin slices each (16 bins per thread, 128-bit loads) of the
+// exclusive scan of the brick counts -> sort cursor (and zero the counts for
+// the next ROI), plus empty super-chunk boxes.  Last block: plane populations
+// (plane_bins_scan) -> start; 256-entry tile pairs per plane -> tstart;
+// 128-entry chunks per plane -> cstart.
+__global__ void __launch_bounds__(kScanThreads) scan_all(unsigned int* __restrict__ sort_counts,
+                                                         unsigned int* __restrict__ sort_cursor,
+                                                         const unsigned int* __restrict__ plane_counts,
+                                                         unsigned int* __restrict__ start,
+                                                         unsigned int* __restrict__ tstart,
+                                                         unsigned int* __restrict__ cstart,
+                                                         long long dcap, Stats* __restrict__ st,
+                                                         int4* __restrict__ sboxes) {
   pdl_enter();
   int bb[6];
 #pragma unroll
   for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
   if (bb[3] < 0) return;
+  const bool brick_block = blockIdx.x < kScanBlocks;
+  constexpr int kPerThread = (kScanSlices << kSortSliceBits) / kScanThreads;  // 16 bins
+  static_assert(kPerThread % 4 == 0, "bins are moved as uint4");
+  uint4* cnt4 = reinterpret_cast<uint4*>(
+      sort_counts + (long long)blockIdx.x * (kScanSlices << kSortSliceBits) + threadIdx.x * kPerThread);
   // More vertices than the diameter-side buffers hold: every later kernel
   // stands down (positions from the full histograms would overflow) and the
   // host re-runs the ROI with exact sizes.
-  const bool brick_block = blockIdx.x < kSortSupers;
   if ((long long)st->n_vert > dcap) {
     if (blockIdx.x == 0 && threadIdx.x == 0) st->ovf = 1u;
     if (brick_block)  // still leave the brick histogram zeroed for the next ROI
-      sort_counts[(blockIdx.x << kSortSliceBits) + threadIdx.x] = 0u;
+#pragma unroll
+      for (int k = 0; k < kPerThread / 4; k++) cnt4[k] = make_uint4(0u, 0u, 0u, 0u);
     return;
   }
   if (brick_block) {
@@ -75,27 +81,37 @@ __global__ void __launch_bounds__(1024) scan_all(unsigned int* __restrict__ sort
         sboxes[2 * t + 1] = make_int4(INT_MIN, INT_MIN, INT_MIN, 0);
       }
     }
-    // Slice b = fine bins [1024 b, 1024 b + 1024): base = super-bin prefix.
-    __shared__ unsigned int s_base[32];
+    // Block base = super-bin prefix of its first slice; within the block one
+    // scan over its kScanSlices slices (the super bins are their sums).
     const unsigned int* sup = sort_counts + kSortBins;
-    unsigned int pre = (threadIdx.x < blockIdx.x) ? sup[threadIdx.x] : 0u;
+    unsigned int base;
+    block_exscan(threadIdx.x < kScanSlices * blockIdx.x ? sup[threadIdx.x] : 0u, &base);
+    uint4 v[kPerThread / 4];
+    unsigned int sum = 0;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
-    if ((threadIdx.x & 31) == 0) s_base[threadIdx.x >> 5] = pre;
-    __syncthreads();
-    unsigned int base = 0;
-    for (int w = 0; w < kSortSupers / 32; w++) base += s_base[w];
-    __syncthreads();  // s_base is reused by the block scan below
-    const int i = (blockIdx.x << kSortSliceBits) + threadIdx.x;
-    const unsigned int v = sort_counts[i];
+    for (int k = 0; k < kPerThread / 4; k++) {
+      v[k] = cnt4[k];
+      sum += v[k].x + v[k].y + v[k].z + v[k].w;
+    }
     unsigned int total;
-    sort_cursor[i] = base + block_exscan_1024(v, &total);
-    sort_counts[i] = 0u;
+    unsigned int run = base + block_exscan(sum, &total);
+    uint4* cur4 = reinterpret_cast<uint4*>(
+        sort_cursor + (long long)blockIdx.x * (kScanSlices << kSortSliceBits) + threadIdx.x * kPerThread);
+#pragma unroll
+    for (int k = 0; k < kPerThread / 4; k++) {
+      uint4 o;
+      o.x = run; run += v[k].x;
+      o.y = run; run += v[k].y;
+      o.z = run; run += v[k].z;
+      o.w = run; run += v[k].w;
+      cur4[k] = o;
+      cnt4[k] = make_uint4(0u, 0u, 0u, 0u);
+    }
     return;
   }
   const PlaneSpace ps = plane_space(bb);
   const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
-  const int per = (P + 1023) / 1024;
+  const int per = (P + kScanThreads - 1) / kScanThreads;
   const int b = threadIdx.x * per, e = min(P, b + per);
   unsigned int s1 = 0, s2 = 0, s3 = 0;
   for (int i = b; i < e; i++) {
@@ -105,9 +121,9 @@ __global__ void __launch_bounds__(1024) scan_all(unsigned int* __restrict__ sort
     s3 += v >= 2 ? (v + kPlaneChunk - 1) / kPlaneChunk : 0u;
   }
   unsigned int t1, t2, t3;
-  unsigned int r1 = block_exscan_1024(s1, &t1);
-  unsigned int r2 = block_exscan_1024(s2, &t2);
-  unsigned int r3 = block_exscan_1024(s3, &t3);
+  unsigned int r1 = block_exscan(s1, &t1);
+  unsigned int r2 = block_exscan(s2, &t2);
+  unsigned int r3 = block_exscan(s3, &t3);
   for (int i = b; i < e; i++) {
     const unsigned int v = plane_counts[i];
     start[i] = r1;

@@ -90,6 +90,9 @@ constexpr int kSortBits = 18;
 constexpr int kSortBins = 1 << kSortBits;
 constexpr int kSortSliceBits = 10;                            // fine bins per scan block
 constexpr int kSortSupers = kSortBins >> kSortSliceBits;      // 256 super-bins
+constexpr int kScanThreads = 256;                           // scan_all block size
+constexpr int kScanSlices = 4;                              // 1024-bin slices per scan block
+constexpr int kScanBlocks = kSortSupers / kScanSlices;      // 64 brick-scan blocks
 constexpr int kChunk3 = 128;  // vertices per 3-D diameter chunk (pair unit = chunk x chunk)
 
 __device__ __forceinline__ unsigned int spread_bits(unsigned int v) {  // <= 10 bits -> every 3rd bit
@@ -320,6 +323,36 @@ __device__ __forceinline__ unsigned int block_exscan_1024(unsigned int v, unsign
   const unsigned int excl = x - v + (wid ? wsum[wid - 1] : 0u);
   *total = wsum[31];
   __syncthreads();  // wsum reusable after return
+  return excl;
+}
+
+// Exclusive scan of one value per thread across a block of any multiple of 32
+// threads (<= 1024).  Returns the exclusive prefix; *total receives the block
+// sum.  Must be called by all threads of the block.
+__device__ __forceinline__ unsigned int block_exscan(unsigned int v, unsigned int* total) {
+  __shared__ unsigned int wsum2[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned int t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
+  }
+  if (lane == 31) wsum2[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned int y = lane < nw ? wsum2[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned int t = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += t;
+    }
+    wsum2[lane] = y;
+  }
+  __syncthreads();
+  const unsigned int excl = x - v + (wid ? wsum2[wid - 1] : 0u);
+  *total = wsum2[nw - 1];
+  __syncthreads();  // wsum2 reusable after return
   return excl;
 }
 
