@@ -2,6 +2,8 @@
 // in a .cu file only so the library builds from one nvcc command.
 #include "host_crop.h"
 
+#include <immintrin.h>
+
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
@@ -85,9 +87,26 @@ Pool& pool() {
   return p;
 }
 
-// Any nonzero byte in p[0, n)?  Word-wide OR over the whole row (vectorisable,
-// no data-dependent exit inside a row: rows are short and mostly background).
-inline bool row_any(const uint8_t* p, int64_t n) {
+// Any nonzero byte in p[0, n)?  OR over the whole row (no data-dependent exit
+// inside a row: rows are short and mostly background).  The AVX2 form (4 x 32
+// B loads in flight per step) reads ~23 GB/s per core on the B200 hosts vs ~12
+// for the portable 64-bit form (tools/microbench/scan_bench.cpp).
+__attribute__((target("avx2"))) bool row_any_avx2(const uint8_t* p, int64_t n) {
+  __m256i acc = _mm256_setzero_si256();
+  int64_t i = 0;
+  for (; i + 128 <= n; i += 128) {
+    const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(p + i));
+    const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(p + i + 32));
+    const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(p + i + 64));
+    const __m256i d = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(p + i + 96));
+    acc = _mm256_or_si256(acc, _mm256_or_si256(_mm256_or_si256(a, b), _mm256_or_si256(c, d)));
+  }
+  bool any = !_mm256_testz_si256(acc, acc);
+  for (; i < n && !any; i++) any = p[i] != 0;
+  return any;
+}
+
+inline bool row_any_u64(const uint8_t* p, int64_t n) {
   uint64_t acc = 0;
   int64_t i = 0;
   for (; i + 32 <= n; i += 32) {
@@ -104,6 +123,10 @@ inline bool row_any(const uint8_t* p, int64_t n) {
 Slab occupied_slab(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, int threads) {
   struct Part {
     int64_t z0 = INT64_MAX, z1 = -1, y0 = INT64_MAX, y1 = -1, read = 0;
+  };
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  auto row_any = [](const uint8_t* p, int64_t n) {
+    return avx2 ? row_any_avx2(p, n) : row_any_u64(p, n);
   };
   const int64_t slice = nx * ny;
   // ~1 MB tasks: enough of them to balance, few enough to keep the counter cold.
