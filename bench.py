@@ -481,7 +481,7 @@ def run_ours(args):
         "config": cfg,
         "path": "sc_calculate_coefficients_device_batch (C ABI), device-resident masks",
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d_bytes),
-                "d2h_bytes_per_step": 2400,  # one Stats record (sc_device.cuh)
+                "d2h_bytes_per_step": 16800,  # one Stats record (sizeof(sc::Stats), 8 histogram copies)
                 "path": "sc_calculate_coefficients_batch (C ABI, pipelined) from pinned host "
                         "memory: host scan of every mask byte for the occupied z/y slab "
                         "(host_threads), then only that slab is copied H2D",

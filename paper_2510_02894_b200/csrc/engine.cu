@@ -625,10 +625,12 @@ void fill_out(const Stats& h, const double sp[3], sc_coeffs* out) {
   double area = 0.0;
   long long T = 0, active = 0;
   for (int k = 0; k < kNumCases; k++) {
-    if (!h.hist[k]) continue;
-    area += (double)h.hist[k] * at[k];
-    T += (long long)h.hist[k] * tri[k];
-    active += (long long)h.hist[k];
+    unsigned long long cnt = 0;
+    for (int c = 0; c < kHistCopies; c++) cnt += h.hist[c][k];
+    if (!cnt) continue;
+    area += (double)cnt * at[k];
+    T += (long long)cnt * tri[k];
+    active += (long long)cnt;
   }
   const long long K = h.vol_k < 0 ? -h.vol_k : h.vol_k;
   out->mesh_volume = (double)K * sp[0] * sp[1] * sp[2] / 48.0;

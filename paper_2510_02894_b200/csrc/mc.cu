@@ -260,7 +260,7 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
       const long long g = (long long)wbase + k;
       if (ok && g < cap) vkeys[g] = key;
       const unsigned int bin = brick_bin(key.x, key.y, key.z, bb, bshift);
-      group_add(sort_counts, bin, ok);
+      seg_add(sort_counts, bin, ok);
       if (ok) atomicAdd(&s_sup[bin >> kSortSliceBits], 1u);
       int id[3];
       unsigned int pbin[3];
@@ -268,7 +268,7 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
       plane_bins(key.x, key.y, key.z, pbk, pbin);
 #pragma unroll
       for (int a2 = 0; a2 < 3; a2++)
-        group_add(pbin_counts, (unsigned int)id[a2] * kPlaneBins + pbin[a2], ok);
+        seg_add(pbin_counts, (unsigned int)id[a2] * kPlaneBins + pbin[a2], ok);
     }
     __syncwarp();  // the stage is refilled next
   };
@@ -453,7 +453,8 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
                                    (unsigned long long)volk);
   __syncthreads();
   for (int i = threadIdx.x; i < kNumCases; i += blockDim.x)
-    if (s_hist[i]) atomicAdd(&st->hist[case_of_idx(i)], (unsigned long long)s_hist[i]);
+    if (s_hist[i])
+      atomicAdd(&st->hist[blockIdx.x % kHistCopies][case_of_idx(i)], (unsigned long long)s_hist[i]);
   if (sort_counts)
     for (int i = threadIdx.x; i < kSortSupers; i += blockDim.x)
       if (s_sup[i]) atomicAdd(&sort_counts[kSortBins + i], s_sup[i]);

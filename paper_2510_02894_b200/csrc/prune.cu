@@ -177,11 +177,11 @@ __global__ void scatter_all(const int4* __restrict__ keys, long long cap,
       plane_ids(k.x, k.y, k.z, ps, id);
       plane_bins(k.x, k.y, k.z, pbk, pb);
     }
-    const unsigned int pk = group_add(sort_cursor, bin, ok);
+    const unsigned int pk = seg_add(sort_cursor, bin, ok);
     unsigned int pos[3];
 #pragma unroll
     for (int a = 0; a < 3; a++)
-      pos[a] = group_add(pbin_cursor, (unsigned int)id[a] * kPlaneBins + pb[a], ok) +
+      pos[a] = seg_add(pbin_cursor, (unsigned int)id[a] * kPlaneBins + pb[a], ok) +
                (ok ? plane_start[id[a]] : 0u);
     if (ok) {
       keys_sorted[pk] = k;

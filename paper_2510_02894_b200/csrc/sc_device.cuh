@@ -10,8 +10,13 @@ constexpr int kNumCases = 256;
 // Device-resident accumulators of one ROI.  Every field is an exact integer
 // (or an fp bit pattern updated with integer atomicMax), so results do not
 // depend on block scheduling.
+// mc_cells blocks flush their case histograms into kHistCopies copies (block
+// index mod kHistCopies) so the end-of-kernel atomics of hundreds of blocks do
+// not all queue on the same 256 addresses; the host sums the copies.
+constexpr int kHistCopies = 8;
+
 struct Stats {
-  unsigned long long hist[kNumCases];  // active cells per MC case (0/255 never counted)
+  unsigned long long hist[kHistCopies][kNumCases];  // active cells per MC case (0/255 never counted)
   unsigned long long n_vert;           // crossed lattice edges == mesh vertices
   long long vol_k;                     // 48*volume/(sx*sy*sz), exact (Appendix A)
   int bbox[6];                         // xmin, ymin, zmin, xmax, ymax, zmax of occupied voxels
@@ -191,6 +196,25 @@ __device__ __forceinline__ unsigned int group_add(unsigned int* base, unsigned i
   if (ok && lane == leader) pos = atomicAdd(base + id, (unsigned int)__popc(peers));
   pos = __shfl_sync(0xffffffffu, pos, leader);
   return pos + __popc(peers & ((1u << lane) - 1));
+}
+
+// Same contract as group_add, aggregating runs of equal ids in consecutive
+// lanes (one shuffle + two ballots instead of __match_any_sync).  Vertices
+// arrive in emission order, so equal bins are mostly adjacent; an id that
+// recurs after a break simply takes a second atomic.
+__device__ __forceinline__ unsigned int seg_add(unsigned int* base, unsigned int id, bool ok) {
+  const int lane = threadIdx.x & 31;
+  const unsigned int prev = __shfl_up_sync(0xffffffffu, id, 1);
+  const unsigned int okm = __ballot_sync(0xffffffffu, ok);
+  const bool start = ok && (lane == 0 || !((okm >> (lane - 1)) & 1u) || prev != id);
+  const unsigned int starts = __ballot_sync(0xffffffffu, start);
+  const unsigned int upto = (2u << lane) - 1u;  // bits 0..lane (all bits for lane 31)
+  const int leader = 31 - __clz(starts & upto);
+  const unsigned int after = (starts | ~okm) & ~upto;  // segment breaks past this lane
+  unsigned int pos = 0;
+  if (start) pos = atomicAdd(base + id, (unsigned int)((after ? __ffs(after) - 1 : 32) - lane));
+  pos = __shfl_sync(0xffffffffu, pos, leader & 31);
+  return pos + (unsigned int)(lane - leader);
 }
 
 // Last-block ticket: returns true in exactly one block, after every block of
