@@ -1,0 +1,22 @@
+#!/bin/bash
+# Round-end evidence: parity tests, smoke, default bench (with CPU baseline),
+# per-workload bench lines, C3 split line, ncu launch lists + full capture.
+set -u
+mkdir -p gpurun_out
+OUT=gpurun_out
+timeout 900 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+timeout 900 python bench.py --steps 20 --warmup 5 > $OUT/bench.json 2> $OUT/bench.err
+for w in c1 c3 c4 c5; do
+  timeout 600 python bench.py --steps 20 --warmup 5 --workload $w --no-cpu-baseline > $OUT/bench_$w.json 2> $OUT/bench_$w.err
+done
+timeout 600 python bench.py --steps 5 --warmup 3 --workload c3 --split > $OUT/bench_c3_split.json 2> $OUT/bench_c3_split.err
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file $OUT/launches.csv python tools/one_roi.py > $OUT/ncu_bench.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file $OUT/launches_c3.csv python tools/one_roi.py c3 > $OUT/ncu_bench_c3.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on \
+    -k regex:"pack_bits_v16|bits_bbox|mc_cells|plane_bins_scan|scan_all|scatter_all|boxes_extremes|unit_filter|plane_boxes|plane_lb|plane_filter|diam_pass1|diam_refine" -s 13 -c 13 \
+    -o $OUT/prof -f python tools/one_roi.py > $OUT/ncu_full.log 2>&1
+echo done
