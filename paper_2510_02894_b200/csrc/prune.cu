@@ -163,32 +163,45 @@ __global__ void scatter_all(const int4* __restrict__ keys, long long cap,
   const int s = brick_shift(bb);
   const PlaneSpace ps = plane_space(bb);
   const PlaneBricks pbk = plane_bricks(bb);
-  for (long long base = (long long)blockIdx.x * blockDim.x; base < n;
-       base += (long long)gridDim.x * blockDim.x) {
-    const long long v = base + threadIdx.x;
-    const bool ok = v < n;
-    int4 k = make_int4(0, 0, 0, 0);
-    int id[3] = {0, 0, 0};
-    unsigned int pb[3] = {0u, 0u, 0u};
-    unsigned int bin = 0;
-    if (ok) {
-      k = keys[v];
-      bin = brick_bin(k.x, k.y, k.z, bb, s);
-      plane_ids(k.x, k.y, k.z, ps, id);
-      plane_bins(k.x, k.y, k.z, pbk, pb);
-    }
-    const unsigned int pk = seg_add(sort_cursor, bin, ok);
-    unsigned int pos[3];
+  // Two vertices per thread per step (the second one grid-stride away), so
+  // the key loads, cursor atomics and start loads of both are in flight
+  // together: the loop is a chain of dependent memory round trips.
+  constexpr int kU = 2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += kU * stride) {
+    bool ok[kU];
+    int4 k[kU];
+    int id[kU][3];
+    unsigned int pb[kU][3], bin[kU];
 #pragma unroll
-    for (int a = 0; a < 3; a++)
-      pos[a] = seg_add(pbin_cursor, (unsigned int)id[a] * kPlaneBins + pb[a], ok) +
-               (ok ? plane_start[id[a]] : 0u);
-    if (ok) {
-      keys_sorted[pk] = k;
-      plane_sorted[pos[0]] = make_int2(k.x, k.y);
-      plane_sorted[pos[1]] = make_int2(k.x, k.z);
-      plane_sorted[pos[2]] = make_int2(k.y, k.z);
+    for (int u = 0; u < kU; u++) {
+      const long long v = base + u * stride + threadIdx.x;
+      ok[u] = v < n;
+      k[u] = ok[u] ? keys[v] : make_int4(0, 0, 0, 0);
     }
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      bin[u] = brick_bin(k[u].x, k[u].y, k[u].z, bb, s);
+      plane_ids(k[u].x, k[u].y, k[u].z, ps, id[u]);
+      plane_bins(k[u].x, k[u].y, k[u].z, pbk, pb[u]);
+    }
+    unsigned int pk[kU], pos[kU][3];
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      pk[u] = seg_add(sort_cursor, bin[u], ok[u]);
+#pragma unroll
+      for (int a = 0; a < 3; a++)
+        pos[u][a] = seg_add(pbin_cursor, (unsigned int)id[u][a] * kPlaneBins + pb[u][a], ok[u]) +
+                    (ok[u] ? plane_start[id[u][a]] : 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; u++)
+      if (ok[u]) {
+        keys_sorted[pk[u]] = k[u];
+        plane_sorted[pos[u][0]] = make_int2(k[u].x, k[u].y);
+        plane_sorted[pos[u][1]] = make_int2(k[u].x, k[u].z);
+        plane_sorted[pos[u][2]] = make_int2(k[u].y, k[u].z);
+      }
   }
 }
 
