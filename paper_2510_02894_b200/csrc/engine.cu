@@ -33,11 +33,11 @@ namespace sc {
 // Kernels (mc.cu, diameter.cu, prune.cu, planar.cu).
 __global__ void init_stats(Stats* st);
 template <int U, bool BOX>
-__global__ void pack_bits_v16(const RoiParams*, uint32_t*, Stats*);
-__global__ void bits_bbox(const RoiParams*, const uint4*, Stats*);
-__global__ void pack_bits_generic(const RoiParams*, uint32_t*, Stats*);
+__global__ void pack_bits_v16(const RoiParams*, uint32_t*, Stats*, uint32_t*);
+__global__ void bits_bbox(const RoiParams*, const uint4*, Stats*, const uint32_t*);
+__global__ void pack_bits_generic(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 __global__ void mc_cells(const RoiParams*, const uint32_t*, const CaseTables*, Stats*, int4*,
-                         long long, unsigned int*, unsigned int*);
+                         long long, unsigned int*, unsigned int*, const uint32_t*);
 __global__ void plane_bins_scan(unsigned int*, unsigned int*, unsigned int*, unsigned long long*,
                                 const Stats*);
 __global__ void scan_all(unsigned int*, unsigned int*, const unsigned int*, unsigned int*,
@@ -99,6 +99,7 @@ std::atomic<long long> g_opt_dcap{2LL << 20};  // default diameter-side vertex c
 std::atomic<long long> g_opt_wcap{1LL << 20};  // default 3-D work-list capacity (chunk pairs)
 std::atomic<bool> g_opt_batch_times{false};  // per-stage event nodes in batch graphs
 std::atomic<bool> g_opt_pdl{false};  // programmatic dependent launch in batch graphs
+std::atomic<bool> g_opt_sparse{true};  // sparse bit volume (segment map), option "sparse_bits"
 std::atomic<int> g_opt_grid_div{2};  // divisor of the latency-bound kernel grids (2: best measured batch rate)
 std::atomic<int> g_opt_pack_bps{0};  // pack blocks per SM (0 = occupancy limit)  // divisor of the latency-bound kernels' grids
 std::atomic<int> g_opt_pack_mode{0};  // bit 0: one step per pack block; bit 1: low-priority pack;
@@ -223,6 +224,7 @@ struct Ctx {
   long long dcap_sz = 0;      // vertices the diameter-side buffers are sized for (monotonic)
   CaseTables* d_tabs = nullptr;
   DevBuf<uint32_t> bits;
+  DevBuf<uint32_t> segmap;  // 1 bit per 16-word bit-volume segment (sparse pack)
   DevBuf<int4> keys, keys_sorted, boxes, sboxes;  // chunk / super-chunk boxes (lo, hi)
   DevBuf<int4> hboxes;  // boxes of the two 64-vertex halves of every chunk
   DevBuf<unsigned int> sort_counts, sort_cursor;
@@ -253,6 +255,7 @@ struct Ctx {
     int grid_div;       // option "grid_div"
     bool events;        // per-stage event nodes present
     bool pdl;           // option "pdl"
+    bool sparse;        // option "sparse_bits"
     unsigned long long gen;
     cudaGraphExec_t exec;
     unsigned long long launches;
@@ -264,7 +267,7 @@ struct Ctx {
 
   unsigned long long fingerprint() const {
     unsigned long long h = 1469598103934665603ull;
-    const void* ps[] = {bits.p, keys.p, keys_sorted.p, boxes.p, sboxes.p, hboxes.p,
+    const void* ps[] = {bits.p, segmap.p, keys.p, keys_sorted.p, boxes.p, sboxes.p, hboxes.p,
                         sort_counts.p, sort_cursor.p,
                         work.p, warp_max.p, plane_umax.p,
                         plane_counts.p, plane_start.p, plane_tstart.p, plane_sorted.p,
@@ -407,6 +410,7 @@ int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, lo
   dcap = c->dcap_sz = std::max(c->dcap_sz, dcap);
   const int W = (int)((nx + 31) / 32);
   CK(c->bits.ensure((size_t)((long long)W * ny * nz)));
+  CK(c->segmap.ensure(c->bits.cap / 512 + 1));
   CK(c->keys.ensure((size_t)cap));
   const long long C = (dcap + kChunk - 1) / kChunk;  // chunk pairs: C(C+1)/2
   const long long wc = std::min(C * (C + 1) / 2, std::max(g_opt_wcap.load(), wunits));
@@ -488,11 +492,14 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   const long long cap = (long long)c->keys.cap, dcap = c->dcap_sz;
   init_stats<<<1, 256, 0, s>>>(c->d_stats);
   CKL(1);
+  if (g_opt_sparse.load())  // the pack marks nonzero segments of a cleared map
+    CK(cudaMemsetAsync(c->segmap.p, 0, sizeof(uint32_t) * c->segmap.cap, s));
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[0], s));  // kev0..kev1 = the HBM pass alone
   if (fast && g_opt_fbox.load()) {
     pack_bits_v16<4, true><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(rp, c->bits.p,
-                                                                              c->d_stats);
+                                                                              c->d_stats,
+                                                                              c->segmap.p);
     CKL(1);
     if (++nk >= lim) return SC_OK;
     CK(record(c, c->kev[1], s));
@@ -517,28 +524,32 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
     if (!(pm & 4)) {  // bit 2 (debug, timing only): reuse the slot's previous bit volume
       const int pu = (pm >> 3) & 3;  // bits 3-4 (experiment): 16-byte loads in flight per thread
       if (pu == 1)
-        CK(cudaLaunchKernelEx(&cfg, pack_bits_v16<8, false>, rp, c->bits.p, c->d_stats));
+        CK(cudaLaunchKernelEx(&cfg, pack_bits_v16<8, false>, rp, c->bits.p, c->d_stats,
+                                  c->segmap.p));
       else if (pu == 2)
-        CK(cudaLaunchKernelEx(&cfg, pack_bits_v16<16, false>, rp, c->bits.p, c->d_stats));
+        CK(cudaLaunchKernelEx(&cfg, pack_bits_v16<16, false>, rp, c->bits.p, c->d_stats,
+                                  c->segmap.p));
       else
-        CK(cudaLaunchKernelEx(&cfg, pack_bits_v16<4, false>, rp, c->bits.p, c->d_stats));
+        CK(cudaLaunchKernelEx(&cfg, pack_bits_v16<4, false>, rp, c->bits.p, c->d_stats,
+                                  c->segmap.p));
       CKL(1);
     }
     if (++nk >= lim) return SC_OK;
     CK(record(c, c->kev[1], s));
     CK(launch_k(c, s, lgrid(c, 4), 256, bits_bbox, rp, reinterpret_cast<const uint4*>(c->bits.p),
-                                         c->d_stats));
+                                         c->d_stats, c->segmap.p));
     CKL(1);
     if (++nk >= lim) return SC_OK;
   } else {
-    pack_bits_generic<<<lgrid(c, 8), 256, 0, s>>>(rp, c->bits.p, c->d_stats);  // after init_stats: no PDL
+    pack_bits_generic<<<lgrid(c, 8), 256, 0, s>>>(rp, c->bits.p, c->d_stats,
+                                                  c->segmap.p);  // after init_stats: no PDL
     CKL(1);
     if (++nk >= lim) return SC_OK;
     CK(record(c, c->kev[1], s));
   }
   CK(launch_k(c, s, lgrid(c, std::max(1, c->occ_mc)), 256, mc_cells, rp, c->bits.p, c->d_tabs, c->d_stats,
                                                           c->keys.p, cap, c->sort_counts.p,
-                                                          c->pbin_counts.p));
+                                                          c->pbin_counts.p, c->segmap.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[2], s));
@@ -691,7 +702,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   h.W = (int)((nx + 31) / 32);
   h.n_words = (long long)h.W * ny * nz;
   h.n_chunks = nx * ny * nz / 16;
-  h.pad = 0;
+  h.sparse = g_opt_sparse.load() ? 1 : 0;
   h.f.cx2 = h.f.cy2 = h.f.cz2 = 0;  // set on the device from the bbox
   h.f.hx = (float)(0.5 * sp[0]);
   h.f.hy = (float)(0.5 * sp[1]);
@@ -719,6 +730,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
         g.packmode == g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load() &&
         g.grid_div == g_opt_grid_div.load() &&
         g.events == c->events_on && g.pdl == g_opt_pdl.load() &&
+        g.sparse == g_opt_sparse.load() &&
         g.gen == c->gen) {
       CK(cudaGraphLaunch(g.exec, s));
       if (hp) g_hprof.launch += wall_ms() - t0;
@@ -747,7 +759,8 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   Ctx::GraphEntry g{fast, s, shard, nshards, d_sq4, cap, dcap, prune, packed, fbox,
                     g_opt_stages.load(), g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load(),
                     g_opt_grid_div.load(),
-                    c->events_on, g_opt_pdl.load(), c->gen, exec, launches};
+                    c->events_on, g_opt_pdl.load(), g_opt_sparse.load(), c->gen, exec,
+                    launches};
   c->graphs.push_back(g);
   CK(cudaGraphLaunch(exec, s));
   g_launches.fetch_add(launches, std::memory_order_relaxed);
@@ -1066,6 +1079,7 @@ int run_mesh(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
   for (int attempt = 0; attempt < 2; attempt++) {
     const unsigned long long fp0 = c->fingerprint();
     CK(c->bits.ensure((size_t)(((nx + 31) / 32) * ny * nz)));
+    CK(c->segmap.ensure(c->bits.cap / 512 + 1));
     CK(c->keys.ensure((size_t)cap));
     if (c->fingerprint() != fp0) {  // scratch moved: cached ROI graphs are stale
       c->gen++;
@@ -1080,22 +1094,23 @@ int run_mesh(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
     h.f.hx = (float)(0.5 * sp[0]); h.f.hy = (float)(0.5 * sp[1]); h.f.hz = (float)(0.5 * sp[2]);
     h.f.sx = sp[0]; h.f.sy = sp[1]; h.f.sz = sp[2];
     h.f.ox2 = h.f.oy2 = h.f.oz2 = 0;
+    h.sparse = 0;  // the export kernels read every bit-volume word
     h.wcap = 0;
     CK(cudaMemcpyAsync(c->d_rp, c->h_rp, sizeof(RoiParams), cudaMemcpyHostToDevice, s));
     init_stats<<<1, 256, 0, s>>>(c->d_stats);
     CKL(1);
     if (nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0) {
       pack_bits_v16<4, true><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(
-          c->d_rp, c->bits.p, c->d_stats);
+          c->d_rp, c->bits.p, c->d_stats, c->segmap.p);
       CKL(1);
     } else {
-      pack_bits_generic<<<c->sms * 8, 256, 0, s>>>(c->d_rp, c->bits.p, c->d_stats);
+      pack_bits_generic<<<c->sms * 8, 256, 0, s>>>(c->d_rp, c->bits.p, c->d_stats, c->segmap.p);
       CKL(1);
     }
     mc_cells<<<c->sms * std::max(1, c->occ_mc), 256, 0, s>>>(c->d_rp, c->bits.p, c->d_tabs,
                                                             c->d_stats, c->keys.p,
                                                             (long long)c->keys.cap, nullptr,
-                                                            nullptr);
+                                                            nullptr, c->segmap.p);
     CKL(1);
     CK(cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -1467,6 +1482,7 @@ int sc_set_option(const char* name, int value) {
   else if (std::strcmp(name, "pack_bps") == 0) g_opt_pack_bps = std::max(0, value);
   else if (std::strcmp(name, "grid_div") == 0) g_opt_grid_div = std::max(1, value);
   else if (std::strcmp(name, "pdl") == 0) g_opt_pdl = value != 0;
+  else if (std::strcmp(name, "sparse_bits") == 0) g_opt_sparse = value != 0;
   else if (std::strcmp(name, "batch_stage_times") == 0) g_opt_batch_times = value != 0;
   else if (std::strcmp(name, "host_threads") == 0) g_opt_host_threads = std::max(1, value);
   else if (std::strcmp(name, "debug_stages") == 0) g_opt_stages = value > 0 ? value : (1 << 30);

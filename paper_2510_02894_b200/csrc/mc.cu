@@ -80,13 +80,21 @@ struct BoxAcc {
 //
 // BOX: also accumulate the occupied bbox in registers (32-bit index math, only
 // for nonzero words) and flush it once per warp -- replaces bits_bbox.
+//
+// SPARSE (rp->sparse): a warp-wide load is exactly one 16-word segment of the
+// bit volume; all-background segments are not written at all (only the
+// nonzero ones, and their bit in the segment map), so the HBM write of the
+// bit volume shrinks to the occupied rows and no later pass has to re-read a
+// full bit volume (bits_bbox walks the map).
 template <int U, bool BOX>
 __global__ void __launch_bounds__(256) pack_bits_v16(const RoiParams* __restrict__ rp,
                                                      uint32_t* __restrict__ bits,
-                                                     Stats* __restrict__ st) {
+                                                     Stats* __restrict__ st,
+                                                     uint32_t* __restrict__ segmap) {
   const uint4* __restrict__ mask = reinterpret_cast<const uint4*>(rp->mask);
   const long long n_chunks = rp->n_chunks;
   const unsigned int W = (unsigned int)rp->W, ny = (unsigned int)rp->ny;
+  const bool sparse = rp->sparse != 0;
   BoxAcc box;
   const long long step = (long long)gridDim.x * blockDim.x * U;
   for (long long base = (long long)blockIdx.x * blockDim.x * U; base < n_chunks; base += step) {
@@ -102,6 +110,13 @@ __global__ void __launch_bounds__(256) pack_bits_v16(const RoiParams* __restrict
       const uint32_t b16 = nib4(v[k].x) | (nib4(v[k].y) << 4) | (nib4(v[k].z) << 8) |
                            (nib4(v[k].w) << 12);
       const uint32_t word = b16 | (__shfl_down_sync(kFull, b16, 1) << 16);
+      if (sparse) {
+        if (!__any_sync(kFull, word != 0u && !(threadIdx.x & 1) && g < n_chunks)) continue;
+        if ((threadIdx.x & 31) == 0) {
+          const long long seg = g >> 5;  // lane 0 holds the segment's first chunk
+          atomicOr(segmap + (seg >> 5), 1u << (seg & 31));
+        }
+      }
       if (!(threadIdx.x & 1) && g < n_chunks) {
         bits[g >> 1] = word;
         if (BOX && word) {
@@ -122,12 +137,42 @@ __global__ void __launch_bounds__(256) pack_bits_v16(const RoiParams* __restrict
 // nonzero words locate themselves.  Four 16-byte loads in flight per thread.
 __global__ void __launch_bounds__(256) bits_bbox(const RoiParams* __restrict__ rp,
                                                  const uint4* __restrict__ bits4,
-                                                 Stats* __restrict__ st) {
+                                                 Stats* __restrict__ st,
+                                                 const uint32_t* __restrict__ segmap) {
   pdl_enter();
   constexpr int kU = 4;
   const long long n_words = rp->n_words;
   const int W = rp->W, ny = (int)rp->ny;
   BoxAcc box;
+  if (rp->sparse) {
+    // Only the marked segments (the occupied rows) are read: one thread per
+    // segment, its 16 words as 4 x 16 bytes.
+    const long long n_seg = (n_words + 15) / 16;
+    const uint32_t* bits = reinterpret_cast<const uint32_t*>(bits4);
+    for (long long sgi = (long long)blockIdx.x * blockDim.x + threadIdx.x; sgi < n_seg;
+         sgi += (long long)gridDim.x * blockDim.x) {
+      if (!seg_on(segmap, 16 * sgi)) continue;
+      if (16 * sgi + 16 <= n_words) {
+        uint4 v[4];
+#pragma unroll
+        for (int t = 0; t < 4; t++) v[t] = __ldcg(bits4 + 4 * sgi + t);
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+          const uint32_t w4[4] = {v[t].x, v[t].y, v[t].z, v[t].w};
+#pragma unroll
+          for (int u = 0; u < 4; u++)
+            if (w4[u]) box.add(w4[u], 16 * sgi + 4 * t + u, W, ny);
+        }
+      } else {
+        for (long long wi = 16 * sgi; wi < n_words; wi++) {
+          const uint32_t w = __ldcg(bits + wi);
+          if (w) box.add(w, wi, W, ny);
+        }
+      }
+    }
+    box.flush(st);
+    return;
+  }
   const long long n4 = n_words / 4;
   const long long step = (long long)gridDim.x * blockDim.x * kU;
   for (long long base = (long long)blockIdx.x * blockDim.x * kU; base < n4; base += step) {
@@ -160,7 +205,8 @@ __global__ void __launch_bounds__(256) bits_bbox(const RoiParams* __restrict__ r
 // (still coalesced across the warp within a row).
 __global__ void __launch_bounds__(256) pack_bits_generic(const RoiParams* __restrict__ rp,
                                                          uint32_t* __restrict__ bits,
-                                                         Stats* __restrict__ st) {
+                                                         Stats* __restrict__ st,
+                                                         uint32_t* __restrict__ segmap) {
   const uint8_t* __restrict__ mask = rp->mask;
   const long long n_words = rp->n_words;
   const int nx = (int)rp->nx, W = rp->W, ny = (int)rp->ny;
@@ -175,8 +221,11 @@ __global__ void __launch_bounds__(256) pack_bits_generic(const RoiParams* __rest
       int n = min(32, nx - 32 * w);
       uint32_t word = 0;
       for (int b = 0; b < n; b++) word |= (uint32_t)(__ldcs(src + b) != 0) << b;
-      bits[wi] = word;
-      if (word) box.add(word, wi, W, ny);
+      bits[wi] = word;  // every word is written; the map marks the nonzero ones
+      if (word) {
+        box.add(word, wi, W, ny);
+        if (rp->sparse) atomicOr(segmap + (wi >> 9), 1u << ((wi >> 4) & 31));
+      }
     }
   }
   box.flush(st);
@@ -205,14 +254,26 @@ __device__ __forceinline__ int case_of_idx(int idx) {
   return (~occ) & 0xff;
 }  // staged vertices per warp and z step (denser steps emit directly)
 
-__device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits, int q, int v, int w,
-                                          int W, int ny, int nz, bool on, uint32_t& cur,
-                                          uint32_t& prev) {
+// Words q and q - 1 of row (v, w); with a sparse bit volume, words of
+// unmarked segments read as 0 (the word and its map bit are loaded together).
+__device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits,
+                                          const uint32_t* __restrict__ segmap, bool sparse, int q,
+                                          int v, int w, int W, int ny, int nz, bool on,
+                                          uint32_t& cur, uint32_t& prev) {
   cur = prev = 0u;
   if (on && v >= 0 && v < ny && w >= 0 && w < nz) {
-    const uint32_t* row = bits + ((long long)w * ny + v) * W;
+    const long long rb = ((long long)w * ny + v) * W;
+    const uint32_t* row = bits + rb;
     if (q < W) cur = row[q];
     if (q > 0) prev = row[q - 1];
+    if (sparse) {
+      // segments of words q and q - 1 (one map word unless they straddle one)
+      const long long wc = rb + q, wp = wc - 1;
+      const uint32_t mc = __ldg(segmap + (wc >> 9));
+      const uint32_t mp = ((wp >> 9) == (wc >> 9)) ? mc : __ldg(segmap + (wp >> 9));
+      if (!((mc >> ((wc >> 4) & 31)) & 1u)) cur = 0u;
+      if (!((mp >> ((wp >> 4) & 31)) & 1u)) prev = 0u;
+    }
   }
 }
 
@@ -230,13 +291,16 @@ __device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits, int
 // its (plane, in-plane brick) bin in each of its three planes (global).
 template <int KZ>
 __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict__ rp,
-                                        const uint32_t* __restrict__ bits, Stats* __restrict__ st,
+                                        const uint32_t* __restrict__ bits,
+                                        const uint32_t* __restrict__ segmap,
+                                        Stats* __restrict__ st,
                                         int4* __restrict__ vkeys, long long cap,
                                         unsigned int* __restrict__ sort_counts,
                                         unsigned int* __restrict__ pbin_counts, const int* bb,
                                         unsigned int* s_hist, const int4* s_tn,
                                         unsigned int* s_sup, int4 (*s_stage)[kStage]) {
   const int ny = (int)rp->ny, nz = (int)rp->nz, W = rp->W;
+  const bool sparse = rp->sparse != 0;
   const PlaneSpace ps = plane_space(bb);
   const PlaneBricks pbk = plane_bricks(bb);
   const int bshift = brick_shift(bb);
@@ -294,8 +358,8 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
 #pragma unroll
       for (int s = 0; s <= KZ; s++) {
         const bool on = valid && s <= kz && w0 + s <= whi + 1;
-        row_words(bits, q, v, w0 + s, W, ny, nz, on, c0[s], p0[s]);
-        row_words(bits, q, v + 1, w0 + s, W, ny, nz, on, c1[s], p1[s]);
+        row_words(bits, segmap, sparse, q, v, w0 + s, W, ny, nz, on, c0[s], p0[s]);
+        row_words(bits, segmap, sparse, q, v + 1, w0 + s, W, ny, nz, on, c1[s], p1[s]);
       }
       const int xbase = 32 * q - 1;
 #pragma unroll
@@ -417,7 +481,8 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
                                                 const CaseTables* __restrict__ tabs,
                                                 Stats* __restrict__ st, int4* __restrict__ vkeys,
                                                 long long cap, unsigned int* __restrict__ sort_counts,
-                                                unsigned int* __restrict__ pbin_counts) {
+                                                unsigned int* __restrict__ pbin_counts,
+                                                const uint32_t* __restrict__ segmap) {
   pdl_enter();
   __shared__ unsigned int s_hist[kNumCases];
   __shared__ int4 s_tn[kNumCases];
@@ -443,8 +508,8 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
   }
   for (int i = threadIdx.x; i < kSortSupers; i += blockDim.x) s_sup[i] = 0;
   __syncthreads();
-  long long volk = mc_body<4>(kz, rp, bits, st, vkeys, cap, sort_counts, pbin_counts, bb, s_hist,
-                              s_tn, s_sup, s_stage);
+  long long volk = mc_body<4>(kz, rp, bits, segmap, st, vkeys, cap, sort_counts, pbin_counts, bb,
+                              s_hist, s_tn, s_sup, s_stage);
   const int lane = threadIdx.x & 31;
   // Block flush: exact integer partials.
 #pragma unroll
@@ -461,9 +526,9 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
 }
 
 
-template __global__ void pack_bits_v16<4, false>(const RoiParams*, uint32_t*, Stats*);
-template __global__ void pack_bits_v16<8, false>(const RoiParams*, uint32_t*, Stats*);
-template __global__ void pack_bits_v16<16, false>(const RoiParams*, uint32_t*, Stats*);
-template __global__ void pack_bits_v16<4, true>(const RoiParams*, uint32_t*, Stats*);
+template __global__ void pack_bits_v16<4, false>(const RoiParams*, uint32_t*, Stats*, uint32_t*);
+template __global__ void pack_bits_v16<8, false>(const RoiParams*, uint32_t*, Stats*, uint32_t*);
+template __global__ void pack_bits_v16<16, false>(const RoiParams*, uint32_t*, Stats*, uint32_t*);
+template __global__ void pack_bits_v16<4, true>(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 
 }  // namespace sc

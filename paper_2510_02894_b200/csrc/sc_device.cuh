@@ -62,6 +62,12 @@ struct Frame {
   double sx, sy, sz;   // spacing (fp64, reference arithmetic)
 };
 
+// Bit-volume segment map: bit s set <=> words [16 s, 16 s + 16) hold a nonzero
+// word (one warp-wide 512-byte mask load of the pack = one segment).
+__device__ __forceinline__ bool seg_on(const uint32_t* __restrict__ segmap, long long wi) {
+  return (__ldg(segmap + (wi >> 9)) >> ((wi >> 4) & 31)) & 1u;
+}
+
 // Per-ROI launch parameters, read by the kernels from device memory (one
 // record per pipeline slot, written by a 96-byte H2D copy before each launch),
 // so a slot's captured CUDA graph is independent of the mask pointer, the
@@ -72,7 +78,9 @@ struct RoiParams {
   long long n_chunks;  // nx*ny*nz/16 (fast pack path)
   long long n_words;   // W*ny*nz
   int W;               // 32-bit words per bit-volume row
-  int pad;
+  int sparse;          // 1: the pack writes only nonzero 16-word segments of the bit
+                       // volume and marks them in the segment map; readers treat
+                       // unmarked segments as zero (0: every word is written)
   Frame f;             // cx2..cz2 are filled on the device from the bbox
   long long wcap;      // capacity of the 3-D work list (overflow -> exact re-run)
 };
