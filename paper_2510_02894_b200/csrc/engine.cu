@@ -492,7 +492,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   const long long cap = (long long)c->keys.cap, dcap = c->dcap_sz;
   init_stats<<<1, 256, 0, s>>>(c->d_stats);
   CKL(1);
-  if (g_opt_sparse.load())  // the pack marks nonzero segments of a cleared map
+  if (g_opt_sparse.load() && !(g_opt_pack_mode.load() & 4))  // the pack marks a cleared map
     CK(cudaMemsetAsync(c->segmap.p, 0, sizeof(uint32_t) * c->segmap.cap, s));
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[0], s));  // kev0..kev1 = the HBM pass alone
