@@ -165,7 +165,10 @@ int sc_last_diagnostics(int device, int64_t* out, int n);
  * "grid_div" (2) = divisor of the per-ROI kernels' grids (SMs x blocks/SM):
  * fewer resident blocks per ROI let more ROIs share the GPU;
  * "batch_stage_times" (0) = per-stage CUDA events in batch graphs (mesh_ms /
- * diameters_ms of batch results are 0 without them).
+ * diameters_ms of batch results are 0 without them);
+ * "sparse_bits" (1) = the pack writes only nonzero 16-word segments of the
+ * bit volume (segment map); "pdl" (0) = programmatic dependent launch of the
+ * per-ROI kernels in batch graphs.
  * Results are identical either way; 0 on success, SC_ERR_INPUT otherwise. */
 int sc_set_option(const char* name, int value);
 uint64_t sc_launch_count(void);
