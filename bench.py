@@ -346,13 +346,13 @@ def run_ours(args):
     step_sps = [sps[i % len(sps)] for i in range(K)]
 
     # ---- device-resident throughput (value): K ROIs through the pipelined
-    # device batch entry (8 slots: ROI i+1 is enqueued before ROI i is
+    # device batch entry (16 slots: ROI i+16 is enqueued when ROI i is
     # collected), CUDA events on `stream`, which the batch is ordered against.
     clocks = ClockSampler(dev)
     W = args.warmup
-    # W warm-up steps, and at least two rounds over the 8 pipeline slots so every
-    # slot has captured its CUDA graph before the timed region.
-    Ww = max(W, 16)
+    # W warm-up steps, and at least two rounds over the 16 pipeline slots so
+    # every slot has captured its CUDA graph before the timed region.
+    Ww = max(W, 32)
     sc.calculate_coefficients_device_batch([d_masks[i % len(d_masks)] for i in range(Ww)],
                                            [sps[i % len(sps)] for i in range(Ww)], stream=stream)
     torch.cuda.synchronize()

@@ -113,8 +113,8 @@ int sc_calculate_coefficients_shard(const uint8_t* d_mask, int64_t nx, int64_t n
                                     int nshards, double* d_sq4, sc_coeffs* out);
 
 /* Batch of ROIs on one device (C4): masks[i] are host pointers with dims
- * dims[3*i..3*i+2] and spacing spacings[3*i..]; out[i] per ROI.  Up to 8
- * pipeline slots (option "slots") round-robin, so the H2D copy and kernels of
+ * dims[3*i..3*i+2] and spacing spacings[3*i..]; out[i] per ROI.  Up to 16
+ * pipeline slots (option "slots", default 16) round-robin, so the H2D copy and kernels of
  * the next ROIs overlap the current one's.
  * The first failing ROI's code is returned; later ROIs are still processed. */
 int sc_calculate_coefficients_batch(const uint8_t* const* masks, const int64_t* dims,
@@ -158,7 +158,7 @@ int sc_last_kernel_times(int device, double* ms, int n);
 int sc_last_diagnostics(int device, int64_t* out, int n);
 /* Process-wide switches: "prune" (default 1) = exact bbox pruning of 3-D and
  * planar work units; "pass1_packed" (1) = FFMA2 variant of the 3-D pass;
- * "graphs" (1) = replay each ROI pipeline as a cached CUDA graph; "slots" (8)
+ * "graphs" (1) = replay each ROI pipeline as a cached CUDA graph; "slots" (16)
  * = pipeline slots (stream + scratch) the batch entries keep in flight;
  * "host_crop" (1) = host-mask entries copy only the occupied z/y slab;
  * "host_threads" (hardware threads, <= 32) = threads of the host slab scan;

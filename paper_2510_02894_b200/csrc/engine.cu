@@ -94,7 +94,7 @@ thread_local std::string g_err;
 std::atomic<bool> g_opt_prune{true}, g_opt_packed{true}, g_opt_graphs{true};
 std::atomic<int> g_opt_stages{1 << 30};  // debug: kernels enqueued per ROI
 std::atomic<bool> g_opt_fbox{false};  // bbox accumulated inside the pack (else bits_bbox; measured faster)
-std::atomic<int> g_opt_slots{8};  // pipeline slots used by the batch entries
+std::atomic<int> g_opt_slots{16};  // pipeline slots used by the batch entries (measured: 16 > 12 > 8)
 std::atomic<long long> g_opt_dcap{2LL << 20};  // default diameter-side vertex capacity
 std::atomic<long long> g_opt_wcap{1LL << 20};  // default 3-D work-list capacity (chunk pairs)
 std::atomic<bool> g_opt_batch_times{false};  // per-stage event nodes in batch graphs
