@@ -522,16 +522,8 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
     cfg.attrs = at;
     cfg.numAttrs = (pm & 2) ? 1 : 0;
     if (!(pm & 4)) {  // bit 2 (debug, timing only): reuse the slot's previous bit volume
-      const int pu = (pm >> 3) & 3;  // bits 3-4 (experiment): 16-byte loads in flight per thread
-      if (pu == 1)
-        CK(cudaLaunchKernelEx(&cfg, pack_bits_v16<8, false>, rp, c->bits.p, c->d_stats,
-                                  c->segmap.p));
-      else if (pu == 2)
-        CK(cudaLaunchKernelEx(&cfg, pack_bits_v16<16, false>, rp, c->bits.p, c->d_stats,
-                                  c->segmap.p));
-      else
-        CK(cudaLaunchKernelEx(&cfg, pack_bits_v16<4, false>, rp, c->bits.p, c->d_stats,
-                                  c->segmap.p));
+      CK(cudaLaunchKernelEx(&cfg, pack_bits_v16<4, false>, rp, c->bits.p, c->d_stats,
+                            c->segmap.p));
       CKL(1);
     }
     if (++nk >= lim) return SC_OK;
@@ -1478,7 +1470,7 @@ int sc_set_option(const char* name, int value) {
   else if (std::strcmp(name, "wcap") == 0) g_opt_wcap = std::max(1, value);
   else if (std::strcmp(name, "fused_bbox") == 0) g_opt_fbox = value != 0;
   else if (std::strcmp(name, "host_crop") == 0) g_opt_crop = value != 0;
-  else if (std::strcmp(name, "pack_mode") == 0) g_opt_pack_mode = value & 31;
+  else if (std::strcmp(name, "pack_mode") == 0) g_opt_pack_mode = value & 7;
   else if (std::strcmp(name, "pack_bps") == 0) g_opt_pack_bps = std::max(0, value);
   else if (std::strcmp(name, "grid_div") == 0) g_opt_grid_div = std::max(1, value);
   else if (std::strcmp(name, "pdl") == 0) g_opt_pdl = value != 0;

@@ -527,8 +527,6 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
 
 
 template __global__ void pack_bits_v16<4, false>(const RoiParams*, uint32_t*, Stats*, uint32_t*);
-template __global__ void pack_bits_v16<8, false>(const RoiParams*, uint32_t*, Stats*, uint32_t*);
-template __global__ void pack_bits_v16<16, false>(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 template __global__ void pack_bits_v16<4, true>(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 
 }  // namespace sc
