@@ -161,6 +161,9 @@ int sc_last_diagnostics(int device, int64_t* out, int n);
  * "graphs" (1) = replay each ROI pipeline as a cached CUDA graph; "slots" (16)
  * = pipeline slots (stream + scratch) the batch entries keep in flight;
  * "host_crop" (1) = host-mask entries copy only the occupied z/y slab;
+ * "host_split" (-1) = % of leading slices sent to the device whole while the
+ * host scans the rest (-1: balanced from the measured host-scan and PCIe
+ * rates and the previous ROI's slab fraction; 0: off);
  * "host_threads" (hardware threads, <= 32) = threads of the host slab scan;
  * "grid_div" (2) = divisor of the per-ROI kernels' grids (SMs x blocks/SM):
  * fewer resident blocks per ROI let more ROIs share the GPU;

@@ -104,7 +104,8 @@ std::atomic<int> g_opt_grid_div{2};  // divisor of the latency-bound kernel grid
 std::atomic<int> g_opt_pack_bps{0};  // pack blocks per SM (0 = occupancy limit)  // divisor of the latency-bound kernels' grids
 std::atomic<int> g_opt_pack_mode{0};  // bit 0: one step per pack block; bit 1: low-priority pack;
                                       // bit 2 (debug): no pack, reuse the slot's bit volume
-std::atomic<bool> g_opt_crop{true};  // host entries: copy only the occupied z/y slab (host_crop.h)
+std::atomic<bool> g_opt_crop{true};
+std::atomic<int> g_opt_split{-1};  // host_split: % of leading slices sent unscanned (-1 adaptive, 0 off)  // host entries: copy only the occupied z/y slab (host_crop.h)
 std::atomic<int> g_opt_host_threads{(int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()))};
 std::atomic<unsigned long long> g_launches{0};
 
@@ -240,6 +241,9 @@ struct Ctx {
   DevBuf<uint8_t> mask_stage, raw_stage;
   double last_scan_ms = 0.0;      // host slab scan of the last host-mask ROI
   long long last_h2d_bytes = 0;   // bytes that crossed PCIe for it
+  long long last_scan_bytes = 0;  // bytes the host scan read for it
+  long long last_slab_bytes = 0;  // bytes of its occupied slab
+  bool last_split = false;        // it used the split read (split_slices)
   DevBuf<double> cloud;
   DevBuf<unsigned long long> cloud_out;
   // CUDA graphs of whole ROIs, keyed by everything baked into the nodes.
@@ -878,6 +882,50 @@ double wall_ms() {
 // slab crosses PCIe, as one 2-D copy of whole x rows; *cy / *cz / org then
 // describe the slab (x is never cropped).  An all-background mask is reported
 // here, before any device work, as the reference does (mesh.py:78-79).
+// Host-read / PCIe balance of the host entries (per device, updated after
+// every host-mask ROI): host scan rate, pinned H2D rate, occupied-slab fraction.
+struct HostRates {
+  std::mutex mu;
+  double scan_bpms = 0.0, h2d_bpms = 0.0, slab_frac = 1.0;
+};
+HostRates& host_rates(int device) {
+  static HostRates r[64];
+  return r[device & 63];
+}
+
+// After a host-mask ROI: refresh the rates split_slices() balances.
+void note_host_rates(const Ctx* c, int64_t total_bytes, double h2d_ms) {
+  HostRates& r = host_rates(c->device);
+  std::lock_guard<std::mutex> lk(r.mu);
+  if (c->last_scan_ms > 0.0 && c->last_scan_bytes > 0)
+    r.scan_bpms = (double)c->last_scan_bytes / c->last_scan_ms;
+  if (!c->last_split && h2d_ms > 0.0 && c->last_h2d_bytes > (1 << 20))
+    r.h2d_bpms = (double)c->last_h2d_bytes / h2d_ms;
+  if (total_bytes > 0) r.slab_frac = (double)c->last_slab_bytes / (double)total_bytes;
+}
+
+// Leading slices [0, a) that go to the device whole, unscanned: the host scan
+// (rate Rc) and the PCIe link (rate Rp) then read the mask concurrently.
+// With s the slab fraction of the previous ROI, (1 - f)/Rc = (f + s)/Rp gives
+// f = (Rp/Rc - s) / (1 + Rp/Rc); f = 0 when the slab alone already keeps PCIe
+// busier than the scan (e.g. C3), and until both rates have been measured.
+int64_t split_slices(int device, int64_t nz) {
+  const int pct = g_opt_split.load();
+  if (pct == 0 || nz < 8) return 0;
+  double f;
+  if (pct > 0) {
+    f = pct / 100.0;
+  } else {
+    HostRates& r = host_rates(device);
+    std::lock_guard<std::mutex> lk(r.mu);
+    if (r.scan_bpms <= 0.0 || r.h2d_bpms <= 0.0) return 0;
+    const double k = r.h2d_bpms / r.scan_bpms;
+    f = (k - r.slab_frac) / (1.0 + k);
+  }
+  if (f <= 0.0) return 0;
+  return std::min<int64_t>(nz - 1, (int64_t)(f * (double)nz));
+}
+
 int stage_host_mask(Ctx* c, const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz,
                     cudaStream_t s, int64_t* cy, int64_t* cz, int org[3]) {
   org[0] = org[1] = org[2] = 0;
@@ -885,10 +933,44 @@ int stage_host_mask(Ctx* c, const uint8_t* mask, int64_t nx, int64_t ny, int64_t
   *cy = ny;
   *cz = nz;
   const uint8_t* src = mask;
+  const size_t S = (size_t)nx * ny;  // bytes per slice
+  const int64_t a = g_opt_crop.load() ? split_slices(c->device, nz) : 0;
+  if (a > 0) {
+    // Split read: slices [0, a) cross PCIe whole while the host scans [a, nz)
+    // for its occupied slab; the device volume is slices [0, Z1] with every
+    // row (rows outside the slab are zeroed on the device), origin 0.
+    CK(cudaEventRecord(c->ev[0], s));
+    CK(cudaMemcpyAsync(c->mask_stage.p, mask, a * S, cudaMemcpyHostToDevice, s));
+    const double t0 = wall_ms();
+    const Slab sl = occupied_slab(mask + a * S, nx, ny, nz - a, g_opt_host_threads.load());
+    c->last_scan_ms = wall_ms() - t0;
+    size_t bytes = a * S;
+    int64_t Z1 = a - 1;
+    if (!sl.empty) {
+      const int64_t z0 = a + sl.z0;
+      Z1 = a + sl.z1;
+      const size_t width = (size_t)nx * (sl.y1 - sl.y0 + 1);
+      CK(cudaMemsetAsync(c->mask_stage.p + a * S, 0, (Z1 - a + 1) * S, s));
+      CK(cudaMemcpy2DAsync(c->mask_stage.p + z0 * S + sl.y0 * nx, S, mask + z0 * S + sl.y0 * nx,
+                           S, width, (size_t)(Z1 - z0 + 1), cudaMemcpyHostToDevice, s));
+      bytes += width * (Z1 - z0 + 1);
+      c->last_slab_bytes = (long long)(width * (Z1 - z0 + 1));
+    } else {
+      c->last_slab_bytes = 0;
+    }
+    CK(cudaEventRecord(c->ev[1], s));
+    *cz = Z1 + 1;
+    c->last_h2d_bytes = (long long)bytes;
+    c->last_scan_bytes = sl.bytes_read;
+    c->last_split = true;
+    return SC_OK;
+  }
+  c->last_split = false;
   if (g_opt_crop.load()) {
     const double t0 = wall_ms();
     const Slab sl = occupied_slab(mask, nx, ny, nz, g_opt_host_threads.load());
     c->last_scan_ms = wall_ms() - t0;
+    c->last_scan_bytes = sl.bytes_read;
     if (sl.empty) {
       set_err("mask has no occupied voxels");
       return SC_ERR_EMPTY_ROI;
@@ -900,6 +982,7 @@ int stage_host_mask(Ctx* c, const uint8_t* mask, int64_t nx, int64_t ny, int64_t
     src = mask + (sl.z0 * ny + sl.y0) * nx;
   }
   const size_t width = (size_t)nx * *cy;
+  c->last_slab_bytes = (long long)(width * *cz);
   CK(cudaEventRecord(c->ev[0], s));
   if (*cy == ny)
     CK(cudaMemcpyAsync(c->mask_stage.p, src, width * *cz, cudaMemcpyHostToDevice, s));
@@ -988,6 +1071,8 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
       o->h2d_bytes = c->last_h2d_bytes;
       o->host_scan_ms = c->last_scan_ms;
       c->last_ms[6] = o->h2d_ms;
+      const int64_t j = idx[k];
+      note_host_rates(c, dims[3 * j] * dims[3 * j + 1] * dims[3 * j + 2], o->h2d_ms);
     }
     o->total_ms = wall_ms() - t_start[k];
     idx[k] = -1;
@@ -1232,6 +1317,7 @@ int sc_calculate_coefficients(const uint8_t* mask, int64_t nx, int64_t ny, int64
   out->h2d_bytes = c->last_h2d_bytes;
   out->host_scan_ms = c->last_scan_ms;
   c->last_ms[6] = out->h2d_ms;
+  if (rc == SC_OK) note_host_rates(c, nx * ny * nz, out->h2d_ms);
   out->total_ms = wall_ms() - t0;
   return rc;
 }
@@ -1470,6 +1556,7 @@ int sc_set_option(const char* name, int value) {
   else if (std::strcmp(name, "wcap") == 0) g_opt_wcap = std::max(1, value);
   else if (std::strcmp(name, "fused_bbox") == 0) g_opt_fbox = value != 0;
   else if (std::strcmp(name, "host_crop") == 0) g_opt_crop = value != 0;
+  else if (std::strcmp(name, "host_split") == 0) g_opt_split = std::max(-1, std::min(90, value));
   else if (std::strcmp(name, "pack_mode") == 0) g_opt_pack_mode = value & 7;
   else if (std::strcmp(name, "pack_bps") == 0) g_opt_pack_bps = std::max(0, value);
   else if (std::strcmp(name, "grid_div") == 0) g_opt_grid_div = std::max(1, value);

@@ -474,9 +474,18 @@ def test_host_crop_is_exact(sc, oracle_mod, cuda_device):
                   (0.37, 0.61, 2.9)))
     try:
         for arr, sp in cases:
+            _native.set_option("host_split", 0)
             cropped = sc.calculate_coefficients(arr, sp, device=cuda_device)
             z0, z1, y0, y1 = _native.occupied_slab(arr)
             assert cropped.h2d_bytes == (z1 - z0 + 1) * (y1 - y0 + 1) * arr.shape[2]
+            # split read: leading slices cross PCIe unscanned, the rest is cropped
+            for pct in (30, 60, 90):
+                _native.set_option("host_split", pct)
+                split = sc.calculate_coefficients(arr, sp, device=cuda_device)
+                assert split.to_dict() == cropped.to_dict(), pct
+                assert (split.triangle_count, split.active_cubes) == \
+                       (cropped.triangle_count, cropped.active_cubes)
+            _native.set_option("host_split", -1)
             dev = sc.calculate_coefficients_device(torch.from_numpy(arr).cuda(), sp)
             _native.set_option("host_crop", 0)
             full = sc.calculate_coefficients(arr, sp, device=cuda_device)
@@ -492,13 +501,16 @@ def test_host_crop_is_exact(sc, oracle_mod, cuda_device):
             assert cropped.triangle_count == want["triangle_count"]
             for k in ("MeshVolume", "SurfaceArea"):
                 assert rel_err(rec[k], want[k]) <= 1e-12
-        # the pipelined host batch crops too
-        outs = sc.calculate_coefficients_batch([a for a, _ in cases], [s for _, s in cases],
-                                               device=cuda_device)
-        for (arr, sp), o in zip(cases, outs):
-            assert o.to_dict() == sc.calculate_coefficients(arr, sp).to_dict()
+        # the pipelined host batch crops (and splits) too
+        for pct in (-1, 50):
+            _native.set_option("host_split", pct)
+            outs = sc.calculate_coefficients_batch([a for a, _ in cases] * 3,
+                                                   [s for _, s in cases] * 3, device=cuda_device)
+            for (arr, sp), o in zip(cases * 3, outs):
+                assert o.to_dict() == sc.calculate_coefficients(arr, sp).to_dict()
     finally:
         _native.set_option("host_crop", 1)
+        _native.set_option("host_split", -1)
 
 
 def _blob_mask(seed):
