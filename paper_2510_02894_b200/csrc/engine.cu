@@ -100,6 +100,7 @@ std::atomic<long long> g_opt_wcap{1LL << 20};  // default 3-D work-list capacity
 std::atomic<bool> g_opt_batch_times{false};  // per-stage event nodes in batch graphs
 std::atomic<bool> g_opt_pdl{false};  // programmatic dependent launch in batch graphs
 std::atomic<bool> g_opt_sparse{true};  // sparse bit volume (segment map), option "sparse_bits"
+std::atomic<bool> g_opt_fork{true};  // planar chain on a second stream (option "fork")
 std::atomic<int> g_opt_grid_div{2};  // divisor of the latency-bound kernel grids (2: best measured batch rate)
 std::atomic<int> g_opt_pack_bps{0};  // pack blocks per SM (0 = occupancy limit)  // divisor of the latency-bound kernels' grids
 std::atomic<int> g_opt_pack_mode{0};  // bit 0: one step per pack block; bit 1: low-priority pack;
@@ -211,7 +212,9 @@ struct Ctx {
   std::mutex mu;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[6] = {};
-  cudaEvent_t kev[8] = {};      // per-kernel boundaries of the last ROI
+  cudaEvent_t kev[10] = {};     // per-kernel boundaries of the last ROI
+  cudaStream_t stream2 = nullptr;  // planar branch of the ROI graph (fork / join)
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   double last_ms[7] = {0, 0, 0, 0, 0, 0, 0};  // pack, mc, prune, pass1, refine, planar, h2d
   bool times_pending = false;  // last_ms[0..5] still to be read from kev[]
   long long cap_floor = 0, dcap_floor = 0, wcap_floor = 0;  // raised by overflow re-runs only
@@ -260,6 +263,7 @@ struct Ctx {
     bool events;        // per-stage event nodes present
     bool pdl;           // option "pdl"
     bool sparse;        // option "sparse_bits"
+    bool fork;          // option "fork"
     unsigned long long gen;
     cudaGraphExec_t exec;
     unsigned long long launches;
@@ -319,6 +323,9 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     // the least (pack_mode bit 1), so other ROIs' short latency-bound kernels
     // take SM slots ahead of queued pack blocks.
     CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, c->prio_hi));
+    CK(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, c->prio_hi));
+    CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     for (auto& e : c->kev) CK(cudaEventCreate(&e));
     CK(cudaMalloc(&c->d_stats, sizeof(Stats)));
@@ -478,7 +485,8 @@ cudaError_t launch_k(const Ctx* c, cudaStream_t s, int grid, int block, void (*k
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = (g_opt_pdl.load() && !c->events_on) ? 1 : 0;
+  // (not with the fork / join: a programmatic edge cannot follow an event wait)
+  cfg.numAttrs = (g_opt_pdl.load() && !c->events_on && !g_opt_fork.load()) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
@@ -573,6 +581,31 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
                                          c->plane_sorted.p, c->sort_counts.p + kSortBins));
   CKL(1);
   if (++nk >= lim) return SC_OK;
+  // After the sort the 3-D chain (boxes -> filter) and the planar chain
+  // (plane boxes -> bound -> filter) are independent: the planar one runs on
+  // the slot's second stream (a fork / join inside the captured graph), so
+  // the ROI's critical path is the longer chain, not their sum.
+  const bool fork = g_opt_fork.load() && lim >= (1 << 20);
+  cudaStream_t sp = s;
+  if (fork) {
+    CK(cudaEventRecord(c->fork_ev, s));
+    CK(cudaStreamWaitEvent(c->stream2, c->fork_ev, 0));
+    sp = c->stream2;
+    CK(record(c, c->kev[7], sp));
+    CK(launch_k(c, sp, lgrid(c, 4), 256, plane_boxes, c->plane_sorted.p, c->plane_start.p,
+                c->plane_cstart.p, rp, c->d_stats, c->plane_boxes_buf.p, c->plane_ext.p,
+                c->plane_hboxes.p));
+    CKL(1);
+    CK(launch_k(c, sp, lgrid(c, 1), 256, plane_lb, c->plane_sorted.p, c->plane_start.p,
+                c->plane_ext.p, rp, c->d_stats));
+    CKL(1);
+    CK(launch_k(c, sp, lgrid(c, 4), 256, plane_filter, c->plane_start.p, c->plane_tstart.p,
+                c->plane_cstart.p, c->plane_boxes_buf.p, rp, prune, shard, nshards, pucap,
+                c->d_stats, c->plane_work.p, c->plane_hboxes.p));
+    CKL(1);
+    CK(record(c, c->kev[8], sp));
+    CK(cudaEventRecord(c->join_ev, sp));
+  }
   CK(launch_k(c, s, lgrid(c, 2), 256, boxes_extremes, c->keys_sorted.p, dcap, rp, c->d_stats, c->boxes.p,
                                             c->sboxes.p, c->hboxes.p));
   CKL(1);
@@ -582,6 +615,8 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[3], s));
+  if (!fork) {
+  CK(record(c, c->kev[7], s));
   CK(launch_k(c, s, lgrid(c, 4), 256, plane_boxes, c->plane_sorted.p, c->plane_start.p, c->plane_cstart.p,
                                          rp, c->d_stats, c->plane_boxes_buf.p, c->plane_ext.p, c->plane_hboxes.p));
   CKL(1);
@@ -595,6 +630,10 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
                                           c->d_stats, c->plane_work.p, c->plane_hboxes.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
+  CK(record(c, c->kev[8], s));
+  } else {
+    CK(cudaStreamWaitEvent(s, c->join_ev, 0));
+  }
   CK(record(c, c->kev[4], s));
   // One pass-1 kernel and one re-check kernel for the 3-D and the planar lists.
   if (g_opt_packed.load())
@@ -726,7 +765,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
         g.packmode == g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load() &&
         g.grid_div == g_opt_grid_div.load() &&
         g.events == c->events_on && g.pdl == g_opt_pdl.load() &&
-        g.sparse == g_opt_sparse.load() &&
+        g.sparse == g_opt_sparse.load() && g.fork == g_opt_fork.load() &&
         g.gen == c->gen) {
       CK(cudaGraphLaunch(g.exec, s));
       if (hp) g_hprof.launch += wall_ms() - t0;
@@ -755,8 +794,8 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   Ctx::GraphEntry g{fast, s, shard, nshards, d_sq4, cap, dcap, prune, packed, fbox,
                     g_opt_stages.load(), g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load(),
                     g_opt_grid_div.load(),
-                    c->events_on, g_opt_pdl.load(), g_opt_sparse.load(), c->gen, exec,
-                    launches};
+                    c->events_on, g_opt_pdl.load(), g_opt_sparse.load(), g_opt_fork.load(),
+                    c->gen, exec, launches};
   c->graphs.push_back(g);
   CK(cudaGraphLaunch(exec, s));
   g_launches.fetch_add(launches, std::memory_order_relaxed);
@@ -1508,8 +1547,9 @@ int sc_last_kernel_times(int device, double* ms, int n) {
   if (rc) return -rc;
   std::lock_guard<std::mutex> lk(c->mu);
   if (c->times_pending) {
-    // pack, mc, prune (3-D), pass 1 (3-D + planar), re-check (both), planar prep
-    static const int from[6] = {0, 1, 2, 4, 5, 3}, to[6] = {1, 2, 3, 5, 6, 4};
+    // pack, mc, prune (sort + 3-D filter), pass 1 (3-D + planar), re-check
+    // (both), planar prep (runs beside the 3-D filter when forked)
+    static const int from[6] = {0, 1, 2, 4, 5, 7}, to[6] = {1, 2, 3, 5, 6, 8};
     for (int i = 0; i < 6; i++) c->last_ms[i] = ev_ms(c->kev[from[i]], c->kev[to[i]]);
     c->times_pending = false;
   }
@@ -1561,6 +1601,7 @@ int sc_set_option(const char* name, int value) {
   else if (std::strcmp(name, "pack_bps") == 0) g_opt_pack_bps = std::max(0, value);
   else if (std::strcmp(name, "grid_div") == 0) g_opt_grid_div = std::max(1, value);
   else if (std::strcmp(name, "pdl") == 0) g_opt_pdl = value != 0;
+  else if (std::strcmp(name, "fork") == 0) g_opt_fork = value != 0;
   else if (std::strcmp(name, "sparse_bits") == 0) g_opt_sparse = value != 0;
   else if (std::strcmp(name, "batch_stage_times") == 0) g_opt_batch_times = value != 0;
   else if (std::strcmp(name, "host_threads") == 0) g_opt_host_threads = std::max(1, value);
