@@ -169,6 +169,8 @@ int sc_last_diagnostics(int device, int64_t* out, int n);
  * fewer resident blocks per ROI let more ROIs share the GPU;
  * "batch_stage_times" (0) = per-stage CUDA events in batch graphs (mesh_ms /
  * diameters_ms of batch results are 0 without them);
+ * "pack_tma" (0) = CTAs per SM of the cp.async.bulk (TMA) variant of the
+ * pack (0 = the 128-bit-load pack);
  * "sparse_bits" (1) = the pack writes only nonzero 16-word segments of the
  * bit volume (segment map); "pdl" (0) = programmatic dependent launch of the
  * per-ROI kernels in batch graphs.

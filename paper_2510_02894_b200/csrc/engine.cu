@@ -35,6 +35,8 @@ __global__ void init_stats(Stats* st);
 template <int U, bool BOX>
 __global__ void pack_bits_v16(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 __global__ void bits_bbox(const RoiParams*, const uint4*, Stats*, const uint32_t*);
+__global__ void pack_bits_tma(const RoiParams*, uint32_t*, Stats*, uint32_t*);
+constexpr int kTmaSmem = 4 * 16384;  // mc.cu kTmaStages x kTmaTile
 __global__ void pack_bits_generic(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 __global__ void mc_cells(const RoiParams*, const uint32_t*, const CaseTables*, Stats*, int4*,
                          long long, unsigned int*, unsigned int*, const uint32_t*);
@@ -100,6 +102,7 @@ std::atomic<long long> g_opt_wcap{1LL << 20};  // default 3-D work-list capacity
 std::atomic<bool> g_opt_batch_times{false};  // per-stage event nodes in batch graphs
 std::atomic<bool> g_opt_pdl{false};  // programmatic dependent launch in batch graphs
 std::atomic<bool> g_opt_sparse{true};  // sparse bit volume (segment map), option "sparse_bits"
+std::atomic<int> g_opt_pack_tma{0};  // TMA bulk-copy pack, CTAs per SM (0 = 128-bit load pack)
 std::atomic<bool> g_opt_fork{true};  // planar chain on a second stream (option "fork")
 std::atomic<int> g_opt_grid_div{2};  // divisor of the latency-bound kernel grids (2: best measured batch rate)
 std::atomic<int> g_opt_pack_bps{0};  // pack blocks per SM (0 = occupancy limit)  // divisor of the latency-bound kernels' grids
@@ -324,6 +327,7 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     // take SM slots ahead of queued pack blocks.
     CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, c->prio_hi));
     CK(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, c->prio_hi));
+    CK(cudaFuncSetAttribute(pack_bits_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
     CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
@@ -533,7 +537,11 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
     at[0].val.priority = c->prio_lo;
     cfg.attrs = at;
     cfg.numAttrs = (pm & 2) ? 1 : 0;
-    if (!(pm & 4)) {  // bit 2 (debug, timing only): reuse the slot's previous bit volume
+    if (!(pm & 4) && g_opt_pack_tma.load() > 0) {  // bulk-copy (TMA) pack
+      pack_bits_tma<<<c->sms * g_opt_pack_tma.load(), 256, kTmaSmem, s>>>(rp, c->bits.p,
+                                                                      c->d_stats, c->segmap.p);
+      CKL(1);
+    } else if (!(pm & 4)) {  // bit 2 (debug, timing only): reuse the slot's previous bit volume
       CK(cudaLaunchKernelEx(&cfg, pack_bits_v16<4, false>, rp, c->bits.p, c->d_stats,
                             c->segmap.p));
       CKL(1);
@@ -762,7 +770,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
     if (g.fast == fast && g.s == s && g.shard == shard && g.nshards == nshards &&
         g.d_sq4 == d_sq4 && g.cap == cap && g.dcap == dcap && g.prune == prune &&
         g.packed == packed && g.fbox == fbox && g.stages == g_opt_stages.load() &&
-        g.packmode == g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load() &&
+        g.packmode == g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load() + 4096 * g_opt_pack_tma.load() &&
         g.grid_div == g_opt_grid_div.load() &&
         g.events == c->events_on && g.pdl == g_opt_pdl.load() &&
         g.sparse == g_opt_sparse.load() && g.fork == g_opt_fork.load() &&
@@ -792,7 +800,8 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
     c->graphs.erase(c->graphs.begin());
   }
   Ctx::GraphEntry g{fast, s, shard, nshards, d_sq4, cap, dcap, prune, packed, fbox,
-                    g_opt_stages.load(), g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load(),
+                    g_opt_stages.load(),
+                    g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load() + 4096 * g_opt_pack_tma.load(),
                     g_opt_grid_div.load(),
                     c->events_on, g_opt_pdl.load(), g_opt_sparse.load(), g_opt_fork.load(),
                     c->gen, exec, launches};
@@ -1602,6 +1611,7 @@ int sc_set_option(const char* name, int value) {
   else if (std::strcmp(name, "grid_div") == 0) g_opt_grid_div = std::max(1, value);
   else if (std::strcmp(name, "pdl") == 0) g_opt_pdl = value != 0;
   else if (std::strcmp(name, "fork") == 0) g_opt_fork = value != 0;
+  else if (std::strcmp(name, "pack_tma") == 0) g_opt_pack_tma = std::max(0, std::min(3, value));
   else if (std::strcmp(name, "sparse_bits") == 0) g_opt_sparse = value != 0;
   else if (std::strcmp(name, "batch_stage_times") == 0) g_opt_batch_times = value != 0;
   else if (std::strcmp(name, "host_threads") == 0) g_opt_host_threads = std::max(1, value);

@@ -133,6 +133,109 @@ __global__ void __launch_bounds__(256) pack_bits_v16(const RoiParams* __restrict
   if (BOX) box.flush(st);
 }
 
+// ---- TMA bulk-copy variant of the fast pack (option "pack_tma") ----
+// One persistent CTA per SM streams a contiguous share of the mask through a
+// 4-stage ring of 16 KB shared-memory tiles filled by cp.async.bulk (the copy
+// engine tracks the bytes on an mbarrier; no registers hold loads in flight),
+// and 8 warps convert each landed tile exactly as pack_bits_v16 does.  The
+// CTA holds ~64 KB of shared memory and 256 threads, so most of the SM stays
+// free for other ROIs' kernels while the HBM stream runs.
+constexpr int kTmaStages = 4;
+constexpr int kTmaTile = 16384;  // bytes per stage
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                          uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar)), "l"(policy)
+      : "memory");
+}
+// Bounded wait: a lost transaction traps instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  for (long long spin = 0;; spin++) {
+    unsigned ok;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (spin > (1LL << 26)) __trap();
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) pack_bits_tma(const RoiParams* __restrict__ rp,
+                                                       uint32_t* __restrict__ bits,
+                                                       Stats* __restrict__ st,
+                                                       uint32_t* __restrict__ segmap) {
+  extern __shared__ __align__(128) unsigned char s_tiles[];  // kTmaStages x kTmaTile
+  __shared__ __align__(8) uint64_t s_full[kTmaStages];
+  const unsigned char* mask = rp->mask;
+  const long long n_bytes = 16LL * rp->n_chunks;
+  const bool sparse = rp->sparse != 0;
+  // contiguous share per CTA, a multiple of the tile size
+  const long long per =
+      ((n_bytes + gridDim.x - 1) / gridDim.x + kTmaTile - 1) / kTmaTile * kTmaTile;
+  const long long beg = min(n_bytes, (long long)blockIdx.x * per);
+  const long long end = min(n_bytes, beg + per);
+  const int tiles = (int)((end - beg + kTmaTile - 1) / kTmaTile);
+  if (tiles <= 0) return;  // block-uniform
+  uint64_t policy;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; s++) mbar_init(&s_full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int t) {  // thread 0 only
+    const int s = t % kTmaStages;
+    const long long off = beg + (long long)t * kTmaTile;
+    const unsigned bytes = (unsigned)min((long long)kTmaTile, end - off);
+    mbar_expect_tx(&s_full[s], bytes);
+    bulk_load(s_tiles + s * kTmaTile, mask + off, bytes, &s_full[s], policy);
+  };
+  if (threadIdx.x == 0)
+    for (int t = 0; t < min(tiles, kTmaStages); t++) issue(t);
+  constexpr int kK = kTmaTile / 16 / 256;  // 16-byte chunks per thread per tile (4)
+  for (int t = 0; t < tiles; t++) {
+    const int s = t % kTmaStages;
+    mbar_wait(&s_full[s], (unsigned)(t / kTmaStages) & 1u);
+    const long long g0 = (beg + (long long)t * kTmaTile) / 16;  // first chunk of the tile
+    const long long gend = end / 16;
+    const uint4* tile = reinterpret_cast<const uint4*>(s_tiles + s * kTmaTile);
+#pragma unroll
+    for (int k = 0; k < kK; k++) {
+      const int ci = k * 256 + threadIdx.x;
+      const long long g = g0 + ci;
+      const uint4 v = g < gend ? tile[ci] : make_uint4(0u, 0u, 0u, 0u);
+      const uint32_t b16 = nib4(v.x) | (nib4(v.y) << 4) | (nib4(v.z) << 8) | (nib4(v.w) << 12);
+      const uint32_t word = b16 | (__shfl_down_sync(kFull, b16, 1) << 16);
+      if (sparse) {
+        if (!__any_sync(kFull, word != 0u && !(threadIdx.x & 1) && g < gend)) continue;
+        if ((threadIdx.x & 31) == 0) {
+          const long long seg = g >> 5;
+          atomicOr(segmap + (seg >> 5), 1u << (seg & 31));
+        }
+      }
+      if (!(threadIdx.x & 1) && g < gend) bits[g >> 1] = word;
+    }
+    __syncthreads();  // every thread is done with stage s
+    if (threadIdx.x == 0 && t + kTmaStages < tiles) issue(t + kTmaStages);
+  }
+}
+
 // Occupied bbox from the bit volume (L2-resident right after the pack): only
 // nonzero words locate themselves.  Four 16-byte loads in flight per thread.
 __global__ void __launch_bounds__(256) bits_bbox(const RoiParams* __restrict__ rp,
