@@ -502,6 +502,11 @@ def test_host_crop_is_exact(sc, oracle_mod, cuda_device):
             assert cropped.triangle_count == want["triangle_count"]
             for k in ("MeshVolume", "SurfaceArea"):
                 assert rel_err(rec[k], want[k]) <= 1e-12
+        # an all-background mask is an EmptyRoi whichever part the host scanned
+        for pct in (0, 50):
+            _native.set_option("host_split", pct)
+            with pytest.raises(sc.EmptyRoi):
+                sc.calculate_coefficients(np.zeros((40, 30, 64), np.uint8), (1, 1, 1))
         # the pipelined host batch crops (and splits) too
         for pct in (-1, 50):
             _native.set_option("host_split", pct)
