@@ -381,6 +381,14 @@ int check_input(const void* mask, int64_t nx, int64_t ny, int64_t nz, const doub
     set_err("dims beyond 2^20 per axis are not supported");
     return SC_ERR_INPUT;
   }
+  // Planar work entries index in-plane 128-vertex chunks with 16 bits, and a
+  // plane holds at most ~2 vertices per voxel of the grid face it spans.
+  const int64_t face = std::max(nx * ny, std::max(nx * nz, ny * nz));
+  if (2 * face > 65535LL * 128) {
+    set_err("grid faces above %lld voxels are not supported (largest face %lld)",
+            65535LL * 64, (long long)face);
+    return SC_ERR_INPUT;
+  }
   if (!sp) { set_err("spacing pointer is NULL"); return SC_ERR_INPUT; }
   for (int i = 0; i < 3; i++)
     if (!(sp[i] > 0.0) || !std::isfinite(sp[i])) {
