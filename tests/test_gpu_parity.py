@@ -562,3 +562,20 @@ def test_sub_pair_pruning_random_masks(sc, oracle_mod, cuda_device):
                 assert rel_err(rec[k], want[k]) <= REL_TOL, (seed, k)
     finally:
         _native.set_option("prune", 1)
+
+
+@pytest.mark.timeout(600)
+def test_randomized_stress_parity(cuda_device):
+    """tools/stress_parity.py: 60 seeded masks of varied kind (random voxels,
+    blobs, sheets, face-touching boxes, nonbinary singles), size, alignment and
+    spacing through the host single call, the host batch (crop / split) and the
+    device batch, against the oracle."""
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    r = subprocess.run([sys.executable, "tools/stress_parity.py", "60", "11"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=580)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "stress parity ok" in r.stdout
