@@ -31,7 +31,7 @@
 namespace sc {
 
 // Kernels (mc.cu, diameter.cu, prune.cu, planar.cu).
-__global__ void init_stats(Stats* st);
+__global__ void init_stats(Stats* st, uint32_t* segmap, long long n_seg);
 template <int U, bool BOX>
 __global__ void pack_bits_v16(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 __global__ void bits_bbox(const RoiParams*, const uint4*, Stats*, const uint32_t*);
@@ -40,10 +40,9 @@ constexpr int kTmaSmem = 4 * 16384;  // mc.cu kTmaStages x kTmaTile
 __global__ void pack_bits_generic(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 __global__ void mc_cells(const RoiParams*, const uint32_t*, const CaseTables*, Stats*, int4*,
                          long long, unsigned int*, unsigned int*, const uint32_t*);
-__global__ void plane_bins_scan(unsigned int*, unsigned int*, unsigned int*, unsigned long long*,
-                                const Stats*);
-__global__ void scan_all(unsigned int*, unsigned int*, const unsigned int*, unsigned int*,
-                         unsigned int*, unsigned int*, long long, Stats*, int4*);
+__global__ void scan_all(unsigned int*, unsigned int*, unsigned int*, unsigned int*,
+                         unsigned int*, unsigned int*, long long, Stats*, int4*, unsigned int*,
+                         unsigned int*, unsigned long long*);
 __global__ void scatter_all(const int4*, long long, const Stats*, unsigned int*, int4*,
                             const unsigned int*, unsigned int*, int2*, unsigned int*);
 __global__ void boxes_extremes(const int4*, long long, const RoiParams*, Stats*, int4*, int4*,
@@ -359,7 +358,7 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
                                (const void*)boxes_extremes, (const void*)unit_filter,
                                (const void*)diam_pass1<true>, (const void*)diam_pass1<false>,
                                (const void*)diam_refine, (const void*)cloud_diameters,
-                               (const void*)plane_bins_scan, (const void*)plane_boxes,
+                               (const void*)plane_boxes,
                                (const void*)plane_lb, (const void*)plane_filter};
       for (const void* k : kernels) CK(cudaFuncGetAttributes(&fa, k));
     }
@@ -514,10 +513,12 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   const int lim = g_opt_stages.load();
   int nk = 0;
   const long long cap = (long long)c->keys.cap, dcap = c->dcap_sz;
-  init_stats<<<1, 256, 0, s>>>(c->d_stats);
+  // (the pack marks nonzero segments of a cleared map; the no-pack debug mode
+  // keeps the previous map)
+  const bool clear_map = g_opt_sparse.load() && !(g_opt_pack_mode.load() & 4);
+  init_stats<<<clear_map ? 8 : 1, 256, 0, s>>>(c->d_stats, c->segmap.p,
+                                               clear_map ? (long long)c->segmap.cap : 0LL);
   CKL(1);
-  if (g_opt_sparse.load() && !(g_opt_pack_mode.load() & 4))  // the pack marks a cleared map
-    CK(cudaMemsetAsync(c->segmap.p, 0, sizeof(uint32_t) * c->segmap.cap, s));
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[0], s));  // kev0..kev1 = the HBM pass alone
   if (fast && g_opt_fbox.load()) {
@@ -582,14 +583,10 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
 
   // Orders (Morton bricks; planes by in-plane brick), chunk boxes + extremes,
   // exact lower bound, pruned 3-D work list.
-  CK(launch_k(c, s, lgrid(c, 2), 256, plane_bins_scan, c->pbin_counts.p, c->pbin_cursor.p,
-                                             c->plane_counts.p, c->plane_ext.p, c->d_stats));
-  CKL(1);
-  if (++nk >= lim) return SC_OK;
-  CK(launch_k(c, s, kScanBlocks + 1, kScanThreads, scan_all, c->sort_counts.p, c->sort_cursor.p,
+  CK(launch_k(c, s, kScanBlocks + std::max(1, c->sms / 2), kScanThreads, scan_all, c->sort_counts.p, c->sort_cursor.p,
                                             c->plane_counts.p, c->plane_start.p,
                                             c->plane_tstart.p, c->plane_cstart.p, dcap,
-                                            c->d_stats, c->sboxes.p));
+                                            c->d_stats, c->sboxes.p, c->pbin_counts.p, c->pbin_cursor.p, c->plane_ext.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(launch_k(c, s, lgrid(c, 4), 256, scatter_all, c->keys.p, dcap, c->d_stats, c->sort_cursor.p,
@@ -1230,7 +1227,7 @@ int run_mesh(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
     h.sparse = 0;  // the export kernels read every bit-volume word
     h.wcap = 0;
     CK(cudaMemcpyAsync(c->d_rp, c->h_rp, sizeof(RoiParams), cudaMemcpyHostToDevice, s));
-    init_stats<<<1, 256, 0, s>>>(c->d_stats);
+    init_stats<<<1, 256, 0, s>>>(c->d_stats, c->segmap.p, 0LL);
     CKL(1);
     if (nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0) {
       pack_bits_v16<4, true><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(

@@ -27,13 +27,20 @@ namespace sc {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-__global__ void init_stats(Stats* st) {
+// Per-ROI reset: block 0 zeroes the accumulator record; every block clears
+// its share of the bit-volume segment map (n_seg words, may be 0).
+__global__ void init_stats(Stats* st, uint32_t* __restrict__ segmap, long long n_seg) {
   int t = threadIdx.x;
-  for (int i = t; i < (int)(sizeof(Stats) / 8); i += blockDim.x)
-    reinterpret_cast<unsigned long long*>(st)[i] = 0ull;
-  __syncthreads();
-  if (t < 3) st->bbox[t] = INT_MAX;
-  if (t >= 3 && t < 6) st->bbox[t] = -1;
+  if (blockIdx.x == 0) {
+    for (int i = t; i < (int)(sizeof(Stats) / 8); i += blockDim.x)
+      reinterpret_cast<unsigned long long*>(st)[i] = 0ull;
+    __syncthreads();
+    if (t < 3) st->bbox[t] = INT_MAX;
+    if (t >= 3 && t < 6) st->bbox[t] = -1;
+  }
+  for (long long i = (long long)blockIdx.x * blockDim.x + t; i < n_seg;
+       i += (long long)gridDim.x * blockDim.x)
+    segmap[i] = 0u;
 }
 
 // 4 mask bytes -> 4 occupancy bits (byte i nonzero -> bit i).  Bit 7 of each

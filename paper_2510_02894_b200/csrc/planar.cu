@@ -6,8 +6,8 @@
 // (plane, in-plane Morton brick) bins, so the counting sort below leaves every
 // plane's list spatially compact; then the same three steps as the 3-D pass:
 //
-//   plane_bins_scan  -- per plane: in-plane bin offsets, plane population
-//   (scan_all)       -- per-plane offsets: entries, 256-entry tile pairs,
+//   (scan_all)       -- per plane: in-plane bin offsets and population, then
+//                       per-plane offsets: entries, 256-entry tile pairs,
 //                       128-entry chunks
 //   (scatter_all)    -- plane lists in brick order
 //   plane_boxes      -- box of every 128-entry in-plane chunk + 8 extremes
@@ -56,47 +56,6 @@ __device__ __forceinline__ const unsigned int* stage_offsets(const unsigned int*
 
 __device__ __forceinline__ unsigned int plane_nchunks(unsigned int np) {
   return np >= 2 ? (np + kPC - 1) / kPC : 0u;
-}
-
-// One warp per plane: exclusive offsets of its 256 brick bins (into
-// pbin_cursor, plane-relative), its population (plane_counts), and reset of
-// its bins and extremes for the next ROI.
-__global__ void plane_bins_scan(unsigned int* __restrict__ pbin_counts,
-                                unsigned int* __restrict__ pbin_cursor,
-                                unsigned int* __restrict__ plane_counts,
-                                unsigned long long* __restrict__ pext,
-                                const Stats* __restrict__ st) {
-  pdl_enter();
-  if (st->bbox[3] < 0) return;
-  const PlaneSpace ps = plane_space(st);
-  const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
-  const int lane = threadIdx.x & 31;
-  const int warps = gridDim.x * (blockDim.x >> 5);
-  for (int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < P; p += warps) {
-    unsigned int* cnt = pbin_counts + (long long)p * kPlaneBins + lane * 8;
-    unsigned int v[8], sum = 0;
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-      v[k] = cnt[k];
-      sum += v[k];
-      cnt[k] = 0u;
-    }
-    unsigned int incl = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    unsigned int run = incl - sum;
-    unsigned int* cur = pbin_cursor + (long long)p * kPlaneBins + lane * 8;
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-      cur[k] = run;
-      run += v[k];
-    }
-    if (lane == 31) plane_counts[p] = incl;
-    if (lane < 8) pext[(long long)p * 8 + lane] = 0ull;
-  }
 }
 
 __device__ __forceinline__ unsigned long long pack_pext(float v, unsigned int idx) {

@@ -37,26 +37,75 @@ __device__ __forceinline__ unsigned int plane_tiles(unsigned int np, int pt) {
   return t * (t + 1) / 2;
 }
 
-// kScanBlocks + 1 blocks of kScanThreads threads.  Blocks [0, kScanBlocks):
-// kScanSlices 1024-bin slices each (16 bins per thread, 128-bit loads) of the
-// exclusive scan of the brick counts -> sort cursor (and zero the counts for
-// the next ROI), plus empty super-chunk boxes.  Last block: plane populations
-// (plane_bins_scan) -> start; 256-entry tile pairs per plane -> tstart;
-// 128-entry chunks per plane -> cstart.
+// kScanBlocks brick blocks + plane blocks, kScanThreads threads each.  Brick
+// blocks: kScanSlices 1024-bin slices each (16 bins per thread, 128-bit loads)
+// of the exclusive scan of the brick counts -> sort cursor (and zero the
+// counts for the next ROI), plus empty super-chunk boxes.  Plane blocks: one
+// warp per plane scans its in-plane bins; the last plane block to finish turns
+// the plane populations into offsets: entries -> start, 256-entry tile pairs
+// -> tstart, 128-entry chunks -> cstart.
 __global__ void __launch_bounds__(kScanThreads) scan_all(unsigned int* __restrict__ sort_counts,
                                                          unsigned int* __restrict__ sort_cursor,
-                                                         const unsigned int* __restrict__ plane_counts,
+                                                         unsigned int* __restrict__ plane_counts,
                                                          unsigned int* __restrict__ start,
                                                          unsigned int* __restrict__ tstart,
                                                          unsigned int* __restrict__ cstart,
                                                          long long dcap, Stats* __restrict__ st,
-                                                         int4* __restrict__ sboxes) {
+                                                         int4* __restrict__ sboxes,
+                                                         unsigned int* __restrict__ pbin_counts,
+                                                         unsigned int* __restrict__ pbin_cursor,
+                                                         unsigned long long* __restrict__ pext) {
   pdl_enter();
   int bb[6];
 #pragma unroll
   for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
   if (bb[3] < 0) return;
   const bool brick_block = blockIdx.x < kScanBlocks;
+  if (!brick_block) {
+    // Plane blocks: one warp per plane -- exclusive offsets of its in-plane
+    // bins (pbin_cursor, plane-relative), its population (plane_counts), reset
+    // of its bins and extremes for the next ROI; then the last plane block to
+    // finish derives the per-plane offsets (start / tstart / cstart).
+    const PlaneSpace ps = plane_space(bb);
+    const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (int)(gridDim.x - kScanBlocks) * (blockDim.x >> 5);
+    for (int p = (int)(blockIdx.x - kScanBlocks) * (blockDim.x >> 5) + (threadIdx.x >> 5); p < P;
+         p += nwarps) {
+      unsigned int* cnt = pbin_counts + (long long)p * kPlaneBins + lane * 8;
+      unsigned int v[8], sum = 0;
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        v[k] = cnt[k];
+        sum += v[k];
+        cnt[k] = 0u;
+      }
+      unsigned int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      unsigned int run = incl - sum;
+      unsigned int* cur = pbin_cursor + (long long)p * kPlaneBins + lane * 8;
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        cur[k] = run;
+        run += v[k];
+      }
+      if (lane == 31) plane_counts[p] = incl;
+      if (lane < 8) pext[(long long)p * 8 + lane] = 0ull;
+    }
+    __shared__ bool s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(&st->done1, 1u) == gridDim.x - kScanBlocks - 1;
+    }
+    __syncthreads();
+    if (!s_last || (long long)st->n_vert > dcap) return;  // overflow: later kernels stand down
+    __threadfence();
+  }
   constexpr int kPerThread = (kScanSlices << kSortSliceBits) / kScanThreads;  // 16 bins
   static_assert(kPerThread % 4 == 0, "bins are moved as uint4");
   uint4* cnt4 = reinterpret_cast<uint4*>(
@@ -64,11 +113,11 @@ __global__ void __launch_bounds__(kScanThreads) scan_all(unsigned int* __restric
   // More vertices than the diameter-side buffers hold: every later kernel
   // stands down (positions from the full histograms would overflow) and the
   // host re-runs the ROI with exact sizes.
-  if ((long long)st->n_vert > dcap) {
+  if (brick_block && (long long)st->n_vert > dcap) {
     if (blockIdx.x == 0 && threadIdx.x == 0) st->ovf = 1u;
-    if (brick_block)  // still leave the brick histogram zeroed for the next ROI
+    // still leave the brick histogram zeroed for the next ROI
 #pragma unroll
-      for (int k = 0; k < kPerThread / 4; k++) cnt4[k] = make_uint4(0u, 0u, 0u, 0u);
+    for (int k = 0; k < kPerThread / 4; k++) cnt4[k] = make_uint4(0u, 0u, 0u, 0u);
     return;
   }
   if (brick_block) {

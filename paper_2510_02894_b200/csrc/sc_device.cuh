@@ -30,7 +30,7 @@ struct Stats {
   unsigned long long ext[26];          // packed (projection, index) of 13-direction extremes
   unsigned long long lb;               // fp64 bits: exact squared distance lower bound
   unsigned long long n_work;           // surviving 3-D work units after pruning
-  unsigned int done1, done2;           // spare block tickets (unused); self-resetting
+  unsigned int done1, done2;           // done1: scan_all plane-block ticket; done2 spare
   unsigned int ovf, pad1;              // V exceeded the diameter-side buffers: skip the rest
   unsigned long long plb[3];           // fp64 bits: exact planar lower bounds per family
   unsigned long long n_pwork;          // surviving planar units after pruning

@@ -6,7 +6,7 @@ import torch, bench
 import paper_2510_02894_b200 as sc
 from paper_2510_02894_b200 import _native
 
-NAMES = ["init", "pack", "bbox", "mc", "plane_bins_scan", "scan_all", "scatter", "boxes",
+NAMES = ["init", "pack", "bbox", "mc", "scan_all", "scatter", "boxes",
          "unit_filter", "plane_boxes", "plane_lb", "plane_filter", "pass1", "refine"]
 for w in sys.argv[1:] or ["c2"]:
     rois, _ = bench.load_workload(w)
@@ -15,7 +15,7 @@ for w in sys.argv[1:] or ["c2"]:
     # Descending, full pipeline first: runs cut before scatter_all leave the
     # self-cleaning histograms dirty, so they go last (and only once per process).
     res = {}
-    for n in (14, 13, 12, 11, 10, 9, 8, 7) + ((4, 3) if w == sys.argv[-1] else ()):
+    for n in (13, 12, 11, 10, 9, 8, 7, 6) + ((4, 3) if w == sys.argv[-1] else ()):
         _native.set_option("debug_stages", n)
         sc.calculate_coefficients_device_batch([d] * 16, [sp] * 16)
         best = 1e9
