@@ -294,8 +294,10 @@ def run_reference(args):
 
 def measure_device(sc, _native, d_mask, sp, stream, steps, warmup, dev, world):
     """One synchronous call per ROI (no cross-ROI overlap): K steps on `stream`,
-    CUDA events around the loop; returns (ms max over ranks, per-kernel median
-    ms, diagnostics, launches, last result)."""
+    CUDA events around the loop (default graph events: mesh / diameters only);
+    then the same number of calls with an event at every stage boundary
+    (option stage_times=2) for the per-kernel medians.  Returns (ms max over
+    ranks, per-kernel median ms, diagnostics, launches, last result)."""
     import torch
 
     with torch.cuda.stream(stream):
@@ -303,20 +305,27 @@ def measure_device(sc, _native, d_mask, sp, stream, steps, warmup, dev, world):
             c = sc.calculate_coefficients_device(d_mask, sp, stream=stream)
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kt = {k: [] for k in _native.KERNEL_TIME_NAMES}
     launches0 = _native.launch_count()
     barrier(world)
     torch.cuda.synchronize()
     ev0.record(stream)
     for _ in range(steps):
         c = sc.calculate_coefficients_device(d_mask, sp, stream=stream)
-        for k, v in _native.last_kernel_times(dev).items():
-            kt[k].append(v)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
     launches = _native.launch_count() - launches0
     ms = max_over_ranks(world, ev0.elapsed_time(ev1))
+    kt = {k: [] for k in _native.KERNEL_TIME_NAMES}
+    _native.set_option("stage_times", 2)
+    try:
+        sc.calculate_coefficients_device(d_mask, sp, stream=stream)  # captures its graph
+        for _ in range(steps):
+            sc.calculate_coefficients_device(d_mask, sp, stream=stream)
+            for k, v in _native.last_kernel_times(dev).items():
+                kt[k].append(v)
+    finally:
+        _native.set_option("stage_times", 1)
     med = {k: statistics.median(v) for k, v in kt.items() if v}
     return ms, med, _native.last_diagnostics(dev), launches, c
 

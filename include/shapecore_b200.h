@@ -142,9 +142,10 @@ int sc_mesh_vertices(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, in
                      int32_t* keys, int64_t cap, int64_t* n_out);
 
 /* Measurement hooks (bench.py).  sc_last_kernel_times fills up to n of
- * {pack_ms, mc_ms, prune_ms, diam3d_pass1_ms, diam3d_refine_ms, planar_ms, h2d_ms} of the
- * last ROI run on `device` (CUDA events on the launching stream) and returns
- * how many were written.  sc_launch_count is the number of kernels this
+ * {pack_ms, mc_ms, prune_ms, pass1_ms, refine_ms, planar_prep_ms, h2d_ms} of the
+ * last single-call ROI run on `device` with option "stage_times" = 2 (CUDA
+ * events on the launching stream; zeros otherwise) and returns how many were
+ * written.  sc_launch_count is the number of kernels this
  * library has launched in the process.  sc_probe_fp32_peak measures the FP32
  * CUDA-core throughput of `device` in TFLOP/s with a dependent-chain-free
  * FFMA2 (mode 0) or scalar FFMA (mode 1) kernel. */
@@ -167,6 +168,9 @@ int sc_last_diagnostics(int device, int64_t* out, int n);
  * "host_threads" (hardware threads, <= 32) = threads of the host slab scan;
  * "grid_div" (2) = divisor of the per-ROI kernels' grids (SMs x blocks/SM):
  * fewer resident blocks per ROI let more ROIs share the GPU;
+ * "stage_times" (1) = CUDA events in single-call graphs: 0 none (mesh_ms /
+ * diameters_ms 0), 1 mesh / diameters boundaries, 2 every stage boundary
+ * (sc_last_kernel_times needs 2; each event node costs latency);
  * "batch_stage_times" (0) = per-stage CUDA events in batch graphs (mesh_ms /
  * diameters_ms of batch results are 0 without them);
  * "pack_tma" (0) = CTAs per SM of the cp.async.bulk (TMA) variant of the

@@ -102,7 +102,8 @@ std::atomic<bool> g_opt_batch_times{false};  // per-stage event nodes in batch g
 std::atomic<bool> g_opt_pdl{false};  // programmatic dependent launch in batch graphs
 std::atomic<bool> g_opt_sparse{true};  // sparse bit volume (segment map), option "sparse_bits"
 std::atomic<int> g_opt_pack_tma{0};  // TMA bulk-copy pack, CTAs per SM (0 = 128-bit load pack)
-std::atomic<bool> g_opt_fork{true};  // planar chain on a second stream (option "fork")
+std::atomic<bool> g_opt_fork{true};
+std::atomic<int> g_opt_stage_times{1};  // single-call graph events: 0 none, 1 mesh/diam, 2 all  // planar chain on a second stream (option "fork")
 std::atomic<int> g_opt_grid_div{2};  // divisor of the latency-bound kernel grids (2: best measured batch rate)
 std::atomic<int> g_opt_pack_bps{0};  // pack blocks per SM (0 = occupancy limit)  // divisor of the latency-bound kernels' grids
 std::atomic<int> g_opt_pack_mode{0};  // bit 0: one step per pack block; bit 1: low-priority pack;
@@ -262,7 +263,8 @@ struct Ctx {
     int stages;
     int packmode;       // pack grid shape / priority (option "pack_mode")
     int grid_div;       // option "grid_div"
-    bool events;        // per-stage event nodes present
+    bool events;        // stage event nodes present
+    bool ev_full;       // ... at every stage boundary
     bool pdl;           // option "pdl"
     bool sparse;        // option "sparse_bits"
     bool fork;          // option "fork"
@@ -273,7 +275,8 @@ struct Ctx {
   std::vector<GraphEntry> graphs;
   unsigned long long gen = 0;  // bumped whenever a scratch buffer moves
   bool capturing = false;      // inside a stream capture of launch_roi
-  bool events_on = true;       // record per-stage events (single calls; batches: option)
+  bool events_on = true;       // record stage events (single calls; batches: option)
+  bool ev_full = true;         // every stage boundary (else mesh / diameters only)
 
   unsigned long long fingerprint() const {
     unsigned long long h = 1469598103934665603ull;
@@ -412,6 +415,8 @@ constexpr long long kPlaneBinsHost = 256;  // sc_device.cuh kPlaneBins
 // graph replays record them (plain records only order the capture).
 cudaError_t record(Ctx* c, cudaEvent_t ev, cudaStream_t s) {
   if (!c->events_on) return cudaSuccess;  // batch graphs: no stage-event nodes
+  // level 1: only the mesh / diameters boundaries (kev 0, 2, 6)
+  if (!c->ev_full && ev != c->kev[0] && ev != c->kev[2] && ev != c->kev[6]) return cudaSuccess;
   return c->capturing ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal)
                       : cudaEventRecord(ev, s);
 }
@@ -777,7 +782,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
         g.packed == packed && g.fbox == fbox && g.stages == g_opt_stages.load() &&
         g.packmode == g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load() + 4096 * g_opt_pack_tma.load() &&
         g.grid_div == g_opt_grid_div.load() &&
-        g.events == c->events_on && g.pdl == g_opt_pdl.load() &&
+        g.events == c->events_on && g.ev_full == c->ev_full && g.pdl == g_opt_pdl.load() &&
         g.sparse == g_opt_sparse.load() && g.fork == g_opt_fork.load() &&
         g.gen == c->gen) {
       CK(cudaGraphLaunch(g.exec, s));
@@ -808,7 +813,8 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
                     g_opt_stages.load(),
                     g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load() + 4096 * g_opt_pack_tma.load(),
                     g_opt_grid_div.load(),
-                    c->events_on, g_opt_pdl.load(), g_opt_sparse.load(), g_opt_fork.load(),
+                    c->events_on, c->ev_full, g_opt_pdl.load(), g_opt_sparse.load(),
+                    g_opt_fork.load(),
                     c->gen, exec, launches};
   c->graphs.push_back(g);
   CK(cudaGraphLaunch(exec, s));
@@ -893,8 +899,8 @@ int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
     return SC_ERR_EMPTY_ROI;
   }
   fill_out(*c->h_stats, p->sp, out);
-  c->times_pending = c->events_on;  // per-stage times: read from kev[] on demand
-  if (!c->events_on)
+  c->times_pending = c->events_on && c->ev_full;  // per-stage times: from kev[] on demand
+  if (!c->times_pending)
     for (int i = 0; i < 6; i++) c->last_ms[i] = 0.0;
   c->last_ms[6] = 0.0;
   {
@@ -919,6 +925,9 @@ int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, c
             cudaStream_t s, int shard, int nshards, double* d_sq4, sc_coeffs* out,
             const int org[3] = nullptr) {
   Pending p{};
+  // single calls: mesh / diameters events (level 1), every stage (2) or none (0)
+  c->events_on = g_opt_stage_times.load() > 0;
+  c->ev_full = g_opt_stage_times.load() > 1;
   int rc = start_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, 0, &p, org);
   if (rc) return rc;
   return finish_roi(c, &p, out);
@@ -1071,9 +1080,10 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
   // nodes = cheaper launches); the slots go back to single-call mode after.
   struct EventsMode {
     Ctx** cs; int n;
-    ~EventsMode() { for (int k = 0; k < n; k++) cs[k]->events_on = true; }
+    ~EventsMode() { for (int k = 0; k < n; k++) cs[k]->events_on = cs[k]->ev_full = true; }
   } events_mode{cs, nslots};
-  for (int k = 0; k < nslots; k++) cs[k]->events_on = g_opt_batch_times.load();
+  for (int k = 0; k < nslots; k++)
+    cs[k]->events_on = cs[k]->ev_full = g_opt_batch_times.load();
   CK(cudaSetDevice(device));
   if (user) {  // order the batch after prior work on the caller's stream
     CK(cudaEventRecord(cs[0]->ev[4], user));
@@ -1616,6 +1626,7 @@ int sc_set_option(const char* name, int value) {
   else if (std::strcmp(name, "grid_div") == 0) g_opt_grid_div = std::max(1, value);
   else if (std::strcmp(name, "pdl") == 0) g_opt_pdl = value != 0;
   else if (std::strcmp(name, "fork") == 0) g_opt_fork = value != 0;
+  else if (std::strcmp(name, "stage_times") == 0) g_opt_stage_times = std::max(0, std::min(2, value));
   else if (std::strcmp(name, "pack_tma") == 0) g_opt_pack_tma = std::max(0, std::min(3, value));
   else if (std::strcmp(name, "sparse_bits") == 0) g_opt_sparse = value != 0;
   else if (std::strcmp(name, "batch_stage_times") == 0) g_opt_batch_times = value != 0;

@@ -5,6 +5,7 @@ import torch
 import bench
 import paper_2510_02894_b200 as sc
 from paper_2510_02894_b200 import _native
+_native.set_option("stage_times", 2)  # per-stage events for last_kernel_times
 
 for w in ("c2", "c3", "c5"):
     rois, _ = bench.load_workload(w)

@@ -2,6 +2,7 @@ import sys; sys.path.insert(0,'.')
 import numpy as np
 import paper_2510_02894_b200 as sc
 from paper_2510_02894_b200 import _native, synth
+_native.set_option("stage_times", 2)  # per-stage events for last_kernel_times
 m = synth.synth_mask("sphere", (24,24,24), radius=8)
 for g in (0, 1):
     _native.set_option("graphs", g)

@@ -40,9 +40,11 @@ for w in sys.argv[3:]:
         _native.set_option(opt, v)
         assert sc.calculate_coefficients_device(d, sp).to_dict() == ref, (opt, v)
         one = []
+        _native.set_option("stage_times", 2)
         for _ in range(10):
             sc.calculate_coefficients_device(d, sp)
             one.append(_native.last_kernel_times(0))
+        _native.set_option("stage_times", 1)
         med = {k: sorted(t[k] for t in one)[5] * 1e3 for k in one[0] if k != "h2d_ms"}
         print(f"{w} {opt}={v}: batch {rate(d, sp, ref=ref):6.1f} us/ROI | single-call stages (us) "
               + " ".join(f"{k[:-3]} {t:.1f}" for k, t in med.items()), flush=True)
