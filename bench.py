@@ -325,7 +325,7 @@ def measure_device(sc, _native, d_mask, sp, stream, steps, warmup, dev, world):
             for k, v in _native.last_kernel_times(dev).items():
                 kt[k].append(v)
     finally:
-        _native.set_option("stage_times", 1)
+        _native.set_option("stage_times", 0)
     med = {k: statistics.median(v) for k, v in kt.items() if v}
     return ms, med, _native.last_diagnostics(dev), launches, c
 

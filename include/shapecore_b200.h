@@ -168,11 +168,12 @@ int sc_last_diagnostics(int device, int64_t* out, int n);
  * "host_threads" (hardware threads, <= 32) = threads of the host slab scan;
  * "grid_div" (2) = divisor of the per-ROI kernels' grids (SMs x blocks/SM):
  * fewer resident blocks per ROI let more ROIs share the GPU;
- * "stage_times" (1) = CUDA events in single-call graphs: 0 none (mesh_ms /
- * diameters_ms 0), 1 mesh / diameters boundaries, 2 every stage boundary
- * (sc_last_kernel_times needs 2; each event node costs latency);
- * "batch_stage_times" (0) = per-stage CUDA events in batch graphs (mesh_ms /
- * diameters_ms of batch results are 0 without them);
+ * "stage_times" (0) = CUDA events in single-call graphs: 0 none (mesh_ms /
+ * diameters_ms then come from device %globaltimer stamps), 1 mesh / diameters
+ * boundaries, 2 every stage boundary (sc_last_kernel_times needs 2; each
+ * event node adds latency);
+ * "batch_stage_times" (0) = per-stage CUDA events in batch graphs (without
+ * them mesh_ms / diameters_ms come from the %globaltimer stamps);
  * "pack_tma" (0) = CTAs per SM of the cp.async.bulk (TMA) variant of the
  * pack (0 = the 128-bit-load pack);
  * "sparse_bits" (1) = the pack writes only nonzero 16-word segments of the

@@ -103,7 +103,7 @@ std::atomic<bool> g_opt_pdl{false};  // programmatic dependent launch in batch g
 std::atomic<bool> g_opt_sparse{true};  // sparse bit volume (segment map), option "sparse_bits"
 std::atomic<int> g_opt_pack_tma{0};  // TMA bulk-copy pack, CTAs per SM (0 = 128-bit load pack)
 std::atomic<bool> g_opt_fork{true};
-std::atomic<int> g_opt_stage_times{1};  // single-call graph events: 0 none, 1 mesh/diam, 2 all  // planar chain on a second stream (option "fork")
+std::atomic<int> g_opt_stage_times{0};  // single-call graph events: 0 none (timer stamps), 1 mesh/diam, 2 all  // planar chain on a second stream (option "fork")
 std::atomic<int> g_opt_grid_div{2};  // divisor of the latency-bound kernel grids (2: best measured batch rate)
 std::atomic<int> g_opt_pack_bps{0};  // pack blocks per SM (0 = occupancy limit)  // divisor of the latency-bound kernels' grids
 std::atomic<int> g_opt_pack_mode{0};  // bit 0: one step per pack block; bit 1: low-priority pack;
@@ -915,8 +915,14 @@ int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
     c->last_diag[6] = (long long)h.n_sub;
     c->last_diag[7] = (long long)h.n_psub;
   }
-  out->mesh_ms = c->events_on ? ev_ms(c->kev[0], c->kev[2]) : 0.0;
-  out->diameters_ms = c->events_on ? ev_ms(c->kev[2], c->kev[6]) : 0.0;
+  if (c->events_on) {
+    out->mesh_ms = ev_ms(c->kev[0], c->kev[2]);
+    out->diameters_ms = ev_ms(c->kev[2], c->kev[6]);
+  } else {  // device %globaltimer stamps (no event nodes in the graph)
+    const Stats& h = *c->h_stats;
+    out->mesh_ms = h.t_mesh > h.t_start ? (double)(h.t_mesh - h.t_start) * 1e-6 : 0.0;
+    out->diameters_ms = h.t_end > h.t_mesh ? (double)(h.t_end - h.t_mesh) * 1e-6 : 0.0;
+  }
   return SC_OK;
 }
 

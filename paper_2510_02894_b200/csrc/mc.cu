@@ -37,6 +37,7 @@ __global__ void init_stats(Stats* st, uint32_t* __restrict__ segmap, long long n
     __syncthreads();
     if (t < 3) st->bbox[t] = INT_MAX;
     if (t >= 3 && t < 6) st->bbox[t] = -1;
+    if (t == 0) st->t_start = global_ns();
   }
   for (long long i = (long long)blockIdx.x * blockDim.x + t; i < n_seg;
        i += (long long)gridDim.x * blockDim.x)

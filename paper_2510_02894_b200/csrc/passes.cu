@@ -46,6 +46,8 @@ __global__ void __launch_bounds__(kDiamThreads) diam_refine(
   __syncthreads();
   if ((long long)st->n_pwork <= pwcap)
     refine_planar(sorted, start, pwork, rp, pumax, st, s_a, s_b, s_red, s_list, s_n);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&st->t_end, global_ns());
 }
 
 }  // namespace sc

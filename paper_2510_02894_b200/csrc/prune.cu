@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_all(unsigned int* __restric
                                                          unsigned int* __restrict__ pbin_cursor,
                                                          unsigned long long* __restrict__ pext) {
   pdl_enter();
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->t_mesh = global_ns();  // marching cubes done
   int bb[6];
 #pragma unroll
   for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];

@@ -37,7 +37,17 @@ struct Stats {
   unsigned long long plane_chunks;     // 256-entry chunks over all planes
   unsigned long long n_sub;            // 3-D 64 x 64 sub-pairs kept (pass 1 evaluates these)
   unsigned long long n_psub;           // planar 64 x 64 sub-pairs kept
+  // %globaltimer stamps (ns): ROI start (init_stats), end of the marching-cubes
+  // stage (scan_all start), end of the diameters (last diam_refine block):
+  // mesh_ms / diameters_ms without event nodes in the graph.
+  unsigned long long t_start, t_mesh, t_end;
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Work entries carry, in the top 4 bits of the J field, which 64 x 64 sub-pairs
 // of the 128 x 128 chunk pair can reach the lower bound (bit 2a + b: I half a,

@@ -579,3 +579,28 @@ def test_randomized_stress_parity(cuda_device):
                        capture_output=True, text=True, timeout=580)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "stress parity ok" in r.stdout
+
+
+def test_stage_times_from_device_timestamps(sc, cuda_device):
+    """mesh_ms / diameters_ms without event nodes (device %globaltimer stamps)
+    are positive and consistent with the event-timed values; all event levels
+    give identical results."""
+    from paper_2510_02894_b200 import _native, synth
+
+    arr = synth.kits_like(128, 128, 96, (0.8, 0.8, 1.0), 20.0)
+    recs = {}
+    try:
+        for lvl in (0, 1, 2):
+            _native.set_option("stage_times", lvl)
+            c = sc.calculate_coefficients(arr, (0.8, 0.8, 1.0))
+            c = sc.calculate_coefficients(arr, (0.8, 0.8, 1.0))
+            assert c.mesh_ms > 0 and c.diameters_ms > 0, lvl
+            assert c.total_ms >= c.mesh_ms + c.diameters_ms
+            recs[lvl] = c.to_dict()
+            times = _native.last_kernel_times(cuda_device)
+            assert (times["pack_ms"] > 0) == (lvl == 2)
+    finally:
+        _native.set_option("stage_times", 0)
+    assert recs[0] == recs[1] == recs[2]
+    outs = sc.calculate_coefficients_batch([arr] * 4, [(0.8, 0.8, 1.0)] * 4)
+    assert all(o.mesh_ms > 0 and o.diameters_ms > 0 for o in outs)

@@ -44,7 +44,7 @@ for w in sys.argv[3:]:
         for _ in range(10):
             sc.calculate_coefficients_device(d, sp)
             one.append(_native.last_kernel_times(0))
-        _native.set_option("stage_times", 1)
+        _native.set_option("stage_times", 0)
         med = {k: sorted(t[k] for t in one)[5] * 1e3 for k in one[0] if k != "h2d_ms"}
         print(f"{w} {opt}={v}: batch {rate(d, sp, ref=ref):6.1f} us/ROI | single-call stages (us) "
               + " ".join(f"{k[:-3]} {t:.1f}" for k, t in med.items()), flush=True)

@@ -14,7 +14,7 @@ for w in sys.argv[1:] or ["c2"]:
     rois, _ = bench.load_workload(w)
     m, sp = rois[0]
     d = torch.from_numpy(m).cuda()
-    for st in (1, 0):
+    for st in (2, 1, 0):
         _native.set_option("stage_times", st)
         for _ in range(10):
             sc.calculate_coefficients_device(d, sp)
@@ -24,4 +24,4 @@ for w in sys.argv[1:] or ["c2"]:
             sc.calculate_coefficients_device(d, sp)
         dt = (time.perf_counter() - t0) / 200 * 1e6
         print(f"{w} stage_times={st}: {dt:.1f} us per synchronous call", flush=True)
-    _native.set_option("stage_times", 1)
+    _native.set_option("stage_times", 0)
