@@ -168,6 +168,9 @@ int sc_last_diagnostics(int device, int64_t* out, int n);
  * "host_threads" (hardware threads, <= 32) = threads of the host slab scan;
  * "grid_div" (2) = divisor of the per-ROI kernels' grids (SMs x blocks/SM):
  * fewer resident blocks per ROI let more ROIs share the GPU;
+ * "zero_copy" (1) = the per-ROI parameter and result records travel through
+ * mapped pinned host memory (read by the first kernel, written by the last)
+ * instead of copy operations around each ROI's graph;
  * "stage_times" (0) = CUDA events in single-call graphs: 0 none (mesh_ms /
  * diameters_ms then come from device %globaltimer stamps), 1 mesh / diameters
  * boundaries, 2 every stage boundary (sc_last_kernel_times needs 2; each

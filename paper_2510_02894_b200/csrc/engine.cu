@@ -31,7 +31,8 @@
 namespace sc {
 
 // Kernels (mc.cu, diameter.cu, prune.cu, planar.cu).
-__global__ void init_stats(Stats* st, uint32_t* segmap, long long n_seg);
+__global__ void init_stats(Stats* st, uint32_t* segmap, long long n_seg, const RoiParams* src_rp,
+                           RoiParams* dst_rp);
 template <int U, bool BOX>
 __global__ void pack_bits_v16(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 __global__ void bits_bbox(const RoiParams*, const uint4*, Stats*, const uint32_t*);
@@ -55,7 +56,7 @@ __global__ void diam_pass1(const int4*, long long, const RoiParams*, const uint2
                            Stats*);
 __global__ void diam_refine(const int4*, long long, const RoiParams*, const uint2*, const float*,
                             const int2*, const unsigned int*, const uint2*, long long,
-                            const float*, Stats*);
+                            const float*, Stats*, Stats*);
 __global__ void plane_boxes(const int2*, const unsigned int*, const unsigned int*,
                             const RoiParams*, const Stats*, int4*, unsigned long long*, int4*);
 __global__ void plane_lb(const int2*, const unsigned int*, const unsigned long long*,
@@ -103,6 +104,7 @@ std::atomic<bool> g_opt_pdl{false};  // programmatic dependent launch in batch g
 std::atomic<bool> g_opt_sparse{true};  // sparse bit volume (segment map), option "sparse_bits"
 std::atomic<int> g_opt_pack_tma{0};  // TMA bulk-copy pack, CTAs per SM (0 = 128-bit load pack)
 std::atomic<bool> g_opt_fork{true};
+std::atomic<bool> g_opt_zc{true};  // option "zero_copy": RoiParams / Stats via mapped host memory
 std::atomic<int> g_opt_stage_times{0};  // single-call graph events: 0 none (timer stamps), 1 mesh/diam, 2 all  // planar chain on a second stream (option "fork")
 std::atomic<int> g_opt_grid_div{2};  // divisor of the latency-bound kernel grids (2: best measured batch rate)
 std::atomic<int> g_opt_pack_bps{0};  // pack blocks per SM (0 = occupancy limit)  // divisor of the latency-bound kernels' grids
@@ -225,7 +227,9 @@ struct Ctx {
   int occ_pass1 = 1, occ_pass1s = 1, occ_pack = 1, occ_mc = 1;  // blocks/SM
   int prio_lo = 0, prio_hi = 0;  // stream priority range (least, greatest)
   Stats* d_stats = nullptr;
-  Stats* h_stats = nullptr;  // pinned
+  Stats* h_stats = nullptr;  // pinned (mapped: the pipeline's last kernel writes it)
+  Stats* h_stats_dev = nullptr;     // its device-side address
+  RoiParams* h_rp_dev = nullptr;    // device-side address of h_rp (read by init_stats)
   RoiParams* d_rp = nullptr;  // per-ROI launch parameters (device)
   RoiParams* h_rp = nullptr;  // staging copy (pinned)
   long long dcap_sz = 0;      // vertices the diameter-side buffers are sized for (monotonic)
@@ -268,6 +272,7 @@ struct Ctx {
     bool pdl;           // option "pdl"
     bool sparse;        // option "sparse_bits"
     bool fork;          // option "fork"
+    bool zc;            // option "zero_copy"
     unsigned long long gen;
     cudaGraphExec_t exec;
     unsigned long long launches;
@@ -338,6 +343,8 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     CK(cudaMallocHost(&c->h_stats, sizeof(Stats)));
     CK(cudaMalloc(&c->d_rp, sizeof(RoiParams)));
     CK(cudaMallocHost(&c->h_rp, sizeof(RoiParams)));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_stats_dev), c->h_stats, 0));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_rp_dev), c->h_rp, 0));
     CK(cudaMalloc(&c->d_tabs, sizeof(CaseTables)));
     CK(cudaMemcpy(c->d_tabs, &case_geom().tabs, sizeof(CaseTables), cudaMemcpyHostToDevice));
     CK(upload_mesh_tables());
@@ -486,6 +493,16 @@ int lgrid(const Ctx* c, int k) {
   return std::max(1, c->sms * k / std::max(1, g_opt_grid_div.load()));
 }
 
+// Zero-copy per-ROI records (option "zero_copy", default on): init_stats reads
+// RoiParams from mapped pinned host memory and diam_refine's last block writes
+// the accumulator record back there, so the ROI is the graph alone -- no H2D
+// copy before it and no D2H copy node inside it.  Off for the debug stage cuts
+// (diam_refine may not run).
+bool zero_copy_records(const Ctx* c) {
+  (void)c;
+  return g_opt_zc.load() && g_opt_stages.load() >= (1 << 20);
+}
+
 // Launch of a per-ROI pipeline kernel.  In batch graphs (no stage-event nodes
 // between the kernels) it carries the programmatic-dependent-launch attribute
 // (option "pdl"): the kernel is scheduled while its predecessor drains and
@@ -521,8 +538,10 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   // (the pack marks nonzero segments of a cleared map; the no-pack debug mode
   // keeps the previous map)
   const bool clear_map = g_opt_sparse.load() && !(g_opt_pack_mode.load() & 4);
+  const bool zc = zero_copy_records(c);
   init_stats<<<clear_map ? 8 : 1, 256, 0, s>>>(c->d_stats, c->segmap.p,
-                                               clear_map ? (long long)c->segmap.cap : 0LL);
+                                               clear_map ? (long long)c->segmap.cap : 0LL,
+                                               zc ? c->h_rp_dev : nullptr, c->d_rp);
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[0], s));  // kev0..kev1 = the HBM pass alone
@@ -667,7 +686,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   CK(record(c, c->kev[5], s));
   CK(launch_k(c, s, lgrid(c, 2), 256, diam_refine, c->keys_sorted.p, dcap, rp, c->work.p, c->warp_max.p,
                                          c->plane_sorted.p, c->plane_start.p, c->plane_work.p,
-                                         pucap, c->plane_umax.p, c->d_stats));
+                                         pucap, c->plane_umax.p, c->d_stats, zc ? c->h_stats_dev : nullptr));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[6], s));
@@ -728,7 +747,8 @@ int enqueue_with_copies(Ctx* c, bool fast, cudaStream_t s, int shard, int nshard
   if (rc) return rc;
   if (d_sq4)
     CK(cudaMemcpyAsync(d_sq4, c->d_stats->sq, 4 * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  CK(cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
+  if (!zero_copy_records(c))  // else diam_refine published the record itself
+    CK(cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
   return SC_OK;
 }
 
@@ -769,7 +789,8 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   h.wcap = (long long)std::min(c->work.cap, c->warp_max.cap);
   const bool hp = host_prof_on();
   double t0 = hp ? wall_ms() : 0.0;
-  CK(cudaMemcpyAsync(c->d_rp, c->h_rp, sizeof(RoiParams), cudaMemcpyHostToDevice, s));
+  if (!zero_copy_records(c))  // else init_stats reads the record from mapped host memory
+    CK(cudaMemcpyAsync(c->d_rp, c->h_rp, sizeof(RoiParams), cudaMemcpyHostToDevice, s));
   if (hp) { const double t1 = wall_ms(); g_hprof.copy += t1 - t0; t0 = t1; }
   const bool fast = nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0;
   if (!g_opt_graphs.load() || s == nullptr)
@@ -784,6 +805,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
         g.grid_div == g_opt_grid_div.load() &&
         g.events == c->events_on && g.ev_full == c->ev_full && g.pdl == g_opt_pdl.load() &&
         g.sparse == g_opt_sparse.load() && g.fork == g_opt_fork.load() &&
+        g.zc == g_opt_zc.load() &&
         g.gen == c->gen) {
       CK(cudaGraphLaunch(g.exec, s));
       if (hp) g_hprof.launch += wall_ms() - t0;
@@ -814,8 +836,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
                     g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load() + 4096 * g_opt_pack_tma.load(),
                     g_opt_grid_div.load(),
                     c->events_on, c->ev_full, g_opt_pdl.load(), g_opt_sparse.load(),
-                    g_opt_fork.load(),
-                    c->gen, exec, launches};
+                    g_opt_fork.load(), g_opt_zc.load(), c->gen, exec, launches};
   c->graphs.push_back(g);
   CK(cudaGraphLaunch(exec, s));
   g_launches.fetch_add(launches, std::memory_order_relaxed);
@@ -1243,7 +1264,7 @@ int run_mesh(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
     h.sparse = 0;  // the export kernels read every bit-volume word
     h.wcap = 0;
     CK(cudaMemcpyAsync(c->d_rp, c->h_rp, sizeof(RoiParams), cudaMemcpyHostToDevice, s));
-    init_stats<<<1, 256, 0, s>>>(c->d_stats, c->segmap.p, 0LL);
+    init_stats<<<1, 256, 0, s>>>(c->d_stats, c->segmap.p, 0LL, nullptr, c->d_rp);
     CKL(1);
     if (nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0) {
       pack_bits_v16<4, true><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(
@@ -1632,6 +1653,7 @@ int sc_set_option(const char* name, int value) {
   else if (std::strcmp(name, "grid_div") == 0) g_opt_grid_div = std::max(1, value);
   else if (std::strcmp(name, "pdl") == 0) g_opt_pdl = value != 0;
   else if (std::strcmp(name, "fork") == 0) g_opt_fork = value != 0;
+  else if (std::strcmp(name, "zero_copy") == 0) g_opt_zc = value != 0;
   else if (std::strcmp(name, "stage_times") == 0) g_opt_stage_times = std::max(0, std::min(2, value));
   else if (std::strcmp(name, "pack_tma") == 0) g_opt_pack_tma = std::max(0, std::min(3, value));
   else if (std::strcmp(name, "sparse_bits") == 0) g_opt_sparse = value != 0;

@@ -29,8 +29,19 @@ constexpr unsigned kFull = 0xffffffffu;
 
 // Per-ROI reset: block 0 zeroes the accumulator record; every block clears
 // its share of the bit-volume segment map (n_seg words, may be 0).
-__global__ void init_stats(Stats* st, uint32_t* __restrict__ segmap, long long n_seg) {
+//
+// src_rp (optional): the slot's RoiParams in mapped pinned host memory, read
+// over PCIe and stored to dst_rp here, so no separate host->device copy has to
+// precede the ROI's graph.
+__global__ void init_stats(Stats* st, uint32_t* __restrict__ segmap, long long n_seg,
+                           const RoiParams* src_rp, RoiParams* dst_rp) {
   int t = threadIdx.x;
+  if (blockIdx.x == 0 && src_rp) {
+    static_assert(sizeof(RoiParams) % 4 == 0, "RoiParams is copied as 32-bit words");
+    const volatile unsigned int* s = reinterpret_cast<const volatile unsigned int*>(src_rp);
+    unsigned int* d = reinterpret_cast<unsigned int*>(dst_rp);
+    for (int i = t; i < (int)(sizeof(RoiParams) / 4); i += blockDim.x) d[i] = s[i];
+  }
   if (blockIdx.x == 0) {
     for (int i = t; i < (int)(sizeof(Stats) / 8); i += blockDim.x)
       reinterpret_cast<unsigned long long*>(st)[i] = 0ull;

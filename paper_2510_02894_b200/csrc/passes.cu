@@ -34,20 +34,30 @@ __global__ void __launch_bounds__(kDiamThreads) diam_refine(
     const uint2* __restrict__ work, const float* __restrict__ umax,
     const int2* __restrict__ sorted, const unsigned int* __restrict__ start,
     const uint2* __restrict__ pwork, long long pwcap, const float* __restrict__ pumax,
-    Stats* __restrict__ st) {
+    Stats* __restrict__ st, Stats* out_host) {
   pdl_enter();
-  if (st->ovf || st->bbox[3] < 0) return;  // block-uniform
   __shared__ double s_a[kChunk], s_b[kChunk], s_c[kChunk];
   __shared__ double s_red[kDiamThreads / 32];
   __shared__ unsigned int s_list[kDiamThreads];
   __shared__ int s_n;
-  if ((long long)st->n_work <= rp->wcap)
-    refine_3d(keys, cap, rp, work, umax, st, s_a, s_b, s_c, s_list, s_n);
-  __syncthreads();
-  if ((long long)st->n_pwork <= pwcap)
-    refine_planar(sorted, start, pwork, rp, pumax, st, s_a, s_b, s_red, s_list, s_n);
-  __syncthreads();
-  if (threadIdx.x == 0) atomicMax(&st->t_end, global_ns());
+  if (!st->ovf && st->bbox[3] >= 0) {  // block-uniform
+    if ((long long)st->n_work <= rp->wcap)
+      refine_3d(keys, cap, rp, work, umax, st, s_a, s_b, s_c, s_list, s_n);
+    __syncthreads();
+    if ((long long)st->n_pwork <= pwcap)
+      refine_planar(sorted, start, pwork, rp, pumax, st, s_a, s_b, s_red, s_list, s_n);
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(&st->t_end, global_ns());
+  }
+  // out_host (optional): the slot's accumulator record in mapped pinned host
+  // memory; the last block to finish publishes the complete record there, so
+  // no device->host copy follows the ROI's graph.
+  if (out_host && last_block(&st->done2)) {
+    const volatile unsigned long long* s = reinterpret_cast<const volatile unsigned long long*>(st);
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(out_host);
+    for (int i = threadIdx.x; i < (int)(sizeof(Stats) / 8); i += blockDim.x) d[i] = s[i];
+    __threadfence_system();
+  }
 }
 
 }  // namespace sc
