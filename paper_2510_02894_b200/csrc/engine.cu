@@ -709,7 +709,7 @@ void fill_out(const Stats& h, const double sp[3], sc_coeffs* out) {
   long long T = 0, active = 0;
   for (int k = 0; k < kNumCases; k++) {
     unsigned long long cnt = 0;
-    for (int c = 0; c < kHistCopies; c++) cnt += h.hist[c][k];
+    for (int c = 0; c < (h.hist_merged ? 1 : kHistCopies); c++) cnt += h.hist[c][k];
     if (!cnt) continue;
     area += (double)cnt * at[k];
     T += (long long)cnt * tri[k];

@@ -52,10 +52,21 @@ __global__ void __launch_bounds__(kDiamThreads) diam_refine(
   // out_host (optional): the slot's accumulator record in mapped pinned host
   // memory; the last block to finish publishes the complete record there, so
   // no device->host copy follows the ROI's graph.
+  // The case histogram goes out merged (hist[0] = sum of the kHistCopies
+  // copies, marked by hist_merged), so ~2.7 KB cross PCIe instead of 16.8 KB.
   if (out_host && last_block(&st->done2)) {
     const volatile unsigned long long* s = reinterpret_cast<const volatile unsigned long long*>(st);
     unsigned long long* d = reinterpret_cast<unsigned long long*>(out_host);
-    for (int i = threadIdx.x; i < (int)(sizeof(Stats) / 8); i += blockDim.x) d[i] = s[i];
+    for (int k = threadIdx.x; k < kNumCases; k += blockDim.x) {
+      unsigned long long sum = 0;
+#pragma unroll
+      for (int c = 0; c < kHistCopies; c++) sum += s[c * kNumCases + k];
+      d[k] = sum;
+    }
+    constexpr int kTail = kHistCopies * kNumCases;  // first word after the histograms
+    for (int i = kTail + threadIdx.x; i < (int)(sizeof(Stats) / 8); i += blockDim.x) d[i] = s[i];
+    __syncthreads();
+    if (threadIdx.x == 0) out_host->hist_merged = 1u;
     __threadfence_system();
   }
 }

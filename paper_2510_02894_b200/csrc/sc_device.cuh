@@ -21,7 +21,7 @@ struct Stats {
   long long vol_k;                     // 48*volume/(sx*sy*sz), exact (Appendix A)
   int bbox[6];                         // xmin, ymin, zmin, xmax, ymax, zmax of occupied voxels
   unsigned int d3_f32;                 // fp32 bits of the pass-1 max squared 3-D distance
-  unsigned int pad0;
+  unsigned int hist_merged;            // host copy only: hist[0] already holds the sum
   unsigned long long sq[4];            // fp64 bits: exact squared maxima (3d, xy, xz, yz)
   unsigned long long n_cand;           // 3-D (tile pair, warp) units re-checked in fp64
   unsigned long long n_pcand;          // planar tile pairs re-checked in fp64
