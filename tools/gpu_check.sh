@@ -12,7 +12,7 @@ if [ "${1:-}" != "quick" ]; then
   timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file $OUT/launches.csv python tools/one_roi.py > $OUT/ncu_bench.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on \
-      -k regex:"pack_bits_v16|bits_bbox|mc_cells|plane_bins_scan|scan_all|scatter_all|boxes_extremes|unit_filter|plane_boxes|plane_lb|plane_filter|diam_pass1|diam_refine" -s 13 -c 13 \
+      -k regex:"pack_bits_v16|bits_bbox|mc_cells|scan_all|scatter_all|boxes_extremes|unit_filter|plane_boxes|plane_lb|plane_filter|diam_pass1|diam_refine" -s 12 -c 12 \
       -o $OUT/prof -f python tools/one_roi.py > $OUT/ncu_full.log 2>&1
 fi
 echo done
