@@ -49,7 +49,9 @@ __global__ void scatter_all(const int4*, long long, const Stats*, unsigned int*,
 __global__ void boxes_extremes(const int4*, long long, const RoiParams*, Stats*, int4*, int4*,
                                int4*);
 __global__ void unit_filter(const int4*, const int4*, long long, const RoiParams*, int, int, int,
-                            Stats*, uint2*, const int4*, const int4*);
+                            Stats*, uint2*, const int4*, const int4*, uint2*, long long);
+__global__ void unit_expand(const int4*, long long, const RoiParams*, int, int, int, Stats*, uint2*,
+                            const int4*, const uint2*, long long);
 template <bool PACKED>
 __global__ void diam_pass1(const int4*, long long, const RoiParams*, const uint2*, float*,
                            const int2*, const unsigned int*, const uint2*, long long, float*,
@@ -238,6 +240,7 @@ struct Ctx {
   DevBuf<uint32_t> segmap;  // 1 bit per 16-word bit-volume segment (sparse pack)
   DevBuf<int4> keys, keys_sorted, boxes, sboxes;  // chunk / super-chunk boxes (lo, hi)
   DevBuf<int4> hboxes;  // boxes of the two 64-vertex halves of every chunk
+  DevBuf<uint2> slist;  // surviving super-chunk pairs (two-level filter of large ROIs)
   DevBuf<unsigned int> sort_counts, sort_cursor;
   DevBuf<uint2> work;  // surviving 3-D chunk pairs (I, J)
   DevBuf<float> warp_max, plane_umax;
@@ -285,7 +288,7 @@ struct Ctx {
 
   unsigned long long fingerprint() const {
     unsigned long long h = 1469598103934665603ull;
-    const void* ps[] = {bits.p, segmap.p, keys.p, keys_sorted.p, boxes.p, sboxes.p, hboxes.p,
+    const void* ps[] = {bits.p, segmap.p, keys.p, keys_sorted.p, boxes.p, sboxes.p, hboxes.p, slist.p,
                         sort_counts.p, sort_cursor.p,
                         work.p, warp_max.p, plane_umax.p,
                         plane_counts.p, plane_start.p, plane_tstart.p, plane_sorted.p,
@@ -366,6 +369,7 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
                                (const void*)pack_bits_generic, (const void*)mc_cells,
                                (const void*)scan_all, (const void*)scatter_all,
                                (const void*)boxes_extremes, (const void*)unit_filter,
+                               (const void*)unit_expand,
                                (const void*)diam_pass1<true>, (const void*)diam_pass1<false>,
                                (const void*)diam_refine, (const void*)cloud_diameters,
                                (const void*)plane_boxes,
@@ -453,6 +457,10 @@ int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, lo
   CK(c->keys_sorted.ensure((size_t)dcap));
   CK(c->boxes.ensure((size_t)(2 * (C + 1))));
   CK(c->hboxes.ensure((size_t)(4 * (C + 1))));
+  {  // every super pair can survive (pruning off): size for all of them
+    const long long CT = (C + 7) / 8;
+    CK(c->slist.ensure((size_t)(C * (C + 1) / 2 > (4LL << 20) ? CT * (CT + 1) / 2 : 1)));
+  }
   CK(c->sboxes.ensure((size_t)(2 * (C / 8 + 1))));
   {
     unsigned int* before = c->sort_counts.p;
@@ -648,7 +656,10 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(launch_k(c, s, lgrid(c, 4), 256, unit_filter, c->keys_sorted.p, c->boxes.p, dcap, rp, prune, shard,
-                                         nshards, c->d_stats, c->work.p, c->sboxes.p, c->hboxes.p));
+                                         nshards, c->d_stats, c->work.p, c->sboxes.p, c->hboxes.p, c->slist.p, (long long)c->slist.cap));
+  CKL(1);
+  CK(launch_k(c, s, lgrid(c, 4), 256, unit_expand, c->boxes.p, dcap, rp, prune, shard, nshards,
+              c->d_stats, c->work.p, c->hboxes.p, c->slist.p, (long long)c->slist.cap));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[3], s));

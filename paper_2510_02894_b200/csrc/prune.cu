@@ -359,6 +359,71 @@ __device__ __forceinline__ double axis_reach(int loA, int hiA, int loB, int hiB,
   return d * d;
 }
 
+// Per-launch constants of the chunk-pair test (unit_filter / unit_expand).
+struct PairTest {
+  const int4* boxes;
+  const int4* hboxes;
+  Stats* st;
+  uint2* work;
+  double h3[3];
+  double thr;
+  long long C, wcap;
+  int prune, shard, nshards;
+};
+
+__device__ __forceinline__ double box_reach(const PairTest& F, int4 alo, int4 ahi, int4 blo,
+                                            int4 bhi) {
+  return axis_reach(alo.x, ahi.x, blo.x, bhi.x, F.h3[0]) +
+         axis_reach(alo.y, ahi.y, blo.y, bhi.y, F.h3[1]) +
+         axis_reach(alo.z, ahi.z, blo.z, bhi.z, F.h3[2]);
+}
+
+// Which 64 x 64 sub-pairs of a kept chunk pair (i, j) can reach LB (bit
+// 2a + b, half a of i, half b of j; for i == j the mirrored (1, 0) is the same
+// pairs as (0, 1)).
+__device__ __forceinline__ unsigned int sub_mask(const PairTest& F, int i, int j) {
+  unsigned int m = 0u;
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int b = 0; b < 2; b++)
+      if (!(i == j && a == 1 && b == 0) &&
+          box_reach(F, F.hboxes[4 * i + 2 * a], F.hboxes[4 * i + 2 * a + 1],
+                    F.hboxes[4 * j + 2 * b], F.hboxes[4 * j + 2 * b + 1]) >= F.thr)
+        m |= 1u << (2 * a + b);
+  return m;
+}
+
+// One chunk pair per lane (all 32 lanes call): shard ownership by the pair's
+// identity (its tile_pair index, so the split is the same whatever order the
+// lists come out in), the box test, the sub-pair mask, and a warp-aggregated
+// append of the kept units.
+__device__ __forceinline__ void test_chunk_pair(const PairTest& F, bool valid, int i, int j) {
+  const int lane = threadIdx.x & 31;
+  bool keep = valid && i < F.C && j < F.C && j >= i &&
+              ((long long)i * F.C - (long long)i * (i - 1) / 2 + (j - i)) % F.nshards == F.shard;
+  if (keep && F.prune)
+    keep = box_reach(F, F.boxes[2 * i], F.boxes[2 * i + 1], F.boxes[2 * j], F.boxes[2 * j + 1]) >=
+           F.thr;
+  unsigned int sub = 0xFu;
+  if (keep && F.prune) {
+    sub = sub_mask(F, i, j);
+    keep = sub != 0u;
+  }
+  const unsigned int mask = __ballot_sync(0xffffffffu, keep);
+  if (!mask) return;
+  const unsigned int nsub = __reduce_add_sync(0xffffffffu, keep ? __popc(sub) : 0u);
+  unsigned long long pos = 0;
+  if (lane == 0) {
+    pos = atomicAdd(&F.st->n_work, (unsigned long long)__popc(mask));
+    atomicAdd(&F.st->n_sub, (unsigned long long)nsub);
+  }
+  pos = __shfl_sync(0xffffffffu, pos, 0);
+  const long long o = (long long)pos + __popc(mask & ((1u << lane) - 1));
+  if (keep && o < F.wcap)
+    F.work[o] = make_uint2((unsigned int)i, (unsigned int)j | (sub << kSubShift));
+}
+
 // Every block: LB = max exact (reference fp64 arithmetic) squared distance
 // among the 26 extreme vertices (a real pair, so LB <= D^2; block 0 also seeds
 // the exact 3-D maximum with it).  Then every chunk pair (I <= J) is kept iff
@@ -370,7 +435,8 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
                                                    int shard, int nshards, Stats* __restrict__ st,
                                                    uint2* __restrict__ work,
                                                    const int4* __restrict__ sboxes,
-                                                   const int4* __restrict__ hboxes) {
+                                                   const int4* __restrict__ hboxes,
+                                                   uint2* __restrict__ slist, long long scap) {
   pdl_enter();
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
@@ -404,72 +470,26 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
   const double thr = lb * (1.0 - 1e-9);  // UB and LB are exact up to fp64 rounding
   // Two levels: a pair of super-chunks (8 chunks = 1024 vertices, boxes from
   // boxes_extremes) is tested first; only if it can reach LB are its (up to
-  // 64) chunk pairs tested and listed -- row by row, so consecutive units of
-  // a pass-1 warp usually share the I chunk.
+  // 64) chunk pairs tested -- by unit_expand, one thread per chunk pair.
   const long long C = (n + kChunkV - 1) / kChunkV;
   const long long CT = (C + kSuper - 1) / kSuper;
   const long long units = CT * (CT + 1) / 2;
-  const double h3[3] = {0.5 * f.sx, 0.5 * f.sy, 0.5 * f.sz};
-  const long long wcap = rp->wcap;
+  PairTest F{boxes, hboxes, st, work, {0.5 * f.sx, 0.5 * f.sy, 0.5 * f.sz}, thr, C, rp->wcap,
+             prune, shard, nshards};
   const int lane = threadIdx.x & 31;
-  auto reach = [&](int4 alo, int4 ahi, int4 blo, int4 bhi) {
-    return axis_reach(alo.x, ahi.x, blo.x, bhi.x, h3[0]) +
-           axis_reach(alo.y, ahi.y, blo.y, bhi.y, h3[1]) +
-           axis_reach(alo.z, ahi.z, blo.z, bhi.z, h3[2]);
-  };
-  // Which 64 x 64 sub-pairs of a kept chunk pair (i, j) can reach LB
-  // (bit 2a + b, half a of i, half b of j; for i == j the mirrored (1, 0) is
-  // the same pairs as (0, 1)).
-  auto subs = [&](int i, int j) {
-    unsigned int m = 0u;
-#pragma unroll
-    for (int a = 0; a < 2; a++)
-#pragma unroll
-      for (int b = 0; b < 2; b++)
-        if (!(i == j && a == 1 && b == 0) &&
-            reach(hboxes[4 * i + 2 * a], hboxes[4 * i + 2 * a + 1], hboxes[4 * j + 2 * b],
-                  hboxes[4 * j + 2 * b + 1]) >= thr)
-          m |= 1u << (2 * a + b);
-    return m;
-  };
-  // Append the kept units of this warp step (all lanes call).
-  auto emit = [&](bool keep, int i, int j, unsigned int sub) {
-    const unsigned int mask = __ballot_sync(0xffffffffu, keep);
-    if (!mask) return;
-    const unsigned int nsub = __reduce_add_sync(0xffffffffu, keep ? __popc(sub) : 0u);
-    unsigned long long pos = 0;
-    if (lane == 0) {
-      pos = atomicAdd(&st->n_work, (unsigned long long)__popc(mask));
-      atomicAdd(&st->n_sub, (unsigned long long)nsub);
-    }
-    pos = __shfl_sync(0xffffffffu, pos, 0);
-    const long long o = (long long)pos + __popc(mask & ((1u << lane) - 1));
-    if (keep && o < wcap)
-      work[o] = make_uint2((unsigned int)i, (unsigned int)j | (sub << kSubShift));
-  };
   const long long fine_units = C * (C + 1) / 2;
   if (fine_units <= kSingleLevelMax) {
-    // Small ROI: every chunk pair tested directly (one level, no serial
-    // expansion chains), listed in tile_pair order (I-major).
+    // Small ROI: every chunk pair tested directly, listed in tile_pair order.
     for (long long base = (long long)blockIdx.x * blockDim.x; base < fine_units;
          base += (long long)gridDim.x * blockDim.x) {
       const long long u = base + threadIdx.x;
-      bool keep = false;
       int i = 0, j = 0;
-      unsigned int sub = 0xFu;
-      if (u < fine_units) {
-        tile_pair(u, C, i, j);
-        keep = u % nshards == shard &&
-               (!prune || reach(boxes[2 * i], boxes[2 * i + 1], boxes[2 * j], boxes[2 * j + 1]) >= thr);
-        if (keep && prune) {
-          sub = subs(i, j);
-          keep = sub != 0u;
-        }
-      }
-      emit(keep, i, j, sub);
+      if (u < fine_units) tile_pair(u, C, i, j);
+      test_chunk_pair(F, u < fine_units, i, j);
     }
     return;
   }
+  // Large ROI: list the surviving super pairs (warp-aggregated append).
   for (long long base = (long long)blockIdx.x * blockDim.x; base < units;
        base += (long long)gridDim.x * blockDim.x) {
     const long long u = base + threadIdx.x;
@@ -477,35 +497,52 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
     int IT = 0, JT = 0;
     if (u < units) {
       tile_pair(u, CT, IT, JT);
-      coarse = !prune || reach(sboxes[2 * IT], sboxes[2 * IT + 1], sboxes[2 * JT],
-                               sboxes[2 * JT + 1]) >= thr;
+      coarse = !prune || box_reach(F, sboxes[2 * IT], sboxes[2 * IT + 1], sboxes[2 * JT],
+                                   sboxes[2 * JT + 1]) >= thr;
     }
-    // The whole warp expands each surviving super pair: lane -> two of its
-    // 64 chunk pairs (rows 0-3, then 4-7), so the chain of dependent loads
-    // per warp is one per survivor rather than 64.
-    unsigned int cm = __ballot_sync(0xffffffffu, coarse);
-    while (cm) {
-      const int src = __ffs(cm) - 1;
-      cm &= cm - 1;
-      const int it = __shfl_sync(0xffffffffu, IT, src), jt = __shfl_sync(0xffffffffu, JT, src);
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int r = h * 32 + lane;
-        const int i = kSuper * it + (r >> 3), j = kSuper * jt + (r & 7);
-        // Shards own chunk pairs by identity (their tile_pair index), so the
-        // split is the same whatever order the lists come out in.
-        bool keep = i < C && j < C && j >= i &&
-                    ((long long)i * C - (long long)i * (i - 1) / 2 + (j - i)) % nshards == shard;
-        if (keep && prune)
-          keep = reach(boxes[2 * i], boxes[2 * i + 1], boxes[2 * j], boxes[2 * j + 1]) >= thr;
-        unsigned int sub = 0xFu;
-        if (keep && prune) {
-          sub = subs(i, j);
-          keep = sub != 0u;
-        }
-        emit(keep, i, j, sub);
-      }
+    const unsigned int cm = __ballot_sync(0xffffffffu, coarse);
+    if (!cm) continue;
+    unsigned long long pos = 0;
+    if (lane == 0) pos = atomicAdd(&st->n_super, (unsigned long long)__popc(cm));
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    const long long o = (long long)pos + __popc(cm & ((1u << lane) - 1));
+    if (coarse && o < scap) slist[o] = make_uint2((unsigned int)IT, (unsigned int)JT);
+  }
+}
+
+// Second level of the large-ROI filter: every chunk pair of every listed super
+// pair, one per thread (lanes 0-31 of a warp = 32 of one super pair's 64), so
+// no warp walks a serial chain of survivors.
+__global__ void __launch_bounds__(256) unit_expand(const int4* __restrict__ boxes, long long cap,
+                                                   const RoiParams* __restrict__ rp, int prune,
+                                                   int shard, int nshards, Stats* __restrict__ st,
+                                                   uint2* __restrict__ work,
+                                                   const int4* __restrict__ hboxes,
+                                                   const uint2* __restrict__ slist,
+                                                   long long scap) {
+  pdl_enter();
+  if (st->ovf) return;
+  const long long ns = min((long long)st->n_super, scap);
+  if (ns == 0) return;  // small ROI: unit_filter listed everything itself
+  const Frame f = rp->f;
+  const long long n = n_verts(st, cap);
+  const long long C = (n + kChunkV - 1) / kChunkV;
+  const double lb = __longlong_as_double((long long)st->lb);
+  PairTest F{boxes, hboxes, st, work, {0.5 * f.sx, 0.5 * f.sy, 0.5 * f.sz}, lb * (1.0 - 1e-9),
+             C, rp->wcap, prune, shard, nshards};
+  const long long total = ns * (kSuper * kSuper);
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < total;
+       base += (long long)gridDim.x * blockDim.x) {
+    const long long t = base + threadIdx.x;
+    const bool valid = t < total;
+    int i = 0, j = 0;
+    if (valid) {
+      const uint2 sp = slist[t >> 6];
+      const int r = (int)(t & 63);
+      i = kSuper * (int)sp.x + (r >> 3);
+      j = kSuper * (int)sp.y + (r & 7);
     }
+    test_chunk_pair(F, valid, i, j);
   }
 }
 

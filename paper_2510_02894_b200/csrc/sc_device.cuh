@@ -37,6 +37,7 @@ struct Stats {
   unsigned long long plane_chunks;     // 256-entry chunks over all planes
   unsigned long long n_sub;            // 3-D 64 x 64 sub-pairs kept (pass 1 evaluates these)
   unsigned long long n_psub;           // planar 64 x 64 sub-pairs kept
+  unsigned long long n_super;          // surviving super-chunk pairs (large ROIs)
   // %globaltimer stamps (ns): ROI start (init_stats), end of the marching-cubes
   // stage (scan_all start), end of the diameters (last diam_refine block):
   // mesh_ms / diameters_ms without event nodes in the graph.
