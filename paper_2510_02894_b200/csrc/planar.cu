@@ -58,11 +58,11 @@ __device__ __forceinline__ unsigned int plane_nchunks(unsigned int np) {
   return np >= 2 ? (np + kPC - 1) / kPC : 0u;
 }
 
-__device__ __forceinline__ unsigned long long pack_pext(float v, unsigned int idx) {
-  unsigned int b = __float_as_uint(v);
-  b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);  // order-preserving
-  return ((unsigned long long)b << 32) | idx;
+__device__ __forceinline__ unsigned int order_key32(float v) {  // order-preserving
+  const unsigned int b = __float_as_uint(v);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
+
 
 // One warp per in-plane chunk c: its 2-D integer box (lo.a, lo.b, hi.a,
 // hi.b) and the plane's 8 arg-extremes (+-a, +-b, +-(a+b), +-(a-b) in the mm
@@ -96,9 +96,9 @@ __global__ void plane_boxes(const int2* __restrict__ sorted,
     // last one, as pass 1 does) and their union.
     int la[2] = {INT_MAX, INT_MAX}, lb[2] = {INT_MAX, INT_MAX};
     int ha[2] = {INT_MIN, INT_MIN}, hb[2] = {INT_MIN, INT_MIN};
-    unsigned long long ext[8];
+    unsigned int ek[8], ei[8];  // per lane: best order key and its entry, per extreme
 #pragma unroll
-    for (int d = 0; d < 8; d++) ext[d] = 0ull;
+    for (int d = 0; d < 8; d++) { ek[d] = 0u; ei[d] = 0u; }
 #pragma unroll
     for (int t = 0; t < kPC / 32; t++) {
       const unsigned int e = min(e0 + t * 32 + lane, e1 - 1);
@@ -110,9 +110,9 @@ __global__ void plane_boxes(const int2* __restrict__ sorted,
       const float pr[4] = {a, b, a + b, a - b};
 #pragma unroll
       for (int d = 0; d < 4; d++) {
-        const unsigned long long hi = pack_pext(pr[d], e), lo = pack_pext(-pr[d], e);
-        ext[2 * d] = hi > ext[2 * d] ? hi : ext[2 * d];
-        ext[2 * d + 1] = lo > ext[2 * d + 1] ? lo : ext[2 * d + 1];
+        const unsigned int hi = order_key32(pr[d]), lo = order_key32(-pr[d]);
+        if (hi > ek[2 * d]) { ek[2 * d] = hi; ei[2 * d] = e; }
+        if (lo > ek[2 * d + 1]) { ek[2 * d + 1] = lo; ei[2 * d + 1] = e; }
       }
     }
 #pragma unroll
@@ -126,15 +126,14 @@ __global__ void plane_boxes(const int2* __restrict__ sorted,
       hpboxes[2 * c] = make_int4(la[0], lb[0], ha[0], hb[0]);
       hpboxes[2 * c + 1] = make_int4(la[1], lb[1], ha[1], hb[1]);
     }
+    // warp arg-max per extreme: hardware u32 max-reduce, the owner by ballot
 #pragma unroll
     for (int d = 0; d < 8; d++) {
-      unsigned long long x = ext[d];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const unsigned long long t = __shfl_xor_sync(0xffffffffu, x, o);
-        x = t > x ? t : x;
-      }
-      if (lane == 0 && x) atomicMax(&pext[(long long)p * 8 + d], x);
+      const unsigned int m = __reduce_max_sync(0xffffffffu, ek[d]);
+      const int owner = __ffs(__ballot_sync(0xffffffffu, ek[d] == m)) - 1;
+      const unsigned int idx = __shfl_sync(0xffffffffu, ei[d], owner);
+      if (lane == 0 && m)
+        atomicMax(&pext[(long long)p * 8 + d], ((unsigned long long)m << 32) | idx);
     }
   }
 }
