@@ -257,9 +257,18 @@ __global__ void scatter_all(const int4* __restrict__ keys, long long cap,
 
 // 13 directions; projections in the (un-centred) mm frame.  Arg-extremes are
 // reduced as packed (order-preserving value bits, vertex index).
-__constant__ int c_dir[kNDir][3] = {{1, 0, 0},  {0, 1, 0},  {0, 0, 1},  {1, 1, 0},  {1, -1, 0},
-                                    {1, 0, 1},  {1, 0, -1}, {0, 1, 1},  {0, 1, -1}, {1, 1, 1},
-                                    {1, 1, -1}, {1, -1, 1}, {-1, 1, 1}};
+// The components are -1 / 0 / 1 and the direction loop is unrolled, so every
+// projection compiles to at most two adds.
+__device__ __forceinline__ float dir_proj(int d, float x, float y, float z) {
+  constexpr int kDir[kNDir][3] = {{1, 0, 0},  {0, 1, 0},  {0, 0, 1},  {1, 1, 0},  {1, -1, 0},
+                                  {1, 0, 1},  {1, 0, -1}, {0, 1, 1},  {0, 1, -1}, {1, 1, 1},
+                                  {1, 1, -1}, {1, -1, 1}, {-1, 1, 1}};
+  float p = 0.f;
+  if (kDir[d][0]) p += kDir[d][0] > 0 ? x : -x;
+  if (kDir[d][1]) p += kDir[d][1] > 0 ? y : -y;
+  if (kDir[d][2]) p += kDir[d][2] > 0 ? z : -z;
+  return p;
+}
 
 __device__ __forceinline__ unsigned int order_key(float v) {  // order-preserving, never 0 for finite v
   const unsigned int b = __float_as_uint(v);
@@ -326,17 +335,20 @@ __global__ void __launch_bounds__(256) boxes_extremes(const int4* __restrict__ k
       atomicMin(slo, lx); atomicMin(slo + 1, ly); atomicMin(slo + 2, lz);
       atomicMax(shi, hx); atomicMax(shi + 1, hy); atomicMax(shi + 2, hz);
     }
+#pragma unroll
     for (int d = 0; d < kNDir; d++) {
-      // Per lane: best order-preserving key (and its vertex) of +p and -p;
-      // warp: hardware u32 max-reduce, the owning lane found by ballot.
-      unsigned int khi = 0u, klo = 0u, ihi = 0u, ilo = 0u;
+      // Per lane: largest and smallest projection (and their vertices);
+      // warp: hardware u32 max-reduce of order-preserving keys, the owning lane
+      // found by ballot.
+      float phi = -3.0e38f, plo = 3.0e38f;
+      unsigned int ihi = 0u, ilo = 0u;
 #pragma unroll
       for (int t = 0; t < kPerLane; t++) {
-        const float p = c_dir[d][0] * px[t] + c_dir[d][1] * py[t] + c_dir[d][2] * pz[t];
-        const unsigned int a = order_key(p), b = order_key(-p);
-        if (a > khi) { khi = a; ihi = idx[t]; }
-        if (b > klo) { klo = b; ilo = idx[t]; }
+        const float p = dir_proj(d, px[t], py[t], pz[t]);
+        if (p > phi) { phi = p; ihi = idx[t]; }
+        if (p < plo) { plo = p; ilo = idx[t]; }
       }
+      const unsigned int khi = order_key(phi), klo = order_key(-plo);
       const unsigned int mhi = __reduce_max_sync(0xffffffffu, khi);
       const unsigned int mlo = __reduce_max_sync(0xffffffffu, klo);
       const int shi = __ffs(__ballot_sync(0xffffffffu, khi == mhi)) - 1;
