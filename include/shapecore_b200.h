@@ -162,6 +162,9 @@ int sc_last_diagnostics(int device, int64_t* out, int n);
  * "graphs" (1) = replay each ROI pipeline as a cached CUDA graph; "slots" (16)
  * = pipeline slots (stream + scratch) the batch entries keep in flight;
  * "host_crop" (1) = host-mask entries copy only the occupied z/y slab;
+ * "host_pack" (-1) = bit-pack the occupied slab on the host and copy only
+ * its bits into the device bit volume (1 always, 0 never, -1 when the raw
+ * slab would keep PCIe busier than the host scan took);
  * "host_split" (-1) = % of leading slices sent to the device whole while the
  * host scans the rest (-1: balanced from the measured host-scan and PCIe
  * rates and the previous ROI's slab fraction; 0: off);

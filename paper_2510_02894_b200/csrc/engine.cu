@@ -113,6 +113,7 @@ std::atomic<int> g_opt_pack_bps{0};  // pack blocks per SM (0 = occupancy limit)
 std::atomic<int> g_opt_pack_mode{0};  // bit 0: one step per pack block; bit 1: low-priority pack;
                                       // bit 2 (debug): no pack, reuse the slot's bit volume
 std::atomic<bool> g_opt_crop{true};
+std::atomic<int> g_opt_host_pack{-1};  // host_pack: bit-pack the slab on the host (1 / 0 / -1 adaptive)
 std::atomic<int> g_opt_split{-1};  // host_split: % of leading slices sent unscanned (-1 adaptive, 0 off)  // host entries: copy only the occupied z/y slab (host_crop.h)
 std::atomic<int> g_opt_host_threads{(int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()))};
 std::atomic<unsigned long long> g_launches{0};
@@ -252,10 +253,14 @@ struct Ctx {
   DevBuf<int4> plane_hboxes;  // boxes of the two 64-entry halves of every in-plane chunk
   DevBuf<int2> plane_sorted;
   DevBuf<uint8_t> mask_stage, raw_stage;
-  double last_scan_ms = 0.0;      // host slab scan of the last host-mask ROI
+  double last_scan_ms = 0.0;      // host time (scan, + pack) of the last host-mask ROI
+  double last_pure_scan_ms = 0.0; // its slab scan alone
   long long last_h2d_bytes = 0;   // bytes that crossed PCIe for it
   long long last_scan_bytes = 0;  // bytes the host scan read for it
   long long last_slab_bytes = 0;  // bytes of its occupied slab
+  bool prepacked = false;         // this ROI's bit volume came packed from the host
+  uint32_t* h_bits = nullptr;     // pinned staging of a host-packed bit volume
+  size_t h_bits_cap = 0;          // words
   bool last_split = false;        // it used the split read (split_slices)
   DevBuf<double> cloud;
   DevBuf<unsigned long long> cloud_out;
@@ -276,6 +281,7 @@ struct Ctx {
     bool sparse;        // option "sparse_bits"
     bool fork;          // option "fork"
     bool zc;            // option "zero_copy"
+    bool prepacked;     // bit volume packed on the host (no pack kernel)
     unsigned long long gen;
     cudaGraphExec_t exec;
     unsigned long long launches;
@@ -545,7 +551,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   const long long cap = (long long)c->keys.cap, dcap = c->dcap_sz;
   // (the pack marks nonzero segments of a cleared map; the no-pack debug mode
   // keeps the previous map)
-  const bool clear_map = g_opt_sparse.load() && !(g_opt_pack_mode.load() & 4);
+  const bool clear_map = g_opt_sparse.load() && !(g_opt_pack_mode.load() & 4) && !c->prepacked;
   const bool zc = zero_copy_records(c);
   init_stats<<<clear_map ? 8 : 1, 256, 0, s>>>(c->d_stats, c->segmap.p,
                                                clear_map ? (long long)c->segmap.cap : 0LL,
@@ -553,7 +559,13 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[0], s));  // kev0..kev1 = the HBM pass alone
-  if (fast && g_opt_fbox.load()) {
+  if (c->prepacked) {  // the host already wrote the bit volume: bbox pass only
+    CK(record(c, c->kev[1], s));
+    CK(launch_k(c, s, lgrid(c, 4), 256, bits_bbox, rp, reinterpret_cast<const uint4*>(c->bits.p),
+                c->d_stats, c->segmap.p));
+    CKL(1);
+    if (++nk >= lim) return SC_OK;
+  } else if (fast && g_opt_fbox.load()) {
     pack_bits_v16<4, true><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(rp, c->bits.p,
                                                                               c->d_stats,
                                                                               c->segmap.p);
@@ -786,7 +798,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   h.W = (int)((nx + 31) / 32);
   h.n_words = (long long)h.W * ny * nz;
   h.n_chunks = nx * ny * nz / 16;
-  h.sparse = g_opt_sparse.load() ? 1 : 0;
+  h.sparse = (g_opt_sparse.load() && !c->prepacked) ? 1 : 0;
   h.f.cx2 = h.f.cy2 = h.f.cz2 = 0;  // set on the device from the bbox
   h.f.hx = (float)(0.5 * sp[0]);
   h.f.hy = (float)(0.5 * sp[1]);
@@ -816,7 +828,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
         g.grid_div == g_opt_grid_div.load() &&
         g.events == c->events_on && g.ev_full == c->ev_full && g.pdl == g_opt_pdl.load() &&
         g.sparse == g_opt_sparse.load() && g.fork == g_opt_fork.load() &&
-        g.zc == g_opt_zc.load() &&
+        g.zc == g_opt_zc.load() && g.prepacked == c->prepacked &&
         g.gen == c->gen) {
       CK(cudaGraphLaunch(g.exec, s));
       if (hp) g_hprof.launch += wall_ms() - t0;
@@ -847,7 +859,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
                     g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load() + 4096 * g_opt_pack_tma.load(),
                     g_opt_grid_div.load(),
                     c->events_on, c->ev_full, g_opt_pdl.load(), g_opt_sparse.load(),
-                    g_opt_fork.load(), g_opt_zc.load(), c->gen, exec, launches};
+                    g_opt_fork.load(), g_opt_zc.load(), c->prepacked, c->gen, exec, launches};
   c->graphs.push_back(g);
   CK(cudaGraphLaunch(exec, s));
   g_launches.fetch_add(launches, std::memory_order_relaxed);
@@ -987,6 +999,7 @@ double wall_ms() {
 struct HostRates {
   std::mutex mu;
   double scan_bpms = 0.0, h2d_bpms = 0.0, slab_frac = 1.0;
+  bool packed = false;  // the last host-mask ROI was packed on the host
 };
 HostRates& host_rates(int device) {
   static HostRates r[64];
@@ -997,8 +1010,9 @@ HostRates& host_rates(int device) {
 void note_host_rates(const Ctx* c, int64_t total_bytes, double h2d_ms) {
   HostRates& r = host_rates(c->device);
   std::lock_guard<std::mutex> lk(r.mu);
-  if (c->last_scan_ms > 0.0 && c->last_scan_bytes > 0)
-    r.scan_bpms = (double)c->last_scan_bytes / c->last_scan_ms;
+  if (c->last_pure_scan_ms > 0.0 && c->last_scan_bytes > 0)
+    r.scan_bpms = (double)c->last_scan_bytes / c->last_pure_scan_ms;
+  r.packed = c->prepacked;
   if (!c->last_split && h2d_ms > 0.0 && c->last_h2d_bytes > (1 << 20))
     r.h2d_bpms = (double)c->last_h2d_bytes / h2d_ms;
   if (total_bytes > 0) r.slab_frac = (double)c->last_slab_bytes / (double)total_bytes;
@@ -1018,7 +1032,8 @@ int64_t split_slices(int device, int64_t nz) {
   } else {
     HostRates& r = host_rates(device);
     std::lock_guard<std::mutex> lk(r.mu);
-    if (r.scan_bpms <= 0.0 || r.h2d_bpms <= 0.0) return 0;
+    // (a slab big enough to be packed on the host makes the split pointless)
+    if (r.scan_bpms <= 0.0 || r.h2d_bpms <= 0.0 || r.packed) return 0;
     const double k = r.h2d_bpms / r.scan_bpms;
     f = (k - r.slab_frac) / (1.0 + k);
   }
@@ -1026,14 +1041,27 @@ int64_t split_slices(int device, int64_t nz) {
   return std::min<int64_t>(nz - 1, (int64_t)(f * (double)nz));
 }
 
+// Pack the occupied slab on the host (option host_pack: 1 always, 0 never, -1
+// when the raw slab would keep PCIe busier than the host scan took, i.e. the
+// link, not the host, would bound the ROI -- C3-like ROIs with large slabs).
+bool pack_on_host(const Ctx* c, double slab_bytes, double scan_ms) {
+  const int mode = g_opt_host_pack.load();
+  if (mode >= 0) return mode == 1;
+  HostRates& r = host_rates(c->device);
+  std::lock_guard<std::mutex> lk(r.mu);
+  const double pcie_bpms = r.h2d_bpms > 0.0 ? r.h2d_bpms : 50e6;  // bytes per ms
+  return slab_bytes / pcie_bpms > scan_ms;
+}
+
 int stage_host_mask(Ctx* c, const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz,
                     cudaStream_t s, int64_t* cy, int64_t* cz, int org[3]) {
   org[0] = org[1] = org[2] = 0;
-  c->last_scan_ms = 0.0;
+  c->last_scan_ms = c->last_pure_scan_ms = 0.0;
   *cy = ny;
   *cz = nz;
   const uint8_t* src = mask;
   const size_t S = (size_t)nx * ny;  // bytes per slice
+  c->prepacked = false;
   const int64_t a = g_opt_crop.load() ? split_slices(c->device, nz) : 0;
   if (a > 0) {
     // Split read: slices [0, a) cross PCIe whole while the host scans [a, nz)
@@ -1043,7 +1071,7 @@ int stage_host_mask(Ctx* c, const uint8_t* mask, int64_t nx, int64_t ny, int64_t
     CK(cudaMemcpyAsync(c->mask_stage.p, mask, a * S, cudaMemcpyHostToDevice, s));
     const double t0 = wall_ms();
     const Slab sl = occupied_slab(mask + a * S, nx, ny, nz - a, g_opt_host_threads.load());
-    c->last_scan_ms = wall_ms() - t0;
+    c->last_scan_ms = c->last_pure_scan_ms = wall_ms() - t0;
     size_t bytes = a * S;
     int64_t Z1 = a - 1;
     if (!sl.empty) {
@@ -1068,8 +1096,9 @@ int stage_host_mask(Ctx* c, const uint8_t* mask, int64_t nx, int64_t ny, int64_t
   c->last_split = false;
   if (g_opt_crop.load()) {
     const double t0 = wall_ms();
-    const Slab sl = occupied_slab(mask, nx, ny, nz, g_opt_host_threads.load());
-    c->last_scan_ms = wall_ms() - t0;
+    const int th = g_opt_host_threads.load();
+    const Slab sl = occupied_slab(mask, nx, ny, nz, th);
+    c->last_scan_ms = c->last_pure_scan_ms = wall_ms() - t0;
     c->last_scan_bytes = sl.bytes_read;
     if (sl.empty) {
       set_err("mask has no occupied voxels");
@@ -1080,6 +1109,38 @@ int stage_host_mask(Ctx* c, const uint8_t* mask, int64_t nx, int64_t ny, int64_t
     org[1] = (int)sl.y0;
     org[2] = (int)sl.z0;
     src = mask + (sl.z0 * ny + sl.y0) * nx;
+    if (pack_on_host(c, (double)nx * *cy * *cz, c->last_scan_ms)) {
+      // Host pack: the same host threads bit-pack the slab's rows into the
+      // device bit-volume layout, and only the bits (1/8 of the slab) cross
+      // PCIe, straight into the slot's bit volume; the ROI's graph then starts
+      // at the bbox pass (no device pack).
+      const double t1 = wall_ms();
+      const size_t W = (size_t)((nx + 31) / 32), words = W * *cy * *cz;
+      if (words > c->h_bits_cap) {
+        if (c->h_bits) cudaFreeHost(c->h_bits);
+        c->h_bits = nullptr;
+        c->h_bits_cap = 0;
+        CK(cudaMallocHost(&c->h_bits, sizeof(uint32_t) * (words + words / 4 + 1024)));
+        c->h_bits_cap = words + words / 4 + 1024;
+      }
+      pack_slab(mask, nx, ny, sl.z0, sl.z1, sl.y0, sl.y1, c->h_bits, th);
+      c->last_scan_ms += wall_ms() - t1;
+      const unsigned long long fp0 = c->fingerprint();
+      CK(c->bits.ensure(words));
+      CK(c->segmap.ensure(c->bits.cap / 512 + 1));
+      if (c->fingerprint() != fp0) {  // scratch moved: cached ROI graphs are stale
+        c->gen++;
+        c->drop_graphs();
+      }
+      CK(cudaEventRecord(c->ev[0], s));
+      CK(cudaMemcpyAsync(c->bits.p, c->h_bits, sizeof(uint32_t) * words,
+                         cudaMemcpyHostToDevice, s));
+      CK(cudaEventRecord(c->ev[1], s));
+      c->last_h2d_bytes = (long long)(sizeof(uint32_t) * words);
+      c->last_slab_bytes = (long long)((size_t)nx * *cy * *cz);
+      c->prepacked = true;
+      return SC_OK;
+    }
   }
   const size_t width = (size_t)nx * *cy;
   c->last_slab_bytes = (long long)(width * *cz);
@@ -1197,6 +1258,8 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
       rc = stage_host_mask(c, masks[i], nx, ny, nz, s, &cy, &cz, org);
       if (rc) { note(rc); continue; }
       dm = c->mask_stage.p;
+    } else {
+      c->prepacked = false;
     }
     pend[k] = Pending{};
     const double ts = host_prof_on() ? wall_ms() : 0.0;
@@ -1391,6 +1454,7 @@ int sc_calculate_coefficients_shard(const uint8_t* d_mask, int64_t nx, int64_t n
   std::lock_guard<std::mutex> lk(c->mu);
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
   std::memset(out, 0, sizeof *out);
+  c->prepacked = false;
   rc = run_roi(c, d_mask, nx, ny, nz, spacing, s, shard, nshards, d_sq4, out);
   out->total_ms = wall_ms() - t0;
   return rc;
@@ -1456,6 +1520,7 @@ int sc_calculate_coefficients_raw(const void* data, int dtype, const int64_t sha
   }
   CKL(1);
   CK(cudaEventRecord(c->ev[1], s));
+  c->prepacked = false;
   rc = run_roi(c, c->mask_stage.p, nx, ny, nz, spacing, s, 0, 1, nullptr, out);
   out->h2d_ms = ev_ms(c->ev[0], c->ev[1]);
   out->h2d_bytes = (int64_t)raw_bytes;
@@ -1585,6 +1650,7 @@ int sc_mesh_vertices(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, in
   {
     const double unit[3] = {1.0, 1.0, 1.0};
     sc_coeffs tmp;
+    c->prepacked = false;
     if ((rc = run_roi(c, c->mask_stage.p, nx, ny, nz, unit, s, 0, 1, nullptr, &tmp))) return rc;
   }
   const long long V = (long long)c->h_stats->n_vert;
@@ -1658,6 +1724,7 @@ int sc_set_option(const char* name, int value) {
   else if (std::strcmp(name, "wcap") == 0) g_opt_wcap = std::max(1, value);
   else if (std::strcmp(name, "fused_bbox") == 0) g_opt_fbox = value != 0;
   else if (std::strcmp(name, "host_crop") == 0) g_opt_crop = value != 0;
+  else if (std::strcmp(name, "host_pack") == 0) g_opt_host_pack = std::max(-1, std::min(1, value));
   else if (std::strcmp(name, "host_split") == 0) g_opt_split = std::max(-1, std::min(90, value));
   else if (std::strcmp(name, "pack_mode") == 0) g_opt_pack_mode = value & 7;
   else if (std::strcmp(name, "pack_bps") == 0) g_opt_pack_bps = std::max(0, value);

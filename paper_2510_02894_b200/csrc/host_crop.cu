@@ -118,7 +118,55 @@ inline bool row_any_u64(const uint8_t* p, int64_t n) {
   return acc != 0;
 }
 
+// One row of nx bytes -> W words.
+__attribute__((target("avx2"))) void pack_row_avx2(const uint8_t* p, int64_t nx, uint32_t* out) {
+  const __m256i zero = _mm256_setzero_si256();
+  int64_t i = 0, w = 0;
+  for (; i + 32 <= nx; i += 32, w++) {
+    const __m256i v = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(p + i));
+    out[w] = ~(uint32_t)_mm256_movemask_epi8(_mm256_cmpeq_epi8(v, zero));
+  }
+  if (i < nx) {
+    uint32_t word = 0;
+    for (int64_t b = 0; i + b < nx; b++) word |= (uint32_t)(p[i + b] != 0) << b;
+    out[w] = word;
+  }
+}
+
+void pack_row_scalar(const uint8_t* p, int64_t nx, uint32_t* out) {
+  for (int64_t w = 0; 32 * w < nx; w++) {
+    uint32_t word = 0;
+    for (int64_t b = 0; b < 32 && 32 * w + b < nx; b++) word |= (uint32_t)(p[32 * w + b] != 0) << b;
+    out[w] = word;
+  }
+}
+
 }  // namespace
+
+void pack_slab(const uint8_t* mask, int64_t nx, int64_t ny, int64_t z0, int64_t z1, int64_t y0,
+               int64_t y1, uint32_t* out, int threads) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  const int64_t W = (nx + 31) / 32, rows = y1 - y0 + 1, nzs = z1 - z0 + 1;
+  if (nzs <= 0 || rows <= 0) return;
+  // tasks of ~256 KB of mask rows (enough of them for every thread)
+  const int64_t per = std::max<int64_t>(1, (int64_t(1) << 18) / std::max<int64_t>(1, nx * rows));
+  const int64_t ntask = (nzs + per - 1) / per;
+  auto job = [&](int64_t t) {
+    for (int64_t zz = t * per; zz < std::min(nzs, (t + 1) * per); zz++)
+      for (int64_t r = 0; r < rows; r++) {
+        const uint8_t* src = mask + ((z0 + zz) * ny + y0 + r) * nx;
+        uint32_t* dst = out + (zz * rows + r) * W;
+        if (avx2) pack_row_avx2(src, nx, dst);
+        else pack_row_scalar(src, nx, dst);
+      }
+  };
+  const int nt = std::max(1, threads);
+  if (nt == 1 || ntask == 1) {
+    for (int64_t t = 0; t < ntask; t++) job(t);
+  } else {
+    pool().run(ntask, nt, job);
+  }
+}
 
 Slab occupied_slab(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, int threads) {
   struct Part {

@@ -25,4 +25,10 @@ struct Slab {
 // `threads` host threads (a process-wide pool; concurrent callers share it).
 Slab occupied_slab(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, int threads);
 
+// Bit-pack rows [y0, y1] of slices [z0, z1] into the device bit-volume layout
+// of that slab: uint32 words [z - z0][y - y0][w], W = ceil(nx / 32) words per
+// row, bit b of word w = voxel 32 w + b nonzero (bits past nx are 0).
+void pack_slab(const uint8_t* mask, int64_t nx, int64_t ny, int64_t z0, int64_t z1, int64_t y0,
+               int64_t y1, uint32_t* out, int threads);
+
 }  // namespace sc

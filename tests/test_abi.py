@@ -149,7 +149,7 @@ def test_occupied_slab_host_scan(native):
         want = (zs.min(), zs.max(), ys.min(), ys.max())
         for t in (1, 2, 7, 0):
             assert native.occupied_slab(arr, threads=t) == tuple(int(v) for v in want)
-    big = np.zeros((600, 64, 512), dtype=np.uint8)
+    big = np.zeros((600, 64, 512), dtype=np.uint8)  # noqa: E501
     big[300, 40, 511] = 1
     big[17, 3, 0] = 9
     assert native.occupied_slab(big, threads=8) == (17, 300, 3, 40)

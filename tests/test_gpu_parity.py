@@ -475,10 +475,19 @@ def test_host_crop_is_exact(sc, oracle_mod, cuda_device):
                   (0.37, 0.61, 2.9)))
     try:
         for arr, sp in cases:
+            z0, z1, y0, y1 = _native.occupied_slab(arr)
+            # host pack: the slab's bits cross PCIe into the bit volume
+            _native.set_option("host_pack", 1)
+            _native.set_option("host_split", 0)
+            packed = sc.calculate_coefficients(arr, sp, device=cuda_device)
+            assert packed.h2d_bytes == 4 * ((arr.shape[2] + 31) // 32) * (z1 - z0 + 1) * (y1 - y0 + 1)
+            _native.set_option("host_pack", 0)
             _native.set_option("host_split", 0)
             cropped = sc.calculate_coefficients(arr, sp, device=cuda_device)
-            z0, z1, y0, y1 = _native.occupied_slab(arr)
             assert cropped.h2d_bytes == (z1 - z0 + 1) * (y1 - y0 + 1) * arr.shape[2]
+            assert packed.to_dict() == cropped.to_dict()
+            assert (packed.triangle_count, packed.active_cubes) == \
+                   (cropped.triangle_count, cropped.active_cubes)
             # split read: leading slices cross PCIe unscanned, the rest is cropped
             for pct in (30, 60, 90):
                 _native.set_option("host_split", pct)
@@ -487,6 +496,7 @@ def test_host_crop_is_exact(sc, oracle_mod, cuda_device):
                 assert (split.triangle_count, split.active_cubes) == \
                        (cropped.triangle_count, cropped.active_cubes)
             _native.set_option("host_split", -1)
+            _native.set_option("host_pack", -1)
             dev = sc.calculate_coefficients_device(torch.from_numpy(arr).cuda(), sp)
             _native.set_option("host_crop", 0)
             full = sc.calculate_coefficients(arr, sp, device=cuda_device)
@@ -503,12 +513,14 @@ def test_host_crop_is_exact(sc, oracle_mod, cuda_device):
             for k in ("MeshVolume", "SurfaceArea"):
                 assert rel_err(rec[k], want[k]) <= 1e-12
         # an all-background mask is an EmptyRoi whichever part the host scanned
-        for pct in (0, 50):
+        for pack, pct in ((1, 0), (-1, -1), (0, 0), (0, 50)):
+            _native.set_option("host_pack", pack)
             _native.set_option("host_split", pct)
             with pytest.raises(sc.EmptyRoi):
                 sc.calculate_coefficients(np.zeros((40, 30, 64), np.uint8), (1, 1, 1))
-        # the pipelined host batch crops (and splits) too
-        for pct in (-1, 50):
+        # the pipelined host batch packs / crops / splits too
+        for pack, pct in ((1, 0), (-1, -1), (0, -1), (0, 50)):
+            _native.set_option("host_pack", pack)
             _native.set_option("host_split", pct)
             outs = sc.calculate_coefficients_batch([a for a, _ in cases] * 3,
                                                    [s for _, s in cases] * 3, device=cuda_device)
@@ -517,6 +529,7 @@ def test_host_crop_is_exact(sc, oracle_mod, cuda_device):
     finally:
         _native.set_option("host_crop", 1)
         _native.set_option("host_split", -1)
+        _native.set_option("host_pack", -1)
 
 
 def _blob_mask(seed):

@@ -77,11 +77,21 @@ def main():
                                                                    [sp for _, sp in cases]),
                                    wants)):
         check(o, w, ("host batch", i))
+    from paper_2510_02894_b200 import _native
+    _native.set_option("host_pack", 1)  # bit volume packed on the host
+    _native.set_option("host_split", 0)
+    try:
+        for i, (o, w) in enumerate(zip(sc.calculate_coefficients_batch(
+                [a for a, _ in cases], [sp for _, sp in cases]), wants)):
+            check(o, w, ("host-packed batch", i))
+    finally:
+        _native.set_option("host_pack", -1)
+        _native.set_option("host_split", -1)
     ds = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a, _ in cases]
     for i, (o, w) in enumerate(zip(sc.calculate_coefficients_device_batch(
             ds, [sp for _, sp in cases]), wants)):
         check(o, w, ("device batch", i))
-    print(f"stress parity ok: {n} masks x 3 entry points (seed {seed0})")
+    print(f"stress parity ok: {n} masks x 4 entry paths (seed {seed0})")
 
 
 if __name__ == "__main__":
