@@ -184,7 +184,12 @@ int sc_last_diagnostics(int device, int64_t* out, int n);
  * pack (0 = the 128-bit-load pack);
  * "sparse_bits" (1) = the pack writes only nonzero 16-word segments of the
  * bit volume (segment map); "pdl" (0) = programmatic dependent launch of the
- * per-ROI kernels in batch graphs.
+ * per-ROI kernels in batch graphs; "fork" (1) = the planar filter chain runs
+ * on a second stream beside the 3-D one; "dcap" / "wcap" = initial vertex /
+ * 3-D work-list capacities (an overflow re-runs the ROI with exact sizes).
+ * Measurement / experiment switches: "fused_bbox" (0), "pack_mode" (0),
+ * "pack_bps" (0), "debug_stages" (off; enqueue only the first N kernels,
+ * results invalid).
  * Results are identical either way; 0 on success, SC_ERR_INPUT otherwise. */
 int sc_set_option(const char* name, int value);
 uint64_t sc_launch_count(void);
