@@ -250,7 +250,11 @@ __device__ __forceinline__ void pass1_planar(const int2* __restrict__ sorted,
   const long long w0 = 0, w1 = (long long)st->n_pwork;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long gwarps = (long long)gridDim.x * kPlaneWarps;
-  const long long gw = (long long)blockIdx.x * kPlaneWarps + warp;
+  // Rotated by the 3-D list's warp count: when both lists are short (fewer
+  // units than warps), the planar units go to the warps the 3-D list left
+  // idle instead of queueing behind 3-D units on the same warps.
+  const long long busy3 = min((long long)st->n_work, gwarps);
+  const long long gw = ((long long)blockIdx.x * kPlaneWarps + warp + gwarps - busy3) % gwarps;
   const long long per = (w1 - w0 + gwarps - 1) / gwarps;
   const long long wb = w0 + gw * per, we = min(w1, wb + per);
   float run0 = 0.f, run1 = 0.f, run2 = 0.f;  // per-family maxima
