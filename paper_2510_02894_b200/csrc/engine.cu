@@ -108,7 +108,12 @@ std::atomic<int> g_opt_pack_tma{0};  // TMA bulk-copy pack, CTAs per SM (0 = 128
 std::atomic<bool> g_opt_fork{true};
 std::atomic<bool> g_opt_zc{true};  // option "zero_copy": RoiParams / Stats via mapped host memory
 std::atomic<int> g_opt_stage_times{0};  // single-call graph events: 0 none (timer stamps), 1 mesh/diam, 2 all  // planar chain on a second stream (option "fork")
-std::atomic<int> g_opt_grid_div{2};  // divisor of the latency-bound kernel grids (2: best measured batch rate)
+// Divisor of the latency-bound per-ROI kernels' grids: batches keep many ROIs
+// in flight and run faster with few resident blocks per ROI (measured C2 div
+// 2 / 4: 50.4 / 45.8 us per ROI); a single call wants the whole GPU for its
+// latency chain (C3 call: div 1 far faster than 4).
+std::atomic<int> g_opt_grid_div{4};         // batch entries ("grid_div")
+std::atomic<int> g_opt_grid_div_single{1};  // single calls ("grid_div_single")
 std::atomic<int> g_opt_pack_bps{0};  // pack blocks per SM (0 = occupancy limit)  // divisor of the latency-bound kernels' grids
 std::atomic<int> g_opt_pack_mode{0};  // bit 0: one step per pack block; bit 1: low-priority pack;
                                       // bit 2 (debug): no pack, reuse the slot's bit volume
@@ -290,6 +295,7 @@ struct Ctx {
   unsigned long long gen = 0;  // bumped whenever a scratch buffer moves
   bool capturing = false;      // inside a stream capture of launch_roi
   bool events_on = true;       // record stage events (single calls; batches: option)
+  int grid_div = 1;            // grid divisor of this ROI's latency-bound kernels
   bool ev_full = true;         // every stage boundary (else mesh / diameters only)
 
   unsigned long long fingerprint() const {
@@ -504,7 +510,7 @@ int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, lo
 // option "grid_div" (fewer blocks = less block-scheduling and prologue work
 // per ROI when several ROIs share the GPU; every kernel is grid-stride).
 int lgrid(const Ctx* c, int k) {
-  return std::max(1, c->sms * k / std::max(1, g_opt_grid_div.load()));
+  return std::max(1, c->sms * k / std::max(1, c->grid_div));
 }
 
 // Zero-copy per-ROI records (option "zero_copy", default on): init_stats reads
@@ -825,7 +831,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
         g.d_sq4 == d_sq4 && g.cap == cap && g.dcap == dcap && g.prune == prune &&
         g.packed == packed && g.fbox == fbox && g.stages == g_opt_stages.load() &&
         g.packmode == g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load() + 4096 * g_opt_pack_tma.load() &&
-        g.grid_div == g_opt_grid_div.load() &&
+        g.grid_div == c->grid_div &&
         g.events == c->events_on && g.ev_full == c->ev_full && g.pdl == g_opt_pdl.load() &&
         g.sparse == g_opt_sparse.load() && g.fork == g_opt_fork.load() &&
         g.zc == g_opt_zc.load() && g.prepacked == c->prepacked &&
@@ -857,7 +863,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   Ctx::GraphEntry g{fast, s, shard, nshards, d_sq4, cap, dcap, prune, packed, fbox,
                     g_opt_stages.load(),
                     g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load() + 4096 * g_opt_pack_tma.load(),
-                    g_opt_grid_div.load(),
+                    c->grid_div,
                     c->events_on, c->ev_full, g_opt_pdl.load(), g_opt_sparse.load(),
                     g_opt_fork.load(), g_opt_zc.load(), c->prepacked, c->gen, exec, launches};
   c->graphs.push_back(g);
@@ -976,6 +982,7 @@ int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, c
             const int org[3] = nullptr) {
   Pending p{};
   // single calls: mesh / diameters events (level 1), every stage (2) or none (0)
+  c->grid_div = g_opt_grid_div_single.load();
   c->events_on = g_opt_stage_times.load() > 0;
   c->ev_full = g_opt_stage_times.load() > 1;
   int rc = start_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, 0, &p, org);
@@ -1181,8 +1188,10 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
     Ctx** cs; int n;
     ~EventsMode() { for (int k = 0; k < n; k++) cs[k]->events_on = cs[k]->ev_full = true; }
   } events_mode{cs, nslots};
-  for (int k = 0; k < nslots; k++)
+  for (int k = 0; k < nslots; k++) {
     cs[k]->events_on = cs[k]->ev_full = g_opt_batch_times.load();
+    cs[k]->grid_div = g_opt_grid_div.load();
+  }
   CK(cudaSetDevice(device));
   if (user) {  // order the batch after prior work on the caller's stream
     CK(cudaEventRecord(cs[0]->ev[4], user));
@@ -1729,6 +1738,7 @@ int sc_set_option(const char* name, int value) {
   else if (std::strcmp(name, "pack_mode") == 0) g_opt_pack_mode = value & 7;
   else if (std::strcmp(name, "pack_bps") == 0) g_opt_pack_bps = std::max(0, value);
   else if (std::strcmp(name, "grid_div") == 0) g_opt_grid_div = std::max(1, value);
+  else if (std::strcmp(name, "grid_div_single") == 0) g_opt_grid_div_single = std::max(1, value);
   else if (std::strcmp(name, "pdl") == 0) g_opt_pdl = value != 0;
   else if (std::strcmp(name, "fork") == 0) g_opt_fork = value != 0;
   else if (std::strcmp(name, "zero_copy") == 0) g_opt_zc = value != 0;
