@@ -75,24 +75,46 @@ class Coefficients(ShapeFeatures):
     host_scan_ms: float = 0.0  # host scan that found the slab
 
 
+# Coefficients field <- sc_coeffs field (same names; ctypes already returns
+# Python int / float for c_int64 / c_double).
+_STRUCT_FIELDS = tuple(name for name, _ in _native.ScCoeffs._fields_)
+
+
+def _check_spacings(spacings, n: int) -> np.ndarray:
+    """Vectorised volume.py:94-101 check of n spacings -> flat float64 (3n)."""
+    try:
+        sp = np.asarray(spacings, dtype=np.float64)
+    except (TypeError, ValueError):
+        sp = None
+    if sp is None or sp.shape != (n, 3) or not (np.isfinite(sp).all() and (sp > 0).all()):
+        for s in spacings:  # the scalar check raises the reference's error
+            _check_spacing(s)
+        if len(spacings) != n:
+            raise ValueError(f"{len(spacings)} spacings for {n} masks")
+    return np.ascontiguousarray(sp, dtype=np.float64).reshape(-1)
+
+
+_STRUCT_DTYPE = np.dtype([(name, "<i8" if t is ctypes.c_int64 else "<f8")
+                          for name, t in _native.ScCoeffs._fields_])
+assert _STRUCT_DTYPE.itemsize == ctypes.sizeof(_native.ScCoeffs)
+
+
+def _record(values) -> Coefficients:
+    # Batches convert hundreds of records inside timed regions: fill the frozen
+    # dataclass's __dict__ directly (what its generated __init__ does, minus
+    # one object.__setattr__ call per field).
+    rec = object.__new__(Coefficients)
+    rec.__dict__.update(zip(_STRUCT_FIELDS, values))
+    return rec
+
+
 def _from_struct(c: _native.ScCoeffs) -> Coefficients:
-    return Coefficients(
-        mesh_volume=c.mesh_volume,
-        surface_area=c.surface_area,
-        max_3d_diameter=c.max_3d_diameter,
-        max_2d_diameter_xy=c.max_2d_diameter_xy,
-        max_2d_diameter_xz=c.max_2d_diameter_xz,
-        max_2d_diameter_yz=c.max_2d_diameter_yz,
-        vertex_count=int(c.vertex_count),
-        triangle_count=int(c.triangle_count),
-        active_cubes=int(c.active_cubes),
-        h2d_ms=c.h2d_ms,
-        mesh_ms=c.mesh_ms,
-        diameters_ms=c.diameters_ms,
-        total_ms=c.total_ms,
-        h2d_bytes=int(c.h2d_bytes),
-        host_scan_ms=c.host_scan_ms,
-    )
+    return _record(getattr(c, k) for k in _STRUCT_FIELDS)
+
+
+def _from_structs(outs) -> List[Coefficients]:
+    """An sc_coeffs array -> records (one numpy pass over the C array)."""
+    return [_record(row) for row in np.frombuffer(outs, dtype=_STRUCT_DTYPE).tolist()]
 
 
 def _as_mask(mask) -> Tuple[np.ndarray, Tuple[int, int, int]]:
@@ -174,7 +196,7 @@ def calculate_coefficients_batch(masks: Sequence, spacings: Sequence[Sequence[fl
         data, d = _as_mask(m)
         bufs.append(data)
         dims.extend(d)
-    sp = np.asarray([_check_spacing(s) for s in spacings], dtype=np.float64).reshape(-1)
+    sp = _check_spacings(spacings, len(bufs))
     n = len(bufs)
     ptrs = (ctypes.POINTER(ctypes.c_uint8) * n)(
         *[b.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)) for b in bufs])
@@ -184,7 +206,7 @@ def calculate_coefficients_batch(masks: Sequence, spacings: Sequence[Sequence[fl
         ptrs, dims_arr.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
         sp.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), n, int(device), outs)
     _native.raise_for(rc, "sc_calculate_coefficients_batch")
-    return [_from_struct(o) for o in outs]
+    return _from_structs(outs)
 
 
 def calculate_coefficients_device_batch(masks: Sequence, spacings: Sequence[Sequence[float]],
@@ -196,7 +218,7 @@ def calculate_coefficients_device_batch(masks: Sequence, spacings: Sequence[Sequ
     ptrs = (ctypes.c_void_p * n)(*[m.data_ptr() for m in masks])
     dims = np.asarray([(int(m.shape[2]), int(m.shape[1]), int(m.shape[0])) for m in masks],
                       dtype=np.int64).reshape(-1)
-    sp = np.asarray([_check_spacing(s) for s in spacings], dtype=np.float64).reshape(-1)
+    sp = _check_spacings(spacings, n)
     for m in masks:
         if not m.is_contiguous():
             raise ValueError("device masks must be contiguous")
@@ -206,7 +228,7 @@ def calculate_coefficients_device_batch(masks: Sequence, spacings: Sequence[Sequ
         ptrs, dims.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
         sp.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), n, ctypes.c_void_p(handle), outs)
     _native.raise_for(rc, "sc_calculate_coefficients_device_batch")
-    return [_from_struct(o) for o in outs]
+    return _from_structs(outs)
 
 
 def _as_coord_arrays(xs, ys, zs):
