@@ -1,12 +1,15 @@
 // Host orchestration and the C ABI (include/shapecore_b200.h).
 //
-// One ROI = init -> pack -> bbox -> mc_cells -> sort / boxes / filters (3-D and
-// planar) -> one fused pass-1 kernel -> one fused exact re-check -> D2H of the
-// accumulators, enqueued without host round trips.  Area, volume, triangle and active-cube counts are formed
-// on the host from exact integer histograms.  Per
-// device the library keeps one context: a stream, events, grow-only scratch
-// arenas and pinned result buffers, reused across calls (SURVEY.md 8b
-// "Ownership"); calls on one device are serialised by a mutex.
+// One ROI = init -> pack -> bbox -> mc_cells -> sort -> boxes / filters (3-D
+// and, on a second stream, planar) -> one fused pass-1 kernel -> one fused
+// exact re-check that publishes the accumulators to mapped host memory, all
+// one CUDA graph per pipeline slot with no host round trip (DESIGN.md section
+// 1).  Area, volume, triangle and active-cube counts are formed on the host
+// from exact integer histograms.  Per device the
+// library keeps up to 16 slots: streams, events, grow-only scratch arenas and
+// pinned records, reused across calls (SURVEY.md 8b "Ownership"); a slot is
+// used by one call at a time (mutex).  Host masks are scanned / cropped /
+// packed on the host first (host_crop.cu).
 #include <cuda_runtime.h>
 
 #include <atomic>

@@ -32,8 +32,9 @@ constexpr int kPC = kPlaneChunk;  // in-plane chunk edge (pair unit = chunk x ch
 constexpr int kPR = kPC / 32;     // 4 i entries per lane
 static_assert(kPC == kChunk, "the fused pass-1 kernel shares one smem chunk per warp");
 
-// Pass 1 (see header).  Work unit = one surviving chunk pair (I <= J, 256 x
-// 256 vertex pairs, listed by unit_filter); every WARP is an independent
+// Pass 1 (see header).  Work unit = one surviving chunk pair (I <= J, 128 x
+// 128 vertex pairs, listed by unit_filter / unit_expand with the mask of its
+// 64 x 64 sub-pairs to evaluate); every WARP is an independent
 // worker with its own shared-memory copy of the J chunk, so load balance is
 // per unit and no block barrier is involved.  Error of the dot form: in the
 // bbox-centred frame |p| <= D*sqrt(3)/2, so the absolute error is
