@@ -186,6 +186,7 @@ const CaseGeom& case_geom() {
       c.ntri[k] = nt;
       c.tabs.tn[k] = make_int4(t_sum, n_sum[0], n_sum[1], n_sum[2]);
     }
+    for (int idx = 0; idx < kNumCases; idx++) c.tabs.tn_raw[idx] = c.tabs.tn[case_of_idx(idx)];
     return c;
   }();
   return g;

@@ -365,16 +365,7 @@ __device__ __forceinline__ unsigned long long window(const uint32_t* __restrict_
   return (cur << 1) | (prev >> 31);
 }
 
-constexpr int kStage = 256;
-
-// Raw corner word of a cell (bits: A_i, A_i+1, B_i, B_i+1, C_i, C_i+1, D_i,
-// D_i+1 with A/B = rows (v, w)/(v+1, w), C/D = rows (v, w+1)/(v+1, w+1)) ->
-// reference case: occupancy in corner order 0..7 = (A_i, A_i+1, B_i+1, B_i,
-// C_i, C_i+1, D_i+1, D_i), complemented (bit set = background corner).
-__device__ __forceinline__ int case_of_idx(int idx) {
-  const int occ = (idx & 0x33) | ((idx >> 1) & 0x44) | ((idx << 1) & 0x88);
-  return (~occ) & 0xff;
-}  // staged vertices per warp and z step (denser steps emit directly)
+constexpr int kStage = 256;  // staged vertices per warp and z step (denser steps emit directly)
 
 // Words q and q - 1 of row (v, w); with a sparse bit volume, words of
 // unmarked segments read as 0 (the word and its map bit are loaded together).
@@ -419,7 +410,7 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
                                         int4* __restrict__ vkeys, long long cap,
                                         unsigned int* __restrict__ sort_counts,
                                         unsigned int* __restrict__ pbin_counts, const int* bb,
-                                        unsigned int* s_hist, const int4* s_tn,
+                                        unsigned int* s_hist, const int4* __restrict__ tn_raw,
                                         unsigned int* s_sup, int4 (*s_stage)[kStage]) {
   const int ny = (int)rp->ny, nz = (int)rp->nz, W = rp->W;
   const bool sparse = rp->sparse != 0;
@@ -501,11 +492,12 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
           const unsigned long long all = A & B & C & D, any = A | B | C | D;
           act = (uint32_t)(~(all & (all >> 1)) & (any | (any >> 1)));
         }
-        // Active cells.  The shared histogram and case table are indexed by
-        // the raw corner word idx = A[i..i+1] | B[i..i+1]<<2 | C[..]<<4 |
-        // D[..]<<6 (4 shift-and pairs); case_of_idx() maps it to the
-        // reference case (bit c set when corner c is background,
-        // mc_tables.py:10-12, mesh.py:103-128) at the table load and flush.
+        // Active cells.  The shared histogram and the case table (tn_raw,
+        // read through L1) are indexed by the raw corner word idx =
+        // A[i..i+1] | B[i..i+1]<<2 | C[..]<<4 | D[..]<<6 (4 shift-and pairs);
+        // case_of_idx() maps it to the reference case (bit c set when corner
+        // c is background, mc_tables.py:10-12, mesh.py:103-128) when the
+        // table is built and at the histogram flush.
         // The volume terms are summed in 32 bits per step, widened once.
         int s0 = 0, sx = 0, sy = 0, sz = 0;
         while (act) {
@@ -514,7 +506,7 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
           const uint32_t idx = (uint32_t)((A >> i) & 3) | ((uint32_t)((B >> i) & 3) << 2) |
                                ((uint32_t)((C >> i) & 3) << 4) | ((uint32_t)((D >> i) & 3) << 6);
           atomicAdd(&s_hist[idx], 1u);
-          const int4 tn = s_tn[idx];
+          const int4 tn = __ldg(tn_raw + idx);  // L1-resident 4 KB table
           s0 += tn.x;
           sx += (xbase + i) * tn.y;
           sy += tn.z;
@@ -607,7 +599,6 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
                                                 const uint32_t* __restrict__ segmap) {
   pdl_enter();
   __shared__ unsigned int s_hist[kNumCases];
-  __shared__ int4 s_tn[kNumCases];
   __shared__ unsigned int s_sup[kSortSupers];
   __shared__ int4 s_stage[256 / 32][kStage];  // per-warp vertex stage (blockDim = 256)
   int bb[6];
@@ -626,12 +617,11 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
   if ((long long)blockIdx.x * blockDim.x >= cols * ((zs + kz - 1) / kz)) return;
   for (int i = threadIdx.x; i < kNumCases; i += blockDim.x) {
     s_hist[i] = 0;
-    s_tn[i] = tabs->tn[case_of_idx(i)];
   }
   for (int i = threadIdx.x; i < kSortSupers; i += blockDim.x) s_sup[i] = 0;
   __syncthreads();
   long long volk = mc_body<4>(kz, rp, bits, segmap, st, vkeys, cap, sort_counts, pbin_counts, bb,
-                              s_hist, s_tn, s_sup, s_stage);
+                              s_hist, tabs->tn_raw, s_sup, s_stage);
   const int lane = threadIdx.x & 31;
   // Block flush: exact integer partials.
 #pragma unroll

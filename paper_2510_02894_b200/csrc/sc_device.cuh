@@ -59,8 +59,18 @@ constexpr unsigned int kIdxMask = (1u << kSubShift) - 1u;
 // Per-case integer tables for the exact volume path: for case k,
 // t = sum over its triangles of a.(b x c) and n = sum of (b-a) x (c-a), with
 // a, b, c the DOUBLED cell-local vertex coordinates (in {0,1,2}^3).
+// Raw corner word of a cell (bits: A_i, A_i+1, B_i, B_i+1, C_i, C_i+1, D_i,
+// D_i+1 with A/B = rows (v, w)/(v+1, w), C/D = rows (v, w+1)/(v+1, w+1)) ->
+// reference case: occupancy in corner order 0..7 = (A_i, A_i+1, B_i+1, B_i,
+// C_i, C_i+1, D_i+1, D_i), complemented (bit set = background corner).
+__host__ __device__ __forceinline__ int case_of_idx(int idx) {
+  const int occ = (idx & 0x33) | ((idx >> 1) & 0x44) | ((idx << 1) & 0x88);
+  return (~occ) & 0xff;
+}
+
 struct CaseTables {
-  int4 tn[kNumCases];  // (t, n.x, n.y, n.z)
+  int4 tn[kNumCases];      // (t, n.x, n.y, n.z) by reference case
+  int4 tn_raw[kNumCases];  // the same, indexed by mc_cells' raw corner word
 };
 
 // Geometry of one launch: doubled-coordinate centre and half spacings used to
