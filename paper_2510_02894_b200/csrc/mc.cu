@@ -390,19 +390,20 @@ __device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits,
   }
 }
 
-// One thread = one (word column q, row v) and kz <= KZ consecutive z steps
-// (kz is chosen per ROI on the device; steps past kz are predicated off, so
-// one straight-line body serves every depth and the warp intrinsics stay
-// converged -- branching between per-depth bodies made ptxas emulate them).
+// One thread = one (word column q, row v) and kz consecutive z steps (kz is
+// chosen per ROI on the device and is grid-uniform, so the rolled step loop
+// keeps the warp intrinsics converged).  The step body is not unrolled: the
+// 4x-unrolled form (4.1 K SASS instructions) spent a quarter of its warp
+// samples in instruction-fetch stalls on C3.
 // Cell (u, v, w) has lower corner at unpadded voxel (u, v, w), u,v,w >= -1
 // (reference padded cell index minus 1).  The thread owns cells and lattice
-// points u = 32q - 1 + i, i in [0, 31].  All 2*(KZ+1) row words are
-// loaded up front (L2-resident bit volume; latency, not bandwidth, bound).
+// points u = 32q - 1 + i, i in [0, 31].  Row words of the layer two steps
+// ahead are loaded at the top of each step (L2-resident bit volume; latency,
+// not bandwidth, bound).
 //
 // Every emitted vertex is also counted into the histograms the diameter stage
 // sorts by: its 3-D Morton brick (block-private, flushed once per block) and
 // its (plane, in-plane brick) bin in each of its three planes (global).
-template <int KZ>
 __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict__ rp,
                                         const uint32_t* __restrict__ bits,
                                         const uint32_t* __restrict__ segmap,
@@ -467,23 +468,32 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
         v = vlo + (int)(r % nv);
         w0 = wlo + (int)(r / nv) * kz;
       }
-      uint32_t c0[KZ + 1], p0[KZ + 1], c1[KZ + 1], p1[KZ + 1];
-#pragma unroll
-      for (int s = 0; s <= KZ; s++) {
-        const bool on = valid && s <= kz && w0 + s <= whi + 1;
-        row_words(bits, segmap, sparse, q, v, w0 + s, W, ny, nz, on, c0[s], p0[s]);
-        row_words(bits, segmap, sparse, q, v + 1, w0 + s, W, ny, nz, on, c1[s], p1[s]);
+      // Rows (v, w) and (v + 1, w) of the step's two z layers; the layer two
+      // steps ahead is loaded at the top of each step (one rolled body keeps
+      // the kernel inside the instruction cache).
+      uint32_t ca0, pa0, cb0, pb0, ca1, pa1, cb1, pb1;
+      {
+        const bool on0 = valid && w0 <= whi + 1, on1 = valid && 1 <= kz && w0 + 1 <= whi + 1;
+        row_words(bits, segmap, sparse, q, v, w0, W, ny, nz, on0, ca0, pa0);
+        row_words(bits, segmap, sparse, q, v + 1, w0, W, ny, nz, on0, cb0, pb0);
+        row_words(bits, segmap, sparse, q, v, w0 + 1, W, ny, nz, on1, ca1, pa1);
+        row_words(bits, segmap, sparse, q, v + 1, w0 + 1, W, ny, nz, on1, cb1, pb1);
       }
       const int xbase = 32 * q - 1;
-#pragma unroll
-      for (int s = 0; s < KZ; s++) {
+#pragma unroll 1
+      for (int s = 0; s < kz; s++) {  // kz is grid-uniform: the warp stays converged
         const int w = w0 + s;
-        if (s >= kz) break;  // block-uniform
+        uint32_t ca2, pa2, cb2, pb2;
+        const bool on2 = valid && s + 2 <= kz && w + 2 <= whi + 1;
+        row_words(bits, segmap, sparse, q, v, w + 2, W, ny, nz, on2, ca2, pa2);
+        row_words(bits, segmap, sparse, q, v + 1, w + 2, W, ny, nz, on2, cb2, pb2);
         const bool on = valid && w <= whi;
-        const unsigned long long A = ((unsigned long long)c0[s] << 1) | (p0[s] >> 31);
-        const unsigned long long B = ((unsigned long long)c1[s] << 1) | (p1[s] >> 31);
-        const unsigned long long C = ((unsigned long long)c0[s + 1] << 1) | (p0[s + 1] >> 31);
-        const unsigned long long D = ((unsigned long long)c1[s + 1] << 1) | (p1[s + 1] >> 31);
+        const unsigned long long A = ((unsigned long long)ca0 << 1) | (pa0 >> 31);
+        const unsigned long long B = ((unsigned long long)cb0 << 1) | (pb0 >> 31);
+        const unsigned long long C = ((unsigned long long)ca1 << 1) | (pa1 >> 31);
+        const unsigned long long D = ((unsigned long long)cb1 << 1) | (pb1 >> 31);
+        ca0 = ca1; pa0 = pa1; cb0 = cb1; pb0 = pb1;
+        ca1 = ca2; pa1 = pa2; cb1 = cb2; pb1 = pb2;
         uint32_t ex = 0, ey = 0, ez = 0, act = 0;
         if (on) {
           ex = (uint32_t)(A ^ (A >> 1));
@@ -620,7 +630,7 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
   }
   for (int i = threadIdx.x; i < kSortSupers; i += blockDim.x) s_sup[i] = 0;
   __syncthreads();
-  long long volk = mc_body<4>(kz, rp, bits, segmap, st, vkeys, cap, sort_counts, pbin_counts, bb,
+  long long volk = mc_body(kz, rp, bits, segmap, st, vkeys, cap, sort_counts, pbin_counts, bb,
                               s_hist, tabs->tn_raw, s_sup, s_stage);
   const int lane = threadIdx.x & 31;
   // Block flush: exact integer partials.
