@@ -75,6 +75,12 @@ struct BoxAcc {
     y0 = min(y0, y);  y1 = max(y1, y);
     z0 = min(z0, z);  z1 = max(z1, z);
   }
+  // Word at column w of row (y, z), already located.
+  __device__ __forceinline__ void add_at(uint32_t word, int w, int y, int z) {
+    x0 = min(x0, 32 * w + __ffs(word) - 1); x1 = max(x1, 32 * w + 31 - __clz(word));
+    y0 = min(y0, y);  y1 = max(y1, y);
+    z0 = min(z0, z);  z1 = max(z1, z);
+  }
   __device__ __forceinline__ void flush(Stats* st) {
     // Integer warp reductions (REDUX), then one atomic per field per warp.
     int hx1 = __reduce_max_sync(kFull, x1);
@@ -278,12 +284,21 @@ __global__ void __launch_bounds__(256) bits_bbox(const RoiParams* __restrict__ r
         uint4 v[4];
 #pragma unroll
         for (int t = 0; t < 4; t++) v[t] = __ldcg(bits4 + 4 * sgi + t);
+        // locate the first word once (one 64-bit division), then step the
+        // (w, y, z) position word by word
+        const long long row = 16 * sgi / W;
+        int w = (int)(16 * sgi - row * W), z = (int)(row / ny), y = (int)(row - (long long)z * ny);
 #pragma unroll
         for (int t = 0; t < 4; t++) {
           const uint32_t w4[4] = {v[t].x, v[t].y, v[t].z, v[t].w};
 #pragma unroll
-          for (int u = 0; u < 4; u++)
-            if (w4[u]) box.add(w4[u], 16 * sgi + 4 * t + u, W, ny);
+          for (int u = 0; u < 4; u++) {
+            if (w4[u]) box.add_at(w4[u], w, y, z);
+            if (++w == W) {
+              w = 0;
+              if (++y == ny) { y = 0; z++; }
+            }
+          }
         }
       } else {
         for (long long wi = 16 * sgi; wi < n_words; wi++) {
@@ -309,9 +324,16 @@ __global__ void __launch_bounds__(256) bits_bbox(const RoiParams* __restrict__ r
       if (v[k].x | v[k].y | v[k].z | v[k].w) {
         const long long i = base + (long long)k * blockDim.x + threadIdx.x;
         const uint32_t w4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+        const long long row = 4 * i / W;
+        int w = (int)(4 * i - row * W), z = (int)(row / ny), y = (int)(row - (long long)z * ny);
 #pragma unroll
-        for (int t = 0; t < 4; t++)
-          if (w4[t]) box.add(w4[t], 4 * i + t, W, ny);
+        for (int t = 0; t < 4; t++) {
+          if (w4[t]) box.add_at(w4[t], w, y, z);
+          if (++w == W) {
+            w = 0;
+            if (++y == ny) { y = 0; z++; }
+          }
+        }
       }
     }
   }
