@@ -637,14 +637,18 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
 #pragma unroll
   for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
   if (bb[3] < 0) return;  // empty ROI (block-uniform)
-  // z steps per thread, chosen per ROI from the bbox: 4 when the bbox gives
-  // every resident thread an item (fewer row loads per step), 1 or 2 for small
+  // z steps per thread, chosen per ROI from the bbox: the deepest of 8 / 4
+  // that still gives every resident thread an item (fewer row loads and chunk
+  // prologues per step; C3 single call 162 -> 150 us at 8), 1 or 2 for small
   // bboxes, where parallelism -- not loads -- is the limit (C2: ~22 K items at
   // depth 4 for ~150 K resident threads).
   const long long cols = (long long)(((bb[3] + 1) >> 5) - (bb[0] >> 5) + 1) * (bb[4] - bb[1] + 2);
   const int zs = bb[5] - bb[2] + 2;
   const long long threads = (long long)gridDim.x * blockDim.x;
-  const int kz = cols * ((zs + 3) / 4) >= threads ? 4 : (cols * ((zs + 1) / 2) >= threads ? 2 : 1);
+  const int kz = cols * ((zs + 7) / 8) >= threads   ? 8
+                 : cols * ((zs + 3) / 4) >= threads ? 4
+                 : cols * ((zs + 1) / 2) >= threads ? 2
+                                                    : 1;
   // blocks past the bbox's work items have nothing to do: skip the prologue too
   if ((long long)blockIdx.x * blockDim.x >= cols * ((zs + kz - 1) / kz)) return;
   for (int i = threadIdx.x; i < kNumCases; i += blockDim.x) {
