@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_all(unsigned int* __restric
       const long long n = (long long)st->n_vert;
       const long long CT = ((n + kChunkV - 1) / kChunkV + kSuper - 1) / kSuper;
       for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < CT;
-           t += (long long)gridDim.x * blockDim.x) {
+           t += (long long)kScanBlocks * blockDim.x) {  // (brick blocks only)
         sboxes[2 * t] = make_int4(INT_MAX, INT_MAX, INT_MAX, 0);
         sboxes[2 * t + 1] = make_int4(INT_MIN, INT_MIN, INT_MIN, 0);
       }
@@ -134,6 +134,13 @@ __global__ void __launch_bounds__(kScanThreads) scan_all(unsigned int* __restric
     // Block base = super-bin prefix of its first slice; within the block one
     // scan over its kScanSlices slices (the super bins are their sums).
     const unsigned int* sup = sort_counts + kSortBins;
+    // No vertex in this block's slices (block-uniform): its counts are still
+    // zero and no vertex will look up its cursors -- nothing to write.  (Most
+    // slices of a small or thin-shelled ROI's Morton range.)
+    bool any = false;
+#pragma unroll
+    for (int i = 0; i < kScanSlices; i++) any |= sup[kScanSlices * blockIdx.x + i] != 0u;
+    if (!any) return;
     unsigned int base;
     block_exscan(threadIdx.x < kScanSlices * blockIdx.x ? sup[threadIdx.x] : 0u, &base);
     uint4 v[kPerThread / 4];
