@@ -375,6 +375,37 @@ __global__ void __launch_bounds__(256) boxes_extremes(const int4* __restrict__ k
   __syncthreads();
   if (threadIdx.x < 2 * kNDir && s_ext[threadIdx.x])
     atomicMax(&st->ext[threadIdx.x], s_ext[threadIdx.x]);
+  // The last block to finish turns the 26 extremes into the exact lower bound
+  // LB = max exact (reference fp64 arithmetic) squared distance among them --
+  // a real pair, so LB <= D^2; it also seeds the exact 3-D maximum.  (Once
+  // here instead of in every unit_filter block.)
+  if (!last_block(&st->done3) || n == 0) return;
+  __shared__ double qx[2 * kNDir], qy[2 * kNDir], qz[2 * kNDir];
+  __shared__ double s_lb[32];
+  if (threadIdx.x < 2 * kNDir) {
+    const unsigned int ix = (unsigned int)(__ldcg(&st->ext[threadIdx.x]) & 0xffffffffu);
+    const int4 k = keys[ix < n ? ix : n - 1];
+    qx[threadIdx.x] = ref_coord(k.x + f.ox2, f.sx);
+    qy[threadIdx.x] = ref_coord(k.y + f.oy2, f.sy);
+    qz[threadIdx.x] = ref_coord(k.z + f.oz2, f.sz);
+  }
+  __syncthreads();
+  double lb = 0.0;
+  for (int p = threadIdx.x; p < 4 * kNDir * kNDir; p += blockDim.x) {
+    const int i = p / (2 * kNDir), j = p % (2 * kNDir);
+    lb = fmax(lb, ref_sq_dist(qx[i], qy[i], qz[i], qx[j], qy[j], qz[j]));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) lb = fmax(lb, __shfl_xor_sync(0xffffffffu, lb, o));
+  if (lane == 0) s_lb[threadIdx.x >> 5] = lb;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); w++) lb = fmax(lb, s_lb[w]);
+    if (lb > 0.0) {
+      atomic_max_pos_f64(&st->lb, lb);
+      atomic_max_pos_f64(&st->sq[0], lb);
+    }
+  }
 }
 
 __device__ __forceinline__ double axis_reach(int loA, int hiA, int loB, int hiB, double h) {
@@ -447,11 +478,9 @@ __device__ __forceinline__ void test_chunk_pair(const PairTest& F, bool valid, i
     F.work[o] = make_uint2((unsigned int)i, (unsigned int)j | (sub << kSubShift));
 }
 
-// Every block: LB = max exact (reference fp64 arithmetic) squared distance
-// among the 26 extreme vertices (a real pair, so LB <= D^2; block 0 also seeds
-// the exact 3-D maximum with it).  Then every chunk pair (I <= J) is kept iff
-// the max distance between the two chunk boxes can reach LB; survivors are
-// compacted into `work` (pair index t over the C x C upper triangle).
+// Every chunk pair (I <= J) is kept iff the max distance between the two
+// chunk boxes can reach LB (from boxes_extremes); survivors are compacted
+// into `work` (pair index t over the C x C upper triangle).
 __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys,
                                                    const int4* __restrict__ boxes, long long cap,
                                                    const RoiParams* __restrict__ rp, int prune,
@@ -463,33 +492,9 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
   pdl_enter();
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
-  __shared__ double px[2 * kNDir], py[2 * kNDir], pz[2 * kNDir];
-  __shared__ double s_lb[8];
   const long long n = n_verts(st, cap);
   if (n == 0) return;
-  if (threadIdx.x < 2 * kNDir) {
-    const unsigned int idx = (unsigned int)(st->ext[threadIdx.x] & 0xffffffffu);
-    const int4 k = keys[idx < n ? idx : n - 1];
-    px[threadIdx.x] = ref_coord(k.x + f.ox2, f.sx);
-    py[threadIdx.x] = ref_coord(k.y + f.oy2, f.sy);
-    pz[threadIdx.x] = ref_coord(k.z + f.oz2, f.sz);
-  }
-  __syncthreads();
-  double lb = 0.0;
-  for (int p = threadIdx.x; p < 4 * kNDir * kNDir; p += blockDim.x) {
-    const int i = p / (2 * kNDir), j = p % (2 * kNDir);
-    lb = fmax(lb, ref_sq_dist(px[i], py[i], pz[i], px[j], py[j], pz[j]));
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) lb = fmax(lb, __shfl_xor_sync(0xffffffffu, lb, o));
-  if ((threadIdx.x & 31) == 0) s_lb[threadIdx.x >> 5] = lb;
-  __syncthreads();
-  lb = 0.0;
-  for (int w = 0; w < 8; w++) lb = fmax(lb, s_lb[w]);
-  if (blockIdx.x == 0 && threadIdx.x == 0 && lb > 0.0) {
-    atomic_max_pos_f64(&st->lb, lb);
-    atomic_max_pos_f64(&st->sq[0], lb);
-  }
+  const double lb = __longlong_as_double((long long)st->lb);  // boxes_extremes' last block
   const double thr = lb * (1.0 - 1e-9);  // UB and LB are exact up to fp64 rounding
   // Two levels: a pair of super-chunks (8 chunks = 1024 vertices, boxes from
   // boxes_extremes) is tested first; only if it can reach LB are its (up to

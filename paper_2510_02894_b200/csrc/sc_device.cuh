@@ -31,7 +31,8 @@ struct Stats {
   unsigned long long lb;               // fp64 bits: exact squared distance lower bound
   unsigned long long n_work;           // surviving 3-D work units after pruning
   unsigned int done1, done2;           // done1: scan_all plane-block ticket; done2 spare
-  unsigned int ovf, pad1;              // V exceeded the diameter-side buffers: skip the rest
+  unsigned int ovf;                    // V exceeded the diameter-side buffers: skip the rest
+  unsigned int done3;                  // boxes_extremes block ticket (last block: the 3-D LB)
   unsigned long long plb[3];           // fp64 bits: exact planar lower bounds per family
   unsigned long long n_pwork;          // surviving planar units after pruning
   unsigned long long plane_chunks;     // 256-entry chunks over all planes
