@@ -83,8 +83,10 @@ __global__ void plane_boxes(const int2* __restrict__ sorted,
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   if ((long long)blockIdx.x * (blockDim.x >> 5) >= chunks) return;  // block-uniform
-  __shared__ unsigned int s_off[kOffSmem];
-  const unsigned int* coff = stage_offsets(cstart, P, s_off);
+  // The chunk offsets are searched in place (L1-resident after the first
+  // warps): staging them in shared memory cost every block a full pass over
+  // them and a barrier before its first chunk.
+  const unsigned int* coff = cstart;
   for (long long c = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < chunks;
        c += warps) {
     const int p = find_plane(coff, P, (unsigned long long)c);
