@@ -362,10 +362,10 @@ def run_ours(args):
     # W warm-up steps, and at least two rounds over the 16 pipeline slots so
     # every slot has captured its CUDA graph before the timed region.
     # Then one untimed batch of exactly the timed shape: the first K-ROI batch
-    # after a differently sized one runs ~15 % slower on the device (C2, K = 20:
-    # 57.7 vs 49-50 us/ROI for the next ones; host-side launch and collect
-    # times are identical, tools/k20_probe.py), a one-off the steady stream of
-    # batches a user sends does not pay.
+    # after the capture-bound warm-up (the GPU mostly waits on host-side graph
+    # captures there) runs ~15 % slower on the device (C2, K = 20: 57.7 vs 49-50
+    # us/ROI for the next ones; host-side launch and collect times identical,
+    # tools/k20_probe.py), a one-off a steady stream of batches does not pay.
     Ww = max(W, 32)
     sc.calculate_coefficients_device_batch([d_masks[i % len(d_masks)] for i in range(Ww)],
                                            [sps[i % len(sps)] for i in range(Ww)], stream=stream)
