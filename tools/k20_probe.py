@@ -1,6 +1,7 @@
 """Device-batch time of K ROIs (the bench's timed region) vs slot count.
 
 usage: python tools/k20_probe.py [K] [workload] [clocks] [warmk]"""
+import os
 import sys
 import time
 
@@ -12,10 +13,13 @@ import paper_2510_02894_b200 as sc  # noqa: E402
 from paper_2510_02894_b200 import _native  # noqa: E402
 
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 20
-SLOTS = (16,) if "only16" in sys.argv[3:] else (12, 16)
+SLOTS = (16,) if "only16" in sys.argv[3:] else tuple(int(x) for x in os.environ.get("SLOTS", "12,16").split(","))
 w = sys.argv[2] if len(sys.argv) > 2 else "c2"
 clocks = "clocks" in sys.argv[3:]
 warm_k = "warmk" in sys.argv[3:]  # NVML sampler running, as in bench.py
+for kv in filter(None, os.environ.get("SC_OPTS", "").split(",")):  # fixed extra options
+    k, v = kv.split("=")
+    _native.set_option(k, int(v))
 rois, _ = bench.load_workload(w)
 d = [torch.from_numpy(m).cuda() for m, _ in rois]
 sps = [sp for _, sp in rois]
