@@ -169,7 +169,7 @@ int sc_last_diagnostics(int device, int64_t* out, int n);
  * host scans the rest (-1: balanced from the measured host-scan and PCIe
  * rates and the previous ROI's slab fraction; 0: off);
  * "host_threads" (hardware threads, <= 32) = threads of the host slab scan;
- * "grid_div" (4) / "grid_div_single" (1) = divisor of the per-ROI kernels'
+ * "grid_div" (5) / "grid_div_single" (1) = divisor of the per-ROI kernels'
  * grids (SMs x blocks/SM) in batch entries / single calls: fewer resident
  * blocks per ROI let more ROIs share the GPU, a single ROI wants all of it;
  * "zero_copy" (1) = the per-ROI parameter and result records travel through

@@ -115,7 +115,7 @@ std::atomic<int> g_opt_stage_times{0};  // single-call graph events: 0 none (tim
 // in flight and run faster with few resident blocks per ROI (measured C2 div
 // 2 / 4: 50.4 / 45.8 us per ROI); a single call wants the whole GPU for its
 // latency chain (C3 call: div 1 far faster than 4).
-std::atomic<int> g_opt_grid_div{4};         // batch entries ("grid_div")
+std::atomic<int> g_opt_grid_div{5};         // batch entries ("grid_div")
 std::atomic<int> g_opt_grid_div_single{1};  // single calls ("grid_div_single")
 std::atomic<int> g_opt_pack_bps{0};  // pack blocks per SM (0 = occupancy limit)  // divisor of the latency-bound kernels' grids
 std::atomic<int> g_opt_pack_mode{0};  // bit 0: one step per pack block; bit 1: low-priority pack;

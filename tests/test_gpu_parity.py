@@ -273,7 +273,7 @@ def test_batch_launch_options_identical(sc, golden, golden_arrays, cuda_device):
     want = [sc.calculate_coefficients(a, sp).to_dict() for a, sp in cases]
     ds = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a, _ in cases]
     sps = [sp for _, sp in cases]
-    defaults = {"grid_div": 4, "pdl": 0, "batch_stage_times": 0, "slots": 16, "pack_mode": 0,
+    defaults = {"grid_div": 5, "pdl": 0, "batch_stage_times": 0, "slots": 16, "pack_mode": 0,
                 "sparse_bits": 1, "fork": 1, "pack_tma": 0, "zero_copy": 1}
     try:
         for opt, val in (("grid_div", 1), ("grid_div", 2), ("pdl", 1), ("batch_stage_times", 1),
