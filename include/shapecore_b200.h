@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define SC_ABI_VERSION 2
+#define SC_ABI_VERSION 3
 
 enum {
   SC_OK = 0,
@@ -95,8 +95,10 @@ int sc_calculate_coefficients_raw(const void* data, int dtype, const int64_t sha
                                   double label_float, const double spacing[3], int device,
                                   sc_coeffs* out);
 
-/* Device-resident mask on the CURRENT device; `stream` is a cudaStream_t (NULL =
- * the library's own stream).  The mask must stay valid for the call. */
+/* Device-resident mask on the CURRENT device; `stream` is a cudaStream_t.  The
+ * ROI runs after all prior work on `stream`; NULL means the legacy default
+ * stream (ordered the same way; the ROI itself then runs on a library slot
+ * stream).  The call is synchronous.  The mask must stay valid for the call. */
 int sc_calculate_coefficients_device(const uint8_t* d_mask, int64_t nx, int64_t ny,
                                      int64_t nz, const double spacing[3], void* stream,
                                      sc_coeffs* out);
@@ -122,8 +124,9 @@ int sc_calculate_coefficients_batch(const uint8_t* const* masks, const int64_t* 
                                     sc_coeffs* out);
 
 /* Same for device-resident masks on the CURRENT device (pipelined likewise).
- * If `stream` (cudaStream_t) is non-NULL the batch is ordered after prior work
- * on it, and work enqueued on it later is ordered after the batch. */
+ * The batch is ordered after prior work on `stream` (cudaStream_t; NULL = the
+ * legacy default stream), and work enqueued on it later is ordered after the
+ * batch. */
 int sc_calculate_coefficients_device_batch(const uint8_t* const* d_masks, const int64_t* dims,
                                            const double* spacings, int64_t count, void* stream,
                                            sc_coeffs* out);
@@ -157,10 +160,14 @@ int sc_last_kernel_times(int device, double* ms, int n);
  * which pass 1 evaluates the listed 64 x 64 sub-pairs.  Returns how many were
  * written (<= 8). */
 int sc_last_diagnostics(int device, int64_t* out, int n);
-/* Process-wide switches: "prune" (default 1) = exact bbox pruning of 3-D and
- * planar work units; "pass1_packed" (1) = FFMA2 variant of the 3-D pass;
- * "graphs" (1) = replay each ROI pipeline as a cached CUDA graph; "slots" (16)
- * = pipeline slots (stream + scratch) the batch entries keep in flight;
+/* Options.  Every call takes a snapshot of the options at entry, so changing
+ * them never affects a call already in flight.  sc_set_option sets the
+ * process-wide value; sc_set_thread_option overrides it for calls made from
+ * the calling thread only (until sc_clear_thread_options).
+ * "prune" (default 1) = exact bbox pruning of 3-D and planar work units;
+ * "pass1_packed" (1) = FFMA2 variant of the 3-D pass;
+ * "graphs" (1) = replay each ROI pipeline as a cached CUDA graph; "slots" (32)
+ * = pipeline slots (stream + scratch) the batch entries keep in flight (1-32);
  * "host_crop" (1) = host-mask entries copy only the occupied z/y slab;
  * "host_pack" (-1) = bit-pack the occupied slab on the host and copy only
  * its bits into the device bit volume (1 always, 0 never, -1 when the raw
@@ -169,7 +176,7 @@ int sc_last_diagnostics(int device, int64_t* out, int n);
  * host scans the rest (-1: balanced from the measured host-scan and PCIe
  * rates and the previous ROI's slab fraction; 0: off);
  * "host_threads" (hardware threads, <= 32) = threads of the host slab scan;
- * "grid_div" (5) / "grid_div_single" (1) = divisor of the per-ROI kernels'
+ * "grid_div" (10) / "grid_div_single" (1) = divisor of the per-ROI kernels'
  * grids (SMs x blocks/SM) in batch entries / single calls: fewer resident
  * blocks per ROI let more ROIs share the GPU, a single ROI wants all of it;
  * "zero_copy" (1) = the per-ROI parameter and result records travel through
@@ -181,18 +188,24 @@ int sc_last_diagnostics(int device, int64_t* out, int n);
  * event node adds latency);
  * "batch_stage_times" (0) = per-stage CUDA events in batch graphs (without
  * them mesh_ms / diameters_ms come from the %globaltimer stamps);
- * "pack_tma" (0) = CTAs per SM of the cp.async.bulk (TMA) variant of the
- * pack (0 = the 128-bit-load pack);
+ * "pack_tma" (1) / "pack_tma_single" (0) = CTAs per SM of the cp.async.bulk
+ * (TMA) pack in batch entries / single calls (0 = the 128-bit-load pack);
+ * "fused_bbox" (1) = the pack accumulates the occupied bbox itself (else a
+ * separate pass over the bit volume);
  * "sparse_bits" (1) = the pack writes only nonzero 16-word segments of the
- * bit volume (segment map); "pdl" (0) = programmatic dependent launch of the
- * per-ROI kernels in batch graphs; "fork" (1) = the planar filter chain runs
- * on a second stream beside the 3-D one; "dcap" / "wcap" = initial vertex /
- * 3-D work-list capacities (an overflow re-runs the ROI with exact sizes).
- * Measurement / experiment switches: "fused_bbox" (0), "pack_mode" (0),
- * "pack_bps" (0), "debug_stages" (off; enqueue only the first N kernels,
- * results invalid).
+ * bit volume (segment map); "pack_skip" (1) = ... and does no conversion work
+ * at all for all-background segments; "pdl" (0) = programmatic dependent
+ * launch of the per-ROI kernels in batch graphs; "fork" (1) = the planar
+ * filter chain runs on a second stream beside the 3-D one; "dcap" / "wcap" =
+ * initial vertex / 3-D work-list capacities (an overflow re-runs the ROI with
+ * exact sizes).
+ * Measurement / experiment switches: "pack_mode" (0), "pack_bps" (0),
+ * "debug_stages" (off; enqueue only the first N kernels, results invalid),
+ * "debug_empty" (0; N empty kernels per ROI, a launch-rate probe).
  * Results are identical either way; 0 on success, SC_ERR_INPUT otherwise. */
 int sc_set_option(const char* name, int value);
+int sc_set_thread_option(const char* name, int value);
+void sc_clear_thread_options(void);
 uint64_t sc_launch_count(void);
 int sc_probe_fp32_peak(int device, int mode, double* tflops);
 

@@ -36,6 +36,8 @@ EXPORTED = (
     "sc_last_kernel_times",
     "sc_last_diagnostics",
     "sc_set_option",
+    "sc_set_thread_option",
+    "sc_clear_thread_options",
     "sc_launch_count",
     "sc_probe_fp32_peak",
     "sc_occupied_slab",
@@ -116,6 +118,8 @@ def load():
         L.sc_launch_count.restype = ctypes.c_uint64
         L.sc_last_diagnostics.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
         L.sc_set_option.argtypes = [ctypes.c_char_p, ctypes.c_int]
+        L.sc_set_thread_option.argtypes = [ctypes.c_char_p, ctypes.c_int]
+        L.sc_clear_thread_options.restype = None
         L.sc_probe_fp32_peak.argtypes = [ctypes.c_int, ctypes.c_int, dp]
         L.sc_occupied_slab.argtypes = [u8p, i64, i64, i64, ctypes.c_int, ctypes.POINTER(i64)]
         L.sc_last_error.restype = ctypes.c_char_p
@@ -193,7 +197,24 @@ def last_diagnostics(device: int = 0) -> dict:
 
 
 def set_option(name: str, value: int) -> None:
+    """Process-wide option (calls already in flight keep their snapshot)."""
     raise_for(load().sc_set_option(name.encode(), int(value)), "sc_set_option")
+
+
+class thread_options:
+    """`with thread_options(prune=0, slots=8): ...` -- options for the calls
+    made from this thread only (sc_set_thread_option); restored on exit."""
+
+    def __init__(self, **opts):
+        self.opts = opts
+
+    def __enter__(self):
+        for k, v in self.opts.items():
+            raise_for(load().sc_set_thread_option(k.encode(), int(v)), "sc_set_thread_option")
+        return self
+
+    def __exit__(self, *exc):
+        load().sc_clear_thread_options()
 
 
 def occupied_slab(mask, threads: int = 0):

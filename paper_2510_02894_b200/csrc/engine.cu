@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <array>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -39,6 +40,7 @@ __global__ void init_stats(Stats* st, uint32_t* segmap, long long n_seg, const R
 template <int U, bool BOX>
 __global__ void pack_bits_v16(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 __global__ void bits_bbox(const RoiParams*, const uint4*, Stats*, const uint32_t*);
+template <bool BOX>
 __global__ void pack_bits_tma(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 constexpr int kTmaSmem = 4 * 16384;  // mc.cu kTmaStages x kTmaTile
 __global__ void pack_bits_generic(const RoiParams*, uint32_t*, Stats*, uint32_t*);
@@ -69,8 +71,8 @@ __global__ void plane_lb(const int2*, const unsigned int*, const unsigned long l
 __global__ void plane_filter(const unsigned int*, const unsigned int*, const unsigned int*,
                              const int4*, const RoiParams*, int, int, int, long long, Stats*,
                              uint2*, const int4*);
-__global__ void cloud_diameters(const double*, const double*, const double*, long long, int,
-                                unsigned long long*);
+__global__ void cloud_diameters(const double*, const double*, const double*, long long,
+                                long long, unsigned long long*);
 int launch_binarize(const void*, int, const long long[3], int, int, long long, double, uint8_t*,
                     int, cudaStream_t);
 __global__ void mesh_count(const RoiParams*, const uint32_t*, const Stats*, unsigned int*);
@@ -91,6 +93,7 @@ __global__ void fold_pass(double*, double*, long long);
 template <int MODE>
 __global__ void fp32_probe(float*, int, float, float);
 
+__global__ void empty_kernel();
 }  // namespace sc
 
 using namespace sc;
@@ -98,32 +101,51 @@ using namespace sc;
 namespace {
 
 thread_local std::string g_err;
-std::atomic<bool> g_opt_prune{true}, g_opt_packed{true}, g_opt_graphs{true};
-std::atomic<int> g_opt_stages{1 << 30};  // debug: kernels enqueued per ROI
-std::atomic<bool> g_opt_fbox{false};  // bbox accumulated inside the pack (else bits_bbox; measured faster)
-std::atomic<int> g_opt_slots{16};  // pipeline slots used by the batch entries (measured: 16 > 12 > 8)
-std::atomic<long long> g_opt_dcap{2LL << 20};  // default diameter-side vertex capacity
-std::atomic<long long> g_opt_wcap{1LL << 20};  // default 3-D work-list capacity (chunk pairs)
-std::atomic<bool> g_opt_batch_times{false};  // per-stage event nodes in batch graphs
-std::atomic<bool> g_opt_pdl{false};  // programmatic dependent launch in batch graphs
-std::atomic<bool> g_opt_sparse{true};  // sparse bit volume (segment map), option "sparse_bits"
-std::atomic<int> g_opt_pack_tma{0};  // TMA bulk-copy pack, CTAs per SM (0 = 128-bit load pack)
-std::atomic<bool> g_opt_fork{true};
-std::atomic<bool> g_opt_zc{true};  // option "zero_copy": RoiParams / Stats via mapped host memory
-std::atomic<int> g_opt_stage_times{0};  // single-call graph events: 0 none (timer stamps), 1 mesh/diam, 2 all  // planar chain on a second stream (option "fork")
-// Divisor of the latency-bound per-ROI kernels' grids: batches keep many ROIs
-// in flight and run faster with few resident blocks per ROI (measured C2 div
-// 2 / 4: 50.4 / 45.8 us per ROI); a single call wants the whole GPU for its
-// latency chain (C3 call: div 1 far faster than 4).
-std::atomic<int> g_opt_grid_div{5};         // batch entries ("grid_div")
-std::atomic<int> g_opt_grid_div_single{1};  // single calls ("grid_div_single")
-std::atomic<int> g_opt_pack_bps{0};  // pack blocks per SM (0 = occupancy limit)  // divisor of the latency-bound kernels' grids
-std::atomic<int> g_opt_pack_mode{0};  // bit 0: one step per pack block; bit 1: low-priority pack;
-                                      // bit 2 (debug): no pack, reuse the slot's bit volume
-std::atomic<bool> g_opt_crop{true};
-std::atomic<int> g_opt_host_pack{-1};  // host_pack: bit-pack the slab on the host (1 / 0 / -1 adaptive)
-std::atomic<int> g_opt_split{-1};  // host_split: % of leading slices sent unscanned (-1 adaptive, 0 off)  // host entries: copy only the occupied z/y slab (host_crop.h)
-std::atomic<int> g_opt_host_threads{(int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()))};
+// Options (sc_set_option).  Every call takes a snapshot at entry (Ctx::o),
+// so a concurrent sc_set_option never changes a call already in flight;
+// sc_set_thread_option overrides them for the calling thread only.
+struct Opts {
+  bool prune = true;         // exact bbox pruning of 3-D and planar work units
+  bool packed = true;        // FFMA2 variant of pass 1 ("pass1_packed")
+  bool graphs = true;        // replay each ROI pipeline as a cached CUDA graph
+  int stages = 1 << 30;      // debug: kernels enqueued per ROI ("debug_stages")
+  int empty = 0;             // debug: empty kernels appended per ROI ("debug_empty")
+  bool fbox = true;          // bbox accumulated inside the pack ("fused_bbox"; else bits_bbox)
+  int slots = 32;            // pipeline slots of the batch entries (measured 32 > 24 > 16 > 12)
+  long long dcap = 2LL << 20;  // default diameter-side vertex capacity
+  long long wcap = 1LL << 20;  // default 3-D work-list capacity (chunk pairs)
+  bool batch_times = false;  // per-stage event nodes in batch graphs
+  bool pdl = false;          // programmatic dependent launch in batch graphs
+  bool sparse = true;        // sparse bit volume (segment map), "sparse_bits"
+  bool pack_skip = true;     // sparse pack: no conversion of all-zero segments
+  int pack_tma = 1;          // batch graphs: TMA bulk-copy pack, CTAs per SM (0 = 128-bit loads)
+  int pack_tma_single = 0;   // the same for single calls (the 128-bit-load pack is faster alone)
+  bool fork = true;          // planar chain on a second stream
+  bool zc = true;            // "zero_copy": RoiParams / Stats via mapped host memory
+  int stage_times = 0;       // single-call graph events: 0 none (timer stamps), 1 mesh/diam, 2 all
+  // Divisor of the latency-bound per-ROI kernels' grids: batches keep many
+  // ROIs in flight and run faster with few resident blocks per ROI (C2, 32
+  // slots: div 5 / 10 / 20 = 33.98 / 32.80 / 33.21 us per ROI); a single call
+  // wants the whole GPU for its latency chain (C3 call: div 1 far faster than 4).
+  int grid_div = 10;         // batch entries ("grid_div")
+  int grid_div_single = 1;   // single calls ("grid_div_single")
+  int pack_bps = 0;          // pack blocks per SM (0 = occupancy limit)
+  int pack_mode = 0;         // bit 0: one step per pack block; bit 1: low-priority pack;
+                             // bit 2 (debug): no pack, reuse the slot's bit volume
+  bool crop = true;          // host entries: copy only the occupied z/y slab (host_crop.h)
+  int host_pack = -1;        // bit-pack the slab on the host (1 / 0 / -1 adaptive)
+  int split = -1;            // % of leading slices sent unscanned (-1 adaptive, 0 off)
+  int host_threads = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+};
+std::mutex g_opt_mu;
+Opts g_opts;                           // process-wide (sc_set_option)
+thread_local bool t_opts_on = false;   // sc_set_thread_option was used on this thread
+thread_local Opts t_opts;
+Opts snapshot_opts() {
+  if (t_opts_on) return t_opts;
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  return g_opts;
+}
 std::atomic<unsigned long long> g_launches{0};
 
 void set_err(const char* fmt, ...) {
@@ -224,6 +246,7 @@ struct DevBuf {
 };
 
 struct Ctx {
+  Opts o;  // options of the call in progress (snapshot taken at its entry)
   int device = 0;
   int sms = 148;
   std::mutex mu;
@@ -322,7 +345,7 @@ struct Ctx {
 // Two independent pipeline slots per device (stream, events, scratch, graphs):
 // single-ROI calls use slot 0; batch calls alternate slots so the H2D copy and
 // kernels of ROI i+1 overlap the tail and the host round trip of ROI i.
-constexpr int kSlots = 16;
+constexpr int kSlots = 32;
 std::mutex g_ctx_mu;
 std::vector<std::array<std::unique_ptr<Ctx>, kSlots>> g_ctx;
 
@@ -358,11 +381,12 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     const char* sp_env = std::getenv("SC_SLOT_PRIO");
     if (!(sp_env && std::strcmp(sp_env, "0") == 0)) {
       const int levels = c->prio_lo - c->prio_hi + 1;
-      sprio = c->prio_hi + std::min(levels - 1, slot * levels / kSlots);
+      sprio = c->prio_hi + std::min(levels - 1, slot * levels / 16);
     }
     CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, sprio));
     CK(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, sprio));
-    CK(cudaFuncSetAttribute(pack_bits_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
     CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
@@ -378,8 +402,13 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     CK(upload_mesh_tables());
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pass1, diam_pass1<true>, 256, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pass1s, diam_pass1<false>, 256, 0));
-    if (const char* v = getenv("SC_PASS1")) g_opt_packed = std::strcmp(v, "scalar") != 0;
-    if (const char* v = getenv("SC_PRUNE")) g_opt_prune = std::strcmp(v, "0") != 0;
+    static bool env_read = false;  // (g_ctx_mu held) environment defaults, once
+    if (!env_read) {
+      env_read = true;
+      std::lock_guard<std::mutex> lk(g_opt_mu);
+      if (const char* v = getenv("SC_PASS1")) g_opts.packed = std::strcmp(v, "scalar") != 0;
+      if (const char* v = getenv("SC_PRUNE")) g_opts.prune = std::strcmp(v, "0") != 0;
+    }
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_pack, pack_bits_v16<4, false>, 256, 0));
     if (const char* v = getenv("SC_PACK_BPS")) c->occ_pack = std::max(1, std::atoi(v));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_mc, mc_cells, 256, 0));
@@ -389,6 +418,7 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
       cudaFuncAttributes fa;
       const void* kernels[] = {(const void*)init_stats, (const void*)pack_bits_v16<4, false>,
                                (const void*)pack_bits_v16<4, true>,
+                               (const void*)pack_bits_tma<false>, (const void*)pack_bits_tma<true>,
                                (const void*)mesh_count, (const void*)mesh_emit,
                                (const void*)bits_bbox,
                                (const void*)pack_bits_generic, (const void*)mc_cells,
@@ -443,7 +473,7 @@ double f64_of(unsigned long long bits) {
 }
 
 constexpr long long kChunk = 128;  // sc_device.cuh kChunk3: pair unit = chunk x chunk
-// The 3-D work list (surviving chunk pairs) starts at g_opt_wcap entries; a
+// The 3-D work list (surviving chunk pairs) starts at Opts::wcap entries; a
 // ROI whose pruned list is longer re-runs with the exact size.
 constexpr long long kPlaneBinsHost = 256;  // sc_device.cuh kPlaneBins
 
@@ -476,15 +506,16 @@ int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, lo
   CK(c->segmap.ensure(c->bits.cap / 512 + 1));
   CK(c->keys.ensure((size_t)cap));
   const long long C = (dcap + kChunk - 1) / kChunk;  // chunk pairs: C(C+1)/2
-  const long long wc = std::min(C * (C + 1) / 2, std::max(g_opt_wcap.load(), wunits));
+  const long long wc = std::min(C * (C + 1) / 2, std::max(c->o.wcap, wunits));
   CK(c->warp_max.ensure((size_t)wc));
   CK(c->work.ensure((size_t)wc));
   CK(c->keys_sorted.ensure((size_t)dcap));
   CK(c->boxes.ensure((size_t)(2 * (C + 1))));
   CK(c->hboxes.ensure((size_t)(4 * (C + 1))));
-  {  // every super pair can survive (pruning off): size for all of them
+  {  // every super pair can survive (pruning off): size for all of them whenever
+     // unit_filter takes the two-level path (same switch, sc_device.cuh)
     const long long CT = (C + 7) / 8;
-    CK(c->slist.ensure((size_t)(C * (C + 1) / 2 > (4LL << 20) ? CT * (CT + 1) / 2 : 1)));
+    CK(c->slist.ensure((size_t)(C * (C + 1) / 2 > kSingleLevelMax ? CT * (CT + 1) / 2 : 1)));
   }
   CK(c->sboxes.ensure((size_t)(2 * (C / 8 + 1))));
   {
@@ -533,7 +564,7 @@ int lgrid(const Ctx* c, int k) {
 // (diam_refine may not run).
 bool zero_copy_records(const Ctx* c) {
   (void)c;
-  return g_opt_zc.load() && g_opt_stages.load() >= (1 << 20);
+  return c->o.zc && c->o.stages >= (1 << 20);
 }
 
 // Launch of a per-ROI pipeline kernel.  In batch graphs (no stage-event nodes
@@ -552,7 +583,7 @@ cudaError_t launch_k(const Ctx* c, cudaStream_t s, int grid, int block, void (*k
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   // (not with the fork / join: a programmatic edge cannot follow an event wait)
-  cfg.numAttrs = (g_opt_pdl.load() && !c->events_on && !g_opt_fork.load()) ? 1 : 0;
+  cfg.numAttrs = (c->o.pdl && !c->events_on && !c->o.fork) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
@@ -565,17 +596,21 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   const RoiParams* rp = c->d_rp;
   // Diagnostic option "debug_stages": enqueue only the first N kernels (results
   // invalid) to measure the marginal batch cost of each stage.
-  const int lim = g_opt_stages.load();
+  const int lim = c->o.stages;
   int nk = 0;
   const long long cap = (long long)c->keys.cap, dcap = c->dcap_sz;
   // (the pack marks nonzero segments of a cleared map; the no-pack debug mode
   // keeps the previous map)
-  const bool clear_map = g_opt_sparse.load() && !(g_opt_pack_mode.load() & 4) && !c->prepacked;
+  const bool clear_map = c->o.sparse && !(c->o.pack_mode & 4) && !c->prepacked;
   const bool zc = zero_copy_records(c);
   init_stats<<<clear_map ? 8 : 1, 256, 0, s>>>(c->d_stats, c->segmap.p,
                                                clear_map ? (long long)c->segmap.cap : 0LL,
                                                zc ? c->h_rp_dev : nullptr, c->d_rp);
   CKL(1);
+  for (int e = 0; e < c->o.empty; e++) {  // debug: launch-rate probe
+    empty_kernel<<<1, 32, 0, s>>>();
+    CKL(1);
+  }
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[0], s));  // kev0..kev1 = the HBM pass alone
   if (c->prepacked) {  // the host already wrote the bit volume: bbox pass only
@@ -584,7 +619,15 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
                 c->d_stats, c->segmap.p));
     CKL(1);
     if (++nk >= lim) return SC_OK;
-  } else if (fast && g_opt_fbox.load()) {
+  } else if (fast && c->o.fbox && c->o.pack_tma > 0 &&
+             !(c->o.pack_mode & 4)) {
+    // TMA pack with the bbox accumulated inside (no bits_bbox kernel)
+    pack_bits_tma<true><<<c->sms * c->o.pack_tma, 256, kTmaSmem, s>>>(rp, c->bits.p,
+                                                                           c->d_stats, c->segmap.p);
+    CKL(1);
+    if (++nk >= lim) return SC_OK;
+    CK(record(c, c->kev[1], s));
+  } else if (fast && c->o.fbox && !(c->o.pack_mode & 4)) {
     pack_bits_v16<4, true><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(rp, c->bits.p,
                                                                               c->d_stats,
                                                                               c->segmap.p);
@@ -595,9 +638,9 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
     // pack_mode bit 0: one 4 KB step per block (grid covers the slot's largest
     // mask; extra blocks exit) instead of a persistent grid, so blocks retire
     // continuously and other streams' kernels interleave; bit 1: low priority.
-    const int pm = g_opt_pack_mode.load();
+    const int pm = c->o.pack_mode;
     cudaLaunchConfig_t cfg = {};
-    const int pbps = g_opt_pack_bps.load() > 0 ? g_opt_pack_bps.load() : std::max(1, c->occ_pack);
+    const int pbps = c->o.pack_bps > 0 ? c->o.pack_bps : std::max(1, c->occ_pack);
     cfg.gridDim = dim3((unsigned)(c->sms * pbps));
     if (pm & 1)
       cfg.gridDim = dim3((unsigned)std::max<long long>(
@@ -609,8 +652,8 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
     at[0].val.priority = c->prio_lo;
     cfg.attrs = at;
     cfg.numAttrs = (pm & 2) ? 1 : 0;
-    if (!(pm & 4) && g_opt_pack_tma.load() > 0) {  // bulk-copy (TMA) pack
-      pack_bits_tma<<<c->sms * g_opt_pack_tma.load(), 256, kTmaSmem, s>>>(rp, c->bits.p,
+    if (!(pm & 4) && c->o.pack_tma > 0) {  // bulk-copy (TMA) pack
+      pack_bits_tma<false><<<c->sms * c->o.pack_tma, 256, kTmaSmem, s>>>(rp, c->bits.p,
                                                                       c->d_stats, c->segmap.p);
       CKL(1);
     } else if (!(pm & 4)) {  // bit 2 (debug, timing only): reuse the slot's previous bit volume
@@ -640,9 +683,9 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
 
   // Persistent grids: exactly the resident blocks, so the static round-robin
   // split of work units is also the load balance.
-  const int pgrid = lgrid(c, std::max(1, g_opt_packed.load() ? c->occ_pass1 : c->occ_pass1s));
+  const int pgrid = lgrid(c, std::max(1, c->o.packed ? c->occ_pass1 : c->occ_pass1s));
   const long long pucap = (long long)c->plane_umax.cap;
-  const int prune = g_opt_prune.load() ? 1 : 0;
+  const int prune = c->o.prune ? 1 : 0;
 
   // Orders (Morton bricks; planes by in-plane brick), chunk boxes + extremes,
   // exact lower bound, pruned 3-D work list.
@@ -661,7 +704,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   // (plane boxes -> bound -> filter) are independent: the planar one runs on
   // the slot's second stream (a fork / join inside the captured graph), so
   // the ROI's critical path is the longer chain, not their sum.
-  const bool fork = g_opt_fork.load() && lim >= (1 << 20);
+  const bool fork = c->o.fork && lim >= (1 << 20);
   cudaStream_t sp = s;
   if (fork) {
     CK(cudaEventRecord(c->fork_ev, s));
@@ -715,7 +758,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   }
   CK(record(c, c->kev[4], s));
   // One pass-1 kernel and one re-check kernel for the 3-D and the planar lists.
-  if (g_opt_packed.load())
+  if (c->o.packed)
     CK(launch_k(c, s, pgrid, 256, diam_pass1<true>, c->keys_sorted.p, dcap, rp, c->work.p,
                 c->warp_max.p, c->plane_sorted.p, c->plane_start.p, c->plane_work.p, pucap,
                 c->plane_umax.p, c->d_stats));
@@ -817,7 +860,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   h.W = (int)((nx + 31) / 32);
   h.n_words = (long long)h.W * ny * nz;
   h.n_chunks = nx * ny * nz / 16;
-  h.sparse = (g_opt_sparse.load() && !c->prepacked) ? 1 : 0;
+  h.sparse = (c->o.sparse && !c->prepacked) ? (c->o.pack_skip ? 3 : 1) : 0;
   h.f.cx2 = h.f.cy2 = h.f.cz2 = 0;  // set on the device from the bbox
   h.f.hx = (float)(0.5 * sp[0]);
   h.f.hy = (float)(0.5 * sp[1]);
@@ -835,19 +878,19 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
     CK(cudaMemcpyAsync(c->d_rp, c->h_rp, sizeof(RoiParams), cudaMemcpyHostToDevice, s));
   if (hp) { const double t1 = wall_ms(); g_hprof.copy += t1 - t0; t0 = t1; }
   const bool fast = nx % 32 == 0 && (reinterpret_cast<uintptr_t>(d_mask) & 15) == 0;
-  if (!g_opt_graphs.load() || s == nullptr)
+  if (!c->o.graphs || s == nullptr)
     return enqueue_with_copies(c, fast, s, shard, nshards, d_sq4);
   const long long cap = (long long)c->keys.cap, dcap = c->dcap_sz;
-  const bool prune = g_opt_prune.load(), packed = g_opt_packed.load(), fbox = g_opt_fbox.load();
+  const bool prune = c->o.prune, packed = c->o.packed, fbox = c->o.fbox;
   for (auto& g : c->graphs)
     if (g.fast == fast && g.s == s && g.shard == shard && g.nshards == nshards &&
         g.d_sq4 == d_sq4 && g.cap == cap && g.dcap == dcap && g.prune == prune &&
-        g.packed == packed && g.fbox == fbox && g.stages == g_opt_stages.load() &&
-        g.packmode == g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load() + 4096 * g_opt_pack_tma.load() &&
+        g.packed == packed && g.fbox == fbox && g.stages == c->o.stages + 7 * c->o.empty &&
+        g.packmode == c->o.pack_mode + 32 * c->o.pack_bps + 4096 * c->o.pack_tma &&
         g.grid_div == c->grid_div &&
-        g.events == c->events_on && g.ev_full == c->ev_full && g.pdl == g_opt_pdl.load() &&
-        g.sparse == g_opt_sparse.load() && g.fork == g_opt_fork.load() &&
-        g.zc == g_opt_zc.load() && g.prepacked == c->prepacked &&
+        g.events == c->events_on && g.ev_full == c->ev_full && g.pdl == c->o.pdl &&
+        g.sparse == c->o.sparse && g.fork == c->o.fork &&
+        g.zc == c->o.zc && g.prepacked == c->prepacked &&
         g.gen == c->gen) {
       CK(cudaGraphLaunch(g.exec, s));
       if (hp) g_hprof.launch += wall_ms() - t0;
@@ -874,11 +917,11 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
     c->graphs.erase(c->graphs.begin());
   }
   Ctx::GraphEntry g{fast, s, shard, nshards, d_sq4, cap, dcap, prune, packed, fbox,
-                    g_opt_stages.load(),
-                    g_opt_pack_mode.load() + 32 * g_opt_pack_bps.load() + 4096 * g_opt_pack_tma.load(),
+                    c->o.stages + 7 * c->o.empty,
+                    c->o.pack_mode + 32 * c->o.pack_bps + 4096 * c->o.pack_tma,
                     c->grid_div,
-                    c->events_on, c->ev_full, g_opt_pdl.load(), g_opt_sparse.load(),
-                    g_opt_fork.load(), g_opt_zc.load(), c->prepacked, c->gen, exec, launches};
+                    c->events_on, c->ev_full, c->o.pdl, c->o.sparse,
+                    c->o.fork, c->o.zc, c->prepacked, c->gen, exec, launches};
   c->graphs.push_back(g);
   CK(cudaGraphLaunch(exec, s));
   g_launches.fetch_add(launches, std::memory_order_relaxed);
@@ -911,7 +954,7 @@ int start_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
     c->wcap_floor = std::max(c->wcap_floor, p->wunits);
   }
   long long cap = vertex_capacity(nx, ny, nz, c->cap_floor);
-  long long dcap = std::min<long long>(cap, std::max<long long>(g_opt_dcap.load(), c->dcap_floor));
+  long long dcap = std::min<long long>(cap, std::max<long long>(c->o.dcap, c->dcap_floor));
   const unsigned long long fp0 = c->fingerprint();
   int rc = ensure_buffers(c, nx, ny, nz, cap, dcap, punits, c->wcap_floor);
   if (rc) return rc;
@@ -961,6 +1004,12 @@ int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
     set_err("mask has no occupied voxels");
     return SC_ERR_EMPTY_ROI;
   }
+  if ((long long)c->h_stats->n_super > (long long)c->slist.cap) {
+    // cannot happen with slist sized from kSingleLevelMax; never report a
+    // maximum from a truncated super-pair list
+    set_err("super-pair list overflow (%llu > %zu)", c->h_stats->n_super, c->slist.cap);
+    return SC_ERR_NOMEM;
+  }
   fill_out(*c->h_stats, p->sp, out);
   c->times_pending = c->events_on && c->ev_full;  // per-stage times: from kev[] on demand
   if (!c->times_pending)
@@ -995,9 +1044,10 @@ int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, c
             const int org[3] = nullptr) {
   Pending p{};
   // single calls: mesh / diameters events (level 1), every stage (2) or none (0)
-  c->grid_div = g_opt_grid_div_single.load();
-  c->events_on = g_opt_stage_times.load() > 0;
-  c->ev_full = g_opt_stage_times.load() > 1;
+  c->grid_div = c->o.grid_div_single;
+  c->o.pack_tma = c->o.pack_tma_single;
+  c->events_on = c->o.stage_times > 0;
+  c->ev_full = c->o.stage_times > 1;
   int rc = start_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, 0, &p, org);
   if (rc) return rc;
   return finish_roi(c, &p, out);
@@ -1043,8 +1093,9 @@ void note_host_rates(const Ctx* c, int64_t total_bytes, double h2d_ms) {
 // With s the slab fraction of the previous ROI, (1 - f)/Rc = (f + s)/Rp gives
 // f = (Rp/Rc - s) / (1 + Rp/Rc); f = 0 when the slab alone already keeps PCIe
 // busier than the scan (e.g. C3), and until both rates have been measured.
-int64_t split_slices(int device, int64_t nz) {
-  const int pct = g_opt_split.load();
+int64_t split_slices(const Ctx* c, int64_t nz) {
+  const int device = c->device;
+  const int pct = c->o.split;
   if (pct == 0 || nz < 8) return 0;
   double f;
   if (pct > 0) {
@@ -1065,7 +1116,7 @@ int64_t split_slices(int device, int64_t nz) {
 // when the raw slab would keep PCIe busier than the host scan took, i.e. the
 // link, not the host, would bound the ROI -- C3-like ROIs with large slabs).
 bool pack_on_host(const Ctx* c, double slab_bytes, double scan_ms) {
-  const int mode = g_opt_host_pack.load();
+  const int mode = c->o.host_pack;
   if (mode >= 0) return mode == 1;
   HostRates& r = host_rates(c->device);
   std::lock_guard<std::mutex> lk(r.mu);
@@ -1082,7 +1133,7 @@ int stage_host_mask(Ctx* c, const uint8_t* mask, int64_t nx, int64_t ny, int64_t
   const uint8_t* src = mask;
   const size_t S = (size_t)nx * ny;  // bytes per slice
   c->prepacked = false;
-  const int64_t a = g_opt_crop.load() ? split_slices(c->device, nz) : 0;
+  const int64_t a = c->o.crop ? split_slices(c, nz) : 0;
   if (a > 0) {
     // Split read: slices [0, a) cross PCIe whole while the host scans [a, nz)
     // for its occupied slab; the device volume is slices [0, Z1] with every
@@ -1090,7 +1141,7 @@ int stage_host_mask(Ctx* c, const uint8_t* mask, int64_t nx, int64_t ny, int64_t
     CK(cudaEventRecord(c->ev[0], s));
     CK(cudaMemcpyAsync(c->mask_stage.p, mask, a * S, cudaMemcpyHostToDevice, s));
     const double t0 = wall_ms();
-    const Slab sl = occupied_slab(mask + a * S, nx, ny, nz - a, g_opt_host_threads.load());
+    const Slab sl = occupied_slab(mask + a * S, nx, ny, nz - a, c->o.host_threads);
     c->last_scan_ms = c->last_pure_scan_ms = wall_ms() - t0;
     size_t bytes = a * S;
     int64_t Z1 = a - 1;
@@ -1114,9 +1165,9 @@ int stage_host_mask(Ctx* c, const uint8_t* mask, int64_t nx, int64_t ny, int64_t
     return SC_OK;
   }
   c->last_split = false;
-  if (g_opt_crop.load()) {
+  if (c->o.crop) {
     const double t0 = wall_ms();
-    const int th = g_opt_host_threads.load();
+    const int th = c->o.host_threads;
     const Slab sl = occupied_slab(mask, nx, ny, nz, th);
     c->last_scan_ms = c->last_pure_scan_ms = wall_ms() - t0;
     c->last_scan_bytes = sl.bytes_read;
@@ -1187,7 +1238,8 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
     return SC_ERR_INPUT;
   }
   if (count == 0) return SC_OK;
-  const int nslots = std::max(1, std::min<int>(kSlots, g_opt_slots.load()));
+  const Opts opts = snapshot_opts();  // one snapshot for the whole batch
+  const int nslots = std::max(1, std::min<int>(kSlots, opts.slots));
   Ctx* cs[kSlots] = {};
   for (int k = 0; k < nslots; k++) {
     int rc = get_ctx(device, &cs[k], k);
@@ -1202,11 +1254,15 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
     ~EventsMode() { for (int k = 0; k < n; k++) cs[k]->events_on = cs[k]->ev_full = true; }
   } events_mode{cs, nslots};
   for (int k = 0; k < nslots; k++) {
-    cs[k]->events_on = cs[k]->ev_full = g_opt_batch_times.load();
-    cs[k]->grid_div = g_opt_grid_div.load();
+    cs[k]->o = opts;
+    cs[k]->events_on = cs[k]->ev_full = opts.batch_times;
+    cs[k]->grid_div = opts.grid_div;
   }
   CK(cudaSetDevice(device));
-  if (user) {  // order the batch after prior work on the caller's stream
+  // Device masks: order the batch after prior work on the caller's stream;
+  // NULL is the legacy default stream (the slot streams are non-blocking).
+  if (!host && !user) user = cudaStreamLegacy;
+  if (user) {
     CK(cudaEventRecord(cs[0]->ev[4], user));
     for (int k = 0; k < nslots; k++) CK(cudaStreamWaitEvent(cs[k]->stream, cs[0]->ev[4], 0));
   }
@@ -1226,7 +1282,7 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
         const unsigned long long fp0 = c->fingerprint();
         const long long cap = vertex_capacity(mx, my, mz, c->cap_floor);
         const long long dcap =
-            std::min<long long>(cap, std::max<long long>(g_opt_dcap.load(), c->dcap_floor));
+            std::min<long long>(cap, std::max<long long>(c->o.dcap, c->dcap_floor));
         int rc = ensure_buffers(c, mx, my, mz, cap, dcap, 0, c->wcap_floor);
         if (rc) return rc;
         if (c->fingerprint() != fp0) {
@@ -1261,6 +1317,15 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
     o->total_ms = wall_ms() - t_start[k];
     idx[k] = -1;
   };
+  // Every exit path (an early CK return included) collects the ROIs still in
+  // flight before the slot locks are released: their out[] entries get
+  // written and no slot's pinned RoiParams is rewritten under a running ROI.
+  struct DrainGuard {
+    std::function<void()> f;
+    ~DrainGuard() { f(); }
+  } drain{[&] {
+    for (int64_t i = 0; i < nslots; i++) collect((int)((count + i) % nslots));
+  }};
   for (int64_t i = 0; i < count; i++) {
     const int k = (int)(i % nslots);
     collect(k);
@@ -1290,7 +1355,7 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
     if (rc) { note(rc); continue; }
     idx[k] = i;
   }
-  for (int64_t i = 0; i < nslots; i++) collect((int)((count + i) % nslots));
+  drain.f();
   if (user) {  // ... and later work on it after the batch
     for (int k = 0; k < nslots; k++) {
       CK(cudaEventRecord(cs[k]->ev[5], cs[k]->stream));
@@ -1443,6 +1508,39 @@ int current_ctx(Ctx** c) {
   return get_ctx(dev, c);
 }
 
+// One option into `o` (sc_set_option / sc_set_thread_option).
+int set_opt(Opts& o, const char* name, int value) {
+  if (!name) { set_err("NULL option name"); return SC_ERR_INPUT; }
+  if (std::strcmp(name, "prune") == 0) o.prune = value != 0;
+  else if (std::strcmp(name, "pass1_packed") == 0) o.packed = value != 0;
+  else if (std::strcmp(name, "graphs") == 0) o.graphs = value != 0;
+  else if (std::strcmp(name, "slots") == 0) o.slots = std::max(1, std::min(32, value));
+  else if (std::strcmp(name, "dcap") == 0) o.dcap = std::max(256, value);
+  else if (std::strcmp(name, "wcap") == 0) o.wcap = std::max(1, value);
+  else if (std::strcmp(name, "fused_bbox") == 0) o.fbox = value != 0;
+  else if (std::strcmp(name, "host_crop") == 0) o.crop = value != 0;
+  else if (std::strcmp(name, "host_pack") == 0) o.host_pack = std::max(-1, std::min(1, value));
+  else if (std::strcmp(name, "host_split") == 0) o.split = std::max(-1, std::min(90, value));
+  else if (std::strcmp(name, "pack_mode") == 0) o.pack_mode = value & 7;
+  else if (std::strcmp(name, "pack_bps") == 0) o.pack_bps = std::max(0, value);
+  else if (std::strcmp(name, "grid_div") == 0) o.grid_div = std::max(1, value);
+  else if (std::strcmp(name, "grid_div_single") == 0) o.grid_div_single = std::max(1, value);
+  else if (std::strcmp(name, "pdl") == 0) o.pdl = value != 0;
+  else if (std::strcmp(name, "fork") == 0) o.fork = value != 0;
+  else if (std::strcmp(name, "zero_copy") == 0) o.zc = value != 0;
+  else if (std::strcmp(name, "stage_times") == 0) o.stage_times = std::max(0, std::min(2, value));
+  else if (std::strcmp(name, "pack_tma") == 0) o.pack_tma = std::max(0, std::min(3, value));
+  else if (std::strcmp(name, "pack_tma_single") == 0) o.pack_tma_single = std::max(0, std::min(3, value));
+  else if (std::strcmp(name, "sparse_bits") == 0) o.sparse = value != 0;
+  else if (std::strcmp(name, "pack_skip") == 0) o.pack_skip = value != 0;
+  else if (std::strcmp(name, "batch_stage_times") == 0) o.batch_times = value != 0;
+  else if (std::strcmp(name, "host_threads") == 0) o.host_threads = std::max(1, value);
+  else if (std::strcmp(name, "debug_empty") == 0) o.empty = std::max(0, value);
+  else if (std::strcmp(name, "debug_stages") == 0) o.stages = value > 0 ? value : (1 << 30);
+  else { set_err("unknown option %s", name); return SC_ERR_INPUT; }
+  return SC_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1474,7 +1572,15 @@ int sc_calculate_coefficients_shard(const uint8_t* d_mask, int64_t nx, int64_t n
   Ctx* c;
   if ((rc = current_ctx(&c))) return rc;
   std::lock_guard<std::mutex> lk(c->mu);
+  c->o = snapshot_opts();
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  if (!stream) {
+    // NULL = the legacy default stream (also torch's default stream): the
+    // slot stream is non-blocking, so order the ROI after prior work on it
+    // explicitly (the call is synchronous, so later work is ordered anyway).
+    CK(cudaEventRecord(c->ev[4], cudaStreamLegacy));
+    CK(cudaStreamWaitEvent(s, c->ev[4], 0));
+  }
   std::memset(out, 0, sizeof *out);
   c->prepacked = false;
   rc = run_roi(c, d_mask, nx, ny, nz, spacing, s, shard, nshards, d_sq4, out);
@@ -1491,6 +1597,7 @@ int sc_calculate_coefficients(const uint8_t* mask, int64_t nx, int64_t ny, int64
   Ctx* c;
   if ((rc = get_ctx(device, &c))) return rc;
   std::lock_guard<std::mutex> lk(c->mu);
+  c->o = snapshot_opts();
   CK(cudaSetDevice(device));
   std::memset(out, 0, sizeof *out);
   CK(c->mask_stage.ensure((size_t)nx * ny * nz));
@@ -1526,6 +1633,7 @@ int sc_calculate_coefficients_raw(const void* data, int dtype, const int64_t sha
   Ctx* c;
   if ((rc = get_ctx(device, &c))) return rc;
   std::lock_guard<std::mutex> lk(c->mu);
+  c->o = snapshot_opts();
   CK(cudaSetDevice(device));
   std::memset(out, 0, sizeof *out);
   const size_t n = (size_t)nx * ny * nz, raw_bytes = n * itemsize[dtype];
@@ -1574,6 +1682,7 @@ int sc_diameters(const double* xs, const double* ys, const double* zs, int64_t n
   int rc = get_ctx(device, &c);
   if (rc) return rc;
   std::lock_guard<std::mutex> lk(c->mu);
+  c->o = snapshot_opts();
   CK(cudaSetDevice(device));
   cudaStream_t s = c->stream;
   CK(c->cloud.ensure((size_t)(3 * n)));
@@ -1582,10 +1691,11 @@ int sc_diameters(const double* xs, const double* ys, const double* zs, int64_t n
   CK(cudaMemcpyAsync(c->cloud.p + n, ys, n * 8, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(c->cloud.p + 2 * n, zs, n * 8, cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(c->cloud_out.p, 0, 32, s));
-  const long long T = (n + 255) / 256;
-  cloud_diameters<<<(unsigned)(T * (T + 1) / 2), 256, 0, s>>>(c->cloud.p, c->cloud.p + n,
-                                                               c->cloud.p + 2 * n, n, (int)T,
-                                                               c->cloud_out.p);
+  const long long T = (n + 255) / 256;  // 256-point tiles; T(T+1)/2 tile pairs, grid-stride
+  const long long units = T * (T + 1) / 2;
+  const unsigned grid = (unsigned)std::min<long long>(units, (long long)c->sms * 8);
+  cloud_diameters<<<grid, 256, 0, s>>>(c->cloud.p, c->cloud.p + n, c->cloud.p + 2 * n, n, T,
+                                       c->cloud_out.p);
   CKL(1);
   unsigned long long hb[4];
   CK(cudaMemcpyAsync(hb, c->cloud_out.p, 32, cudaMemcpyDeviceToHost, s));
@@ -1604,6 +1714,7 @@ int sc_marching_cubes(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz,
   Ctx* c;
   if ((rc = get_ctx(device, &c))) return rc;
   std::lock_guard<std::mutex> lk(c->mu);
+  c->o = snapshot_opts();
   CK(cudaSetDevice(device));
   const size_t bytes = (size_t)nx * ny * nz;
   CK(c->mask_stage.ensure(bytes));
@@ -1625,6 +1736,7 @@ int sc_mesh_measure(const double* xs, const double* ys, const double* zs, int64_
   int rc = get_ctx(device, &c);
   if (rc) return rc;
   std::lock_guard<std::mutex> lk(c->mu);
+  c->o = snapshot_opts();
   CK(cudaSetDevice(device));
   cudaStream_t s = c->stream;
   long long padded = 1;
@@ -1664,6 +1776,7 @@ int sc_mesh_vertices(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, in
   Ctx* c;
   if ((rc = get_ctx(device, &c))) return rc;
   std::lock_guard<std::mutex> lk(c->mu);
+  c->o = snapshot_opts();
   CK(cudaSetDevice(device));
   const size_t bytes = (size_t)nx * ny * nz;
   CK(c->mask_stage.ensure(bytes));
@@ -1696,6 +1809,7 @@ int sc_last_kernel_times(int device, double* ms, int n) {
   int rc = get_ctx(device, &c);
   if (rc) return -rc;
   std::lock_guard<std::mutex> lk(c->mu);
+  c->o = snapshot_opts();
   if (c->times_pending) {
     // pack, mc, prune (sort + 3-D filter), pass 1 (3-D + planar), re-check
     // (both), planar prep (runs beside the 3-D filter when forked)
@@ -1717,7 +1831,7 @@ int sc_occupied_slab(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, in
     return SC_ERR_INPUT;
   }
   const Slab sl = occupied_slab(mask, nx, ny, nz,
-                                threads > 0 ? threads : g_opt_host_threads.load());
+                                threads > 0 ? threads : snapshot_opts().host_threads);
   if (sl.empty) {
     set_err("mask has no occupied voxels");
     return SC_ERR_EMPTY_ROI;
@@ -1731,39 +1845,34 @@ int sc_last_diagnostics(int device, int64_t* out, int n) {
   int rc = get_ctx(device, &c);
   if (rc) return -rc;
   std::lock_guard<std::mutex> lk(c->mu);
+  c->o = snapshot_opts();
   int m = n < 8 ? n : 8;
   for (int i = 0; i < m; i++) out[i] = c->last_diag[i];
   return m;
 }
 
 int sc_set_option(const char* name, int value) {
-  if (!name) { set_err("NULL option name"); return SC_ERR_INPUT; }
-  if (std::strcmp(name, "prune") == 0) g_opt_prune = value != 0;
-  else if (std::strcmp(name, "pass1_packed") == 0) g_opt_packed = value != 0;
-  else if (std::strcmp(name, "graphs") == 0) g_opt_graphs = value != 0;
-  else if (std::strcmp(name, "slots") == 0) g_opt_slots = value;
-  else if (std::strcmp(name, "dcap") == 0) g_opt_dcap = std::max(256, value);
-  else if (std::strcmp(name, "wcap") == 0) g_opt_wcap = std::max(1, value);
-  else if (std::strcmp(name, "fused_bbox") == 0) g_opt_fbox = value != 0;
-  else if (std::strcmp(name, "host_crop") == 0) g_opt_crop = value != 0;
-  else if (std::strcmp(name, "host_pack") == 0) g_opt_host_pack = std::max(-1, std::min(1, value));
-  else if (std::strcmp(name, "host_split") == 0) g_opt_split = std::max(-1, std::min(90, value));
-  else if (std::strcmp(name, "pack_mode") == 0) g_opt_pack_mode = value & 7;
-  else if (std::strcmp(name, "pack_bps") == 0) g_opt_pack_bps = std::max(0, value);
-  else if (std::strcmp(name, "grid_div") == 0) g_opt_grid_div = std::max(1, value);
-  else if (std::strcmp(name, "grid_div_single") == 0) g_opt_grid_div_single = std::max(1, value);
-  else if (std::strcmp(name, "pdl") == 0) g_opt_pdl = value != 0;
-  else if (std::strcmp(name, "fork") == 0) g_opt_fork = value != 0;
-  else if (std::strcmp(name, "zero_copy") == 0) g_opt_zc = value != 0;
-  else if (std::strcmp(name, "stage_times") == 0) g_opt_stage_times = std::max(0, std::min(2, value));
-  else if (std::strcmp(name, "pack_tma") == 0) g_opt_pack_tma = std::max(0, std::min(3, value));
-  else if (std::strcmp(name, "sparse_bits") == 0) g_opt_sparse = value != 0;
-  else if (std::strcmp(name, "batch_stage_times") == 0) g_opt_batch_times = value != 0;
-  else if (std::strcmp(name, "host_threads") == 0) g_opt_host_threads = std::max(1, value);
-  else if (std::strcmp(name, "debug_stages") == 0) g_opt_stages = value > 0 ? value : (1 << 30);
-  else { set_err("unknown option %s", name); return SC_ERR_INPUT; }
-  return SC_OK;
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  return set_opt(g_opts, name, value);
 }
+
+int sc_set_thread_option(const char* name, int value) {
+  if (!t_opts_on) {
+    Opts o;
+    {
+      std::lock_guard<std::mutex> lk(g_opt_mu);
+      o = g_opts;
+    }
+    int rc = set_opt(o, name, value);
+    if (rc) return rc;
+    t_opts = o;
+    t_opts_on = true;
+    return SC_OK;
+  }
+  return set_opt(t_opts, name, value);
+}
+
+void sc_clear_thread_options(void) { t_opts_on = false; }
 
 int sc_probe_fp32_peak(int device, int mode, double* tflops) {
   if (!tflops) { set_err("NULL argument"); return SC_ERR_INPUT; }
@@ -1771,6 +1880,7 @@ int sc_probe_fp32_peak(int device, int mode, double* tflops) {
   int rc = get_ctx(device, &c);
   if (rc) return rc;
   std::lock_guard<std::mutex> lk(c->mu);
+  c->o = snapshot_opts();
   CK(cudaSetDevice(device));
   cudaStream_t s = c->stream;
   float* d_out;

@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(256) pack_bits_v16(const RoiParams* __restrict
   const long long n_chunks = rp->n_chunks;
   const unsigned int W = (unsigned int)rp->W, ny = (unsigned int)rp->ny;
   const bool sparse = rp->sparse != 0;
+  const bool skip = (rp->sparse & 2) != 0;  // option "pack_skip"
   BoxAcc box;
   const long long step = (long long)gridDim.x * blockDim.x * U;
   for (long long base = (long long)blockIdx.x * blockDim.x * U; base < n_chunks; base += step) {
@@ -132,11 +133,15 @@ __global__ void __launch_bounds__(256) pack_bits_v16(const RoiParams* __restrict
 #pragma unroll
     for (int k = 0; k < U; k++) {
       const long long g = base + (long long)k * blockDim.x + threadIdx.x;
+      // Sparse: an all-background 512-byte segment (most of a KiTS-like grid)
+      // costs 2 LOP3 + 1 vote here and no conversion at all, so the pack
+      // leaves the SMs' issue slots to the other ROIs' latency-bound kernels.
+      // (out-of-range chunks were loaded as zero)
+      if (skip && !__any_sync(kFull, (v[k].x | v[k].y | v[k].z | v[k].w) != 0u)) continue;
       const uint32_t b16 = nib4(v[k].x) | (nib4(v[k].y) << 4) | (nib4(v[k].z) << 8) |
                            (nib4(v[k].w) << 12);
       const uint32_t word = b16 | (__shfl_down_sync(kFull, b16, 1) << 16);
       if (sparse) {
-        if (!__any_sync(kFull, word != 0u && !(threadIdx.x & 1) && g < n_chunks)) continue;
         if ((threadIdx.x & 31) == 0) {
           const long long seg = g >> 5;  // lane 0 holds the segment's first chunk
           atomicOr(segmap + (seg >> 5), 1u << (seg & 31));
@@ -201,6 +206,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   }
 }
 
+template <bool BOX>
 __global__ void __launch_bounds__(256, 1) pack_bits_tma(const RoiParams* __restrict__ rp,
                                                        uint32_t* __restrict__ bits,
                                                        Stats* __restrict__ st,
@@ -210,13 +216,16 @@ __global__ void __launch_bounds__(256, 1) pack_bits_tma(const RoiParams* __restr
   const unsigned char* mask = rp->mask;
   const long long n_bytes = 16LL * rp->n_chunks;
   const bool sparse = rp->sparse != 0;
+  const bool skip = (rp->sparse & 2) != 0;
+  const unsigned int W = (unsigned int)rp->W, ny = (unsigned int)rp->ny;
+  BoxAcc box;  // BOX: occupied bbox of the nonzero words (replaces bits_bbox)
   // contiguous share per CTA, a multiple of the tile size
   const long long per =
       ((n_bytes + gridDim.x - 1) / gridDim.x + kTmaTile - 1) / kTmaTile * kTmaTile;
   const long long beg = min(n_bytes, (long long)blockIdx.x * per);
   const long long end = min(n_bytes, beg + per);
   const int tiles = (int)((end - beg + kTmaTile - 1) / kTmaTile);
-  if (tiles <= 0) return;  // block-uniform
+  if (tiles <= 0) return;  // block-uniform (no box to flush)
   uint64_t policy;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
   if (threadIdx.x == 0) {
@@ -240,12 +249,28 @@ __global__ void __launch_bounds__(256, 1) pack_bits_tma(const RoiParams* __restr
     const long long g0 = (beg + (long long)t * kTmaTile) / 16;  // first chunk of the tile
     const long long gend = end / 16;
     const uint4* tile = reinterpret_cast<const uint4*>(s_tiles + s * kTmaTile);
+    // Only the last tile can be partial: bytes past `end` in its stage are stale.
+    const bool full = t + 1 < tiles || (end - beg) % kTmaTile == 0;
+    uint4 v[kK];
+    uint32_t any = 0u;
+#pragma unroll
+    for (int k = 0; k < kK; k++) {
+      const int ci = k * 256 + threadIdx.x;
+      v[k] = tile[ci];
+      if (!full && g0 + ci >= gend) v[k] = make_uint4(0u, 0u, 0u, 0u);
+      any |= v[k].x | v[k].y | v[k].z | v[k].w;
+    }
+    // Sparse: one vote clears the warp's kK segments (2 KB) at once when they
+    // are all background -- most of a KiTS-like grid -- so the pack costs ~15
+    // issue slots per 2 KB there and leaves the SMs to other ROIs' kernels.
+    if (!skip || __any_sync(kFull, any != 0u)) {
 #pragma unroll
     for (int k = 0; k < kK; k++) {
       const int ci = k * 256 + threadIdx.x;
       const long long g = g0 + ci;
-      const uint4 v = g < gend ? tile[ci] : make_uint4(0u, 0u, 0u, 0u);
-      const uint32_t b16 = nib4(v.x) | (nib4(v.y) << 4) | (nib4(v.z) << 8) | (nib4(v.w) << 12);
+      if (skip && !__any_sync(kFull, (v[k].x | v[k].y | v[k].z | v[k].w) != 0u)) continue;
+      const uint32_t b16 = nib4(v[k].x) | (nib4(v[k].y) << 4) | (nib4(v[k].z) << 8) |
+                           (nib4(v[k].w) << 12);
       const uint32_t word = b16 | (__shfl_down_sync(kFull, b16, 1) << 16);
       if (sparse) {
         if (!__any_sync(kFull, word != 0u && !(threadIdx.x & 1) && g < gend)) continue;
@@ -254,12 +279,26 @@ __global__ void __launch_bounds__(256, 1) pack_bits_tma(const RoiParams* __restr
           atomicOr(segmap + (seg >> 5), 1u << (seg & 31));
         }
       }
-      if (!(threadIdx.x & 1) && g < gend) bits[g >> 1] = word;
+      if (!(threadIdx.x & 1) && g < gend) {
+        bits[g >> 1] = word;
+        if (BOX && word) {
+          const unsigned int wi = (unsigned int)(g >> 1), row = wi / W, col = wi - row * W;
+          const unsigned int z = row / ny, y = row - z * ny;
+          box.x0 = min(box.x0, (int)(32 * col) + __ffs(word) - 1);
+          box.x1 = max(box.x1, (int)(32 * col) + 31 - __clz(word));
+          box.y0 = min(box.y0, (int)y); box.y1 = max(box.y1, (int)y);
+          box.z0 = min(box.z0, (int)z); box.z1 = max(box.z1, (int)z);
+        }
+      }
+    }
     }
     __syncthreads();  // every thread is done with stage s
     if (threadIdx.x == 0 && t + kTmaStages < tiles) issue(t + kTmaStages);
   }
+  if (BOX) box.flush(st);
 }
+template __global__ void pack_bits_tma<false>(const RoiParams*, uint32_t*, Stats*, uint32_t*);
+template __global__ void pack_bits_tma<true>(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 
 // Occupied bbox from the bit volume (L2-resident right after the pack): only
 // nonzero words locate themselves.  Four 16-byte loads in flight per thread.

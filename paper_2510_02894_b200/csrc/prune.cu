@@ -23,11 +23,10 @@ namespace sc {
 constexpr int kChunkV = kChunk3;
 constexpr int kPerLane = kChunkV / 32;
 constexpr int kSuper = 8;  // super-chunk = 8 chunks (1024 vertices): first level of unit_filter
-// Chunk pairs tested directly (one level) up to this many; above it the
-// super-chunk level goes first.  Two levels pay off from ~300 chunks on (C2
-// batch 42.5 -> 41.8 us/ROI, C5 30.9 -> 27.8 moving the switch from 2^22 to
-// 2^16 pairs): fewer warp-slot microseconds per ROI in the pipelined batch.
-constexpr long long kSingleLevelMax = 1LL << 16;
+// kSingleLevelMax (sc_device.cuh): chunk pairs tested directly (one level) up
+// to this many; above it the super-chunk level goes first.  Two levels pay off
+// from ~300 chunks on (C2 batch 42.5 -> 41.8 us/ROI, C5 30.9 -> 27.8 moving the
+// switch from 2^22 to 2^16 pairs): fewer warp-slot microseconds per ROI.
 constexpr int kNDir = 13;
 
 __device__ __forceinline__ long long n_verts(const Stats* st, long long cap) {

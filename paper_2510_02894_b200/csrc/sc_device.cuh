@@ -51,6 +51,11 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
+// 3-D chunk pairs (128 x 128 vertices) tested directly by unit_filter up to
+// this many; above it the 1024-vertex super pairs are listed first (slist)
+// and expanded by unit_expand.  The host sizes slist from the same constant.
+constexpr long long kSingleLevelMax = 1LL << 16;
+
 // Work entries carry, in the top 4 bits of the J field, which 64 x 64 sub-pairs
 // of the 128 x 128 chunk pair can reach the lower bound (bit 2a + b: I half a,
 // J half b); pass 1 evaluates only those.  0xF = the whole unit.
@@ -100,9 +105,10 @@ struct RoiParams {
   long long n_chunks;  // nx*ny*nz/16 (fast pack path)
   long long n_words;   // W*ny*nz
   int W;               // 32-bit words per bit-volume row
-  int sparse;          // 1: the pack writes only nonzero 16-word segments of the bit
+  int sparse;          // bit 0: the pack writes only nonzero 16-word segments of the bit
                        // volume and marks them in the segment map; readers treat
-                       // unmarked segments as zero (0: every word is written)
+                       // unmarked segments as zero (0: every word is written); bit 1:
+                       // the pack skips the conversion of all-zero segments
   Frame f;             // cx2..cz2 are filled on the device from the bbox
   long long wcap;      // capacity of the 3-D work list (overflow -> exact re-run)
 };

@@ -133,15 +133,16 @@ def _as_mask(mask) -> Tuple[np.ndarray, Tuple[int, int, int]]:
     return arr.reshape(-1), (nx, ny, nz)
 
 
-def calculate_coefficients(mask, spacing: Sequence[float] = (1.0, 1.0, 1.0),
+def calculate_coefficients(mask, spacing: Optional[Sequence[float]] = None,
                            device: int = 0) -> Coefficients:
     """Full shape coefficients of a host mask ((nz, ny, nx) array or MaskVolume).
 
+    `spacing` defaults to the MaskVolume's own spacing, else (1, 1, 1) mm.
     Raises EmptyRoi for an all-background mask and NonPositiveSpacing for a
     bad spacing, as the reference does (mesh.py:78-79, volume.py:94-101).
     """
-    if isinstance(mask, MaskVolume) and spacing is None:
-        spacing = mask.spacing
+    if spacing is None:
+        spacing = mask.spacing if isinstance(mask, MaskVolume) else (1.0, 1.0, 1.0)
     sp = np.asarray(_check_spacing(spacing), dtype=np.float64)
     data, (nx, ny, nz) = _as_mask(mask)
     lib = _native.load()
@@ -153,14 +154,25 @@ def calculate_coefficients(mask, spacing: Sequence[float] = (1.0, 1.0, 1.0),
     return _from_struct(out)
 
 
+def _stream_handle(tensor, stream) -> int:
+    """cudaStream_t of `stream`, default torch's current stream on the tensor's
+    device (0 = the legacy default stream, which the library orders against)."""
+    if stream is None:
+        import torch
+
+        stream = torch.cuda.current_stream(tensor.device)
+    return int(stream.cuda_stream)
+
+
 def calculate_coefficients_device(mask, spacing: Sequence[float], stream=None) -> Coefficients:
     """Coefficients of a device-resident mask: a CUDA uint8 tensor (nz, ny, nx)
-    on the current device (torch is plumbing only: pointer + stream)."""
+    on the current device (torch is plumbing only: pointer + stream), ordered
+    after prior work on `stream` (default: torch's current stream)."""
     sp = np.asarray(_check_spacing(spacing), dtype=np.float64)
     nz, ny, nx = (int(d) for d in mask.shape)
     if not mask.is_contiguous():
         raise ValueError("device mask must be contiguous")
-    handle = 0 if stream is None else int(stream.cuda_stream)
+    handle = _stream_handle(mask, stream)
     out = _native.ScCoeffs()
     rc = _native.load().sc_calculate_coefficients_device(
         ctypes.c_void_p(mask.data_ptr()), nx, ny, nz,
@@ -178,7 +190,7 @@ def calculate_coefficients_shard(mask, spacing: Sequence[float], shard: int, nsh
     squared maxima (3d, xy, xz, yz) for an all_reduce(MAX) across ranks."""
     sp = np.asarray(_check_spacing(spacing), dtype=np.float64)
     nz, ny, nx = (int(d) for d in mask.shape)
-    handle = 0 if stream is None else int(stream.cuda_stream)
+    handle = _stream_handle(mask, stream)
     out = _native.ScCoeffs()
     rc = _native.load().sc_calculate_coefficients_shard(
         ctypes.c_void_p(mask.data_ptr()), nx, ny, nz,
@@ -223,7 +235,7 @@ def calculate_coefficients_device_batch(masks: Sequence, spacings: Sequence[Sequ
         if not m.is_contiguous():
             raise ValueError("device masks must be contiguous")
     outs = (_native.ScCoeffs * n)()
-    handle = 0 if stream is None else int(stream.cuda_stream)
+    handle = _stream_handle(masks[0], stream) if n else 0
     rc = _native.load().sc_calculate_coefficients_device_batch(
         ptrs, dims.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
         sp.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), n, ctypes.c_void_p(handle), outs)

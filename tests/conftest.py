@@ -55,6 +55,13 @@ def rel_err(a, b):
     return abs(a - b) / max(abs(b), 1e-300)
 
 
+@pytest.fixture(scope="session")
+def sc():
+    import paper_2510_02894_b200 as pkg
+
+    return pkg
+
+
 @pytest.fixture
 def cuda_device():
     torch = pytest.importorskip("torch")

@@ -23,13 +23,6 @@ DIAM_KEYS = ("Maximum3DDiameter", "Maximum2DDiameterXY", "Maximum2DDiameterXZ",
              "Maximum2DDiameterYZ")
 
 
-@pytest.fixture(scope="module")
-def sc():
-    import paper_2510_02894_b200 as pkg
-
-    return pkg
-
-
 def assert_matches(got, want_features, triangles, active, label=""):
     rec = got.to_dict()
     assert rec["VertexCount"] == want_features["VertexCount"], label
@@ -242,17 +235,11 @@ def test_pruning_and_pass1_variants_identical(sc, golden, golden_arrays, cuda_de
     cases.append((synth.thin_slab(), (0.5, 0.5, 5.0)))
     cases.append((synth.kits_like(tumor_mm=60.0), (0.8, 0.8, 1.0)))
     base = [sc.calculate_coefficients(a, sp).to_dict() for a, sp in cases]
-    try:
-        for opt, val in (("prune", 0), ("pass1_packed", 0), ("graphs", 0), ("fused_bbox", 0)):
-            _native.set_option(opt, val)
+    for opt, val in (("prune", 0), ("pass1_packed", 0), ("graphs", 0), ("fused_bbox", 0),
+                     ("pack_skip", 0), ("pack_tma_single", 1)):
+        with _native.thread_options(**{opt: val}):
             for (a, sp), want in zip(cases, base):
                 assert sc.calculate_coefficients(a, sp).to_dict() == want, opt
-            _native.set_option(opt, 1)
-    finally:
-        _native.set_option("prune", 1)
-        _native.set_option("pass1_packed", 1)
-        _native.set_option("graphs", 1)
-        _native.set_option("fused_bbox", 1)
     _native.set_option("prune", 1)
     sc.calculate_coefficients(cases[-1][0], cases[-1][1])
     d = _native.last_diagnostics(cuda_device)
@@ -273,21 +260,15 @@ def test_batch_launch_options_identical(sc, golden, golden_arrays, cuda_device):
     want = [sc.calculate_coefficients(a, sp).to_dict() for a, sp in cases]
     ds = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a, _ in cases]
     sps = [sp for _, sp in cases]
-    defaults = {"grid_div": 5, "pdl": 0, "batch_stage_times": 0, "slots": 16, "pack_mode": 0,
-                "sparse_bits": 1, "fork": 1, "pack_tma": 0, "zero_copy": 1}
-    try:
-        for opt, val in (("grid_div", 1), ("grid_div", 2), ("pdl", 1), ("batch_stage_times", 1),
-                         ("slots", 8), ("slots", 1), ("pack_mode", 3), ("sparse_bits", 0),
-                         ("fork", 0), ("pack_tma", 1), ("pack_tma", 2), ("zero_copy", 0)):
-            _native.set_option(opt, val)
+    for opt, val in (("grid_div", 1), ("grid_div", 2), ("pdl", 1), ("batch_stage_times", 1),
+                     ("slots", 8), ("slots", 1), ("pack_mode", 3), ("sparse_bits", 0),
+                     ("fork", 0), ("pack_tma", 0), ("pack_tma", 2), ("zero_copy", 0),
+                     ("fused_bbox", 0), ("pack_skip", 0)):
+        with _native.thread_options(**{opt: val}):
             got = sc.calculate_coefficients_device_batch(ds * 2, sps * 2)
             assert [g.to_dict() for g in got] == want * 2, (opt, val)
             got = sc.calculate_coefficients_batch([a for a, _ in cases], sps)
             assert [g.to_dict() for g in got] == want, (opt, val)
-            _native.set_option(opt, defaults[opt])
-    finally:
-        for k, v in defaults.items():
-            _native.set_option(k, v)
 
 
 def test_graph_replay_sees_new_mask_contents(sc, cuda_device):
@@ -617,3 +598,35 @@ def test_stage_times_from_device_timestamps(sc, cuda_device):
     assert recs[0] == recs[1] == recs[2]
     outs = sc.calculate_coefficients_batch([arr] * 4, [(0.8, 0.8, 1.0)] * 4)
     assert all(o.mesh_ms > 0 and o.diameters_ms > 0 for o in outs)
+
+
+def test_two_level_filter_list_sized_for_every_super_pair(sc, cuda_device):
+    """with a small diameter-side capacity (option dcap) the ROI
+    is re-run with exact sizes; its super-pair list must still hold every
+    super pair the two-level filter can list (pruning off lists them all),
+    or the maximum pair could be skipped silently."""
+    from paper_2510_02894_b200 import _native, synth
+
+    a = synth.kits_like(512, 512, 300, (0.8, 0.8, 1.0), 45.0)  # C(C+1)/2 in (2^16, 2^22]
+    want = sc.calculate_coefficients(a, (0.8, 0.8, 1.0)).to_dict()
+    for opts in ({"dcap": 256, "prune": 0}, {"dcap": 256}, {"dcap": 4096, "prune": 0}):
+        with _native.thread_options(**opts):
+            got = sc.calculate_coefficients(a, (0.8, 0.8, 1.0)).to_dict()
+        assert got == want, opts
+
+
+def test_cloud_diameters_grid_covers_every_tile_pair(sc, cuda_device):
+    """sc_diameters walks the T(T+1)/2 tile pairs with a bounded,
+    grid-stride launch (SMs x 8 blocks); a cloud of 2^20 points (4096 tiles,
+    8.4e6 tile pairs, ~7 K per block) whose extreme pair sits in the last
+    tile must still be found."""
+    rng = np.random.default_rng(5)
+    n = 1 << 20
+    xs = rng.uniform(0, 10, n)
+    ys = rng.uniform(0, 10, n)
+    zs = rng.uniform(0, 10, n)
+    xs[-1], ys[-1], zs[-1] = 100.0, 100.0, 100.0  # far point in the last tile
+    xs[-2], ys[-2], zs[-2] = -100.0, -100.0, 100.0  # same z: also the XY maximum
+    got = sc.diameters(xs, ys, zs)
+    d3 = math.sqrt(200.0 ** 2 + 200.0 ** 2)
+    assert got[0] == d3 and got[1] == d3
