@@ -6,31 +6,39 @@ processes its own ROIs (ROI-batch sharding: independent masks, no data-path
 collective -> "scaling": "weak"); the timed region is bracketed by a barrier
 and torch.cuda.synchronize() and the reported time is the max over ranks.
 
-Workload (BASELINE.json configs[1]): one synthetic KiTS19-shaped mask,
-512x512x600 uint8 at 0.8x0.8x1.0 mm, two kidneys + a 30 mm tumour
-(SURVEY.md Appendix D, V = 73,406 vertices).  One step = calculate_coefficients
-of one ROI: marching cubes -> area/volume -> 3-D and planar diameters.  The
-mask (157 MB) is larger than L2 (126 MB), so no L2 flush is needed.
+Workload (default, BASELINE.json configs[3]): C4, the batch of 300 varied
+KiTS19-shaped masks (512x512x[200..700], seed 2025); each rank
+takes its LPT share.  One step = one call of the batch entry on B (--batch,
+default 64) ROIs of the rank's share, cycling through it, so consecutive
+steps see different masks.  Every mask is staged in HBM before timing; every
+mask is larger than the 126 MB L2 or, cycling 300 distinct masks, evicted
+long before it comes back, so no L2 flush is needed.  C2 (configs[1], one
+512x512x600 mask at 0.8x0.8x1.0 mm) is measured the same way beside it
+(key "c2").  --workload c1|c2|c3|c5 selects another SURVEY.md 8(d) config.
 
-  value      device-resident throughput: mask already in HBM, K ROIs through the
-             pipelined device batch entry, CUDA events on the caller's stream
-             (the batch is ordered against it), host round trips included.
-  e2e        the same metric through the C ABI with a HOST (pinned) mask: the
-             pipelined host batch entry copies the 157 MB mask H2D for every
-             ROI and reads every result back.
-  single_roi one synchronous call per ROI (no cross-ROI overlap); its
-             per-kernel CUDA-event times feed kernel_ms and the rooflines.
-  roofline   the dominant kernel of the step.  diam3d_pass1 is FP32
-             CUDA-core bound: achieved = 8 flop x evaluated pairs / kernel time,
-             peak = FP32 rate measured by sc_probe_fp32_peak on this GPU.
-             pack_bits_v16 is HBM-bound: achieved = mask bytes / kernel time vs
-             the measured copy bandwidth in MEASURED_PEAKS.json.
-  allpairs   the same exact results with work pruning disabled (every pair
-             through pass 1): the brute-force pass-1 roofline.
-  cpu_baseline  the CPU oracle (C restatement of the reference, OpenMP strip-
-             parallel diameters, serial MC as in the reference) on one ROI.
+  value      device-resident throughput: K batch calls of B ROIs
+             (sc_calculate_coefficients_device_batch, 32 pipeline slots),
+             CUDA events on the caller's stream (each call is ordered against
+             it and synchronous).
+  e2e        the same metric through the C ABI with HOST (pinned) masks:
+             sc_calculate_coefficients_batch, B ROIs per step; the host scans
+             every mask byte for the occupied slab and only the slab crosses
+             PCIe; every result record is read back.
+  roi_ceiling  per-ROI HBM bound: mask bytes / measured copy bandwidth vs the
+             measured time per ROI.
+  roofline   the dominant kernel of the batch path, the HBM-bound TMA pack
+             (pack_bits_tma: mask bytes read once per launch), timed with CUDA
+             events around the kernel; roofline_pass1 = the FP32 diameter
+             pass (8 flop per evaluated pair vs the FP32 rate measured by
+             sc_probe_fp32_peak on this GPU).
+  cpu_baseline  the reference itself (shapecore, numba, installed under
+             baseline/_ref) on all host cores on a bounded sample of the
+             workload; the C port in oracle/ when the install is missing.
 
-`--impl reference` times that CPU path alone (rank 0; other ranks exit 0).
+`--impl reference` times the reference's CPU path alone (rank 0; other ranks
+exit 0): extract_features(vol, resolve_backend("parallel")) per ROI
+(features.py:224-265, dispatch.py:103-146), plus the "sequential" backend on
+C1 (PyRadiomics' shape class is single-threaded, PAPER.md:151).
 """
 
 from __future__ import annotations
@@ -49,52 +57,54 @@ sys.path.insert(0, ROOT)
 METRIC = "ROIs/sec full 3D shape coefficients (KiTS19-shaped masks) at 1/2/4/8 B200"
 UNIT = "ROIs/s"
 
-# SURVEY.md 8(d) configurations.  The default (headline, BASELINE.json
-# configs[1]) is c2; the others are selectable with --workload.
+# SURVEY.md 8(d) configurations.  The default (headline) is c4, the batch of
+# varied KiTS19-shaped masks; the others are selectable with --workload.
 WORKLOADS = {
     "c1": "C1 synthetic 64^3 sphere mask (r=24, spacing 1 mm, V=10824; the reference's own "
-          "CPU-runnable case), one ROI per step per GPU",
+          "CPU-runnable case)",
     "c2": "C2 KiTS19-shaped synthetic kidney+tumor mask 512x512x600 uint8 at 0.8x0.8x1.0 mm "
-          "(tumor 30 mm, V=73406), one ROI per step per GPU",
+          "(tumor 30 mm, V=73406)",
     "c3": "C3 noisy-boundary ellipsoid 512^3 at 1 mm (sigma 0.02, seed 1234, V=1963474, "
-          "1.93e12 pairs), one ROI per step per GPU",
-    "c4": "C4 batch of 300 varied KiTS19-shaped masks (512x512x[200..700], seed 2025), "
-          "LPT-sharded across GPUs, one ROI per step, cycling the rank's share",
-    "c5": "C5 thin slab 512x512x24 at 0.5x0.5x5 mm, 400 blobs (seed 7, V=127664), "
-          "one ROI per step per GPU",
+          "1.93e12 pairs)",
+    "c4": "C4 batch of 300 varied KiTS19-shaped masks (512x512x[200..700] uint8, in-plane "
+          "spacing 0.6-0.9 mm, tumour 10-75 mm, seed 2025), LPT-sharded across GPUs",
+    "c5": "C5 thin slab 512x512x24 at 0.5x0.5x5 mm, 400 blobs (seed 7, V=127664)",
 }
 
 
-def load_workload(name, rank=0, world=1):
-    """[(mask (nz,ny,nx) uint8, spacing)] for this rank, plus a config dict."""
+def workload_params(name, rank=0, world=1):
+    """[(generator, spacing)] of this rank's ROIs (masks are generated lazily,
+    one at a time, so 300 C4 masks never sit in host memory together)."""
     from paper_2510_02894_b200 import sharding, synth
 
     if name == "c1":
-        rois = [(synth.synth_mask("sphere", (64, 64, 64), radius=24), (1.0, 1.0, 1.0))]
-    elif name == "c2":
-        rois = [(synth.kits_like(512, 512, 600, (0.8, 0.8, 1.0), 30.0), (0.8, 0.8, 1.0))]
-    elif name == "c3":
-        rois = [(synth.noisy_ellipsoid(512, 0.02, 1234), (1.0, 1.0, 1.0))]
-    elif name == "c5":
-        rois = [(synth.thin_slab(), (0.5, 0.5, 5.0))]
-    elif name == "c4":
+        return [(lambda: synth.synth_mask("sphere", (64, 64, 64), radius=24), (1.0, 1.0, 1.0))]
+    if name == "c2":
+        return [(lambda: synth.kits_like(512, 512, 600, (0.8, 0.8, 1.0), 30.0), (0.8, 0.8, 1.0))]
+    if name == "c3":
+        return [(lambda: synth.noisy_ellipsoid(512, 0.02, 1234), (1.0, 1.0, 1.0))]
+    if name == "c5":
+        return [(lambda: synth.thin_slab(), (0.5, 0.5, 5.0))]
+    if name == "c4":
         params = synth.kits_batch_params(300, 2025)
         # cost: streamed voxels + (surface ~ tumour/kidney size)^2 pairs
         costs = [sharding.roi_cost(int((p["tumor_mm"] / p["sp"][0]) ** 3 * 4.2 + 2.6e5),
                                    p["nx"] * p["ny"] * p["nz"]) for p in params]
         mine = sharding.assign_rois(costs, world)[rank]
-        rois = [(synth.kits_from_params(params[i]), tuple(params[i]["sp"])) for i in mine]
-    else:
-        raise SystemExit(f"unknown workload {name}")
+        return [((lambda p=params[i]: synth.kits_from_params(p)), tuple(params[i]["sp"]))
+                for i in mine]
+    raise SystemExit(f"unknown workload {name}")
+
+
+def load_workload(name, rank=0, world=1):
+    """[(mask (nz,ny,nx) uint8, spacing)] for this rank, plus a config dict
+    (host masks; tools/ use this)."""
+    rois = [(g(), sp) for g, sp in workload_params(name, rank, world)]
     cfg = {
         "workload": WORKLOADS[name],
         "name": name,
-        "global_batch": None,
         "roi_bytes_mean": sum(m.size for m, _ in rois) / max(1, len(rois)),
         "rois_per_rank": len(rois),
-        "l2": "every mask > 126 MB L2 (no flush needed)" if min(m.size for m, _ in rois) > 126e6
-              else "mask < L2: steps cycle distinct ROIs / the mask is re-read from L2",
-        "parallelism": None,
     }
     return rois, cfg
 
@@ -218,120 +228,251 @@ def max_over_ranks(world, value):
     return float(t.item())
 
 
-def cpu_reference_time(mask, spacing, max_seconds=150.0, steps=1, warmup=0):
-    """The oracle (C port of the reference path) on all host cores: MC serial
-    (mesh.py:68-199), diameters strip-parallel (features.py:151-192).
-    Returns (per-ROI seconds list, threads, sample description).  When the
-    full pair loop would exceed the budget (C3), the diameters are timed on a
-    random vertex subset and extrapolated by pair count (labelled as such)."""
-    import numpy as np
+def reference_module():
+    """The reference itself (shapecore: Python + numba), installed under
+    baseline/_ref by build(); None when the install is missing."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "shapecore")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import shapecore
 
+        return shapecore
+    except Exception:  # numba missing or broken: fall back to the C port
+        return None
+
+
+def reference_roi_seconds(ref, mask, sp, backend="parallel"):
+    """One ROI through the reference's public path: MaskVolume ->
+    extract_features(vol, resolve_backend(backend, workers=all host cores))
+    (features.py:224-265, dispatch.py:103-146).  Returns (seconds, record)."""
+    nz, ny, nx = mask.shape
+    vol = ref.MaskVolume(dims=(nx, ny, nz), spacing=tuple(float(v) for v in sp),
+                         data=mask.reshape(-1))
+    sel = ref.resolve_backend(backend, workers=os.cpu_count()) if backend == "parallel" \
+        else ref.resolve_backend(backend)
+    t0 = time.perf_counter()
+    feats, _ = ref.extract_features(vol, sel)
+    return time.perf_counter() - t0, feats.to_dict()
+
+
+def reference_warmup(ref, n=1):
+    """JIT-compile (numba, cache=True) and warm the reference on the C1 sphere."""
+    from paper_2510_02894_b200 import synth
+
+    c1 = synth.synth_mask("sphere", (64, 64, 64), radius=24)
+    for _ in range(max(1, n)):
+        reference_roi_seconds(ref, c1, (1.0, 1.0, 1.0), "parallel")
+        reference_roi_seconds(ref, c1, (1.0, 1.0, 1.0), "sequential")
+
+
+def reference_layer():
+    import numba
+
+    try:
+        return numba.threading_layer()
+    except Exception:
+        return "unknown"
+
+
+def port_roi_seconds(mask, sp):
+    """The C restatement of the reference (oracle/, OpenMP strip-parallel
+    diameters, serial MC) on one ROI: the fallback CPU baseline."""
     from oracle import oracle
 
-    threads = oracle.max_threads()
     t0 = time.perf_counter()
-    mesh = oracle.marching_cubes(mask, spacing)
-    t_mc = time.perf_counter() - t0
-    V = mesh.vertex_count
-    pairs = V * (V - 1) / 2
-    if pairs <= 4e10:
-        t_start = time.perf_counter()
-        for _ in range(warmup):
-            oracle.extract_features(mask, spacing, threads=0, with_active=False)
-            if time.perf_counter() - t_start > max_seconds / 2:
-                break
-        times = []
-        for _ in range(max(1, steps)):
-            t1 = time.perf_counter()
-            oracle.extract_features(mask, spacing, threads=0, with_active=False)
-            times.append(time.perf_counter() - t1)
+    oracle.extract_features(mask, sp, threads=0, with_active=False)
+    return time.perf_counter() - t0, oracle.max_threads()
+
+
+def cpu_baseline_sample(gens, max_seconds, max_rois):
+    """Bounded sample of the workload on the host cores: the reference when
+    installed, else the C port.  Returns the cpu_baseline object."""
+    ref = reference_module()
+    times = []
+    t_start = time.perf_counter()
+    if ref is not None:
+        import numba
+
+        reference_warmup(ref)
+        for i in range(max_rois):
+            g, sp = gens[i % len(gens)]
+            dt, _ = reference_roi_seconds(ref, g(), sp)
+            times.append(dt)
             if time.perf_counter() - t_start > max_seconds:
                 break
-        return times, threads, f"{len(times)} full ROI(s)"
-    m = int((2 * 2e10) ** 0.5)
-    idx = np.sort(np.random.default_rng(0).choice(V, size=m, replace=False))
-    t1 = time.perf_counter()
-    oracle.diameters(mesh.xs[idx], mesh.ys[idx], mesh.zs[idx], threads=0)
-    t_d = (time.perf_counter() - t1) * pairs / (m * (m - 1) / 2)
-    t_area = 0.0
-    t2 = time.perf_counter()
-    oracle.surface_area(mesh)
-    oracle.mesh_volume(mesh)
-    t_area = time.perf_counter() - t2
-    return [t_mc + t_area + t_d], threads, (
-        f"full MC ({t_mc:.1f}s) + area/volume + diameters timed on a {m}-vertex random subset "
-        f"and extrapolated by pair count ({pairs:.3g} pairs -> {t_d:.0f}s)")
+        per = statistics.mean(times)
+        return {"value": 1.0 / per, "unit": UNIT, "cores": int(numba.get_num_threads()),
+                "kind": "reference",
+                "sample": f"{len(times)} ROI(s) of the workload through the reference itself "
+                          "(baseline/_ref shapecore: extract_features(vol, resolve_backend("
+                          "'parallel', workers=os.cpu_count())), numba threading layer "
+                          f"{reference_layer()}), after a JIT warm-up",
+                "seconds_per_roi": per}
+    threads = 1
+    for i in range(max_rois):
+        g, sp = gens[i % len(gens)]
+        dt, threads = port_roi_seconds(g(), sp)
+        times.append(dt)
+        if time.perf_counter() - t_start > max_seconds:
+            break
+    per = statistics.mean(times)
+    return {"value": 1.0 / per, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{len(times)} ROI(s) through oracle/shape_oracle.c (reference algorithm "
+                      "restated in C: serial canonical MC, strip-parallel fp64 diameters); "
+                      "baseline/_ref missing", "seconds_per_roi": per}
 
 
 def run_reference(args):
+    """The reference's own CPU path (shapecore, numba) on the host cores.
+    Rank 0 alone runs and prints; other ranks exit 0 without work."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    rois, cfg = load_workload(args.workload, 0, 1)
-    mask, sp = rois[len(rois) // 2]
-    times, threads, sample = cpu_reference_time(mask, sp, max_seconds=args.cpu_seconds,
-                                                steps=args.steps, warmup=min(args.warmup, 1))
+    gens = workload_params(args.workload, 0, 1)
+    ref = reference_module()
+    extra = {}
+    if ref is None:
+        kind, cores = "port", 1
+        times = []
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            g, sp = gens[i % len(gens)]
+            dt, cores = port_roi_seconds(g(), sp)
+            times.append(dt)
+            if time.perf_counter() - t0 > args.cpu_seconds:
+                break
+        sample = "oracle/shape_oracle.c, the C restatement (baseline/_ref missing)"
+    else:
+        import numba
+
+        kind, cores = "reference", int(numba.get_num_threads())
+        # W warm-up steps: JIT compile + numba cache on the C1 sphere (a full
+        # C4 ROI costs seconds on the CPU; the warm-up only has to compile).
+        reference_warmup(ref, args.warmup)
+        times = []
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            g, sp = gens[i % len(gens)]
+            dt, _ = reference_roi_seconds(ref, g(), sp)
+            times.append(dt)
+            if time.perf_counter() - t0 > args.cpu_seconds:
+                break
+        # PyRadiomics' shape class is single-threaded (PAPER.md:151): the
+        # reference's "sequential" backend on C1, for the record.
+        from paper_2510_02894_b200 import synth
+
+        c1 = synth.synth_mask("sphere", (64, 64, 64), radius=24)
+        seq = [reference_roi_seconds(ref, c1, (1.0, 1.0, 1.0), "sequential")[0] for _ in range(5)]
+        par = [reference_roi_seconds(ref, c1, (1.0, 1.0, 1.0), "parallel")[0] for _ in range(5)]
+        extra = {"c1_sequential": {"value": 1.0 / statistics.median(seq), "unit": UNIT,
+                                   "cores": 1, "note": "C1 64^3 sphere, backend 'sequential', "
+                                                       "median of 5"},
+                 "c1_parallel": {"value": 1.0 / statistics.median(par), "unit": UNIT,
+                                 "cores": cores, "note": "C1, backend 'parallel', median of 5"},
+                 "numba_threading_layer": reference_layer(), "host_cpu_count": os.cpu_count()}
+        sample = ("the reference itself: baseline/_ref shapecore (pip install of "
+                  "/root/reference/pkg), extract_features(vol, resolve_backend('parallel', "
+                  f"workers=os.cpu_count())) per ROI, numba layer {reference_layer()}")
     per = statistics.mean(times)
     value = 1.0 / per
-    cfg.update({"parallelism": "host cores (OpenMP)", "global_batch": 1})
+    cfg = {"workload": WORKLOADS[args.workload], "name": args.workload,
+           "global_batch": 1, "parallelism": "host cores (numba prange)" if kind == "reference"
+           else "host cores (OpenMP)",
+           "sample_rois": len(times), "l2": "n/a (CPU)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
-        "n_gpus": world, "steps": len(times), "warmup": min(args.warmup, 1),
+        "n_gpus": world, "steps": len(times), "warmup": args.warmup,
         "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8/fp64", "data": "synthetic",
-        "config": cfg,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{sample} through oracle/shape_oracle.c (reference "
-                                   "algorithm restated in C: serial canonical MC, "
-                                   "strip-parallel fp64 diameters), time-capped at "
+        "vs_baseline": None, "dtype": "u8 mask / fp64 (reference arithmetic)",
+        "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{len(times)} ROI(s) of the workload (one per step, "
+                                   f"distinct masks) through {sample}; time-capped at "
                                    f"{args.cpu_seconds:.0f}s"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    line.update(extra)
     print(json.dumps(line), flush=True)
     return 0
 
 
-def measure_device(sc, _native, d_mask, sp, stream, steps, warmup, dev, world):
-    """One synchronous call per ROI (no cross-ROI overlap): K steps on `stream`,
-    CUDA events around the loop (default graph events: mesh / diameters only);
-    then the same number of calls with an event at every stage boundary
-    (option stage_times=2) for the per-kernel medians.  Returns (ms max over
-    ranks, per-kernel median ms, diagnostics, launches, last result)."""
+def stage_on_device(gens, dev, keep_host):
+    """Generate the rank's masks one at a time and copy each to HBM; keep the
+    first `keep_host` on the host in pinned memory (the e2e leg)."""
     import torch
 
-    with torch.cuda.stream(stream):
-        for _ in range(warmup):
-            c = sc.calculate_coefficients_device(d_mask, sp, stream=stream)
+    d_masks, host = [], []
+    for i, (g, sp) in enumerate(gens):
+        m = g()
+        t = torch.from_numpy(m)
+        if i < keep_host:
+            t = t.pin_memory()
+            host.append(t.numpy())
+        d_masks.append(t.to(f"cuda:{dev}", non_blocking=False))
+    return d_masks, host
+
+
+def timed_batches(sc, _native, d_masks, sps, B, K, W, stream, world):
+    """W warm-up and K timed steps; step k = one device-batch call on ROIs
+    [(k*B + i) % n].  Returns (ms max over ranks, launches, outputs of the
+    timed steps, clocks)."""
+    import torch
+
+    n = len(d_masks)
+
+    def step(k):
+        idx = [(k * B + i) % n for i in range(B)]
+        return idx, sc.calculate_coefficients_device_batch([d_masks[i] for i in idx],
+                                                           [sps[i] for i in idx], stream=stream)
+
+    for k in range(W):
+        step(k)
     torch.cuda.synchronize()
+    clocks = ClockSampler(torch.cuda.current_device())
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = _native.launch_count()
     barrier(world)
     torch.cuda.synchronize()
+    clocks.__enter__()
     ev0.record(stream)
-    for _ in range(steps):
-        c = sc.calculate_coefficients_device(d_mask, sp, stream=stream)
+    outs = [step(W + k) for k in range(K)]
     ev1.record(stream)
     torch.cuda.synchronize()
+    clocks.__exit__(None, None, None)
     barrier(world)
     launches = _native.launch_count() - launches0
-    ms = max_over_ranks(world, ev0.elapsed_time(ev1))
+    return max_over_ranks(world, ev0.elapsed_time(ev1)), launches, outs, clocks
+
+
+def check_repeats(outs):
+    """Results of the same mask must be identical wherever it recurs."""
+    seen = {}
+    for idx, recs in outs:
+        for i, r in zip(idx, recs):
+            d = r.to_dict()
+            assert seen.setdefault(i, d) == d, f"ROI {i}: results differ between steps"
+    return seen
+
+
+def kernel_times(sc, _native, d_mask, sp, stream, reps, dev, **opts):
+    """Per-stage CUDA-event times (option stage_times=2) of single calls on
+    one ROI: medians over `reps` calls, plus the diagnostics and record."""
     kt = {k: [] for k in _native.KERNEL_TIME_NAMES}
-    _native.set_option("stage_times", 2)
-    try:
+    with _native.thread_options(stage_times=2, **opts):
         sc.calculate_coefficients_device(d_mask, sp, stream=stream)  # captures its graph
-        for _ in range(steps):
-            sc.calculate_coefficients_device(d_mask, sp, stream=stream)
+        for _ in range(reps):
+            c = sc.calculate_coefficients_device(d_mask, sp, stream=stream)
             for k, v in _native.last_kernel_times(dev).items():
                 kt[k].append(v)
-    finally:
-        _native.set_option("stage_times", 0)
     med = {k: statistics.median(v) for k, v in kt.items() if v}
-    return ms, med, _native.last_diagnostics(dev), launches, c
+    return med, _native.last_diagnostics(dev), c
 
 
 def run_ours(args):
-    import numpy as np
     import torch
 
     import paper_2510_02894_b200 as sc
@@ -344,110 +485,107 @@ def run_ours(args):
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
     host_threads = max(1, (os.cpu_count() or 1) // max(1, local_world))
     _native.set_option("host_threads", min(32, host_threads))
-    rois, cfg = load_workload(args.workload, rank, world)
-    d_masks = [torch.from_numpy(m).to(f"cuda:{dev}") for m, _ in rois]
-    sps = [sp for _, sp in rois]
+    gens = workload_params(args.workload, rank, world)
+    sps = [sp for _, sp in gens]
+    n_host = min(len(gens), args.e2e_masks)
+    d_masks, h_masks = stage_on_device(gens, dev, n_host)
+    roi_bytes = [m.numel() for m in d_masks]
     stream = torch.cuda.Stream()
-    n_host = min(len(rois), 8)
-    h_masks = [torch.from_numpy(m).pin_memory().numpy() for m, _ in rois[:n_host]]
-    K = args.steps
-    step_masks = [d_masks[i % len(d_masks)] for i in range(K)]
-    step_sps = [sps[i % len(sps)] for i in range(K)]
+    B, K = args.batch, args.steps
+    W = max(args.warmup, 3)
+    peaks, peak_kind = measured_peaks()
+    hbm = peaks["hbm_gbs"]
 
-    # ---- device-resident throughput (value): K ROIs through the pipelined
-    # device batch entry (16 slots: ROI i+16 is enqueued when ROI i is
-    # collected), CUDA events on `stream`, which the batch is ordered against.
-    clocks = ClockSampler(dev)
-    W = args.warmup
-    # W warm-up steps, and at least two rounds over the 16 pipeline slots so
-    # every slot has captured its CUDA graph before the timed region.
-    # Then one untimed batch of exactly the timed shape: the first K-ROI batch
-    # after the capture-bound warm-up (the GPU mostly waits on host-side graph
-    # captures there) runs ~15 % slower on the device (C2, K = 20: 57.7 vs 49-50
-    # us/ROI for the next ones; host-side launch and collect times identical,
-    # tools/k20_probe.py), a one-off a steady stream of batches does not pay.
-    Ww = max(W, 32)
-    sc.calculate_coefficients_device_batch([d_masks[i % len(d_masks)] for i in range(Ww)],
-                                           [sps[i % len(sps)] for i in range(Ww)], stream=stream)
-    sc.calculate_coefficients_device_batch(step_masks, step_sps, stream=stream)
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = _native.launch_count()
-    barrier(world)
-    torch.cuda.synchronize()
-    clocks.__enter__()
-    ev0.record(stream)
-    outs = sc.calculate_coefficients_device_batch(step_masks, step_sps, stream=stream)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    clocks.__exit__(None, None, None)
-    barrier(world)
-    launches = _native.launch_count() - launches0
-    dev_ms = max_over_ranks(world, ev0.elapsed_time(ev1))
-    value = world * K / (dev_ms / 1e3)
-    for i, o in enumerate(outs[len(d_masks):]):
-        assert o.to_dict() == outs[i % len(d_masks)].to_dict()
+    # ---- device-resident throughput (value) ----
+    dev_ms, launches, outs, clocks = timed_batches(sc, _native, d_masks, sps, B, K, W, stream,
+                                                   world)
+    value = world * B * K / (dev_ms / 1e3)
+    recs = check_repeats(outs)
+    us_roi = dev_ms * 1e3 / (B * K)
+    step_bytes = sum(roi_bytes[(k * B + i) % len(d_masks)]
+                     for k in range(W, W + K) for i in range(B)) / (B * K)
+    ceiling_us = step_bytes / (hbm * 1e3)
 
-    # ---- one ROI per call on the first ROI: per-kernel times ----
-    d0, sp0 = d_masks[0], sps[0]
-    one_steps = max(3, min(K, 30))
-    one_ms, med, diag, _, c = measure_device(sc, _native, d0, sp0, stream, one_steps, 3, dev, world)
-    assert c.to_dict() == outs[0].to_dict()
+    def ceiling(us, nbytes):
+        return {"bytes_per_roi": nbytes, "hbm_gbs": hbm, "peak_kind": peak_kind,
+                "ceiling_us_per_roi": nbytes / (hbm * 1e3), "measured_us_per_roi": us,
+                "frac": nbytes / (hbm * 1e3) / us,
+                "note": "every mask byte read once from HBM at the measured copy bandwidth: "
+                        "the per-ROI floor of the whole pipeline"}
 
-    # ---- same, all pairs evaluated (no pruning): the pass-1 roofline case ----
-    _native.set_option("prune", 0)
-    bf_steps = 3 if args.workload == "c3" else max(3, one_steps // 2)
-    bf_ms, bf_med, bf_diag, _, c_bf = measure_device(sc, _native, d0, sp0, stream, bf_steps, 1,
-                                                     dev, world)
-    _native.set_option("prune", 1)
+    # ---- C2 side by side (BASELINE.json configs[1]) ----
+    side = None
+    if args.workload == "c4" and not args.no_side:
+        g2 = workload_params("c2")
+        d2, _ = stage_on_device(g2, dev, 0)
+        ms2, _, outs2, _ = timed_batches(sc, _native, d2, [g2[0][1]], B, K, W, stream, world)
+        check_repeats(outs2)
+        u2 = ms2 * 1e3 / (B * K)
+        side = {"workload": WORKLOADS["c2"], "value": world * B * K / (ms2 / 1e3), "unit": UNIT,
+                "us_per_roi": u2, "roi_ceiling": ceiling(u2, d2[0].numel()),
+                "protocol": "same as value: K batch calls of B ROIs (the C2 mask repeated)"}
+        del d2
+
+    # ---- per-kernel times (single calls, CUDA events at every stage) ----
+    i0 = max(range(len(d_masks)), key=lambda i: roi_bytes[i]) if args.workload != "c4" else 0
+    d0, sp0 = d_masks[i0], sps[i0]
+    reps = max(3, min(K, 20))
+    med, diag, c = kernel_times(sc, _native, d0, sp0, stream, reps, dev)
+    assert c.to_dict() == recs.get(i0, c.to_dict())
+    # the batch path's pack (TMA bulk copy + fused bbox) timed the same way
+    med_tma, _, c_tma = kernel_times(sc, _native, d0, sp0, stream, reps, dev,
+                                     pack_tma_single=1, fused_bbox_single=1)
+    assert c_tma.to_dict() == c.to_dict()
+    # all pairs evaluated (no pruning): the brute-force pass-1 roofline
+    bf_reps = 3 if args.workload == "c3" else max(3, reps // 2)
+    bf_med, bf_diag, c_bf = kernel_times(sc, _native, d0, sp0, stream, bf_reps, dev, prune=0)
     assert c_bf.to_dict() == c.to_dict(), "pruned and all-pairs results differ"
+    single_ms = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        sc.calculate_coefficients_device(d0, sp0, stream=stream)
+        single_ms.append((time.perf_counter() - t0) * 1e3)
 
-    # ---- end to end through the C ABI from pinned host memory (e2e): the
-    # pipelined host batch entry; every step copies its mask H2D.
-    sc.calculate_coefficients_batch([h_masks[i % n_host] for i in range(16)],
-                                    [sps[i % n_host] for i in range(16)], device=dev)
-    barrier(world)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    e_outs = sc.calculate_coefficients_batch([h_masks[i % n_host] for i in range(K)],
-                                             [sps[i % n_host] for i in range(K)], device=dev)
-    torch.cuda.synchronize()
-    e2e_s = max_over_ranks(world, time.perf_counter() - t0)
-    barrier(world)
-    e2e_value = world * K / e2e_s
-    h2d_bytes = sum(o.h2d_bytes for o in e_outs) / K
-    scan_ms = statistics.median(o.host_scan_ms for o in e_outs)
-    assert e_outs[0].to_dict() == outs[0].to_dict()
-    # same, copying every mask byte (option host_crop off): the PCIe-bound figure
-    _native.set_option("host_crop", 0)
-    sc.calculate_coefficients_batch([h_masks[i % n_host] for i in range(8)],
-                                    [sps[i % n_host] for i in range(8)], device=dev)
-    barrier(world)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    f_outs = sc.calculate_coefficients_batch([h_masks[i % n_host] for i in range(K)],
-                                             [sps[i % n_host] for i in range(K)], device=dev)
-    torch.cuda.synchronize()
-    full_s = max_over_ranks(world, time.perf_counter() - t0)
-    barrier(world)
-    _native.set_option("host_crop", 1)
-    assert f_outs[0].to_dict() == outs[0].to_dict()
+    # ---- end to end through the C ABI from pinned host memory (e2e) ----
+    def e2e_run(opts):
+        with _native.thread_options(**opts):
+            hs = [h_masks[i % n_host] for i in range(B)]
+            hsp = [sps[i % n_host] for i in range(B)]
+            sc.calculate_coefficients_batch(hs, hsp, device=dev)  # warm-up
+            barrier(world)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e_outs = []
+            for k in range(K):
+                idx = [(k * B + i) % n_host for i in range(B)]
+                e_outs.append((idx, sc.calculate_coefficients_batch(
+                    [h_masks[i] for i in idx], [sps[i] for i in idx], device=dev)))
+            torch.cuda.synchronize()
+            s = max_over_ranks(world, time.perf_counter() - t0)
+            barrier(world)
+        flat = [o for _, os_ in e_outs for o in os_]
+        for idx, os_ in e_outs:
+            for i, o in zip(idx, os_):
+                if i in recs:
+                    assert o.to_dict() == recs[i], "host and device paths differ"
+        return s, flat
+
+    e2e_s, e_flat = e2e_run({})
+    full_s, f_flat = e2e_run({"host_crop": 0})
+    e2e_value = world * B * K / e2e_s
+    h2d_bytes = sum(o.h2d_bytes for o in e_flat) / len(e_flat)
 
     # ---- rooflines ----
     V = c.vertex_count
-    pairs_alg = V * (V - 1) / 2
     fp32_peak = max(_native.probe_fp32_peak(dev, m) for m in (0, 1, 3))
     fp32_ffma2 = _native.probe_fp32_peak(dev, 0)
-    # the committed ncu capture (tools/gpu_final.sh) is of the C2 workload
-    traffic = ncu_traffic() if args.workload == "c2" else {}
-    peaks, peak_kind = measured_peaks()
+    traffic = ncu_traffic()
     mask_bytes = d0.numel()
 
     def pass1_roof(m, d, label):
         # One fused kernel runs the 3-D list (8 flop per pair: 3 FMA + |p|^2
         # fold + max) and the planar list (6 flop per pair: 2 FMA + fold + max).
         # Pass 1 evaluates the listed 64 x 64 sub-pairs of every kept unit.
-        edge = 64
         sub = _native.PAIRS_PER_UNIT // 4
         p3 = d["work_subunits"] * sub
         p2 = d["planar_work_subunits"] * sub
@@ -456,7 +594,7 @@ def run_ours(args):
         return {"kernel": "diam_pass1", "bound": "fp32", "achieved": ach, "peak": fp32_peak,
                 "unit": "TFLOP/s", "frac": ach / fp32_peak,
                 "traffic": traffic.get("diam_pass1"),
-                "work": f"{label}: 8 flop x {p3:.4g} 3-D pairs ({d['work_subunits']} {edge}x{edge} "
+                "work": f"{label}: 8 flop x {p3:.4g} 3-D pairs ({d['work_subunits']} 64x64 "
                         f"sub-pairs of {d['work_units']} kept / {d['total_units']} 128x128 "
                         f"chunk pairs) + 6 flop x {p2:.4g} in-plane pairs "
                         f"({d['planar_work_subunits']} sub-pairs)",
@@ -465,21 +603,31 @@ def run_ours(args):
                              f"(best of FFMA/FFMA-imm/FFMA2; FFMA2 alone {fp32_ffma2:.1f} "
                              "TFLOP/s); nominal 74.4 at 1965 MHz"}
 
-    pack_s = med["pack_ms"] / 1e3
-    mc_gbs = mask_bytes / pack_s / 1e9
-    roof_mc = {"kernel": "pack_bits_v16", "bound": "hbm", "achieved": mc_gbs,
-               "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": mc_gbs / peaks["hbm_gbs"],
-               "traffic": traffic.get("pack_bits_v16"), "peak_kind": peak_kind,
-               "work": f"{mask_bytes} mask bytes read once per launch",
-               "mvoxels_per_s": mask_bytes / pack_s / 1e6,
-               "mc_stage_mvoxels_per_s": mask_bytes / ((med["pack_ms"] + med["mc_ms"]) / 1e3) / 1e6}
+    def pack_roof(ms, kernel, note):
+        gbs = mask_bytes / (ms / 1e3) / 1e9
+        return {"kernel": kernel, "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                "frac": gbs / hbm, "traffic": traffic.get(kernel), "peak_kind": peak_kind,
+                "work": f"{mask_bytes} mask bytes read once per launch (one launch per ROI)",
+                "mvoxels_per_s": mask_bytes / (ms / 1e3) / 1e6, "timing": note}
+
+    roof_tma = pack_roof(med_tma["pack_ms"], "pack_bits_tma",
+                         "CUDA events around the kernel in a single call (option "
+                         "pack_tma_single=1, fused bbox), the batch path's pack")
+    roof_v16 = pack_roof(med["pack_ms"], "pack_bits_v16",
+                         "CUDA events around the kernel in a single call (128-bit-load pack, "
+                         "the single-call path)")
+    roof_mc = dict(roof_v16)
+    roof_mc["mc_stage_mvoxels_per_s"] = mask_bytes / ((med["pack_ms"] + med["mc_ms"]) / 1e3) / 1e6
+    roof_mc["mc_stage_frac_hbm"] = (mask_bytes / ((med["pack_ms"] + med["mc_ms"]) / 1e3) / 1e9
+                                    / hbm)
     roof_p1 = pass1_roof(med, diag, "pruned")
     roof_p1_bf = pass1_roof(bf_med, bf_diag, "all pairs")
     stage = {k: v for k, v in med.items() if k != "h2d_ms"}
     dominant = max(stage, key=stage.get)
-    roofline = roof_p1 if dominant == "pass1_ms" else roof_mc
+    # The batch path's dominant kernel is the HBM stream unless pass 1 is the
+    # largest single-call stage (C3-like meshes).
+    roofline = roof_p1 if dominant == "pass1_ms" else roof_tma
     total_k = sum(stage.values())
-    cfg.update({"global_batch": world, "parallelism": f"roi-batch x{world}"})
 
     line = {
         "metric": METRIC,
@@ -492,51 +640,58 @@ def run_ours(args):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "fp32",
+        "dtype": "u8 mask; exact int64 MC sums; fp32 screen + fp64 exact diameters",
         "data": "synthetic",
-        "config": cfg,
-        "path": "sc_calculate_coefficients_device_batch (C ABI), device-resident masks",
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d_bytes),
-                "d2h_bytes_per_step": 16800,  # one Stats record (sizeof(sc::Stats), 8 histogram copies)
-                "path": "sc_calculate_coefficients_batch (C ABI, pipelined) from pinned host "
-                        "memory: host scan of every mask byte for the occupied z/y slab "
-                        "(host_threads), then only that slab is copied H2D",
-                "mask_bytes_per_step": int(sum(h_masks[i % n_host].size for i in range(K)) / K),
+        "config": {"workload": WORKLOADS[args.workload], "name": args.workload,
+                   "global_batch": B * world, "rois_per_step_per_gpu": B,
+                   "distinct_rois_per_rank": len(d_masks),
+                   "roi_bytes_mean": step_bytes,
+                   "l2": "no flush: every mask (>= 100 MB) streams from HBM; consecutive ROIs "
+                         "of a step are distinct masks" if args.workload == "c4" else
+                         ("no flush: the mask (> 126 MB L2) streams from HBM every ROI"
+                          if mask_bytes > 126e6 else "mask < L2 (re-read from L2)"),
+                   "parallelism": f"roi-batch x{world} (LPT shares, no collective)"},
+        "path": "sc_calculate_coefficients_device_batch (C ABI), device-resident masks, one "
+                "call of B ROIs per step",
+        "roi_ceiling": ceiling(us_roi, step_bytes),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d_bytes * B),
+                "d2h_bytes_per_step": 16800 * B,  # one Stats record per ROI (mapped pinned)
+                "path": "sc_calculate_coefficients_batch (C ABI) from pinned host memory, B ROIs "
+                        "per step: host scan of every mask byte for the occupied z/y slab "
+                        "(host_threads), then only that slab crosses PCIe",
+                "distinct_host_masks": n_host,
+                "mask_bytes_per_step": int(sum(h_masks[i % n_host].size for i in range(B))),
                 "host_threads_per_rank": min(32, host_threads),
-                "host_scan_ms_per_roi": scan_ms,
-                "h2d_ms_per_roi": e_outs[-1].h2d_ms,
-                "full_copy": {"value": world * K / full_s, "unit": UNIT,
-                              "h2d_bytes_per_step": int(sum(o.h2d_bytes for o in f_outs) / K),
+                "host_scan_ms_per_roi": statistics.median(o.host_scan_ms for o in e_flat),
+                "full_copy": {"value": world * B * K / full_s, "unit": UNIT,
+                              "h2d_bytes_per_step": int(sum(o.h2d_bytes for o in f_flat)
+                                                        / len(f_flat) * B),
                               "note": "option host_crop=0: every mask byte crosses PCIe"}},
-        "single_roi": {"value": world * one_steps / (one_ms / 1e3), "unit": UNIT,
-                       "path": "sc_calculate_coefficients_device, one synchronous call per ROI"},
+        "single_roi": {"value": world * 1e3 / statistics.median(single_ms), "unit": UNIT,
+                       "path": "sc_calculate_coefficients_device, one synchronous call per ROI "
+                               "(host wall time, median)"},
         "gpu_launches": int(launches),
         "roofline": roofline,
-        "roofline_mc": roof_mc,
+        "roofline_pack_single": roof_mc,
         "roofline_pass1": roof_p1,
-        "allpairs": {"value": world * bf_steps / (bf_ms / 1e3), "unit": UNIT,
-                     "note": "same exact results with pruning disabled (every pair evaluated)",
+        "allpairs": {"value": world * 1e3 / sum(bf_med.values()), "unit": UNIT,
+                     "note": "same exact results with pruning disabled (every pair evaluated); "
+                             "value from the summed stage times",
                      "kernel_ms": bf_med, "roofline_pass1": roof_p1_bf},
         "kernel_ms": med,
+        "kernel_ms_batch_pack": {"pack_ms": med_tma["pack_ms"]},
         "kernel_share": {k: v / total_k for k, v in stage.items()},
         "dominant_stage": dominant,
         "diagnostics": diag,
         "clocks": clocks.summary(),
         "result": {"VertexCount": V, "triangles": c.triangle_count, "active_cubes": c.active_cubes,
                    "Maximum3DDiameter": c.max_3d_diameter, "MeshVolume": c.mesh_volume,
-                   "pairs": pairs_alg},
+                   "pairs": V * (V - 1) / 2},
     }
-
+    if side is not None:
+        line["c2"] = side
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        m, sp = rois[0]
-        times, threads, sample = cpu_reference_time(m, sp, max_seconds=args.cpu_seconds, steps=1)
-        per = statistics.mean(times)
-        line["cpu_baseline"] = {
-            "value": 1.0 / per, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{sample} through oracle/shape_oracle.c (reference algorithm in C: "
-                      "serial canonical MC + strip-parallel fp64 diameters on all host threads)",
-            "seconds_per_roi": per,
-        }
+        line["cpu_baseline"] = cpu_baseline_sample(gens, args.cpu_seconds / 5, 3)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -583,7 +738,8 @@ def run_split(args):
     cfg.update({"global_batch": 1, "parallelism": f"pair-grid split x{world} + NCCL all_reduce(MAX)"})
     line = {"metric": METRIC, "value": args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u8 mask; exact int64 MC sums; fp32 screen + fp64 exact diameters",
             "data": "synthetic", "config": cfg, "clocks": clocks.summary(),
             "path": "sharding.sharded_coefficients -> sc_calculate_coefficients_shard",
             "result": {k: rec[k] for k in ("VertexCount", "Maximum3DDiameter")}}
@@ -602,9 +758,13 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=64, help="ROIs per step per GPU")
+    ap.add_argument("--e2e-masks", type=int, default=16,
+                    help="distinct pinned host masks cycled by the e2e leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=150.0)
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-side", action="store_true", help="skip the C2 side-by-side line")
+    ap.add_argument("--cpu-seconds", type=float, default=170.0)
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--split", action="store_true",
                     help="strong scaling of ONE ROI: every rank evaluates its share of the pair "
                          "grid (sc_calculate_coefficients_shard) + one NCCL all_reduce(MAX)")

@@ -190,8 +190,9 @@ int sc_last_diagnostics(int device, int64_t* out, int n);
  * them mesh_ms / diameters_ms come from the %globaltimer stamps);
  * "pack_tma" (1) / "pack_tma_single" (0) = CTAs per SM of the cp.async.bulk
  * (TMA) pack in batch entries / single calls (0 = the 128-bit-load pack);
- * "fused_bbox" (1) = the pack accumulates the occupied bbox itself (else a
- * separate pass over the bit volume);
+ * "fused_bbox" (1) / "fused_bbox_single" (0) = the pack accumulates the
+ * occupied bbox itself (else a separate pass over the bit volume), in batch
+ * entries / single calls;
  * "sparse_bits" (1) = the pack writes only nonzero 16-word segments of the
  * bit volume (segment map); "pack_skip" (1) = ... and does no conversion work
  * at all for all-background segments; "pdl" (0) = programmatic dependent

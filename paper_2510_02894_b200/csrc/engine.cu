@@ -110,7 +110,10 @@ struct Opts {
   bool graphs = true;        // replay each ROI pipeline as a cached CUDA graph
   int stages = 1 << 30;      // debug: kernels enqueued per ROI ("debug_stages")
   int empty = 0;             // debug: empty kernels appended per ROI ("debug_empty")
-  bool fbox = true;          // bbox accumulated inside the pack ("fused_bbox"; else bits_bbox)
+  bool fbox = true;          // batch graphs: bbox accumulated inside the pack ("fused_bbox";
+                             // else a bits_bbox pass)
+  bool fbox_single = false;  // the same for single calls (C2 call: pack 28.7 + bbox ~6 us
+                             // separate vs 38.8 us fused)
   int slots = 32;            // pipeline slots of the batch entries (measured 32 > 24 > 16 > 12)
   long long dcap = 2LL << 20;  // default diameter-side vertex capacity
   long long wcap = 1LL << 20;  // default 3-D work-list capacity (chunk pairs)
@@ -1046,6 +1049,7 @@ int run_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz, c
   // single calls: mesh / diameters events (level 1), every stage (2) or none (0)
   c->grid_div = c->o.grid_div_single;
   c->o.pack_tma = c->o.pack_tma_single;
+  c->o.fbox = c->o.fbox_single;
   c->events_on = c->o.stage_times > 0;
   c->ev_full = c->o.stage_times > 1;
   int rc = start_roi(c, d_mask, nx, ny, nz, sp, s, shard, nshards, d_sq4, 0, &p, org);
@@ -1518,6 +1522,7 @@ int set_opt(Opts& o, const char* name, int value) {
   else if (std::strcmp(name, "dcap") == 0) o.dcap = std::max(256, value);
   else if (std::strcmp(name, "wcap") == 0) o.wcap = std::max(1, value);
   else if (std::strcmp(name, "fused_bbox") == 0) o.fbox = value != 0;
+  else if (std::strcmp(name, "fused_bbox_single") == 0) o.fbox_single = value != 0;
   else if (std::strcmp(name, "host_crop") == 0) o.crop = value != 0;
   else if (std::strcmp(name, "host_pack") == 0) o.host_pack = std::max(-1, std::min(1, value));
   else if (std::strcmp(name, "host_split") == 0) o.split = std::max(-1, std::min(90, value));

@@ -12,11 +12,12 @@
 //  * pass1_planar -- the same over the surviving in-plane chunk pairs listed by
 //    plane_filter (planar.cu), 2-D (1 FFMA2 + 0.5 FMNMX3 per pair).
 //  * refine_3d / refine_planar -- exactness: every unit whose pass-1 maximum
-//    lies within kRefineRel of its family's pass-1 maximum is re-evaluated in
+//    reaches its family's threshold tau (refine_tau: an absolute margin of
+//    96 u R^2 below the family's pass-1 maximum) is re-evaluated in
 //    fp64 with the reference's own arithmetic on the reference's own
 //    coordinates, so every diameter is the reference's value bit for bit.
 //    Units below the threshold provably cannot hold the maximum (pass-1 error
-//    < ~1e-6 of D^2).
+//    <= 35 u R^2; sc_device.cuh refine_tau).
 #pragma once
 #include "sc_device.cuh"
 
@@ -170,7 +171,7 @@ __device__ __forceinline__ void pass1_3d(const int4* __restrict__ keys, long lon
 }
 
 // Exact re-check.  Every block sweeps 256 work entries at a time: the units
-// whose pass-1 maximum lies within kRefineRel of the (now complete) pass-1
+// whose pass-1 maximum reaches refine_tau of the (now complete) pass-1
 // maximum are listed in shared memory and each is re-evaluated, 128 x 128 in
 // fp64 with the reference arithmetic on the reference coordinates (thread =
 // one i vertex x half of the j chunk).  Selection is fully parallel: no
@@ -188,7 +189,10 @@ __device__ __forceinline__ void refine_3d(const int4* __restrict__ keys, long lo
   long long w0, w1;
   w0 = 0;
   w1 = (long long)st->n_work;
-  const float tau = __uint_as_float(st->d3_f32) * (1.f - kRefineRel);
+  const int* bb = st->bbox;
+  const double R2 = half_extent_sq(bb[0], bb[3], f.sx) + half_extent_sq(bb[1], bb[4], f.sy) +
+                    half_extent_sq(bb[2], bb[5], f.sz);
+  const float tau = refine_tau(__uint_as_float(st->d3_f32), R2);
   const int ti = threadIdx.x % kChunk, tj = (threadIdx.x / kChunk) * kJ;
   double best = 0.0;
   // Block b sweeps entries w0 + b, w0 + b + G, ... (G = grid size), 256 at a
@@ -348,7 +352,7 @@ __device__ __forceinline__ void pass1_planar(const int2* __restrict__ sorted,
 // Exact planar re-check (fp64, reference arithmetic: the out-of-plane delta
 // is exactly 0, so da*da + db*db is the reference's 3-term sum bit for bit).
 // Every block sweeps 256 work entries at a time, lists those within
-// kRefineRel of their family's pass-1 maximum in shared memory and re-checks
+// their family threshold (refine_tau) in shared memory and re-checks
 // each: 128 i entries x two halves of the j chunk.
 __device__ __forceinline__ void refine_planar(const int2* __restrict__ sorted,
                                               const unsigned int* __restrict__ start,
@@ -362,8 +366,14 @@ __device__ __forceinline__ void refine_planar(const int2* __restrict__ sorted,
   const PlaneSpace ps = plane_space(st);
   const long long w0 = 0, w1 = (long long)st->n_pwork;
   float tau[3];
+  {
+    const int* bb = st->bbox;
+    const double ex = half_extent_sq(bb[0], bb[3], f.sx), ey = half_extent_sq(bb[1], bb[4], f.sy),
+                 ez = half_extent_sq(bb[2], bb[5], f.sz);
+    const double R2[3] = {ex + ey, ex + ez, ey + ez};  // XY, XZ, YZ frames (plane_axes)
 #pragma unroll
-  for (int a = 0; a < 3; a++) tau[a] = __uint_as_float(st->pl_f32[a]) * (1.f - kRefineRel);
+    for (int a = 0; a < 3; a++) tau[a] = refine_tau(__uint_as_float(st->pl_f32[a]), R2[a]);
+  }
   const int ti = threadIdx.x % kPC, tj = (threadIdx.x / kPC) * kJ;
   // Block b sweeps entries w0 + b, w0 + b + G, ... (G = grid size), 256 at a
   // time, so candidates (adjacent in the work list) spread over the blocks.

@@ -271,10 +271,34 @@ __device__ __forceinline__ bool last_block(unsigned int* ticket) {
 }
 
 // ---- helpers shared by the diameter, pruning and planar kernels ----
-// Relative margin of the re-check threshold.  Pass-1 error is below ~1e-6 of
-// D^2; a unit whose pass-1 maximum is below M*(1 - kRefineRel)
-// provably cannot hold the exact maximum pair.
+// Re-check threshold.  Pass 1 evaluates the dot form
+// |pj|^2 - 2 pi.pj + |pi|^2 in fp32 on frame coordinates |p| <= R, where R^2
+// is the squared half-diagonal of the ROI bbox in the pass's own axes (3-D:
+// x, y, z; a plane family: its two in-plane axes).  Its absolute error is
+// e <= 35 u R^2 (u = 2^-24: 2u per frame coordinate, 7u R^2 per |p|^2, 3 FMA
+// roundings on terms <= 3 R^2, 8u R^2 from the coordinates in the product,
+// the |pi|^2 fold).  With M the family's pass-1 maximum (M <= D^2 + e), the
+// unit holding the exact maximum pair has pass-1 value >= D^2 - e >= M - 2e,
+// so every unit at or above tau = M - 2 e_max is re-checked, e_max = 48 u R^2
+// (kRefineAbs = 96 u).  The margin is ABSOLUTE in R^2: a plane family whose
+// maximum is far below R^2 (small lesions spread over the field) is covered.
+// tau is never above the previous relative rule M (1 - kRefineRel).
 constexpr float kRefineRel = 8e-6f;
+constexpr double kRefineAbs = 96.0 / 16777216.0;
+
+__device__ __forceinline__ float refine_tau(float M, double R2) {
+  const double rel = (double)M * (1.0 - (double)kRefineRel);
+  const double abs_ = (double)M - kRefineAbs * R2;
+  return __double2float_rd(fmin(rel, abs_));
+}
+
+// Squared half-extent of the ROI bbox along one axis in mm^2: vertex keys lie
+// in [2 lo - 1, 2 hi + 1] (doubled units), the frame centre at lo + hi, so
+// |frame coordinate| <= (hi - lo + 1) * s / 2.
+__device__ __forceinline__ double half_extent_sq(int lo, int hi, double s) {
+  const double h = 0.5 * (double)(hi - lo + 1) * s;
+  return h * h;
+}
 
 __device__ __forceinline__ float fmax3f(float a, float b, float c) {
   float r;

@@ -23,10 +23,65 @@ import math
 from typing import Callable, List, Optional, Sequence, Tuple
 
 
-def shard_range(n_items: int, shard: int, nshards: int) -> Tuple[int, int]:
-    """[begin, end) of shard `shard` -- the exact integer split the C engine
-    uses for tile pairs and planes (engine.cu run_diameters)."""
-    return n_items * shard // nshards, n_items * (shard + 1) // nshards
+# ---- pair-grid ownership (mirrors of the engine's rules) ---------------------
+# The shard entry splits the pair grid by the IDENTITY of each unit, not by
+# position in a list, so the split is exact whatever order the device's
+# atomically compacted work lists come out in.  These restate the rules the
+# kernels apply; tests/test_sharding.py runs a CPU shard stub built on them.
+
+CHUNK_3D = 128      # vertices per 3-D chunk (sc_device.cuh kChunk3)
+CHUNK_PLANAR = 128  # entries per in-plane chunk (kPlaneChunk)
+TILE_PLANAR = 256   # entries per in-plane tile = 2 chunks (planar.cu kPT)
+
+
+def tile_pair_index(i: int, j: int, n: int) -> int:
+    """Row-major index of (i, j), i <= j, in the upper triangle of an n x n
+    grid (sc_device.cuh tile_pair is its inverse)."""
+    return i * n - i * (i - 1) // 2 + (j - i)
+
+
+def owner_3d(i: int, j: int, n_chunks: int, nshards: int) -> int:
+    """Shard owning 3-D chunk pair (i, j), i <= j: its tile-pair index mod
+    nshards (csrc/prune.cu test_chunk_pair, :457)."""
+    return tile_pair_index(i, j, n_chunks) % nshards
+
+
+def owner_planar(u: int, h: int, b: int, nshards: int) -> int:
+    """Shard owning chunk pair (2I + h, 2J + b) of planar tile pair u (u = the
+    tile pair's global index over all planes, plane_tstart order):
+    (4u + 2h + b) mod nshards (csrc/planar.cu plane_filter, :251-252)."""
+    return (4 * u + 2 * h + b) % nshards
+
+
+def shard_pairs_3d(n: int, shard: int, nshards: int, chunk: int = CHUNK_3D):
+    """Chunk pairs (i, j), i <= j, of n vertices owned by `shard`."""
+    C = (n + chunk - 1) // chunk
+    for i in range(C):
+        for j in range(i, C):
+            if owner_3d(i, j, C, nshards) == shard:
+                yield i, j
+
+
+def shard_pairs_planar(plane_sizes: Sequence[int], shard: int, nshards: int,
+                       chunk: int = CHUNK_PLANAR, tile: int = TILE_PLANAR):
+    """(plane, ci, cj) in-plane chunk pairs, ci <= cj, owned by `shard`.
+    Planes in engine order (XY by z, then XZ by y, then YZ by x, ascending);
+    a plane with < 2 entries has no tile pairs."""
+    u0 = 0
+    for p, np_ in enumerate(plane_sizes):
+        if np_ < 2:
+            continue
+        nc = (np_ + chunk - 1) // chunk
+        T = (np_ + tile - 1) // tile
+        for I in range(T):
+            for J in range(I, T):
+                u = u0 + tile_pair_index(I, J, T)
+                for h in range(2):
+                    for b in range(2):
+                        i, j = 2 * I + h, 2 * J + b
+                        if i < nc and j < nc and j >= i and owner_planar(u, h, b, nshards) == shard:
+                            yield p, i, j
+        u0 += T * (T + 1) // 2
 
 
 def roi_cost(occupied_voxels: int, voxels: int) -> float:

@@ -236,7 +236,8 @@ def test_pruning_and_pass1_variants_identical(sc, golden, golden_arrays, cuda_de
     cases.append((synth.kits_like(tumor_mm=60.0), (0.8, 0.8, 1.0)))
     base = [sc.calculate_coefficients(a, sp).to_dict() for a, sp in cases]
     for opt, val in (("prune", 0), ("pass1_packed", 0), ("graphs", 0), ("fused_bbox", 0),
-                     ("pack_skip", 0), ("pack_tma_single", 1)):
+                     ("pack_skip", 0), ("pack_tma_single", 1),
+                     ("fused_bbox_single", 1)):
         with _native.thread_options(**{opt: val}):
             for (a, sp), want in zip(cases, base):
                 assert sc.calculate_coefficients(a, sp).to_dict() == want, opt
@@ -335,6 +336,23 @@ def test_c3_noisy_ellipsoid(sc, oracle_mod, cuda_device):
             if len(grp) >= 2:
                 best = max(best, _hull_max_sq(pts[grp][:, inplane], oracle_mod))
         assert rel_err(getattr(got, key), math.sqrt(best)) <= 1e-12, key
+    # SURVEY 8e pair-grid split: the shard entry at N = 2 / 4 / 8, run in
+    # sequence and MAX-combined, equals the full call bit for bit.
+    import torch
+
+    d = torch.from_numpy(arr).cuda()
+    full = sc.calculate_coefficients_device(d, (1.0, 1.0, 1.0)).to_dict()
+    assert full == got.to_dict()
+    sq = torch.zeros(4, dtype=torch.float64, device="cuda")
+    for n in (2, 4, 8):
+        best = torch.zeros(4, dtype=torch.float64, device="cuda")
+        for shard in range(n):
+            part = sc.calculate_coefficients_shard(d, (1.0, 1.0, 1.0), shard, n, sq)
+            assert part.vertex_count == full["VertexCount"]
+            assert part.triangle_count == got.triangle_count
+            torch.maximum(best, sq, out=best)
+        comb = [math.sqrt(v) for v in best.cpu().tolist()]
+        assert comb == [full[k] for k in DIAM_KEYS], n
 
 
 _OVERFLOW_SCRIPT = r"""
@@ -630,3 +648,92 @@ def test_cloud_diameters_grid_covers_every_tile_pair(sc, cuda_device):
     got = sc.diameters(xs, ys, zs)
     d3 = math.sqrt(200.0 ** 2 + 200.0 ** 2)
     assert got[0] == d3 and got[1] == d3
+
+
+def _lesion_field(seed, sp, diagonal):
+    """Many small lesions (radius 1.2-3 voxels) spread over a 512 x 512 field:
+    each plane family's maximum is a lesion diameter (a few mm) while the
+    pass-1 frame spans the whole field (R ~ 190 mm), the case where a margin
+    relative to the family maximum would not cover the fp32 error."""
+    rng = np.random.default_rng(seed)
+    nz = 14
+    arr = np.zeros((nz, 512, 512), dtype=np.uint8)
+    n = 48
+    if diagonal:  # no two lesions share an x or y row: XZ / YZ maxima = one lesion
+        t = np.sort(rng.choice(np.arange(8, 504, 9), size=n, replace=False))
+        cx, cy = t.astype(float), t[::-1].astype(float) if seed % 2 else t.astype(float)
+    else:
+        cx, cy = rng.uniform(6, 506, n), rng.uniform(6, 506, n)
+    zz, yy, xx = np.ogrid[:nz, :16, :16]
+    for x, y in zip(cx, cy):
+        r = rng.uniform(1.2, 3.0)
+        z = rng.uniform(4, nz - 5)
+        x0, y0 = int(x) - 8, int(y) - 8
+        blob = ((zz - z) ** 2 + (yy - (y - y0)) ** 2 + (xx - (x - x0)) ** 2) <= r * r
+        arr[:, y0:y0 + 16, x0:x0 + 16] |= blob.astype(np.uint8)
+    return arr, sp
+
+
+def test_planar_recheck_margin_on_spread_lesions(sc, oracle_mod, cuda_device):
+    """adversarial multi-lesion masks at 0.7421875 and 0.8
+    mm in-plane spacing (random and row-disjoint diagonal placements): the
+    re-check threshold is absolute in the frame extent (refine_tau), so every
+    diameter -- the XZ / YZ families above all -- is the reference's bit for
+    bit, through the single call and the device batch."""
+    import torch
+
+    cases = []
+    for seed in range(8):
+        for sp in ((0.7421875, 0.7421875, 1.0), (0.8, 0.8, 1.0)):
+            cases.append(_lesion_field(seed, sp, diagonal=seed >= 4))
+    wants = [oracle_mod.extract_features(a, sp, threads=0) for a, sp in cases]
+    ds = [torch.from_numpy(a).cuda() for a, _ in cases]
+    batch = sc.calculate_coefficients_device_batch(ds, [sp for _, sp in cases])
+    for (a, sp), want, b in zip(cases, wants, batch):
+        got = sc.calculate_coefficients(a, sp).to_dict()
+        assert got == b.to_dict()
+        assert got["VertexCount"] == want["VertexCount"]
+        for k in DIAM_KEYS:
+            assert got[k] == want[k], (k, sp, got[k], want[k])
+
+
+def test_c4_sample_against_reference_goldens(sc, cuda_device):
+    """12 of C4's 300 varied KiTS-like masks (every 25th of
+    kits_batch_params(300, 2025): nz 230-597, in-plane spacing 0.6-0.9 mm,
+    V 56 K - 184 K) through the device batch entry (mixed dims in one call)
+    and the host batch entry, against the records the reference itself
+    produced (tools/make_golden_c4.py): counts exact, diameters bit-exact,
+    area / volume within the north_star tolerance (1e-6 relative)."""
+    import hashlib
+    import json
+    import os
+
+    import torch
+
+    from conftest import GOLD
+    from paper_2510_02894_b200 import synth
+
+    with open(os.path.join(GOLD, "c4_golden.json")) as fh:
+        gold = json.load(fh)["cases"]
+    params = synth.kits_batch_params(300, 2025)
+    masks, sps = [], []
+    for g in gold:
+        m = synth.kits_from_params(params[g["index"]])
+        assert hashlib.sha256(m.tobytes()).hexdigest() == g["sha256"], g["index"]
+        masks.append(m)
+        sps.append(tuple(g["spacing"]))
+    ds = [torch.from_numpy(m).cuda() for m in masks]
+    dev = sc.calculate_coefficients_device_batch(ds, sps)
+    del ds
+    host = sc.calculate_coefficients_batch(masks, sps)
+    for g, d, h in zip(gold, dev, host):
+        want = g["features"]
+        for got in (d, h):
+            rec = got.to_dict()
+            assert rec["VertexCount"] == want["VertexCount"], g["index"]
+            assert got.triangle_count == g["triangle_count"], g["index"]
+            assert got.active_cubes == g["active_cubes"], g["index"]
+            for k in DIAM_KEYS:
+                assert rec[k] == want[k], (g["index"], k, rec[k], want[k])
+            for k in ("MeshVolume", "SurfaceArea"):
+                assert rel_err(rec[k], want[k]) <= REL_TOL, (g["index"], k)

@@ -107,3 +107,31 @@ def test_big_configs_match_reference(golden, oracle_mod, name):
     assert hashlib.sha256(arr.tobytes()).hexdigest() == case["sha256"]
     got = oracle_mod.extract_features(arr, case["spacing"], threads=0)
     check_record(got, case)
+
+
+def test_oracle_matches_c4_reference_golden(oracle_mod, golden):
+    """The C4 golden file (made by the reference itself) is pinned to the
+    oracle too: its smallest case (V = 56,188) bit for bit on counts and
+    diameters."""
+    import hashlib
+    import json
+    import os
+
+    from conftest import GOLD
+    from paper_2510_02894_b200 import synth
+
+    with open(os.path.join(GOLD, "c4_golden.json")) as fh:
+        cases = json.load(fh)["cases"]
+    g = min(cases, key=lambda c: c["features"]["VertexCount"])
+    m = synth.kits_from_params(synth.kits_batch_params(300, 2025)[g["index"]])
+    assert hashlib.sha256(m.tobytes()).hexdigest() == g["sha256"]
+    r = oracle_mod.extract_features(m, tuple(g["spacing"]), threads=0)
+    want = g["features"]
+    assert r["VertexCount"] == want["VertexCount"]
+    assert r["triangle_count"] == g["triangle_count"]
+    assert r["active_cubes"] == g["active_cubes"]
+    for k in ("Maximum3DDiameter", "Maximum2DDiameterXY", "Maximum2DDiameterXZ",
+              "Maximum2DDiameterYZ"):
+        assert r[k] == want[k], k
+    for k in ("MeshVolume", "SurfaceArea"):
+        assert abs(r[k] - want[k]) <= 1e-12 * abs(want[k]), k

@@ -1,7 +1,8 @@
 """Multi-rank host logic on CPU (gloo, world_size 2): ROI-batch assignment and
 the pair-grid shard + all_reduce(MAX) combine.  The per-shard compute is a CPU
-stub that follows the C engine's partition exactly (shard_range over the
-triangular tile grid), with the oracle's reference-arithmetic pair loop."""
+stub that follows the engine's partition exactly -- ownership by unit identity
+(sharding.owner_3d = prune.cu:457, sharding.owner_planar = planar.cu:251-252) --
+with the reference's pair arithmetic (features.py:140-148)."""
 
 import math
 import os
@@ -11,18 +12,30 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
-from paper_2510_02894_b200.sharding import assign_rois, shard_range
+from paper_2510_02894_b200.sharding import (assign_rois, owner_3d, shard_pairs_3d,
+                                            shard_pairs_planar, tile_pair_index)
 
 
-def test_shard_ranges_cover_exactly():
-    for n in (0, 1, 5, 17, 1000, 123457):
+def test_identity_ownership_partitions_every_pair_once():
+    for n in (1, 2, 127, 128, 129, 1000, 5000):
+        C = (n + 127) // 128
+        all_pairs = [(i, j) for i in range(C) for j in range(i, C)]
         for g in (1, 2, 3, 4, 8):
-            spans = [shard_range(n, s, g) for s in range(g)]
-            assert spans[0][0] == 0 and spans[-1][1] == n
-            for (a, b), (c, d) in zip(spans, spans[1:]):
-                assert b == c and a <= b
-            sizes = [b - a for a, b in spans]
-            assert max(sizes) - min(sizes) <= 1
+            got = sorted(p for s in range(g) for p in shard_pairs_3d(n, s, g))
+            assert got == all_pairs
+            assert [tile_pair_index(i, j, C) for i, j in all_pairs] == list(range(len(all_pairs)))
+            if len(all_pairs) >= g:  # balanced: shard sizes differ by <= 1
+                sizes = [sum(1 for _ in shard_pairs_3d(n, s, g)) for s in range(g)]
+                assert max(sizes) - min(sizes) <= 1
+    sizes = [0, 1, 2, 127, 128, 129, 255, 256, 257, 600, 1]
+    want = []
+    for p, m in enumerate(sizes):
+        nc = (m + 127) // 128 if m >= 2 else 0
+        want += [(p, i, j) for i in range(nc) for j in range(i, nc)]
+    for g in (1, 2, 3, 4, 8):
+        got = sorted(t for s in range(g) for t in shard_pairs_planar(sizes, s, g))
+        assert got == sorted(want), g
+    assert owner_3d(0, 0, 5, 4) == 0 and owner_3d(1, 1, 5, 4) == 5 % 4
 
 
 def test_lpt_assignment_balanced_and_complete():
@@ -36,44 +49,67 @@ def test_lpt_assignment_balanced_and_complete():
         assert max(loads) <= sum(costs) / g + max(costs)  # LPT bound
 
 
-def _tile_pairs(T):
-    return [(i, j) for i in range(T) for j in range(i, T)]
+def _planes(key):
+    """Engine plane order within one family: ascending key."""
+    return sorted(set(key.tolist()))
 
 
-def _shard_stub(pts, tile):
-    """CPU stand-in for sc_calculate_coefficients_shard: squared maxima over
-    this shard's tile pairs (3-D) and planes (planar), reference arithmetic."""
-    from oracle import oracle
-
+def _shard_stub(pts, chunk=8):
+    """CPU stand-in for sc_calculate_coefficients_shard on a point set: squared
+    maxima over this shard's 3-D chunk pairs and planar chunk pairs, owned by
+    identity as on the device (small chunks so the grid has many units)."""
     xs, ys, zs = pts
+    n = len(xs)
+
+    def sq_max(ii, jj, cols):
+        d = 0.0
+        for c in cols:
+            diff = c[jj][None, :] - c[ii][:, None]
+            d = d + diff * diff
+        return float(np.max(d)) if np.size(d) else 0.0
 
     def compute(shard, nshards, sq4):
-        n = len(xs)
-        T = (n + tile - 1) // tile
-        items = _tile_pairs(T)
-        a, b = shard_range(len(items), shard, nshards)
         m3 = 0.0
-        for (I, J) in items[a:b]:
-            ii = np.arange(I * tile, min(n, (I + 1) * tile))
-            jj = np.arange(J * tile, min(n, (J + 1) * tile))
-            dx = xs[jj][None, :] - xs[ii][:, None]
-            dy = ys[jj][None, :] - ys[ii][:, None]
-            dz = zs[jj][None, :] - zs[ii][:, None]
-            m3 = max(m3, float((dx * dx + dy * dy + dz * dz).max()))
-        planar = []
-        for key, (u, v) in ((zs, (xs, ys)), (ys, (xs, zs)), (xs, (ys, zs))):
-            planes = sorted(set(key.tolist()))
-            pa, pb = shard_range(len(planes), shard, nshards)
-            best = 0.0
-            for p in planes[pa:pb]:
-                sel = key == p
-                if sel.sum() >= 2:
-                    best = max(best, oracle.diameters(u[sel], v[sel], np.zeros(sel.sum()))[0] ** 2)
-            planar.append(best)
+        for i, j in shard_pairs_3d(n, shard, nshards, chunk=chunk):
+            ii = np.arange(i * chunk, min(n, (i + 1) * chunk))
+            jj = np.arange(j * chunk, min(n, (j + 1) * chunk))
+            m3 = max(m3, sq_max(ii, jj, (xs, ys, zs)))
+        # planes: XY (same z), XZ (same y), YZ (same x), each family in key order
+        fams = ((zs, (xs, ys)), (ys, (xs, zs)), (xs, (ys, zs)))
+        members, sizes, fam_of = [], [], []
+        for f, (key, _) in enumerate(fams):
+            for k in _planes(key):
+                idx = np.flatnonzero(key == k)
+                members.append(idx)
+                sizes.append(len(idx))
+                fam_of.append(f)
+        planar = [0.0, 0.0, 0.0]
+        for p, i, j in shard_pairs_planar(sizes, shard, nshards, chunk=chunk, tile=2 * chunk):
+            idx = members[p]
+            ii, jj = idx[i * chunk:(i + 1) * chunk], idx[j * chunk:(j + 1) * chunk]
+            f = fam_of[p]
+            planar[f] = max(planar[f], sq_max(ii, jj, fams[f][1]))
         sq4[0], sq4[1], sq4[2], sq4[3] = m3, planar[0], planar[1], planar[2]
         return {"VertexCount": n}
 
     return compute
+
+
+def test_identity_shards_combine_to_the_full_maxima(oracle_mod):
+    """Sequential shards + MAX == the reference's diameters, for N = 1..8."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    n = 300
+    pts = tuple((rng.integers(0, 12, size=n) * 0.5).astype(np.float64) for _ in range(3))
+    want = oracle_mod.diameters(*pts)
+    for g in (1, 2, 3, 4, 8):
+        acc = np.zeros(4)
+        for s in range(g):
+            sq4 = torch.zeros(4, dtype=torch.float64)
+            _shard_stub(pts)(s, g, sq4)
+            acc = np.maximum(acc, sq4.numpy())
+        assert tuple(math.sqrt(v) for v in acc) == tuple(want), g
 
 
 def _worker(rank, world, port, pts, want, q):
@@ -84,7 +120,7 @@ def _worker(rank, world, port, pts, want, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        rec = sharding.sharded_coefficients(None, (1, 1, 1), compute=_shard_stub(pts, tile=16))
+        rec = sharding.sharded_coefficients(None, (1, 1, 1), compute=_shard_stub(pts))
         got = [rec[k] for k in ("Maximum3DDiameter", "Maximum2DDiameterXY",
                                 "Maximum2DDiameterXZ", "Maximum2DDiameterYZ")]
         costs = [float(c) for c in range(1, 11)]
