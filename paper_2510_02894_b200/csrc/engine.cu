@@ -94,6 +94,9 @@ template <int MODE>
 __global__ void fp32_probe(float*, int, float, float);
 
 __global__ void empty_kernel();
+__global__ void canon_keys(const int4*, int4*, long long, const Stats*);
+__global__ void canon_copy_keys(const int4*, int4*, long long, const Stats*);
+__global__ void canon_planes(const int2*, int2*, const unsigned int*, const Stats*, int);
 }  // namespace sc
 
 using namespace sc;
@@ -287,6 +290,7 @@ struct Ctx {
   DevBuf<int4> plane_boxes_buf;
   DevBuf<int4> plane_hboxes;  // boxes of the two 64-entry halves of every in-plane chunk
   DevBuf<int2> plane_sorted;
+  DevBuf<int2> canon_tmp;  // shard entry: canonical planar order (canon_planes)
   DevBuf<uint8_t> mask_stage, raw_stage;
   double last_scan_ms = 0.0;      // host time (scan, + pack) of the last host-mask ROI
   double last_pure_scan_ms = 0.0; // its slab scan alone
@@ -335,7 +339,7 @@ struct Ctx {
                         work.p, warp_max.p, plane_umax.p,
                         plane_counts.p, plane_start.p, plane_tstart.p, plane_sorted.p,
                         plane_work.p, plane_cstart.p, pbin_counts.p, pbin_cursor.p,
-                        plane_ext.p, plane_boxes_buf.p, plane_hboxes.p};
+                        plane_ext.p, plane_boxes_buf.p, plane_hboxes.p, canon_tmp.p};
     for (const void* p : ps) h = (h ^ (unsigned long long)(uintptr_t)p) * 1099511628211ull;
     return h;
   }
@@ -431,7 +435,9 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
                                (const void*)diam_pass1<true>, (const void*)diam_pass1<false>,
                                (const void*)diam_refine, (const void*)cloud_diameters,
                                (const void*)plane_boxes,
-                               (const void*)plane_lb, (const void*)plane_filter};
+                               (const void*)plane_lb, (const void*)plane_filter,
+                               (const void*)canon_keys, (const void*)canon_copy_keys,
+                               (const void*)canon_planes};
       for (const void* k : kernels) CK(cudaFuncGetAttributes(&fa, k));
     }
     g_ctx[device][slot] = std::move(c);
@@ -703,6 +709,19 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
                                          c->plane_sorted.p, c->sort_counts.p + kSortBins));
   CKL(1);
   if (++nk >= lim) return SC_OK;
+  if (nshards > 1) {
+    // Shards own chunk pairs by identity: give every shard (every GPU) the
+    // same vertex order -- each bin's segment sorted by vertex key.
+    CK(launch_k(c, s, lgrid(c, 4), 256, canon_keys, c->keys_sorted.p, c->keys.p, dcap,
+                c->d_stats));
+    CK(launch_k(c, s, lgrid(c, 4), 256, canon_copy_keys, c->keys.p, c->keys_sorted.p, dcap,
+                c->d_stats));
+    CK(launch_k(c, s, lgrid(c, 4), 256, canon_planes, c->plane_sorted.p, c->canon_tmp.p,
+                c->plane_start.p, c->d_stats, 0));
+    CK(launch_k(c, s, lgrid(c, 4), 256, canon_planes, c->canon_tmp.p, c->plane_sorted.p,
+                c->plane_start.p, c->d_stats, 1));
+    CKL(4);
+  }
   // After the sort the 3-D chain (boxes -> filter) and the planar chain
   // (plane boxes -> bound -> filter) are independent: the planar one runs on
   // the slot's second stream (a fork / join inside the captured graph), so
@@ -961,6 +980,7 @@ int start_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
   const unsigned long long fp0 = c->fingerprint();
   int rc = ensure_buffers(c, nx, ny, nz, cap, dcap, punits, c->wcap_floor);
   if (rc) return rc;
+  if (nshards > 1) CK(c->canon_tmp.ensure((size_t)(3 * c->dcap_sz)));
   if (c->fingerprint() != fp0) {
     c->gen++;
     c->drop_graphs();

@@ -574,3 +574,118 @@ __global__ void __launch_bounds__(256) unit_expand(const int4* __restrict__ boxe
 }
 
 }  // namespace sc
+
+namespace sc {
+
+// ---- canonical vertex order (shard entry only) ------------------------------
+// scatter_all places the vertices of one brick bin (and the entries of one
+// in-plane bin) in atomic-arrival order, which differs run to run.  The pair-
+// grid shards of one ROI run on different GPUs (or one after another), and a
+// shard owns chunk pairs by their IDENTITY (prune.cu test_chunk_pair,
+// planar.cu plane_filter): that partition covers every vertex pair exactly
+// once only if every shard sees the same vertex -> chunk assignment.  These
+// kernels sort each bin's segment by the vertex key (a total order), so the
+// order after them is a function of the mask alone.  Segment bounds are found
+// from the data itself: bins are contiguous and ascending after the scatter.
+
+__device__ __forceinline__ bool key_less(int4 a, int4 b) {
+  if (a.z != b.z) return a.z < b.z;
+  if (a.y != b.y) return a.y < b.y;
+  return a.x < b.x;
+}
+
+__global__ void __launch_bounds__(256) canon_keys(const int4* __restrict__ in,
+                                                  int4* __restrict__ out, long long cap,
+                                                  const Stats* __restrict__ st) {
+  if (st->ovf) return;
+  const long long n = n_verts(st, cap);
+  int bb[6];
+#pragma unroll
+  for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
+  if (bb[3] < 0) return;
+  const int s = brick_shift(bb);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int4 k = in[i];
+    const unsigned int b = brick_bin(k.x, k.y, k.z, bb, s);
+    long long lo = i, hi = i + 1;
+    while (lo > 0) {
+      const int4 q = in[lo - 1];
+      if (brick_bin(q.x, q.y, q.z, bb, s) != b) break;
+      lo--;
+    }
+    while (hi < n) {
+      const int4 q = in[hi];
+      if (brick_bin(q.x, q.y, q.z, bb, s) != b) break;
+      hi++;
+    }
+    long long rank = 0;
+    for (long long j = lo; j < hi; j++) rank += key_less(in[j], k) ? 1 : 0;
+    out[lo + rank] = k;
+  }
+}
+
+__global__ void __launch_bounds__(256) canon_copy_keys(const int4* __restrict__ in,
+                                                       int4* __restrict__ out, long long cap,
+                                                       const Stats* __restrict__ st) {
+  if (st->ovf) return;
+  const long long n = n_verts(st, cap);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+__device__ __forceinline__ unsigned int inplane_bin(int2 e, int axis, const PlaneBricks& pb) {
+  // family 0 (XY): (X, Y); 1 (XZ): (X, Z); 2 (YZ): (Y, Z) -- as plane_bins
+  const int ia = axis == 2 ? 1 : 0, ib = axis == 0 ? 1 : 2;
+  const unsigned int ba = (unsigned int)(e.x - pb.lo[ia]) >> pb.shift[ia];
+  const unsigned int bbv = (unsigned int)(e.y - pb.lo[ib]) >> pb.shift[ib];
+  return spread2x4(ba) | (spread2x4(bbv) << 1);
+}
+
+// Planar entries: plane p of the entry at position i by binary search over
+// the plane offsets, then its (plane, in-plane bin) segment sorted by (a, b)
+// (distinct within a plane: the plane key is the vertex's third coordinate).
+// mode 0: sort `in` into `out`; mode 1: copy `in` back into `out`.
+__global__ void __launch_bounds__(256) canon_planes(const int2* __restrict__ in,
+                                                    int2* __restrict__ out,
+                                                    const unsigned int* __restrict__ start,
+                                                    const Stats* __restrict__ st, int mode) {
+  if (st->ovf) return;
+  int bb[6];
+#pragma unroll
+  for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
+  if (bb[3] < 0) return;
+  const PlaneSpace ps = plane_space(bb);
+  const PlaneBricks pbk = plane_bricks(bb);
+  const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
+  const long long total = start[P];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int2 e = in[i];
+    if (mode == 1) {
+      out[i] = e;
+      continue;
+    }
+    int lo_p = 0, hi_p = P;  // largest p with start[p] <= i
+    while (hi_p - lo_p > 1) {
+      const int mid = (lo_p + hi_p) >> 1;
+      if ((long long)start[mid] <= i) lo_p = mid; else hi_p = mid;
+    }
+    const int p = lo_p;
+    const int axis = plane_axis(p, ps);
+    const long long pb0 = start[p], pb1 = start[p + 1];
+    const unsigned int b = inplane_bin(e, axis, pbk);
+    long long lo = i, hi = i + 1;
+    while (lo > pb0 && inplane_bin(in[lo - 1], axis, pbk) == b) lo--;
+    while (hi < pb1 && inplane_bin(in[hi], axis, pbk) == b) hi++;
+    long long rank = 0;
+    for (long long j = lo; j < hi; j++) {
+      const int2 q = in[j];
+      rank += (q.x < e.x || (q.x == e.x && q.y < e.y)) ? 1 : 0;
+    }
+    out[lo + rank] = e;
+  }
+}
+
+}  // namespace sc

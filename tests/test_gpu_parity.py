@@ -660,10 +660,10 @@ def _lesion_field(seed, sp, diagonal):
     arr = np.zeros((nz, 512, 512), dtype=np.uint8)
     n = 48
     if diagonal:  # no two lesions share an x or y row: XZ / YZ maxima = one lesion
-        t = np.sort(rng.choice(np.arange(8, 504, 9), size=n, replace=False))
+        t = np.sort(rng.choice(np.arange(10, 500, 9), size=n, replace=False))
         cx, cy = t.astype(float), t[::-1].astype(float) if seed % 2 else t.astype(float)
     else:
-        cx, cy = rng.uniform(6, 506, n), rng.uniform(6, 506, n)
+        cx, cy = rng.uniform(10, 500, n), rng.uniform(10, 500, n)
     zz, yy, xx = np.ogrid[:nz, :16, :16]
     for x, y in zip(cx, cy):
         r = rng.uniform(1.2, 3.0)
