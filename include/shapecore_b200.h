@@ -85,15 +85,39 @@ int sc_calculate_coefficients(const uint8_t* mask, int64_t nx, int64_t ny, int64
 /* Typed mask payload straight from an NPY file: `data` is the
  * host payload of an array of NPY shape (s0, s1, s2) = (nz, ny, nx), C order
  * or Fortran order; dtype code 0 |b1, 1 |u1, 2 <i2, 3 <i4, 4 <i8, 5 <f4, 6 <f8
- * (reference volume.py:34-42).  Binarization runs on the device: with
- * has_label, voxels equal to the label (label_int for integer/bool codes,
- * label_float for float codes, already converted to the payload dtype) are
- * foreground, otherwise any nonzero voxel (volume.py:173-177).  h2d_ms covers
- * the copy and the binarization. */
+ * (reference volume.py:34-42).  With has_label, voxels equal to the label
+ * (label_int for integer/bool codes, label_float for float codes, already
+ * converted to the payload dtype) are foreground, otherwise any nonzero voxel
+ * (volume.py:173-177).
+ * Path: all host threads scan the payload once for its occupied extent over
+ * the two slowest axes (C order: z and y; Fortran order: x and y; option
+ * "host_crop"); only that slab crosses PCIe, in chunks of whole planes staged
+ * through two pinned buffers (the host copies chunk k+1 while chunk k is in
+ * flight; a pinned payload is copied directly), and each chunk is binarized on
+ * the device as it lands -- Fortran chunks through a shared-memory tile
+ * transpose.  h2d_ms covers the copies and the binarization, h2d_bytes the
+ * payload bytes that crossed PCIe, host_scan_ms the scan. */
 int sc_calculate_coefficients_raw(const void* data, int dtype, const int64_t shape[3],
                                   int fortran_order, int has_label, int64_t label_int,
                                   double label_float, const double spacing[3], int device,
                                   sc_coeffs* out);
+
+/* One typed payload of a raw batch (the arguments of sc_calculate_coefficients_raw). */
+typedef struct {
+  const void* data;
+  int dtype;
+  int fortran_order;
+  int has_label;
+  int64_t label_int;
+  double label_float;
+  int64_t shape[3]; /* NPY shape (nz, ny, nx) */
+} sc_raw_mask;
+
+/* Batch of typed payloads on one device, pipelined over the batch slots like
+ * sc_calculate_coefficients_batch (the host scan and staging of ROI i+1 overlap
+ * the device work of the ROIs in flight).  spacings[3*i..] per ROI. */
+int sc_calculate_coefficients_raw_batch(const sc_raw_mask* masks, const double* spacings,
+                                        int64_t count, int device, sc_coeffs* out);
 
 /* Device-resident mask on the CURRENT device; `stream` is a cudaStream_t.  The
  * ROI runs after all prior work on `stream`; NULL means the legacy default
@@ -122,6 +146,19 @@ int sc_calculate_coefficients_shard(const uint8_t* d_mask, int64_t nx, int64_t n
 int sc_calculate_coefficients_batch(const uint8_t* const* masks, const int64_t* dims,
                                     const double* spacings, int64_t count, int device,
                                     sc_coeffs* out);
+
+/* Batch of host ROIs fanned out over several devices (SURVEY 8b "batch entry
+ * fans out over devices internally"; replaces the reference's per-case loop,
+ * bench.py:122-182, and its worker pinning, dispatch.py:130-146): ROIs are
+ * placed on devices[0..ndev) by longest-processing-time on their byte size,
+ * one host thread per device entry runs the pipelined single-device batch
+ * on its share, and out[i] is ROI i's record whatever device ran it.  A
+ * device may be listed more than once (its shares then run one after the
+ * other).  The first failing share's code is returned; every ROI is still
+ * processed. */
+int sc_calculate_coefficients_batch_multi(const uint8_t* const* masks, const int64_t* dims,
+                                          const double* spacings, int64_t count,
+                                          const int* devices, int ndev, sc_coeffs* out);
 
 /* Same for device-resident masks on the CURRENT device (pipelined likewise).
  * The batch is ordered after prior work on `stream` (cudaStream_t; NULL = the

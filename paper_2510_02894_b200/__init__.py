@@ -41,7 +41,8 @@ from .mesh import (
     write_off,
     write_stl,
 )
-from .npy import coefficients_from_npy, load_npy, parse_npy_header
+from .npy import (coefficients_from_npy, coefficients_from_npy_batch, coefficients_from_payloads,
+                  load_npy, parse_npy_header)
 from .pipeline import BenchRecord, bench_run, emit_tsv, parse_tsv, render_tsv, run_pipeline
 from .synth import synth_mask
 from .timing import StageTimings
@@ -56,7 +57,8 @@ __all__ = [
     "calculate_coefficients_device", "calculate_coefficients_device_batch",
     "calculate_coefficients_shard", "diameters",
     "diameters_parallel", "extract_features", "mesh_vertices", "synth_mask",
-    "coefficients_from_npy", "load_npy", "parse_npy_header", "BenchRecord", "bench_run",
+    "coefficients_from_npy", "coefficients_from_npy_batch", "coefficients_from_payloads",
+    "load_npy", "parse_npy_header", "BenchRecord", "bench_run",
     "emit_tsv", "parse_tsv", "render_tsv", "run_pipeline", "TriangleMesh", "marching_cubes",
     "mesh_dump", "mesh_volume", "signed_mesh_volume", "surface_area", "write_off", "write_stl",
 ]

@@ -27,8 +27,10 @@ EXPORTED = (
     "sc_calculate_coefficients_device",
     "sc_calculate_coefficients_shard",
     "sc_calculate_coefficients_raw",
+    "sc_calculate_coefficients_raw_batch",
     "sc_calculate_coefficients_batch",
     "sc_calculate_coefficients_device_batch",
+    "sc_calculate_coefficients_batch_multi",
     "sc_diameters",
     "sc_mesh_vertices",
     "sc_marching_cubes",
@@ -45,6 +47,20 @@ EXPORTED = (
     "sc_abi_version",
     "sc_device_count",
 )
+
+
+class ScRawMask(ctypes.Structure):
+    """Mirror of `sc_raw_mask` (include/shapecore_b200.h)."""
+
+    _fields_ = [
+        ("data", ctypes.c_void_p),
+        ("dtype", ctypes.c_int),
+        ("fortran_order", ctypes.c_int),
+        ("has_label", ctypes.c_int),
+        ("label_int", ctypes.c_int64),
+        ("label_float", ctypes.c_double),
+        ("shape", ctypes.c_int64 * 3),
+    ]
 
 
 class ScCoeffs(ctypes.Structure):
@@ -98,6 +114,10 @@ def load():
         L.sc_calculate_coefficients_batch.argtypes = [ctypes.POINTER(u8p),
                                                       ctypes.POINTER(i64), dp, i64,
                                                       ctypes.c_int, cp]
+        L.sc_calculate_coefficients_batch_multi.argtypes = [ctypes.POINTER(u8p),
+                                                            ctypes.POINTER(i64), dp, i64,
+                                                            ctypes.POINTER(ctypes.c_int),
+                                                            ctypes.c_int, cp]
         L.sc_calculate_coefficients_device_batch.argtypes = [ctypes.POINTER(ctypes.c_void_p),
                                                              ctypes.POINTER(i64), dp, i64,
                                                              ctypes.c_void_p, cp]
@@ -105,6 +125,8 @@ def load():
                                                     ctypes.POINTER(i64), ctypes.c_int,
                                                     ctypes.c_int, i64, ctypes.c_double, dp,
                                                     ctypes.c_int, cp]
+        L.sc_calculate_coefficients_raw_batch.argtypes = [ctypes.POINTER(ScRawMask), dp, i64,
+                                                          ctypes.c_int, cp]
         L.sc_diameters.argtypes = [dp, dp, dp, i64, ctypes.c_int, dp]
         L.sc_mesh_vertices.argtypes = [u8p, i64, i64, i64, ctypes.c_int,
                                        ctypes.POINTER(ctypes.c_int32), i64,

@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <array>
 #include <functional>
 #include <memory>
@@ -73,8 +74,8 @@ __global__ void plane_filter(const unsigned int*, const unsigned int*, const uns
                              uint2*, const int4*);
 __global__ void cloud_diameters(const double*, const double*, const double*, long long,
                                 long long, unsigned long long*);
-int launch_binarize(const void*, int, const long long[3], int, int, long long, double, uint8_t*,
-                    int, cudaStream_t);
+int launch_binarize(const void*, int, int, long long, long long, long long, int, int, int,
+                    long long, double, uint8_t*, int, cudaStream_t);
 __global__ void mesh_count(const RoiParams*, const uint32_t*, const Stats*, unsigned int*);
 __global__ void scan_blocks(unsigned int*, long long, unsigned int*);
 __global__ void scan_sums(unsigned int*, int, unsigned long long*);
@@ -291,7 +292,10 @@ struct Ctx {
   DevBuf<int4> plane_hboxes;  // boxes of the two 64-entry halves of every in-plane chunk
   DevBuf<int2> plane_sorted;
   DevBuf<int2> canon_tmp;  // shard entry: canonical planar order (canon_planes)
-  DevBuf<uint8_t> mask_stage, raw_stage;
+  DevBuf<uint8_t> mask_stage, raw_stage;  // raw_stage: two chunk buffers (typed payloads)
+  uint8_t* h_raw = nullptr;               // pinned staging of typed payload chunks (two halves)
+  size_t h_raw_cap = 0;                   // bytes
+  cudaEvent_t cev[2] = {};                // DMA out of h_raw half k finished
   double last_scan_ms = 0.0;      // host time (scan, + pack) of the last host-mask ROI
   double last_pure_scan_ms = 0.0; // its slab scan alone
   long long last_h2d_bytes = 0;   // bytes that crossed PCIe for it
@@ -396,6 +400,7 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     CK(cudaFuncSetAttribute(pack_bits_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
     CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
+    for (auto& e : c->cev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     for (auto& e : c->kev) CK(cudaEventCreate(&e));
     CK(cudaMalloc(&c->d_stats, sizeof(Stats)));
@@ -1250,13 +1255,120 @@ int stage_host_mask(Ctx* c, const uint8_t* mask, int64_t nx, int64_t ny, int64_t
   return SC_OK;
 }
 
+// Typed NPY payload -> the slot's uint8 mask stage (sc_calculate_coefficients_raw*):
+// host scan for the occupied slab over the payload's two slowest axes, then
+// the slab in chunks of whole planes through two pinned staging halves (the
+// host copies chunk k+1 while chunk k's DMA runs; a pinned payload is copied
+// directly), each chunk binarized on the device right behind its copy.  The
+// mask stage then holds the slab in C order with dims (*cx, *cy, *cz) and
+// origin org in the payload's grid.
+int stage_host_raw(Ctx* c, const sc_raw_mask& m, cudaStream_t s, int64_t* cx, int64_t* cy,
+                   int64_t* cz, int org[3]) {
+  static const int itemsize[7] = {1, 1, 2, 4, 8, 4, 8};
+  const int isz = itemsize[m.dtype];
+  const int64_t nz = m.shape[0], ny = m.shape[1], nx = m.shape[2];
+  const bool F = m.fortran_order != 0;
+  const int64_t planes = F ? nx : nz, rows = ny, row_elems = F ? nz : nx;
+  const int64_t row_bytes = row_elems * isz;
+  int64_t p0 = 0, p1 = planes - 1, r0 = 0, r1 = rows - 1;
+  c->prepacked = false;
+  c->last_split = false;
+  c->last_scan_ms = c->last_pure_scan_ms = 0.0;
+  c->last_scan_bytes = 0;
+  if (c->o.crop) {
+    const double t0 = wall_ms();
+    const Slab sl = occupied_slab_typed(m.data, m.dtype, row_elems, rows, planes, m.has_label,
+                                        m.label_int, m.label_float, c->o.host_threads);
+    c->last_scan_ms = c->last_pure_scan_ms = wall_ms() - t0;
+    c->last_scan_bytes = sl.bytes_read;
+    if (sl.empty) {
+      set_err("mask has no occupied voxels");
+      return SC_ERR_EMPTY_ROI;
+    }
+    p0 = sl.z0; p1 = sl.z1; r0 = sl.y0; r1 = sl.y1;
+    if (F && nx % 32 == 0) {  // keep x 32-aligned: the slab stays on the 128-bit pack path
+      p0 &= ~(int64_t)31;
+      p1 = std::min(planes - 1, ((p1 + 32) & ~(int64_t)31) - 1);
+    }
+  }
+  const int64_t np = p1 - p0 + 1, nr = r1 - r0 + 1;
+  const int64_t width = nr * row_bytes, pitch = rows * row_bytes;  // slab / payload plane bytes
+  const uint8_t* src = static_cast<const uint8_t*>(m.data) + p0 * pitch + r0 * row_bytes;
+  if (!F) {
+    *cx = nx; *cy = nr; *cz = np;
+    org[0] = 0; org[1] = (int)r0; org[2] = (int)p0;
+  } else {
+    *cx = np; *cy = nr; *cz = nz;
+    org[0] = (int)p0; org[1] = (int)r0; org[2] = 0;
+  }
+  CK(c->mask_stage.ensure((size_t)(np * nr * row_elems)));
+  const int64_t kChunkBytes = 4LL << 20;
+  const int64_t per = std::max<int64_t>(1, kChunkBytes / std::max<int64_t>(1, width));
+  const int64_t chunk = per * width;
+  CK(c->raw_stage.ensure((size_t)(2 * chunk)));
+  cudaPointerAttributes attr{};
+  const bool pinned = cudaPointerGetAttributes(&attr, m.data) == cudaSuccess &&
+                      attr.type == cudaMemoryTypeHost;
+  (void)cudaGetLastError();  // pageable memory may report an error on older drivers
+  if (!pinned && (size_t)(2 * chunk) > c->h_raw_cap) {
+    if (c->h_raw) CK(cudaFreeHost(c->h_raw));
+    c->h_raw = nullptr;
+    c->h_raw_cap = 0;
+    CK(cudaMallocHost(&c->h_raw, (size_t)(2 * chunk)));
+    c->h_raw_cap = (size_t)(2 * chunk);
+  }
+  CK(cudaEventRecord(c->ev[0], s));
+  int64_t idx = 0;
+  for (int64_t a = 0; a < np; a += per, idx++) {
+    const int64_t b = std::min(np, a + per), bytes = (b - a) * width;
+    uint8_t* dev = c->raw_stage.p + (idx & 1) * chunk;  // reused in stream order
+    if (pinned) {
+      CK(cudaMemcpy2DAsync(dev, (size_t)width, src + a * pitch, (size_t)pitch, (size_t)width,
+                           (size_t)(b - a), cudaMemcpyHostToDevice, s));
+    } else {
+      uint8_t* hb = c->h_raw + (idx & 1) * chunk;
+      if (idx >= 2) CK(cudaEventSynchronize(c->cev[idx & 1]));  // its previous DMA is done
+      copy_rows(hb, src + a * pitch, pitch, width, b - a, c->o.host_threads);
+      CK(cudaMemcpyAsync(dev, hb, (size_t)bytes, cudaMemcpyHostToDevice, s));
+      CK(cudaEventRecord(c->cev[idx & 1], s));
+    }
+    const int rc = F ? launch_binarize(dev, m.dtype, 1, b - a, nr, row_elems, (int)np, (int)a,
+                                       m.has_label, m.label_int, m.label_float,
+                                       c->mask_stage.p, c->sms * 4, s)
+                     : launch_binarize(dev, m.dtype, 0, b - a, nr, row_elems, 0, 0, m.has_label,
+                                       m.label_int, m.label_float,
+                                       c->mask_stage.p + a * nr * row_elems, c->sms * 4, s);
+    if (rc) {
+      set_err("unsupported element type code %d", m.dtype);
+      return SC_ERR_INPUT;
+    }
+    CKL(1);
+  }
+  CK(cudaEventRecord(c->ev[1], s));
+  c->last_h2d_bytes = np * width;
+  c->last_slab_bytes = np * width;
+  return SC_OK;
+}
+
+int check_raw(const sc_raw_mask& m) {
+  if (m.dtype < 0 || m.dtype > 6) {
+    set_err("unsupported element type code %d", m.dtype);
+    return SC_ERR_INPUT;
+  }
+  if (!m.data) {
+    set_err("payload pointer is NULL");
+    return SC_ERR_INPUT;
+  }
+  return SC_OK;
+}
+
 // Pipelined batch over the slots of `device` (option "slots", default 8): ROI i+1 is enqueued (H2D copy
 // included for host masks) before ROI i is collected, so copies, kernels and
 // the host round trip of neighbouring ROIs overlap.  The first failing ROI's
 // code is returned; every other ROI is still processed.
 int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
               const double* spacings, int64_t count, bool host, sc_coeffs* out,
-              cudaStream_t user) {
+              cudaStream_t user, const sc_raw_mask* raws = nullptr) {
   if (count < 0 || (count > 0 && (!masks || !dims || !spacings || !out))) {
     set_err("bad batch arguments");
     return SC_ERR_INPUT;
@@ -1336,7 +1448,8 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
       o->host_scan_ms = c->last_scan_ms;
       c->last_ms[6] = o->h2d_ms;
       const int64_t j = idx[k];
-      note_host_rates(c, dims[3 * j] * dims[3 * j + 1] * dims[3 * j + 2], o->h2d_ms);
+      if (!raws)  // (typed payloads do not feed the uint8 split-read balance)
+        note_host_rates(c, dims[3 * j] * dims[3 * j + 1] * dims[3 * j + 2], o->h2d_ms);
     }
     o->total_ms = wall_ms() - t_start[k];
     idx[k] = -1;
@@ -1364,7 +1477,13 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
     const uint8_t* dm = masks[i];
     int64_t cx = nx, cy = ny, cz = nz;
     int org[3] = {0, 0, 0};
-    if (host) {
+    if (raws) {
+      if ((rc = check_raw(raws[i])) || (rc = stage_host_raw(c, raws[i], s, &cx, &cy, &cz, org))) {
+        note(rc);
+        continue;
+      }
+      dm = c->mask_stage.p;
+    } else if (host) {
       CK(c->mask_stage.ensure((size_t)nx * ny * nz));
       rc = stage_host_mask(c, masks[i], nx, ny, nz, s, &cy, &cz, org);
       if (rc) { note(rc); continue; }
@@ -1646,14 +1765,13 @@ int sc_calculate_coefficients_raw(const void* data, int dtype, const int64_t sha
                                   double label_float, const double spacing[3], int device,
                                   sc_coeffs* out) {
   const double t0 = wall_ms();
-  static const int itemsize[7] = {1, 1, 2, 4, 8, 4, 8};
-  if (!shape || dtype < 0 || dtype > 6) {
-    set_err("unsupported element type code %d", dtype);
-    return SC_ERR_INPUT;
-  }
-  const int64_t nx = shape[2], ny = shape[1], nz = shape[0];
-  int rc = check_input(data, nx, ny, nz, spacing);
+  if (!shape) { set_err("shape pointer is NULL"); return SC_ERR_INPUT; }
+  sc_raw_mask m{data, dtype, fortran_order, has_label, label_int, label_float,
+                {shape[0], shape[1], shape[2]}};
+  int rc = check_raw(m);
   if (rc) return rc;
+  const int64_t nx = shape[2], ny = shape[1], nz = shape[0];
+  if ((rc = check_input(data, nx, ny, nz, spacing))) return rc;
   if (!out) { set_err("out is NULL"); return SC_ERR_INPUT; }
   Ctx* c;
   if ((rc = get_ctx(device, &c))) return rc;
@@ -1661,33 +1779,104 @@ int sc_calculate_coefficients_raw(const void* data, int dtype, const int64_t sha
   c->o = snapshot_opts();
   CK(cudaSetDevice(device));
   std::memset(out, 0, sizeof *out);
-  const size_t n = (size_t)nx * ny * nz, raw_bytes = n * itemsize[dtype];
-  CK(c->raw_stage.ensure(raw_bytes));
-  CK(c->mask_stage.ensure(n));
   cudaStream_t s = c->stream;
-  CK(cudaEventRecord(c->ev[0], s));
-  CK(cudaMemcpyAsync(c->raw_stage.p, data, raw_bytes, cudaMemcpyHostToDevice, s));
-  const long long shp[3] = {(long long)shape[0], (long long)shape[1], (long long)shape[2]};
-  if (launch_binarize(c->raw_stage.p, dtype, shp, fortran_order ? 1 : 0, has_label ? 1 : 0,
-                      (long long)label_int, label_float, c->mask_stage.p, c->sms * 8, s)) {
-    set_err("unsupported element type code %d", dtype);
-    return SC_ERR_INPUT;
-  }
-  CKL(1);
-  CK(cudaEventRecord(c->ev[1], s));
-  c->prepacked = false;
-  rc = run_roi(c, c->mask_stage.p, nx, ny, nz, spacing, s, 0, 1, nullptr, out);
+  int64_t cx = nx, cy = ny, cz = nz;
+  int org[3] = {0, 0, 0};
+  if ((rc = stage_host_raw(c, m, s, &cx, &cy, &cz, org))) return rc;
+  rc = run_roi(c, c->mask_stage.p, cx, cy, cz, spacing, s, 0, 1, nullptr, out, org);
   out->h2d_ms = ev_ms(c->ev[0], c->ev[1]);
-  out->h2d_bytes = (int64_t)raw_bytes;
+  out->h2d_bytes = c->last_h2d_bytes;
+  out->host_scan_ms = c->last_scan_ms;
   c->last_ms[6] = out->h2d_ms;
   out->total_ms = wall_ms() - t0;
   return rc;
+}
+
+int sc_calculate_coefficients_raw_batch(const sc_raw_mask* masks, const double* spacings,
+                                        int64_t count, int device, sc_coeffs* out) {
+  if (count < 0 || (count > 0 && (!masks || !spacings || !out))) {
+    set_err("bad batch arguments");
+    return SC_ERR_INPUT;
+  }
+  std::vector<const uint8_t*> ptrs((size_t)count);
+  std::vector<int64_t> dims((size_t)(3 * count));
+  for (int64_t i = 0; i < count; i++) {
+    ptrs[(size_t)i] = static_cast<const uint8_t*>(masks[i].data);
+    dims[(size_t)(3 * i)] = masks[i].shape[2];
+    dims[(size_t)(3 * i + 1)] = masks[i].shape[1];
+    dims[(size_t)(3 * i + 2)] = masks[i].shape[0];
+  }
+  return run_batch(device, ptrs.data(), dims.data(), spacings, count, true, out, nullptr, masks);
 }
 
 int sc_calculate_coefficients_batch(const uint8_t* const* masks, const int64_t* dims,
                                     const double* spacings, int64_t count, int device,
                                     sc_coeffs* out) {
   return run_batch(device, masks, dims, spacings, count, true, out, nullptr);
+}
+
+int sc_calculate_coefficients_batch_multi(const uint8_t* const* masks, const int64_t* dims,
+                                          const double* spacings, int64_t count,
+                                          const int* devices, int ndev, sc_coeffs* out) {
+  if (count < 0 || ndev < 1 || !devices || (count > 0 && (!masks || !dims || !spacings || !out))) {
+    set_err("bad batch arguments");
+    return SC_ERR_INPUT;
+  }
+  if (count == 0) return SC_OK;
+  // LPT over the devices by streamed bytes (the HBM pass sets the per-ROI
+  // floor; V is unknown before marching cubes): largest ROI first onto the
+  // least-loaded device.  One host thread per device entry runs the
+  // pipelined single-device batch on its share; results land in input order.
+  std::vector<int64_t> order((size_t)count);
+  for (int64_t i = 0; i < count; i++) order[(size_t)i] = i;
+  auto bytes = [&](int64_t i) {
+    return std::max<int64_t>(1, dims[3 * i]) * std::max<int64_t>(1, dims[3 * i + 1]) *
+           std::max<int64_t>(1, dims[3 * i + 2]);
+  };
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int64_t a, int64_t b) { return bytes(a) > bytes(b); });
+  std::vector<std::vector<int64_t>> share((size_t)ndev);
+  std::vector<double> load((size_t)ndev, 0.0);
+  for (int64_t i : order) {
+    const size_t d = (size_t)(std::min_element(load.begin(), load.end()) - load.begin());
+    share[d].push_back(i);
+    load[d] += (double)bytes(i);
+  }
+  for (auto& v : share) std::sort(v.begin(), v.end());  // each share in input order
+  const Opts opts = snapshot_opts();  // the caller's options, for every worker thread
+  std::vector<int> rcs((size_t)ndev, SC_OK);
+  std::vector<std::string> errs((size_t)ndev);
+  std::vector<std::thread> workers;
+  for (int d = 0; d < ndev; d++) {
+    if (share[(size_t)d].empty()) continue;
+    workers.emplace_back([&, d] {
+      t_opts = opts;
+      t_opts_on = true;
+      const std::vector<int64_t>& mine = share[(size_t)d];
+      std::vector<const uint8_t*> m(mine.size());
+      std::vector<int64_t> dm(3 * mine.size());
+      std::vector<double> sp(3 * mine.size());
+      std::vector<sc_coeffs> o(mine.size());
+      for (size_t k = 0; k < mine.size(); k++) {
+        m[k] = masks[mine[k]];
+        for (int a = 0; a < 3; a++) {
+          dm[3 * k + a] = dims[3 * mine[k] + a];
+          sp[3 * k + a] = spacings[3 * mine[k] + a];
+        }
+      }
+      rcs[(size_t)d] = run_batch(devices[d], m.data(), dm.data(), sp.data(), (int64_t)mine.size(),
+                                 true, o.data(), nullptr);
+      if (rcs[(size_t)d]) errs[(size_t)d] = g_err;
+      for (size_t k = 0; k < mine.size(); k++) out[mine[k]] = o[k];
+    });
+  }
+  for (auto& t : workers) t.join();
+  for (int d = 0; d < ndev; d++)
+    if (rcs[(size_t)d]) {
+      g_err = errs[(size_t)d];
+      return rcs[(size_t)d];
+    }
+  return SC_OK;
 }
 
 int sc_calculate_coefficients_device_batch(const uint8_t* const* d_masks, const int64_t* dims,

@@ -222,4 +222,105 @@ Slab occupied_slab(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, int 
   return out;
 }
 
+namespace {
+
+template <typename T>
+bool row_has(const uint8_t* p, int64_t n, T label) {
+  T v;
+  bool any = false;
+  for (int64_t i = 0; i < n; i++) {
+    std::memcpy(&v, p + i * (int64_t)sizeof(T), sizeof(T));
+    any |= v == label;
+  }
+  return any;
+}
+
+}  // namespace
+
+Slab occupied_slab_typed(const void* data, int dtype, int64_t row_elems, int64_t rows,
+                         int64_t planes, int has_label, int64_t label_i, double label_f,
+                         int threads) {
+  static const int itemsize[7] = {1, 1, 2, 4, 8, 4, 8};
+  const int isz = itemsize[dtype];
+  const uint8_t* base = static_cast<const uint8_t*>(data);
+  if (!has_label)  // any nonzero byte: the uint8 scanner over rows of row_elems * isz bytes
+    return occupied_slab(base, row_elems * isz, rows, planes, threads);
+  struct Part {
+    int64_t z0 = INT64_MAX, z1 = -1, y0 = INT64_MAX, y1 = -1, read = 0;
+  };
+  const int64_t row_bytes = row_elems * isz, plane = row_bytes * rows;
+  auto row_any = [&](const uint8_t* p) -> bool {
+    switch (dtype) {
+      case 0: case 1: return row_has<uint8_t>(p, row_elems, (uint8_t)label_i);
+      case 2: return row_has<int16_t>(p, row_elems, (int16_t)label_i);
+      case 3: return row_has<int32_t>(p, row_elems, (int32_t)label_i);
+      case 4: return row_has<int64_t>(p, row_elems, (int64_t)label_i);
+      case 5: return row_has<float>(p, row_elems, (float)label_f);
+      default: return row_has<double>(p, row_elems, label_f);
+    }
+  };
+  const int64_t per = std::max<int64_t>(1, (int64_t(1) << 20) / std::max<int64_t>(1, plane));
+  const int64_t ntask = (planes + per - 1) / per;
+  std::vector<Part> parts((size_t)ntask);
+  auto scan = [&](int64_t t) {
+    Part& r = parts[(size_t)t];
+    for (int64_t z = t * per; z < std::min(planes, (t + 1) * per); z++) {
+      const uint8_t* s = base + z * plane;
+      int64_t lo = -1;
+      for (int64_t y = 0; y < rows; y++)
+        if (row_any(s + y * row_bytes)) { lo = y; break; }
+      if (lo < 0) { r.read += plane; continue; }
+      int64_t hi = lo;
+      for (int64_t y = rows - 1; y > lo; y--)
+        if (row_any(s + y * row_bytes)) { hi = y; break; }
+      r.read += (lo + 1 + (rows - hi)) * row_bytes;
+      r.z0 = std::min(r.z0, z); r.z1 = std::max(r.z1, z);
+      r.y0 = std::min(r.y0, lo); r.y1 = std::max(r.y1, hi);
+    }
+  };
+  const int nt = std::max(1, threads);
+  if (nt == 1 || ntask == 1) {
+    for (int64_t t = 0; t < ntask; t++) scan(t);
+  } else {
+    pool().run(ntask, nt, scan);
+  }
+  Part all;
+  for (const Part& r : parts) {
+    all.z0 = std::min(all.z0, r.z0); all.z1 = std::max(all.z1, r.z1);
+    all.y0 = std::min(all.y0, r.y0); all.y1 = std::max(all.y1, r.y1);
+    all.read += r.read;
+  }
+  Slab out;
+  out.empty = all.z1 < 0;
+  out.z0 = out.empty ? 0 : all.z0;
+  out.z1 = out.empty ? -1 : all.z1;
+  out.y0 = out.empty ? 0 : all.y0;
+  out.y1 = out.empty ? -1 : all.y1;
+  out.bytes_read = all.read;
+  return out;
+}
+
+void copy_rows(void* dst, const void* src, int64_t pitch, int64_t width, int64_t nrows,
+               int threads) {
+  uint8_t* d = static_cast<uint8_t*>(dst);
+  const uint8_t* s = static_cast<const uint8_t*>(src);
+  // tasks of ~1 MB
+  const int64_t per = std::max<int64_t>(1, (int64_t(1) << 20) / std::max<int64_t>(1, width));
+  const int64_t ntask = (nrows + per - 1) / per;
+  auto job = [&](int64_t t) {
+    const int64_t a = t * per, b = std::min(nrows, a + per);
+    if (pitch == width) {
+      std::memcpy(d + a * width, s + a * pitch, (size_t)((b - a) * width));
+      return;
+    }
+    for (int64_t r = a; r < b; r++) std::memcpy(d + r * width, s + r * pitch, (size_t)width);
+  };
+  const int nt = std::max(1, threads);
+  if (nt == 1 || ntask == 1) {
+    for (int64_t t = 0; t < ntask; t++) job(t);
+  } else {
+    pool().run(ntask, nt, job);
+  }
+}
+
 }  // namespace sc

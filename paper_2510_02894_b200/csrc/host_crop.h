@@ -31,4 +31,22 @@ Slab occupied_slab(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, int 
 void pack_slab(const uint8_t* mask, int64_t nx, int64_t ny, int64_t z0, int64_t z1, int64_t y0,
                int64_t y1, uint32_t* out, int threads);
 
+// Typed NPY payloads (sc_calculate_coefficients_raw*): the occupied extent
+// over the payload's two slowest axes, i.e. `planes` x `rows` rows of
+// `row_elems` elements each (C order: z, y rows of x; Fortran order: x, y
+// rows of z).  Without a label an element is occupied iff it is nonzero; the
+// test runs on the raw bytes (any nonzero byte), exact for the integer and
+// bool codes and conservative for floats (-0.0 counts: the slab only has to
+// contain every occupied voxel; the device binarize is exact).  With a label,
+// elements equal to it (already in the payload dtype) are occupied.  dtype
+// codes as sc_calculate_coefficients_raw.  Slab::z0/z1 = planes, y0/y1 = rows.
+Slab occupied_slab_typed(const void* data, int dtype, int64_t row_elems, int64_t rows,
+                         int64_t planes, int has_label, int64_t label_i, double label_f,
+                         int threads);
+
+// memcpy of `nrows` rows of `width` bytes (source pitch `pitch`) into a
+// contiguous destination, on up to `threads` host threads.
+void copy_rows(void* dst, const void* src, int64_t pitch, int64_t width, int64_t nrows,
+               int threads);
+
 }  // namespace sc

@@ -201,8 +201,11 @@ def calculate_coefficients_shard(mask, spacing: Sequence[float], shard: int, nsh
 
 
 def calculate_coefficients_batch(masks: Sequence, spacings: Sequence[Sequence[float]],
-                                 device: int = 0) -> List[Coefficients]:
-    """C4: many host ROIs on one device, one C call."""
+                                 device: int = 0,
+                                 devices: Optional[Sequence[int]] = None) -> List[Coefficients]:
+    """C4: many host ROIs in one C call -- on `device`, or fanned out over
+    `devices` inside the library (sc_calculate_coefficients_batch_multi: LPT
+    placement, one host thread per device); records come back in input order."""
     bufs, dims = [], []
     for m in masks:
         data, d = _as_mask(m)
@@ -214,6 +217,13 @@ def calculate_coefficients_batch(masks: Sequence, spacings: Sequence[Sequence[fl
         *[b.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)) for b in bufs])
     dims_arr = np.asarray(dims, dtype=np.int64)
     outs = (_native.ScCoeffs * n)()
+    if devices is not None:
+        devs = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
+        rc = _native.load().sc_calculate_coefficients_batch_multi(
+            ptrs, dims_arr.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+            sp.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), n, devs, len(devices), outs)
+        _native.raise_for(rc, "sc_calculate_coefficients_batch_multi")
+        return _from_structs(outs)
     rc = _native.load().sc_calculate_coefficients_batch(
         ptrs, dims_arr.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
         sp.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), n, int(device), outs)

@@ -188,3 +188,24 @@ def test_null_stream_means_legacy_default_stream(sc, cuda_device):
     from paper_2510_02894_b200.features import _from_struct
 
     assert _from_struct(out).to_dict() == want
+
+
+def test_batch_multi_fans_out_in_input_order(sc, cuda_device):
+    """sc_calculate_coefficients_batch_multi: LPT fan-out over a device list
+    inside the C ABI; on one GPU the list repeats device 0 (two / three host
+    worker threads sharing it) -- records equal the single-device batch, in
+    input order, and an input error in one ROI leaves the others computed."""
+    from paper_2510_02894_b200 import errors
+
+    cases = _masks()
+    masks, sps = [a for a, _ in cases], [sp for _, sp in cases]
+    want = [c.to_dict() for c in sc.calculate_coefficients_batch(masks, sps)]
+    for devs in ([0], [0, 0], [0, 0, 0]):
+        got = sc.calculate_coefficients_batch(masks, sps, devices=devs)
+        assert [g.to_dict() for g in got] == want, devs
+    bad = list(sps)
+    bad[3] = (1.0, -1.0, 1.0)
+    with pytest.raises(errors.ShapeCoreError):
+        sc.calculate_coefficients_batch(masks, bad, devices=[0, 0])
+    with pytest.raises((ValueError, errors.ShapeCoreError)):
+        sc.calculate_coefficients_batch(masks, sps, devices=[0, 57])  # no such device
