@@ -227,6 +227,9 @@ int sc_last_diagnostics(int device, int64_t* out, int n);
  * them mesh_ms / diameters_ms come from the %globaltimer stamps);
  * "pack_tma" (1) / "pack_tma_single" (0) = CTAs per SM of the cp.async.bulk
  * (TMA) pack in batch entries / single calls (0 = the 128-bit-load pack);
+ * "pack_chain" (4) = batch entries: a ROI starts only once the pack of the ROI
+ * 4 places earlier has finished, so at most 4 HBM passes run at a time and the
+ * latency-bound kernels of earlier ROIs overlap them (0 = unchained);
  * "fused_bbox" (1) / "fused_bbox_single" (0) = the pack accumulates the
  * occupied bbox itself (else a separate pass over the bit volume), in batch
  * entries / single calls;

@@ -127,6 +127,11 @@ struct Opts {
   bool pack_skip = true;     // sparse pack: no conversion of all-zero segments
   int pack_tma = 1;          // batch graphs: TMA bulk-copy pack, CTAs per SM (0 = 128-bit loads)
   int pack_tma_single = 0;   // the same for single calls (the 128-bit-load pack is faster alone)
+  int pack_chain = 4;        // batch: ROI i's graph starts after ROI i - pack_chain's pack
+                             // (at most pack_chain HBM passes in flight; 0 = unchained).
+                             // C2 / C4 / C5 K=200 us per ROI, chain 0 / 1 / 2 / 3 / 4 / 8:
+                             // 33.0 / 57.9 / 34.5 / 29.4 / 29.7 / 32.3, 34.7 / 59.6 / 39.0 /
+                             // 32.5 / 32.0 / 33.8, 26.3 / 31.0 / 25.0 / 25.3 / 25.4 / 26.1
   bool fork = true;          // planar chain on a second stream
   bool zc = true;            // "zero_copy": RoiParams / Stats via mapped host memory
   int stage_times = 0;       // single-call graph events: 0 none (timer stamps), 1 mesh/diam, 2 all
@@ -261,6 +266,8 @@ struct Ctx {
   cudaEvent_t ev[6] = {};
   cudaEvent_t kev[10] = {};     // per-kernel boundaries of the last ROI
   cudaStream_t stream2 = nullptr;  // planar branch of the ROI graph (fork / join)
+  cudaEvent_t pack_ev = nullptr;   // batch pack chain: recorded after this slot's pack
+  cudaEvent_t chain_wait = nullptr;  // ... and this slot's ROI waits on another slot's
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   double last_ms[7] = {0, 0, 0, 0, 0, 0, 0};  // pack, mc, prune, pass1, refine, planar, h2d
   bool times_pending = false;  // last_ms[0..5] still to be read from kev[]
@@ -325,6 +332,7 @@ struct Ctx {
     bool fork;          // option "fork"
     bool zc;            // option "zero_copy"
     bool prepacked;     // bit volume packed on the host (no pack kernel)
+    cudaEvent_t chain;  // pack-chain event waited on (nullptr: none)
     unsigned long long gen;
     cudaGraphExec_t exec;
     unsigned long long launches;
@@ -401,6 +409,7 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
     for (auto& e : c->cev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->pack_ev, cudaEventDisableTiming));
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     for (auto& e : c->kev) CK(cudaEventCreate(&e));
     CK(cudaMalloc(&c->d_stats, sizeof(Stats)));
@@ -601,6 +610,17 @@ cudaError_t launch_k(const Ctx* c, cudaStream_t s, int grid, int block, void (*k
   return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
+// Batch pack chain (option "pack_chain"): the end of this slot's HBM pass is
+// marked on pack_ev, and the ROI waits for another slot's mark before it
+// starts, so the packs of consecutive ROIs run one (or pack_chain) at a time
+// at the full HBM rate while the latency-bound kernels of earlier ROIs
+// overlap them.  Inside a capture both are external event nodes.
+cudaError_t chain_mark(Ctx* c, cudaStream_t s) {
+  if (!c->chain_wait) return cudaSuccess;
+  return c->capturing ? cudaEventRecordWithFlags(c->pack_ev, s, cudaEventRecordExternal)
+                      : cudaEventRecord(c->pack_ev, s);
+}
+
 // Enqueue one whole ROI on stream s; no host synchronisation.  Everything
 // ROI-specific (mask pointer, dims, spacing) is read by the kernels from the
 // slot's RoiParams record, so the enqueued sequence -- and a graph captured
@@ -617,6 +637,8 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   // keeps the previous map)
   const bool clear_map = c->o.sparse && !(c->o.pack_mode & 4) && !c->prepacked;
   const bool zc = zero_copy_records(c);
+  if (c->chain_wait)
+    CK(cudaStreamWaitEvent(s, c->chain_wait, c->capturing ? cudaEventWaitExternal : 0));
   init_stats<<<clear_map ? 8 : 1, 256, 0, s>>>(c->d_stats, c->segmap.p,
                                                clear_map ? (long long)c->segmap.cap : 0LL,
                                                zc ? c->h_rp_dev : nullptr, c->d_rp);
@@ -629,6 +651,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   CK(record(c, c->kev[0], s));  // kev0..kev1 = the HBM pass alone
   if (c->prepacked) {  // the host already wrote the bit volume: bbox pass only
     CK(record(c, c->kev[1], s));
+    CK(chain_mark(c, s));
     CK(launch_k(c, s, lgrid(c, 4), 256, bits_bbox, rp, reinterpret_cast<const uint4*>(c->bits.p),
                 c->d_stats, c->segmap.p));
     CKL(1);
@@ -641,6 +664,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
     CKL(1);
     if (++nk >= lim) return SC_OK;
     CK(record(c, c->kev[1], s));
+    CK(chain_mark(c, s));
   } else if (fast && c->o.fbox && !(c->o.pack_mode & 4)) {
     pack_bits_v16<4, true><<<c->sms * std::max(1, c->occ_pack), 256, 0, s>>>(rp, c->bits.p,
                                                                               c->d_stats,
@@ -648,6 +672,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
     CKL(1);
     if (++nk >= lim) return SC_OK;
     CK(record(c, c->kev[1], s));
+    CK(chain_mark(c, s));
   } else if (fast) {
     // pack_mode bit 0: one 4 KB step per block (grid covers the slot's largest
     // mask; extra blocks exit) instead of a persistent grid, so blocks retire
@@ -677,6 +702,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
     }
     if (++nk >= lim) return SC_OK;
     CK(record(c, c->kev[1], s));
+    CK(chain_mark(c, s));
     CK(launch_k(c, s, lgrid(c, 4), 256, bits_bbox, rp, reinterpret_cast<const uint4*>(c->bits.p),
                                          c->d_stats, c->segmap.p));
     CKL(1);
@@ -687,6 +713,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
     CKL(1);
     if (++nk >= lim) return SC_OK;
     CK(record(c, c->kev[1], s));
+    CK(chain_mark(c, s));
   }
   CK(launch_k(c, s, lgrid(c, std::max(1, c->occ_mc)), 256, mc_cells, rp, c->bits.p, c->d_tabs, c->d_stats,
                                                           c->keys.p, cap, c->sort_counts.p,
@@ -917,7 +944,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
         g.grid_div == c->grid_div &&
         g.events == c->events_on && g.ev_full == c->ev_full && g.pdl == c->o.pdl &&
         g.sparse == c->o.sparse && g.fork == c->o.fork &&
-        g.zc == c->o.zc && g.prepacked == c->prepacked &&
+        g.zc == c->o.zc && g.prepacked == c->prepacked && g.chain == c->chain_wait &&
         g.gen == c->gen) {
       CK(cudaGraphLaunch(g.exec, s));
       if (hp) g_hprof.launch += wall_ms() - t0;
@@ -948,7 +975,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
                     c->o.pack_mode + 32 * c->o.pack_bps + 4096 * c->o.pack_tma,
                     c->grid_div,
                     c->events_on, c->ev_full, c->o.pdl, c->o.sparse,
-                    c->o.fork, c->o.zc, c->prepacked, c->gen, exec, launches};
+                    c->o.fork, c->o.zc, c->prepacked, c->chain_wait, c->gen, exec, launches};
   c->graphs.push_back(g);
   CK(cudaGraphLaunch(exec, s));
   g_launches.fetch_add(launches, std::memory_order_relaxed);
@@ -1387,12 +1414,20 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
   // nodes = cheaper launches); the slots go back to single-call mode after.
   struct EventsMode {
     Ctx** cs; int n;
-    ~EventsMode() { for (int k = 0; k < n; k++) cs[k]->events_on = cs[k]->ev_full = true; }
+    ~EventsMode() {
+      for (int k = 0; k < n; k++) {
+        cs[k]->events_on = cs[k]->ev_full = true;
+        cs[k]->chain_wait = nullptr;
+      }
+    }
   } events_mode{cs, nslots};
   for (int k = 0; k < nslots; k++) {
     cs[k]->o = opts;
     cs[k]->events_on = cs[k]->ev_full = opts.batch_times;
     cs[k]->grid_div = opts.grid_div;
+    // slots are used round-robin: slot k's ROI follows slot k - pack_chain's
+    cs[k]->chain_wait = (opts.pack_chain > 0 && opts.pack_chain < nslots)
+                            ? cs[(k - opts.pack_chain + nslots) % nslots]->pack_ev : nullptr;
   }
   CK(cudaSetDevice(device));
   // Device masks: order the batch after prior work on the caller's stream;
@@ -1674,6 +1709,7 @@ int set_opt(Opts& o, const char* name, int value) {
   else if (std::strcmp(name, "zero_copy") == 0) o.zc = value != 0;
   else if (std::strcmp(name, "stage_times") == 0) o.stage_times = std::max(0, std::min(2, value));
   else if (std::strcmp(name, "pack_tma") == 0) o.pack_tma = std::max(0, std::min(3, value));
+  else if (std::strcmp(name, "pack_chain") == 0) o.pack_chain = std::max(0, std::min(8, value));
   else if (std::strcmp(name, "pack_tma_single") == 0) o.pack_tma_single = std::max(0, std::min(3, value));
   else if (std::strcmp(name, "sparse_bits") == 0) o.sparse = value != 0;
   else if (std::strcmp(name, "pack_skip") == 0) o.pack_skip = value != 0;
