@@ -655,7 +655,9 @@ def run_ours(args):
                 "call of B ROIs per step",
         "roi_ceiling": ceiling(us_roi, step_bytes),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d_bytes * B),
-                "d2h_bytes_per_step": 16800 * B,  # one Stats record per ROI (mapped pinned)
+                # per ROI the last kernel publishes the merged record (2,504 B: the
+                # summed case histogram + the tail of sc::Stats) to mapped pinned memory
+                "d2h_bytes_per_step": 2504 * B,
                 "path": "sc_calculate_coefficients_batch (C ABI) from pinned host memory, B ROIs "
                         "per step: host scan of every mask byte for the occupied z/y slab "
                         "(host_threads), then only that slab crosses PCIe",

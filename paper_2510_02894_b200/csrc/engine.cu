@@ -472,12 +472,10 @@ int check_input(const void* mask, int64_t nx, int64_t ny, int64_t nz, const doub
     set_err("dims beyond 2^20 per axis are not supported");
     return SC_ERR_INPUT;
   }
-  // Planar work entries index in-plane 128-vertex chunks with 16 bits, and a
-  // plane holds at most ~2 vertices per voxel of the grid face it spans.
-  const int64_t face = std::max(nx * ny, std::max(nx * nz, ny * nz));
-  if (2 * face > 65535LL * 128) {
-    set_err("grid faces above %lld voxels are not supported (largest face %lld)",
-            65535LL * 64, (long long)face);
+  // (the planar chunk-index width is checked per plane at run time: scan_all
+  // sets Stats::plane_ovf, finish_roi reports it)
+  if (((nx + 31) / 32) * ny * nz >= (1LL << 32)) {  // bit-volume word indices are 32-bit
+    set_err("masks above 2^37 voxels are not supported");
     return SC_ERR_INPUT;
   }
   if (!sp) { set_err("spacing pointer is NULL"); return SC_ERR_INPUT; }
@@ -1058,6 +1056,11 @@ int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
   if (c->h_stats->bbox[3] < 0) {
     set_err("mask has no occupied voxels");
     return SC_ERR_EMPTY_ROI;
+  }
+  if (c->h_stats->plane_ovf) {
+    set_err("a plane of the mesh holds more than %lld vertices (planar chunk index width)",
+            kPlaneMaxEntries);
+    return SC_ERR_INPUT;
   }
   if ((long long)c->h_stats->n_super > (long long)c->slist.cap) {
     // cannot happen with slist sized from kSingleLevelMax; never report a

@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kDiamThreads) diam_refine(
   // memory; the last block to finish publishes the complete record there, so
   // no device->host copy follows the ROI's graph.
   // The case histogram goes out merged (hist[0] = sum of the kHistCopies
-  // copies, marked by hist_merged), so ~2.7 KB cross PCIe instead of 16.8 KB.
+  // copies, marked by hist_merged), so 2.5 KB cross PCIe instead of 16.8 KB.
   if (out_host && last_block(&st->done2)) {
     const volatile unsigned long long* s = reinterpret_cast<const volatile unsigned long long*>(st);
     unsigned long long* d = reinterpret_cast<unsigned long long*>(out_host);

@@ -97,7 +97,15 @@ __global__ void __launch_bounds__(kScanThreads) scan_all(unsigned int* __restric
         cur[k] = run;
         run += v[k];
       }
-      if (lane == 31) plane_counts[p] = incl;
+      if (lane == 31) {
+        plane_counts[p] = incl;
+        // planar work entries index a plane's 128-entry chunks with 16 bits:
+        // a larger plane stops the ROI (the host reports it as an input error)
+        if ((long long)incl > kPlaneMaxEntries) {
+          st->plane_ovf = 1u;
+          st->ovf = 1u;
+        }
+      }
       if (lane < 8) pext[(long long)p * 8 + lane] = 0ull;
     }
     __shared__ bool s_last;

@@ -30,7 +30,7 @@ struct Stats {
   unsigned long long ext[26];          // packed (projection, index) of 13-direction extremes
   unsigned long long lb;               // fp64 bits: exact squared distance lower bound
   unsigned long long n_work;           // surviving 3-D work units after pruning
-  unsigned int done1, done2;           // done1: scan_all plane-block ticket; done2 spare
+  unsigned int done1, done2;           // scan_all plane-block / diam_refine tickets
   unsigned int ovf;                    // V exceeded the diameter-side buffers: skip the rest
   unsigned int done3;                  // boxes_extremes block ticket (last block: the 3-D LB)
   unsigned long long plb[3];           // fp64 bits: exact planar lower bounds per family
@@ -43,6 +43,8 @@ struct Stats {
   // stage (scan_all start), end of the diameters (last diam_refine block):
   // mesh_ms / diameters_ms without event nodes in the graph.
   unsigned long long t_start, t_mesh, t_end;
+  unsigned int plane_ovf;              // a plane holds more than kPlaneMaxEntries entries
+  unsigned int pad_;
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -182,6 +184,11 @@ __device__ __forceinline__ void plane_ids(int X, int Y, int Z, const PlaneSpace&
 constexpr int kPlaneBins = 256;
 constexpr int kPlaneTile = 256;   // in-plane tile edge (first level of plane_filter)
 constexpr int kPlaneChunk = 128;  // in-plane chunk edge (planar pair unit)
+// Planar work entries hold a plane's chunk indices in 16 bits each, so one
+// plane can hold at most this many entries (mesh vertices in that plane; a
+// plane's vertices lie on its cross-section contours, far below the bound for
+// any real mask).  scan_all checks it per plane at run time.
+constexpr long long kPlaneMaxEntries = 65536LL * kPlaneChunk;
 
 __device__ __forceinline__ int axis_shift(int lo, int hi) {  // voxel bbox [lo, hi]
   const int ext = 2 * (hi - lo) + 3;

@@ -737,3 +737,29 @@ def test_c4_sample_against_reference_goldens(sc, cuda_device):
                 assert rec[k] == want[k], (g["index"], k, rec[k], want[k])
             for k in ("MeshVolume", "SurfaceArea"):
                 assert rel_err(rec[k], want[k]) <= REL_TOL, (g["index"], k)
+
+
+def test_large_face_grid_against_oracle(sc, oracle_mod, cuda_device):
+    """no up-front refusal of large grid faces (2048 x 2048
+    slices); the planar chunk-index width is checked per plane at run time.
+    A 2048 x 2048 x 8 mask with blobs spread over the slice equals the oracle
+    (counts exact, diameters bit-exact)."""
+    rng = np.random.default_rng(3)
+    arr = np.zeros((8, 2048, 2048), np.uint8)
+    zz, yy, xx = np.ogrid[:8, :24, :24]
+    for _ in range(40):
+        y0, x0 = (int(v) for v in rng.integers(8, 2048 - 32, size=2))
+        r = rng.uniform(2.0, 3.4)
+        blob = ((zz - 3.5) ** 2 + (yy - 12) ** 2 + (xx - 12) ** 2) <= r * r
+        arr[:, y0:y0 + 24, x0:x0 + 24] |= blob.astype(np.uint8)
+    sp = (0.3, 0.3, 2.0)
+    want = oracle_mod.extract_features(arr, sp, threads=0)
+    for got in (sc.calculate_coefficients(arr, sp),
+                sc.calculate_coefficients_batch([arr, arr], [sp, sp])[1]):
+        rec = got.to_dict()
+        assert rec["VertexCount"] == want["VertexCount"]
+        assert got.triangle_count == want["triangle_count"]
+        for k in DIAM_KEYS:
+            assert rec[k] == want[k], k
+        for k in ("MeshVolume", "SurfaceArea"):
+            assert rel_err(rec[k], want[k]) <= REL_TOL, k
