@@ -245,6 +245,10 @@ template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t cap = 0;  // elements
+  // Grow-only.  Fresh memory is zeroed once: the sparse bit volume reads words
+  // of unwritten segments together with their (clear) map bit and discards
+  // them, and those reads must not touch uninitialised memory
+  // (compute-sanitizer initcheck).
   cudaError_t ensure(size_t n) {
     if (n <= cap) return cudaSuccess;
     if (p) cudaFree(p);
@@ -252,6 +256,7 @@ struct DevBuf {
     cap = 0;
     size_t want = n + n / 4 + 1024;
     cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+    if (e == cudaSuccess) e = cudaMemset(p, 0, want * sizeof(T));
     if (e == cudaSuccess) cap = want;
     return e;
   }

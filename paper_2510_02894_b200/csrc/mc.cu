@@ -443,10 +443,14 @@ __device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits,
     if (sparse) {
       // segments of words q and q - 1 (one map word unless they straddle one)
       const long long wc = rb + q, wp = wc - 1;
-      const uint32_t mc = __ldg(segmap + (wc >> 9));
-      const uint32_t mp = ((wp >> 9) == (wc >> 9)) ? mc : __ldg(segmap + (wp >> 9));
-      if (!((mc >> ((wc >> 4) & 31)) & 1u)) cur = 0u;
-      if (!((mp >> ((wp >> 4) & 31)) & 1u)) prev = 0u;
+      if (q < W) {
+        const uint32_t mc = __ldg(segmap + (wc >> 9));
+        if (!((mc >> ((wc >> 4) & 31)) & 1u)) cur = 0u;
+      }
+      if (q > 0) {  // (word q - 1 exists: wp >= rb >= 0)
+        const uint32_t mp = __ldg(segmap + (wp >> 9));
+        if (!((mp >> ((wp >> 4) & 31)) & 1u)) prev = 0u;
+      }
     }
   }
 }
