@@ -66,9 +66,6 @@ def test_input_validation_without_gpu(native):
     bad = (ctypes.c_double * 3)(1.0, -1.0, 1.0)
     rc = lib.sc_calculate_coefficients(buf, 2, 2, 2, bad, 0, ctypes.byref(out))
     assert rc == native.SC_ERR_INPUT and "spacing" in native.last_error()
-    # planar chunk indices are 16-bit: grid faces beyond ~4.19 M voxels are refused
-    rc = lib.sc_calculate_coefficients(buf, 4096, 2048, 2, sp, 0, ctypes.byref(out))
-    assert rc == native.SC_ERR_INPUT and "faces" in native.last_error()
     dp = ctypes.POINTER(ctypes.c_double)
     out4 = (ctypes.c_double * 4)()
     rc = lib.sc_diameters(None, None, None, 0, 0, out4)
