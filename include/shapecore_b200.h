@@ -193,9 +193,11 @@ int sc_last_kernel_times(int device, double* ms, int n);
 /* Work counters of the last ROI on `device`: {3-D work units kept, 3-D work
  * units total, 3-D fp64 re-check candidates, planar tile pairs total, planar
  * re-check candidates, planar units kept, 3-D 64 x 64 sub-pairs evaluated,
- * planar 64 x 64 sub-pairs evaluated}; a unit is a 128 x 128 chunk pair, of
- * which pass 1 evaluates the listed 64 x 64 sub-pairs.  Returns how many were
- * written (<= 8). */
+ * planar 64 x 64 sub-pairs listed, 3-D pair slots pass 1 evaluated after its
+ * vertex filter, planar pair slots pass 1 evaluated}; a unit is a 128 x 128
+ * chunk pair, of which pass 1 evaluates the vertices of the listed 64 x 64
+ * sub-pairs that can reach the lower bound.  Returns how many were written
+ * (<= 10). */
 int sc_last_diagnostics(int device, int64_t* out, int n);
 /* Options.  Every call takes a snapshot of the options at entry, so changing
  * them never affects a call already in flight.  sc_set_option sets the

@@ -206,13 +206,14 @@ def probe_fp32_peak(device: int = 0, mode: int = 0) -> float:
 
 
 DIAG_NAMES = ("work_units", "total_units", "refine_candidates", "planar_units",
-              "planar_candidates", "planar_work_units", "work_subunits", "planar_work_subunits")
+              "planar_candidates", "planar_work_units", "work_subunits", "planar_work_subunits",
+              "pass1_pairs", "pass1_planar_pairs")
 PAIRS_PER_UNIT = 128 * 128
 
 
 def last_diagnostics(device: int = 0) -> dict:
-    buf = (ctypes.c_int64 * 8)()
-    n = load().sc_last_diagnostics(int(device), buf, 8)
+    buf = (ctypes.c_int64 * len(DIAG_NAMES))()
+    n = load().sc_last_diagnostics(int(device), buf, len(DIAG_NAMES))
     if n < 0:
         raise_for(-n, "sc_last_diagnostics")
     return {k: int(buf[i]) for i, k in enumerate(DIAG_NAMES[:n])}

@@ -61,7 +61,8 @@ __global__ void unit_expand(const int4*, long long, const RoiParams*, int, int, 
 template <bool PACKED>
 __global__ void diam_pass1(const int4*, long long, const RoiParams*, const uint2*, float*,
                            const int2*, const unsigned int*, const uint2*, long long, float*,
-                           Stats*);
+                           Stats*, const int4*, const int4*, int, const unsigned int*,
+                           const int4*, const int4*);
 __global__ void diam_refine(const int4*, long long, const RoiParams*, const uint2*, const float*,
                             const int2*, const unsigned int*, const uint2*, long long,
                             const float*, Stats*, Stats*);
@@ -277,7 +278,7 @@ struct Ctx {
   double last_ms[7] = {0, 0, 0, 0, 0, 0, 0};  // pack, mc, prune, pass1, refine, planar, h2d
   bool times_pending = false;  // last_ms[0..5] still to be read from kev[]
   long long cap_floor = 0, dcap_floor = 0, wcap_floor = 0;  // raised by overflow re-runs only
-  long long last_diag[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long last_diag[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   int occ_pass1 = 1, occ_pass1s = 1, occ_pack = 1, occ_mc = 1;  // blocks/SM
   int prio_lo = 0, prio_hi = 0;  // stream priority range (least, greatest)
   Stats* d_stats = nullptr;
@@ -369,7 +370,7 @@ struct Ctx {
 // Two independent pipeline slots per device (stream, events, scratch, graphs):
 // single-ROI calls use slot 0; batch calls alternate slots so the H2D copy and
 // kernels of ROI i+1 overlap the tail and the host round trip of ROI i.
-constexpr int kSlots = 32;
+constexpr int kSlots = 64;
 std::mutex g_ctx_mu;
 std::vector<std::array<std::unique_ptr<Ctx>, kSlots>> g_ctx;
 
@@ -818,11 +819,14 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   if (c->o.packed)
     CK(launch_k(c, s, pgrid, 256, diam_pass1<true>, c->keys_sorted.p, dcap, rp, c->work.p,
                 c->warp_max.p, c->plane_sorted.p, c->plane_start.p, c->plane_work.p, pucap,
-                c->plane_umax.p, c->d_stats));
+                c->plane_umax.p, c->d_stats, c->boxes.p, c->hboxes.p, prune, c->plane_cstart.p,
+                c->plane_boxes_buf.p, c->plane_hboxes.p));
   else
     CK(launch_k(c, s, pgrid, 256, diam_pass1<false>, c->keys_sorted.p, dcap, rp, c->work.p, c->warp_max.p,
                                             c->plane_sorted.p, c->plane_start.p, c->plane_work.p,
-                                            pucap, c->plane_umax.p, c->d_stats));
+                                            pucap, c->plane_umax.p, c->d_stats, c->boxes.p,
+                                            c->hboxes.p, prune, c->plane_cstart.p,
+                                            c->plane_boxes_buf.p, c->plane_hboxes.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[5], s));
@@ -1089,6 +1093,8 @@ int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
     c->last_diag[5] = (long long)h.n_pwork;
     c->last_diag[6] = (long long)h.n_sub;
     c->last_diag[7] = (long long)h.n_psub;
+    c->last_diag[8] = (long long)h.n_eval;
+    c->last_diag[9] = (long long)h.n_peval;
   }
   if (c->events_on) {
     out->mesh_ms = ev_ms(c->kev[0], c->kev[2]);
@@ -1700,7 +1706,7 @@ int set_opt(Opts& o, const char* name, int value) {
   if (std::strcmp(name, "prune") == 0) o.prune = value != 0;
   else if (std::strcmp(name, "pass1_packed") == 0) o.packed = value != 0;
   else if (std::strcmp(name, "graphs") == 0) o.graphs = value != 0;
-  else if (std::strcmp(name, "slots") == 0) o.slots = std::max(1, std::min(32, value));
+  else if (std::strcmp(name, "slots") == 0) o.slots = std::max(1, std::min(kSlots, value));
   else if (std::strcmp(name, "dcap") == 0) o.dcap = std::max(256, value);
   else if (std::strcmp(name, "wcap") == 0) o.wcap = std::max(1, value);
   else if (std::strcmp(name, "fused_bbox") == 0) o.fbox = value != 0;
@@ -2104,7 +2110,7 @@ int sc_last_diagnostics(int device, int64_t* out, int n) {
   if (rc) return -rc;
   std::lock_guard<std::mutex> lk(c->mu);
   c->o = snapshot_opts();
-  int m = n < 8 ? n : 8;
+  int m = n < 10 ? n : 10;
   for (int i = 0; i < m; i++) out[i] = c->last_diag[i];
   return m;
 }

@@ -33,38 +33,194 @@ constexpr int kPC = kPlaneChunk;  // in-plane chunk edge (pair unit = chunk x ch
 constexpr int kPR = kPC / 32;     // 4 i entries per lane
 static_assert(kPC == kChunk, "the fused pass-1 kernel shares one smem chunk per warp");
 
+// Vertex-level reach filter of pass 1.  A vertex p of chunk I can only be
+// an end of a pair of unit (I, J) reaching LB if its squared max distance to
+// J's box reaches LB: reach(p, box J) >= |p - q| for every q in J, and the
+// maximum pair has |p* - q*|^2 = D^2 >= LB.  reach is formed in fp32 on the
+// same frame coordinates as pass 1: a frame coordinate is off by <= 2u|t|
+// (the int -> float is exact, one rounding each for h and the product), a
+// box-side difference by <= 6u R_a, its square by <= 28u R_a^2, the FMA sum
+// adds <= 8u R^2: |error| <= 36 u R^2 < kReachMargin R^2.  Dropping only
+// vertices below LB - kReachMargin R^2 keeps both ends of the maximum pair,
+// so the unit holding it still reaches refine_tau and is re-checked in fp64
+// (the re-check itself always evaluates the full unit).
+constexpr double kReachMargin = 64.0 / 16777216.0;
+
+struct FBox {  // chunk (or half-chunk) box in pass-1 frame coordinates
+  float lx, ly, lz, hx, hy, hz;
+};
+
+__device__ __forceinline__ FBox frame_box(int4 lo, int4 hi, const Frame& f) {
+  FBox b;
+  b.lx = (float)(lo.x - f.cx2) * f.hx; b.hx = (float)(hi.x - f.cx2) * f.hx;
+  b.ly = (float)(lo.y - f.cy2) * f.hy; b.hy = (float)(hi.y - f.cy2) * f.hy;
+  b.lz = (float)(lo.z - f.cz2) * f.hz; b.hz = (float)(hi.z - f.cz2) * f.hz;
+  return b;
+}
+
+__device__ __forceinline__ float reach_sq(float3 p, const FBox& b) {
+  const float dx = fmaxf(p.x - b.lx, b.hx - p.x), dy = fmaxf(p.y - b.ly, b.hy - p.y),
+              dz = fmaxf(p.z - b.lz, b.hz - p.z);
+  return fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+}
+
+// Box of chunk c restricted to its 64-vertex halves selected by `halves`
+// (bit h = half h; 3 = the whole chunk).
+__device__ __forceinline__ FBox half_box(const int4* __restrict__ boxes,
+                                         const int4* __restrict__ hboxes, int c,
+                                         unsigned int halves, const Frame& f) {
+  if (halves == 3u) return frame_box(boxes[2 * c], boxes[2 * c + 1], f);
+  const int h = halves == 2u ? 1 : 0;
+  return frame_box(hboxes[4 * c + 2 * h], hboxes[4 * c + 2 * h + 1], f);
+}
+
+// Stream-compact this lane's candidate into buf (warp-uniform count n).
+__device__ __forceinline__ void warp_append(float4* buf, int& n, bool keep, float4 v) {
+  const unsigned int bal = __ballot_sync(0xffffffffu, keep);
+  if (keep) buf[n + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = v;
+  n += __popc(bal);
+}
+
+// Max over i entries si[i0 .. i0 + 64 P) (clamped to ni: repeats are
+// harmless) x the j list sj[0, nj2) of the dot-form pass-1 value; lane
+// holds P packed i pairs (i0 + 64 p + {0, 32} + lane).
+template <int P>
+__device__ __forceinline__ float eval_rows(const float4* __restrict__ si,
+                                           const float4* __restrict__ sj, int i0, int ni,
+                                           int nj2) {
+  const int lane = threadIdx.x & 31;
+  float2 a2[P], b2[P], c2[P];
+  float n0[P], n1[P], m0[P], m1[P];
+#pragma unroll
+  for (int p = 0; p < P; p++) {
+    const float4 e0 = si[min(i0 + 64 * p + lane, ni - 1)];
+    const float4 e1 = si[min(i0 + 64 * p + 32 + lane, ni - 1)];
+    a2[p] = make_float2(-2.f * e0.x, -2.f * e1.x);
+    b2[p] = make_float2(-2.f * e0.y, -2.f * e1.y);
+    c2[p] = make_float2(-2.f * e0.z, -2.f * e1.z);
+    n0[p] = e0.w;
+    n1[p] = e1.w;
+    m0[p] = m1[p] = -3.0e38f;
+  }
+#pragma unroll 4
+  for (int j = 0; j < nj2; j += 2) {
+    const float4 q0 = sj[j], q1 = sj[j + 1];
+#pragma unroll
+    for (int p = 0; p < P; p++) {
+      float2 t0 = __ffma2_rn(a2[p], make_float2(q0.x, q0.x), make_float2(q0.w, q0.w));
+      float2 t1 = __ffma2_rn(a2[p], make_float2(q1.x, q1.x), make_float2(q1.w, q1.w));
+      t0 = __ffma2_rn(b2[p], make_float2(q0.y, q0.y), t0);
+      t1 = __ffma2_rn(b2[p], make_float2(q1.y, q1.y), t1);
+      t0 = __ffma2_rn(c2[p], make_float2(q0.z, q0.z), t0);
+      t1 = __ffma2_rn(c2[p], make_float2(q1.z, q1.z), t1);
+      m0[p] = fmax3f(m0[p], t0.x, t1.x);
+      m1[p] = fmax3f(m1[p], t0.y, t1.y);
+    }
+  }
+  float best = 0.f;
+#pragma unroll
+  for (int p = 0; p < P; p++) best = fmaxf(best, fmaxf(m0[p] + n0[p], m1[p] + n1[p]));
+  return best;
+}
+
 // Pass 1 (see header).  Work unit = one surviving chunk pair (I <= J, 128 x
 // 128 vertex pairs, listed by unit_filter / unit_expand with the mask of its
-// 64 x 64 sub-pairs to evaluate); every WARP is an independent
-// worker with its own shared-memory copy of the J chunk, so load balance is
-// per unit and no block barrier is involved.  Error of the dot form: in the
-// bbox-centred frame |p| <= D*sqrt(3)/2, so the absolute error is
-// < ~12 * 2^-24 * D^2.
+// 64 x 64 sub-pairs that can reach LB); every WARP is an independent worker,
+// so load balance is per unit and no block barrier is involved.  Error of the
+// dot form: in the bbox-centred frame |p| <= R, absolute error <= 35 u R^2.
 //
-// PACKED: two i vertices share one FFMA2 (the j coordinate is the broadcast
-// scalar operand), so 4 pairs cost 6 FFMA2 + 2 FMNMX3 = 2 issue slots per
-// pair instead of 3.5 for scalar FFMA.
-template <bool PACKED>
+// FILTER (the product path): the warp first keeps only the vertices of each
+// side whose reach to the other side's (sub-pair-selected) box can attain LB
+// (kReachMargin), stream-compacted into two shared-memory lists (si, sj) as
+// (x, y, z, |p|^2); then every lane takes 2 (or 4) i entries and loops over
+// the j list, two i per FFMA2 (4 pairs = 6 FFMA2 + 2 FMNMX3).  Only the
+// compacted cross product is evaluated.
+// !FILTER (option pass1_packed=0): every listed 64 x 64 sub-pair, scalar FFMA
+// (the unfiltered baseline).
+template <bool FILTER>
 __device__ __forceinline__ void pass1_3d(const int4* __restrict__ keys, long long cap,
                                          const RoiParams* __restrict__ rp,
                                          const uint2* __restrict__ work, float* __restrict__ umax,
-                                         Stats* __restrict__ st, float4* __restrict__ sj) {
+                                         Stats* __restrict__ st, float4* __restrict__ sj,
+                                         float4* __restrict__ si,
+                                         const int4* __restrict__ boxes,
+                                         const int4* __restrict__ hboxes, int vfilter) {
   Frame f = rp->f;
   const long long n = n_vertices(st, cap);
   if (n == 0) return;
   frame_centre(st, f);
   const long long n_work = (long long)st->n_work;
-  long long w0, w1;
-  w0 = 0;
-  w1 = n_work;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // Each warp takes a contiguous run of units, so consecutive units usually
-  // share the I chunk (always, without pruning) and its registers are reused.
+  // Each warp takes a contiguous run of units.
   const long long gwarps = (long long)gridDim.x * kWarps;
   const long long gw = (long long)blockIdx.x * kWarps + warp;
-  const long long per = (w1 - w0 + gwarps - 1) / gwarps;
-  const long long wb = w0 + gw * per, we = min(w1, wb + per);
+  const long long per = (n_work + gwarps - 1) / gwarps;
+  const long long wb = gw * per, we = min(n_work, wb + per);
+  if (wb >= we) return;
   float run = 0.f;
+  if (FILTER) {
+    const int* bb = st->bbox;
+    const double R2 = half_extent_sq(bb[0], bb[3], f.sx) + half_extent_sq(bb[1], bb[4], f.sy) +
+                      half_extent_sq(bb[2], bb[5], f.sz);
+    const double lb = __longlong_as_double((long long)st->lb);
+    // (no filtering when pruning is off: every pair is evaluated)
+    const float thr = vfilter ? __double2float_rd(lb - kReachMargin * R2) : -3.0e38f;
+    unsigned long long evals = 0;  // pair slots evaluated (diagnostics)
+    for (long long w = wb; w < we; w++) {
+      const uint2 ij = work[w];
+      const int I = (int)ij.x, J = (int)(ij.y & kIdxMask);
+      const unsigned int sub = ij.y >> kSubShift;  // bit 2a + b: i half a x j half b
+      // i half a meets the j halves (sub >> 2a) & 3; j half b the i halves
+      // bit b | bit (2 + b) << 1.
+      const unsigned int ja0 = sub & 3u, ja1 = (sub >> 2) & 3u;
+      const unsigned int ib0 = (sub & 1u) | ((sub >> 1) & 2u), ib1 = ((sub >> 1) & 1u) | ((sub >> 2) & 2u);
+      __syncwarp();  // the previous unit is done with si / sj
+      int ni = 0, nj = 0;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const unsigned int jh = h ? ja1 : ja0, ih = h ? ib1 : ib0;
+        const FBox bj = half_box(boxes, hboxes, J, jh ? jh : 3u, f);  // reach target of i half h
+        const FBox bi = half_box(boxes, hboxes, I, ih ? ih : 3u, f);  // reach target of j half h
+#pragma unroll
+        for (int r = 2 * h; r < 2 * h + 2; r++) {
+          const long long i = (long long)I * kChunk + r * 32 + lane;
+          const long long j = (long long)J * kChunk + r * 32 + lane;
+          const float3 p = frame_coord(keys[i < n ? i : n - 1], f);
+          const float3 q = frame_coord(keys[j < n ? j : n - 1], f);
+          warp_append(si, ni, i < n && jh && reach_sq(p, bj) >= thr,
+                      make_float4(p.x, p.y, p.z, fmaf(p.x, p.x, fmaf(p.y, p.y, p.z * p.z))));
+          warp_append(sj, nj, j < n && ih && reach_sq(q, bi) >= thr,
+                      make_float4(q.x, q.y, q.z, fmaf(q.x, q.x, fmaf(q.y, q.y, q.z * q.z))));
+        }
+      }
+      __syncwarp();
+      float best = 0.f;
+      if (ni > 0 && nj > 0) {
+        if ((nj & 1) && lane == 0) sj[nj] = sj[nj - 1];  // even trip count (a repeat is harmless)
+        __syncwarp();
+        const int nj2 = (nj + 1) & ~1;
+        // 4 i entries per lane (two FFMA2 pairs) while more than 64 remain, else 2.
+        int i0 = 0;
+        for (; ni - i0 > 64; i0 += 128) {
+          best = fmaxf(best, eval_rows<2>(si, sj, i0, ni, nj2));
+          evals += 128ull * (unsigned long long)nj2;
+        }
+        if (i0 < ni) {
+          best = fmaxf(best, eval_rows<1>(si, sj, i0, ni, nj2));
+          evals += 64ull * (unsigned long long)nj2;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+      if (lane == 0) umax[w] = best;
+      run = fmaxf(run, best);
+    }
+    if (lane == 0) {
+      atomic_max_pos_f32(&st->d3_f32, run);
+      if (evals) atomicAdd(&st->n_eval, evals);
+    }
+    return;
+  }
   int prevI = -1;
   float a[kR], b[kR], c[kR], ni[kR];
   for (long long w = wb; w < we; w++) {
@@ -91,74 +247,26 @@ __device__ __forceinline__ void pass1_3d(const int4* __restrict__ keys, long lon
     }
     prevI = I;
     __syncwarp();
-    if (PACKED) {
-      float2 a2[kR / 2], b2[kR / 2], c2[kR / 2];
 #pragma unroll
-      for (int r = 0; r < kR / 2; r++) {
-        a2[r] = make_float2(a[2 * r], a[2 * r + 1]);
-        b2[r] = make_float2(b[2 * r], b[2 * r + 1]);
-        c2[r] = make_float2(c[2 * r], c[2 * r + 1]);
-      }
-      if (sub == 0xFu) {
+    for (int ha = 0; ha < 2; ha++)
+#pragma unroll
+      for (int hb = 0; hb < 2; hb++) {
+        if (!(sub & (1u << (2 * ha + hb)))) continue;
 #pragma unroll 2
-        for (int j = 0; j < kChunk; j += 2) {
+        for (int j = 64 * hb; j < 64 * hb + 64; j += 2) {
           const float4 q0 = sj[j], q1 = sj[j + 1];
 #pragma unroll
-          for (int r = 0; r < kR / 2; r++) {
-            float2 t0 = __ffma2_rn(a2[r], make_float2(q0.x, q0.x), make_float2(q0.w, q0.w));
-            float2 t1 = __ffma2_rn(a2[r], make_float2(q1.x, q1.x), make_float2(q1.w, q1.w));
-            t0 = __ffma2_rn(b2[r], make_float2(q0.y, q0.y), t0);
-            t1 = __ffma2_rn(b2[r], make_float2(q1.y, q1.y), t1);
-            t0 = __ffma2_rn(c2[r], make_float2(q0.z, q0.z), t0);
-            t1 = __ffma2_rn(c2[r], make_float2(q1.z, q1.z), t1);
-            m[2 * r] = fmax3f(m[2 * r], t0.x, t1.x);
-            m[2 * r + 1] = fmax3f(m[2 * r + 1], t0.y, t1.y);
+          for (int r = 2 * ha; r < 2 * ha + 2; r++) {
+            float t0 = fmaf(q0.x, a[r], q0.w);
+            float t1 = fmaf(q1.x, a[r], q1.w);
+            t0 = fmaf(q0.y, b[r], t0);
+            t1 = fmaf(q1.y, b[r], t1);
+            t0 = fmaf(q0.z, c[r], t0);
+            t1 = fmaf(q1.z, c[r], t1);
+            m[r] = fmax3f(m[r], t0, t1);
           }
         }
-      } else {
-        // Only the listed 64 x 64 sub-pairs: i half a = packed pair a (i = a*64
-        // + {0, 32} + lane), j half b.  a, b are compile-time in each body.
-#pragma unroll
-        for (int a = 0; a < 2; a++)
-#pragma unroll
-          for (int b = 0; b < 2; b++) {
-            if (!(sub & (1u << (2 * a + b)))) continue;
-#pragma unroll 2
-            for (int j = 64 * b; j < 64 * b + 64; j += 2) {
-              const float4 q0 = sj[j], q1 = sj[j + 1];
-              float2 t0 = __ffma2_rn(a2[a], make_float2(q0.x, q0.x), make_float2(q0.w, q0.w));
-              float2 t1 = __ffma2_rn(a2[a], make_float2(q1.x, q1.x), make_float2(q1.w, q1.w));
-              t0 = __ffma2_rn(b2[a], make_float2(q0.y, q0.y), t0);
-              t1 = __ffma2_rn(b2[a], make_float2(q1.y, q1.y), t1);
-              t0 = __ffma2_rn(c2[a], make_float2(q0.z, q0.z), t0);
-              t1 = __ffma2_rn(c2[a], make_float2(q1.z, q1.z), t1);
-              m[2 * a] = fmax3f(m[2 * a], t0.x, t1.x);
-              m[2 * a + 1] = fmax3f(m[2 * a + 1], t0.y, t1.y);
-            }
-          }
       }
-    } else {
-#pragma unroll
-      for (int ha = 0; ha < 2; ha++)
-#pragma unroll
-        for (int hb = 0; hb < 2; hb++) {
-          if (!(sub & (1u << (2 * ha + hb)))) continue;
-#pragma unroll 2
-          for (int j = 64 * hb; j < 64 * hb + 64; j += 2) {
-            const float4 q0 = sj[j], q1 = sj[j + 1];
-#pragma unroll
-            for (int r = 2 * ha; r < 2 * ha + 2; r++) {
-              float t0 = fmaf(q0.x, a[r], q0.w);
-              float t1 = fmaf(q1.x, a[r], q1.w);
-              t0 = fmaf(q0.y, b[r], t0);
-              t1 = fmaf(q1.y, b[r], t1);
-              t0 = fmaf(q0.z, c[r], t0);
-              t1 = fmaf(q1.z, c[r], t1);
-              m[r] = fmax3f(m[r], t0, t1);
-            }
-          }
-        }
-    }
     float best = 0.f;
 #pragma unroll
     for (int r = 0; r < kR; r++) best = fmaxf(best, m[r] + ni[r]);
@@ -234,22 +342,79 @@ __device__ __forceinline__ void refine_3d(const int4* __restrict__ keys, long lo
   if ((threadIdx.x & 31) == 0 && best > 0.0) atomic_max_pos_f64(&st->sq[0], best);
 }
 
+// In-plane box of a chunk (or of its halves selected by `halves`, bit h =
+// half h; 3 = whole chunk) in the planar pass-1 frame: (lo.a, lo.b, hi.a, hi.b).
+__device__ __forceinline__ float4 plane_half_box(const int4* __restrict__ pboxes,
+                                                 const int4* __restrict__ hpboxes, unsigned int c,
+                                                 unsigned int halves, const PlaneAxes& ax) {
+  const int4 b = halves == 3u ? pboxes[c] : hpboxes[2 * c + (halves == 2u ? 1 : 0)];
+  return make_float4((float)(b.x - ax.ca) * ax.ha, (float)(b.y - ax.cb) * ax.hb,
+                     (float)(b.z - ax.ca) * ax.ha, (float)(b.w - ax.cb) * ax.hb);
+}
+
+__device__ __forceinline__ float reach_sq2(float2 p, float4 b) {
+  const float da = fmaxf(p.x - b.x, b.z - p.x), db = fmaxf(p.y - b.y, b.w - p.y);
+  return fmaf(da, da, db * db);
+}
+
+// 2-D counterpart of eval_rows: entries (a, b, |p|^2, -).
+template <int P>
+__device__ __forceinline__ float eval_rows2(const float4* __restrict__ si,
+                                            const float4* __restrict__ sj, int i0, int ni,
+                                            int nj2) {
+  const int lane = threadIdx.x & 31;
+  float2 a2[P], b2[P];
+  float n0[P], n1[P], m0[P], m1[P];
+#pragma unroll
+  for (int p = 0; p < P; p++) {
+    const float4 e0 = si[min(i0 + 64 * p + lane, ni - 1)];
+    const float4 e1 = si[min(i0 + 64 * p + 32 + lane, ni - 1)];
+    a2[p] = make_float2(-2.f * e0.x, -2.f * e1.x);
+    b2[p] = make_float2(-2.f * e0.y, -2.f * e1.y);
+    n0[p] = e0.z;
+    n1[p] = e1.z;
+    m0[p] = m1[p] = -3.0e38f;
+  }
+#pragma unroll 4
+  for (int j = 0; j < nj2; j += 2) {
+    const float4 q0 = sj[j], q1 = sj[j + 1];
+#pragma unroll
+    for (int p = 0; p < P; p++) {
+      float2 t0 = __ffma2_rn(a2[p], make_float2(q0.x, q0.x), make_float2(q0.z, q0.z));
+      float2 t1 = __ffma2_rn(a2[p], make_float2(q1.x, q1.x), make_float2(q1.z, q1.z));
+      t0 = __ffma2_rn(b2[p], make_float2(q0.y, q0.y), t0);
+      t1 = __ffma2_rn(b2[p], make_float2(q1.y, q1.y), t1);
+      m0[p] = fmax3f(m0[p], t0.x, t1.x);
+      m1[p] = fmax3f(m1[p], t0.y, t1.y);
+    }
+  }
+  float best = 0.f;
+#pragma unroll
+  for (int p = 0; p < P; p++) best = fmaxf(best, fmaxf(m0[p] + n0[p], m1[p] + n1[p]));
+  return best;
+}
+
 __device__ __forceinline__ float2 plane_point(int2 k, const PlaneAxes& ax) {
   return make_float2((float)(k.x - ax.ca) * ax.ha, (float)(k.y - ax.cb) * ax.hb);
 }
 
-// Planar pass 1: fp32 dot form over every surviving in-plane chunk pair
-// (128 x 128).  Every warp is an independent worker (own shared-memory copy
-// of the J chunk as (a, b, |p|^2)); each lane register-blocks 4 i entries and
-// evaluates two of them per FFMA2, so a pair costs one FFMA2 + half an FMNMX3.
-// One maximum per work entry; per-family maxima in st->pl_f32[axis].  The
-// refine kernel selects the re-check candidates from the unit maxima.
+// Planar pass 1: the same scheme as pass1_3d over every surviving in-plane
+// chunk pair (128 x 128 entries of one plane): per side, the entries whose
+// in-plane reach to the other side's (sub-pair-selected) box can attain the
+// family's lower bound plb (margin kReachMargin R_family^2, the 2-D case of
+// the 3-D argument), stream-compacted into si / sj as (a, b, |p|^2); then the
+// compacted cross product in the fp32 dot form, two i per FFMA2 (4 pairs = 4
+// FFMA2 + 2 FMNMX3).  One maximum per work entry; per-family maxima in
+// st->pl_f32[axis].  The refine kernel selects the re-check candidates.
 __device__ __forceinline__ void pass1_planar(const int2* __restrict__ sorted,
                                              const unsigned int* __restrict__ start,
                                              const uint2* __restrict__ pwork,
                                              const RoiParams* __restrict__ rp,
                                              float* __restrict__ umax, Stats* __restrict__ st,
-                                             float4* __restrict__ sj) {
+                                             float4* __restrict__ sj, float4* __restrict__ si,
+                                             const unsigned int* __restrict__ cstart,
+                                             const int4* __restrict__ pboxes,
+                                             const int4* __restrict__ hpboxes, int vfilter) {
   Frame f = rp->f;
   const PlaneSpace ps = plane_space(st);
   const long long w0 = 0, w1 = (long long)st->n_pwork;
@@ -262,79 +427,65 @@ __device__ __forceinline__ void pass1_planar(const int2* __restrict__ sorted,
   const long long gw = ((long long)blockIdx.x * kPlaneWarps + warp + gwarps - busy3) % gwarps;
   const long long per = (w1 - w0 + gwarps - 1) / gwarps;
   const long long wb = w0 + gw * per, we = min(w1, wb + per);
+  if (wb >= we) return;
+  float thr[3];
+  {
+    const int* bb = st->bbox;
+    const double ex = half_extent_sq(bb[0], bb[3], f.sx), ey = half_extent_sq(bb[1], bb[4], f.sy),
+                 ez = half_extent_sq(bb[2], bb[5], f.sz);
+    const double R2[3] = {ex + ey, ex + ez, ey + ez};  // XY, XZ, YZ frames (plane_axes)
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+      thr[a] = vfilter ? __double2float_rd(__longlong_as_double((long long)st->plb[a]) -
+                                           kReachMargin * R2[a])
+                       : -3.0e38f;
+  }
   float run0 = 0.f, run1 = 0.f, run2 = 0.f;  // per-family maxima
-  unsigned int prev_p = 0xffffffffu, prev_i = 0xffffffffu;
-  float2 a2[kPR / 2], b2[kPR / 2];
-  float ni[kPR];
-  int axis = 0;
+  unsigned long long evals = 0;
   for (long long w = wb; w < we; w++) {
     const uint2 u = pwork[w];
     const unsigned int p = u.x & kIdxMask, I = u.y >> 16, J = u.y & 0xffffu;
-    const unsigned int sub = u.x >> kSubShift;  // 64 x 64 sub-pairs to evaluate
-    const unsigned int b0 = start[p], np = start[p + 1] - b0;
-    axis = plane_axis((int)p, ps);
+    const unsigned int sub = u.x >> kSubShift;  // bit 2a + b: i half a x j half b
+    const unsigned int b0 = start[p], np = start[p + 1] - b0, c0 = cstart[p];
+    const int axis = plane_axis((int)p, ps);
     const PlaneAxes ax = plane_axes(axis, st, f);
-    __syncwarp();  // previous unit is done with sj
-    if (p != prev_p || I != prev_i) {
+    const float th = axis == 0 ? thr[0] : (axis == 1 ? thr[1] : thr[2]);
+    const unsigned int ja0 = sub & 3u, ja1 = (sub >> 2) & 3u;
+    const unsigned int ib0 = (sub & 1u) | ((sub >> 1) & 2u), ib1 = ((sub >> 1) & 1u) | ((sub >> 2) & 2u);
+    __syncwarp();  // previous unit is done with si / sj
+    int ni = 0, nj = 0;
 #pragma unroll
-      for (int r = 0; r < kPR / 2; r++) {
-        unsigned int i0 = I * kPC + (2 * r) * 32 + lane, i1 = i0 + 32;
-        const float2 q0 = plane_point(sorted[b0 + min(i0, np - 1)], ax);
-        const float2 q1 = plane_point(sorted[b0 + min(i1, np - 1)], ax);
-        a2[r] = make_float2(-2.f * q0.x, -2.f * q1.x);
-        b2[r] = make_float2(-2.f * q0.y, -2.f * q1.y);
-        ni[2 * r] = fmaf(q0.x, q0.x, q0.y * q0.y);
-        ni[2 * r + 1] = fmaf(q1.x, q1.x, q1.y * q1.y);
+    for (int h = 0; h < 2; h++) {
+      const unsigned int jh = h ? ja1 : ja0, ih = h ? ib1 : ib0;
+      const float4 bj = plane_half_box(pboxes, hpboxes, c0 + J, jh ? jh : 3u, ax);
+      const float4 bi = plane_half_box(pboxes, hpboxes, c0 + I, ih ? ih : 3u, ax);
+#pragma unroll
+      for (int r = 2 * h; r < 2 * h + 2; r++) {
+        const unsigned int i = I * kPC + r * 32 + lane, j = J * kPC + r * 32 + lane;
+        const float2 pi = plane_point(sorted[b0 + min(i, np - 1)], ax);
+        const float2 qj = plane_point(sorted[b0 + min(j, np - 1)], ax);
+        warp_append(si, ni, i < np && jh && reach_sq2(pi, bj) >= th,
+                    make_float4(pi.x, pi.y, fmaf(pi.x, pi.x, pi.y * pi.y), 0.f));
+        warp_append(sj, nj, j < np && ih && reach_sq2(qj, bi) >= th,
+                    make_float4(qj.x, qj.y, fmaf(qj.x, qj.x, qj.y * qj.y), 0.f));
       }
-      prev_p = p;
-      prev_i = I;
-    }
-#pragma unroll
-    for (int r = 0; r < kPR; r++) {
-      const unsigned int j = J * kPC + r * 32 + lane;
-      const float2 q = plane_point(sorted[b0 + min(j, np - 1)], ax);  // repeats are harmless
-      sj[r * 32 + lane] = make_float4(q.x, q.y, fmaf(q.x, q.x, q.y * q.y), 0.f);
     }
     __syncwarp();
-    float m[kPR];
-#pragma unroll
-    for (int r = 0; r < kPR; r++) m[r] = -3.0e38f;
-    if (sub == 0xFu) {
-#pragma unroll 2
-      for (int j = 0; j < kPC; j += 2) {
-        const float4 q0 = sj[j], q1 = sj[j + 1];
-#pragma unroll
-        for (int r = 0; r < kPR / 2; r++) {
-          float2 t0 = __ffma2_rn(a2[r], make_float2(q0.x, q0.x), make_float2(q0.z, q0.z));
-          float2 t1 = __ffma2_rn(a2[r], make_float2(q1.x, q1.x), make_float2(q1.z, q1.z));
-          t0 = __ffma2_rn(b2[r], make_float2(q0.y, q0.y), t0);
-          t1 = __ffma2_rn(b2[r], make_float2(q1.y, q1.y), t1);
-          m[2 * r] = fmax3f(m[2 * r], t0.x, t1.x);
-          m[2 * r + 1] = fmax3f(m[2 * r + 1], t0.y, t1.y);
-        }
-      }
-    } else {
-      // Only the listed 64 x 64 sub-pairs (i half a = packed pair a).
-#pragma unroll
-      for (int a = 0; a < 2; a++)
-#pragma unroll
-        for (int b = 0; b < 2; b++) {
-          if (!(sub & (1u << (2 * a + b)))) continue;
-#pragma unroll 2
-          for (int j = 64 * b; j < 64 * b + 64; j += 2) {
-            const float4 q0 = sj[j], q1 = sj[j + 1];
-            float2 t0 = __ffma2_rn(a2[a], make_float2(q0.x, q0.x), make_float2(q0.z, q0.z));
-            float2 t1 = __ffma2_rn(a2[a], make_float2(q1.x, q1.x), make_float2(q1.z, q1.z));
-            t0 = __ffma2_rn(b2[a], make_float2(q0.y, q0.y), t0);
-            t1 = __ffma2_rn(b2[a], make_float2(q1.y, q1.y), t1);
-            m[2 * a] = fmax3f(m[2 * a], t0.x, t1.x);
-            m[2 * a + 1] = fmax3f(m[2 * a + 1], t0.y, t1.y);
-          }
-        }
-    }
     float best = 0.f;
-#pragma unroll
-    for (int r = 0; r < kPR; r++) best = fmaxf(best, m[r] + ni[r]);
+    if (ni > 0 && nj > 0) {
+      if ((nj & 1) && lane == 0) sj[nj] = sj[nj - 1];  // even trip count (repeat is harmless)
+      __syncwarp();
+      const int nj2 = (nj + 1) & ~1;
+      int i0 = 0;
+      for (; ni - i0 > 64; i0 += 128) {
+        best = fmaxf(best, eval_rows2<2>(si, sj, i0, ni, nj2));
+        evals += 128ull * (unsigned long long)nj2;
+      }
+      if (i0 < ni) {
+        best = fmaxf(best, eval_rows2<1>(si, sj, i0, ni, nj2));
+        evals += 64ull * (unsigned long long)nj2;
+      }
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
     if (lane == 0) umax[w] = best;
@@ -346,6 +497,7 @@ __device__ __forceinline__ void pass1_planar(const int2* __restrict__ sorted,
     if (run0 > 0.f) atomic_max_pos_f32(&st->pl_f32[0], run0);
     if (run1 > 0.f) atomic_max_pos_f32(&st->pl_f32[1], run1);
     if (run2 > 0.f) atomic_max_pos_f32(&st->pl_f32[2], run2);
+    if (evals) atomicAdd(&st->n_peval, evals);
   }
 }
 

@@ -45,6 +45,8 @@ struct Stats {
   unsigned long long t_start, t_mesh, t_end;
   unsigned int plane_ovf;              // a plane holds more than kPlaneMaxEntries entries
   unsigned int pad_;
+  unsigned long long n_eval;           // 3-D pair slots pass 1 evaluated (after the vertex filter)
+  unsigned long long n_peval;          // planar pair slots pass 1 evaluated
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {

@@ -46,4 +46,4 @@ m = sc.marching_cubes(sc.MaskVolume.from_array(cases[0][0], cases[0][1]))
 assert m.vertex_count == want[0]["VertexCount"]
 sc.diameters(m.xs, m.ys, m.zs)
 torch.cuda.synchronize()
-print("sanitize workload ok", flush=True)
+print("sanitize workload ok:", _native.load().sc_launch_count(), "library kernel launches", flush=True)
