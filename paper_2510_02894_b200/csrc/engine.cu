@@ -41,9 +41,10 @@ __global__ void init_stats(Stats* st, uint32_t* segmap, long long n_seg, const R
 template <int U, bool BOX>
 __global__ void pack_bits_v16(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 __global__ void bits_bbox(const RoiParams*, const uint4*, Stats*, const uint32_t*);
-template <bool BOX>
-__global__ void pack_bits_tma(const RoiParams*, uint32_t*, Stats*, uint32_t*);
-constexpr int kTmaSmem = 4 * 16384;  // mc.cu kTmaStages x kTmaTile
+template <bool BOX, int NT>
+__global__ void pack_bits_tma(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
+constexpr int kTmaTileBytes = 16384;  // mc.cu kTmaTile
+constexpr int kTmaMaxSmem = 8 * kTmaTileBytes;  // mc.cu kTmaMaxStages x kTmaTile
 __global__ void pack_bits_generic(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 __global__ void mc_cells(const RoiParams*, const uint32_t*, const CaseTables*, Stats*, int4*,
                          long long, unsigned int*, unsigned int*, const uint32_t*);
@@ -128,6 +129,11 @@ struct Opts {
   bool pack_skip = true;     // sparse pack: no conversion of all-zero segments
   int pack_tma = 1;          // batch graphs: TMA bulk-copy pack, CTAs per SM (0 = 128-bit loads)
   int pack_tma_single = 0;   // the same for single calls (the 128-bit-load pack is faster alone)
+  bool pack_prio = true;      // init_stats + pack at the greatest stream priority ("pack_prio")
+  int pack_threads = 256;     // TMA pack CTA size (128 / 256, "pack_threads")
+  int pack_stages = 4;       // TMA pack ring depth, 16 KB tiles (2..8, "pack_stages")
+  int pack_dyn = 0;          // TMA pack: dynamic tile claims ("pack_dyn"; C4 batch 33.5 -> 36.6 us/ROI: off)
+  int pack_sleep = 0;        // TMA pack: suspend-hinted mbarrier waits ("pack_sleep")
   int pack_chain = 4;        // batch: ROI i's graph starts after ROI i - pack_chain's pack
                              // (at most pack_chain HBM passes in flight; 0 = unchained).
                              // C2 / C4 / C5 K=200 us per ROI, chain 0 / 1 / 2 / 3 / 4 / 8:
@@ -410,8 +416,10 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     }
     CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, sprio));
     CK(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, sprio));
-    CK(cudaFuncSetAttribute(pack_bits_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
-    CK(cudaFuncSetAttribute(pack_bits_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tma<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tma<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tma<false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tma<true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
     CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
     for (auto& e : c->cev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -445,7 +453,8 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
       cudaFuncAttributes fa;
       const void* kernels[] = {(const void*)init_stats, (const void*)pack_bits_v16<4, false>,
                                (const void*)pack_bits_v16<4, true>,
-                               (const void*)pack_bits_tma<false>, (const void*)pack_bits_tma<true>,
+                               (const void*)pack_bits_tma<false, 256>, (const void*)pack_bits_tma<true, 256>,
+                               (const void*)pack_bits_tma<false, 128>, (const void*)pack_bits_tma<true, 128>,
                                (const void*)mesh_count, (const void*)mesh_emit,
                                (const void*)bits_bbox,
                                (const void*)pack_bits_generic, (const void*)mc_cells,
@@ -625,6 +634,41 @@ cudaError_t chain_mark(Ctx* c, cudaStream_t s) {
                       : cudaEventRecord(c->pack_ev, s);
 }
 
+// Launch with an explicit priority (the batch's HBM chain -- init_stats and
+// the pack -- runs at the greatest priority, option "pack_prio": its CTAs are
+// scheduled ahead of the latency-bound kernels of the ROIs already in flight,
+// so the next pack of the chain does not queue behind them).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_prio(const Ctx* c, cudaStream_t s, dim3 grid, int block, size_t smem,
+                        void (*k)(KArgs...), Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributePriority;
+  at[0].val.priority = c->prio_hi;
+  cfg.attrs = at;
+  cfg.numAttrs = c->o.pack_prio ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+// TMA bulk-copy pack: `pack_tma` CTAs per SM of `pack_threads` threads, each
+// streaming through a ring of `pack_stages` 16 KB shared-memory tiles.
+template <bool BOX>
+cudaError_t launch_tma_pack(Ctx* c, cudaStream_t s) {
+  const int st = std::max(2, std::min(8, c->o.pack_stages));
+  const size_t smem = (size_t)st * kTmaTileBytes;
+  const dim3 grid((unsigned)(c->sms * c->o.pack_tma));
+  const RoiParams* rp = c->d_rp;
+  if (c->o.pack_threads == 128)
+    return launch_prio(c, s, grid, 128, smem, pack_bits_tma<BOX, 128>, rp, c->bits.p, c->d_stats,
+                       c->segmap.p, st);
+  return launch_prio(c, s, grid, 256, smem, pack_bits_tma<BOX, 256>, rp, c->bits.p, c->d_stats,
+                     c->segmap.p, st);
+}
+
 // Enqueue one whole ROI on stream s; no host synchronisation.  Everything
 // ROI-specific (mask pointer, dims, spacing) is read by the kernels from the
 // slot's RoiParams record, so the enqueued sequence -- and a graph captured
@@ -643,9 +687,9 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   const bool zc = zero_copy_records(c);
   if (c->chain_wait)
     CK(cudaStreamWaitEvent(s, c->chain_wait, c->capturing ? cudaEventWaitExternal : 0));
-  init_stats<<<clear_map ? 8 : 1, 256, 0, s>>>(c->d_stats, c->segmap.p,
-                                               clear_map ? (long long)c->segmap.cap : 0LL,
-                                               zc ? c->h_rp_dev : nullptr, c->d_rp);
+  CK(launch_prio(c, s, dim3(clear_map ? 8 : 1), 256, 0, init_stats, c->d_stats, c->segmap.p,
+                 clear_map ? (long long)c->segmap.cap : 0LL,
+                 (const RoiParams*)(zc ? c->h_rp_dev : nullptr), c->d_rp));
   CKL(1);
   for (int e = 0; e < c->o.empty; e++) {  // debug: launch-rate probe
     empty_kernel<<<1, 32, 0, s>>>();
@@ -663,8 +707,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   } else if (fast && c->o.fbox && c->o.pack_tma > 0 &&
              !(c->o.pack_mode & 4)) {
     // TMA pack with the bbox accumulated inside (no bits_bbox kernel)
-    pack_bits_tma<true><<<c->sms * c->o.pack_tma, 256, kTmaSmem, s>>>(rp, c->bits.p,
-                                                                           c->d_stats, c->segmap.p);
+    CK(launch_tma_pack<true>(c, s));
     CKL(1);
     if (++nk >= lim) return SC_OK;
     CK(record(c, c->kev[1], s));
@@ -696,8 +739,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
     cfg.attrs = at;
     cfg.numAttrs = (pm & 2) ? 1 : 0;
     if (!(pm & 4) && c->o.pack_tma > 0) {  // bulk-copy (TMA) pack
-      pack_bits_tma<false><<<c->sms * c->o.pack_tma, 256, kTmaSmem, s>>>(rp, c->bits.p,
-                                                                      c->d_stats, c->segmap.p);
+      CK(launch_tma_pack<false>(c, s));
       CKL(1);
     } else if (!(pm & 4)) {  // bit 2 (debug, timing only): reuse the slot's previous bit volume
       CK(cudaLaunchKernelEx(&cfg, pack_bits_v16<4, false>, rp, c->bits.p, c->d_stats,
@@ -734,7 +776,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
 
   // Orders (Morton bricks; planes by in-plane brick), chunk boxes + extremes,
   // exact lower bound, pruned 3-D work list.
-  CK(launch_k(c, s, kScanBlocks + std::max(1, c->sms / 2), kScanThreads, scan_all, c->sort_counts.p, c->sort_cursor.p,
+  CK(launch_k(c, s, kScanBlocks + std::max(1, lgrid(c, 1) / 2), kScanThreads, scan_all, c->sort_counts.p, c->sort_cursor.p,
                                             c->plane_counts.p, c->plane_start.p,
                                             c->plane_tstart.p, c->plane_cstart.p, dcap,
                                             c->d_stats, c->sboxes.p, c->pbin_counts.p, c->pbin_cursor.p, c->plane_ext.p));
@@ -910,6 +952,83 @@ bool host_prof_on() {
   return on;
 }
 
+// Batch timeline from the kernels' %globaltimer spans (Stats::tr), SC_TRACE=1:
+// per kernel its mean start offset from the ROI start (init_stats) and mean
+// span, plus the mean ROI latency; printed at the end of each batch.
+struct TraceAcc {
+  double off[kTrCount] = {}, span[kTrCount] = {};
+  long long n[kTrCount] = {};
+  double lat = 0;
+  long long rois = 0;
+  std::vector<std::array<unsigned long long, 4>> seq;  // (t_start, pack start, pack end, t_end)
+};
+TraceAcc g_trace;
+bool trace_on() {
+  static const bool on = std::getenv("SC_TRACE") != nullptr;
+  return on;
+}
+void trace_add(const Stats& h) {
+  if (!h.t_start) return;
+  for (int k = 1; k < kTrCount; k++) {
+    // (the refine's last block publishes the record before its own end
+    // stamp: its end is t_end)
+    const unsigned long long end = k == kTrRefine ? h.t_end : h.tr[k][1];
+    if (h.tr[k][0] == ~0ull || end < h.tr[k][0]) continue;
+    g_trace.off[k] += 1e-3 * (double)(h.tr[k][0] - h.t_start);
+    g_trace.span[k] += 1e-3 * (double)(end - h.tr[k][0]);
+    g_trace.n[k]++;
+  }
+  if (h.t_end > h.t_start) {
+    g_trace.lat += 1e-3 * (double)(h.t_end - h.t_start);
+    g_trace.rois++;
+  }
+  g_trace.seq.push_back({h.t_start, h.tr[kTrPack][0], h.tr[kTrPack][1], h.t_end});
+}
+void trace_print() {
+  static const char* names[kTrCount] = {"init", "pack", "mc_cells", "scan_all", "scatter_all",
+                                         "plane_boxes", "plane_lb", "plane_filter",
+                                         "boxes_extremes", "unit_filter", "unit_expand",
+                                         "pass1", "refine"};
+  if (!g_trace.rois) return;
+  std::fprintf(stderr, "[sc trace] %lld ROIs, mean ROI latency %.1f us (init -> refine end)\n",
+               g_trace.rois, g_trace.lat / (double)g_trace.rois);
+  for (int k = 1; k < kTrCount; k++)
+    if (g_trace.n[k])
+      std::fprintf(stderr, "[sc trace]   %-15s start +%8.1f us  span %8.1f us\n", names[k],
+                   g_trace.off[k] / (double)g_trace.n[k], g_trace.span[k] / (double)g_trace.n[k]);
+  // Admission: ROI i (slot i mod S) starts after ROI i - S ended (slot reuse:
+  // host collect + relaunch) and after ROI i - chain's pack (pack chain).
+  const auto& q = g_trace.seq;
+  const int S = std::getenv("SC_TRACE_SLOTS") ? std::atoi(std::getenv("SC_TRACE_SLOTS")) : 32;
+  const int ch = std::getenv("SC_TRACE_CHAIN") ? std::atoi(std::getenv("SC_TRACE_CHAIN")) : 4;
+  double g_slot = 0, g_chain = 0, pack_gap = 0;
+  long long n_slot = 0, n_chain = 0, n_pg = 0;
+  for (size_t i = 0; i < q.size(); i++) {
+    if (i >= (size_t)S && q[i - S][3] && q[i][0] > q[i - S][3]) {
+      g_slot += 1e-3 * (double)(q[i][0] - q[i - S][3]);
+      n_slot++;
+    }
+    if (ch > 0 && i >= (size_t)ch && q[i][0] > q[i - ch][2]) {
+      g_chain += 1e-3 * (double)(q[i][0] - q[i - ch][2]);
+      n_chain++;
+    }
+    if (i >= 1 && q[i][1] > q[i - 1][1]) {
+      pack_gap += 1e-3 * (double)(q[i][1] - q[i - 1][1]);
+      n_pg++;
+    }
+  }
+  if (n_slot) std::fprintf(stderr, "[sc trace]   init(i) - end(i-%d)      %8.1f us (slot reuse)\n", S, g_slot / n_slot);
+  if (n_chain) std::fprintf(stderr, "[sc trace]   init(i) - pack end(i-%d)  %8.1f us (pack chain)\n", ch, g_chain / n_chain);
+  if (n_pg) std::fprintf(stderr, "[sc trace]   pack start spacing       %8.1f us\n", pack_gap / n_pg);
+  g_trace = TraceAcc{};
+}
+
+// Everything about the pack that a captured graph bakes in.
+int pack_key(const Opts& o) {
+  return o.pack_mode + 32 * o.pack_bps + 4096 * o.pack_tma + 16384 * o.pack_stages +
+         (o.pack_threads == 128 ? (1 << 20) : 0) + (o.pack_prio ? (1 << 21) : 0);
+}
+
 int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
                const double sp[3], cudaStream_t s, int shard, int nshards, double* d_sq4,
                const int org[3]) {
@@ -922,6 +1041,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   h.n_words = (long long)h.W * ny * nz;
   h.n_chunks = nx * ny * nz / 16;
   h.sparse = (c->o.sparse && !c->prepacked) ? (c->o.pack_skip ? 3 : 1) : 0;
+  h.pflags = (c->o.pack_dyn ? 1 : 0) | (c->o.pack_sleep ? 2 : 0);
   h.f.cx2 = h.f.cy2 = h.f.cz2 = 0;  // set on the device from the bbox
   h.f.hx = (float)(0.5 * sp[0]);
   h.f.hy = (float)(0.5 * sp[1]);
@@ -947,7 +1067,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
     if (g.fast == fast && g.s == s && g.shard == shard && g.nshards == nshards &&
         g.d_sq4 == d_sq4 && g.cap == cap && g.dcap == dcap && g.prune == prune &&
         g.packed == packed && g.fbox == fbox && g.stages == c->o.stages + 7 * c->o.empty &&
-        g.packmode == c->o.pack_mode + 32 * c->o.pack_bps + 4096 * c->o.pack_tma &&
+        g.packmode == pack_key(c->o) &&
         g.grid_div == c->grid_div &&
         g.events == c->events_on && g.ev_full == c->ev_full && g.pdl == c->o.pdl &&
         g.sparse == c->o.sparse && g.fork == c->o.fork &&
@@ -979,7 +1099,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   }
   Ctx::GraphEntry g{fast, s, shard, nshards, d_sq4, cap, dcap, prune, packed, fbox,
                     c->o.stages + 7 * c->o.empty,
-                    c->o.pack_mode + 32 * c->o.pack_bps + 4096 * c->o.pack_tma,
+                    pack_key(c->o),
                     c->grid_div,
                     c->events_on, c->ev_full, c->o.pdl, c->o.sparse,
                     c->o.fork, c->o.zc, c->prepacked, c->chain_wait, c->gen, exec, launches};
@@ -1078,6 +1198,7 @@ int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
     return SC_ERR_NOMEM;
   }
   fill_out(*c->h_stats, p->sp, out);
+  if (trace_on()) trace_add(*c->h_stats);
   c->times_pending = c->events_on && c->ev_full;  // per-stage times: from kev[] on demand
   if (!c->times_pending)
     for (int i = 0; i < 6; i++) c->last_ms[i] = 0.0;
@@ -1555,6 +1676,7 @@ int run_batch(int device, const uint8_t* const* masks, const int64_t* dims,
     }
   }
   if (first) g_err = first_err;
+  if (trace_on()) trace_print();
   if (host_prof_on() && g_hprof.n) {
     const double n = (double)g_hprof.n;
     std::fprintf(stderr,
@@ -1730,6 +1852,11 @@ int set_opt(Opts& o, const char* name, int value) {
   else if (std::strcmp(name, "batch_stage_times") == 0) o.batch_times = value != 0;
   else if (std::strcmp(name, "host_threads") == 0) o.host_threads = std::max(1, value);
   else if (std::strcmp(name, "debug_empty") == 0) o.empty = std::max(0, value);
+  else if (std::strcmp(name, "pack_dyn") == 0) o.pack_dyn = value != 0;
+  else if (std::strcmp(name, "pack_prio") == 0) o.pack_prio = value != 0;
+  else if (std::strcmp(name, "pack_threads") == 0) o.pack_threads = value == 128 ? 128 : 256;
+  else if (std::strcmp(name, "pack_stages") == 0) o.pack_stages = std::max(2, std::min(8, value));
+  else if (std::strcmp(name, "pack_sleep") == 0) o.pack_sleep = value != 0;
   else if (std::strcmp(name, "debug_stages") == 0) o.stages = value > 0 ? value : (1 << 30);
   else { set_err("unknown option %s", name); return SC_ERR_INPUT; }
   return SC_OK;

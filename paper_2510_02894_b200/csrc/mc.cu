@@ -48,6 +48,7 @@ __global__ void init_stats(Stats* st, uint32_t* __restrict__ segmap, long long n
     __syncthreads();
     if (t < 3) st->bbox[t] = INT_MAX;
     if (t >= 3 && t < 6) st->bbox[t] = -1;
+    if (t < kTrCount) st->tr[t][0] = ~0ull;
     if (t == 0) st->t_start = global_ns();
   }
   for (long long i = (long long)blockIdx.x * blockDim.x + t; i < n_seg;
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(256) pack_bits_v16(const RoiParams* __restrict
                                                      uint32_t* __restrict__ bits,
                                                      Stats* __restrict__ st,
                                                      uint32_t* __restrict__ segmap) {
+  KTrace kt_(st, kTrPack);
   const uint4* __restrict__ mask = reinterpret_cast<const uint4*>(rp->mask);
   const long long n_chunks = rp->n_chunks;
   const unsigned int W = (unsigned int)rp->W, ny = (unsigned int)rp->ny;
@@ -170,7 +172,7 @@ __global__ void __launch_bounds__(256) pack_bits_v16(const RoiParams* __restrict
 // and 8 warps convert each landed tile exactly as pack_bits_v16 does.  The
 // CTA holds ~64 KB of shared memory and 256 threads, so most of the SM stays
 // free for other ROIs' kernels while the HBM stream runs.
-constexpr int kTmaStages = 4;
+constexpr int kTmaMaxStages = 8;
 constexpr int kTmaTile = 16384;  // bytes per stage
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -191,114 +193,138 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
       "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar)), "l"(policy)
       : "memory");
 }
-// Bounded wait: a lost transaction traps instead of hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+// Bounded wait: a lost transaction traps instead of hanging the GPU.  SLEEP:
+// each try suspends the warp in hardware until the phase completes (or up to
+// a 20 us hint) instead of returning at once (option "pack_sleep").
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity, bool sleep) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
   for (long long spin = 0;; spin++) {
     unsigned ok;
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
+    if (sleep)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; "
+          "selp.u32 %0, 1, 0, p; }"
+          : "=r"(ok)
+          : "r"(a), "r"(parity), "r"(20000u)
+          : "memory");
+    else
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+          "selp.u32 %0, 1, 0, p; }"
+          : "=r"(ok)
+          : "r"(a), "r"(parity)
+          : "memory");
     if (ok) return;
     if (spin > (1LL << 26)) __trap();
   }
 }
 
-template <bool BOX>
-__global__ void __launch_bounds__(256, 1) pack_bits_tma(const RoiParams* __restrict__ rp,
-                                                       uint32_t* __restrict__ bits,
-                                                       Stats* __restrict__ st,
-                                                       uint32_t* __restrict__ segmap) {
-  extern __shared__ __align__(128) unsigned char s_tiles[];  // kTmaStages x kTmaTile
-  __shared__ __align__(8) uint64_t s_full[kTmaStages];
+template <bool BOX, int NT>
+__global__ void __launch_bounds__(NT, 1) pack_bits_tma(const RoiParams* __restrict__ rp,
+                                                      uint32_t* __restrict__ bits,
+                                                      Stats* __restrict__ st,
+                                                      uint32_t* __restrict__ segmap,
+                                                      int stages) {
+  KTrace kt_(st, kTrPack);
+  extern __shared__ __align__(128) unsigned char s_tiles[];  // stages x kTmaTile
+  __shared__ __align__(8) uint64_t s_full[kTmaMaxStages];
+  __shared__ int s_tile[kTmaMaxStages];  // tile held by each stage (>= tiles: none)
   const unsigned char* mask = rp->mask;
   const long long n_bytes = 16LL * rp->n_chunks;
   const bool sparse = rp->sparse != 0;
   const bool skip = (rp->sparse & 2) != 0;
   const unsigned int W = (unsigned int)rp->W, ny = (unsigned int)rp->ny;
   BoxAcc box;  // BOX: occupied bbox of the nonzero words (replaces bits_bbox)
-  // contiguous share per CTA, a multiple of the tile size
-  const long long per =
-      ((n_bytes + gridDim.x - 1) / gridDim.x + kTmaTile - 1) / kTmaTile * kTmaTile;
-  const long long beg = min(n_bytes, (long long)blockIdx.x * per);
-  const long long end = min(n_bytes, beg + per);
-  const int tiles = (int)((end - beg + kTmaTile - 1) / kTmaTile);
-  if (tiles <= 0) return;  // block-uniform (no box to flush)
+  // Tile claims: a contiguous share per CTA, or (rp->pflags bit 0) dynamic,
+  // one atomic per 16 KB tile on the ROI's record (zeroed by init_stats), so
+  // CTAs that start late in a busy batch simply take fewer tiles.
+  const int tiles = (int)((n_bytes + kTmaTile - 1) / kTmaTile);
+  const bool dyn = (rp->pflags & 1) != 0, sleep = (rp->pflags & 2) != 0;
+  const int per = (tiles + (int)gridDim.x - 1) / (int)gridDim.x;
+  int t_next = min(tiles, (int)blockIdx.x * per);  // static share [t_next, t_end)
+  const int t_end = min(tiles, t_next + per);
   uint64_t policy;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  auto issue = [&](int s) {  // thread 0 only: claim the next tile into stage s
+    const int t = dyn ? (int)atomicAdd(&st->pack_next, 1u) : (t_next < t_end ? t_next++ : tiles);
+    s_tile[s] = t;
+    if (t < tiles) {
+      const long long off = (long long)t * kTmaTile;
+      const unsigned bytes = (unsigned)min((long long)kTmaTile, n_bytes - off);
+      mbar_expect_tx(&s_full[s], bytes);
+      bulk_load(s_tiles + s * kTmaTile, mask + off, bytes, &s_full[s], policy);
+    }
+  };
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kTmaStages; s++) mbar_init(&s_full[s], 1);
+    for (int s = 0; s < stages; s++) mbar_init(&s_full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < stages; s++) issue(s);
   }
   __syncthreads();
-  auto issue = [&](int t) {  // thread 0 only
-    const int s = t % kTmaStages;
-    const long long off = beg + (long long)t * kTmaTile;
-    const unsigned bytes = (unsigned)min((long long)kTmaTile, end - off);
-    mbar_expect_tx(&s_full[s], bytes);
-    bulk_load(s_tiles + s * kTmaTile, mask + off, bytes, &s_full[s], policy);
-  };
-  if (threadIdx.x == 0)
-    for (int t = 0; t < min(tiles, kTmaStages); t++) issue(t);
-  constexpr int kK = kTmaTile / 16 / 256;  // 16-byte chunks per thread per tile (4)
-  for (int t = 0; t < tiles; t++) {
-    const int s = t % kTmaStages;
-    mbar_wait(&s_full[s], (unsigned)(t / kTmaStages) & 1u);
-    const long long g0 = (beg + (long long)t * kTmaTile) / 16;  // first chunk of the tile
-    const long long gend = end / 16;
+  constexpr int kK = kTmaTile / 16 / NT;  // 16-byte chunks per thread per tile (4 or 8)
+  const long long gend = n_bytes / 16;
+  // Stage s is consumed at steps s, s + stages, ...; its next claim is
+  // written after the step's barrier and read stages - 1 barriers later.
+  // Claims only grow, so the first stage without a tile ends the loop.
+  for (int k = 0;; k++) {
+    const int s = k % stages;
+    const int t = s_tile[s];
+    if (t >= tiles) break;  // block-uniform
+    mbar_wait(&s_full[s], (unsigned)(k / stages) & 1u, sleep);
+    const long long g0 = (long long)t * (kTmaTile / 16);  // first chunk of the tile
     const uint4* tile = reinterpret_cast<const uint4*>(s_tiles + s * kTmaTile);
-    // Only the last tile can be partial: bytes past `end` in its stage are stale.
-    const bool full = t + 1 < tiles || (end - beg) % kTmaTile == 0;
+    // Only the last tile can be partial: bytes past the mask in its stage are stale.
+    const bool full = t + 1 < tiles || n_bytes % kTmaTile == 0;
     uint4 v[kK];
     uint32_t any = 0u;
 #pragma unroll
-    for (int k = 0; k < kK; k++) {
-      const int ci = k * 256 + threadIdx.x;
-      v[k] = tile[ci];
-      if (!full && g0 + ci >= gend) v[k] = make_uint4(0u, 0u, 0u, 0u);
-      any |= v[k].x | v[k].y | v[k].z | v[k].w;
+    for (int q = 0; q < kK; q++) {
+      const int ci = q * NT + threadIdx.x;
+      v[q] = tile[ci];
+      if (!full && g0 + ci >= gend) v[q] = make_uint4(0u, 0u, 0u, 0u);
+      any |= v[q].x | v[q].y | v[q].z | v[q].w;
     }
     // Sparse: one vote clears the warp's kK segments (2 KB) at once when they
     // are all background -- most of a KiTS-like grid -- so the pack costs ~15
     // issue slots per 2 KB there and leaves the SMs to other ROIs' kernels.
     if (!skip || __any_sync(kFull, any != 0u)) {
 #pragma unroll
-    for (int k = 0; k < kK; k++) {
-      const int ci = k * 256 + threadIdx.x;
-      const long long g = g0 + ci;
-      if (skip && !__any_sync(kFull, (v[k].x | v[k].y | v[k].z | v[k].w) != 0u)) continue;
-      const uint32_t b16 = nib4(v[k].x) | (nib4(v[k].y) << 4) | (nib4(v[k].z) << 8) |
-                           (nib4(v[k].w) << 12);
-      const uint32_t word = b16 | (__shfl_down_sync(kFull, b16, 1) << 16);
-      if (sparse) {
-        if (!__any_sync(kFull, word != 0u && !(threadIdx.x & 1) && g < gend)) continue;
-        if ((threadIdx.x & 31) == 0) {
-          const long long seg = g >> 5;
-          atomicOr(segmap + (seg >> 5), 1u << (seg & 31));
+      for (int q = 0; q < kK; q++) {
+        const int ci = q * NT + threadIdx.x;
+        const long long g = g0 + ci;
+        if (skip && !__any_sync(kFull, (v[q].x | v[q].y | v[q].z | v[q].w) != 0u)) continue;
+        const uint32_t b16 = nib4(v[q].x) | (nib4(v[q].y) << 4) | (nib4(v[q].z) << 8) |
+                             (nib4(v[q].w) << 12);
+        const uint32_t word = b16 | (__shfl_down_sync(kFull, b16, 1) << 16);
+        if (sparse) {
+          if (!__any_sync(kFull, word != 0u && !(threadIdx.x & 1) && g < gend)) continue;
+          if ((threadIdx.x & 31) == 0) {
+            const long long seg = g >> 5;
+            atomicOr(segmap + (seg >> 5), 1u << (seg & 31));
+          }
+        }
+        if (!(threadIdx.x & 1) && g < gend) {
+          bits[g >> 1] = word;
+          if (BOX && word) {
+            const unsigned int wi = (unsigned int)(g >> 1), row = wi / W, col = wi - row * W;
+            const unsigned int z = row / ny, y = row - z * ny;
+            box.x0 = min(box.x0, (int)(32 * col) + __ffs(word) - 1);
+            box.x1 = max(box.x1, (int)(32 * col) + 31 - __clz(word));
+            box.y0 = min(box.y0, (int)y); box.y1 = max(box.y1, (int)y);
+            box.z0 = min(box.z0, (int)z); box.z1 = max(box.z1, (int)z);
+          }
         }
       }
-      if (!(threadIdx.x & 1) && g < gend) {
-        bits[g >> 1] = word;
-        if (BOX && word) {
-          const unsigned int wi = (unsigned int)(g >> 1), row = wi / W, col = wi - row * W;
-          const unsigned int z = row / ny, y = row - z * ny;
-          box.x0 = min(box.x0, (int)(32 * col) + __ffs(word) - 1);
-          box.x1 = max(box.x1, (int)(32 * col) + 31 - __clz(word));
-          box.y0 = min(box.y0, (int)y); box.y1 = max(box.y1, (int)y);
-          box.z0 = min(box.z0, (int)z); box.z1 = max(box.z1, (int)z);
-        }
-      }
-    }
     }
     __syncthreads();  // every thread is done with stage s
-    if (threadIdx.x == 0 && t + kTmaStages < tiles) issue(t + kTmaStages);
+    if (threadIdx.x == 0) issue(s);
   }
   if (BOX) box.flush(st);
 }
-template __global__ void pack_bits_tma<false>(const RoiParams*, uint32_t*, Stats*, uint32_t*);
-template __global__ void pack_bits_tma<true>(const RoiParams*, uint32_t*, Stats*, uint32_t*);
+template __global__ void pack_bits_tma<false, 256>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
+template __global__ void pack_bits_tma<true, 256>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
+template __global__ void pack_bits_tma<false, 128>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
+template __global__ void pack_bits_tma<true, 128>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
 
 // Occupied bbox from the bit volume (L2-resident right after the pack): only
 // nonzero words locate themselves.  Four 16-byte loads in flight per thread.
@@ -390,6 +416,7 @@ __global__ void __launch_bounds__(256) pack_bits_generic(const RoiParams* __rest
                                                          uint32_t* __restrict__ bits,
                                                          Stats* __restrict__ st,
                                                          uint32_t* __restrict__ segmap) {
+  KTrace kt_(st, kTrPack);
   const uint8_t* __restrict__ mask = rp->mask;
   const long long n_words = rp->n_words;
   const int nx = (int)rp->nx, W = rp->W, ny = (int)rp->ny;
@@ -414,46 +441,38 @@ __global__ void __launch_bounds__(256) pack_bits_generic(const RoiParams* __rest
   box.flush(st);
 }
 
-// Occupancy window of lattice row (v, w) for word column q: bit i <-> voxel
-// x = 32q - 1 + i, i in [0, 32].  Out-of-grid voxels are background (this IS
-// the reference's zero padding, mesh.py:55-65).
-__device__ __forceinline__ unsigned long long window(const uint32_t* __restrict__ bits, int q,
-                                                     int v, int w, int W, int ny, int nz) {
-  if (v < 0 || v >= ny || w < 0 || w >= nz) return 0ull;
-  const uint32_t* row = bits + ((long long)w * ny + v) * W;
-  unsigned long long cur = q < W ? __ldcg(row + q) : 0u;
-  unsigned long long prev = q > 0 ? __ldcg(row + q - 1) : 0u;
-  return (cur << 1) | (prev >> 31);
+// Lattice row (v, w) seen by word column q: bit i <-> voxel x = 32q - 1 + i,
+// i in [0, 32] (word q shifted up by one, bit 31 of word q - 1 below it).
+// Out-of-grid voxels are background (this IS the reference's zero padding,
+// mesh.py:55-65).
+// Word wi of the bit volume; with a sparse bit volume, words of unmarked
+// segments read as 0 (the word and its map bit are loaded together).
+__device__ __forceinline__ uint32_t seg_word(const uint32_t* __restrict__ bits,
+                                             const uint32_t* __restrict__ segmap, bool sparse,
+                                             long long wi) {
+  uint32_t x = bits[wi];
+  if (sparse && !((__ldg(segmap + (wi >> 9)) >> ((wi >> 4) & 31)) & 1u)) x = 0u;
+  return x;
+}
+
+// Words q and q - 1 of row (v, w).  All lanes call (converged).  Lanes hold
+// consecutive word columns of one row (item order: q fastest), so word q - 1
+// is the previous lane's word q; at q == qlo (q_first) it is zero (left of the
+// occupied bbox), and only lane 0 with q > qlo loads it itself.
+__device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits,
+                                          const uint32_t* __restrict__ segmap, bool sparse, int q,
+                                          bool q_first, int v, int w, int W, int ny, int nz,
+                                          bool on, uint32_t& cur, uint32_t& prev) {
+  cur = 0u;
+  const bool in = on && v >= 0 && v < ny && w >= 0 && w < nz;
+  const long long rb = ((long long)w * ny + v) * W;
+  if (in && q < W) cur = seg_word(bits, segmap, sparse, rb + q);
+  prev = __shfl_up_sync(kFull, cur, 1);
+  if (q_first) prev = 0u;
+  else if ((threadIdx.x & 31) == 0) prev = in ? seg_word(bits, segmap, sparse, rb + q - 1) : 0u;
 }
 
 constexpr int kStage = 256;  // staged vertices per warp and z step (denser steps emit directly)
-
-// Words q and q - 1 of row (v, w); with a sparse bit volume, words of
-// unmarked segments read as 0 (the word and its map bit are loaded together).
-__device__ __forceinline__ void row_words(const uint32_t* __restrict__ bits,
-                                          const uint32_t* __restrict__ segmap, bool sparse, int q,
-                                          int v, int w, int W, int ny, int nz, bool on,
-                                          uint32_t& cur, uint32_t& prev) {
-  cur = prev = 0u;
-  if (on && v >= 0 && v < ny && w >= 0 && w < nz) {
-    const long long rb = ((long long)w * ny + v) * W;
-    const uint32_t* row = bits + rb;
-    if (q < W) cur = row[q];
-    if (q > 0) prev = row[q - 1];
-    if (sparse) {
-      // segments of words q and q - 1 (one map word unless they straddle one)
-      const long long wc = rb + q, wp = wc - 1;
-      if (q < W) {
-        const uint32_t mc = __ldg(segmap + (wc >> 9));
-        if (!((mc >> ((wc >> 4) & 31)) & 1u)) cur = 0u;
-      }
-      if (q > 0) {  // (word q - 1 exists: wp >= rb >= 0)
-        const uint32_t mp = __ldg(segmap + (wp >> 9));
-        if (!((mp >> ((wp >> 4) & 31)) & 1u)) prev = 0u;
-      }
-    }
-  }
-}
 
 // One thread = one (word column q, row v) and kz consecutive z steps (kz is
 // chosen per ROI on the device and is grid-uniform, so the rolled step loop
@@ -490,11 +509,8 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
   const int lane = threadIdx.x & 31;
   // Warp-private vertex stage (warp-uniform fill level), see the emission.
   uint32_t staged = 0;
-  auto flush = [&]() {
-    __syncwarp();
-    unsigned long long wbase = 0;
-    if (lane == 0) wbase = atomicAdd(&st->n_vert, (unsigned long long)staged);
-    wbase = __shfl_sync(kFull, wbase, 0);
+  // Write the warp's staged vertices at [wbase, wbase + staged) and bin them.
+  auto flush_at = [&](unsigned long long wbase) {
     const int4* stg = s_stage[threadIdx.x >> 5];
     for (uint32_t k0 = 0; k0 < staged; k0 += 32) {
       const uint32_t k = k0 + lane;
@@ -515,6 +531,13 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
     }
     __syncwarp();  // the stage is refilled next
   };
+  // Mid-kernel flush of a full stage: the warp reserves its own range.
+  auto flush = [&]() {
+    __syncwarp();
+    unsigned long long wbase = 0;
+    if (lane == 0) wbase = atomicAdd(&st->n_vert, (unsigned long long)staged);
+    flush_at(__shfl_sync(kFull, wbase, 0));
+  };
   if (xmax >= 0) {
     // Points/cells that can be crossed or active: [min-1, max] on every axis.
     const int qlo = xmin >> 5, qhi = (xmax + 1) >> 5;
@@ -533,16 +556,17 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
         v = vlo + (int)(r % nv);
         w0 = wlo + (int)(r / nv) * kz;
       }
+      const bool qf = !valid || q == qlo;  // word q - 1 is background (see row_words)
       // Rows (v, w) and (v + 1, w) of the step's two z layers; the layer two
       // steps ahead is loaded at the top of each step (one rolled body keeps
       // the kernel inside the instruction cache).
       uint32_t ca0, pa0, cb0, pb0, ca1, pa1, cb1, pb1;
       {
         const bool on0 = valid && w0 <= whi + 1, on1 = valid && 1 <= kz && w0 + 1 <= whi + 1;
-        row_words(bits, segmap, sparse, q, v, w0, W, ny, nz, on0, ca0, pa0);
-        row_words(bits, segmap, sparse, q, v + 1, w0, W, ny, nz, on0, cb0, pb0);
-        row_words(bits, segmap, sparse, q, v, w0 + 1, W, ny, nz, on1, ca1, pa1);
-        row_words(bits, segmap, sparse, q, v + 1, w0 + 1, W, ny, nz, on1, cb1, pb1);
+        row_words(bits, segmap, sparse, q, qf, v, w0, W, ny, nz, on0, ca0, pa0);
+        row_words(bits, segmap, sparse, q, qf, v + 1, w0, W, ny, nz, on0, cb0, pb0);
+        row_words(bits, segmap, sparse, q, qf, v, w0 + 1, W, ny, nz, on1, ca1, pa1);
+        row_words(bits, segmap, sparse, q, qf, v + 1, w0 + 1, W, ny, nz, on1, cb1, pb1);
       }
       const int xbase = 32 * q - 1;
 #pragma unroll 1
@@ -550,8 +574,8 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
         const int w = w0 + s;
         uint32_t ca2, pa2, cb2, pb2;
         const bool on2 = valid && s + 2 <= kz && w + 2 <= whi + 1;
-        row_words(bits, segmap, sparse, q, v, w + 2, W, ny, nz, on2, ca2, pa2);
-        row_words(bits, segmap, sparse, q, v + 1, w + 2, W, ny, nz, on2, cb2, pb2);
+        row_words(bits, segmap, sparse, q, qf, v, w + 2, W, ny, nz, on2, ca2, pa2);
+        row_words(bits, segmap, sparse, q, qf, v + 1, w + 2, W, ny, nz, on2, cb2, pb2);
         const bool on = valid && w <= whi;
         const unsigned long long A = ((unsigned long long)ca0 << 1) | (pa0 >> 31);
         const unsigned long long B = ((unsigned long long)cb0 << 1) | (pb0 >> 31);
@@ -559,6 +583,9 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
         const unsigned long long D = ((unsigned long long)cb1 << 1) | (pb1 >> 31);
         ca0 = ca1; pa0 = pa1; cb0 = cb1; pb0 = pb1;
         ca1 = ca2; pa1 = pa2; cb1 = cb2; pb1 = pb2;
+        // Background around the whole warp (most steps of a sparse bbox): no
+        // active cell, no crossed edge -- nothing else to do this step.
+        if (!__any_sync(kFull, on && (A | B | C | D) != 0ull)) continue;
         uint32_t ex = 0, ey = 0, ez = 0, act = 0;
         if (on) {
           ex = (uint32_t)(A ^ (A >> 1));
@@ -661,7 +688,24 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
       }
     }
   }
-  if (staged) flush();
+  // Final flush: one reservation per block for the last stage of all its
+  // warps (every warp ends here; per-warp reservations were thousands of
+  // returning atomics on the one n_vert counter per ROI).
+  __shared__ unsigned int s_wcnt[256 / 32];
+  __shared__ unsigned long long s_wbase;
+  if (lane == 0) s_wcnt[threadIdx.x >> 5] = staged;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+      const unsigned int c = s_wcnt[w];
+      s_wcnt[w] = tot;
+      tot += c;
+    }
+    s_wbase = tot ? atomicAdd(&st->n_vert, (unsigned long long)tot) : 0ull;
+  }
+  __syncthreads();
+  if (staged) flush_at(s_wbase + s_wcnt[threadIdx.x >> 5]);
   return volk;
 }
 
@@ -673,6 +717,7 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
                                                 unsigned int* __restrict__ pbin_counts,
                                                 const uint32_t* __restrict__ segmap) {
   pdl_enter();
+  KTrace kt_(st, kTrMc);
   __shared__ unsigned int s_hist[kNumCases];
   __shared__ unsigned int s_sup[kSortSupers];
   __shared__ int4 s_stage[256 / 32][kStage];  // per-warp vertex stage (blockDim = 256)

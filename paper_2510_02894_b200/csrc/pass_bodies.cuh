@@ -166,8 +166,10 @@ __device__ __forceinline__ void pass1_3d(const int4* __restrict__ keys, long lon
     // (no filtering when pruning is off: every pair is evaluated)
     const float thr = vfilter ? __double2float_rd(lb - kReachMargin * R2) : -3.0e38f;
     unsigned long long evals = 0;  // pair slots evaluated (diagnostics)
+    uint2 ij_next = work[wb];
     for (long long w = wb; w < we; w++) {
-      const uint2 ij = work[w];
+      const uint2 ij = ij_next;
+      if (w + 1 < we) ij_next = work[w + 1];  // next unit's entry in flight during this one
       const int I = (int)ij.x, J = (int)(ij.y & kIdxMask);
       const unsigned int sub = ij.y >> kSubShift;  // bit 2a + b: i half a x j half b
       // i half a meets the j halves (sub >> 2a) & 3; j half b the i halves
@@ -175,22 +177,33 @@ __device__ __forceinline__ void pass1_3d(const int4* __restrict__ keys, long lon
       const unsigned int ja0 = sub & 3u, ja1 = (sub >> 2) & 3u;
       const unsigned int ib0 = (sub & 1u) | ((sub >> 1) & 2u), ib1 = ((sub >> 1) & 1u) | ((sub >> 2) & 2u);
       __syncwarp();  // the previous unit is done with si / sj
+      // j side first; the i side only when some j survives (most units keep
+      // no vertex on at least one side once the reach filter applies).
       int ni = 0, nj = 0;
 #pragma unroll
       for (int h = 0; h < 2; h++) {
-        const unsigned int jh = h ? ja1 : ja0, ih = h ? ib1 : ib0;
-        const FBox bj = half_box(boxes, hboxes, J, jh ? jh : 3u, f);  // reach target of i half h
+        const unsigned int ih = h ? ib1 : ib0;
         const FBox bi = half_box(boxes, hboxes, I, ih ? ih : 3u, f);  // reach target of j half h
 #pragma unroll
         for (int r = 2 * h; r < 2 * h + 2; r++) {
-          const long long i = (long long)I * kChunk + r * 32 + lane;
           const long long j = (long long)J * kChunk + r * 32 + lane;
-          const float3 p = frame_coord(keys[i < n ? i : n - 1], f);
           const float3 q = frame_coord(keys[j < n ? j : n - 1], f);
-          warp_append(si, ni, i < n && jh && reach_sq(p, bj) >= thr,
-                      make_float4(p.x, p.y, p.z, fmaf(p.x, p.x, fmaf(p.y, p.y, p.z * p.z))));
           warp_append(sj, nj, j < n && ih && reach_sq(q, bi) >= thr,
                       make_float4(q.x, q.y, q.z, fmaf(q.x, q.x, fmaf(q.y, q.y, q.z * q.z))));
+        }
+      }
+      if (nj > 0) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const unsigned int jh = h ? ja1 : ja0;
+          const FBox bj = half_box(boxes, hboxes, J, jh ? jh : 3u, f);  // reach target of i half h
+#pragma unroll
+          for (int r = 2 * h; r < 2 * h + 2; r++) {
+            const long long i = (long long)I * kChunk + r * 32 + lane;
+            const float3 p = frame_coord(keys[i < n ? i : n - 1], f);
+            warp_append(si, ni, i < n && jh && reach_sq(p, bj) >= thr,
+                        make_float4(p.x, p.y, p.z, fmaf(p.x, p.x, fmaf(p.y, p.y, p.z * p.z))));
+          }
         }
       }
       __syncwarp();
@@ -442,8 +455,10 @@ __device__ __forceinline__ void pass1_planar(const int2* __restrict__ sorted,
   }
   float run0 = 0.f, run1 = 0.f, run2 = 0.f;  // per-family maxima
   unsigned long long evals = 0;
+  uint2 u_next = pwork[wb];
   for (long long w = wb; w < we; w++) {
-    const uint2 u = pwork[w];
+    const uint2 u = u_next;
+    if (w + 1 < we) u_next = pwork[w + 1];  // next unit's entry in flight during this one
     const unsigned int p = u.x & kIdxMask, I = u.y >> 16, J = u.y & 0xffffu;
     const unsigned int sub = u.x >> kSubShift;  // bit 2a + b: i half a x j half b
     const unsigned int b0 = start[p], np = start[p + 1] - b0, c0 = cstart[p];
@@ -453,21 +468,31 @@ __device__ __forceinline__ void pass1_planar(const int2* __restrict__ sorted,
     const unsigned int ja0 = sub & 3u, ja1 = (sub >> 2) & 3u;
     const unsigned int ib0 = (sub & 1u) | ((sub >> 1) & 2u), ib1 = ((sub >> 1) & 1u) | ((sub >> 2) & 2u);
     __syncwarp();  // previous unit is done with si / sj
-    int ni = 0, nj = 0;
+    int ni = 0, nj = 0;  // j side first, the i side only if some j survives
 #pragma unroll
     for (int h = 0; h < 2; h++) {
-      const unsigned int jh = h ? ja1 : ja0, ih = h ? ib1 : ib0;
-      const float4 bj = plane_half_box(pboxes, hpboxes, c0 + J, jh ? jh : 3u, ax);
+      const unsigned int ih = h ? ib1 : ib0;
       const float4 bi = plane_half_box(pboxes, hpboxes, c0 + I, ih ? ih : 3u, ax);
 #pragma unroll
       for (int r = 2 * h; r < 2 * h + 2; r++) {
-        const unsigned int i = I * kPC + r * 32 + lane, j = J * kPC + r * 32 + lane;
-        const float2 pi = plane_point(sorted[b0 + min(i, np - 1)], ax);
+        const unsigned int j = J * kPC + r * 32 + lane;
         const float2 qj = plane_point(sorted[b0 + min(j, np - 1)], ax);
-        warp_append(si, ni, i < np && jh && reach_sq2(pi, bj) >= th,
-                    make_float4(pi.x, pi.y, fmaf(pi.x, pi.x, pi.y * pi.y), 0.f));
         warp_append(sj, nj, j < np && ih && reach_sq2(qj, bi) >= th,
                     make_float4(qj.x, qj.y, fmaf(qj.x, qj.x, qj.y * qj.y), 0.f));
+      }
+    }
+    if (nj > 0) {
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const unsigned int jh = h ? ja1 : ja0;
+        const float4 bj = plane_half_box(pboxes, hpboxes, c0 + J, jh ? jh : 3u, ax);
+#pragma unroll
+        for (int r = 2 * h; r < 2 * h + 2; r++) {
+          const unsigned int i = I * kPC + r * 32 + lane;
+          const float2 pi = plane_point(sorted[b0 + min(i, np - 1)], ax);
+          warp_append(si, ni, i < np && jh && reach_sq2(pi, bj) >= th,
+                      make_float4(pi.x, pi.y, fmaf(pi.x, pi.x, pi.y * pi.y), 0.f));
+        }
       }
     }
     __syncwarp();

@@ -16,6 +16,7 @@ __global__ void __launch_bounds__(kDiamThreads, 4) diam_pass1(
     const int4* __restrict__ hboxes, int vfilter, const unsigned int* __restrict__ cstart,
     const int4* __restrict__ pboxes, const int4* __restrict__ hpboxes) {
   pdl_enter();
+  KTrace kt_(st, kTrPass1);
   if (st->ovf || st->bbox[3] < 0) return;  // re-run pending (scan_all) / empty
   __shared__ float4 sj_all[kWarps][kChunk];  // per-warp J chunk, (x, y, z | -, |p|^2)
   __shared__ float4 si_all[kWarps][kChunk];  // per-warp filtered I list
@@ -45,6 +46,7 @@ __global__ void __launch_bounds__(kDiamThreads) diam_refine(
     const uint2* __restrict__ pwork, long long pwcap, const float* __restrict__ pumax,
     Stats* __restrict__ st, Stats* out_host) {
   pdl_enter();
+  KTrace kt_(st, kTrRefine);
   __shared__ double s_a[kChunk], s_b[kChunk], s_c[kChunk];
   __shared__ double s_red[kDiamThreads / 32];
   __shared__ unsigned int s_list[kDiamThreads];

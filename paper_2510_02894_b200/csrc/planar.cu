@@ -74,6 +74,7 @@ __global__ void plane_boxes(const int2* __restrict__ sorted,
                             const Stats* __restrict__ st, int4* __restrict__ pboxes,
                             unsigned long long* __restrict__ pext, int4* __restrict__ hpboxes) {
   pdl_enter();
+  KTrace kt_(st, kTrPlaneBoxes);
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   if (st->bbox[3] < 0) return;
@@ -147,6 +148,7 @@ __global__ void plane_lb(const int2* __restrict__ sorted, const unsigned int* __
                          const unsigned long long* __restrict__ pext, const RoiParams* __restrict__ rp,
                          Stats* __restrict__ st) {
   pdl_enter();
+  KTrace kt_(st, kTrPlaneLb);
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   if (st->bbox[3] < 0) return;
@@ -200,6 +202,7 @@ __global__ void plane_filter(const unsigned int* __restrict__ start,
                              Stats* __restrict__ st, uint2* __restrict__ pwork,
                              const int4* __restrict__ hpboxes) {
   pdl_enter();
+  KTrace kt_(st, kTrPlaneFilter);
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   const long long units = (long long)st->plane_units;

@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_all(unsigned int* __restric
                                                          unsigned int* __restrict__ pbin_cursor,
                                                          unsigned long long* __restrict__ pext) {
   pdl_enter();
+  KTrace kt_(st, kTrScan);
   if (blockIdx.x == 0 && threadIdx.x == 0) st->t_mesh = global_ns();  // marching cubes done
   int bb[6];
 #pragma unroll
@@ -221,6 +222,7 @@ __global__ void scatter_all(const int4* __restrict__ keys, long long cap,
                             int2* __restrict__ plane_sorted,
                             unsigned int* __restrict__ sort_supers) {
   pdl_enter();
+  KTrace kt_(st, kTrScatter);
   // scan_all has consumed the super-bin counts: leave them zeroed for the next ROI.
   if (blockIdx.x == 0) sort_supers[threadIdx.x] = 0u;
   if (st->ovf) return;  // re-run pending (scan_all)
@@ -302,6 +304,7 @@ __global__ void __launch_bounds__(256) boxes_extremes(const int4* __restrict__ k
                                                       int4* __restrict__ sboxes,
                                                       int4* __restrict__ hboxes) {
   pdl_enter();
+  KTrace kt_(st, kTrBoxes);
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   __shared__ unsigned long long s_ext[2 * kNDir];
@@ -497,6 +500,7 @@ __global__ void __launch_bounds__(256) unit_filter(const int4* __restrict__ keys
                                                    const int4* __restrict__ hboxes,
                                                    uint2* __restrict__ slist, long long scap) {
   pdl_enter();
+  KTrace kt_(st, kTrUnitFilter);
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   const long long n = n_verts(st, cap);
@@ -556,6 +560,7 @@ __global__ void __launch_bounds__(256) unit_expand(const int4* __restrict__ boxe
                                                    const uint2* __restrict__ slist,
                                                    long long scap) {
   pdl_enter();
+  KTrace kt_(st, kTrUnitExpand);
   if (st->ovf) return;
   const long long ns = min((long long)st->n_super, scap);
   if (ns == 0) return;  // small ROI: unit_filter listed everything itself

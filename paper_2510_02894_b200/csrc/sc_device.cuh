@@ -44,9 +44,17 @@ struct Stats {
   // mesh_ms / diameters_ms without event nodes in the graph.
   unsigned long long t_start, t_mesh, t_end;
   unsigned int plane_ovf;              // a plane holds more than kPlaneMaxEntries entries
-  unsigned int pad_;
+  unsigned int pack_next;              // next 16 KB mask tile to claim (TMA pack)
   unsigned long long n_eval;           // 3-D pair slots pass 1 evaluated (after the vertex filter)
   unsigned long long n_peval;          // planar pair slots pass 1 evaluated
+  // %globaltimer of each pipeline kernel's first block start / last block
+  // end (index: TraceId), for the batch timeline (SC_TRACE=1 on the host).
+  unsigned long long tr[16][2];
+};
+
+enum TraceId {
+  kTrPack = 1, kTrMc, kTrScan, kTrScatter, kTrPlaneBoxes, kTrPlaneLb, kTrPlaneFilter, kTrBoxes,
+  kTrUnitFilter, kTrUnitExpand, kTrPass1, kTrRefine, kTrCount
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -54,6 +62,20 @@ __device__ __forceinline__ unsigned long long global_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+
+// Block-granular kernel span on the ROI record: earliest block start (min)
+// and latest block end (max; thread 0 leaving the kernel), two reductions per
+// block.  init_stats seeds the starts with ~0.
+struct KTrace {
+  unsigned long long* e;
+  __device__ __forceinline__ KTrace(const Stats* st, int id)
+      : e(const_cast<Stats*>(st)->tr[id]) {
+    if (threadIdx.x == 0) atomicMin(e, global_ns());
+  }
+  __device__ __forceinline__ ~KTrace() {
+    if (threadIdx.x == 0) atomicMax(e + 1, global_ns());
+  }
+};
 
 // 3-D chunk pairs (128 x 128 vertices) tested directly by unit_filter up to
 // this many; above it the 1024-vertex super pairs are listed first (slist)
@@ -113,6 +135,8 @@ struct RoiParams {
                        // volume and marks them in the segment map; readers treat
                        // unmarked segments as zero (0: every word is written); bit 1:
                        // the pack skips the conversion of all-zero segments
+  int pflags;          // TMA pack: bit 0 dynamic tile claims, bit 1 suspend-hinted waits
+  int pad0_;
   Frame f;             // cx2..cz2 are filled on the device from the bbox
   long long wcap;      // capacity of the 3-D work list (overflow -> exact re-run)
 };
@@ -152,9 +176,7 @@ __device__ __forceinline__ unsigned int spread_bits(unsigned int v) {  // <= 10 
 // Brick shift (doubled units) so the bbox spans <= 64 bricks per axis.
 __device__ __forceinline__ int brick_shift(const int* bb) {
   const int ext = max(bb[3] - bb[0], max(bb[4] - bb[1], bb[5] - bb[2])) * 2 + 3;
-  int s = 0;
-  while ((ext >> s) >= 64) s++;
-  return s;
+  return max(0, (32 - __clz(ext)) - 6);  // smallest s with (ext >> s) < 64
 }
 
 __device__ __forceinline__ unsigned int brick_bin(int X, int Y, int Z, const int* bb, int s) {
@@ -194,9 +216,7 @@ constexpr long long kPlaneMaxEntries = 65536LL * kPlaneChunk;
 
 __device__ __forceinline__ int axis_shift(int lo, int hi) {  // voxel bbox [lo, hi]
   const int ext = 2 * (hi - lo) + 3;
-  int s = 0;
-  while ((ext >> s) >= 16) s++;
-  return s;
+  return max(0, (32 - __clz(ext)) - 4);  // smallest s with (ext >> s) < 16
 }
 
 __device__ __forceinline__ unsigned int spread2x4(unsigned int v) {  // 4 bits -> even bits
