@@ -43,7 +43,10 @@ __global__ void pack_bits_v16(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 __global__ void bits_bbox(const RoiParams*, const uint4*, Stats*, const uint32_t*);
 template <bool BOX, int NT>
 __global__ void pack_bits_tma(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
+template <bool BOX, int NT>
+__global__ void pack_bits_tmaw(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
 constexpr int kTmaTileBytes = 16384;  // mc.cu kTmaTile
+constexpr int kWarpTileBytes = 4096;  // mc.cu kWarpTile
 constexpr int kTmaMaxSmem = 8 * kTmaTileBytes;  // mc.cu kTmaMaxStages x kTmaTile
 __global__ void pack_bits_generic(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 __global__ void mc_cells(const RoiParams*, const uint32_t*, const CaseTables*, Stats*, int4*,
@@ -129,6 +132,7 @@ struct Opts {
   bool pack_skip = true;     // sparse pack: no conversion of all-zero segments
   int pack_tma = 1;          // batch graphs: TMA bulk-copy pack, CTAs per SM (0 = 128-bit loads)
   int pack_tma_single = 0;   // the same for single calls (the 128-bit-load pack is faster alone)
+  bool pack_warpring = false; // TMA pack as per-warp rings (pack_bits_tmaw, "pack_warpring")
   bool pack_prio = true;      // init_stats + pack at the greatest stream priority ("pack_prio")
   int pack_threads = 256;     // TMA pack CTA size (128 / 256, "pack_threads")
   int pack_stages = 4;       // TMA pack ring depth, 16 KB tiles (2..8, "pack_stages")
@@ -420,6 +424,13 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     CK(cudaFuncSetAttribute(pack_bits_tma<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
     CK(cudaFuncSetAttribute(pack_bits_tma<false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
     CK(cudaFuncSetAttribute(pack_bits_tma<true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tmaw<false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tmaw<true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tmaw<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tmaw<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
+    // (32 / 64-thread rings need at most 2 x 8 x 4 KB = 64 KB: under the default limit + opt-in)
+    CK(cudaFuncSetAttribute(pack_bits_tmaw<false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tmaw<true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
     CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
     for (auto& e : c->cev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -455,6 +466,10 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
                                (const void*)pack_bits_v16<4, true>,
                                (const void*)pack_bits_tma<false, 256>, (const void*)pack_bits_tma<true, 256>,
                                (const void*)pack_bits_tma<false, 128>, (const void*)pack_bits_tma<true, 128>,
+                               (const void*)pack_bits_tmaw<false, 128>, (const void*)pack_bits_tmaw<true, 128>,
+                               (const void*)pack_bits_tmaw<false, 256>, (const void*)pack_bits_tmaw<true, 256>,
+                               (const void*)pack_bits_tmaw<false, 64>, (const void*)pack_bits_tmaw<true, 64>,
+                               (const void*)pack_bits_tmaw<false, 32>, (const void*)pack_bits_tmaw<true, 32>,
                                (const void*)mesh_count, (const void*)mesh_emit,
                                (const void*)bits_bbox,
                                (const void*)pack_bits_generic, (const void*)mc_cells,
@@ -662,7 +677,25 @@ cudaError_t launch_tma_pack(Ctx* c, cudaStream_t s) {
   const size_t smem = (size_t)st * kTmaTileBytes;
   const dim3 grid((unsigned)(c->sms * c->o.pack_tma));
   const RoiParams* rp = c->d_rp;
-  if (c->o.pack_threads == 128)
+  if (c->o.pack_warpring) {  // per-warp rings of `pack_stages` 4 KB tiles
+    const int nt = c->o.pack_threads, ws = st;
+    const size_t wsmem = (size_t)(nt / 32) * ws * kWarpTileBytes;
+    switch (nt) {
+      case 32:
+        return launch_prio(c, s, grid, 32, wsmem, pack_bits_tmaw<BOX, 32>, rp, c->bits.p,
+                           c->d_stats, c->segmap.p, ws);
+      case 64:
+        return launch_prio(c, s, grid, 64, wsmem, pack_bits_tmaw<BOX, 64>, rp, c->bits.p,
+                           c->d_stats, c->segmap.p, ws);
+      case 128:
+        return launch_prio(c, s, grid, 128, wsmem, pack_bits_tmaw<BOX, 128>, rp, c->bits.p,
+                           c->d_stats, c->segmap.p, ws);
+      default:
+        return launch_prio(c, s, grid, 256, wsmem, pack_bits_tmaw<BOX, 256>, rp, c->bits.p,
+                           c->d_stats, c->segmap.p, ws);
+    }
+  }
+  if (c->o.pack_threads <= 128)  // (the block-ring pack has 128- and 256-thread forms)
     return launch_prio(c, s, grid, 128, smem, pack_bits_tma<BOX, 128>, rp, c->bits.p, c->d_stats,
                        c->segmap.p, st);
   return launch_prio(c, s, grid, 256, smem, pack_bits_tma<BOX, 256>, rp, c->bits.p, c->d_stats,
@@ -956,7 +989,7 @@ bool host_prof_on() {
 // per kernel its mean start offset from the ROI start (init_stats) and mean
 // span, plus the mean ROI latency; printed at the end of each batch.
 struct TraceAcc {
-  double off[kTrCount] = {}, span[kTrCount] = {};
+  double off[kTrCount] = {}, span[kTrCount] = {}, busy[kTrCount] = {};
   long long n[kTrCount] = {};
   double lat = 0;
   long long rois = 0;
@@ -976,6 +1009,7 @@ void trace_add(const Stats& h) {
     if (h.tr[k][0] == ~0ull || end < h.tr[k][0]) continue;
     g_trace.off[k] += 1e-3 * (double)(h.tr[k][0] - h.t_start);
     g_trace.span[k] += 1e-3 * (double)(end - h.tr[k][0]);
+    g_trace.busy[k] += 1e-3 * (double)h.busy[k];
     g_trace.n[k]++;
   }
   if (h.t_end > h.t_start) {
@@ -994,8 +1028,9 @@ void trace_print() {
                g_trace.rois, g_trace.lat / (double)g_trace.rois);
   for (int k = 1; k < kTrCount; k++)
     if (g_trace.n[k])
-      std::fprintf(stderr, "[sc trace]   %-15s start +%8.1f us  span %8.1f us\n", names[k],
-                   g_trace.off[k] / (double)g_trace.n[k], g_trace.span[k] / (double)g_trace.n[k]);
+      std::fprintf(stderr, "[sc trace]   %-15s start +%8.1f us  span %8.1f us  block-us %9.1f\n",
+                   names[k], g_trace.off[k] / (double)g_trace.n[k],
+                   g_trace.span[k] / (double)g_trace.n[k], g_trace.busy[k] / (double)g_trace.n[k]);
   // Admission: ROI i (slot i mod S) starts after ROI i - S ended (slot reuse:
   // host collect + relaunch) and after ROI i - chain's pack (pack chain).
   const auto& q = g_trace.seq;
@@ -1025,8 +1060,9 @@ void trace_print() {
 
 // Everything about the pack that a captured graph bakes in.
 int pack_key(const Opts& o) {
-  return o.pack_mode + 32 * o.pack_bps + 4096 * o.pack_tma + 16384 * o.pack_stages +
-         (o.pack_threads == 128 ? (1 << 20) : 0) + (o.pack_prio ? (1 << 21) : 0);
+  return (o.pack_mode & 7) | ((o.pack_bps & 63) << 3) | ((o.pack_tma & 15) << 9) |
+         ((o.pack_stages & 15) << 13) | (((o.pack_threads / 32) & 15) << 17) |
+         ((o.pack_prio ? 1 : 0) << 21) | ((o.pack_warpring ? 1 : 0) << 22);
 }
 
 int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
@@ -1837,16 +1873,16 @@ int set_opt(Opts& o, const char* name, int value) {
   else if (std::strcmp(name, "host_pack") == 0) o.host_pack = std::max(-1, std::min(1, value));
   else if (std::strcmp(name, "host_split") == 0) o.split = std::max(-1, std::min(90, value));
   else if (std::strcmp(name, "pack_mode") == 0) o.pack_mode = value & 7;
-  else if (std::strcmp(name, "pack_bps") == 0) o.pack_bps = std::max(0, value);
+  else if (std::strcmp(name, "pack_bps") == 0) o.pack_bps = std::max(0, std::min(63, value));
   else if (std::strcmp(name, "grid_div") == 0) o.grid_div = std::max(1, value);
   else if (std::strcmp(name, "grid_div_single") == 0) o.grid_div_single = std::max(1, value);
   else if (std::strcmp(name, "pdl") == 0) o.pdl = value != 0;
   else if (std::strcmp(name, "fork") == 0) o.fork = value != 0;
   else if (std::strcmp(name, "zero_copy") == 0) o.zc = value != 0;
   else if (std::strcmp(name, "stage_times") == 0) o.stage_times = std::max(0, std::min(2, value));
-  else if (std::strcmp(name, "pack_tma") == 0) o.pack_tma = std::max(0, std::min(3, value));
+  else if (std::strcmp(name, "pack_tma") == 0) o.pack_tma = std::max(0, std::min(8, value));
   else if (std::strcmp(name, "pack_chain") == 0) o.pack_chain = std::max(0, std::min(8, value));
-  else if (std::strcmp(name, "pack_tma_single") == 0) o.pack_tma_single = std::max(0, std::min(3, value));
+  else if (std::strcmp(name, "pack_tma_single") == 0) o.pack_tma_single = std::max(0, std::min(8, value));
   else if (std::strcmp(name, "sparse_bits") == 0) o.sparse = value != 0;
   else if (std::strcmp(name, "pack_skip") == 0) o.pack_skip = value != 0;
   else if (std::strcmp(name, "batch_stage_times") == 0) o.batch_times = value != 0;
@@ -1854,7 +1890,9 @@ int set_opt(Opts& o, const char* name, int value) {
   else if (std::strcmp(name, "debug_empty") == 0) o.empty = std::max(0, value);
   else if (std::strcmp(name, "pack_dyn") == 0) o.pack_dyn = value != 0;
   else if (std::strcmp(name, "pack_prio") == 0) o.pack_prio = value != 0;
-  else if (std::strcmp(name, "pack_threads") == 0) o.pack_threads = value == 128 ? 128 : 256;
+  else if (std::strcmp(name, "pack_warpring") == 0) o.pack_warpring = value != 0;
+  else if (std::strcmp(name, "pack_threads") == 0)
+    o.pack_threads = (value == 32 || value == 64 || value == 128) ? value : 256;
   else if (std::strcmp(name, "pack_stages") == 0) o.pack_stages = std::max(2, std::min(8, value));
   else if (std::strcmp(name, "pack_sleep") == 0) o.pack_sleep = value != 0;
   else if (std::strcmp(name, "debug_stages") == 0) o.stages = value > 0 ? value : (1 << 30);

@@ -321,6 +321,110 @@ __global__ void __launch_bounds__(NT, 1) pack_bits_tma(const RoiParams* __restri
   }
   if (BOX) box.flush(st);
 }
+// Warp-ring variant (option "pack_warpring"): every warp streams its own
+// contiguous share of the mask through a private ring of `stages` 4 KB tiles
+// (its own mbarriers, lane 0 issues the bulk copies), so no block barrier
+// ever couples the warps: a warp converts a landed tile and immediately
+// refills that stage.  One 512-byte warp load = one bit-volume segment, as in
+// pack_bits_v16.
+constexpr int kWarpTile = 4096;
+constexpr int kWarpMaxStages = 8;
+
+template <bool BOX, int NT>
+__global__ void __launch_bounds__(NT, 1) pack_bits_tmaw(const RoiParams* __restrict__ rp,
+                                                       uint32_t* __restrict__ bits,
+                                                       Stats* __restrict__ st,
+                                                       uint32_t* __restrict__ segmap,
+                                                       int stages) {
+  KTrace kt_(st, kTrPack);
+  constexpr int NW = NT / 32;
+  extern __shared__ __align__(128) unsigned char s_ring[];  // NW x stages x kWarpTile
+  __shared__ __align__(8) uint64_t s_full[NW][kWarpMaxStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* ring = s_ring + (size_t)warp * stages * kWarpTile;
+  const unsigned char* mask = rp->mask;
+  const long long n_bytes = 16LL * rp->n_chunks;
+  const bool sparse = rp->sparse != 0;
+  const bool skip = (rp->sparse & 2) != 0;
+  const bool sleep = (rp->pflags & 2) != 0;
+  const unsigned int W = (unsigned int)rp->W, ny = (unsigned int)rp->ny;
+  BoxAcc box;
+  const long long tiles = (n_bytes + kWarpTile - 1) / kWarpTile;
+  const long long G = (long long)gridDim.x * NW, gw = (long long)blockIdx.x * NW + warp;
+  const long long per = (tiles + G - 1) / G;
+  const long long t0 = min(tiles, gw * per), t1 = min(tiles, t0 + per);
+  uint64_t policy;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  auto issue = [&](long long t, int s) {  // lane 0 only
+    const long long off = t * kWarpTile;
+    const unsigned bytes = (unsigned)min((long long)kWarpTile, n_bytes - off);
+    mbar_expect_tx(&s_full[warp][s], bytes);
+    bulk_load(ring + s * kWarpTile, mask + off, bytes, &s_full[warp][s], policy);
+  };
+  if (lane == 0) {
+    for (int s = 0; s < stages; s++) mbar_init(&s_full[warp][s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < stages && t0 + s < t1; s++) issue(t0 + s, s);
+  }
+  __syncwarp();
+  constexpr int kQ = kWarpTile / 512;  // 512-byte warp loads (segments) per tile
+  const long long gend = n_bytes / 16;
+  for (long long t = t0; t < t1; t++) {
+    const int k = (int)(t - t0), s = k % stages;
+    mbar_wait(&s_full[warp][s], (unsigned)(k / stages) & 1u, sleep);
+    const uint4* tile = reinterpret_cast<const uint4*>(ring + s * kWarpTile);
+    const long long g0 = t * (kWarpTile / 16);
+    const bool full = t + 1 < tiles || n_bytes % kWarpTile == 0;
+    uint4 v[kQ];
+    uint32_t any = 0u;
+#pragma unroll
+    for (int q = 0; q < kQ; q++) {
+      v[q] = tile[q * 32 + lane];
+      if (!full && g0 + q * 32 + lane >= gend) v[q] = make_uint4(0u, 0u, 0u, 0u);
+      any |= v[q].x | v[q].y | v[q].z | v[q].w;
+    }
+    __syncwarp();  // every lane has its data: the stage can be refilled now
+    if (lane == 0 && t + stages < t1) issue(t + stages, s);
+    if (!skip || __any_sync(kFull, any != 0u)) {
+#pragma unroll
+      for (int q = 0; q < kQ; q++) {
+        const long long g = g0 + q * 32 + lane;
+        if (skip && !__any_sync(kFull, (v[q].x | v[q].y | v[q].z | v[q].w) != 0u)) continue;
+        const uint32_t b16 = nib4(v[q].x) | (nib4(v[q].y) << 4) | (nib4(v[q].z) << 8) |
+                             (nib4(v[q].w) << 12);
+        const uint32_t word = b16 | (__shfl_down_sync(kFull, b16, 1) << 16);
+        if (sparse) {
+          if (!__any_sync(kFull, word != 0u && !(lane & 1) && g < gend)) continue;
+          if (lane == 0) {
+            const long long seg = g >> 5;
+            atomicOr(segmap + (seg >> 5), 1u << (seg & 31));
+          }
+        }
+        if (!(lane & 1) && g < gend) {
+          bits[g >> 1] = word;
+          if (BOX && word) {
+            const unsigned int wi = (unsigned int)(g >> 1), row = wi / W, col = wi - row * W;
+            const unsigned int z = row / ny, y = row - z * ny;
+            box.x0 = min(box.x0, (int)(32 * col) + __ffs(word) - 1);
+            box.x1 = max(box.x1, (int)(32 * col) + 31 - __clz(word));
+            box.y0 = min(box.y0, (int)y); box.y1 = max(box.y1, (int)y);
+            box.z0 = min(box.z0, (int)z); box.z1 = max(box.z1, (int)z);
+          }
+        }
+      }
+    }
+  }
+  if (BOX) box.flush(st);
+}
+template __global__ void pack_bits_tmaw<false, 128>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
+template __global__ void pack_bits_tmaw<true, 128>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
+template __global__ void pack_bits_tmaw<false, 256>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
+template __global__ void pack_bits_tmaw<true, 256>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
+template __global__ void pack_bits_tmaw<false, 32>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
+template __global__ void pack_bits_tmaw<true, 32>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
+template __global__ void pack_bits_tmaw<false, 64>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
+template __global__ void pack_bits_tmaw<true, 64>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
+
 template __global__ void pack_bits_tma<false, 256>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
 template __global__ void pack_bits_tma<true, 256>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
 template __global__ void pack_bits_tma<false, 128>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
@@ -451,7 +555,10 @@ __device__ __forceinline__ uint32_t seg_word(const uint32_t* __restrict__ bits,
                                              const uint32_t* __restrict__ segmap, bool sparse,
                                              long long wi) {
   uint32_t x = bits[wi];
-  if (sparse && !((__ldg(segmap + (wi >> 9)) >> ((wi >> 4) & 31)) & 1u)) x = 0u;
+  if (sparse) {
+    const unsigned int lo = (unsigned int)wi;  // bit (wi >> 4) & 31 needs only the low word
+    if (!((__ldg(segmap + (wi >> 9)) >> ((lo >> 4) & 31u)) & 1u)) x = 0u;
+  }
   return x;
 }
 
@@ -551,10 +658,18 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
       const bool valid = item < n_items;
       int q = 0, v = 0, w0 = 0;
       if (valid) {
-        q = qlo + (int)(item % nq);
-        long long r = item / nq;
-        v = vlo + (int)(r % nv);
-        w0 = wlo + (int)(r / nv) * kz;
+        if (n_items < (1LL << 32)) {  // (grid-uniform) 32-bit decomposition
+          const unsigned int it = (unsigned int)item, r = it / (unsigned int)nq;
+          q = qlo + (int)(it - r * (unsigned int)nq);
+          const unsigned int r2 = r / (unsigned int)nv;
+          v = vlo + (int)(r - r2 * (unsigned int)nv);
+          w0 = wlo + (int)r2 * kz;
+        } else {
+          q = qlo + (int)(item % nq);
+          long long r = item / nq;
+          v = vlo + (int)(r % nv);
+          w0 = wlo + (int)(r / nv) * kz;
+        }
       }
       const bool qf = !valid || q == qlo;  // word q - 1 is background (see row_words)
       // Rows (v, w) and (v + 1, w) of the step's two z layers; the layer two

@@ -152,10 +152,12 @@ __device__ __forceinline__ void pass1_3d(const int4* __restrict__ keys, long lon
   const long long n_work = (long long)st->n_work;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Each warp takes a contiguous run of units.
-  const long long gwarps = (long long)gridDim.x * kWarps;
-  const long long gw = (long long)blockIdx.x * kWarps + warp;
-  const long long per = (n_work + gwarps - 1) / gwarps;
-  const long long wb = gw * per, we = min(n_work, wb + per);
+  // (32-bit split: a work list never exceeds 2^32 entries -- it is capped by
+  // wcap -- and a 64-bit division per warp was ~3 % of the kernel)
+  const unsigned int gwarps = gridDim.x * kWarps;
+  const unsigned int gw = blockIdx.x * kWarps + warp;
+  const unsigned int per = ((unsigned int)n_work + gwarps - 1) / gwarps;
+  const long long wb = (long long)gw * per, we = min(n_work, wb + per);
   if (wb >= we) return;
   float run = 0.f;
   if (FILTER) {
@@ -432,14 +434,14 @@ __device__ __forceinline__ void pass1_planar(const int2* __restrict__ sorted,
   const PlaneSpace ps = plane_space(st);
   const long long w0 = 0, w1 = (long long)st->n_pwork;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long gwarps = (long long)gridDim.x * kPlaneWarps;
+  const unsigned int gwarps = gridDim.x * kPlaneWarps;
   // Rotated by the 3-D list's warp count: when both lists are short (fewer
   // units than warps), the planar units go to the warps the 3-D list left
   // idle instead of queueing behind 3-D units on the same warps.
-  const long long busy3 = min((long long)st->n_work, gwarps);
-  const long long gw = ((long long)blockIdx.x * kPlaneWarps + warp + gwarps - busy3) % gwarps;
-  const long long per = (w1 - w0 + gwarps - 1) / gwarps;
-  const long long wb = w0 + gw * per, we = min(w1, wb + per);
+  const unsigned int busy3 = (unsigned int)min((unsigned long long)st->n_work, (unsigned long long)gwarps);
+  const unsigned int gw = (blockIdx.x * kPlaneWarps + warp + gwarps - busy3) % gwarps;
+  const unsigned int per = ((unsigned int)(w1 - w0) + gwarps - 1) / gwarps;
+  const long long wb = w0 + (long long)gw * per, we = min(w1, wb + per);
   if (wb >= we) return;
   float thr[3];
   {

@@ -50,6 +50,7 @@ struct Stats {
   // %globaltimer of each pipeline kernel's first block start / last block
   // end (index: TraceId), for the batch timeline (SC_TRACE=1 on the host).
   unsigned long long tr[16][2];
+  unsigned long long busy[16];         // summed block residency (ns) per kernel
 };
 
 enum TraceId {
@@ -68,12 +69,21 @@ __device__ __forceinline__ unsigned long long global_ns() {
 // block.  init_stats seeds the starts with ~0.
 struct KTrace {
   unsigned long long* e;
+  unsigned long long* b;
+  unsigned long long t0;
   __device__ __forceinline__ KTrace(const Stats* st, int id)
-      : e(const_cast<Stats*>(st)->tr[id]) {
-    if (threadIdx.x == 0) atomicMin(e, global_ns());
+      : e(const_cast<Stats*>(st)->tr[id]), b(const_cast<Stats*>(st)->busy + id), t0(0) {
+    if (threadIdx.x == 0) {
+      t0 = global_ns();
+      atomicMin(e, t0);
+    }
   }
   __device__ __forceinline__ ~KTrace() {
-    if (threadIdx.x == 0) atomicMax(e + 1, global_ns());
+    if (threadIdx.x == 0) {
+      const unsigned long long t1 = global_ns();
+      atomicMax(e + 1, t1);
+      atomicAdd(b, t1 - t0);
+    }
   }
 };
 

@@ -11,8 +11,8 @@ from paper_2510_02894_b200 import _native
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 opts = {"pack_tma_single": 1, "fused_bbox_single": 1} if "tma" in sys.argv[2:] else {}
-rois, _ = bench.load_workload(name)
-mask, sp = rois[0]
+g, sp = bench.workload_params(name)[0]  # the workload's first ROI only
+mask = g()
 d = torch.from_numpy(mask).cuda()
 with _native.thread_options(**opts):
     for _ in range(3):
