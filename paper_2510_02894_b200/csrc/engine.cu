@@ -53,7 +53,7 @@ __global__ void mc_cells(const RoiParams*, const uint32_t*, const CaseTables*, S
                          long long, unsigned int*, unsigned int*, const uint32_t*);
 __global__ void scan_all(unsigned int*, unsigned int*, unsigned int*, unsigned int*,
                          unsigned int*, unsigned int*, long long, Stats*, int4*, unsigned int*,
-                         unsigned int*, unsigned long long*);
+                         unsigned int*, unsigned long long*, unsigned int*);
 __global__ void scatter_all(const int4*, long long, const Stats*, unsigned int*, int4*,
                             const unsigned int*, unsigned int*, int2*, unsigned int*);
 __global__ void boxes_extremes(const int4*, long long, const RoiParams*, Stats*, int4*, int4*,
@@ -71,7 +71,8 @@ __global__ void diam_refine(const int4*, long long, const RoiParams*, const uint
                             const int2*, const unsigned int*, const uint2*, long long,
                             const float*, Stats*, Stats*);
 __global__ void plane_boxes(const int2*, const unsigned int*, const unsigned int*,
-                            const RoiParams*, const Stats*, int4*, unsigned long long*, int4*);
+                            const RoiParams*, const Stats*, int4*, unsigned long long*, int4*,
+                            const unsigned int*);
 __global__ void plane_lb(const int2*, const unsigned int*, const unsigned long long*,
                          const RoiParams*, Stats*);
 __global__ void plane_filter(const unsigned int*, const unsigned int*, const unsigned int*,
@@ -313,6 +314,7 @@ struct Ctx {
   DevBuf<unsigned long long> plane_ext;
   DevBuf<int4> plane_boxes_buf;
   DevBuf<int4> plane_hboxes;  // boxes of the two 64-entry halves of every in-plane chunk
+  DevBuf<unsigned int> plane_cmap;  // plane of every in-plane chunk (scan_all)
   DevBuf<int2> plane_sorted;
   DevBuf<int2> canon_tmp;  // shard entry: canonical planar order (canon_planes)
   DevBuf<uint8_t> mask_stage, raw_stage;  // raw_stage: two chunk buffers (typed payloads)
@@ -367,7 +369,8 @@ struct Ctx {
                         work.p, warp_max.p, plane_umax.p,
                         plane_counts.p, plane_start.p, plane_tstart.p, plane_sorted.p,
                         plane_work.p, plane_cstart.p, pbin_counts.p, pbin_cursor.p,
-                        plane_ext.p, plane_boxes_buf.p, plane_hboxes.p, canon_tmp.p};
+                        plane_ext.p, plane_boxes_buf.p, plane_hboxes.p, canon_tmp.p,
+                        plane_cmap.p};
     for (const void* p : ps) h = (h ^ (unsigned long long)(uintptr_t)p) * 1099511628211ull;
     return h;
   }
@@ -598,6 +601,7 @@ int ensure_buffers(Ctx* c, int64_t nx, int64_t ny, int64_t nz, long long cap, lo
   CK(c->plane_work.ensure((size_t)pu));
   CK(c->plane_boxes_buf.ensure((size_t)t));
   CK(c->plane_hboxes.ensure((size_t)(2 * t)));
+  CK(c->plane_cmap.ensure((size_t)t));
   return SC_OK;
 }
 
@@ -812,7 +816,8 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   CK(launch_k(c, s, kScanBlocks + std::max(1, lgrid(c, 1) / 2), kScanThreads, scan_all, c->sort_counts.p, c->sort_cursor.p,
                                             c->plane_counts.p, c->plane_start.p,
                                             c->plane_tstart.p, c->plane_cstart.p, dcap,
-                                            c->d_stats, c->sboxes.p, c->pbin_counts.p, c->pbin_cursor.p, c->plane_ext.p));
+                                            c->d_stats, c->sboxes.p, c->pbin_counts.p, c->pbin_cursor.p, c->plane_ext.p,
+                                            c->plane_cmap.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(launch_k(c, s, lgrid(c, 4), 256, scatter_all, c->keys.p, dcap, c->d_stats, c->sort_cursor.p,
@@ -846,7 +851,7 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
     CK(record(c, c->kev[7], sp));
     CK(launch_k(c, sp, lgrid(c, 4), 256, plane_boxes, c->plane_sorted.p, c->plane_start.p,
                 c->plane_cstart.p, rp, c->d_stats, c->plane_boxes_buf.p, c->plane_ext.p,
-                c->plane_hboxes.p));
+                c->plane_hboxes.p, c->plane_cmap.p));
     CKL(1);
     CK(launch_k(c, sp, lgrid(c, 1), 256, plane_lb, c->plane_sorted.p, c->plane_start.p,
                 c->plane_ext.p, rp, c->d_stats));
@@ -873,7 +878,8 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   if (!fork) {
   CK(record(c, c->kev[7], s));
   CK(launch_k(c, s, lgrid(c, 4), 256, plane_boxes, c->plane_sorted.p, c->plane_start.p, c->plane_cstart.p,
-                                         rp, c->d_stats, c->plane_boxes_buf.p, c->plane_ext.p, c->plane_hboxes.p));
+                                         rp, c->d_stats, c->plane_boxes_buf.p, c->plane_ext.p, c->plane_hboxes.p,
+                                         c->plane_cmap.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(launch_k(c, s, lgrid(c, 1), 256, plane_lb, c->plane_sorted.p, c->plane_start.p, c->plane_ext.p, rp,
@@ -1077,7 +1083,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   h.n_words = (long long)h.W * ny * nz;
   h.n_chunks = nx * ny * nz / 16;
   h.sparse = (c->o.sparse && !c->prepacked) ? (c->o.pack_skip ? 3 : 1) : 0;
-  h.pflags = (c->o.pack_dyn ? 1 : 0) | (c->o.pack_sleep ? 2 : 0);
+  h.pflags = (c->o.pack_dyn ? 1 : 0) | (c->o.pack_sleep ? 2 : 0) | (trace_on() ? 4 : 0);
   h.f.cx2 = h.f.cy2 = h.f.cz2 = 0;  // set on the device from the bbox
   h.f.hx = (float)(0.5 * sp[0]);
   h.f.hy = (float)(0.5 * sp[1]);

@@ -49,7 +49,12 @@ __global__ void init_stats(Stats* st, uint32_t* __restrict__ segmap, long long n
     if (t < 3) st->bbox[t] = INT_MAX;
     if (t >= 3 && t < 6) st->bbox[t] = -1;
     if (t < kTrCount) st->tr[t][0] = ~0ull;
-    if (t == 0) st->t_start = global_ns();
+    if (t == 0) {
+      st->t_start = global_ns();
+      const int pf = src_rp ? reinterpret_cast<const volatile RoiParams*>(src_rp)->pflags
+                            : dst_rp->pflags;
+      st->trace_on = (unsigned int)(pf >> 2) & 1u;
+    }
   }
   for (long long i = (long long)blockIdx.x * blockDim.x + t; i < n_seg;
        i += (long long)gridDim.x * blockDim.x)
@@ -550,16 +555,17 @@ __global__ void __launch_bounds__(256) pack_bits_generic(const RoiParams* __rest
 // Out-of-grid voxels are background (this IS the reference's zero padding,
 // mesh.py:55-65).
 // Word wi of the bit volume; with a sparse bit volume, words of unmarked
-// segments read as 0 (the word and its map bit are loaded together).
+// segments read as 0.
 __device__ __forceinline__ uint32_t seg_word(const uint32_t* __restrict__ bits,
                                              const uint32_t* __restrict__ segmap, bool sparse,
                                              long long wi) {
-  uint32_t x = bits[wi];
+  // The map bit first: the data word is only loaded for a marked segment
+  // (most rows of a sparse bbox are background: one L1-resident map load).
   if (sparse) {
     const unsigned int lo = (unsigned int)wi;  // bit (wi >> 4) & 31 needs only the low word
-    if (!((__ldg(segmap + (wi >> 9)) >> ((lo >> 4) & 31u)) & 1u)) x = 0u;
+    if (!((__ldg(segmap + (wi >> 9)) >> ((lo >> 4) & 31u)) & 1u)) return 0u;
   }
-  return x;
+  return bits[wi];
 }
 
 // Words q and q - 1 of row (v, w).  All lanes call (converged).  Lanes hold

@@ -18,8 +18,8 @@
 //    pass-1 and re-check kernels of passes.cu)
 //
 // A unit (work entry) is one in-plane chunk pair: uint2 {plane, I << 16 | J}.
-// The owning plane of a tile pair / chunk is found by binary search over the
-// per-plane offsets, so no per-unit maps are materialised.
+// The owning plane of a chunk comes from scan_all's chunk -> plane map; that
+// of a tile pair (plane_filter) by binary search over the per-plane offsets.
 #include <climits>
 
 #include "sc_device.cuh"
@@ -72,25 +72,22 @@ __global__ void plane_boxes(const int2* __restrict__ sorted,
                             const unsigned int* __restrict__ cstart,
                             const RoiParams* __restrict__ rp,
                             const Stats* __restrict__ st, int4* __restrict__ pboxes,
-                            unsigned long long* __restrict__ pext, int4* __restrict__ hpboxes) {
+                            unsigned long long* __restrict__ pext, int4* __restrict__ hpboxes,
+                            const unsigned int* __restrict__ cmap) {
   pdl_enter();
   KTrace kt_(st, kTrPlaneBoxes);
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
   if (st->bbox[3] < 0) return;
   const PlaneSpace ps = plane_space(st);
-  const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
   const long long chunks = (long long)st->plane_chunks;
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   if ((long long)blockIdx.x * (blockDim.x >> 5) >= chunks) return;  // block-uniform
-  // The chunk offsets are searched in place (L1-resident after the first
-  // warps): staging them in shared memory cost every block a full pass over
-  // them and a barrier before its first chunk.
   const unsigned int* coff = cstart;
   for (long long c = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < chunks;
        c += warps) {
-    const int p = find_plane(coff, P, (unsigned long long)c);
+    const int p = (int)cmap[c];  // (scan_all's chunk -> plane map: no binary search)
     const PlaneAxes ax = plane_axes(plane_axis(p, ps), st, f);
     const unsigned int b0 = start[p], np = start[p + 1] - b0;
     const unsigned int e0 = (unsigned int)(c - coff[p]) * kPC;

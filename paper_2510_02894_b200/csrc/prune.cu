@@ -57,7 +57,8 @@ __global__ void __launch_bounds__(kScanThreads) scan_all(unsigned int* __restric
                                                          int4* __restrict__ sboxes,
                                                          unsigned int* __restrict__ pbin_counts,
                                                          unsigned int* __restrict__ pbin_cursor,
-                                                         unsigned long long* __restrict__ pext) {
+                                                         unsigned long long* __restrict__ pext,
+                                                         unsigned int* __restrict__ cmap) {
   pdl_enter();
   KTrace kt_(st, kTrScan);
   if (blockIdx.x == 0 && threadIdx.x == 0) st->t_mesh = global_ns();  // marching cubes done
@@ -77,14 +78,16 @@ __global__ void __launch_bounds__(kScanThreads) scan_all(unsigned int* __restric
     const int nwarps = (int)(gridDim.x - kScanBlocks) * (blockDim.x >> 5);
     for (int p = (int)(blockIdx.x - kScanBlocks) * (blockDim.x >> 5) + (threadIdx.x >> 5); p < P;
          p += nwarps) {
-      unsigned int* cnt = pbin_counts + (long long)p * kPlaneBins + lane * 8;
-      unsigned int v[8], sum = 0;
+      // 8 bins per lane as two 16-byte accesses (scalar 4-byte accesses
+      // strided by 32 B across the warp cost 8x the L2 sector requests)
+      uint4* cnt4 = reinterpret_cast<uint4*>(pbin_counts + (long long)p * kPlaneBins + lane * 8);
+      const uint4 c0 = cnt4[0], c1 = cnt4[1];
+      const unsigned int v[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      unsigned int sum = 0;
 #pragma unroll
-      for (int k = 0; k < 8; k++) {
-        v[k] = cnt[k];
-        sum += v[k];
-        cnt[k] = 0u;
-      }
+      for (int k = 0; k < 8; k++) sum += v[k];
+      cnt4[0] = make_uint4(0u, 0u, 0u, 0u);
+      cnt4[1] = make_uint4(0u, 0u, 0u, 0u);
       unsigned int incl = sum;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -92,12 +95,15 @@ __global__ void __launch_bounds__(kScanThreads) scan_all(unsigned int* __restric
         if (lane >= o) incl += t;
       }
       unsigned int run = incl - sum;
-      unsigned int* cur = pbin_cursor + (long long)p * kPlaneBins + lane * 8;
+      unsigned int o[8];
 #pragma unroll
       for (int k = 0; k < 8; k++) {
-        cur[k] = run;
+        o[k] = run;
         run += v[k];
       }
+      uint4* cur4 = reinterpret_cast<uint4*>(pbin_cursor + (long long)p * kPlaneBins + lane * 8);
+      cur4[0] = make_uint4(o[0], o[1], o[2], o[3]);
+      cur4[1] = make_uint4(o[4], o[5], o[6], o[7]);
       if (lane == 31) {
         plane_counts[p] = incl;
         // planar work entries index a plane's 128-entry chunks with 16 bits:
@@ -195,12 +201,14 @@ __global__ void __launch_bounds__(kScanThreads) scan_all(unsigned int* __restric
   unsigned int r3 = block_exscan(s3, &t3);
   for (int i = b; i < e; i++) {
     const unsigned int v = plane_counts[i];
+    const unsigned int nch = v >= 2 ? (v + kPlaneChunk - 1) / kPlaneChunk : 0u;
     start[i] = r1;
     tstart[i] = r2;
     cstart[i] = r3;
+    for (unsigned int k = 0; k < nch; k++) cmap[r3 + k] = (unsigned int)i;  // chunk -> plane
     r1 += v;
     r2 += plane_tiles(v, kPlaneTile);
-    r3 += v >= 2 ? (v + kPlaneChunk - 1) / kPlaneChunk : 0u;
+    r3 += nch;
   }
   if (threadIdx.x == 0) {
     start[P] = t1;

@@ -45,6 +45,8 @@ struct Stats {
   unsigned long long t_start, t_mesh, t_end;
   unsigned int plane_ovf;              // a plane holds more than kPlaneMaxEntries entries
   unsigned int pack_next;              // next 16 KB mask tile to claim (TMA pack)
+  unsigned int trace_on;               // kernels record their spans (RoiParams::pflags bit 2)
+  unsigned int pad2_;
   unsigned long long n_eval;           // 3-D pair slots pass 1 evaluated (after the vertex filter)
   unsigned long long n_peval;          // planar pair slots pass 1 evaluated
   // %globaltimer of each pipeline kernel's first block start / last block
@@ -64,22 +66,23 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
-// Block-granular kernel span on the ROI record: earliest block start (min)
-// and latest block end (max; thread 0 leaving the kernel), two reductions per
-// block.  init_stats seeds the starts with ~0.
+// Block-granular kernel span on the ROI record: earliest block start (min),
+// latest block end (max; thread 0 leaving the kernel) and summed block
+// residency -- three reductions per block, only while tracing (SC_TRACE=1 ->
+// RoiParams::pflags bit 2 -> Stats::trace_on).  init_stats seeds the starts.
 struct KTrace {
   unsigned long long* e;
   unsigned long long* b;
   unsigned long long t0;
   __device__ __forceinline__ KTrace(const Stats* st, int id)
       : e(const_cast<Stats*>(st)->tr[id]), b(const_cast<Stats*>(st)->busy + id), t0(0) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && st->trace_on) {
       t0 = global_ns();
       atomicMin(e, t0);
     }
   }
   __device__ __forceinline__ ~KTrace() {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && t0) {
       const unsigned long long t1 = global_ns();
       atomicMax(e + 1, t1);
       atomicAdd(b, t1 - t0);
@@ -145,7 +148,8 @@ struct RoiParams {
                        // volume and marks them in the segment map; readers treat
                        // unmarked segments as zero (0: every word is written); bit 1:
                        // the pack skips the conversion of all-zero segments
-  int pflags;          // TMA pack: bit 0 dynamic tile claims, bit 1 suspend-hinted waits
+  int pflags;          // TMA pack: bit 0 dynamic tile claims, bit 1 suspend-hinted waits;
+                       // bit 2: kernels record their timeline spans (SC_TRACE)
   int pad0_;
   Frame f;             // cx2..cz2 are filled on the device from the bbox
   long long wcap;      // capacity of the 3-D work list (overflow -> exact re-run)
