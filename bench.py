@@ -611,19 +611,20 @@ def run_ours(args):
     def pass1_roof(m, d, label):
         # One fused kernel runs the 3-D list (8 flop per pair: 3 FMA + |p|^2
         # fold + max) and the planar list (6 flop per pair: 2 FMA + fold + max).
-        # Pass 1 evaluates the listed 64 x 64 sub-pairs of every kept unit.
-        sub = _native.PAIRS_PER_UNIT // 4
-        p3 = d["work_subunits"] * sub
-        p2 = d["planar_work_subunits"] * sub
+        # Pass 1 evaluates the vertices of every kept unit that pass its reach
+        # filter: the pair slots it actually evaluates are counted on the
+        # device (diagnostics pass1_pairs / pass1_planar_pairs).
+        p3 = d["pass1_pairs"]
+        p2 = d["pass1_planar_pairs"]
         t = m["pass1_ms"] / 1e3
         ach = (8.0 * p3 + 6.0 * p2) / t / 1e12
         return {"kernel": "diam_pass1", "bound": "fp32", "achieved": ach, "peak": fp32_peak,
                 "unit": "TFLOP/s", "frac": ach / fp32_peak,
                 "traffic": traffic.get("diam_pass1"),
-                "work": f"{label}: 8 flop x {p3:.4g} 3-D pairs ({d['work_subunits']} 64x64 "
-                        f"sub-pairs of {d['work_units']} kept / {d['total_units']} 128x128 "
-                        f"chunk pairs) + 6 flop x {p2:.4g} in-plane pairs "
-                        f"({d['planar_work_subunits']} sub-pairs)",
+                "work": f"{label}: 8 flop x {p3:.4g} evaluated 3-D pair slots (vertex-filtered "
+                        f"{d['work_subunits']} listed 64x64 sub-pairs of {d['work_units']} kept / "
+                        f"{d['total_units']} 128x128 chunk pairs) + 6 flop x {p2:.4g} in-plane "
+                        f"pair slots ({d['planar_work_subunits']} listed sub-pairs)",
                 "pair_evals_per_s": (p3 + p2) / t,
                 "peak_note": "FP32 CUDA-core rate measured on this GPU by sc_probe_fp32_peak "
                              f"(best of FFMA/FFMA-imm/FFMA2; FFMA2 alone {fp32_ffma2:.1f} "

@@ -41,13 +41,14 @@ __global__ void init_stats(Stats* st, uint32_t* segmap, long long n_seg, const R
 template <int U, bool BOX>
 __global__ void pack_bits_v16(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 __global__ void bits_bbox(const RoiParams*, const uint4*, Stats*, const uint32_t*);
-template <bool BOX, int NT>
+template <bool BOX, int NT, int TILE>
 __global__ void pack_bits_tma(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
 template <bool BOX, int NT>
 __global__ void pack_bits_tmaw(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
 constexpr int kTmaTileBytes = 16384;  // mc.cu kTmaTile
 constexpr int kWarpTileBytes = 4096;  // mc.cu kWarpTile
 constexpr int kTmaMaxSmem = 8 * kTmaTileBytes;  // mc.cu kTmaMaxStages x kTmaTile
+constexpr int kTmaMaxSmemBig = 6 * 32768;      // 32 KB tiles: up to 6 stages
 __global__ void pack_bits_generic(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 __global__ void mc_cells(const RoiParams*, const uint32_t*, const CaseTables*, Stats*, int4*,
                          long long, unsigned int*, unsigned int*, const uint32_t*);
@@ -136,6 +137,8 @@ struct Opts {
   bool pack_warpring = false; // TMA pack as per-warp rings (pack_bits_tmaw, "pack_warpring")
   bool pack_prio = true;      // init_stats + pack at the greatest stream priority ("pack_prio")
   int pack_threads = 256;     // TMA pack CTA size (128 / 256, "pack_threads")
+  bool pack_nohint = false;  // TMA pack without the L2 evict-first hint ("pack_nohint")
+  int pack_tile = 16;         // TMA pack tile KB (8 / 16 / 32, "pack_tile")
   int pack_stages = 4;       // TMA pack ring depth, 16 KB tiles (2..8, "pack_stages")
   int pack_dyn = 0;          // TMA pack: dynamic tile claims ("pack_dyn"; C4 batch 33.5 -> 36.6 us/ROI: off)
   int pack_sleep = 0;        // TMA pack: suspend-hinted mbarrier waits ("pack_sleep")
@@ -423,10 +426,14 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     }
     CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, sprio));
     CK(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, sprio));
-    CK(cudaFuncSetAttribute(pack_bits_tma<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
-    CK(cudaFuncSetAttribute(pack_bits_tma<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
-    CK(cudaFuncSetAttribute(pack_bits_tma<false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
-    CK(cudaFuncSetAttribute(pack_bits_tma<true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tma<false, 256, 16384>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tma<true, 256, 16384>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tma<false, 128, 16384>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tma<true, 128, 16384>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tma<false, 256, 32768>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmemBig));
+    CK(cudaFuncSetAttribute(pack_bits_tma<true, 256, 32768>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmemBig));
+    CK(cudaFuncSetAttribute(pack_bits_tma<false, 256, 8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tma<true, 256, 8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
     CK(cudaFuncSetAttribute(pack_bits_tmaw<false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
     CK(cudaFuncSetAttribute(pack_bits_tmaw<true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
     CK(cudaFuncSetAttribute(pack_bits_tmaw<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
@@ -467,8 +474,10 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
       cudaFuncAttributes fa;
       const void* kernels[] = {(const void*)init_stats, (const void*)pack_bits_v16<4, false>,
                                (const void*)pack_bits_v16<4, true>,
-                               (const void*)pack_bits_tma<false, 256>, (const void*)pack_bits_tma<true, 256>,
-                               (const void*)pack_bits_tma<false, 128>, (const void*)pack_bits_tma<true, 128>,
+                               (const void*)pack_bits_tma<false, 256, 16384>, (const void*)pack_bits_tma<true, 256, 16384>,
+                               (const void*)pack_bits_tma<false, 128, 16384>, (const void*)pack_bits_tma<true, 128, 16384>,
+                               (const void*)pack_bits_tma<false, 256, 32768>, (const void*)pack_bits_tma<true, 256, 32768>,
+                               (const void*)pack_bits_tma<false, 256, 8192>, (const void*)pack_bits_tma<true, 256, 8192>,
                                (const void*)pack_bits_tmaw<false, 128>, (const void*)pack_bits_tmaw<true, 128>,
                                (const void*)pack_bits_tmaw<false, 256>, (const void*)pack_bits_tmaw<true, 256>,
                                (const void*)pack_bits_tmaw<false, 64>, (const void*)pack_bits_tmaw<true, 64>,
@@ -699,11 +708,18 @@ cudaError_t launch_tma_pack(Ctx* c, cudaStream_t s) {
                            c->d_stats, c->segmap.p, ws);
     }
   }
-  if (c->o.pack_threads <= 128)  // (the block-ring pack has 128- and 256-thread forms)
-    return launch_prio(c, s, grid, 128, smem, pack_bits_tma<BOX, 128>, rp, c->bits.p, c->d_stats,
-                       c->segmap.p, st);
-  return launch_prio(c, s, grid, 256, smem, pack_bits_tma<BOX, 256>, rp, c->bits.p, c->d_stats,
-                     c->segmap.p, st);
+  if (c->o.pack_tile == 32)  // 32 KB tiles (256 threads, <= 6 stages)
+    return launch_prio(c, s, grid, 256, (size_t)std::min(st, 6) * 32768,
+                       pack_bits_tma<BOX, 256, 32768>, rp, c->bits.p, c->d_stats, c->segmap.p,
+                       std::min(st, 6));
+  if (c->o.pack_tile == 8)  // 8 KB tiles (256 threads)
+    return launch_prio(c, s, grid, 256, (size_t)st * 8192, pack_bits_tma<BOX, 256, 8192>, rp,
+                       c->bits.p, c->d_stats, c->segmap.p, st);
+  if (c->o.pack_threads <= 128)  // (the 16 KB block-ring pack has 128- and 256-thread forms)
+    return launch_prio(c, s, grid, 128, smem, pack_bits_tma<BOX, 128, 16384>, rp, c->bits.p,
+                       c->d_stats, c->segmap.p, st);
+  return launch_prio(c, s, grid, 256, smem, pack_bits_tma<BOX, 256, 16384>, rp, c->bits.p,
+                     c->d_stats, c->segmap.p, st);
 }
 
 // Enqueue one whole ROI on stream s; no host synchronisation.  Everything
@@ -1068,7 +1084,8 @@ void trace_print() {
 int pack_key(const Opts& o) {
   return (o.pack_mode & 7) | ((o.pack_bps & 63) << 3) | ((o.pack_tma & 15) << 9) |
          ((o.pack_stages & 15) << 13) | (((o.pack_threads / 32) & 15) << 17) |
-         ((o.pack_prio ? 1 : 0) << 21) | ((o.pack_warpring ? 1 : 0) << 22);
+         ((o.pack_prio ? 1 : 0) << 21) | ((o.pack_warpring ? 1 : 0) << 22) |
+         ((o.pack_tile / 8) << 23);
 }
 
 int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
@@ -1083,7 +1100,8 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   h.n_words = (long long)h.W * ny * nz;
   h.n_chunks = nx * ny * nz / 16;
   h.sparse = (c->o.sparse && !c->prepacked) ? (c->o.pack_skip ? 3 : 1) : 0;
-  h.pflags = (c->o.pack_dyn ? 1 : 0) | (c->o.pack_sleep ? 2 : 0) | (trace_on() ? 4 : 0);
+  h.pflags = (c->o.pack_dyn ? 1 : 0) | (c->o.pack_sleep ? 2 : 0) | (trace_on() ? 4 : 0) |
+             (c->o.pack_nohint ? 8 : 0);
   h.f.cx2 = h.f.cy2 = h.f.cz2 = 0;  // set on the device from the bbox
   h.f.hx = (float)(0.5 * sp[0]);
   h.f.hy = (float)(0.5 * sp[1]);
@@ -1897,6 +1915,8 @@ int set_opt(Opts& o, const char* name, int value) {
   else if (std::strcmp(name, "pack_dyn") == 0) o.pack_dyn = value != 0;
   else if (std::strcmp(name, "pack_prio") == 0) o.pack_prio = value != 0;
   else if (std::strcmp(name, "pack_warpring") == 0) o.pack_warpring = value != 0;
+  else if (std::strcmp(name, "pack_nohint") == 0) o.pack_nohint = value != 0;
+  else if (std::strcmp(name, "pack_tile") == 0) o.pack_tile = (value == 8 || value == 32) ? value : 16;
   else if (std::strcmp(name, "pack_threads") == 0)
     o.pack_threads = (value == 32 || value == 64 || value == 128) ? value : 256;
   else if (std::strcmp(name, "pack_stages") == 0) o.pack_stages = std::max(2, std::min(8, value));

@@ -191,12 +191,19 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
                : "memory");
 }
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar,
-                                          uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1], %2, [%3], %4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
-      "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar)), "l"(policy)
-      : "memory");
+                                          uint64_t policy, bool hint = true) {
+  if (hint)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar)), "l"(policy)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1], %2, [%3];" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+        : "memory");
 }
 // Bounded wait: a lost transaction traps instead of hanging the GPU.  SLEEP:
 // each try suspends the warp in hardware until the phase completes (or up to
@@ -224,14 +231,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity, bool s
   }
 }
 
-template <bool BOX, int NT>
+template <bool BOX, int NT, int TILE>
 __global__ void __launch_bounds__(NT, 1) pack_bits_tma(const RoiParams* __restrict__ rp,
                                                       uint32_t* __restrict__ bits,
                                                       Stats* __restrict__ st,
                                                       uint32_t* __restrict__ segmap,
                                                       int stages) {
   KTrace kt_(st, kTrPack);
-  extern __shared__ __align__(128) unsigned char s_tiles[];  // stages x kTmaTile
+  extern __shared__ __align__(128) unsigned char s_tiles[];  // stages x TILE
   __shared__ __align__(8) uint64_t s_full[kTmaMaxStages];
   __shared__ int s_tile[kTmaMaxStages];  // tile held by each stage (>= tiles: none)
   const unsigned char* mask = rp->mask;
@@ -243,7 +250,7 @@ __global__ void __launch_bounds__(NT, 1) pack_bits_tma(const RoiParams* __restri
   // Tile claims: a contiguous share per CTA, or (rp->pflags bit 0) dynamic,
   // one atomic per 16 KB tile on the ROI's record (zeroed by init_stats), so
   // CTAs that start late in a busy batch simply take fewer tiles.
-  const int tiles = (int)((n_bytes + kTmaTile - 1) / kTmaTile);
+  const int tiles = (int)((n_bytes + TILE - 1) / TILE);
   const bool dyn = (rp->pflags & 1) != 0, sleep = (rp->pflags & 2) != 0;
   const int per = (tiles + (int)gridDim.x - 1) / (int)gridDim.x;
   int t_next = min(tiles, (int)blockIdx.x * per);  // static share [t_next, t_end)
@@ -254,10 +261,10 @@ __global__ void __launch_bounds__(NT, 1) pack_bits_tma(const RoiParams* __restri
     const int t = dyn ? (int)atomicAdd(&st->pack_next, 1u) : (t_next < t_end ? t_next++ : tiles);
     s_tile[s] = t;
     if (t < tiles) {
-      const long long off = (long long)t * kTmaTile;
-      const unsigned bytes = (unsigned)min((long long)kTmaTile, n_bytes - off);
+      const long long off = (long long)t * TILE;
+      const unsigned bytes = (unsigned)min((long long)TILE, n_bytes - off);
       mbar_expect_tx(&s_full[s], bytes);
-      bulk_load(s_tiles + s * kTmaTile, mask + off, bytes, &s_full[s], policy);
+      bulk_load(s_tiles + s * TILE, mask + off, bytes, &s_full[s], policy, !(rp->pflags & 8));
     }
   };
   if (threadIdx.x == 0) {
@@ -266,7 +273,7 @@ __global__ void __launch_bounds__(NT, 1) pack_bits_tma(const RoiParams* __restri
     for (int s = 0; s < stages; s++) issue(s);
   }
   __syncthreads();
-  constexpr int kK = kTmaTile / 16 / NT;  // 16-byte chunks per thread per tile (4 or 8)
+  constexpr int kK = TILE / 16 / NT;  // 16-byte chunks per thread per tile (4 or 8)
   const long long gend = n_bytes / 16;
   // Stage s is consumed at steps s, s + stages, ...; its next claim is
   // written after the step's barrier and read stages - 1 barriers later.
@@ -276,10 +283,10 @@ __global__ void __launch_bounds__(NT, 1) pack_bits_tma(const RoiParams* __restri
     const int t = s_tile[s];
     if (t >= tiles) break;  // block-uniform
     mbar_wait(&s_full[s], (unsigned)(k / stages) & 1u, sleep);
-    const long long g0 = (long long)t * (kTmaTile / 16);  // first chunk of the tile
-    const uint4* tile = reinterpret_cast<const uint4*>(s_tiles + s * kTmaTile);
+    const long long g0 = (long long)t * (TILE / 16);  // first chunk of the tile
+    const uint4* tile = reinterpret_cast<const uint4*>(s_tiles + s * TILE);
     // Only the last tile can be partial: bytes past the mask in its stage are stale.
-    const bool full = t + 1 < tiles || n_bytes % kTmaTile == 0;
+    const bool full = t + 1 < tiles || n_bytes % TILE == 0;
     uint4 v[kK];
     uint32_t any = 0u;
 #pragma unroll
@@ -430,10 +437,13 @@ template __global__ void pack_bits_tmaw<true, 32>(const RoiParams*, uint32_t*, S
 template __global__ void pack_bits_tmaw<false, 64>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
 template __global__ void pack_bits_tmaw<true, 64>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
 
-template __global__ void pack_bits_tma<false, 256>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
-template __global__ void pack_bits_tma<true, 256>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
-template __global__ void pack_bits_tma<false, 128>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
-template __global__ void pack_bits_tma<true, 128>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
+#define SC_TMA_INST(BOX, NT, TILE) \
+  template __global__ void pack_bits_tma<BOX, NT, TILE>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
+SC_TMA_INST(false, 256, 16384) SC_TMA_INST(true, 256, 16384)
+SC_TMA_INST(false, 128, 16384) SC_TMA_INST(true, 128, 16384)
+SC_TMA_INST(false, 256, 32768) SC_TMA_INST(true, 256, 32768)
+SC_TMA_INST(false, 256, 8192) SC_TMA_INST(true, 256, 8192)
+#undef SC_TMA_INST
 
 // Occupied bbox from the bit volume (L2-resident right after the pack): only
 // nonzero words locate themselves.  Four 16-byte loads in flight per thread.
