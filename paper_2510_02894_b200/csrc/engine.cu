@@ -54,9 +54,10 @@ __global__ void mc_cells(const RoiParams*, const uint32_t*, const CaseTables*, S
                          long long, unsigned int*, unsigned int*, const uint32_t*);
 __global__ void scan_all(unsigned int*, unsigned int*, unsigned int*, unsigned int*,
                          unsigned int*, unsigned int*, long long, Stats*, int4*, unsigned int*,
-                         unsigned int*, unsigned long long*, unsigned int*);
+                         unsigned int*, unsigned long long*);
 __global__ void scatter_all(const int4*, long long, const Stats*, unsigned int*, int4*,
-                            const unsigned int*, unsigned int*, int2*, unsigned int*);
+                            const unsigned int*, unsigned int*, int2*, unsigned int*,
+                            const unsigned int*, unsigned int*);
 __global__ void boxes_extremes(const int4*, long long, const RoiParams*, Stats*, int4*, int4*,
                                int4*);
 __global__ void unit_filter(const int4*, const int4*, long long, const RoiParams*, int, int, int,
@@ -317,7 +318,7 @@ struct Ctx {
   DevBuf<unsigned long long> plane_ext;
   DevBuf<int4> plane_boxes_buf;
   DevBuf<int4> plane_hboxes;  // boxes of the two 64-entry halves of every in-plane chunk
-  DevBuf<unsigned int> plane_cmap;  // plane of every in-plane chunk (scan_all)
+  DevBuf<unsigned int> plane_cmap;  // plane of every in-plane chunk (scatter_all)
   DevBuf<int2> plane_sorted;
   DevBuf<int2> canon_tmp;  // shard entry: canonical planar order (canon_planes)
   DevBuf<uint8_t> mask_stage, raw_stage;  // raw_stage: two chunk buffers (typed payloads)
@@ -832,13 +833,13 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   CK(launch_k(c, s, kScanBlocks + std::max(1, lgrid(c, 1) / 2), kScanThreads, scan_all, c->sort_counts.p, c->sort_cursor.p,
                                             c->plane_counts.p, c->plane_start.p,
                                             c->plane_tstart.p, c->plane_cstart.p, dcap,
-                                            c->d_stats, c->sboxes.p, c->pbin_counts.p, c->pbin_cursor.p, c->plane_ext.p,
-                                            c->plane_cmap.p));
+                                            c->d_stats, c->sboxes.p, c->pbin_counts.p, c->pbin_cursor.p, c->plane_ext.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(launch_k(c, s, lgrid(c, 4), 256, scatter_all, c->keys.p, dcap, c->d_stats, c->sort_cursor.p,
                                          c->keys_sorted.p, c->plane_start.p, c->pbin_cursor.p,
-                                         c->plane_sorted.p, c->sort_counts.p + kSortBins));
+                                         c->plane_sorted.p, c->sort_counts.p + kSortBins,
+                                         c->plane_cstart.p, c->plane_cmap.p));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   if (nshards > 1) {

@@ -18,7 +18,7 @@
 //    pass-1 and re-check kernels of passes.cu)
 //
 // A unit (work entry) is one in-plane chunk pair: uint2 {plane, I << 16 | J}.
-// The owning plane of a chunk comes from scan_all's chunk -> plane map; that
+// The owning plane of a chunk comes from scatter_all's chunk -> plane map; that
 // of a tile pair (plane_filter) by binary search over the per-plane offsets.
 #include <climits>
 
@@ -28,19 +28,6 @@ namespace sc {
 
 constexpr int kPT = kPlaneTile;      // in-plane tile edge (first filter level)
 constexpr int kPC = kPlaneChunk;     // in-plane chunk edge (pair unit = chunk x chunk)
-
-// Largest p in [0, P) with off[p] <= x (off non-decreasing, off[0] = 0): the
-// plane owning global tile pair / chunk x.
-__device__ __forceinline__ int find_plane(const unsigned int* __restrict__ off, int P,
-                                          unsigned long long x) {
-  int lo = 0, hi = P - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if ((unsigned long long)off[mid] <= x) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
 
 // Per-plane offsets staged in shared memory for the binary searches (volumes
 // up to ~2700 voxels per axis summed; larger ones search global memory).
@@ -87,7 +74,7 @@ __global__ void plane_boxes(const int2* __restrict__ sorted,
   const unsigned int* coff = cstart;
   for (long long c = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < chunks;
        c += warps) {
-    const int p = (int)cmap[c];  // (scan_all's chunk -> plane map: no binary search)
+    const int p = (int)cmap[c];  // (scatter_all's chunk -> plane map)
     const PlaneAxes ax = plane_axes(plane_axis(p, ps), st, f);
     const unsigned int b0 = start[p], np = start[p + 1] - b0;
     const unsigned int e0 = (unsigned int)(c - coff[p]) * kPC;

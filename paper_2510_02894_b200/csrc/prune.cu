@@ -57,8 +57,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_all(unsigned int* __restric
                                                          int4* __restrict__ sboxes,
                                                          unsigned int* __restrict__ pbin_counts,
                                                          unsigned int* __restrict__ pbin_cursor,
-                                                         unsigned long long* __restrict__ pext,
-                                                         unsigned int* __restrict__ cmap) {
+                                                         unsigned long long* __restrict__ pext) {
   pdl_enter();
   KTrace kt_(st, kTrScan);
   if (blockIdx.x == 0 && threadIdx.x == 0) st->t_mesh = global_ns();  // marching cubes done
@@ -205,7 +204,6 @@ __global__ void __launch_bounds__(kScanThreads) scan_all(unsigned int* __restric
     start[i] = r1;
     tstart[i] = r2;
     cstart[i] = r3;
-    for (unsigned int k = 0; k < nch; k++) cmap[r3 + k] = (unsigned int)i;  // chunk -> plane
     r1 += v;
     r2 += plane_tiles(v, kPlaneTile);
     r3 += nch;
@@ -228,7 +226,9 @@ __global__ void scatter_all(const int4* __restrict__ keys, long long cap,
                             const unsigned int* __restrict__ plane_start,
                             unsigned int* __restrict__ pbin_cursor,
                             int2* __restrict__ plane_sorted,
-                            unsigned int* __restrict__ sort_supers) {
+                            unsigned int* __restrict__ sort_supers,
+                            const unsigned int* __restrict__ cstart,
+                            unsigned int* __restrict__ cmap) {
   pdl_enter();
   KTrace kt_(st, kTrScatter);
   // scan_all has consumed the super-bin counts: leave them zeroed for the next ROI.
@@ -241,6 +241,14 @@ __global__ void scatter_all(const int4* __restrict__ keys, long long cap,
   const int s = brick_shift(bb);
   const PlaneSpace ps = plane_space(bb);
   const PlaneBricks pbk = plane_bricks(bb);
+  {  // in-plane chunk -> plane map for plane_boxes (one search per chunk here
+     // instead of one per chunk-warp there)
+    const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
+    const long long nch = (long long)st->plane_chunks;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < nch;
+         c += (long long)gridDim.x * blockDim.x)
+      cmap[c] = (unsigned int)find_plane(cstart, P, (unsigned long long)c);
+  }
   // Two vertices per thread per step (the second one grid-stride away), so
   // the key loads, cursor atomics and start loads of both are in flight
   // together: the loop is a chain of dependent memory round trips.

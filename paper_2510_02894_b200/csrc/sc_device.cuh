@@ -418,6 +418,19 @@ __device__ __forceinline__ PlaneAxes plane_axes(int axis, const Stats* st, const
   return x;
 }
 
+// Largest p in [0, P) with off[p] <= x (off non-decreasing, off[0] = 0): the
+// plane owning global tile pair / chunk x.
+__device__ __forceinline__ int find_plane(const unsigned int* __restrict__ off, int P,
+                                          unsigned long long x) {
+  int lo = 0, hi = P - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((unsigned long long)off[mid] <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
 __device__ __forceinline__ int plane_axis(int p, const PlaneSpace& ps) {
   return p < ps.cnt[0] ? 0 : (p < ps.cnt[0] + ps.cnt[1] ? 1 : 2);
 }
