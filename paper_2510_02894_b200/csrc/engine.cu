@@ -139,8 +139,8 @@ struct Opts {
   bool pack_prio = true;      // init_stats + pack at the greatest stream priority ("pack_prio")
   int pack_threads = 256;     // TMA pack CTA size (128 / 256, "pack_threads")
   bool pack_nohint = false;  // TMA pack without the L2 evict-first hint ("pack_nohint")
-  int pack_tile = 16;         // TMA pack tile KB (8 / 16 / 32, "pack_tile")
-  int pack_stages = 4;       // TMA pack ring depth, 16 KB tiles (2..8, "pack_stages")
+  int pack_tile = 32;         // TMA pack tile KB (8 / 16 / 32, "pack_tile"; 32: C4 -2 %, alone 51 -> 43 us)
+  int pack_stages = 2;       // TMA pack ring depth (2..8, "pack_stages"; a CTA's copies complete serially)
   int pack_dyn = 0;          // TMA pack: dynamic tile claims ("pack_dyn"; C4 batch 33.5 -> 36.6 us/ROI: off)
   int pack_sleep = 0;        // TMA pack: suspend-hinted mbarrier waits ("pack_sleep")
   int pack_chain = 4;        // batch: ROI i's graph starts after ROI i - pack_chain's pack
