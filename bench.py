@@ -547,9 +547,19 @@ def run_ours(args):
         ms2, _, outs2, _ = timed_batches(sc, _native, d2, [g2[0][1]], B, K, W, stream, world)
         check_repeats(outs2)
         u2 = ms2 * 1e3 / (B * K)
+        # the marching-cubes stage of one C2 call (pack + mc_cells, CUDA
+        # events at every stage) against HBM: mask bytes / stage time
+        med2, _, _ = kernel_times(sc, _native, d2[0], g2[0][1], stream,
+                                  max(3, min(K, 10)), dev)
+        mc_s = (med2["pack_ms"] + med2["mc_ms"]) / 1e3
         side = {"workload": WORKLOADS["c2"], "value": world * B * K / (ms2 / 1e3), "unit": UNIT,
                 "us_per_roi": u2, "roi_ceiling": ceiling(u2, d2[0].numel()),
-                "protocol": "same as value: K batch calls of B ROIs (the C2 mask repeated)"}
+                "protocol": "same as value: K batch calls of B ROIs (the C2 mask repeated)",
+                "mc_stage": {"pack_ms": med2["pack_ms"], "mc_ms": med2["mc_ms"],
+                             "achieved_gbs": d2[0].numel() / mc_s / 1e9,
+                             "frac_hbm": d2[0].numel() / mc_s / 1e9 / hbm,
+                             "note": "single call: 128-bit-load pack + mc_cells, mask bytes / "
+                                     "(pack + mc) time"}}
         del d2
 
     # ---- per-kernel times (single calls, CUDA events at every stage) ----

@@ -139,8 +139,8 @@ int sc_calculate_coefficients_shard(const uint8_t* d_mask, int64_t nx, int64_t n
                                     int nshards, double* d_sq4, sc_coeffs* out);
 
 /* Batch of ROIs on one device (C4): masks[i] are host pointers with dims
- * dims[3*i..3*i+2] and spacing spacings[3*i..]; out[i] per ROI.  Up to 16
- * pipeline slots (option "slots", default 16) round-robin, so the H2D copy and kernels of
+ * dims[3*i..3*i+2] and spacing spacings[3*i..]; out[i] per ROI.  Up to 64
+ * pipeline slots (option "slots", default 32) round-robin, so the H2D copy and kernels of
  * the next ROIs overlap the current one's.
  * The first failing ROI's code is returned; later ROIs are still processed. */
 int sc_calculate_coefficients_batch(const uint8_t* const* masks, const int64_t* dims,

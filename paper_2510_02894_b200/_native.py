@@ -13,7 +13,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libshapecore_b200.so")
+# (SC_LIB: an alternative build of the same library, for A/B measurements)
+LIB_PATH = os.environ.get("SC_LIB") or os.path.join(_HERE, "libshapecore_b200.so")
 
 SC_OK = 0
 SC_ERR_INPUT = 2

@@ -435,6 +435,10 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     CK(cudaFuncSetAttribute(pack_bits_tma<true, 256, 32768>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmemBig));
     CK(cudaFuncSetAttribute(pack_bits_tma<false, 256, 8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
     CK(cudaFuncSetAttribute(pack_bits_tma<true, 256, 8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
+    CK(cudaFuncSetAttribute(pack_bits_tma<false, 128, 32768>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmemBig));
+    CK(cudaFuncSetAttribute(pack_bits_tma<true, 128, 32768>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmemBig));
+    CK(cudaFuncSetAttribute(pack_bits_tma<false, 64, 32768>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmemBig));
+    CK(cudaFuncSetAttribute(pack_bits_tma<true, 64, 32768>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmemBig));
     CK(cudaFuncSetAttribute(pack_bits_tmaw<false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
     CK(cudaFuncSetAttribute(pack_bits_tmaw<true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
     CK(cudaFuncSetAttribute(pack_bits_tmaw<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
@@ -479,6 +483,8 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
                                (const void*)pack_bits_tma<false, 128, 16384>, (const void*)pack_bits_tma<true, 128, 16384>,
                                (const void*)pack_bits_tma<false, 256, 32768>, (const void*)pack_bits_tma<true, 256, 32768>,
                                (const void*)pack_bits_tma<false, 256, 8192>, (const void*)pack_bits_tma<true, 256, 8192>,
+                               (const void*)pack_bits_tma<false, 128, 32768>, (const void*)pack_bits_tma<true, 128, 32768>,
+                               (const void*)pack_bits_tma<false, 64, 32768>, (const void*)pack_bits_tma<true, 64, 32768>,
                                (const void*)pack_bits_tmaw<false, 128>, (const void*)pack_bits_tmaw<true, 128>,
                                (const void*)pack_bits_tmaw<false, 256>, (const void*)pack_bits_tmaw<true, 256>,
                                (const void*)pack_bits_tmaw<false, 64>, (const void*)pack_bits_tmaw<true, 64>,
@@ -709,10 +715,18 @@ cudaError_t launch_tma_pack(Ctx* c, cudaStream_t s) {
                            c->d_stats, c->segmap.p, ws);
     }
   }
-  if (c->o.pack_tile == 32)  // 32 KB tiles (256 threads, <= 6 stages)
-    return launch_prio(c, s, grid, 256, (size_t)std::min(st, 6) * 32768,
-                       pack_bits_tma<BOX, 256, 32768>, rp, c->bits.p, c->d_stats, c->segmap.p,
-                       std::min(st, 6));
+  if (c->o.pack_tile == 32) {  // 32 KB tiles (64 / 128 / 256 threads, <= 6 stages)
+    const int st32 = std::min(st, 6);
+    const size_t sm32 = (size_t)st32 * 32768;
+    if (c->o.pack_threads <= 64)
+      return launch_prio(c, s, grid, 64, sm32, pack_bits_tma<BOX, 64, 32768>, rp, c->bits.p,
+                         c->d_stats, c->segmap.p, st32);
+    if (c->o.pack_threads <= 128)
+      return launch_prio(c, s, grid, 128, sm32, pack_bits_tma<BOX, 128, 32768>, rp, c->bits.p,
+                         c->d_stats, c->segmap.p, st32);
+    return launch_prio(c, s, grid, 256, sm32, pack_bits_tma<BOX, 256, 32768>, rp, c->bits.p,
+                       c->d_stats, c->segmap.p, st32);
+  }
   if (c->o.pack_tile == 8)  // 8 KB tiles (256 threads)
     return launch_prio(c, s, grid, 256, (size_t)st * 8192, pack_bits_tma<BOX, 256, 8192>, rp,
                        c->bits.p, c->d_stats, c->segmap.p, st);

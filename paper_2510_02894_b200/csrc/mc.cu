@@ -276,7 +276,8 @@ __global__ void __launch_bounds__(NT, 1) pack_bits_tma(const RoiParams* __restri
   constexpr int kK = TILE / 16 / NT;  // 16-byte chunks per thread per tile (4 or 8)
   const long long gend = n_bytes / 16;
   // Stage s is consumed at steps s, s + stages, ...; its next claim is
-  // written after the step's barrier and read stages - 1 barriers later.
+  // written after the step's barrier and read stages - 1 barriers later
+  // (stages >= 2: with one stage that read would race the write).
   // Claims only grow, so the first stage without a tile ends the loop.
   for (int k = 0;; k++) {
     const int s = k % stages;
@@ -287,22 +288,27 @@ __global__ void __launch_bounds__(NT, 1) pack_bits_tma(const RoiParams* __restri
     const uint4* tile = reinterpret_cast<const uint4*>(s_tiles + s * TILE);
     // Only the last tile can be partial: bytes past the mask in its stage are stale.
     const bool full = t + 1 < tiles || n_bytes % TILE == 0;
-    uint4 v[kK];
-    uint32_t any = 0u;
+    // Groups of (up to) 4 chunks per thread: registers stay bounded for any
+    // tile / CTA size.
+    constexpr int kG = kK < 4 ? kK : 4;
+#pragma unroll 1
+    for (int q0 = 0; q0 < kK; q0 += kG) {
+      uint4 v[kG];
+      uint32_t any = 0u;
 #pragma unroll
-    for (int q = 0; q < kK; q++) {
-      const int ci = q * NT + threadIdx.x;
-      v[q] = tile[ci];
-      if (!full && g0 + ci >= gend) v[q] = make_uint4(0u, 0u, 0u, 0u);
-      any |= v[q].x | v[q].y | v[q].z | v[q].w;
-    }
-    // Sparse: one vote clears the warp's kK segments (2 KB) at once when they
-    // are all background -- most of a KiTS-like grid -- so the pack costs ~15
-    // issue slots per 2 KB there and leaves the SMs to other ROIs' kernels.
-    if (!skip || __any_sync(kFull, any != 0u)) {
+      for (int q = 0; q < kG; q++) {
+        const int ci = (q0 + q) * NT + threadIdx.x;
+        v[q] = tile[ci];
+        if (!full && g0 + ci >= gend) v[q] = make_uint4(0u, 0u, 0u, 0u);
+        any |= v[q].x | v[q].y | v[q].z | v[q].w;
+      }
+      // Sparse: one vote clears the warp's kG segments at once when they are
+      // all background -- most of a KiTS-like grid -- so the pack costs a few
+      // issue slots per 2 KB there and leaves the SMs to other ROIs' kernels.
+      if (skip && !__any_sync(kFull, any != 0u)) continue;
 #pragma unroll
-      for (int q = 0; q < kK; q++) {
-        const int ci = q * NT + threadIdx.x;
+      for (int q = 0; q < kG; q++) {
+        const int ci = (q0 + q) * NT + threadIdx.x;
         const long long g = g0 + ci;
         if (skip && !__any_sync(kFull, (v[q].x | v[q].y | v[q].z | v[q].w) != 0u)) continue;
         const uint32_t b16 = nib4(v[q].x) | (nib4(v[q].y) << 4) | (nib4(v[q].z) << 8) |
@@ -443,6 +449,8 @@ SC_TMA_INST(false, 256, 16384) SC_TMA_INST(true, 256, 16384)
 SC_TMA_INST(false, 128, 16384) SC_TMA_INST(true, 128, 16384)
 SC_TMA_INST(false, 256, 32768) SC_TMA_INST(true, 256, 32768)
 SC_TMA_INST(false, 256, 8192) SC_TMA_INST(true, 256, 8192)
+SC_TMA_INST(false, 128, 32768) SC_TMA_INST(true, 128, 32768)
+SC_TMA_INST(false, 64, 32768) SC_TMA_INST(true, 64, 32768)
 #undef SC_TMA_INST
 
 // Occupied bbox from the bit volume (L2-resident right after the pack): only

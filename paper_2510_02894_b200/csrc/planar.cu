@@ -178,7 +178,7 @@ __device__ __forceinline__ int4 box_union(int4 a, int4 b) {
 // union of its two chunk boxes) is tested against the family's lower bound
 // (margin 1e-9 covers fp64 rounding of both sides); only if it can reach it
 // are its 2 x 2 chunk pairs tested and listed in pwork.
-__global__ void plane_filter(const unsigned int* __restrict__ start,
+__global__ void __launch_bounds__(256, 4) plane_filter(const unsigned int* __restrict__ start,
                              const unsigned int* __restrict__ tstart,
                              const unsigned int* __restrict__ cstart,
                              const int4* __restrict__ pboxes, const RoiParams* __restrict__ rp,
