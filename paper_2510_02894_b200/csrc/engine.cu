@@ -1073,8 +1073,8 @@ void trace_print() {
   const auto& q = g_trace.seq;
   const int S = std::getenv("SC_TRACE_SLOTS") ? std::atoi(std::getenv("SC_TRACE_SLOTS")) : 32;
   const int ch = std::getenv("SC_TRACE_CHAIN") ? std::atoi(std::getenv("SC_TRACE_CHAIN")) : 4;
-  double g_slot = 0, g_chain = 0, pack_gap = 0;
-  long long n_slot = 0, n_chain = 0, n_pg = 0;
+  double g_slot = 0, g_chain = 0, pack_gap = 0, g_link = 0;
+  long long n_slot = 0, n_chain = 0, n_pg = 0, n_link = 0;
   for (size_t i = 0; i < q.size(); i++) {
     if (i >= (size_t)S && q[i - S][3] && q[i][0] > q[i - S][3]) {
       g_slot += 1e-3 * (double)(q[i][0] - q[i - S][3]);
@@ -1084,6 +1084,10 @@ void trace_print() {
       g_chain += 1e-3 * (double)(q[i][0] - q[i - ch][2]);
       n_chain++;
     }
+    if (ch > 0 && i >= (size_t)ch && q[i][1] > q[i - ch][2] && q[i - ch][2]) {
+      g_link += 1e-3 * (double)(q[i][1] - q[i - ch][2]);
+      n_link++;
+    }
     if (i >= 1 && q[i][1] > q[i - 1][1]) {
       pack_gap += 1e-3 * (double)(q[i][1] - q[i - 1][1]);
       n_pg++;
@@ -1092,6 +1096,9 @@ void trace_print() {
   if (n_slot) std::fprintf(stderr, "[sc trace]   init(i) - end(i-%d)      %8.1f us (slot reuse)\n", S, g_slot / n_slot);
   if (n_chain) std::fprintf(stderr, "[sc trace]   init(i) - pack end(i-%d)  %8.1f us (pack chain)\n", ch, g_chain / n_chain);
   if (n_pg) std::fprintf(stderr, "[sc trace]   pack start spacing       %8.1f us\n", pack_gap / n_pg);
+  if (n_link)
+    std::fprintf(stderr, "[sc trace]   pack start(i) - pack end(i-%d) %6.1f us (%lld of %zu ROIs)\n", ch,
+                 g_link / n_link, n_link, q.size());
   g_trace = TraceAcc{};
 }
 
