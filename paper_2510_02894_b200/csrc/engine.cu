@@ -43,10 +43,7 @@ __global__ void pack_bits_v16(const RoiParams*, uint32_t*, Stats*, uint32_t*);
 __global__ void bits_bbox(const RoiParams*, const uint4*, Stats*, const uint32_t*);
 template <bool BOX, int NT, int TILE>
 __global__ void pack_bits_tma(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
-template <bool BOX, int NT>
-__global__ void pack_bits_tmaw(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
 constexpr int kTmaTileBytes = 16384;  // mc.cu kTmaTile
-constexpr int kWarpTileBytes = 4096;  // mc.cu kWarpTile
 constexpr int kTmaMaxSmem = 8 * kTmaTileBytes;  // mc.cu kTmaMaxStages x kTmaTile
 constexpr int kTmaMaxSmemBig = 6 * 32768;      // 32 KB tiles: up to 6 stages
 __global__ void pack_bits_generic(const RoiParams*, uint32_t*, Stats*, uint32_t*);
@@ -135,14 +132,10 @@ struct Opts {
   bool pack_skip = true;     // sparse pack: no conversion of all-zero segments
   int pack_tma = 1;          // batch graphs: TMA bulk-copy pack, CTAs per SM (0 = 128-bit loads)
   int pack_tma_single = 0;   // the same for single calls (the 128-bit-load pack is faster alone)
-  bool pack_warpring = false; // TMA pack as per-warp rings (pack_bits_tmaw, "pack_warpring")
   bool pack_prio = true;      // init_stats + pack at the greatest stream priority ("pack_prio")
-  int pack_threads = 256;     // TMA pack CTA size (128 / 256, "pack_threads")
-  bool pack_nohint = false;  // TMA pack without the L2 evict-first hint ("pack_nohint")
+  int pack_threads = 256;     // TMA pack CTA size (64 / 128 / 256, "pack_threads")
   int pack_tile = 32;         // TMA pack tile KB (8 / 16 / 32, "pack_tile"; 32: C4 -2 %, alone 51 -> 43 us)
   int pack_stages = 2;       // TMA pack ring depth (2..8, "pack_stages"; a CTA's copies complete serially)
-  int pack_dyn = 0;          // TMA pack: dynamic tile claims ("pack_dyn"; C4 batch 33.5 -> 36.6 us/ROI: off)
-  int pack_sleep = 0;        // TMA pack: suspend-hinted mbarrier waits ("pack_sleep")
   int pack_chain = 4;        // batch: ROI i's graph starts after ROI i - pack_chain's pack
                              // (at most pack_chain HBM passes in flight; 0 = unchained).
                              // C2 / C4 / C5 K=200 us per ROI, chain 0 / 1 / 2 / 3 / 4 / 8:
@@ -439,13 +432,6 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
     CK(cudaFuncSetAttribute(pack_bits_tma<true, 128, 32768>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmemBig));
     CK(cudaFuncSetAttribute(pack_bits_tma<false, 64, 32768>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmemBig));
     CK(cudaFuncSetAttribute(pack_bits_tma<true, 64, 32768>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmemBig));
-    CK(cudaFuncSetAttribute(pack_bits_tmaw<false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
-    CK(cudaFuncSetAttribute(pack_bits_tmaw<true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
-    CK(cudaFuncSetAttribute(pack_bits_tmaw<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
-    CK(cudaFuncSetAttribute(pack_bits_tmaw<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
-    // (32 / 64-thread rings need at most 2 x 8 x 4 KB = 64 KB: under the default limit + opt-in)
-    CK(cudaFuncSetAttribute(pack_bits_tmaw<false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
-    CK(cudaFuncSetAttribute(pack_bits_tmaw<true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaMaxSmem));
     CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
     for (auto& e : c->cev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -485,10 +471,6 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
                                (const void*)pack_bits_tma<false, 256, 8192>, (const void*)pack_bits_tma<true, 256, 8192>,
                                (const void*)pack_bits_tma<false, 128, 32768>, (const void*)pack_bits_tma<true, 128, 32768>,
                                (const void*)pack_bits_tma<false, 64, 32768>, (const void*)pack_bits_tma<true, 64, 32768>,
-                               (const void*)pack_bits_tmaw<false, 128>, (const void*)pack_bits_tmaw<true, 128>,
-                               (const void*)pack_bits_tmaw<false, 256>, (const void*)pack_bits_tmaw<true, 256>,
-                               (const void*)pack_bits_tmaw<false, 64>, (const void*)pack_bits_tmaw<true, 64>,
-                               (const void*)pack_bits_tmaw<false, 32>, (const void*)pack_bits_tmaw<true, 32>,
                                (const void*)mesh_count, (const void*)mesh_emit,
                                (const void*)bits_bbox,
                                (const void*)pack_bits_generic, (const void*)mc_cells,
@@ -697,24 +679,6 @@ cudaError_t launch_tma_pack(Ctx* c, cudaStream_t s) {
   const size_t smem = (size_t)st * kTmaTileBytes;
   const dim3 grid((unsigned)(c->sms * c->o.pack_tma));
   const RoiParams* rp = c->d_rp;
-  if (c->o.pack_warpring) {  // per-warp rings of `pack_stages` 4 KB tiles
-    const int nt = c->o.pack_threads, ws = st;
-    const size_t wsmem = (size_t)(nt / 32) * ws * kWarpTileBytes;
-    switch (nt) {
-      case 32:
-        return launch_prio(c, s, grid, 32, wsmem, pack_bits_tmaw<BOX, 32>, rp, c->bits.p,
-                           c->d_stats, c->segmap.p, ws);
-      case 64:
-        return launch_prio(c, s, grid, 64, wsmem, pack_bits_tmaw<BOX, 64>, rp, c->bits.p,
-                           c->d_stats, c->segmap.p, ws);
-      case 128:
-        return launch_prio(c, s, grid, 128, wsmem, pack_bits_tmaw<BOX, 128>, rp, c->bits.p,
-                           c->d_stats, c->segmap.p, ws);
-      default:
-        return launch_prio(c, s, grid, 256, wsmem, pack_bits_tmaw<BOX, 256>, rp, c->bits.p,
-                           c->d_stats, c->segmap.p, ws);
-    }
-  }
   if (c->o.pack_tile == 32) {  // 32 KB tiles (64 / 128 / 256 threads, <= 6 stages)
     const int st32 = std::min(st, 6);
     const size_t sm32 = (size_t)st32 * 32768;
@@ -1106,8 +1070,7 @@ void trace_print() {
 int pack_key(const Opts& o) {
   return (o.pack_mode & 7) | ((o.pack_bps & 63) << 3) | ((o.pack_tma & 15) << 9) |
          ((o.pack_stages & 15) << 13) | (((o.pack_threads / 32) & 15) << 17) |
-         ((o.pack_prio ? 1 : 0) << 21) | ((o.pack_warpring ? 1 : 0) << 22) |
-         ((o.pack_tile / 8) << 23);
+         ((o.pack_prio ? 1 : 0) << 21) | ((o.pack_tile / 8) << 23);
 }
 
 int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
@@ -1122,8 +1085,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   h.n_words = (long long)h.W * ny * nz;
   h.n_chunks = nx * ny * nz / 16;
   h.sparse = (c->o.sparse && !c->prepacked) ? (c->o.pack_skip ? 3 : 1) : 0;
-  h.pflags = (c->o.pack_dyn ? 1 : 0) | (c->o.pack_sleep ? 2 : 0) | (trace_on() ? 4 : 0) |
-             (c->o.pack_nohint ? 8 : 0);
+  h.pflags = trace_on() ? 4 : 0;
   h.f.cx2 = h.f.cy2 = h.f.cz2 = 0;  // set on the device from the bbox
   h.f.hx = (float)(0.5 * sp[0]);
   h.f.hy = (float)(0.5 * sp[1]);
@@ -1934,15 +1896,11 @@ int set_opt(Opts& o, const char* name, int value) {
   else if (std::strcmp(name, "batch_stage_times") == 0) o.batch_times = value != 0;
   else if (std::strcmp(name, "host_threads") == 0) o.host_threads = std::max(1, value);
   else if (std::strcmp(name, "debug_empty") == 0) o.empty = std::max(0, value);
-  else if (std::strcmp(name, "pack_dyn") == 0) o.pack_dyn = value != 0;
   else if (std::strcmp(name, "pack_prio") == 0) o.pack_prio = value != 0;
-  else if (std::strcmp(name, "pack_warpring") == 0) o.pack_warpring = value != 0;
-  else if (std::strcmp(name, "pack_nohint") == 0) o.pack_nohint = value != 0;
   else if (std::strcmp(name, "pack_tile") == 0) o.pack_tile = (value == 8 || value == 32) ? value : 16;
   else if (std::strcmp(name, "pack_threads") == 0)
-    o.pack_threads = (value == 32 || value == 64 || value == 128) ? value : 256;
+    o.pack_threads = (value == 64 || value == 128) ? value : 256;
   else if (std::strcmp(name, "pack_stages") == 0) o.pack_stages = std::max(2, std::min(8, value));
-  else if (std::strcmp(name, "pack_sleep") == 0) o.pack_sleep = value != 0;
   else if (std::strcmp(name, "debug_stages") == 0) o.stages = value > 0 ? value : (1 << 30);
   else { set_err("unknown option %s", name); return SC_ERR_INPUT; }
   return SC_OK;

@@ -191,41 +191,24 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
                : "memory");
 }
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar,
-                                          uint64_t policy, bool hint = true) {
-  if (hint)
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-        "[%0], [%1], %2, [%3], %4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
-        "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar)), "l"(policy)
-        : "memory");
-  else
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
-        "[%0], [%1], %2, [%3];" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
-        "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
-        : "memory");
+                                          uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar)), "l"(policy)
+      : "memory");
 }
-// Bounded wait: a lost transaction traps instead of hanging the GPU.  SLEEP:
-// each try suspends the warp in hardware until the phase completes (or up to
-// a 20 us hint) instead of returning at once (option "pack_sleep").
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity, bool sleep) {
+// Bounded wait: a lost transaction traps instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
   for (long long spin = 0;; spin++) {
     unsigned ok;
-    if (sleep)
-      asm volatile(
-          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; "
-          "selp.u32 %0, 1, 0, p; }"
-          : "=r"(ok)
-          : "r"(a), "r"(parity), "r"(20000u)
-          : "memory");
-    else
-      asm volatile(
-          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
-          "selp.u32 %0, 1, 0, p; }"
-          : "=r"(ok)
-          : "r"(a), "r"(parity)
-          : "memory");
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
     if (ok) return;
     if (spin > (1LL << 26)) __trap();
   }
@@ -247,24 +230,22 @@ __global__ void __launch_bounds__(NT, 1) pack_bits_tma(const RoiParams* __restri
   const bool skip = (rp->sparse & 2) != 0;
   const unsigned int W = (unsigned int)rp->W, ny = (unsigned int)rp->ny;
   BoxAcc box;  // BOX: occupied bbox of the nonzero words (replaces bits_bbox)
-  // Tile claims: a contiguous share per CTA, or (rp->pflags bit 0) dynamic,
-  // one atomic per 16 KB tile on the ROI's record (zeroed by init_stats), so
-  // CTAs that start late in a busy batch simply take fewer tiles.
+  // A contiguous share of tiles per CTA (dynamic per-tile claims measured
+  // slower in the batch: C4 +3 us/ROI).
   const int tiles = (int)((n_bytes + TILE - 1) / TILE);
-  const bool dyn = (rp->pflags & 1) != 0, sleep = (rp->pflags & 2) != 0;
   const int per = (tiles + (int)gridDim.x - 1) / (int)gridDim.x;
   int t_next = min(tiles, (int)blockIdx.x * per);  // static share [t_next, t_end)
   const int t_end = min(tiles, t_next + per);
   uint64_t policy;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
   auto issue = [&](int s) {  // thread 0 only: claim the next tile into stage s
-    const int t = dyn ? (int)atomicAdd(&st->pack_next, 1u) : (t_next < t_end ? t_next++ : tiles);
+    const int t = t_next < t_end ? t_next++ : tiles;
     s_tile[s] = t;
     if (t < tiles) {
       const long long off = (long long)t * TILE;
       const unsigned bytes = (unsigned)min((long long)TILE, n_bytes - off);
       mbar_expect_tx(&s_full[s], bytes);
-      bulk_load(s_tiles + s * TILE, mask + off, bytes, &s_full[s], policy, !(rp->pflags & 8));
+      bulk_load(s_tiles + s * TILE, mask + off, bytes, &s_full[s], policy);
     }
   };
   if (threadIdx.x == 0) {
@@ -283,7 +264,7 @@ __global__ void __launch_bounds__(NT, 1) pack_bits_tma(const RoiParams* __restri
     const int s = k % stages;
     const int t = s_tile[s];
     if (t >= tiles) break;  // block-uniform
-    mbar_wait(&s_full[s], (unsigned)(k / stages) & 1u, sleep);
+    mbar_wait(&s_full[s], (unsigned)(k / stages) & 1u);
     const long long g0 = (long long)t * (TILE / 16);  // first chunk of the tile
     const uint4* tile = reinterpret_cast<const uint4*>(s_tiles + s * TILE);
     // Only the last tile can be partial: bytes past the mask in its stage are stale.
@@ -339,110 +320,6 @@ __global__ void __launch_bounds__(NT, 1) pack_bits_tma(const RoiParams* __restri
   }
   if (BOX) box.flush(st);
 }
-// Warp-ring variant (option "pack_warpring"): every warp streams its own
-// contiguous share of the mask through a private ring of `stages` 4 KB tiles
-// (its own mbarriers, lane 0 issues the bulk copies), so no block barrier
-// ever couples the warps: a warp converts a landed tile and immediately
-// refills that stage.  One 512-byte warp load = one bit-volume segment, as in
-// pack_bits_v16.
-constexpr int kWarpTile = 4096;
-constexpr int kWarpMaxStages = 8;
-
-template <bool BOX, int NT>
-__global__ void __launch_bounds__(NT, 1) pack_bits_tmaw(const RoiParams* __restrict__ rp,
-                                                       uint32_t* __restrict__ bits,
-                                                       Stats* __restrict__ st,
-                                                       uint32_t* __restrict__ segmap,
-                                                       int stages) {
-  KTrace kt_(st, kTrPack);
-  constexpr int NW = NT / 32;
-  extern __shared__ __align__(128) unsigned char s_ring[];  // NW x stages x kWarpTile
-  __shared__ __align__(8) uint64_t s_full[NW][kWarpMaxStages];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* ring = s_ring + (size_t)warp * stages * kWarpTile;
-  const unsigned char* mask = rp->mask;
-  const long long n_bytes = 16LL * rp->n_chunks;
-  const bool sparse = rp->sparse != 0;
-  const bool skip = (rp->sparse & 2) != 0;
-  const bool sleep = (rp->pflags & 2) != 0;
-  const unsigned int W = (unsigned int)rp->W, ny = (unsigned int)rp->ny;
-  BoxAcc box;
-  const long long tiles = (n_bytes + kWarpTile - 1) / kWarpTile;
-  const long long G = (long long)gridDim.x * NW, gw = (long long)blockIdx.x * NW + warp;
-  const long long per = (tiles + G - 1) / G;
-  const long long t0 = min(tiles, gw * per), t1 = min(tiles, t0 + per);
-  uint64_t policy;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-  auto issue = [&](long long t, int s) {  // lane 0 only
-    const long long off = t * kWarpTile;
-    const unsigned bytes = (unsigned)min((long long)kWarpTile, n_bytes - off);
-    mbar_expect_tx(&s_full[warp][s], bytes);
-    bulk_load(ring + s * kWarpTile, mask + off, bytes, &s_full[warp][s], policy);
-  };
-  if (lane == 0) {
-    for (int s = 0; s < stages; s++) mbar_init(&s_full[warp][s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < stages && t0 + s < t1; s++) issue(t0 + s, s);
-  }
-  __syncwarp();
-  constexpr int kQ = kWarpTile / 512;  // 512-byte warp loads (segments) per tile
-  const long long gend = n_bytes / 16;
-  for (long long t = t0; t < t1; t++) {
-    const int k = (int)(t - t0), s = k % stages;
-    mbar_wait(&s_full[warp][s], (unsigned)(k / stages) & 1u, sleep);
-    const uint4* tile = reinterpret_cast<const uint4*>(ring + s * kWarpTile);
-    const long long g0 = t * (kWarpTile / 16);
-    const bool full = t + 1 < tiles || n_bytes % kWarpTile == 0;
-    uint4 v[kQ];
-    uint32_t any = 0u;
-#pragma unroll
-    for (int q = 0; q < kQ; q++) {
-      v[q] = tile[q * 32 + lane];
-      if (!full && g0 + q * 32 + lane >= gend) v[q] = make_uint4(0u, 0u, 0u, 0u);
-      any |= v[q].x | v[q].y | v[q].z | v[q].w;
-    }
-    __syncwarp();  // every lane has its data: the stage can be refilled now
-    if (lane == 0 && t + stages < t1) issue(t + stages, s);
-    if (!skip || __any_sync(kFull, any != 0u)) {
-#pragma unroll
-      for (int q = 0; q < kQ; q++) {
-        const long long g = g0 + q * 32 + lane;
-        if (skip && !__any_sync(kFull, (v[q].x | v[q].y | v[q].z | v[q].w) != 0u)) continue;
-        const uint32_t b16 = nib4(v[q].x) | (nib4(v[q].y) << 4) | (nib4(v[q].z) << 8) |
-                             (nib4(v[q].w) << 12);
-        const uint32_t word = b16 | (__shfl_down_sync(kFull, b16, 1) << 16);
-        if (sparse) {
-          if (!__any_sync(kFull, word != 0u && !(lane & 1) && g < gend)) continue;
-          if (lane == 0) {
-            const long long seg = g >> 5;
-            atomicOr(segmap + (seg >> 5), 1u << (seg & 31));
-          }
-        }
-        if (!(lane & 1) && g < gend) {
-          bits[g >> 1] = word;
-          if (BOX && word) {
-            const unsigned int wi = (unsigned int)(g >> 1), row = wi / W, col = wi - row * W;
-            const unsigned int z = row / ny, y = row - z * ny;
-            box.x0 = min(box.x0, (int)(32 * col) + __ffs(word) - 1);
-            box.x1 = max(box.x1, (int)(32 * col) + 31 - __clz(word));
-            box.y0 = min(box.y0, (int)y); box.y1 = max(box.y1, (int)y);
-            box.z0 = min(box.z0, (int)z); box.z1 = max(box.z1, (int)z);
-          }
-        }
-      }
-    }
-  }
-  if (BOX) box.flush(st);
-}
-template __global__ void pack_bits_tmaw<false, 128>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
-template __global__ void pack_bits_tmaw<true, 128>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
-template __global__ void pack_bits_tmaw<false, 256>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
-template __global__ void pack_bits_tmaw<true, 256>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
-template __global__ void pack_bits_tmaw<false, 32>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
-template __global__ void pack_bits_tmaw<true, 32>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
-template __global__ void pack_bits_tmaw<false, 64>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
-template __global__ void pack_bits_tmaw<true, 64>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
-
 #define SC_TMA_INST(BOX, NT, TILE) \
   template __global__ void pack_bits_tma<BOX, NT, TILE>(const RoiParams*, uint32_t*, Stats*, uint32_t*, int);
 SC_TMA_INST(false, 256, 16384) SC_TMA_INST(true, 256, 16384)

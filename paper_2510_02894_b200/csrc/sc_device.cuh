@@ -44,7 +44,6 @@ struct Stats {
   // mesh_ms / diameters_ms without event nodes in the graph.
   unsigned long long t_start, t_mesh, t_end;
   unsigned int plane_ovf;              // a plane holds more than kPlaneMaxEntries entries
-  unsigned int pack_next;              // next 16 KB mask tile to claim (TMA pack)
   unsigned int trace_on;               // kernels record their spans (RoiParams::pflags bit 2)
   unsigned int pad2_;
   unsigned long long n_eval;           // 3-D pair slots pass 1 evaluated (after the vertex filter)
@@ -148,8 +147,7 @@ struct RoiParams {
                        // volume and marks them in the segment map; readers treat
                        // unmarked segments as zero (0: every word is written); bit 1:
                        // the pack skips the conversion of all-zero segments
-  int pflags;          // TMA pack: bit 0 dynamic tile claims, bit 1 suspend-hinted waits;
-                       // bit 2: kernels record their timeline spans (SC_TRACE)
+  int pflags;          // bit 2: kernels record their timeline spans (SC_TRACE)
   int pad0_;
   Frame f;             // cx2..cz2 are filled on the device from the bbox
   long long wcap;      // capacity of the 3-D work list (overflow -> exact re-run)

@@ -264,9 +264,9 @@ def test_batch_launch_options_identical(sc, golden, golden_arrays, cuda_device):
     for opt, val in (("grid_div", 1), ("grid_div", 2), ("pdl", 1), ("batch_stage_times", 1),
                      ("slots", 8), ("slots", 1), ("pack_mode", 3), ("sparse_bits", 0),
                      ("fork", 0), ("pack_tma", 0), ("pack_tma", 2), ("zero_copy", 0),
-                     ("fused_bbox", 0), ("pack_skip", 0), ("pack_dyn", 1), ("pack_sleep", 1),
-                     ("pack_threads", 128), ("pack_stages", 8), ("pack_warpring", 1),
-                     ("pack_prio", 0), ("slots", 64), ("pack_chain", 0)):
+                     ("fused_bbox", 0), ("pack_skip", 0), ("pack_threads", 128),
+                     ("pack_stages", 6), ("pack_tile", 16), ("pack_tile", 8), ("pack_prio", 0),
+                     ("slots", 64), ("pack_chain", 0)):
         with _native.thread_options(**{opt: val}):
             got = sc.calculate_coefficients_device_batch(ds * 2, sps * 2)
             assert [g.to_dict() for g in got] == want * 2, (opt, val)
