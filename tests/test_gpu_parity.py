@@ -765,3 +765,48 @@ def test_large_face_grid_against_oracle(sc, oracle_mod, cuda_device):
             assert rec[k] == want[k], k
         for k in ("MeshVolume", "SurfaceArea"):
             assert rel_err(rec[k], want[k]) <= REL_TOL, k
+
+
+def _tie_masks():
+    """Shapes whose maximum pair is massively tied or sits exactly at the
+    extremes-based lower bound, at odd spacings: solid boxes (four tied space
+    diagonals and many tied in-plane diagonals), a thin plate, two isolated
+    voxels far apart, an L, a hollow shell and a one-voxel-thick ring."""
+    out = []
+    a = np.zeros((24, 24, 24), np.uint8); a[2:22, 2:22, 2:22] = 1
+    out.append(("cube", a, (1.0, 1.0, 1.0)))
+    a = np.zeros((17, 11, 34), np.uint8); a[2:15, 2:9, 3:31] = 1
+    out.append(("box", a, (0.7, 1.3, 2.1)))
+    a = np.zeros((5, 60, 60), np.uint8); a[2, 3:57, 3:57] = 1
+    out.append(("plate", a, (0.8, 0.8, 5.0)))
+    a = np.zeros((40, 40, 64), np.uint8); a[3, 4, 5] = 1; a[36, 35, 58] = 1
+    out.append(("two_voxels", a, (0.9, 0.6, 1.1)))
+    a = np.zeros((30, 30, 30), np.uint8); a[2:28, 2:6, 2:28] = 1; a[2:6, 2:28, 2:28] = 1
+    out.append(("l_shape", a, (1.0, 0.5, 2.0)))
+    zz, yy, xx = np.mgrid[:48, :48, :48]
+    r = np.sqrt((zz - 23.5) ** 2 + (yy - 23.5) ** 2 + (xx - 23.5) ** 2)
+    out.append(("shell", ((r > 17) & (r < 20)).astype(np.uint8), (0.75, 0.75, 1.5)))
+    yy, xx = np.mgrid[:64, :64]
+    ring = (np.abs(np.hypot(yy - 31.5, xx - 31.5) - 25) < 0.75).astype(np.uint8)
+    a = np.zeros((3, 64, 64), np.uint8); a[1] = ring
+    out.append(("ring", a, (0.8, 0.8, 3.0)))
+    return out
+
+
+def test_reach_filter_on_tied_maxima(sc, oracle_mod, cuda_device):
+    """Pass 1's vertex reach filter (and the box pruning) on shapes whose
+    maximum is tied many times or equals the extremes' lower bound: pruned
+    (filter on) == unpruned (filter off) == oracle, bit for bit."""
+    from paper_2510_02894_b200 import _native
+
+    try:
+        for name, arr, sp in _tie_masks():
+            _native.set_option("prune", 1)
+            got = sc.calculate_coefficients(arr, sp, device=cuda_device)
+            _native.set_option("prune", 0)
+            full = sc.calculate_coefficients(arr, sp, device=cuda_device)
+            assert got.to_dict() == full.to_dict(), name
+            want = oracle_mod.extract_features(arr, sp, threads=0)
+            assert_matches(got, want, want["triangle_count"], want["active_cubes"], name)
+    finally:
+        _native.set_option("prune", 1)
