@@ -997,12 +997,14 @@ struct TraceAcc {
   std::vector<std::array<unsigned long long, 4>> seq;  // (t_start, pack start, pack end, t_end)
 };
 TraceAcc g_trace;
+std::mutex g_trace_mu;  // batches on several host threads share the accumulator
 bool trace_on() {
   static const bool on = std::getenv("SC_TRACE") != nullptr;
   return on;
 }
 void trace_add(const Stats& h) {
   if (!h.t_start) return;
+  std::lock_guard<std::mutex> lk(g_trace_mu);
   for (int k = 1; k < kTrCount; k++) {
     // (the refine's last block publishes the record before its own end
     // stamp: its end is t_end)
@@ -1024,6 +1026,7 @@ void trace_print() {
                                          "plane_boxes", "plane_lb", "plane_filter",
                                          "boxes_extremes", "unit_filter", "unit_expand",
                                          "pass1", "refine"};
+  std::lock_guard<std::mutex> lk(g_trace_mu);
   if (!g_trace.rois) return;
   std::fprintf(stderr, "[sc trace] %lld ROIs, mean ROI latency %.1f us (init -> refine end)\n",
                g_trace.rois, g_trace.lat / (double)g_trace.rois);
