@@ -56,7 +56,7 @@ __global__ void scatter_all(const int4*, long long, const Stats*, unsigned int*,
                             const unsigned int*, unsigned int*, int2*, unsigned int*,
                             const unsigned int*, unsigned int*);
 __global__ void boxes_extremes(const int4*, long long, const RoiParams*, Stats*, int4*, int4*,
-                               int4*);
+                               int4*, float4*);
 __global__ void unit_filter(const int4*, const int4*, long long, const RoiParams*, int, int, int,
                             Stats*, uint2*, const int4*, const int4*, uint2*, long long);
 __global__ void unit_expand(const int4*, long long, const RoiParams*, int, int, int, Stats*, uint2*,
@@ -65,7 +65,7 @@ template <bool PACKED>
 __global__ void diam_pass1(const int4*, long long, const RoiParams*, const uint2*, float*,
                            const int2*, const unsigned int*, const uint2*, long long, float*,
                            Stats*, const int4*, const int4*, int, const unsigned int*,
-                           const int4*, const int4*);
+                           const int4*, const int4*, const float4*);
 __global__ void diam_refine(const int4*, long long, const RoiParams*, const uint2*, const float*,
                             const int2*, const unsigned int*, const uint2*, long long,
                             const float*, Stats*, Stats*);
@@ -858,8 +858,11 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
     CK(record(c, c->kev[8], sp));
     CK(cudaEventRecord(c->join_ev, sp));
   }
+  // (the unsorted mc output is dead after the sort: its buffer takes the
+  // pass-1 frame coordinates of the sorted keys)
+  float4* fkeys = reinterpret_cast<float4*>(c->keys.p);
   CK(launch_k(c, s, lgrid(c, 2), 256, boxes_extremes, c->keys_sorted.p, dcap, rp, c->d_stats, c->boxes.p,
-                                            c->sboxes.p, c->hboxes.p));
+                                            c->sboxes.p, c->hboxes.p, fkeys));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(launch_k(c, s, lgrid(c, 4), 256, unit_filter, c->keys_sorted.p, c->boxes.p, dcap, rp, prune, shard,
@@ -896,13 +899,14 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
     CK(launch_k(c, s, pgrid, 256, diam_pass1<true>, c->keys_sorted.p, dcap, rp, c->work.p,
                 c->warp_max.p, c->plane_sorted.p, c->plane_start.p, c->plane_work.p, pucap,
                 c->plane_umax.p, c->d_stats, c->boxes.p, c->hboxes.p, prune, c->plane_cstart.p,
-                c->plane_boxes_buf.p, c->plane_hboxes.p));
+                c->plane_boxes_buf.p, c->plane_hboxes.p, (const float4*)fkeys));
   else
     CK(launch_k(c, s, pgrid, 256, diam_pass1<false>, c->keys_sorted.p, dcap, rp, c->work.p, c->warp_max.p,
                                             c->plane_sorted.p, c->plane_start.p, c->plane_work.p,
                                             pucap, c->plane_umax.p, c->d_stats, c->boxes.p,
                                             c->hboxes.p, prune, c->plane_cstart.p,
-                                            c->plane_boxes_buf.p, c->plane_hboxes.p));
+                                            c->plane_boxes_buf.p, c->plane_hboxes.p,
+                                            (const float4*)fkeys));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[5], s));
@@ -2231,7 +2235,9 @@ int sc_mesh_vertices(const uint8_t* mask, int64_t nx, int64_t ny, int64_t nz, in
   const long long m = V < cap ? V : cap;
   if (m > 0) {
     std::vector<int4> tmp((size_t)m);
-    CK(cudaMemcpyAsync(tmp.data(), c->keys.p, m * sizeof(int4), cudaMemcpyDeviceToHost, s));
+    // (the sorted copy: the unsorted buffer is reused by the diameter stage)
+    CK(cudaMemcpyAsync(tmp.data(), c->keys_sorted.p, m * sizeof(int4), cudaMemcpyDeviceToHost,
+                       s));
     CK(cudaStreamSynchronize(s));
     for (long long i = 0; i < m; i++) {
       keys[3 * i] = tmp[i].x;

@@ -138,7 +138,8 @@ __device__ __forceinline__ float eval_rows(const float4* __restrict__ si,
 // !FILTER (option pass1_packed=0): every listed 64 x 64 sub-pair, scalar FFMA
 // (the unfiltered baseline).
 template <bool FILTER>
-__device__ __forceinline__ void pass1_3d(const int4* __restrict__ keys, long long cap,
+__device__ __forceinline__ void pass1_3d(const int4* __restrict__ keys,
+                                         const float4* __restrict__ fkeys, long long cap,
                                          const RoiParams* __restrict__ rp,
                                          const uint2* __restrict__ work, float* __restrict__ umax,
                                          Stats* __restrict__ st, float4* __restrict__ sj,
@@ -189,9 +190,8 @@ __device__ __forceinline__ void pass1_3d(const int4* __restrict__ keys, long lon
 #pragma unroll
         for (int r = 2 * h; r < 2 * h + 2; r++) {
           const long long j = (long long)J * kChunk + r * 32 + lane;
-          const float3 q = frame_coord(keys[j < n ? j : n - 1], f);
-          warp_append(sj, nj, j < n && ih && reach_sq(q, bi) >= thr,
-                      make_float4(q.x, q.y, q.z, fmaf(q.x, q.x, fmaf(q.y, q.y, q.z * q.z))));
+          const float4 q = fkeys[j < n ? j : n - 1];
+          warp_append(sj, nj, j < n && ih && reach_sq(make_float3(q.x, q.y, q.z), bi) >= thr, q);
         }
       }
       if (nj > 0) {
@@ -202,9 +202,8 @@ __device__ __forceinline__ void pass1_3d(const int4* __restrict__ keys, long lon
 #pragma unroll
           for (int r = 2 * h; r < 2 * h + 2; r++) {
             const long long i = (long long)I * kChunk + r * 32 + lane;
-            const float3 p = frame_coord(keys[i < n ? i : n - 1], f);
-            warp_append(si, ni, i < n && jh && reach_sq(p, bj) >= thr,
-                        make_float4(p.x, p.y, p.z, fmaf(p.x, p.x, fmaf(p.y, p.y, p.z * p.z))));
+            const float4 p = fkeys[i < n ? i : n - 1];
+            warp_append(si, ni, i < n && jh && reach_sq(make_float3(p.x, p.y, p.z), bj) >= thr, p);
           }
         }
       }

@@ -14,7 +14,8 @@ __global__ void __launch_bounds__(kDiamThreads, 4) diam_pass1(
     const unsigned int* __restrict__ start, const uint2* __restrict__ pwork, long long pwcap,
     float* __restrict__ pumax, Stats* __restrict__ st, const int4* __restrict__ boxes,
     const int4* __restrict__ hboxes, int vfilter, const unsigned int* __restrict__ cstart,
-    const int4* __restrict__ pboxes, const int4* __restrict__ hpboxes) {
+    const int4* __restrict__ pboxes, const int4* __restrict__ hpboxes,
+    const float4* __restrict__ fkeys) {
   pdl_enter();
   KTrace kt_(st, kTrPass1);
   if (st->ovf || st->bbox[3] < 0) return;  // re-run pending (scan_all) / empty
@@ -24,7 +25,7 @@ __global__ void __launch_bounds__(kDiamThreads, 4) diam_pass1(
   float4* si = si_all[threadIdx.x >> 5];
   // A list longer than its buffer means a re-run with exact sizes is pending.
   if ((long long)st->n_work <= rp->wcap)
-    pass1_3d<PACKED>(keys, cap, rp, work, umax, st, sj, si, boxes, hboxes, vfilter);
+    pass1_3d<PACKED>(keys, fkeys, cap, rp, work, umax, st, sj, si, boxes, hboxes, vfilter);
   __syncwarp();
   if ((long long)st->n_pwork <= pwcap)
     pass1_planar(sorted, start, pwork, rp, pumax, st, sj, si, cstart, pboxes, hpboxes, vfilter);
@@ -32,12 +33,13 @@ __global__ void __launch_bounds__(kDiamThreads, 4) diam_pass1(
 template __global__ void diam_pass1<true>(const int4*, long long, const RoiParams*, const uint2*,
                                           float*, const int2*, const unsigned int*, const uint2*,
                                           long long, float*, Stats*, const int4*, const int4*, int,
-                                          const unsigned int*, const int4*, const int4*);
+                                          const unsigned int*, const int4*, const int4*,
+                                          const float4*);
 template __global__ void diam_pass1<false>(const int4*, long long, const RoiParams*, const uint2*,
                                            float*, const int2*, const unsigned int*,
                                            const uint2*, long long, float*, Stats*, const int4*,
                                            const int4*, int, const unsigned int*, const int4*,
-                                           const int4*);
+                                           const int4*, const float4*);
 
 __global__ void __launch_bounds__(kDiamThreads) diam_refine(
     const int4* __restrict__ keys, long long cap, const RoiParams* __restrict__ rp,

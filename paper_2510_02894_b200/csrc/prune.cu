@@ -318,11 +318,14 @@ __global__ void __launch_bounds__(256) boxes_extremes(const int4* __restrict__ k
                                                       Stats* __restrict__ st,
                                                       int4* __restrict__ boxes,
                                                       int4* __restrict__ sboxes,
-                                                      int4* __restrict__ hboxes) {
+                                                      int4* __restrict__ hboxes,
+                                                      float4* __restrict__ fkeys) {
   pdl_enter();
   KTrace kt_(st, kTrBoxes);
   if (st->ovf) return;  // re-run pending (scan_all)
   Frame f = rp->f;
+  Frame fc = f;  // pass 1's bbox-centred frame
+  frame_centre(st, fc);
   __shared__ unsigned long long s_ext[2 * kNDir];
   if (threadIdx.x < 2 * kNDir) s_ext[threadIdx.x] = 0ull;
   __syncthreads();
@@ -343,8 +346,13 @@ __global__ void __launch_bounds__(256) boxes_extremes(const int4* __restrict__ k
 #pragma unroll
     for (int t = 0; t < kPerLane; t++) {
       long long v = c * kChunkV + t * 32 + lane;
+      const bool real = v < n;
       if (v >= n) v = n - 1;  // pass 1 clamps the same way
       const int4 k = keys[v];
+      if (real) {  // pass-1 operand (x, y, z, |p|^2), formed once per vertex
+        const float3 q = frame_coord(k, fc);
+        fkeys[v] = make_float4(q.x, q.y, q.z, fmaf(q.x, q.x, fmaf(q.y, q.y, q.z * q.z)));
+      }
       const int hh = t / (kPerLane / 2);
       l[hh][0] = min(l[hh][0], k.x); l[hh][1] = min(l[hh][1], k.y); l[hh][2] = min(l[hh][2], k.z);
       u[hh][0] = max(u[hh][0], k.x); u[hh][1] = max(u[hh][1], k.y); u[hh][2] = max(u[hh][2], k.z);
