@@ -1,7 +1,7 @@
 """Marginal batch cost of each pipeline stage for the batch configuration
 (TMA pack with fused bbox): throughput with only the first N kernels enqueued
 per ROI (option debug_stages; results invalid, timing only).  Distinct masks
-cycle as in the bench.  usage: dbg_stages2.py workload [K]"""
+cycle as in the bench.  usage: stage_marginals_batch.py workload [K]"""
 import os
 import sys
 import time
