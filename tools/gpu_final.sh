@@ -7,6 +7,7 @@ mkdir -p gpurun_out
 OUT=gpurun_out
 timeout 900 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+timeout 900 python tools/stress_parity.py 600 21000 > $OUT/stress_parity.txt 2>&1; echo "rc=$?" >> $OUT/stress_parity.txt
 timeout 900 python bench.py --steps 20 --warmup 5 > $OUT/bench.json 2> $OUT/bench.err
 for w in c1 c3 c5; do
   timeout 600 python bench.py --steps 10 --warmup 3 --workload $w --no-cpu-baseline > $OUT/bench_$w.json 2> $OUT/bench_$w.err
