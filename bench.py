@@ -773,8 +773,12 @@ def run_split(args):
     rois, cfg = load_workload(args.workload, 0, 1)
     mask, sp = rois[0]
     d_mask = torch.from_numpy(mask).to(f"cuda:{dev}")
+    if args.sim_shards:
+        return run_split_sim(args, d_mask, sp, cfg)
+    split = (sharding.slab_sharded_coefficients if args.split_mode == "slab"
+             else sharding.sharded_coefficients)
     for _ in range(max(3, args.warmup)):
-        rec = sharding.sharded_coefficients(d_mask, sp)
+        rec = split(d_mask, sp)
     torch.cuda.synchronize()
     barrier(world)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -782,7 +786,7 @@ def run_split(args):
     clocks.__enter__()
     ev0.record()
     for _ in range(args.steps):
-        rec = sharding.sharded_coefficients(d_mask, sp)
+        rec = split(d_mask, sp)
     ev1.record()
     torch.cuda.synchronize()
     clocks.__exit__(None, None, None)
@@ -792,13 +796,19 @@ def run_split(args):
     for k in ("Maximum3DDiameter", "Maximum2DDiameterXY", "Maximum2DDiameterXZ",
               "Maximum2DDiameterYZ", "VertexCount"):
         assert rec[k] == full.to_dict()[k], k
-    cfg.update({"global_batch": 1, "parallelism": f"pair-grid split x{world} + NCCL all_reduce(MAX)"})
+    cfg.update({"global_batch": 1, "parallelism": (
+        f"slab split x{world}: marching cubes by cell layers + NCCL all_reduce(SUM) / all_gather "
+        f"of the partials and keys, pair grid by identity + NCCL all_reduce(MAX)"
+        if args.split_mode == "slab" else
+        f"pair-grid split x{world} + NCCL all_reduce(MAX)")})
     line = {"metric": METRIC, "value": args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u8 mask; exact int64 MC sums; fp32 screen + fp64 exact diameters",
             "data": "synthetic", "config": cfg, "clocks": clocks.summary(),
-            "path": "sharding.sharded_coefficients -> sc_calculate_coefficients_shard",
+            "path": ("sharding.slab_sharded_coefficients -> sc_shard_mesh / sc_shard_diameters"
+                     if args.split_mode == "slab" else
+                     "sharding.sharded_coefficients -> sc_calculate_coefficients_shard"),
             "result": {k: rec[k] for k in ("VertexCount", "Maximum3DDiameter")}}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -806,6 +816,72 @@ def run_split(args):
         import torch.distributed as dist
 
         dist.destroy_process_group()
+    return 0
+
+
+def run_split_sim(args, d_mask, sp, cfg):
+    """1-GPU view of the N-GPU split: every shard's phases run one after
+    another here, each timed alone (synchronous calls, host wall clock, median
+    of the repeats).  The critical path of an N-GPU run is then max over shards
+    of phase 1 + max over shards of phase 2 (+ the exchange, not simulated);
+    reported beside the single call and the one-call pair-grid shard entry."""
+    import statistics
+
+    import torch
+
+    import paper_2510_02894_b200 as sc
+    from paper_2510_02894_b200 import sharding
+
+    def wall(fn, reps):
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append((time.perf_counter() - t0) * 1e3)
+        return statistics.median(ts)
+
+    reps = max(3, args.steps)
+    for _ in range(max(3, args.warmup)):
+        full = sc.calculate_coefficients_device(d_mask, sp)
+    single_ms = wall(lambda: sc.calculate_coefficients_device(d_mask, sp), reps)
+    out = {}
+    for n in args.sim_shards:
+        times = {}
+
+        def timer(phase, shard, fn):
+            res = [None]
+
+            def call():
+                res[0] = fn()
+            times.setdefault((phase, shard), []).append(wall(call, 1))
+            return res[0]
+
+        for _ in range(max(2, args.warmup)):
+            rec = sharding.simulate_slab_shards(d_mask, sp, n)
+        times.clear()
+        for _ in range(reps):
+            rec = sharding.simulate_slab_shards(d_mask, sp, n, timer=timer)
+        fd = full.to_dict()
+        assert all(rec[k] == fd[k] for k in fd if k in rec and not k.endswith("_ms")), n
+        p1 = [statistics.median(times[(1, s)]) for s in range(n)]
+        p2 = [statistics.median(times[(2, s)]) for s in range(n)]
+        sq = torch.zeros(4, dtype=torch.float64, device=d_mask.device)
+        pair_ms = [wall(lambda s=s: sc.calculate_coefficients_shard(d_mask, sp, s, n, sq), reps)
+                   for s in range(n)]
+        crit = max(p1) + max(p2)
+        out[str(n)] = {"phase1_ms": p1, "phase2_ms": p2, "critical_ms": crit,
+                       "critical_frac_of_single": crit / single_ms,
+                       "pair_grid_entry_ms": pair_ms,
+                       "pair_grid_frac_of_single": max(pair_ms) / single_ms}
+    line = {"metric": "per-shard critical path of the C3 split, simulated on 1 GPU",
+            "unit": "ms", "workload": cfg.get("workload"), "single_call_ms": single_ms,
+            "shards": out, "exact": True,
+            "note": "phase 1 = sc_shard_mesh (pack + marching cubes on the shard's cell "
+                    "layers), phase 2 = sc_shard_diameters (load summed partials + gathered "
+                    "keys, shard of the pair grid); exchange (all_reduce SUM + all_gather of "
+                    "keys over NVLink) not included; host wall clock of synchronous calls, "
+                    f"median of {reps}"}
+    print(json.dumps(line), flush=True)
     return 0
 
 
@@ -826,6 +902,12 @@ def main():
     ap.add_argument("--split", action="store_true",
                     help="strong scaling of ONE ROI: every rank evaluates its share of the pair "
                          "grid (sc_calculate_coefficients_shard) + one NCCL all_reduce(MAX)")
+    ap.add_argument("--split-mode", default="slab", choices=["slab", "pairs"],
+                    help="slab: marching cubes split by cell layers too (sc_shard_mesh / "
+                         "sc_shard_diameters); pairs: one-call pair-grid shard entry")
+    ap.add_argument("--sim-shards", type=int, nargs="*", default=None,
+                    help="with --split on 1 GPU: time every shard of an N-way slab split "
+                         "(one after another) and report the per-shard critical path")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # contract: W >= 3 warm-up steps

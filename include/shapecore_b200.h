@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define SC_ABI_VERSION 3
+#define SC_ABI_VERSION 4
 
 enum {
   SC_OK = 0,
@@ -137,6 +137,36 @@ int sc_calculate_coefficients_device(const uint8_t* d_mask, int64_t nx, int64_t 
 int sc_calculate_coefficients_shard(const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
                                     const double spacing[3], void* stream, int shard,
                                     int nshards, double* d_sq4, sc_coeffs* out);
+
+/* Two-phase (slab-split) shard entry for one very large mesh split across G
+ * devices, so that marching cubes -- not only the pair grid -- is divided
+ * (replaces the per-rank full mesh of the entry above).  Same pair
+ * ownership and results as sc_calculate_coefficients_shard.
+ *
+ * Phase 1, sc_shard_mesh: bit-pack the whole device mask (every shard gets the
+ * global occupied bbox, written to bbox[6] = xmin, ymin, zmin, xmax, ymax,
+ * zmax) and run marching cubes over shard `shard`'s contiguous share of the
+ * cell layers.  Writes the shard's exact integer partials to d_sums (device,
+ * n_sums int64 from sc_shard_exchange_sizes) and its vertex keys (int32 x 4
+ * per vertex, device) to d_keys (room for key_cap vertices); *n_keys = the
+ * shard's vertex count.  The caller then all-reduces d_sums (SUM, int64) and
+ * all-gathers the keys of every shard (any order).
+ *
+ * Phase 2, sc_shard_diameters: the summed d_sums, the gathered keys
+ * (n_keys = their total, must equal the summed vertex count) and phase 1's
+ * bbox; evaluates shard `shard` of the pair grid and writes the 4 partial
+ * squared maxima (fp64) to d_sq4 for an all-reduce(MAX), as above.  `out`
+ * holds the complete counts, area and volume.  Both calls are synchronous and
+ * ordered after prior work on `stream` (NULL = the legacy default stream). */
+int sc_shard_exchange_sizes(int64_t nx, int64_t ny, int64_t nz, int64_t* n_sums,
+                            int64_t* key_cap);
+int sc_shard_mesh(const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
+                  const double spacing[3], void* stream, int shard, int nshards,
+                  int64_t* d_sums, int32_t* d_keys, int64_t key_cap, int64_t* n_keys,
+                  int32_t bbox[6]);
+int sc_shard_diameters(const int64_t* d_sums, const int32_t* d_keys, int64_t n_keys, int64_t nx,
+                       int64_t ny, int64_t nz, const int32_t bbox[6], const double spacing[3],
+                       void* stream, int shard, int nshards, double* d_sq4, sc_coeffs* out);
 
 /* Batch of ROIs on one device (C4): masks[i] are host pointers with dims
  * dims[3*i..3*i+2] and spacing spacings[3*i..]; out[i] per ROI.  Up to 64

@@ -30,6 +30,9 @@ from .features import (
     diameters_parallel,
     extract_features,
     mesh_vertices,
+    shard_diameters,
+    shard_exchange_sizes,
+    shard_mesh,
 )
 from .mesh import (
     TriangleMesh,
@@ -55,7 +58,8 @@ __all__ = [
     "NonPositiveSpacing", "ShapeCoreError", "ShapeExceedsBounds", "ShapeFeatures",
     "StageTimings", "attach_spacing", "calculate_coefficients", "calculate_coefficients_batch",
     "calculate_coefficients_device", "calculate_coefficients_device_batch",
-    "calculate_coefficients_shard", "diameters",
+    "calculate_coefficients_shard", "diameters", "shard_diameters", "shard_exchange_sizes",
+    "shard_mesh",
     "diameters_parallel", "extract_features", "mesh_vertices", "synth_mask",
     "coefficients_from_npy", "coefficients_from_npy_batch", "coefficients_from_payloads",
     "load_npy", "parse_npy_header", "BenchRecord", "bench_run",

@@ -27,6 +27,9 @@ EXPORTED = (
     "sc_calculate_coefficients",
     "sc_calculate_coefficients_device",
     "sc_calculate_coefficients_shard",
+    "sc_shard_exchange_sizes",
+    "sc_shard_mesh",
+    "sc_shard_diameters",
     "sc_calculate_coefficients_raw",
     "sc_calculate_coefficients_raw_batch",
     "sc_calculate_coefficients_batch",
@@ -112,6 +115,15 @@ def load():
         L.sc_calculate_coefficients_shard.argtypes = [ctypes.c_void_p, i64, i64, i64, dp,
                                                       ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                                       ctypes.c_void_p, cp]
+        i64p = ctypes.POINTER(i64)
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        L.sc_shard_exchange_sizes.argtypes = [i64, i64, i64, i64p, i64p]
+        L.sc_shard_mesh.argtypes = [ctypes.c_void_p, i64, i64, i64, dp, ctypes.c_void_p,
+                                    ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                    i64, i64p, i32p]
+        L.sc_shard_diameters.argtypes = [ctypes.c_void_p, ctypes.c_void_p, i64, i64, i64, i64,
+                                         i32p, dp, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_void_p, cp]
         L.sc_calculate_coefficients_batch.argtypes = [ctypes.POINTER(u8p),
                                                       ctypes.POINTER(i64), dp, i64,
                                                       ctypes.c_int, cp]

@@ -51,7 +51,7 @@ __global__ void mc_cells(const RoiParams*, const uint32_t*, const CaseTables*, S
                          long long, unsigned int*, unsigned int*, const uint32_t*);
 __global__ void scan_all(unsigned int*, unsigned int*, unsigned int*, unsigned int*,
                          unsigned int*, unsigned int*, long long, Stats*, int4*, unsigned int*,
-                         unsigned int*, unsigned long long*);
+                         unsigned int*, unsigned long long*, int);
 __global__ void scatter_all(const int4*, long long, const Stats*, unsigned int*, int4*,
                             const unsigned int*, unsigned int*, int2*, unsigned int*,
                             const unsigned int*, unsigned int*);
@@ -100,9 +100,9 @@ template <int MODE>
 __global__ void fp32_probe(float*, int, float, float);
 
 __global__ void empty_kernel();
-__global__ void canon_keys(const int4*, int4*, long long, const Stats*);
-__global__ void canon_copy_keys(const int4*, int4*, long long, const Stats*);
-__global__ void canon_planes(const int2*, int2*, const unsigned int*, const Stats*, int);
+__global__ void canon_keys(int4*, int4*, const unsigned int*, const Stats*);
+__global__ void canon_planes(int2*, int2*, const unsigned int*, const unsigned int*,
+                             const Stats*);
 }  // namespace sc
 
 using namespace sc;
@@ -324,6 +324,8 @@ struct Ctx {
   long long last_scan_bytes = 0;  // bytes the host scan read for it
   long long last_slab_bytes = 0;  // bytes of its occupied slab
   bool prepacked = false;         // this ROI's bit volume came packed from the host
+  int mc_slab = 0;                // RoiParams::mc_slab of the next ROI (two-phase shard entry)
+  bool mesh_only = false;         // enqueue_roi stops after mc_cells (two-phase shard entry)
   uint32_t* h_bits = nullptr;     // pinned staging of a host-packed bit volume
   size_t h_bits_cap = 0;          // words
   bool last_split = false;        // it used the split read (split_slices)
@@ -481,7 +483,7 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
                                (const void*)diam_refine, (const void*)cloud_diameters,
                                (const void*)plane_boxes,
                                (const void*)plane_lb, (const void*)plane_filter,
-                               (const void*)canon_keys, (const void*)canon_copy_keys,
+                               (const void*)canon_keys,
                                (const void*)canon_planes};
       for (const void* k : kernels) CK(cudaFuncGetAttributes(&fa, k));
     }
@@ -706,6 +708,8 @@ cudaError_t launch_tma_pack(Ctx* c, cudaStream_t s) {
 // slot's RoiParams record, so the enqueued sequence -- and a graph captured
 // from it -- depends only on the pack path, the shard and the slot buffers.
 // kev[] brackets the stages for sc_last_kernel_times.
+int enqueue_diam(Ctx* c, cudaStream_t s, int shard, int nshards, int& nk);
+
 int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   const RoiParams* rp = c->d_rp;
   // Diagnostic option "debug_stages": enqueue only the first N kernels (results
@@ -799,7 +803,19 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(record(c, c->kev[2], s));
+  if (c->mesh_only) return SC_OK;
+  return enqueue_diam(c, s, shard, nshards, nk);
+}
 
+// Diameter half of the pipeline (sort -> bounds -> filters -> pass 1 ->
+// re-check): reads only the slot's Stats (bbox, n_vert), the vertex keys and
+// the brick / plane-bin histograms mc_cells left -- or, in the two-phase shard
+// entry, the gathered keys and summed histograms loaded into the same buffers.
+int enqueue_diam(Ctx* c, cudaStream_t s, int shard, int nshards, int& nk) {
+  const RoiParams* rp = c->d_rp;
+  const int lim = c->o.stages;
+  const long long dcap = c->dcap_sz;
+  const bool zc = zero_copy_records(c);
   // Persistent grids: exactly the resident blocks, so the static round-robin
   // split of work units is also the load balance.
   const int pgrid = lgrid(c, std::max(1, c->o.packed ? c->occ_pass1 : c->occ_pass1s));
@@ -811,7 +827,8 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   CK(launch_k(c, s, kScanBlocks + std::max(1, lgrid(c, 1) / 2), kScanThreads, scan_all, c->sort_counts.p, c->sort_cursor.p,
                                             c->plane_counts.p, c->plane_start.p,
                                             c->plane_tstart.p, c->plane_cstart.p, dcap,
-                                            c->d_stats, c->sboxes.p, c->pbin_counts.p, c->pbin_cursor.p, c->plane_ext.p));
+                                            c->d_stats, c->sboxes.p, c->pbin_counts.p, c->pbin_cursor.p, c->plane_ext.p,
+                                            nshards > 1 ? 1 : 0));
   CKL(1);
   if (++nk >= lim) return SC_OK;
   CK(launch_k(c, s, lgrid(c, 4), 256, scatter_all, c->keys.p, dcap, c->d_stats, c->sort_cursor.p,
@@ -823,15 +840,12 @@ int enqueue_roi(Ctx* c, bool fast, cudaStream_t s, int shard, int nshards) {
   if (nshards > 1) {
     // Shards own chunk pairs by identity: give every shard (every GPU) the
     // same vertex order -- each bin's segment sorted by vertex key.
-    CK(launch_k(c, s, lgrid(c, 4), 256, canon_keys, c->keys_sorted.p, c->keys.p, dcap,
-                c->d_stats));
-    CK(launch_k(c, s, lgrid(c, 4), 256, canon_copy_keys, c->keys.p, c->keys_sorted.p, dcap,
-                c->d_stats));
-    CK(launch_k(c, s, lgrid(c, 4), 256, canon_planes, c->plane_sorted.p, c->canon_tmp.p,
-                c->plane_start.p, c->d_stats, 0));
-    CK(launch_k(c, s, lgrid(c, 4), 256, canon_planes, c->canon_tmp.p, c->plane_sorted.p,
-                c->plane_start.p, c->d_stats, 1));
-    CKL(4);
+    // (one warp per bin, 4-warp blocks: 16 blocks per SM)
+    CK(launch_k(c, s, c->sms * 16, 128, canon_keys, c->keys_sorted.p, c->keys.p,
+                c->sort_cursor.p, c->d_stats));
+    CK(launch_k(c, s, c->sms * 16, 128, canon_planes, c->plane_sorted.p, c->canon_tmp.p,
+                c->plane_start.p, c->pbin_cursor.p, c->d_stats));
+    CKL(2);
   }
   // After the sort the 3-D chain (boxes -> filter) and the planar chain
   // (plane boxes -> bound -> filter) are independent: the planar one runs on
@@ -1080,10 +1094,11 @@ int pack_key(const Opts& o) {
          ((o.pack_prio ? 1 : 0) << 21) | ((o.pack_tile / 8) << 23);
 }
 
-int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
-               const double sp[3], cudaStream_t s, int shard, int nshards, double* d_sq4,
-               const int org[3]) {
-  RoiParams& h = *c->h_rp;  // the slot's previous ROI has been collected: safe to rewrite
+// The slot's RoiParams record for the next ROI (host copy; the slot's
+// previous ROI has been collected, so it is safe to rewrite).
+void fill_rp(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
+             const double sp[3], const int org[3]) {
+  RoiParams& h = *c->h_rp;
   h.mask = d_mask;
   h.nx = nx;
   h.ny = ny;
@@ -1093,6 +1108,7 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   h.n_chunks = nx * ny * nz / 16;
   h.sparse = (c->o.sparse && !c->prepacked) ? (c->o.pack_skip ? 3 : 1) : 0;
   h.pflags = trace_on() ? 4 : 0;
+  h.mc_slab = c->mc_slab;
   h.f.cx2 = h.f.cy2 = h.f.cz2 = 0;  // set on the device from the bbox
   h.f.hx = (float)(0.5 * sp[0]);
   h.f.hy = (float)(0.5 * sp[1]);
@@ -1104,6 +1120,12 @@ int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz
   h.f.oy2 = 2 * org[1];
   h.f.oz2 = 2 * org[2];
   h.wcap = (long long)std::min(c->work.cap, c->warp_max.cap);
+}
+
+int launch_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
+               const double sp[3], cudaStream_t s, int shard, int nshards, double* d_sq4,
+               const int org[3]) {
+  fill_rp(c, d_mask, nx, ny, nz, sp, org);
   const bool hp = host_prof_on();
   double t0 = hp ? wall_ms() : 0.0;
   if (!zero_copy_records(c))  // else init_stats reads the record from mapped host memory
@@ -1202,6 +1224,54 @@ int start_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
 
 // Wait for the ROI started on slot c, re-run it once with exact buffer sizes
 // if the device reported an overflow, and fill `out`.
+// Checks and output record of a ROI whose Stats are on the host.
+int collect_roi(Ctx* c, const double sp[3], sc_coeffs* out) {
+  if (c->h_stats->bbox[3] < 0) {
+    set_err("mask has no occupied voxels");
+    return SC_ERR_EMPTY_ROI;
+  }
+  if (c->h_stats->plane_ovf) {
+    set_err("a plane of the mesh holds more than %lld vertices (planar chunk index width)",
+            kPlaneMaxEntries);
+    return SC_ERR_INPUT;
+  }
+  if ((long long)c->h_stats->n_super > (long long)c->slist.cap) {
+    // cannot happen with slist sized from kSingleLevelMax; never report a
+    // maximum from a truncated super-pair list
+    set_err("super-pair list overflow (%llu > %zu)", c->h_stats->n_super, c->slist.cap);
+    return SC_ERR_NOMEM;
+  }
+  fill_out(*c->h_stats, sp, out);
+  if (trace_on()) trace_add(*c->h_stats);
+  c->times_pending = c->events_on && c->ev_full;  // per-stage times: from kev[] on demand
+  if (!c->times_pending)
+    for (int i = 0; i < 6; i++) c->last_ms[i] = 0.0;
+  c->last_ms[6] = 0.0;
+  {
+    const Stats& h = *c->h_stats;
+    const long long Vv = (long long)h.n_vert, C = (Vv + kChunk - 1) / kChunk;
+    c->last_diag[0] = (long long)h.n_work;
+    c->last_diag[1] = C * (C + 1) / 2;
+    c->last_diag[2] = (long long)h.n_cand;
+    c->last_diag[3] = (long long)h.plane_units;
+    c->last_diag[4] = (long long)h.n_pcand;
+    c->last_diag[5] = (long long)h.n_pwork;
+    c->last_diag[6] = (long long)h.n_sub;
+    c->last_diag[7] = (long long)h.n_psub;
+    c->last_diag[8] = (long long)h.n_eval;
+    c->last_diag[9] = (long long)h.n_peval;
+  }
+  if (c->events_on) {
+    out->mesh_ms = ev_ms(c->kev[0], c->kev[2]);
+    out->diameters_ms = ev_ms(c->kev[2], c->kev[6]);
+  } else {  // device %globaltimer stamps (no event nodes in the graph)
+    const Stats& h = *c->h_stats;
+    out->mesh_ms = h.t_mesh > h.t_start ? (double)(h.t_mesh - h.t_start) * 1e-6 : 0.0;
+    out->diameters_ms = h.t_end > h.t_mesh ? (double)(h.t_end - h.t_mesh) * 1e-6 : 0.0;
+  }
+  return SC_OK;
+}
+
 int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
   const bool hp = host_prof_on();
   const double t0 = hp ? wall_ms() : 0.0;
@@ -1233,50 +1303,7 @@ int finish_roi(Ctx* c, Pending* p, sc_coeffs* out) {
       return SC_ERR_NOMEM;
     }
   }
-  if (c->h_stats->bbox[3] < 0) {
-    set_err("mask has no occupied voxels");
-    return SC_ERR_EMPTY_ROI;
-  }
-  if (c->h_stats->plane_ovf) {
-    set_err("a plane of the mesh holds more than %lld vertices (planar chunk index width)",
-            kPlaneMaxEntries);
-    return SC_ERR_INPUT;
-  }
-  if ((long long)c->h_stats->n_super > (long long)c->slist.cap) {
-    // cannot happen with slist sized from kSingleLevelMax; never report a
-    // maximum from a truncated super-pair list
-    set_err("super-pair list overflow (%llu > %zu)", c->h_stats->n_super, c->slist.cap);
-    return SC_ERR_NOMEM;
-  }
-  fill_out(*c->h_stats, p->sp, out);
-  if (trace_on()) trace_add(*c->h_stats);
-  c->times_pending = c->events_on && c->ev_full;  // per-stage times: from kev[] on demand
-  if (!c->times_pending)
-    for (int i = 0; i < 6; i++) c->last_ms[i] = 0.0;
-  c->last_ms[6] = 0.0;
-  {
-    const Stats& h = *c->h_stats;
-    const long long Vv = (long long)h.n_vert, C = (Vv + kChunk - 1) / kChunk;
-    c->last_diag[0] = (long long)h.n_work;
-    c->last_diag[1] = C * (C + 1) / 2;
-    c->last_diag[2] = (long long)h.n_cand;
-    c->last_diag[3] = (long long)h.plane_units;
-    c->last_diag[4] = (long long)h.n_pcand;
-    c->last_diag[5] = (long long)h.n_pwork;
-    c->last_diag[6] = (long long)h.n_sub;
-    c->last_diag[7] = (long long)h.n_psub;
-    c->last_diag[8] = (long long)h.n_eval;
-    c->last_diag[9] = (long long)h.n_peval;
-  }
-  if (c->events_on) {
-    out->mesh_ms = ev_ms(c->kev[0], c->kev[2]);
-    out->diameters_ms = ev_ms(c->kev[2], c->kev[6]);
-  } else {  // device %globaltimer stamps (no event nodes in the graph)
-    const Stats& h = *c->h_stats;
-    out->mesh_ms = h.t_mesh > h.t_start ? (double)(h.t_mesh - h.t_start) * 1e-6 : 0.0;
-    out->diameters_ms = h.t_end > h.t_mesh ? (double)(h.t_end - h.t_mesh) * 1e-6 : 0.0;
-  }
-  return SC_OK;
+  return collect_roi(c, p->sp, out);
 }
 
 // Full pipeline on a device-resident mask (context lock held by the caller).
@@ -1788,6 +1815,7 @@ int run_mesh(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
     h.f.sx = sp[0]; h.f.sy = sp[1]; h.f.sz = sp[2];
     h.f.ox2 = h.f.oy2 = h.f.oz2 = 0;
     h.sparse = 0;  // the export kernels read every bit-volume word
+    h.mc_slab = 0;
     h.wcap = 0;
     CK(cudaMemcpyAsync(c->d_rp, c->h_rp, sizeof(RoiParams), cudaMemcpyHostToDevice, s));
     init_stats<<<1, 256, 0, s>>>(c->d_stats, c->segmap.p, 0LL, nullptr, c->d_rp);
@@ -1956,6 +1984,244 @@ int sc_calculate_coefficients_shard(const uint8_t* d_mask, int64_t nx, int64_t n
   std::memset(out, 0, sizeof *out);
   c->prepacked = false;
   rc = run_roi(c, d_mask, nx, ny, nz, spacing, s, shard, nshards, d_sq4, out);
+  out->total_ms = wall_ms() - t0;
+  return rc;
+}
+
+// ---- two-phase (slab-split) shard entry -------------------------------------
+//
+// Phase 1 (sc_shard_mesh): the pack (replicated: every rank gets the global
+// bbox, which fixes the brick / plane binning and the pass-1 frame) and
+// marching cubes over the shard's share of the cell layers only.  Its exact
+// integer partials -- case histogram, volume sum, vertex count, brick and
+// plane-bin histograms -- go to an int64 "sums" vector the caller all-reduces
+// (SUM), its vertex keys to a buffer the caller all-gathers.  Phase 2
+// (sc_shard_diameters) loads the summed histograms and the gathered keys into
+// the slot and runs the diameter half with identity ownership, so the
+// marching-cubes work as well as the pair grid falls with the shard count.
+// Layout of the sums vector (int64): [0, 256) case histogram, 256 vol_k,
+// 257 n_vert, then kSortBins + kSortSupers brick counts, then P x kPlaneBins
+// plane-bin counts (P = 2 (nx + ny + nz) + 9, the host bound of the plane space).
+constexpr long long kSumHist = 0, kSumVol = 256, kSumVert = 257, kSumSort = 258;
+constexpr long long kSumPlane = kSumSort + kSortBins + kSortSupers;
+
+long long shard_sums_len(int64_t nx, int64_t ny, int64_t nz) {
+  return kSumPlane + (2 * (nx + ny + nz) + 9) * kPlaneBinsHost;
+}
+
+// Phase 1 export: partials -> sums (and zero the slot's histograms, which no
+// scan_all consumed this time).
+__global__ void shard_export(const Stats* __restrict__ st, unsigned int* __restrict__ sort_counts,
+                             unsigned int* __restrict__ pbin_counts, long long n_pbin,
+                             long long* __restrict__ sums) {
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long step = (long long)gridDim.x * blockDim.x;
+  for (long long i = t0; i < kNumCases; i += step) {
+    unsigned long long h = 0;
+    for (int c = 0; c < kHistCopies; c++) h += st->hist[c][i];
+    sums[kSumHist + i] = (long long)h;
+  }
+  if (t0 == 0) {
+    sums[kSumVol] = st->vol_k;
+    sums[kSumVert] = (long long)st->n_vert;
+  }
+  for (long long i = t0; i < kSortBins + kSortSupers; i += step) {
+    sums[kSumSort + i] = sort_counts[i];
+    sort_counts[i] = 0u;
+  }
+  for (long long i = t0; i < n_pbin; i += step) {
+    sums[kSumPlane + i] = pbin_counts[i];
+    pbin_counts[i] = 0u;
+  }
+}
+
+// Phase 2 import (after init_stats): the global bbox and the summed partials.
+__global__ void shard_import(Stats* __restrict__ st, int4 bb_lo, int4 bb_hi,
+                             unsigned int* __restrict__ sort_counts,
+                             unsigned int* __restrict__ pbin_counts, long long n_pbin,
+                             const long long* __restrict__ sums) {
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long step = (long long)gridDim.x * blockDim.x;
+  if (t0 == 0) {
+    st->bbox[0] = bb_lo.x; st->bbox[1] = bb_lo.y; st->bbox[2] = bb_lo.z;
+    st->bbox[3] = bb_hi.x; st->bbox[4] = bb_hi.y; st->bbox[5] = bb_hi.z;
+    st->vol_k = sums[kSumVol];
+    st->n_vert = (unsigned long long)sums[kSumVert];
+  }
+  for (long long i = t0; i < kNumCases; i += step) st->hist[0][i] = (unsigned long long)sums[kSumHist + i];
+  for (long long i = t0; i < kSortBins + kSortSupers; i += step)
+    sort_counts[i] = (unsigned int)sums[kSumSort + i];
+  for (long long i = t0; i < n_pbin; i += step)
+    pbin_counts[i] = (unsigned int)sums[kSumPlane + i];
+}
+
+int sc_shard_exchange_sizes(int64_t nx, int64_t ny, int64_t nz, int64_t* n_sums,
+                            int64_t* key_cap) {
+  if (nx <= 0 || ny <= 0 || nz <= 0 || !n_sums || !key_cap) {
+    set_err("bad dims or NULL output");
+    return SC_ERR_INPUT;
+  }
+  *n_sums = shard_sums_len(nx, ny, nz);
+  *key_cap = vertex_capacity(nx, ny, nz, 0);
+  return SC_OK;
+}
+
+namespace {
+// Per-call state of a two-phase entry: no graphs (one-off pipeline cuts), the
+// Stats record copied back explicitly, single-call launch shapes.
+void two_phase_opts(Ctx* c) {
+  c->o = snapshot_opts();
+  c->o.graphs = 0;
+  c->o.zc = 0;
+  c->grid_div = c->o.grid_div_single;
+  c->o.pack_tma = c->o.pack_tma_single;
+  c->o.fbox = c->o.fbox_single;
+  c->events_on = c->o.stage_times > 0;
+  c->ev_full = c->o.stage_times > 1;
+  c->prepacked = false;
+}
+cudaStream_t order_after_legacy(Ctx* c, void* stream) {
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  if (!stream) {
+    cudaEventRecord(c->ev[4], cudaStreamLegacy);
+    cudaStreamWaitEvent(s, c->ev[4], 0);
+  }
+  return s;
+}
+}  // namespace
+
+int sc_shard_mesh(const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
+                  const double spacing[3], void* stream, int shard, int nshards,
+                  int64_t* d_sums, int32_t* d_keys, int64_t key_cap, int64_t* n_keys,
+                  int32_t bbox[6]) {
+  int rc = check_input(d_mask, nx, ny, nz, spacing);
+  if (rc) return rc;
+  if (!d_sums || !d_keys || !n_keys || !bbox || nshards < 1 || nshards > 0x7fff || shard < 0 ||
+      shard >= nshards) {
+    set_err("NULL buffer or bad shard %d of %d", shard, nshards);
+    return SC_ERR_INPUT;
+  }
+  Ctx* c;
+  if ((rc = current_ctx(&c))) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  two_phase_opts(c);
+  cudaStream_t s = order_after_legacy(c, stream);
+  struct Reset {  // the slot's next ROI is a plain one again, whatever happens
+    Ctx* c;
+    ~Reset() { c->mc_slab = 0; c->mesh_only = false; }
+  } reset{c};
+  Pending p{};
+  for (int attempt = 0; attempt < 2; attempt++) {
+    c->mc_slab = (nshards << 16) | shard;
+    c->mesh_only = true;
+    if ((rc = start_roi(c, d_mask, nx, ny, nz, spacing, s, 0, 1, nullptr, 0, &p))) return rc;
+    CK(cudaStreamSynchronize(s));
+    const long long V = (long long)c->h_stats->n_vert;
+    if (V <= (long long)c->keys.cap) break;
+    if (attempt) { set_err("vertex buffer overflow"); return SC_ERR_NOMEM; }
+    p.cap = V;  // exact re-run (raises the slot's floors)
+    p.dcap = std::max(p.dcap, V);
+  }
+  const Stats& h = *c->h_stats;
+  for (int i = 0; i < 6; i++) bbox[i] = h.bbox[i];
+  const long long V = (long long)h.n_vert;
+  *n_keys = V;
+  if (h.bbox[3] < 0) {
+    set_err("mask has no occupied voxels");
+    return SC_ERR_EMPTY_ROI;
+  }
+  if (V > key_cap) {
+    set_err("key buffer holds %lld keys, the shard has %lld", (long long)key_cap, V);
+    return SC_ERR_NOMEM;
+  }
+  const long long n_pbin = (2 * (nx + ny + nz) + 9) * kPlaneBinsHost;
+  shard_export<<<c->sms * 2, 256, 0, s>>>(c->d_stats, c->sort_counts.p, c->pbin_counts.p, n_pbin,
+                                          reinterpret_cast<long long*>(d_sums));
+  CKL(1);
+  if (V) CK(cudaMemcpyAsync(d_keys, c->keys.p, (size_t)V * sizeof(int4), cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  return SC_OK;
+}
+
+int sc_shard_diameters(const int64_t* d_sums, const int32_t* d_keys, int64_t n_keys, int64_t nx,
+                       int64_t ny, int64_t nz, const int32_t bbox[6], const double spacing[3],
+                       void* stream, int shard, int nshards, double* d_sq4, sc_coeffs* out) {
+  const double t0 = wall_ms();
+  if (!d_sums || (!d_keys && n_keys) || n_keys < 0 || !bbox || !spacing || !out || nshards < 1 ||
+      shard < 0 || shard >= nshards || nx <= 0 || ny <= 0 || nz <= 0) {
+    set_err("bad input to sc_shard_diameters");
+    return SC_ERR_INPUT;
+  }
+  for (int i = 0; i < 3; i++)
+    if (!(spacing[i] > 0.0) || !std::isfinite(spacing[i])) {
+      set_err("spacing must be positive and finite");
+      return SC_ERR_INPUT;
+    }
+  if (bbox[3] < 0) {
+    set_err("mask has no occupied voxels");
+    return SC_ERR_EMPTY_ROI;
+  }
+  Ctx* c;
+  int rc;
+  if ((rc = current_ctx(&c))) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  two_phase_opts(c);
+  cudaStream_t s = order_after_legacy(c, stream);
+  std::memset(out, 0, sizeof *out);
+  {  // the summed vertex count must be the gathered key count
+    long long nv = -1;
+    CK(cudaMemcpyAsync(&nv, d_sums + kSumVert, sizeof nv, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (nv != (long long)n_keys) {
+      set_err("summed vertex count %lld != gathered keys %lld", nv, (long long)n_keys);
+      return SC_ERR_INPUT;
+    }
+  }
+  long long punits = 0;
+  const long long n_pbin = (2 * (nx + ny + nz) + 9) * kPlaneBinsHost;
+  const int4 lo = make_int4(bbox[0], bbox[1], bbox[2], 0), hi = make_int4(bbox[3], bbox[4], bbox[5], 0);
+  for (int attempt = 0; attempt < 2; attempt++) {
+    const long long cap = std::max<long long>(vertex_capacity(nx, ny, nz, c->cap_floor), n_keys);
+    const long long dcap =
+        std::min<long long>(cap, std::max<long long>(c->o.dcap, std::max<long long>(c->dcap_floor, 0)));
+    const unsigned long long fp0 = c->fingerprint();
+    if ((rc = ensure_buffers(c, nx, ny, nz, cap, dcap, punits, c->wcap_floor))) return rc;
+    if (nshards > 1) CK(c->canon_tmp.ensure((size_t)(3 * c->dcap_sz)));
+    if (c->fingerprint() != fp0) {
+      c->gen++;
+      c->drop_graphs();
+    }
+    static const int kZero[3] = {0, 0, 0};
+    fill_rp(c, nullptr, nx, ny, nz, spacing, kZero);
+    CK(cudaMemcpyAsync(c->d_rp, c->h_rp, sizeof(RoiParams), cudaMemcpyHostToDevice, s));
+    init_stats<<<1, 256, 0, s>>>(c->d_stats, c->segmap.p, 0LL, nullptr, c->d_rp);
+    CKL(1);
+    shard_import<<<c->sms * 2, 256, 0, s>>>(c->d_stats, lo, hi, c->sort_counts.p, c->pbin_counts.p,
+                                            n_pbin, reinterpret_cast<const long long*>(d_sums));
+    CKL(1);
+    if (n_keys)
+      CK(cudaMemcpyAsync(c->keys.p, d_keys, (size_t)n_keys * sizeof(int4), cudaMemcpyDeviceToDevice, s));
+    CK(record(c, c->kev[2], s));
+    int nk = 0;
+    if ((rc = enqueue_diam(c, s, shard, nshards, nk))) return rc;
+    if (d_sq4)
+      CK(cudaMemcpyAsync(d_sq4, c->d_stats->sq, 4 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const Stats& h = *c->h_stats;
+    if ((long long)h.n_vert != n_keys) {
+      set_err("summed vertex count %llu != gathered keys %lld", h.n_vert, (long long)n_keys);
+      return SC_ERR_INPUT;
+    }
+    const long long PU = (long long)h.n_pwork, WU = (long long)h.n_work;
+    if (n_keys <= c->dcap_sz && PU <= (long long)c->plane_umax.cap && WU <= c->h_rp->wcap) break;
+    if (attempt) { set_err("vertex buffer overflow"); return SC_ERR_NOMEM; }
+    c->cap_floor = std::max(c->cap_floor, cap);  // exact sizes from now on
+    c->dcap_floor = std::max<long long>(c->dcap_floor, n_keys);
+    c->wcap_floor = std::max(c->wcap_floor, WU);
+    punits = PU;
+  }
+  rc = collect_roi(c, spacing, out);
   out->total_ms = wall_ms() - t0;
   return rc;
 }

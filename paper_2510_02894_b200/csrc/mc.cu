@@ -496,7 +496,12 @@ constexpr int kStage = 256;  // staged vertices per warp and z step (denser step
 // Every emitted vertex is also counted into the histograms the diameter stage
 // sorts by: its 3-D Morton brick (block-private, flushed once per block) and
 // its (plane, in-plane brick) bin in each of its three planes (global).
-__device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict__ rp,
+//
+// Cells and vertices are owned by the z layer w of their lower corner (x / y
+// edges in layer w, z edges from w to w + 1), so the layers [wlo, whi] of a
+// slab split (RoiParams::mc_slab) partition cells and vertices exactly.
+__device__ __forceinline__ long long mc_body(int kz, int wlo, int whi,
+                                        const RoiParams* __restrict__ rp,
                                         const uint32_t* __restrict__ bits,
                                         const uint32_t* __restrict__ segmap,
                                         Stats* __restrict__ st,
@@ -511,8 +516,8 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
   const PlaneBricks pbk = plane_bricks(bb);
   const int bshift = brick_shift(bb);
 
-  const int xmin = bb[0], ymin = bb[1], zmin = bb[2];
-  const int xmax = bb[3], ymax = bb[4], zmax = bb[5];
+  const int xmin = bb[0], ymin = bb[1];
+  const int xmax = bb[3], ymax = bb[4];
   long long volk = 0;
   const int lane = threadIdx.x & 31;
   // Warp-private vertex stage (warp-uniform fill level), see the emission.
@@ -549,7 +554,7 @@ __device__ __forceinline__ long long mc_body(int kz, const RoiParams* __restrict
   if (xmax >= 0) {
     // Points/cells that can be crossed or active: [min-1, max] on every axis.
     const int qlo = xmin >> 5, qhi = (xmax + 1) >> 5;
-    const int vlo = ymin - 1, whi = zmax, wlo = zmin - 1;
+    const int vlo = ymin - 1;
     const int nq = qhi - qlo + 1, nv = ymax - vlo + 1;
     const int nzc = (whi - wlo + 1 + kz - 1) / kz;
     const long long n_items = (long long)nq * nv * nzc;
@@ -747,7 +752,18 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
   // bboxes, where parallelism -- not loads -- is the limit (C2: ~22 K items at
   // depth 4 for ~150 K resident threads).
   const long long cols = (long long)(((bb[3] + 1) >> 5) - (bb[0] >> 5) + 1) * (bb[4] - bb[1] + 2);
-  const int zs = bb[5] - bb[2] + 2;
+  // Cell layers [zmin - 1, zmax]; a slab split (the two-phase shard entry)
+  // takes the shard's contiguous share of them.
+  int wlo = bb[2] - 1, whi = bb[5];
+  if (rp->mc_slab) {
+    const int ns = rp->mc_slab >> 16, sh = rp->mc_slab & 0xffff;
+    const long long L = (long long)whi - wlo + 1;
+    const int a = wlo + (int)(L * sh / ns), b = wlo + (int)(L * (sh + 1) / ns);
+    wlo = a;
+    whi = b - 1;
+    if (whi < wlo) return;  // more shards than layers: nothing here (grid-uniform)
+  }
+  const int zs = whi - wlo + 1;
   const long long threads = (long long)gridDim.x * blockDim.x;
   const int kz = cols * ((zs + 7) / 8) >= threads   ? 8
                  : cols * ((zs + 3) / 4) >= threads ? 4
@@ -760,7 +776,7 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
   }
   for (int i = threadIdx.x; i < kSortSupers; i += blockDim.x) s_sup[i] = 0;
   __syncthreads();
-  long long volk = mc_body(kz, rp, bits, segmap, st, vkeys, cap, sort_counts, pbin_counts, bb,
+  long long volk = mc_body(kz, wlo, whi, rp, bits, segmap, st, vkeys, cap, sort_counts, pbin_counts, bb,
                               s_hist, tabs->tn_raw, s_sup, s_stage);
   const int lane = threadIdx.x & 31;
   // Block flush: exact integer partials.

@@ -57,7 +57,8 @@ __global__ void __launch_bounds__(kScanThreads) scan_all(unsigned int* __restric
                                                          int4* __restrict__ sboxes,
                                                          unsigned int* __restrict__ pbin_counts,
                                                          unsigned int* __restrict__ pbin_cursor,
-                                                         unsigned long long* __restrict__ pext) {
+                                                         unsigned long long* __restrict__ pext,
+                                                         int full_cursor) {
   pdl_enter();
   KTrace kt_(st, kTrScan);
   if (blockIdx.x == 0 && threadIdx.x == 0) st->t_mesh = global_ns();  // marching cubes done
@@ -157,7 +158,8 @@ __global__ void __launch_bounds__(kScanThreads) scan_all(unsigned int* __restric
     bool any = false;
 #pragma unroll
     for (int i = 0; i < kScanSlices; i++) any |= sup[kScanSlices * blockIdx.x + i] != 0u;
-    if (!any) return;
+    // (the shard entry's canonical order reads every bin's cursor: write them all)
+    if (!any && !full_cursor) return;
     unsigned int base;
     block_exscan(threadIdx.x < kScanSlices * blockIdx.x ? sup[threadIdx.x] : 0u, &base);
     uint4 v[kPerThread / 4];
@@ -631,63 +633,209 @@ __device__ __forceinline__ bool key_less(int4 a, int4 b) {
   return a.x < b.x;
 }
 
-__global__ void __launch_bounds__(256) canon_keys(const int4* __restrict__ in,
-                                                  int4* __restrict__ out, long long cap,
-                                                  const Stats* __restrict__ st) {
+// Warp-stable LSD radix sort of one segment [lo, hi) by a W-bit local key
+// (the element's coordinates inside its bin; distinct within the bin), 5 bits
+// per pass: per pass a digit histogram (match_any peers, leader adds), a
+// 32-way exclusive scan, and a stable scatter (rank among equal-digit peers
+// of the 32-element step + running digit offset).  O(B) per pass, so large
+// bins cost linear, not quadratic, time.  Ping-pongs between `a` (input and
+// final output) and `t` (scratch of the same layout).  s_run: 32 ints per warp.
+template <typename T, typename LocalKey>
+__device__ __forceinline__ void canon_segment(T* __restrict__ a, T* __restrict__ t,
+                                              unsigned int lo, unsigned int hi, int W,
+                                              int* s_run, LocalKey lkey) {
+  const int lane = threadIdx.x & 31;
+  const unsigned int lt = (1u << lane) - 1u;
+  if (hi - lo <= 1) return;
+  T* src = a;
+  T* dst = t;
+  const int passes = (W + 4) / 5;
+  for (int pz = 0; pz < passes; pz++) {
+    const int sh = 5 * pz;
+    __syncwarp();
+    s_run[lane] = 0;  // digit histogram (one leader per distinct digit per step)
+    __syncwarp();
+    for (unsigned int i0 = lo; i0 < hi; i0 += 32) {
+      const unsigned int i = i0 + lane;
+      const unsigned int d = i < hi ? (lkey(src[i]) >> sh) & 31u : 32u;
+      const unsigned int peers = __match_any_sync(0xffffffffu, d);
+      if (d < 32u && !(peers & lt)) s_run[d] += __popc(peers);
+      __syncwarp();
+    }
+    const unsigned int cnt = (unsigned int)s_run[lane];
+    unsigned int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    __syncwarp();
+    s_run[lane] = (int)(incl - cnt);
+    __syncwarp();
+    for (unsigned int i0 = lo; i0 < hi; i0 += 32) {
+      const unsigned int i = i0 + lane;
+      const bool ok = i < hi;
+      T e{};
+      if (ok) e = src[i];
+      const unsigned int d = ok ? (lkey(e) >> sh) & 31u : 32u;
+      const unsigned int peers = __match_any_sync(0xffffffffu, d);
+      const unsigned int r = __popc(peers & lt);
+      const int base = ok ? s_run[d] : 0;
+      __syncwarp();
+      if (ok) {
+        dst[lo + (unsigned int)base + r] = e;
+        if (r == 0) s_run[d] = base + __popc(peers);
+      }
+      __syncwarp();
+    }
+    T* x = src; src = dst; dst = x;
+  }
+  if (src != a)  // odd pass count: the sorted segment is in the scratch
+    for (unsigned int i = lo + lane; i < hi; i += 32) a[i] = src[i];
+}
+
+// One warp per segment: every element ranked through a warp-private bitmap of
+// the bin's local key space (keys are distinct within a bin, so a key's rank
+// is the number of set bits below it): set bits, per-word prefix popcounts
+// (16-bit: a bin holds < 2^16 entries), place each element at lo + rank in
+// the scratch, copy back.  O(B / 32 + 2^W / 1024) steps per warp and one warp
+// per bin, so thousands of bins are in flight at once.  W <= kCanonBitsMax.
+constexpr int kCanonBitsMax = 15;  // 1024 bitmap words per warp
+constexpr int kCanonWarps = 4;     // warps per block (shared memory: 6 KB per warp)
+
+template <typename T, typename LocalKey>
+__device__ __forceinline__ void canon_warp_bitmap(T* __restrict__ a, T* __restrict__ t,
+                                                  unsigned int lo, unsigned int hi, int W,
+                                                  unsigned int* bits, unsigned short* pre,
+                                                  LocalKey lkey) {
+  const int lane = threadIdx.x & 31;
+  const int nwords = 1 << (W > 5 ? W - 5 : 0);
+  for (int w = lane; w < nwords; w += 32) bits[w] = 0u;
+  __syncwarp();
+  // (8 elements per lane in flight per step: the longest segment bounds the
+  // kernel, so its steps must not each pay a full memory latency)
+  constexpr int U = 4;
+  for (unsigned int b0 = lo; b0 < hi; b0 += 32 * U) {
+    T e[U];
+#pragma unroll
+    for (int q = 0; q < U; q++)
+      if (b0 + 32 * q + lane < hi) e[q] = a[b0 + 32 * q + lane];
+#pragma unroll
+    for (int q = 0; q < U; q++)
+      if (b0 + 32 * q + lane < hi) {
+        const unsigned int L = lkey(e[q]);
+        atomicOr(&bits[L >> 5], 1u << (L & 31u));
+      }
+  }
+  __syncwarp();
+  const int per = (nwords + 31) >> 5, w0 = lane * per;
+  unsigned int v = 0;
+  for (int k = 0; k < per; k++)
+    if (w0 + k < nwords) v += __popc(bits[w0 + k]);
+  unsigned int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned int x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += x;
+  }
+  unsigned int run = incl - v;
+  for (int k = 0; k < per; k++)
+    if (w0 + k < nwords) {
+      pre[w0 + k] = (unsigned short)run;
+      run += __popc(bits[w0 + k]);
+    }
+  __syncwarp();
+  for (unsigned int b0 = lo; b0 < hi; b0 += 32 * U) {
+    T e[U];
+#pragma unroll
+    for (int q = 0; q < U; q++)
+      if (b0 + 32 * q + lane < hi) e[q] = a[b0 + 32 * q + lane];
+#pragma unroll
+    for (int q = 0; q < U; q++)
+      if (b0 + 32 * q + lane < hi) {
+        const unsigned int L = lkey(e[q]);
+        t[lo + pre[L >> 5] + __popc(bits[L >> 5] & ((1u << (L & 31u)) - 1u))] = e[q];
+      }
+  }
+  __syncwarp();
+  for (unsigned int b0 = lo; b0 < hi; b0 += 32 * U) {
+    T e[U];
+#pragma unroll
+    for (int q = 0; q < U; q++)
+      if (b0 + 32 * q + lane < hi) e[q] = t[b0 + 32 * q + lane];
+#pragma unroll
+    for (int q = 0; q < U; q++)
+      if (b0 + 32 * q + lane < hi) a[b0 + 32 * q + lane] = e[q];
+  }
+  __syncwarp();
+}
+
+template <typename T, typename LocalKey>
+__device__ __forceinline__ void canon_one(T* __restrict__ a, T* __restrict__ t, unsigned int lo,
+                                          unsigned int hi, int W, LocalKey lkey) {
+  __shared__ unsigned int s_bits[kCanonWarps][1 << (kCanonBitsMax - 5)];
+  __shared__ unsigned short s_pre[kCanonWarps][1 << (kCanonBitsMax - 5)];
+  __shared__ int s_run[kCanonWarps][32];
+  const int w = threadIdx.x >> 5;
+  if (hi <= lo + 1) return;
+  if (hi - lo <= 32) {  // small segment: one element per lane, ranked by shuffles
+    const int lane = threadIdx.x & 31;
+    const bool ok = lo + lane < hi;
+    T e{};
+    unsigned int k = 0xffffffffu;  // (never below a real key: local keys have < 32 bits)
+    if (ok) {
+      e = a[lo + lane];
+      k = lkey(e);
+    }
+    unsigned int r = 0;
+#pragma unroll
+    for (int j = 0; j < 32; j++) r += __shfl_sync(0xffffffffu, k, j) < k ? 1u : 0u;
+    __syncwarp();  // every element is in registers: sort in place
+    if (ok) a[lo + r] = e;
+    __syncwarp();
+    return;
+  }
+  if (W <= kCanonBitsMax)
+    canon_warp_bitmap(a, t, lo, hi, W, s_bits[w], s_pre[w], lkey);
+  else  // very large grids: the linear radix passes
+    canon_segment(a, t, lo, hi, W, s_run[w], lkey);
+}
+
+// Canonical order of the brick bins: one warp per bin, its segment
+// [cursor[b - 1], cursor[b]) (scatter_all advanced every cursor from the bin's
+// start to its end; scan_all wrote every cursor, full_cursor = 1) sorted in
+// place by the vertex's coordinates inside its brick (z major).
+__global__ void __launch_bounds__(32 * kCanonWarps) canon_keys(int4* __restrict__ keys,
+                                                               int4* __restrict__ tmp,
+                                                               const unsigned int* __restrict__ cursor,
+                                                               const Stats* __restrict__ st) {
   if (st->ovf) return;
-  const long long n = n_verts(st, cap);
   int bb[6];
 #pragma unroll
   for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
   if (bb[3] < 0) return;
-  const int s = brick_shift(bb);
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int4 k = in[i];
-    const unsigned int b = brick_bin(k.x, k.y, k.z, bb, s);
-    long long lo = i, hi = i + 1;
-    while (lo > 0) {
-      const int4 q = in[lo - 1];
-      if (brick_bin(q.x, q.y, q.z, bb, s) != b) break;
-      lo--;
-    }
-    while (hi < n) {
-      const int4 q = in[hi];
-      if (brick_bin(q.x, q.y, q.z, bb, s) != b) break;
-      hi++;
-    }
-    long long rank = 0;
-    for (long long j = lo; j < hi; j++) rank += key_less(in[j], k) ? 1 : 0;
-    out[lo + rank] = k;
+  const int sft = brick_shift(bb);
+  const int x0 = 2 * bb[0] - 1, y0 = 2 * bb[1] - 1, z0 = 2 * bb[2] - 1;
+  const unsigned int m = (1u << sft) - 1u;
+  auto lkey = [=](int4 k) {
+    return ((((unsigned int)(k.z - z0) & m) << (2 * sft)) |
+            (((unsigned int)(k.y - y0) & m) << sft) | ((unsigned int)(k.x - x0) & m));
+  };
+  const int nw = (int)(gridDim.x * kCanonWarps);
+  for (int b = (int)(blockIdx.x * kCanonWarps + (threadIdx.x >> 5)); b < kSortBins; b += nw) {
+    const unsigned int hi = cursor[b], lo = b ? cursor[b - 1] : 0u;
+    canon_one(keys, tmp, lo, hi, 3 * sft, lkey);
   }
 }
 
-__global__ void __launch_bounds__(256) canon_copy_keys(const int4* __restrict__ in,
-                                                       int4* __restrict__ out, long long cap,
-                                                       const Stats* __restrict__ st) {
-  if (st->ovf) return;
-  const long long n = n_verts(st, cap);
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    out[i] = in[i];
-}
-
-__device__ __forceinline__ unsigned int inplane_bin(int2 e, int axis, const PlaneBricks& pb) {
-  // family 0 (XY): (X, Y); 1 (XZ): (X, Z); 2 (YZ): (Y, Z) -- as plane_bins
-  const int ia = axis == 2 ? 1 : 0, ib = axis == 0 ? 1 : 2;
-  const unsigned int ba = (unsigned int)(e.x - pb.lo[ia]) >> pb.shift[ia];
-  const unsigned int bbv = (unsigned int)(e.y - pb.lo[ib]) >> pb.shift[ib];
-  return spread2x4(ba) | (spread2x4(bbv) << 1);
-}
-
-// Planar entries: plane p of the entry at position i by binary search over
-// the plane offsets, then its (plane, in-plane bin) segment sorted by (a, b)
-// (distinct within a plane: the plane key is the vertex's third coordinate).
-// mode 0: sort `in` into `out`; mode 1: copy `in` back into `out`.
-__global__ void __launch_bounds__(256) canon_planes(const int2* __restrict__ in,
-                                                    int2* __restrict__ out,
-                                                    const unsigned int* __restrict__ start,
-                                                    const Stats* __restrict__ st, int mode) {
+// Canonical order of the planar entries: each (plane, in-plane bin)
+// segment -- plane start + the bin cursors scatter_all advanced to the bin
+// ends -- sorted in place by the entry's coordinates inside its in-plane brick.
+__global__ void __launch_bounds__(32 * kCanonWarps) canon_planes(int2* __restrict__ ent,
+                                                                 int2* __restrict__ tmp,
+                                                                 const unsigned int* __restrict__ start,
+                                                                 const unsigned int* __restrict__ pcur,
+                                                                 const Stats* __restrict__ st) {
   if (st->ovf) return;
   int bb[6];
 #pragma unroll
@@ -696,32 +844,32 @@ __global__ void __launch_bounds__(256) canon_planes(const int2* __restrict__ in,
   const PlaneSpace ps = plane_space(bb);
   const PlaneBricks pbk = plane_bricks(bb);
   const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
-  const long long total = start[P];
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int2 e = in[i];
-    if (mode == 1) {
-      out[i] = e;
-      continue;
-    }
-    int lo_p = 0, hi_p = P;  // largest p with start[p] <= i
-    while (hi_p - lo_p > 1) {
-      const int mid = (lo_p + hi_p) >> 1;
-      if ((long long)start[mid] <= i) lo_p = mid; else hi_p = mid;
-    }
-    const int p = lo_p;
+  // one warp per 32 in-plane bins of a plane (most are empty): the non-empty
+  // ones one after another
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * kCanonWarps;
+  for (long long g = (long long)blockIdx.x * kCanonWarps + (threadIdx.x >> 5);
+       g < (long long)P * (kPlaneBins / 32); g += nw) {
+    const long long t = 32 * g + lane;
+    const int p = (int)(t / kPlaneBins), k = (int)(t % kPlaneBins);  // p warp-uniform
+    const unsigned int base = start[p];
+    const unsigned int lo0 = base + (k ? pcur[t - 1] : 0u), hi0 = base + pcur[t];
+    unsigned int work = __ballot_sync(0xffffffffu, hi0 > lo0 + 1);
+    if (!work) continue;
+    // family 0 (XY): (X, Y); 1 (XZ): (X, Z); 2 (YZ): (Y, Z) -- as plane_bins
     const int axis = plane_axis(p, ps);
-    const long long pb0 = start[p], pb1 = start[p + 1];
-    const unsigned int b = inplane_bin(e, axis, pbk);
-    long long lo = i, hi = i + 1;
-    while (lo > pb0 && inplane_bin(in[lo - 1], axis, pbk) == b) lo--;
-    while (hi < pb1 && inplane_bin(in[hi], axis, pbk) == b) hi++;
-    long long rank = 0;
-    for (long long j = lo; j < hi; j++) {
-      const int2 q = in[j];
-      rank += (q.x < e.x || (q.x == e.x && q.y < e.y)) ? 1 : 0;
+    const int ia = axis == 2 ? 1 : 0, ib = axis == 0 ? 1 : 2;
+    const int la = pbk.lo[ia], lb = pbk.lo[ib], sa = pbk.shift[ia], sb = pbk.shift[ib];
+    const unsigned int ma = (1u << sa) - 1u, mb = (1u << sb) - 1u;
+    auto lkey = [=](int2 e) {
+      return (((unsigned int)(e.x - la) & ma) << sb) | ((unsigned int)(e.y - lb) & mb);
+    };
+    while (work) {
+      const int l = __ffs(work) - 1;
+      work &= work - 1;
+      const unsigned int lo = __shfl_sync(0xffffffffu, lo0, l), hi = __shfl_sync(0xffffffffu, hi0, l);
+      canon_one(ent, tmp, lo, hi, sa + sb, lkey);
     }
-    out[lo + rank] = e;
   }
 }
 

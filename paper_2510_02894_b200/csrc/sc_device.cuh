@@ -148,7 +148,8 @@ struct RoiParams {
                        // unmarked segments as zero (0: every word is written); bit 1:
                        // the pack skips the conversion of all-zero segments
   int pflags;          // bit 2: kernels record their timeline spans (SC_TRACE)
-  int pad0_;
+  int mc_slab;         // 0, or (nshards << 16) | shard: mc_cells walks only that shard's
+                       // contiguous share of the cell layers (two-phase shard entry)
   Frame f;             // cx2..cz2 are filled on the device from the bbox
   long long wcap;      // capacity of the 3-D work list (overflow -> exact re-run)
 };

@@ -200,6 +200,61 @@ def calculate_coefficients_shard(mask, spacing: Sequence[float], shard: int, nsh
     return _from_struct(out)
 
 
+def shard_exchange_sizes(shape) -> Tuple[int, int]:
+    """(n_sums, key_cap) of the two-phase shard entry for a (nz, ny, nx) grid:
+    int64 elements of the partial-sums vector and vertex capacity of a key
+    buffer (4 int32 per vertex)."""
+    nz, ny, nx = (int(d) for d in shape)
+    n_sums, key_cap = ctypes.c_int64(), ctypes.c_int64()
+    rc = _native.load().sc_shard_exchange_sizes(nx, ny, nz, ctypes.byref(n_sums),
+                                                 ctypes.byref(key_cap))
+    _native.raise_for(rc, "sc_shard_exchange_sizes")
+    return int(n_sums.value), int(key_cap.value)
+
+
+def shard_mesh(mask, spacing: Sequence[float], shard: int, nshards: int, sums, keys,
+               stream=None) -> Tuple[int, Tuple[int, ...]]:
+    """Phase 1 of the slab-split shard (sc_shard_mesh): marching cubes over the
+    shard's share of the cell layers of a device-resident mask.  `sums` (CUDA
+    int64, n_sums) receives the exact integer partials to all-reduce(SUM);
+    `keys` (CUDA int32, 4 x key_cap) the shard's vertex keys to all-gather.
+    Returns (vertex count of the shard, global bbox)."""
+    sp = np.asarray(_check_spacing(spacing), dtype=np.float64)
+    nz, ny, nx = (int(d) for d in mask.shape)
+    if not mask.is_contiguous():
+        raise ValueError("device mask must be contiguous")
+    handle = _stream_handle(mask, stream)
+    n = ctypes.c_int64()
+    bbox = (ctypes.c_int32 * 6)()
+    rc = _native.load().sc_shard_mesh(
+        ctypes.c_void_p(mask.data_ptr()), nx, ny, nz,
+        sp.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.c_void_p(handle),
+        int(shard), int(nshards), ctypes.c_void_p(sums.data_ptr()),
+        ctypes.c_void_p(keys.data_ptr()), int(keys.numel() // 4), ctypes.byref(n), bbox)
+    _native.raise_for(rc, "sc_shard_mesh")
+    return int(n.value), tuple(int(b) for b in bbox)
+
+
+def shard_diameters(sums, keys, n_keys: int, shape, bbox, spacing: Sequence[float], shard: int,
+                    nshards: int, sq4, stream=None) -> Coefficients:
+    """Phase 2 of the slab-split shard (sc_shard_diameters): the summed partials,
+    the gathered keys (first n_keys vertices of `keys`) and phase 1's bbox;
+    shard `shard` of the pair grid, squared maxima into `sq4` (CUDA float64[4])
+    for an all-reduce(MAX).  Counts, area and volume are complete."""
+    sp = np.asarray(_check_spacing(spacing), dtype=np.float64)
+    nz, ny, nx = (int(d) for d in shape)
+    handle = _stream_handle(sums, stream)
+    bb = (ctypes.c_int32 * 6)(*bbox)
+    out = _native.ScCoeffs()
+    rc = _native.load().sc_shard_diameters(
+        ctypes.c_void_p(sums.data_ptr()), ctypes.c_void_p(keys.data_ptr()), int(n_keys),
+        nx, ny, nz, bb, sp.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+        ctypes.c_void_p(handle), int(shard), int(nshards), ctypes.c_void_p(sq4.data_ptr()),
+        ctypes.byref(out))
+    _native.raise_for(rc, "sc_shard_diameters")
+    return _from_struct(out)
+
+
 def calculate_coefficients_batch(masks: Sequence, spacings: Sequence[Sequence[float]],
                                  device: int = 0,
                                  devices: Optional[Sequence[int]] = None) -> List[Coefficients]:

@@ -5,11 +5,14 @@ Two shapes of work shard naturally; nothing else is split:
 * ROI batches (C4): independent masks.  `assign_rois` places them on ranks by
   longest-processing-time on an estimated cost; each rank runs its ROIs with
   no data-path collective; the 9-scalar records are gathered once at the end.
-* One very large mesh (C3): every rank runs the (cheap, ~50 us) marching-cubes
-  stage on the full mask, then only its slice of the triangular pair-tile grid
-  and of the planar groups (`sc_calculate_coefficients_shard`).  The four
-  partial squared maxima are combined with one all_reduce(MAX) over NCCL /
-  NVLink -- the only exchange the path has.
+* One very large mesh (C3), `slab_sharded_coefficients`: every rank packs the
+  mask (global bbox), runs marching cubes over its contiguous share of the cell
+  layers only (`sc_shard_mesh`), then the exact integer partials are
+  all-reduced (SUM) and the vertex keys all-gathered; every rank evaluates its
+  slice of the triangular pair-tile grid and of the planar groups
+  (`sc_shard_diameters`), and the four partial squared maxima are combined
+  with one all_reduce(MAX) over NCCL / NVLink.  `sharded_coefficients` is the
+  one-call form (full marching cubes on every rank, only the pair grid split).
 
 One process per GPU; torch.distributed is plumbing (process group, NCCL
 all-reduce), the compute is the C ABI.  The combine logic takes an injectable
@@ -168,3 +171,117 @@ def sharded_coefficients(mask, spacing: Sequence[float], group=None,
     rec.update({"Maximum3DDiameter": d[0], "Maximum2DDiameterXY": d[1],
                 "Maximum2DDiameterXZ": d[2], "Maximum2DDiameterYZ": d[3]})
     return rec
+
+
+# ---- slab split: marching cubes divided too (sc_shard_mesh / _diameters) -----
+
+def exchange_mesh(sums, keys, n_local: int, group=None):
+    """The slab split's one data exchange between the two phases: all-reduce
+    (SUM) of the int64 partials `sums` in place, and all-gather of every rank's
+    first n_local vertex keys (4 int32 each; ragged, padded to the largest
+    share).  Returns (gathered keys, their total count)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return keys, n_local
+    dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
+    cnt = torch.tensor([n_local], dtype=torch.int64, device=sums.device)
+    counts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(counts, cnt, group=group)
+    counts = [int(c.item()) for c in counts]
+    m = max(counts)
+    local = keys[: 4 * m] if keys.numel() >= 4 * m else torch.cat(
+        [keys, keys.new_zeros(4 * m - keys.numel())])
+    parts = [torch.empty_like(local) for _ in range(world)]
+    dist.all_gather(parts, local.contiguous(), group=group)
+    gathered = torch.cat([p[: 4 * c] for p, c in zip(parts, counts)])
+    return gathered, sum(counts)
+
+
+def slab_sharded_coefficients(mask, spacing: Sequence[float], group=None,
+                              mesh: Optional[Callable] = None,
+                              diameters: Optional[Callable] = None):
+    """One large ROI, marching cubes and pair grid both split across the ranks
+    of `group`: phase 1 on this rank's cell layers, one
+    exchange (`exchange_mesh`), phase 2 on this rank's pair units, one
+    all_reduce(MAX) of the 4 squared maxima.
+
+    mesh(shard, nshards) -> (sums, keys, n_local, bbox) and
+    diameters(sums, keys, n_all, bbox, shard, nshards, sq4) -> record dict
+    default to the C ABI (device-resident mask); injectable for CPU tests."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if mesh is None:
+        from .features import shard_diameters, shard_exchange_sizes, shard_mesh
+
+        shape = tuple(int(d) for d in mask.shape)
+        n_sums, key_cap = shard_exchange_sizes(shape)
+
+        def mesh(shard, nshards):
+            sums = torch.empty(n_sums, dtype=torch.int64, device=mask.device)
+            keys = torch.empty(4 * key_cap, dtype=torch.int32, device=mask.device)
+            n, bbox = shard_mesh(mask, spacing, shard, nshards, sums, keys)
+            return sums, keys, n, bbox
+
+        def diameters(sums, keys, n_all, bbox, shard, nshards, sq4):
+            c = shard_diameters(sums, keys, n_all, shape, bbox, spacing, shard, nshards, sq4)
+            return c.to_dict() | {"triangle_count": c.triangle_count,
+                                  "active_cubes": c.active_cubes}
+        device = mask.device
+    else:
+        device = torch.device("cpu")
+    sums, keys, n_local, bbox = mesh(rank, world)
+    keys_all, n_all = exchange_mesh(sums, keys, n_local, group)
+    sq4 = torch.zeros(4, dtype=torch.float64, device=device)
+    rec = dict(diameters(sums, keys_all, n_all, bbox, rank, world, sq4))
+    if world > 1:
+        dist.all_reduce(sq4, op=dist.ReduceOp.MAX, group=group)
+    d = [math.sqrt(v) for v in sq4.cpu().tolist()]
+    rec.update({"Maximum3DDiameter": d[0], "Maximum2DDiameterXY": d[1],
+                "Maximum2DDiameterXZ": d[2], "Maximum2DDiameterYZ": d[3]})
+    return rec
+
+
+def simulate_slab_shards(mask, spacing: Sequence[float], nshards: int, timer=None):
+    """All `nshards` shards of the slab split run one after another on this
+    GPU, the exchange done locally (sum / concatenate): the N-GPU result on 1
+    GPU.  timer(phase, shard, fn) may wrap each phase call (bench timing).
+    Returns (record, per-shard list of (phase-1 record, phase-2 record))."""
+    import torch
+
+    from .features import shard_diameters, shard_exchange_sizes, shard_mesh
+
+    run = timer or (lambda phase, shard, fn: fn())
+    shape = tuple(int(d) for d in mask.shape)
+    n_sums, key_cap = shard_exchange_sizes(shape)
+    tot = torch.zeros(n_sums, dtype=torch.int64, device=mask.device)
+    parts, bbox = [], None
+    for s in range(nshards):
+        sums = torch.empty(n_sums, dtype=torch.int64, device=mask.device)
+        keys = torch.empty(4 * key_cap, dtype=torch.int32, device=mask.device)
+        n, bb = run(1, s, lambda: shard_mesh(mask, spacing, s, nshards, sums, keys))
+        assert bbox is None or bb == bbox
+        bbox = bb
+        tot += sums
+        parts.append(keys[: 4 * n].clone())
+    keys_all = torch.cat(parts)
+    n_all = keys_all.numel() // 4
+    sq = torch.zeros(4, dtype=torch.float64, device=mask.device)
+    rec = None
+    for s in range(nshards):
+        sq4 = torch.zeros(4, dtype=torch.float64, device=mask.device)
+        c = run(2, s, lambda: shard_diameters(tot, keys_all, n_all, shape, bbox, spacing, s,
+                                              nshards, sq4))
+        sq = torch.maximum(sq, sq4)
+        rec = c
+    d = [math.sqrt(v) for v in sq.cpu().tolist()]
+    out = rec.to_dict() | {"triangle_count": rec.triangle_count,
+                           "active_cubes": rec.active_cubes}
+    out.update({"Maximum3DDiameter": d[0], "Maximum2DDiameterXY": d[1],
+                "Maximum2DDiameterXZ": d[2], "Maximum2DDiameterYZ": d[3]})
+    return out

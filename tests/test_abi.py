@@ -37,7 +37,7 @@ def test_library_exports_header(native):
     for name in names:
         assert hasattr(lib, name), name
     assert set(names) == set(native.EXPORTED)
-    assert lib.sc_abi_version() == 3
+    assert lib.sc_abi_version() == 4
 
 
 def test_nm_shows_c_symbols(native):

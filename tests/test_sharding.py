@@ -160,3 +160,70 @@ def test_gloo_world2_sharded_max_and_batch(oracle_mod):
         assert ok, "sharded max != full max"
         assert ids == list(range(10))
         assert ranks == [0, 1]  # both ranks did work
+
+
+# ---- slab split: the exchange between the two phases (gloo, world 3) ---------
+
+def _slab_parts(shard):
+    """Shard-local phase-1 output of the CPU stub: int64 partials and a ragged
+    key share (shard 1 has none)."""
+    import torch
+
+    g = torch.Generator().manual_seed(100 + shard)
+    sums = torch.randint(0, 1 << 40, (37,), generator=g, dtype=torch.int64)
+    n = (0, 5, 3)[shard]
+    keys = torch.arange(4 * n, dtype=torch.int32) + 1000 * shard
+    pad = torch.full((4 * 7,), -1, dtype=torch.int32)  # a key buffer larger than the share
+    pad[: 4 * n] = keys
+    return sums, pad, n
+
+
+def _slab_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_02894_b200 import sharding
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        want_sums = sum(_slab_parts(s)[0] for s in range(world))
+        want_keys = torch.cat([_slab_parts(s)[1][: 4 * _slab_parts(s)[2]] for s in range(world)])
+        seen = {}
+
+        def mesh(shard, nshards):
+            assert (shard, nshards) == (rank, world)
+            sums, keys, n = _slab_parts(shard)
+            return sums.clone(), keys, n, (1, 2, 3, 4, 5, 6)
+
+        def diameters(sums, keys, n_all, bbox, shard, nshards, sq4):
+            seen["ok"] = (torch.equal(sums, want_sums) and n_all == want_keys.numel() // 4
+                          and torch.equal(keys[: 4 * n_all], want_keys)
+                          and bbox == (1, 2, 3, 4, 5, 6))
+            sq4.copy_(torch.tensor([1.0 + shard, 4.0 - shard, 9.0, 16.0 * (shard == 1)],
+                                   dtype=torch.float64))
+            return {"VertexCount": n_all}
+
+        rec = sharding.slab_sharded_coefficients(None, (1, 1, 1), mesh=mesh, diameters=diameters)
+        got = [rec[k] for k in ("Maximum3DDiameter", "Maximum2DDiameterXY",
+                                "Maximum2DDiameterXZ", "Maximum2DDiameterYZ")]
+        q.put((rank, seen.get("ok", False), got, rec["VertexCount"]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world3_slab_exchange():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok, got, nv in res:
+        assert ok, f"rank {rank}: summed partials / gathered keys differ"
+        assert got == [math.sqrt(3.0), 2.0, 3.0, 4.0]
+        assert nv == 8
