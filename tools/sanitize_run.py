@@ -1,7 +1,7 @@
 """Workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
 C1 and C5 plus a small KiTS-like mask through every entry -- single host call,
 device call, host batch (crop / split / host pack), device batch (32 slots,
-pack chain, TMA pack), shard entry, raw typed payloads (C and Fortran), mesh
+pack chain, TMA pack), shard entry, two-phase slab split, raw typed payloads (C and Fortran), mesh
 export, diameters -- and checks the results agree.  Small sizes: the tools
 slow kernels down by 10-100x.  usage: sanitize_run.py [quick]"""
 import os
@@ -12,7 +12,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2510_02894_b200 as sc  # noqa: E402
-from paper_2510_02894_b200 import _native, synth  # noqa: E402
+from paper_2510_02894_b200 import _native, sharding, synth  # noqa: E402
 
 quick = len(sys.argv) > 1 and sys.argv[1] == "quick"
 cases = [(synth.synth_mask("sphere", (64, 64, 64), radius=24), (1.0, 1.0, 1.0)),
@@ -29,6 +29,9 @@ for (a, sp), d, w in zip(cases, ds, want):
         sc.calculate_coefficients_shard(d, sp, s, 2, sq)
         torch.maximum(best, sq, out=best)
     assert abs(best[0].item() ** 0.5 - w["Maximum3DDiameter"]) == 0.0
+    # two-phase slab split (sc_shard_mesh / sc_shard_diameters), 3 shards
+    rec = sharding.simulate_slab_shards(d, sp, 3)
+    assert all(rec[k] == w[k] for k in w), (rec, w)
 got = sc.calculate_coefficients_device_batch(ds * 3, [sp for _, sp in cases] * 3)
 assert [g.to_dict() for g in got] == want * 3
 for opts in ({}, {"host_pack": 1}, {"host_split": 30}, {"host_crop": 0}):
