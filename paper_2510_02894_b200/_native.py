@@ -117,13 +117,16 @@ def load():
                                                       ctypes.c_void_p, cp]
         i64p = ctypes.POINTER(i64)
         i32p = ctypes.POINTER(ctypes.c_int32)
-        L.sc_shard_exchange_sizes.argtypes = [i64, i64, i64, i64p, i64p]
-        L.sc_shard_mesh.argtypes = [ctypes.c_void_p, i64, i64, i64, dp, ctypes.c_void_p,
-                                    ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
-                                    i64, i64p, i32p]
-        L.sc_shard_diameters.argtypes = [ctypes.c_void_p, ctypes.c_void_p, i64, i64, i64, i64,
-                                         i32p, dp, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
-                                         ctypes.c_void_p, cp]
+        ab = bool(os.environ.get("SC_LIB"))  # an older A/B build may lack newer entries
+        if not ab or hasattr(L, "sc_shard_mesh"):
+            L.sc_shard_exchange_sizes.argtypes = [i64, i64, i64, i64p, i64p]
+            L.sc_shard_mesh.argtypes = [ctypes.c_void_p, i64, i64, i64, dp, ctypes.c_void_p,
+                                        ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                        ctypes.c_void_p,
+                                        i64, i64p, i32p]
+            L.sc_shard_diameters.argtypes = [ctypes.c_void_p, ctypes.c_void_p, i64, i64, i64,
+                                             i64, i32p, dp, ctypes.c_void_p, ctypes.c_int,
+                                             ctypes.c_int, ctypes.c_void_p, cp]
         L.sc_calculate_coefficients_batch.argtypes = [ctypes.POINTER(u8p),
                                                       ctypes.POINTER(i64), dp, i64,
                                                       ctypes.c_int, cp]
@@ -161,7 +164,7 @@ def load():
         L.sc_abi_version.restype = ctypes.c_int
         L.sc_device_count.restype = ctypes.c_int
         for name in EXPORTED:
-            if not hasattr(L, name):
+            if not hasattr(L, name) and not (ab and name.startswith("sc_shard_")):
                 raise OSError(f"{LIB_PATH} does not export {name}")
         _lib = L
         return L

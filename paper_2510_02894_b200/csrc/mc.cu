@@ -756,8 +756,10 @@ __global__ void __launch_bounds__(256, 4) mc_cells(const RoiParams* __restrict__
   // takes the shard's contiguous share of them.
   int wlo = bb[2] - 1, whi = bb[5];
   if (rp->mc_slab) {
-    const int ns = rp->mc_slab >> 16, sh = rp->mc_slab & 0xffff;
-    const long long L = (long long)whi - wlo + 1;
+    // (32-bit: a 64-bit division would inline a long routine into a kernel
+    // that sits at the edge of the instruction cache; L < 2^16, shards < 2^15)
+    const unsigned int ns = (unsigned int)rp->mc_slab >> 16, sh = (unsigned int)rp->mc_slab & 0xffffu;
+    const unsigned int L = (unsigned int)(whi - wlo + 1);
     const int a = wlo + (int)(L * sh / ns), b = wlo + (int)(L * (sh + 1) / ns);
     wlo = a;
     whi = b - 1;
