@@ -101,8 +101,6 @@ __global__ void fp32_probe(float*, int, float, float);
 
 __global__ void empty_kernel();
 __global__ void canon_keys(int4*, int4*, const unsigned int*, const Stats*);
-__global__ void canon_planes(int2*, int2*, const unsigned int*, const unsigned int*,
-                             const Stats*);
 }  // namespace sc
 
 using namespace sc;
@@ -313,7 +311,6 @@ struct Ctx {
   DevBuf<int4> plane_hboxes;  // boxes of the two 64-entry halves of every in-plane chunk
   DevBuf<unsigned int> plane_cmap;  // plane of every in-plane chunk (scatter_all)
   DevBuf<int2> plane_sorted;
-  DevBuf<int2> canon_tmp;  // shard entry: canonical planar order (canon_planes)
   DevBuf<uint8_t> mask_stage, raw_stage;  // raw_stage: two chunk buffers (typed payloads)
   uint8_t* h_raw = nullptr;               // pinned staging of typed payload chunks (two halves)
   size_t h_raw_cap = 0;                   // bytes
@@ -368,7 +365,7 @@ struct Ctx {
                         work.p, warp_max.p, plane_umax.p,
                         plane_counts.p, plane_start.p, plane_tstart.p, plane_sorted.p,
                         plane_work.p, plane_cstart.p, pbin_counts.p, pbin_cursor.p,
-                        plane_ext.p, plane_boxes_buf.p, plane_hboxes.p, canon_tmp.p,
+                        plane_ext.p, plane_boxes_buf.p, plane_hboxes.p,
                         plane_cmap.p};
     for (const void* p : ps) h = (h ^ (unsigned long long)(uintptr_t)p) * 1099511628211ull;
     return h;
@@ -483,8 +480,7 @@ int get_ctx(int device, Ctx** out, int slot = 0) {
                                (const void*)diam_refine, (const void*)cloud_diameters,
                                (const void*)plane_boxes,
                                (const void*)plane_lb, (const void*)plane_filter,
-                               (const void*)canon_keys,
-                               (const void*)canon_planes};
+                               (const void*)canon_keys};
       for (const void* k : kernels) CK(cudaFuncGetAttributes(&fa, k));
     }
     g_ctx[device][slot] = std::move(c);
@@ -838,14 +834,15 @@ int enqueue_diam(Ctx* c, cudaStream_t s, int shard, int nshards, int& nk) {
   CKL(1);
   if (++nk >= lim) return SC_OK;
   if (nshards > 1) {
-    // Shards own chunk pairs by identity: give every shard (every GPU) the
-    // same vertex order -- each bin's segment sorted by vertex key.
+    // Shards own 3-D chunk pairs by identity: give every shard (every GPU)
+    // the same vertex order -- each brick bin's segment sorted by the vertex's
+    // coordinates inside the brick.
     // (one warp per bin, 4-warp blocks: 16 blocks per SM)
     CK(launch_k(c, s, c->sms * 16, 128, canon_keys, c->keys_sorted.p, c->keys.p,
                 c->sort_cursor.p, c->d_stats));
-    CK(launch_k(c, s, c->sms * 16, 128, canon_planes, c->plane_sorted.p, c->canon_tmp.p,
-                c->plane_start.p, c->pbin_cursor.p, c->d_stats));
-    CKL(2);
+    CKL(1);
+    // (planar units are owned by whole planes, planar.cu plane_filter: the
+    // order of a plane's entries does not matter)
   }
   // After the sort the 3-D chain (boxes -> filter) and the planar chain
   // (plane boxes -> bound -> filter) are independent: the planar one runs on
@@ -1212,7 +1209,6 @@ int start_roi(Ctx* c, const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
   const unsigned long long fp0 = c->fingerprint();
   int rc = ensure_buffers(c, nx, ny, nz, cap, dcap, punits, c->wcap_floor);
   if (rc) return rc;
-  if (nshards > 1) CK(c->canon_tmp.ensure((size_t)(3 * c->dcap_sz)));
   if (c->fingerprint() != fp0) {
     c->gen++;
     c->drop_graphs();
@@ -2186,7 +2182,6 @@ int sc_shard_diameters(const int64_t* d_sums, const int32_t* d_keys, int64_t n_k
         std::min<long long>(cap, std::max<long long>(c->o.dcap, std::max<long long>(c->dcap_floor, 0)));
     const unsigned long long fp0 = c->fingerprint();
     if ((rc = ensure_buffers(c, nx, ny, nz, cap, dcap, punits, c->wcap_floor))) return rc;
-    if (nshards > 1) CK(c->canon_tmp.ensure((size_t)(3 * c->dcap_sz)));
     if (c->fingerprint() != fp0) {
       c->gen++;
       c->drop_graphs();

@@ -233,10 +233,12 @@ __global__ void __launch_bounds__(256, 4) plane_filter(const unsigned int* __res
       const int i = 2 * I + h, j0 = 2 * J, j1 = 2 * J + 1;
       bool k0 = false, k1 = false;
       if (coarse && i < nc) {
-        // Shards own chunk pairs by identity (coarse unit u, sub-pair), so the
-        // split is the same whatever order the lists come out in.
-        k0 = j0 >= i && j0 < nc && (u * 4 + 2 * h) % nshards == shard;
-        k1 = j1 < nc && (u * 4 + 2 * h + 1) % nshards == shard;  // j1 = 2J + 1 >= i always
+        // Shards own whole planes (plane index mod N): every pair of a plane
+        // is evaluated by one shard, so the split is exact whatever order the
+        // plane's entries come out in on each GPU (no canonical planar order).
+        const bool own = p % nshards == shard;
+        k0 = own && j0 >= i && j0 < nc;
+        k1 = own && j1 < nc;  // j1 = 2J + 1 >= i always
         if (prune && (k0 || k1)) {
           const int4 bi = pboxes[c0 + i];
           if (k0) {

@@ -828,49 +828,4 @@ __global__ void __launch_bounds__(32 * kCanonWarps) canon_keys(int4* __restrict_
   }
 }
 
-// Canonical order of the planar entries: each (plane, in-plane bin)
-// segment -- plane start + the bin cursors scatter_all advanced to the bin
-// ends -- sorted in place by the entry's coordinates inside its in-plane brick.
-__global__ void __launch_bounds__(32 * kCanonWarps) canon_planes(int2* __restrict__ ent,
-                                                                 int2* __restrict__ tmp,
-                                                                 const unsigned int* __restrict__ start,
-                                                                 const unsigned int* __restrict__ pcur,
-                                                                 const Stats* __restrict__ st) {
-  if (st->ovf) return;
-  int bb[6];
-#pragma unroll
-  for (int i = 0; i < 6; i++) bb[i] = st->bbox[i];
-  if (bb[3] < 0) return;
-  const PlaneSpace ps = plane_space(bb);
-  const PlaneBricks pbk = plane_bricks(bb);
-  const int P = ps.cnt[0] + ps.cnt[1] + ps.cnt[2];
-  // one warp per 32 in-plane bins of a plane (most are empty): the non-empty
-  // ones one after another
-  const int lane = threadIdx.x & 31;
-  const long long nw = (long long)gridDim.x * kCanonWarps;
-  for (long long g = (long long)blockIdx.x * kCanonWarps + (threadIdx.x >> 5);
-       g < (long long)P * (kPlaneBins / 32); g += nw) {
-    const long long t = 32 * g + lane;
-    const int p = (int)(t / kPlaneBins), k = (int)(t % kPlaneBins);  // p warp-uniform
-    const unsigned int base = start[p];
-    const unsigned int lo0 = base + (k ? pcur[t - 1] : 0u), hi0 = base + pcur[t];
-    unsigned int work = __ballot_sync(0xffffffffu, hi0 > lo0 + 1);
-    if (!work) continue;
-    // family 0 (XY): (X, Y); 1 (XZ): (X, Z); 2 (YZ): (Y, Z) -- as plane_bins
-    const int axis = plane_axis(p, ps);
-    const int ia = axis == 2 ? 1 : 0, ib = axis == 0 ? 1 : 2;
-    const int la = pbk.lo[ia], lb = pbk.lo[ib], sa = pbk.shift[ia], sb = pbk.shift[ib];
-    const unsigned int ma = (1u << sa) - 1u, mb = (1u << sb) - 1u;
-    auto lkey = [=](int2 e) {
-      return (((unsigned int)(e.x - la) & ma) << sb) | ((unsigned int)(e.y - lb) & mb);
-    };
-    while (work) {
-      const int l = __ffs(work) - 1;
-      work &= work - 1;
-      const unsigned int lo = __shfl_sync(0xffffffffu, lo0, l), hi = __shfl_sync(0xffffffffu, hi0, l);
-      canon_one(ent, tmp, lo, hi, sa + sb, lkey);
-    }
-  }
-}
-
 }  // namespace sc

@@ -49,11 +49,12 @@ def owner_3d(i: int, j: int, n_chunks: int, nshards: int) -> int:
     return tile_pair_index(i, j, n_chunks) % nshards
 
 
-def owner_planar(u: int, h: int, b: int, nshards: int) -> int:
-    """Shard owning chunk pair (2I + h, 2J + b) of planar tile pair u (u = the
-    tile pair's global index over all planes, plane_tstart order):
-    (4u + 2h + b) mod nshards (csrc/planar.cu plane_filter, :251-252)."""
-    return (4 * u + 2 * h + b) % nshards
+def owner_planar(p: int, nshards: int) -> int:
+    """Shard owning every in-plane chunk pair of plane p (engine plane order:
+    XY by z, then XZ by y, then YZ by x): p mod nshards (csrc/planar.cu
+    plane_filter).  Whole planes, so no shard depends on the order of a
+    plane's entries."""
+    return p % nshards
 
 
 def shard_pairs_3d(n: int, shard: int, nshards: int, chunk: int = CHUNK_3D):
@@ -82,7 +83,7 @@ def shard_pairs_planar(plane_sizes: Sequence[int], shard: int, nshards: int,
                 for h in range(2):
                     for b in range(2):
                         i, j = 2 * I + h, 2 * J + b
-                        if i < nc and j < nc and j >= i and owner_planar(u, h, b, nshards) == shard:
+                        if i < nc and j < nc and j >= i and owner_planar(p, nshards) == shard:
                             yield p, i, j
         u0 += T * (T + 1) // 2
 

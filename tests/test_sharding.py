@@ -1,7 +1,7 @@
 """Multi-rank host logic on CPU (gloo, world_size 2): ROI-batch assignment and
 the pair-grid shard + all_reduce(MAX) combine.  The per-shard compute is a CPU
 stub that follows the engine's partition exactly -- ownership by unit identity
-(sharding.owner_3d = prune.cu:457, sharding.owner_planar = planar.cu:251-252) --
+(sharding.owner_3d = prune.cu test_chunk_pair, sharding.owner_planar = planar.cu plane_filter) --
 with the reference's pair arithmetic (features.py:140-148)."""
 
 import math
