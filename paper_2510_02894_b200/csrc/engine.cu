@@ -2032,23 +2032,39 @@ __global__ void shard_export(const Stats* __restrict__ st, unsigned int* __restr
 }
 
 // Phase 2 import (after init_stats): the global bbox and the summed partials.
+// A summed vertex count that differs from the gathered key count is refused
+// here, on the device (no host round trip before the run): the record is
+// flagged, and with no histograms loaded the pipeline has nothing to do.
 __global__ void shard_import(Stats* __restrict__ st, int4 bb_lo, int4 bb_hi,
                              unsigned int* __restrict__ sort_counts,
                              unsigned int* __restrict__ pbin_counts, long long n_pbin,
-                             const long long* __restrict__ sums) {
+                             const long long* __restrict__ sums, long long n_keys) {
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long step = (long long)gridDim.x * blockDim.x;
+  const bool ok = sums[kSumVert] == n_keys;
   if (t0 == 0) {
     st->bbox[0] = bb_lo.x; st->bbox[1] = bb_lo.y; st->bbox[2] = bb_lo.z;
     st->bbox[3] = bb_hi.x; st->bbox[4] = bb_hi.y; st->bbox[5] = bb_hi.z;
     st->vol_k = sums[kSumVol];
-    st->n_vert = (unsigned long long)sums[kSumVert];
+    st->n_vert = ok ? (unsigned long long)n_keys : 0ull;
+    st->bad_input = ok ? 0u : 1u;
   }
+  if (!ok) return;  // (the slot's histograms stay zero)
   for (long long i = t0; i < kNumCases; i += step) st->hist[0][i] = (unsigned long long)sums[kSumHist + i];
   for (long long i = t0; i < kSortBins + kSortSupers; i += step)
     sort_counts[i] = (unsigned int)sums[kSumSort + i];
   for (long long i = t0; i < n_pbin; i += step)
     pbin_counts[i] = (unsigned int)sums[kSumPlane + i];
+}
+
+// Phase 1: the shard's vertex keys to the caller's buffer, sized on the device
+// (no host round trip for the count); at most `room` keys.
+__global__ void shard_copy_keys(const int4* __restrict__ src, int4* __restrict__ dst,
+                                const Stats* __restrict__ st, long long room) {
+  const long long n = min((long long)st->n_vert, room);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
 }
 
 int sc_shard_exchange_sizes(int64_t nx, int64_t ny, int64_t nz, int64_t* n_sums,
@@ -2107,10 +2123,19 @@ int sc_shard_mesh(const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
     ~Reset() { c->mc_slab = 0; c->mesh_only = false; }
   } reset{c};
   Pending p{};
+  const long long n_pbin = (2 * (nx + ny + nz) + 9) * kPlaneBinsHost;
   for (int attempt = 0; attempt < 2; attempt++) {
     c->mc_slab = (nshards << 16) | shard;
     c->mesh_only = true;
     if ((rc = start_roi(c, d_mask, nx, ny, nz, spacing, s, 0, 1, nullptr, 0, &p))) return rc;
+    // export and key copy enqueued behind the mesh: one synchronisation per call
+    shard_export<<<c->sms * 2, 256, 0, s>>>(c->d_stats, c->sort_counts.p, c->pbin_counts.p,
+                                            n_pbin, reinterpret_cast<long long*>(d_sums));
+    CKL(1);
+    shard_copy_keys<<<c->sms * 4, 256, 0, s>>>(
+        c->keys.p, reinterpret_cast<int4*>(d_keys), c->d_stats,
+        std::min<long long>((long long)key_cap, (long long)c->keys.cap));
+    CKL(1);
     CK(cudaStreamSynchronize(s));
     const long long V = (long long)c->h_stats->n_vert;
     if (V <= (long long)c->keys.cap) break;
@@ -2130,12 +2155,6 @@ int sc_shard_mesh(const uint8_t* d_mask, int64_t nx, int64_t ny, int64_t nz,
     set_err("key buffer holds %lld keys, the shard has %lld", (long long)key_cap, V);
     return SC_ERR_NOMEM;
   }
-  const long long n_pbin = (2 * (nx + ny + nz) + 9) * kPlaneBinsHost;
-  shard_export<<<c->sms * 2, 256, 0, s>>>(c->d_stats, c->sort_counts.p, c->pbin_counts.p, n_pbin,
-                                          reinterpret_cast<long long*>(d_sums));
-  CKL(1);
-  if (V) CK(cudaMemcpyAsync(d_keys, c->keys.p, (size_t)V * sizeof(int4), cudaMemcpyDeviceToDevice, s));
-  CK(cudaStreamSynchronize(s));
   return SC_OK;
 }
 
@@ -2164,15 +2183,8 @@ int sc_shard_diameters(const int64_t* d_sums, const int32_t* d_keys, int64_t n_k
   two_phase_opts(c);
   cudaStream_t s = order_after_legacy(c, stream);
   std::memset(out, 0, sizeof *out);
-  {  // the summed vertex count must be the gathered key count
-    long long nv = -1;
-    CK(cudaMemcpyAsync(&nv, d_sums + kSumVert, sizeof nv, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (nv != (long long)n_keys) {
-      set_err("summed vertex count %lld != gathered keys %lld", nv, (long long)n_keys);
-      return SC_ERR_INPUT;
-    }
-  }
+  // (the summed vertex count must be the gathered key count: shard_import
+  // checks it on the device)
   long long punits = 0;
   const long long n_pbin = (2 * (nx + ny + nz) + 9) * kPlaneBinsHost;
   const int4 lo = make_int4(bbox[0], bbox[1], bbox[2], 0), hi = make_int4(bbox[3], bbox[4], bbox[5], 0);
@@ -2192,7 +2204,8 @@ int sc_shard_diameters(const int64_t* d_sums, const int32_t* d_keys, int64_t n_k
     init_stats<<<1, 256, 0, s>>>(c->d_stats, c->segmap.p, 0LL, nullptr, c->d_rp);
     CKL(1);
     shard_import<<<c->sms * 2, 256, 0, s>>>(c->d_stats, lo, hi, c->sort_counts.p, c->pbin_counts.p,
-                                            n_pbin, reinterpret_cast<const long long*>(d_sums));
+                                            n_pbin, reinterpret_cast<const long long*>(d_sums),
+                                            (long long)n_keys);
     CKL(1);
     if (n_keys)
       CK(cudaMemcpyAsync(c->keys.p, d_keys, (size_t)n_keys * sizeof(int4), cudaMemcpyDeviceToDevice, s));
@@ -2204,8 +2217,8 @@ int sc_shard_diameters(const int64_t* d_sums, const int32_t* d_keys, int64_t n_k
     CK(cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     const Stats& h = *c->h_stats;
-    if ((long long)h.n_vert != n_keys) {
-      set_err("summed vertex count %llu != gathered keys %lld", h.n_vert, (long long)n_keys);
+    if (h.bad_input) {
+      set_err("summed vertex count != gathered keys (%lld)", (long long)n_keys);
       return SC_ERR_INPUT;
     }
     const long long PU = (long long)h.n_pwork, WU = (long long)h.n_work;

@@ -45,7 +45,7 @@ struct Stats {
   unsigned long long t_start, t_mesh, t_end;
   unsigned int plane_ovf;              // a plane holds more than kPlaneMaxEntries entries
   unsigned int trace_on;               // kernels record their spans (RoiParams::pflags bit 2)
-  unsigned int pad2_;
+  unsigned int bad_input;              // shard_import: summed vertex count != gathered keys
   unsigned long long n_eval;           // 3-D pair slots pass 1 evaluated (after the vertex filter)
   unsigned long long n_peval;          // planar pair slots pass 1 evaluated
   // %globaltimer of each pipeline kernel's first block start / last block
