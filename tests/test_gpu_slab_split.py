@@ -106,3 +106,20 @@ def test_more_shards_than_layers_and_errors(sc, cuda_device):
         sc.shard_diameters(sums, keys, n - 1, arr.shape, bbox, (1.0, 1.0, 1.0), 0, 1, sq4)
     # the slot is a plain ROI again afterwards
     assert _full(sc, d, (1.0, 1.0, 1.0)) == full
+
+
+def test_slab_sharded_coefficients_single_rank(sc, golden, cuda_device):
+    """The torch.distributed driver itself at world size 1 (no process group):
+    phase 1, the (trivial) exchange, phase 2, and the MAX combine."""
+    import torch
+
+    from paper_2510_02894_b200 import sharding, synth
+
+    case = next(c for c in golden["big"] if c["name"] == "C2_kits_R30")
+    d = torch.from_numpy(synth.kits_like(tumor_mm=30.0)).cuda()
+    full = _full(sc, d, case["spacing"])
+    rec = sharding.slab_sharded_coefficients(d, case["spacing"])
+    _check_equal(rec, full, "world 1")
+    for k in ("Maximum3DDiameter", "Maximum2DDiameterXY", "Maximum2DDiameterXZ",
+              "Maximum2DDiameterYZ", "VertexCount"):
+        assert rec[k] == case["features"][k], k
