@@ -31,6 +31,8 @@ long before it comes back, so no L2 flush is needed.  C2 (configs[1], one
              events around the kernel; roofline_pass1 = the FP32 diameter
              pass (8 flop per evaluated pair vs the FP32 rate measured by
              sc_probe_fp32_peak on this GPU).
+  dominant_kernel  the largest single kernel of this workload's one-ROI call
+             (C3: mc_cells), its share, its bound and its committed ncu counters.
   cpu_baseline  the reference itself (shapecore, numba, installed under
              baseline/_ref) on all host cores on a bounded sample of the
              workload; the C port in oracle/ when the install is missing.
@@ -683,6 +685,31 @@ def run_ours(args):
     # largest single-call stage (C3-like meshes).
     roofline = roof_p1 if dominant == "pass1_ms" else roof_batch
     total_k = sum(stage.values())
+    # The largest single kernel of this workload's one-ROI call (the stage
+    # groups prune_ms / planar_prep_ms are 3-6 latency-bound kernels each and
+    # are reported as groups in kernel_share): its time, share and bound, with
+    # the committed ncu counters of that kernel where a capture exists.
+    kname = {"pack_ms": "pack_bits_v16", "mc_ms": "mc_cells", "pass1_ms": "diam_pass1",
+             "refine_ms": "diam_refine"}
+    single = {k: stage[k] for k in kname if k in stage}
+    dk = max(single, key=single.get)
+    kbound = {"pack_ms": "HBM (roofline_pack_single)",
+              "mc_ms": "ALU issue + L2 latency: integer bit ops on the L2-resident bit volume "
+                       "(no HBM or FMA roofline applies; see issue_pct)",
+              "pass1_ms": "FP32 FMA pipe after pruning: per-unit overhead (roofline_pass1)",
+              "refine_ms": "FP64 / latency: re-check of the candidate units"}[dk]
+    dom_k = {"kernel": kname[dk], "us": single[dk] * 1e3, "share_of_call": single[dk] / total_k,
+             "bound": kbound, "largest_group": max(stage, key=stage.get),
+             "largest_group_share": max(stage.values()) / total_k}
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
+            kc = json.load(fh).get("kernels", {}).get(kname[dk])
+        if kc:
+            dom_k["ncu_c2_capture"] = {k: kc[k] for k in ("issue_pct", "occupancy_pct",
+                                                          "pipe_alu_pct", "pipe_fma_pct",
+                                                          "dram_pct") if k in kc}
+    except (OSError, ValueError):
+        pass
 
     line = {
         "metric": METRIC,
@@ -739,6 +766,7 @@ def run_ours(args):
         "kernel_ms_batch_pack": {"pack_ms": med_tma["pack_ms"]},
         "kernel_share": {k: v / total_k for k, v in stage.items()},
         "dominant_stage": dominant,
+        "dominant_kernel": dom_k,
         "diagnostics": diag,
         "clocks": clocks.summary(),
         "result": {"VertexCount": V, "triangles": c.triangle_count, "active_cubes": c.active_cubes,
